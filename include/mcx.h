@@ -1,0 +1,127 @@
+/*
+ * mcx.h — C ABI of the B200 mesh-intersection backend (libmcx.so).
+ *
+ * This is the drop-in boundary for the reference's mesh-search backend seam:
+ * the `backend` argument of isect.pair_candidates / isect.find_intersections
+ * (reference SPEC.md:469, 478; CLI `intersect --backend`).
+ * The reference is a Python package with no FFI of its own, so
+ * each entry point below names the reference operation it replaces; the ctypes
+ * binding a maintainer would add is in INTEGRATION.md.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  "dev" pointers are CUDA device pointers
+ *    owned by the caller (the Python host allocates them as torch tensors);
+ *    the library never allocates device or host memory, scratch comes from the
+ *    caller's workspace (size from mcx_workspace_bytes).
+ *  - Every call returns a status: MCX_OK, or an error whose text is available
+ *    from mcx_last_error() (thread-local).  MCX_E_CAPACITY means the hit buffer
+ *    was too small; stats->n_hits then holds the exact required count, so the
+ *    caller grows the buffer and reruns (results are deterministic as a set).
+ *  - Reentrant across devices: one host thread per GPU; no global mutable
+ *    state.  Work is enqueued on opts->stream.
+ *  - Arithmetic contract: SURVEY.md §7.3 (canonical FMA-free FP64 op sequence),
+ *    bit-identical to the CPU oracle on identically packed triangles.
+ */
+#ifndef MCX_H_
+#define MCX_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MCX_ABI_VERSION 1
+
+#define MCX_OK 0
+#define MCX_E_CAPACITY 1
+#define MCX_E_CUDA 2
+#define MCX_E_ARG 3
+
+/* Per-triangle records in HBM.
+ *  box: [n_tri][8] doubles = lo[4], hi[4] (exact AABB over the 3 vertices), 64 B.
+ *  geo: [n_tri][MCX_GEO_STRIDE] doubles = p[4], e1[4], e2[4],
+ *       P[6] (= e1∧e2 in order 01,02,03,12,13,23), nrm (= ‖e1‖·‖e2‖), pad. */
+#define MCX_BOX_STRIDE 8
+#define MCX_GEO_STRIDE 20
+
+/* Search modes. */
+#define MCX_MODE_BRUTE 0 /* every (iA, iB) pair gets the 8-compare AABB test       */
+#define MCX_MODE_CULL 1  /* exact block-AABB culling first; identical hit set      */
+
+typedef struct mcx_mesh_dev {
+  uint64_t n_tri;     /* number of triangles = 2·N·(M−1)                        */
+  const double* box;  /* device, [n_tri][8], 16-byte aligned                    */
+  const double* geo;  /* device, [n_tri][20], 16-byte aligned                   */
+} mcx_mesh_dev;
+
+/* One intersecting triangle pair: A triangle ia, B triangle ib, and the
+ * solution of p + s·e1 + t·e2 = q + a·f1 + b·f2 (Eq. 26; the SPEC's
+ * (a, b, c, d) = (s, t, a, b)).  40 bytes. */
+typedef struct mcx_hit {
+  uint32_t ia, ib;
+  double s, t, a, b;
+} mcx_hit;
+
+typedef struct mcx_stats {
+  uint64_t n_pairs;     /* logical triangle pairs covered by the call               */
+  uint64_t n_tested;    /* pair AABB tests executed (== n_pairs in MCX_MODE_BRUTE)   */
+  uint64_t n_aabb_pass; /* pairs that passed the triangle AABB test (solved)        */
+  uint64_t n_singular;  /* solved pairs rejected by the singular gate */
+  uint64_t n_hits;      /* accepted pairs (may exceed the hit capacity)            */
+  double kernel_ms;     /* device time of the search kernels (CUDA events)         */
+} mcx_stats;
+
+typedef struct mcx_opts {
+  int device;            /* CUDA device ordinal                                      */
+  void* stream;          /* cudaStream_t (NULL = legacy default stream)              */
+  uint64_t a_begin;      /* A triangle range [a_begin, a_end); a_end = 0 → n_tri     */
+  uint64_t a_end;
+  uint32_t shard_index;  /* cyclic sharding of A blocks (MCX_A_BLOCK triangles each): */
+  uint32_t shard_count;  /*   this call takes blocks b with b % count == index; 0 → 1 */
+  int mode;              /* MCX_MODE_BRUTE or MCX_MODE_CULL                           */
+  int timing;            /* nonzero: record CUDA events and fill stats->kernel_ms    */
+  void* workspace;       /* device scratch, >= mcx_workspace_bytes() bytes           */
+  uint64_t workspace_bytes;
+} mcx_opts;
+
+/* A-block granularity of the kernel and of cyclic sharding. */
+uint32_t mcx_a_block(void);
+
+/* Device scratch the search needs for these meshes and options. */
+uint64_t mcx_workspace_bytes(const mcx_mesh_dev* A, const mcx_mesh_dev* B, const mcx_opts* opts);
+
+/* Canonical triangle packing on the device (replaces the host-side triangle
+ * construction of PAPER.md kernel steps 3-4 / SPEC Quad4 split).
+ * coords: device, (4, M, N) float64 = four column-major N×M planes (x, y, px, py)
+ * of one half-layer.  Writes box/geo for the
+ * 2·N·(M−1) triangles, bit-identical to the CPU oracle's packing. */
+int mcx_pack(const double* coords, uint32_t N, uint32_t M, double* box, double* geo,
+             int device, void* stream);
+
+/* Triangle-level intersection search of A against B (replaces the reference's
+ * rejection kernel + findall compaction + host precise test: PAPER.md kernel
+ * steps 1-9 and Fig. 1, SPEC isect.pair_candidates + find_intersections,
+ * SPEC.md:469-486).  Writes up to `cap` hits (unordered) to hits (device) and
+ * fills *stats (host).  Synchronises opts->stream before returning. */
+int mcx_search(const mcx_mesh_dev* A, const mcx_mesh_dev* B, const mcx_opts* opts,
+               mcx_hit* hits, uint64_t cap, mcx_stats* stats);
+
+/* Quad-pair candidate list of the SPEC-literal predicate: not aabb_reject (quad
+ * boxes) and not moller_reject (PAPER.md kernel steps
+ * 5-7).  A, B given as half-layer grids (device, (4, M, N)).  Writes up to cap
+ * quad-pair gids (u64, unordered; gid = i + N1·j + N1·N2·k1 + N1·N2·(M1−1)·l1,
+ * SPEC.md:433) and *n_out = exact survivor count (the compaction counter,
+ * SPEC.md:491).  Synchronises the stream. */
+int mcx_pair_candidates(const double* coords_a, uint32_t NA, uint32_t MA,
+                        const double* coords_b, uint32_t NB, uint32_t MB,
+                        int device, void* stream, void* workspace, uint64_t workspace_bytes,
+                        uint64_t* gids, uint64_t cap, uint64_t* n_out);
+
+const char* mcx_last_error(void);
+int mcx_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MCX_H_ */

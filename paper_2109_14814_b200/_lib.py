@@ -1,0 +1,96 @@
+"""ctypes binding of the C ABI in include/mcx.h (libmcx.so, built in-tree).
+
+There is no fallback: if the library is missing or fails to load, every entry
+point raises ``BackendError`` ("the product path must fail loudly").  ctypes
+releases the GIL during foreign calls, so one host thread per GPU runs its
+search concurrently.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .errors import BackendError, CapacityError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmcx.so")
+
+MCX_OK, MCX_E_CAPACITY, MCX_E_CUDA, MCX_E_ARG = 0, 1, 2, 3
+MODE_BRUTE, MODE_CULL = 0, 1
+BOX_STRIDE, GEO_STRIDE = 8, 20
+
+EXPORTS = ("mcx_a_block", "mcx_workspace_bytes", "mcx_pack", "mcx_search", "mcx_pair_candidates",
+           "mcx_last_error", "mcx_version")
+
+
+class MeshDev(ctypes.Structure):
+    _fields_ = [("n_tri", ctypes.c_uint64), ("box", ctypes.c_void_p), ("geo", ctypes.c_void_p)]
+
+
+class Hit(ctypes.Structure):
+    _fields_ = [("ia", ctypes.c_uint32), ("ib", ctypes.c_uint32), ("s", ctypes.c_double),
+                ("t", ctypes.c_double), ("a", ctypes.c_double), ("b", ctypes.c_double)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("n_pairs", ctypes.c_uint64), ("n_tested", ctypes.c_uint64), ("n_aabb_pass", ctypes.c_uint64),
+                ("n_singular", ctypes.c_uint64), ("n_hits", ctypes.c_uint64), ("kernel_ms", ctypes.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class Opts(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int), ("stream", ctypes.c_void_p), ("a_begin", ctypes.c_uint64),
+                ("a_end", ctypes.c_uint64), ("shard_index", ctypes.c_uint32), ("shard_count", ctypes.c_uint32),
+                ("mode", ctypes.c_int), ("timing", ctypes.c_int), ("workspace", ctypes.c_void_p),
+                ("workspace_bytes", ctypes.c_uint64)]
+
+
+assert ctypes.sizeof(Hit) == 40
+
+_lib = None
+
+
+def load():
+    """Load libmcx.so (raises BackendError if absent — no CPU fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise BackendError(f"CUDA backend library not built: {LIB_PATH} (run __graft_entry__.build())")
+    try:
+        L = ctypes.CDLL(LIB_PATH)
+    except OSError as exc:
+        raise BackendError(f"cannot load {LIB_PATH}: {exc}") from None
+    u32, u64, i32, vp = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int, ctypes.c_void_p
+    P = ctypes.POINTER
+    L.mcx_a_block.restype = u32
+    L.mcx_a_block.argtypes = []
+    L.mcx_workspace_bytes.restype = u64
+    L.mcx_workspace_bytes.argtypes = [P(MeshDev), P(MeshDev), P(Opts)]
+    L.mcx_pack.restype = i32
+    L.mcx_pack.argtypes = [vp, u32, u32, vp, vp, i32, vp]
+    L.mcx_search.restype = i32
+    L.mcx_search.argtypes = [P(MeshDev), P(MeshDev), P(Opts), vp, u64, P(Stats)]
+    L.mcx_pair_candidates.restype = i32
+    L.mcx_pair_candidates.argtypes = [vp, u32, u32, vp, u32, u32, i32, vp, vp, u64, vp, u64, P(u64)]
+    L.mcx_last_error.restype = ctypes.c_char_p
+    L.mcx_last_error.argtypes = []
+    L.mcx_version.restype = i32
+    L.mcx_version.argtypes = []
+    _lib = L
+    return L
+
+
+def last_error() -> str:
+    return load().mcx_last_error().decode(errors="replace")
+
+
+def check(rc: int, what: str, task=None, required: int = 0):
+    if rc == MCX_OK:
+        return
+    msg = f"{what}: {last_error()}"
+    if rc == MCX_E_CAPACITY:
+        raise CapacityError(msg, required=required, task=task)
+    raise BackendError(msg, task=task, status=rc)

@@ -1,0 +1,206 @@
+// mcx_common.cuh — shared device helpers: error state, mbarrier / bulk-copy PTX,
+// and the canonical FP64 triangle-pair solve.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "../../include/mcx.h"
+
+namespace mcx {
+
+// ------------------------------------------------------------ error state
+// Thread-local, so concurrent host threads (one per GPU) never clobber each other.
+extern thread_local char g_err[512];
+
+inline int set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                        \
+  do {                                                                                        \
+    cudaError_t _e = (expr);                                                                  \
+    if (_e != cudaSuccess)                                                                    \
+      return ::mcx::set_error(MCX_E_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #expr,          \
+                              cudaGetErrorString(_e));                                        \
+  } while (0)
+
+// ------------------------------------------------------- mbarrier + bulk copy
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred done;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n"
+      " @!done bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// 1-D bulk async copy global → shared (SASS: UBLKCP), completion on `bar`.
+// bytes must be a multiple of 16 and both addresses 16-byte aligned.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// ------------------------------------------------------- canonical FP64 solve
+// FMA-free, fixed association order; see oracle/canonical.py:solve_pairs.
+#define MCX_SING_RTOL 1e-12
+
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+
+// g_j = Σ_i r_i K_ij for the antisymmetric K of bivector B (order 01,02,03,12,13,23)
+__device__ __forceinline__ void contract(const double r[4], const double B[6], double c[4]) {
+  c[0] = dsub(dsub(dmul(r[2], B[4]), dmul(r[1], B[5])), dmul(r[3], B[3]));
+  c[1] = dadd(dsub(dmul(r[0], B[5]), dmul(r[2], B[2])), dmul(r[3], B[1]));
+  c[2] = dsub(dsub(dmul(r[1], B[2]), dmul(r[0], B[4])), dmul(r[3], B[0]));
+  c[3] = dadd(dsub(dmul(r[0], B[3]), dmul(r[1], B[1])), dmul(r[2], B[0]));
+}
+
+__device__ __forceinline__ double dot4(const double c[4], const double x[4]) {
+  double d = dmul(c[0], x[0]);
+  d = dadd(d, dmul(c[1], x[1]));
+  d = dadd(d, dmul(c[2], x[2]));
+  d = dadd(d, dmul(c[3], x[3]));
+  return d;
+}
+
+__device__ __forceinline__ void load_geo(const double* __restrict__ g, double out[20]) {
+  const double2* p = reinterpret_cast<const double2*>(g);
+#pragma unroll
+  for (int k = 0; k < 10; ++k) {
+    const double2 v = __ldg(p + k);
+    out[2 * k] = v.x;
+    out[2 * k + 1] = v.y;
+  }
+}
+
+// Returns 0 = miss, 1 = hit (sol = s, t, a, b), 2 = singular (gate).
+__device__ __forceinline__ int solve_pair(const double* __restrict__ gA, const double* __restrict__ gB,
+                                          double sol[4]) {
+  double A[20], B[20];
+  load_geo(gA, A);
+  load_geo(gB, B);
+  const double* p = A;
+  const double* e1 = A + 4;
+  const double* e2 = A + 8;
+  const double* Pa = A + 12;
+  const double* q = B;
+  const double* f1 = B + 4;
+  const double* f2 = B + 8;
+  const double* Qb = B + 12;
+  double r[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) r[c] = dsub(q[c], p[c]);
+  double D = dsub(dmul(Pa[0], Qb[5]), dmul(Pa[1], Qb[4]));
+  D = dadd(D, dmul(Pa[2], Qb[3]));
+  D = dadd(D, dmul(Pa[3], Qb[2]));
+  D = dsub(D, dmul(Pa[4], Qb[1]));
+  D = dadd(D, dmul(Pa[5], Qb[0]));
+  const double thr = dmul(dmul(A[18], B[18]), MCX_SING_RTOL);
+  if (fabs(D) <= thr) return 2;
+  double g[4], h[4];
+  contract(r, Qb, g);
+  contract(r, Pa, h);
+  const double s = __ddiv_rn(dot4(g, e2), D);
+  const double t = __ddiv_rn(-dot4(g, e1), D);
+  const double a = __ddiv_rn(-dot4(h, f2), D);
+  const double b = __ddiv_rn(dot4(h, f1), D);
+  if (s >= 0.0 && t >= 0.0 && a >= 0.0 && b >= 0.0 && dadd(s, t) <= 1.0 && dadd(a, b) <= 1.0) {
+    sol[0] = s;
+    sol[1] = t;
+    sol[2] = a;
+    sol[3] = b;
+    return 1;
+  }
+  return 0;
+}
+
+// ------------------------------------------- SPEC-literal Moller quick test
+// Mirrors oracle/serial.py (_plane/_side_reject) op for op.  Quad q = i + N·k1 of a
+// (4, M, N) grid; vertices v00 v10 v01 v11; projection (x, y, px).
+#define MCX_DEGEN_RTOL2 1e-28
+
+__device__ __forceinline__ void quad_verts(const double* __restrict__ c, uint32_t N, uint32_t M, uint32_t q,
+                                           double V[4][3]) {
+  const uint32_t i = q % N, k = q / N;
+  const uint32_t ip = (i + 1 == N) ? 0 : i + 1;
+  const uint64_t idx[4] = {(uint64_t)k * N + i, (uint64_t)k * N + ip, (uint64_t)(k + 1) * N + i,
+                           (uint64_t)(k + 1) * N + ip};
+#pragma unroll
+  for (int v = 0; v < 4; ++v)
+#pragma unroll
+    for (int d = 0; d < 3; ++d) V[v][d] = __ldg(c + (uint64_t)d * M * N + idx[v]);
+}
+
+// All four Vo vertices strictly on one side of the plane of T¹(Vq) and of T²(Vq).
+__device__ __forceinline__ bool side_reject(const double Vq[4][3], const double Vo[4][3]) {
+  const int tri[2][3] = {{0, 1, 2}, {2, 1, 3}};
+  bool out = true;
+#pragma unroll
+  for (int T = 0; T < 2; ++T) {
+    const double* O = Vq[tri[T][0]];
+    double U[3], W[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      U[d] = dsub(Vq[tri[T][1]][d], O[d]);
+      W[d] = dsub(Vq[tri[T][2]][d], O[d]);
+    }
+    const double N0 = dsub(dmul(U[1], W[2]), dmul(U[2], W[1]));
+    const double N1 = dsub(dmul(U[2], W[0]), dmul(U[0], W[2]));
+    const double N2 = dsub(dmul(U[0], W[1]), dmul(U[1], W[0]));
+    const double nn = dadd(dadd(dmul(N0, N0), dmul(N1, N1)), dmul(N2, N2));
+    const double uu = dadd(dadd(dmul(U[0], U[0]), dmul(U[1], U[1])), dmul(U[2], U[2]));
+    const double ww = dadd(dadd(dmul(W[0], W[0]), dmul(W[1], W[1])), dmul(W[2], W[2]));
+    const bool degen = nn < dmul(dmul(uu, ww), MCX_DEGEN_RTOL2);
+    bool pos = true, neg = true;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const double f = dadd(dadd(dmul(N0, dsub(Vo[m][0], O[0])), dmul(N1, dsub(Vo[m][1], O[1]))),
+                            dmul(N2, dsub(Vo[m][2], O[2])));
+      pos = pos && (f > 0.0);
+      neg = neg && (f < 0.0);
+    }
+    out = out && !degen && (pos || neg);
+  }
+  return out;
+}
+
+__device__ __forceinline__ bool moller_reject(const double* cA, uint32_t NA, uint32_t MA, uint32_t qa,
+                                              const double* cB, uint32_t NB, uint32_t MB, uint32_t qb) {
+  double VA[4][3], VB[4][3];
+  quad_verts(cA, NA, MA, qa, VA);
+  quad_verts(cB, NB, MB, qb, VB);
+  return side_reject(VA, VB) || side_reject(VB, VA);
+}
+
+}  // namespace mcx

@@ -1,0 +1,517 @@
+// mcx_search.cu — sm_100a triangle-pair intersection search (libmcx.so).
+//
+// Replaces the reference's rejection kernel, findall compaction and host-side
+// precise test (PAPER.md "Computational Implementation", kernel steps 1-9 and
+// Fig. 1; SPEC isect.pair_candidates / find_intersections) with
+// one fused kernel:
+//
+//   * A triangles live in registers: each thread owns R = 4 triangle AABBs
+//     (8 doubles each), so a CTA of 256 threads owns an A block of 1024
+//     triangles (a warp covers 32 consecutive triangles per r, i.e. one θ-strip
+//     of the mesh).
+//   * B triangle AABBs stream through shared memory in tiles of 512 (32 KB)
+//     with a 2-stage ring of 1-D bulk async copies (cp.async.bulk → UBLKCP)
+//     completed on mbarriers.  Every B box is a warp-uniform broadcast
+//     (4 × LDS.128) that serves 32·R = 128 pair tests.
+//   * Pair test = 8 FP64 compares (DSETP), strict-separation semantics of
+//     SPEC.md:442-450 (touching boxes are not rejected).
+//   * Rare survivors are pushed by warp ballot into a per-warp shared-memory
+//     queue; when 32 are queued the warp solves them lane-parallel with the
+//     canonical FMA-free FP64 bivector-Cramer sequence, reading
+//     the two triangles' geometry from L2.  Hits are compacted with one atomic
+//     per warp into the global (iA, iB, s, t, a, b) list (no flag buffer).
+//
+// The solve uses only __dadd_rn/__dsub_rn/__dmul_rn/__ddiv_rn (never contracted
+// into DFMA) and the file is compiled with --fmad=false, so the op sequence is
+// bit-identical to oracle/canonical.py.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+
+#include "../../include/mcx.h"
+#include "mcx_common.cuh"
+
+namespace mcx {
+
+// ------------------------------------------------------------------ packing
+// One thread per triangle; same op sequence as oracle/canonical.py:pack.
+__global__ void pack_kernel(const double* __restrict__ coords, uint32_t N, uint32_t M,
+                            double* __restrict__ box, double* __restrict__ geo) {
+  const uint64_t n_tri = 2ull * N * (M - 1);
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n_tri;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t q = t >> 1;
+    const int tau = (int)(t & 1);
+    const uint32_t i = (uint32_t)(q % N), k = (uint32_t)(q / N);
+    const uint32_t ip = (i + 1 == N) ? 0 : i + 1;
+    double v0[4], v1[4], v2[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const double* pl = coords + (uint64_t)c * M * N;
+      const double w00 = pl[(uint64_t)k * N + i], w10 = pl[(uint64_t)k * N + ip];
+      const double w01 = pl[(uint64_t)(k + 1) * N + i], w11 = pl[(uint64_t)(k + 1) * N + ip];
+      v0[c] = __dadd_rn(tau ? w01 : w00, 0.0);
+      v1[c] = __dadd_rn(w10, 0.0);
+      v2[c] = __dadd_rn(tau ? w11 : w01, 0.0);
+    }
+    double e1[4], e2[4];
+    double* b = box + t * MCX_BOX_STRIDE;
+    double* g = geo + t * MCX_GEO_STRIDE;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      b[c] = fmin(fmin(v0[c], v1[c]), v2[c]);
+      b[4 + c] = fmax(fmax(v0[c], v1[c]), v2[c]);
+      e1[c] = __dsub_rn(v1[c], v0[c]);
+      e2[c] = __dsub_rn(v2[c], v0[c]);
+      g[c] = v0[c];
+      g[4 + c] = e1[c];
+      g[8 + c] = e2[c];
+    }
+    const int bi[6] = {0, 0, 0, 1, 1, 2}, bj[6] = {1, 2, 3, 2, 3, 3};
+#pragma unroll
+    for (int p = 0; p < 6; ++p)
+      g[12 + p] = __dsub_rn(__dmul_rn(e1[bi[p]], e2[bj[p]]), __dmul_rn(e1[bj[p]], e2[bi[p]]));
+    double n1 = __dmul_rn(e1[0], e1[0]);
+    n1 = __dadd_rn(n1, __dmul_rn(e1[1], e1[1]));
+    n1 = __dadd_rn(n1, __dmul_rn(e1[2], e1[2]));
+    n1 = __dadd_rn(n1, __dmul_rn(e1[3], e1[3]));
+    double n2 = __dmul_rn(e2[0], e2[0]);
+    n2 = __dadd_rn(n2, __dmul_rn(e2[1], e2[1]));
+    n2 = __dadd_rn(n2, __dmul_rn(e2[2], e2[2]));
+    n2 = __dadd_rn(n2, __dmul_rn(e2[3], e2[3]));
+    g[18] = __dmul_rn(__dsqrt_rn(n1), __dsqrt_rn(n2));
+    g[19] = 0.0;
+  }
+}
+
+// ------------------------------------------------------------ search kernel
+constexpr int A_BLOCK = 1024;        // A triangles per CTA (= THREADS · R for every variant)
+constexpr int TILE = 512;            // B triangles per shared-memory tile
+constexpr int STAGES = 2;
+
+// Kernel variant: R A triangles per thread, MINB resident CTAs per SM (register cap).
+template <int R_, int MINB_>
+struct Cfg {
+  static constexpr int R = R_;
+  static constexpr int MINB = MINB_;
+  static constexpr int THREADS = A_BLOCK / R_;
+  static constexpr int WARPS = THREADS / 32;
+  static constexpr int QCAP = 32 * R_ + 32;  // per-warp survivor queue capacity
+};
+
+struct __align__(16) Box {
+  double lo[4];
+  double hi[4];
+};
+
+enum Kind { KIND_TRI = 0, KIND_QUAD = 1 };
+
+struct SearchParams {
+  const Box* boxA;
+  const double* geoA;
+  const Box* boxB;
+  const double* geoB;
+  uint64_t a_begin, a_end;  // A triangle range
+  uint64_t nB;
+  uint64_t b_chunk;         // B triangles per CTA (multiple of TILE)
+  uint32_t shard_index, shard_count;
+  mcx_hit* hits;
+  uint64_t cap;
+  unsigned long long* counters;  // [0] emitted, [1] aabb pass, [2] singular / Moller-rejected
+  // KIND_QUAD only: half-layer grids (4, M, N) for the Moller stage, and gid output
+  const double* coordsA;
+  const double* coordsB;
+  uint32_t NA, MA, NB, MB;
+  uint64_t* gids;
+};
+
+template <class C>
+struct __align__(16) SearchSmem {
+  Box tile[STAGES][TILE];
+  uint2 queue[C::WARPS][C::QCAP];
+  unsigned long long full[STAGES];
+};
+
+// Process the queued pairs [0, n) of this warp's queue slice, one per lane:
+// KIND_TRI  — canonical solve, emit (iA, iB, s, t, a, b) hits;
+// KIND_QUAD — SPEC-literal Moller quick test, emit surviving quad-pair gids.
+template <int KIND>
+__device__ __forceinline__ void flush_queue(const SearchParams& P, const uint2* q, int n, int lane,
+                                            unsigned long long& n_pass, unsigned long long& n_sing) {
+  const bool valid = lane < n;
+  uint2 e = valid ? q[lane] : make_uint2(0, 0);
+  __syncwarp();
+  double sol[4];
+  int rc = 0;
+  if (KIND == KIND_TRI) {
+    if (valid) rc = solve_pair(P.geoA + (uint64_t)e.x * MCX_GEO_STRIDE, P.geoB + (uint64_t)e.y * MCX_GEO_STRIDE, sol);
+  } else {
+    if (valid) rc = moller_reject(P.coordsA, P.NA, P.MA, e.x, P.coordsB, P.NB, P.MB, e.y) ? 2 : 1;
+  }
+  n_pass += valid ? 1 : 0;
+  n_sing += (rc == 2) ? 1 : 0;
+  const bool hit = (rc == 1);
+  const unsigned hm = __ballot_sync(0xffffffffu, hit);
+  if (hm) {
+    const int leader = __ffs(hm) - 1;
+    unsigned long long base = 0;
+    if (lane == leader) base = atomicAdd(P.counters + 0, (unsigned long long)__popc(hm));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (hit) {
+      const unsigned long long pos = base + __popc(hm & ((1u << lane) - 1u));
+      if (pos < P.cap) {
+        if (KIND == KIND_TRI) {
+          mcx_hit h;
+          h.ia = e.x; h.ib = e.y; h.s = sol[0]; h.t = sol[1]; h.a = sol[2]; h.b = sol[3];
+          P.hits[pos] = h;
+        } else {
+          // quad indices qa = i + N1·k1, qb = j + N2·l1 → gid (PAPER.md kernel step 2)
+          const uint64_t i = e.x % P.NA, k1 = e.x / P.NA, j = e.y % P.NB, l1 = e.y / P.NB;
+          const uint64_t n12 = (uint64_t)P.NA * P.NB;
+          P.gids[pos] = i + (uint64_t)P.NA * j + n12 * k1 + n12 * (uint64_t)(P.MA - 1) * l1;
+        }
+      }
+    }
+  }
+}
+
+template <int KIND, class C>
+__global__ void __launch_bounds__(C::THREADS, C::MINB) search_brute_kernel(const SearchParams P) {
+  constexpr int R = C::R, THREADS = C::THREADS;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  SearchSmem<C>& S = *reinterpret_cast<SearchSmem<C>*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  // ---- A block (cyclic shard) and B chunk of this CTA
+  const uint64_t gblk = P.shard_index + (uint64_t)blockIdx.x * P.shard_count;
+  const uint64_t a0 = P.a_begin + gblk * A_BLOCK;
+  const uint64_t b0 = (uint64_t)blockIdx.y * P.b_chunk;
+  const uint64_t b1 = min(b0 + P.b_chunk, P.nB);
+  const int ntiles = (int)((b1 - b0 + TILE - 1) / TILE);
+
+  // ---- mbarrier ring setup + prologue copies (one elected thread)
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&S.full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int s = 0; s < STAGES && s < ntiles; ++s) {
+      const uint64_t tb = b0 + (uint64_t)s * TILE;
+      const uint32_t bytes = (uint32_t)(min((uint64_t)TILE, b1 - tb) * sizeof(Box));
+      mbar_arrive_expect_tx(&S.full[s], bytes);
+      bulk_g2s(&S.tile[s][0], P.boxB + tb, bytes, &S.full[s]);
+    }
+  }
+
+  // ---- A triangles into registers (invalid slots can never overlap)
+  double alo[R][4], ahi[R][4];
+  uint32_t aidx[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const uint64_t ia = a0 + (uint64_t)r * THREADS + tid;
+    aidx[r] = (uint32_t)ia;
+    if (ia < P.a_end) {
+      const double2* src = reinterpret_cast<const double2*>(P.boxA + ia);
+      double2 x0 = __ldg(src + 0), x1 = __ldg(src + 1), x2 = __ldg(src + 2), x3 = __ldg(src + 3);
+      alo[r][0] = x0.x; alo[r][1] = x0.y; alo[r][2] = x1.x; alo[r][3] = x1.y;
+      ahi[r][0] = x2.x; ahi[r][1] = x2.y; ahi[r][2] = x3.x; ahi[r][3] = x3.y;
+    } else {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) { alo[r][c] = __longlong_as_double(0x7ff0000000000000ll); ahi[r][c] = -alo[r][c]; }
+    }
+  }
+
+  uint2* q = S.queue[warp];
+  int qn = 0;
+  unsigned long long n_pass = 0, n_sing = 0;
+  const unsigned lt_mask = (1u << lane) - 1u;
+
+  for (int t = 0; t < ntiles; ++t) {
+    const int s = t % STAGES;
+    mbar_wait(&S.full[s], (uint32_t)((t / STAGES) & 1));
+    const uint64_t tb = b0 + (uint64_t)t * TILE;
+    const int nvalid = (int)min((uint64_t)TILE, b1 - tb);
+    const Box* tile = S.tile[s];
+#pragma unroll 2
+    for (int j = 0; j < nvalid; ++j) {
+      const double2* bp = reinterpret_cast<const double2*>(tile + j);
+      const double2 l01 = bp[0], l23 = bp[1], h01 = bp[2], h23 = bp[3];
+      bool p[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        p[r] = (l01.x <= ahi[r][0]) & (alo[r][0] <= h01.x) & (l01.y <= ahi[r][1]) & (alo[r][1] <= h01.y) &
+               (l23.x <= ahi[r][2]) & (alo[r][2] <= h23.x) & (l23.y <= ahi[r][3]) & (alo[r][3] <= h23.y);
+      }
+      bool any = p[0];
+#pragma unroll
+      for (int r = 1; r < R; ++r) any |= p[r];
+      if (__any_sync(0xffffffffu, any)) {
+        const uint32_t ib = (uint32_t)(tb + j);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const unsigned m = __ballot_sync(0xffffffffu, p[r]);
+          if (p[r]) q[qn + __popc(m & lt_mask)] = make_uint2(aidx[r], ib);
+          qn += __popc(m);
+        }
+        __syncwarp();
+        while (qn >= 32) {
+          qn -= 32;
+          flush_queue<KIND>(P, q + qn, 32, lane, n_pass, n_sing);
+        }
+      }
+    }
+    __syncthreads();  // every warp is done reading stage s
+    if (tid == 0 && t + STAGES < ntiles) {
+      const uint64_t nb = b0 + (uint64_t)(t + STAGES) * TILE;
+      const uint32_t bytes = (uint32_t)(min((uint64_t)TILE, b1 - nb) * sizeof(Box));
+      mbar_arrive_expect_tx(&S.full[s], bytes);
+      bulk_g2s(&S.tile[s][0], P.boxB + nb, bytes, &S.full[s]);
+    }
+  }
+  __syncwarp();
+  if (qn > 0) flush_queue<KIND>(P, q, qn, lane, n_pass, n_sing);
+
+  // ---- per-warp counter reduction
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    n_pass += __shfl_xor_sync(0xffffffffu, n_pass, o);
+    n_sing += __shfl_xor_sync(0xffffffffu, n_sing, o);
+  }
+  if (lane == 0) {
+    if (n_pass) atomicAdd(P.counters + 1, n_pass);
+    if (n_sing) atomicAdd(P.counters + 2, n_sing);
+  }
+}
+
+// --------------------------------------------------------------- host side
+// Grid: x = A blocks of this shard, y = B chunks (multiple of TILE), sized for
+// ~16 waves at 2 CTAs/SM so the tail wave is a small fraction.
+template <int KIND, class C>
+static int launch_brute_cfg(SearchParams P, uint64_t my_blocks, int device, cudaStream_t stream) {
+  if (my_blocks == 0 || P.nB == 0) return MCX_OK;
+  int dev_sms = 148;
+  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device);
+  const uint64_t want = (uint64_t)dev_sms * C::MINB * 16;
+  uint64_t nchunk = (want + my_blocks - 1) / my_blocks;
+  const uint64_t max_chunks = (P.nB + TILE - 1) / TILE;
+  if (nchunk > max_chunks) nchunk = max_chunks;
+  if (nchunk < 1) nchunk = 1;
+  uint64_t chunk = (P.nB + nchunk - 1) / nchunk;
+  chunk = (chunk + TILE - 1) / TILE * TILE;
+  nchunk = (P.nB + chunk - 1) / chunk;
+  if (my_blocks > 0x7fffffffull || nchunk > 65535) return set_error(MCX_E_ARG, "grid too large");
+  P.b_chunk = chunk;
+  const size_t smem = sizeof(SearchSmem<C>);
+  CUDA_TRY(cudaFuncSetAttribute(search_brute_kernel<KIND, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 grid((unsigned)my_blocks, (unsigned)nchunk);
+  search_brute_kernel<KIND, C><<<grid, C::THREADS, smem, stream>>>(P);
+  CUDA_TRY(cudaGetLastError());
+  return MCX_OK;
+}
+
+// Variant selection (experiments: MCX_VARIANT=0..3; default 0).
+static int variant_from_env() {
+  const char* v = getenv("MCX_VARIANT");
+  return v ? atoi(v) : 0;
+}
+
+template <int KIND>
+static int launch_brute(SearchParams P, uint64_t my_blocks, int device, cudaStream_t stream) {
+  switch (variant_from_env()) {
+    case 1: return launch_brute_cfg<KIND, Cfg<4, 2>>(P, my_blocks, device, stream);
+    case 2: return launch_brute_cfg<KIND, Cfg<8, 1>>(P, my_blocks, device, stream);
+    case 3: return launch_brute_cfg<KIND, Cfg<2, 1>>(P, my_blocks, device, stream);
+    default: return launch_brute_cfg<KIND, Cfg<4, 1>>(P, my_blocks, device, stream);
+  }
+}
+
+struct Timing {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  ~Timing() {
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+  }
+};
+
+static int launch_search(const mcx_mesh_dev* A, const mcx_mesh_dev* B, const mcx_opts* o, mcx_hit* hits,
+                         uint64_t cap, mcx_stats* st) {
+  cudaStream_t stream = (cudaStream_t)o->stream;
+  const uint64_t a_begin = o->a_begin;
+  const uint64_t a_end = o->a_end ? o->a_end : A->n_tri;
+  const uint32_t scount = o->shard_count ? o->shard_count : 1;
+  const uint32_t sidx = o->shard_index;
+  if (a_end > A->n_tri || a_begin > a_end)
+    return set_error(MCX_E_ARG, "A range [%llu, %llu) outside [0, %llu)", (unsigned long long)a_begin,
+                     (unsigned long long)a_end, (unsigned long long)A->n_tri);
+  if (sidx >= scount) return set_error(MCX_E_ARG, "shard_index %u >= shard_count %u", sidx, scount);
+  if (A->n_tri >= (1ull << 32) || B->n_tri >= (1ull << 32))
+    return set_error(MCX_E_ARG, "triangle counts must be < 2^32");
+  if (o->mode != MCX_MODE_BRUTE && o->mode != MCX_MODE_CULL) return set_error(MCX_E_ARG, "unknown mode %d", o->mode);
+  if (!o->workspace || o->workspace_bytes < mcx_workspace_bytes(A, B, o))
+    return set_error(MCX_E_ARG, "workspace too small (need %llu bytes)",
+                     (unsigned long long)mcx_workspace_bytes(A, B, o));
+  if (((uintptr_t)A->box | (uintptr_t)B->box | (uintptr_t)A->geo | (uintptr_t)B->geo) & 15)
+    return set_error(MCX_E_ARG, "box/geo pointers must be 16-byte aligned");
+  if (cap > 0 && !hits) return set_error(MCX_E_ARG, "null hit buffer with nonzero capacity");
+
+  unsigned long long* counters = (unsigned long long*)o->workspace;
+  CUDA_TRY(cudaMemsetAsync(counters, 0, 4 * sizeof(unsigned long long), stream));
+
+  const uint64_t nblk_total = (a_end - a_begin + A_BLOCK - 1) / A_BLOCK;
+  const uint64_t my_blocks = nblk_total > sidx ? (nblk_total - sidx + scount - 1) / scount : 0;
+  const uint64_t nB = B->n_tri;
+  uint64_t na = 0;  // A triangles in this shard's blocks
+  if (my_blocks > 0) {
+    na = my_blocks * (uint64_t)A_BLOCK;
+    const uint64_t last = sidx + (my_blocks - 1) * scount;  // only the globally last block can be ragged
+    if (last == nblk_total - 1) na -= (uint64_t)A_BLOCK - ((a_end - a_begin) - last * A_BLOCK);
+  }
+  st->n_pairs = na * nB;
+  st->n_tested = st->n_pairs;
+
+  Timing tm;
+  if (o->timing) {
+    CUDA_TRY(cudaEventCreate(&tm.e0));
+    CUDA_TRY(cudaEventCreate(&tm.e1));
+    CUDA_TRY(cudaEventRecord(tm.e0, stream));
+  }
+  SearchParams P = {};
+  P.boxA = reinterpret_cast<const Box*>(A->box);
+  P.geoA = A->geo;
+  P.boxB = reinterpret_cast<const Box*>(B->box);
+  P.geoB = B->geo;
+  P.a_begin = a_begin;
+  P.a_end = a_end;
+  P.nB = nB;
+  P.shard_index = sidx;
+  P.shard_count = scount;
+  P.hits = hits;
+  P.cap = cap;
+  P.counters = counters;
+  int rc = launch_brute<KIND_TRI>(P, my_blocks, o->device, stream);
+  if (rc != MCX_OK) return rc;
+  if (o->timing) CUDA_TRY(cudaEventRecord(tm.e1, stream));
+  unsigned long long h[4];
+  CUDA_TRY(cudaMemcpyAsync(h, counters, sizeof(h), cudaMemcpyDeviceToHost, stream));
+  CUDA_TRY(cudaStreamSynchronize(stream));
+  st->n_hits = h[0];
+  st->n_aabb_pass = h[1];
+  st->n_singular = h[2];
+  st->kernel_ms = 0.0;
+  if (o->timing) {
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, tm.e0, tm.e1));
+    st->kernel_ms = ms;
+  }
+  if (h[0] > cap) return set_error(MCX_E_CAPACITY, "hit capacity %llu < %llu hits", (unsigned long long)cap, h[0]);
+  return MCX_OK;
+}
+
+// Quad AABBs of a half-layer grid: quad q = i + N·k1 over vertices v00 v10 v01 v11.
+__global__ void quad_box_kernel(const double* __restrict__ coords, uint32_t N, uint32_t M, Box* __restrict__ box) {
+  const uint64_t nq = (uint64_t)N * (M - 1);
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < nq; q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t i = (uint32_t)(q % N), k = (uint32_t)(q / N);
+    const uint32_t ip = (i + 1 == N) ? 0 : i + 1;
+    Box b;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const double* pl = coords + (uint64_t)c * M * N;
+      const double w00 = pl[(uint64_t)k * N + i], w10 = pl[(uint64_t)k * N + ip];
+      const double w01 = pl[(uint64_t)(k + 1) * N + i], w11 = pl[(uint64_t)(k + 1) * N + ip];
+      b.lo[c] = fmin(fmin(fmin(w00, w10), w01), w11);
+      b.hi[c] = fmax(fmax(fmax(w00, w10), w01), w11);
+    }
+    box[q] = b;
+  }
+}
+
+static int launch_pair_candidates(const double* cA, uint32_t NA, uint32_t MA, const double* cB, uint32_t NB,
+                                  uint32_t MB, int device, cudaStream_t stream, void* ws, uint64_t ws_bytes,
+                                  uint64_t* gids, uint64_t cap, uint64_t* n_out) {
+  if (NA < 1 || NB < 1 || MA < 2 || MB < 2) return set_error(MCX_E_ARG, "half-layers need >= 2 columns");
+  const uint64_t nqA = (uint64_t)NA * (MA - 1), nqB = (uint64_t)NB * (MB - 1);
+  if (nqA >= (1ull << 32) || nqB >= (1ull << 32)) return set_error(MCX_E_ARG, "quad counts must be < 2^32");
+  const uint64_t need = 256 + (nqA + nqB) * sizeof(Box);
+  if (!ws || ws_bytes < need)
+    return set_error(MCX_E_ARG, "workspace too small (need %llu bytes)", (unsigned long long)need);
+  unsigned long long* counters = (unsigned long long*)ws;
+  Box* boxA = reinterpret_cast<Box*>((char*)ws + 256);
+  Box* boxB = boxA + nqA;
+  CUDA_TRY(cudaMemsetAsync(counters, 0, 4 * sizeof(unsigned long long), stream));
+  quad_box_kernel<<<(unsigned)min((nqA + 255) / 256, (uint64_t)148 * 64), 256, 0, stream>>>(cA, NA, MA, boxA);
+  quad_box_kernel<<<(unsigned)min((nqB + 255) / 256, (uint64_t)148 * 64), 256, 0, stream>>>(cB, NB, MB, boxB);
+  CUDA_TRY(cudaGetLastError());
+  SearchParams P = {};
+  P.boxA = boxA;
+  P.boxB = boxB;
+  P.a_begin = 0;
+  P.a_end = nqA;
+  P.nB = nqB;
+  P.shard_index = 0;
+  P.shard_count = 1;
+  P.cap = cap;
+  P.counters = counters;
+  P.coordsA = cA;
+  P.coordsB = cB;
+  P.NA = NA; P.MA = MA; P.NB = NB; P.MB = MB;
+  P.gids = gids;
+  int rc = launch_brute<KIND_QUAD>(P, (nqA + A_BLOCK - 1) / A_BLOCK, device, stream);
+  if (rc != MCX_OK) return rc;
+  unsigned long long h[4];
+  CUDA_TRY(cudaMemcpyAsync(h, counters, sizeof(h), cudaMemcpyDeviceToHost, stream));
+  CUDA_TRY(cudaStreamSynchronize(stream));
+  *n_out = h[0];
+  if (h[0] > cap) return set_error(MCX_E_CAPACITY, "candidate capacity %llu < %llu", (unsigned long long)cap, h[0]);
+  return MCX_OK;
+}
+
+thread_local char g_err[512] = "";
+
+}  // namespace mcx
+
+extern "C" {
+
+uint32_t mcx_a_block(void) { return mcx::A_BLOCK; }
+
+uint64_t mcx_workspace_bytes(const mcx_mesh_dev*, const mcx_mesh_dev*, const mcx_opts*) { return 256; }
+
+int mcx_pack(const double* coords, uint32_t N, uint32_t M, double* box, double* geo, int device, void* stream) {
+  using namespace mcx;
+  if (N < 1 || M < 2) return set_error(MCX_E_ARG, "pack needs N >= 1 and M >= 2 (got N=%u, M=%u)", N, M);
+  if (((uintptr_t)box | (uintptr_t)geo) & 15) return set_error(MCX_E_ARG, "box/geo must be 16-byte aligned");
+  CUDA_TRY(cudaSetDevice(device));
+  const uint64_t n = 2ull * N * (M - 1);
+  const int threads = 256;
+  uint64_t blocks = (n + threads - 1) / threads;
+  if (blocks > 148ull * 64) blocks = 148ull * 64;
+  pack_kernel<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(coords, N, M, box, geo);
+  CUDA_TRY(cudaGetLastError());
+  return MCX_OK;
+}
+
+int mcx_search(const mcx_mesh_dev* A, const mcx_mesh_dev* B, const mcx_opts* o, mcx_hit* hits, uint64_t cap,
+               mcx_stats* st) {
+  using namespace mcx;
+  if (!A || !B || !o || !st) return set_error(MCX_E_ARG, "null argument");
+  CUDA_TRY(cudaSetDevice(o->device));
+  return launch_search(A, B, o, hits, cap, st);
+}
+
+int mcx_pair_candidates(const double* coords_a, uint32_t NA, uint32_t MA, const double* coords_b, uint32_t NB,
+                        uint32_t MB, int device, void* stream, void* workspace, uint64_t workspace_bytes,
+                        uint64_t* gids, uint64_t cap, uint64_t* n_out) {
+  using namespace mcx;
+  if (!coords_a || !coords_b || !n_out) return set_error(MCX_E_ARG, "null argument");
+  CUDA_TRY(cudaSetDevice(device));
+  return launch_pair_candidates(coords_a, NA, MA, coords_b, NB, MB, device, (cudaStream_t)stream, workspace,
+                                workspace_bytes, gids, cap, n_out);
+}
+
+const char* mcx_last_error(void) { return mcx::g_err; }
+
+int mcx_version(void) { return MCX_ABI_VERSION; }
+
+}  // extern "C"

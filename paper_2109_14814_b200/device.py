@@ -1,0 +1,256 @@
+"""Device-side orchestration: HBM buffers (torch as the allocator), packing,
+search calls through the C ABI, capacity handling and multi-GPU sharding.
+
+HBM layout per mesh (DESIGN.md §Data layout):
+  coords  (4, M, N) f64  — the half-layer grid as uploaded (32·N·M bytes)
+  box     (n, 8)    f64  — per-triangle AABB lo[4], hi[4] (64 B/tri), the only
+                           array the hot loop streams
+  geo     (n, 20)   f64  — origin, edges, bivector, norm (160 B/tri), read only
+                           for AABB survivors
+Hits come back as (iA, iB, s, t, a, b) records of 40 B.
+
+Multi-GPU: A's triangle range is cut into blocks of
+``mcx_a_block()`` triangles assigned cyclically (block b → GPU b mod G), B is
+replicated, each GPU searches its blocks independently on its own host thread
+and the host concatenates and sorts the small hit lists.  No collective.
+"""
+from __future__ import annotations
+
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import BackendError, CapacityError, ConfigError
+
+HIT_DTYPE = np.dtype([("ia", "<u4"), ("ib", "<u4"), ("s", "<f8"), ("t", "<f8"), ("a", "<f8"), ("b", "<f8")])
+assert HIT_DTYPE.itemsize == 40
+
+_torch = None
+
+
+def torch():
+    global _torch
+    if _torch is None:
+        import torch as _t
+        _torch = _t
+    return _torch
+
+
+def _require_cuda(device: int):
+    t = torch()
+    if not t.cuda.is_available():
+        raise BackendError("backend='cuda' requires a CUDA device (none visible)")
+    if device >= t.cuda.device_count():
+        raise ConfigError(f"device {device} not present ({t.cuda.device_count()} visible)")
+
+
+def _check_coords(coords) -> None:
+    if coords.ndim != 3 or coords.shape[0] != 4:
+        raise ConfigError(f"coords must have shape (4, M, N), got {tuple(coords.shape)}")
+    if coords.shape[1] < 2 or coords.shape[2] < 1:
+        raise ConfigError("a half-layer needs >= 2 columns (SPEC.md:473)")
+
+
+class DeviceMesh:
+    """A half-layer grid resident in HBM, packed into triangle records on the device."""
+
+    def __init__(self, coords, device: int = 0, stream=None):
+        t = torch()
+        _require_cuda(device)
+        dev = t.device("cuda", device)
+        if isinstance(coords, np.ndarray):
+            _check_coords(coords)
+            if not np.all(np.isfinite(coords)):
+                raise ConfigError("mesh coordinates must be finite (NaN/Inf would break the AABB contract)")
+            host = t.from_numpy(np.ascontiguousarray(coords, dtype=np.float64))
+            with t.cuda.device(device):
+                s = stream or t.cuda.current_stream(device)
+                with t.cuda.stream(s):
+                    self.coords = host.to(dev, non_blocking=True)
+        else:
+            _check_coords(coords)
+            self.coords = coords.to(dev, dtype=t.float64).contiguous()
+        self.device = device
+        _, self.M, self.N = (int(v) for v in self.coords.shape)
+        self.n_tri = 2 * self.N * (self.M - 1)
+        if self.n_tri >= 2 ** 32:
+            raise ConfigError("triangle count must be < 2^32")
+        self.box = t.empty((self.n_tri, _lib.BOX_STRIDE), dtype=t.float64, device=dev)
+        self.geo = t.empty((self.n_tri, _lib.GEO_STRIDE), dtype=t.float64, device=dev)
+        L = _lib.load()
+        s = stream or t.cuda.current_stream(device)
+        rc = L.mcx_pack(self.coords.data_ptr(), self.N, self.M, self.box.data_ptr(), self.geo.data_ptr(),
+                        device, s.cuda_stream)
+        _lib.check(rc, "mcx_pack")
+
+    def struct(self) -> _lib.MeshDev:
+        return _lib.MeshDev(self.n_tri, self.box.data_ptr(), self.geo.data_ptr())
+
+
+@dataclass
+class SearchResult:
+    hits: np.ndarray       # HIT_DTYPE, sorted by (ia, ib)
+    stats: dict
+
+    @property
+    def ia(self):
+        return self.hits["ia"]
+
+    @property
+    def ib(self):
+        return self.hits["ib"]
+
+
+class _Workspace:
+    """Per-device scratch (counters) and a growable hit buffer, reused across calls."""
+
+    _per_thread = threading.local()
+
+    @classmethod
+    def get(cls, device: int):
+        cache = getattr(cls._per_thread, "cache", None)
+        if cache is None:
+            cache = cls._per_thread.cache = {}
+        if device not in cache:
+            cache[device] = cls(device)
+        return cache[device]
+
+    def __init__(self, device: int):
+        t = torch()
+        self.device = device
+        self.ws = t.empty(1 << 16, dtype=t.uint8, device=t.device("cuda", device))
+        self.hits = None
+
+    def hit_buffer(self, cap: int):
+        t = torch()
+        if self.hits is None or self.hits.numel() < cap * 5:
+            self.hits = t.empty(max(cap, 1) * 5, dtype=t.float64, device=t.device("cuda", self.device))
+        return self.hits
+
+    def workspace(self, nbytes: int):
+        t = torch()
+        if self.ws.numel() < nbytes:
+            self.ws = t.empty(nbytes, dtype=t.uint8, device=t.device("cuda", self.device))
+        return self.ws
+
+
+def search_device(A: DeviceMesh, B: DeviceMesh, *, mode: int = _lib.MODE_BRUTE, a_range=None,
+                  shard=(0, 1), cap: int = 1 << 16, timing: bool = False, stream=None, task=None,
+                  sort: bool = True) -> SearchResult:
+    """Run one search call on A.device; grows the hit buffer and reruns on overflow."""
+    t = torch()
+    if A.device != B.device:
+        raise ConfigError("A and B must live on the same device")
+    L = _lib.load()
+    s = stream or t.cuda.current_stream(A.device)
+    W = _Workspace.get(A.device)
+    a0, a1 = (0, 0) if a_range is None else (int(a_range[0]), int(a_range[1]))
+    opts = _lib.Opts(A.device, s.cuda_stream, a0, a1, int(shard[0]), int(shard[1]), int(mode), int(timing), None, 0)
+    As, Bs = A.struct(), B.struct()
+    need = L.mcx_workspace_bytes(As, Bs, opts)
+    ws = W.workspace(need)
+    opts.workspace = ws.data_ptr()
+    opts.workspace_bytes = ws.numel()
+    st = _lib.Stats()
+    for _attempt in range(3):
+        buf = W.hit_buffer(cap)
+        cap_eff = buf.numel() // 5
+        rc = L.mcx_search(As, Bs, opts, buf.data_ptr(), cap_eff, st)
+        if rc == _lib.MCX_E_CAPACITY:
+            cap = int(st.n_hits) + 1024
+            continue
+        _lib.check(rc, "mcx_search", task=task)
+        break
+    else:
+        raise CapacityError("hit buffer overflow persisted after regrowing", required=int(st.n_hits), task=task)
+    n = int(st.n_hits)
+    raw = buf[: n * 5].cpu().numpy() if n else np.zeros(0)
+    hits = raw.view(HIT_DTYPE).copy() if n else np.zeros(0, HIT_DTYPE)
+    if sort and n:
+        hits = hits[np.lexsort((hits["ib"], hits["ia"]))]
+    return SearchResult(hits=hits, stats=st.as_dict())
+
+
+def _merge(results) -> SearchResult:
+    hits = np.concatenate([r.hits for r in results]) if results else np.zeros(0, HIT_DTYPE)
+    hits = hits[np.lexsort((hits["ib"], hits["ia"]))]
+    stats = {}
+    for r in results:
+        for k, v in r.stats.items():
+            stats[k] = stats.get(k, 0) + v
+    if results:
+        stats["kernel_ms"] = max(r.stats["kernel_ms"] for r in results)
+    return SearchResult(hits=hits, stats=stats)
+
+
+def search(coords_a, coords_b, *, devices=(0,), mode: int = _lib.MODE_BRUTE, timing: bool = False,
+           task=None) -> SearchResult:
+    """Host-to-host triangle search: upload, pack, search (sharded over ``devices``), gather, sort."""
+    devices = list(devices)
+    if not devices:
+        raise ConfigError("devices must be non-empty")
+    for d in devices:
+        _require_cuda(d)
+    G = len(devices)
+    results = [None] * G
+    errors = [None] * G
+
+    def run(rank: int):
+        try:
+            d = devices[rank]
+            t = torch()
+            with t.cuda.device(d):
+                A = DeviceMesh(coords_a, d)
+                B = DeviceMesh(coords_b, d)
+                results[rank] = search_device(A, B, mode=mode, shard=(rank, G), timing=timing, task=task)
+        except Exception as exc:  # surfaced below with the task id
+            errors[rank] = exc
+
+    if G == 1:
+        run(0)
+    else:
+        threads = [threading.Thread(target=run, args=(r,)) for r in range(G)]
+        for th in threads:
+            th.start()
+        for th in threads:
+            th.join()
+    for e in errors:
+        if e is not None:
+            raise e
+    return _merge(results)
+
+
+def pair_candidates_device(coords_a, coords_b, device: int = 0, cap: int = 1 << 16, task=None) -> np.ndarray:
+    """Sorted u64 quad-pair gids surviving ¬aabb_reject ∧ ¬moller_reject."""
+    t = torch()
+    _require_cuda(device)
+    L = _lib.load()
+    dev = t.device("cuda", device)
+    with t.cuda.device(device):
+        ca = t.from_numpy(np.ascontiguousarray(coords_a, dtype=np.float64)).to(dev)
+        cb = t.from_numpy(np.ascontiguousarray(coords_b, dtype=np.float64)).to(dev)
+        _, MA, NA = ca.shape
+        _, MB, NB = cb.shape
+        nq = NA * (MA - 1) + NB * (MB - 1)
+        ws = t.empty(256 + 64 * nq, dtype=t.uint8, device=dev)
+        s = t.cuda.current_stream(device)
+        n_out = ctypes_u64()
+        for _ in range(3):
+            gids = t.empty(max(cap, 1), dtype=t.int64, device=dev)
+            rc = L.mcx_pair_candidates(ca.data_ptr(), NA, MA, cb.data_ptr(), NB, MB, device, s.cuda_stream,
+                                       ws.data_ptr(), ws.numel(), gids.data_ptr(), cap, n_out)
+            if rc == _lib.MCX_E_CAPACITY:
+                cap = int(n_out.value) + 1024
+                continue
+            _lib.check(rc, "mcx_pair_candidates", task=task)
+            break
+        n = int(n_out.value)
+        out = gids[:n].cpu().numpy().view(np.uint64)
+    return np.sort(out)
+
+
+def ctypes_u64():
+    import ctypes
+    return ctypes.c_uint64(0)
