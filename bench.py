@@ -1,0 +1,319 @@
+#!/usr/bin/env python
+"""Benchmark: triangle-pair tests/s and full-search wall time of the 4D
+mesh-intersection search (BASELINE.json metric) on N B200s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
+
+One step = one complete search of mesh A against mesh B (every triangle pair
+gets the AABB test, survivors the canonical FP64 solve, hits compacted) for the
+named synthetic configuration (default C3: 1024×512 vs 1024×512 grids,
+1,046,528 triangles each, 1.095e12 pairs).  Under torchrun each rank owns one
+GPU and searches its cyclic share of A's 1024-triangle blocks (no collective on
+the data path); timing is the max over ranks of CUDA-event device time.
+
+``--impl reference`` times the reference's CPU search (the C port of the
+SPEC's all-pairs "parallel" backend, oracle/mcx_oracle.c, all host threads) on a
+bounded deterministic slice of the same workload; see DESIGN.md §Measurement.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "triangle-pair tests/s"
+UNIT = "pair-tests/s"
+FP64_LANES_PER_CLK_PER_SM = 64  # B200 FP64 pipe; verified by tools/microbench/pipes.cu (dadd 63.5)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--mode", default="brute", choices=["brute", "cull"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU-baseline sample duration")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def workload_desc(name, A, B):
+    nA = 2 * A.shape[2] * (A.shape[1] - 1)
+    nB = 2 * B.shape[2] * (B.shape[1] - 1)
+    return {"workload": f"{name}: synthetic 4D mesh pair, A {A.shape[2]}x{A.shape[1]} grid ({nA} tri) vs "
+                        f"B {B.shape[2]}x{B.shape[1]} grid ({nB} tri), float64",
+            "triangles_a": nA, "triangles_b": nB, "pairs_per_step": nA * nB}
+
+
+# ------------------------------------------------------------------ CPU baseline
+def cpu_reference_sample(A, B, target_s, threads=0):
+    """Time the C port of the SPEC all-pairs search (brute force, all threads) on a
+    deterministic slice A[0, n) × all of B, sized to ~target_s seconds."""
+    from oracle import c_oracle
+    c_oracle.build()
+    nB = 2 * B.shape[2] * (B.shape[1] - 1)
+    nA = 2 * A.shape[2] * (A.shape[1] - 1)
+    n = min(nA, 256)
+    t0 = time.perf_counter()
+    c_oracle.search(A, B, a_range=(0, n), sweep=False, threads=threads)
+    dt = time.perf_counter() - t0
+    # the call includes packing both meshes; estimate pack time with an empty slice
+    t1 = time.perf_counter()
+    c_oracle.search(A, B, a_range=(0, 0), sweep=False, threads=threads)
+    pack = time.perf_counter() - t1
+    rate = n * nB / max(dt - pack, 1e-6)
+    n = int(min(nA, max(256, rate * target_s / nB)))
+    t0 = time.perf_counter()
+    r = c_oracle.search(A, B, a_range=(0, n), sweep=False, threads=threads)
+    dt = time.perf_counter() - t0 - pack
+    return {"value": n * nB / dt, "seconds": dt, "a_triangles": n, "pairs": n * nB, "hits": len(r["ia"]),
+            "threads": c_oracle.max_threads() if threads == 0 else threads, "pack_seconds": pack}
+
+
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2109_14814_b200.mesh import config_pair
+    A, _, B, _ = config_pair(args.config)
+    desc = workload_desc(args.config, A, B)
+    cores = len(os.sched_getaffinity(0))
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    for _ in range(max(0, args.warmup)):
+        cpu_reference_sample(A, B, min(2.0, args.cpu_seconds / 4))
+    vals, secs = [], []
+    for _ in range(max(1, args.steps)):
+        s = cpu_reference_sample(A, B, args.cpu_seconds / max(1, args.steps))
+        vals.append(s["value"])
+        secs.append(s["seconds"])
+    v = statistics.median(vals)
+    sample = (f"A triangles [0, {s['a_triangles']}) x all {desc['triangles_b']} B triangles per step "
+              f"({s['pairs']:.3e} pairs, brute force, packing excluded); full search extrapolated linearly")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": desc["pairs_per_step"] / v * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {**desc, "mode": "brute"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": s["threads"], "kind": "port",
+                             "sample": sample, "cpu": cpu_model()},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "search_wall_s_extrapolated": desc["pairs_per_step"] / v}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    def __init__(self, index):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[0]))
+                mx.append(float(r[1]))
+            except (ValueError, IndexError):
+                continue
+            for n, v in zip(names, r[4:8]):
+                if v.strip().lower() in ("active", "1"):
+                    reasons.add(n)
+        load = [v for v in sm if v > 500] or sm
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2109_14814_b200 import _lib, device as D
+    from paper_2109_14814_b200.mesh import config_pair
+
+    rank, world, local = dist_env()
+    if world != args.gpus and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    A, sa, B, sb = config_pair(args.config)
+    desc = workload_desc(args.config, A, B)
+    mode = {"brute": _lib.MODE_BRUTE, "cull": _lib.MODE_CULL}[args.mode]
+    shard = (rank, world)
+
+    stream = torch.cuda.current_stream(dev)
+    Am, Bm = D.DeviceMesh(A, local), D.DeviceMesh(B, local)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    # ---- device-resident search (value)
+    for _ in range(args.warmup):
+        res = D.search_device(Am, Bm, mode=mode, shard=shard, stream=stream)
+    barrier()
+    clk = ClockSampler(local) if rank == 0 else None
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches = 0
+    my_pairs = 0
+    for k in range(args.steps):
+        flush.zero_()  # L2 flush between timed steps (outside the events)
+        ev[k][0].record(stream)
+        res = D.search_device(Am, Bm, mode=mode, shard=shard, stream=stream)
+        ev[k][1].record(stream)
+        launches += 1
+        my_pairs += res.stats["n_pairs"]
+    barrier()
+    clocks = clk.stop() if clk else None
+    dev_ms = sum(s.elapsed_time(e) for s, e in ev)
+    t_max = max_over_ranks(dev_ms)
+    total_pairs = sum_over_ranks(my_pairs)
+    n_hits = int(sum_over_ranks(len(res.hits)))
+    value = total_pairs / (t_max * 1e-3)
+    ms_per_step = t_max / args.steps
+
+    # ---- roofline of the search kernel (kernel-only events, one more launch)
+    st = D.search_device(Am, Bm, mode=mode, shard=shard, stream=stream, timing=True).stats
+    kern_ms = max_over_ranks(st["kernel_ms"])
+    props = torch.cuda.get_device_properties(dev)
+    sms = props.multi_processor_count
+    f_max = (clocks or {}).get("sm_max_mhz") or 1965.0
+    f_run = (clocks or {}).get("sm_mhz") or f_max
+    lane_ops = 8.0 * st["n_tested"] + 100.0 * st["n_aabb_pass"]
+    achieved = lane_ops / (st["kernel_ms"] * 1e-3) / 1e12
+    peak = sms * FP64_LANES_PER_CLK_PER_SM * f_max * 1e6 / 1e12
+    peak_run = sms * FP64_LANES_PER_CLK_PER_SM * f_run * 1e6 / 1e12
+    roofline = {"bound": "fp64_pipe", "achieved": achieved, "peak": peak, "unit": "Tlane-op/s",
+                "frac": achieved / peak, "frac_at_observed_clock": achieved / peak_run,
+                "peak_source": f"{sms} SMs x {FP64_LANES_PER_CLK_PER_SM} FP64 lanes/clk x {f_max:.0f} MHz "
+                               "(measured: DADD 63.5 lanes/clk/SM, profiles/r01_pipes.jsonl)",
+                "work_per_pair": "8 FP64 compares (AABB) + ~100 FP64 ops per AABB survivor",
+                "kernel_ms": st["kernel_ms"], "traffic": None,
+                "traffic_note": "ncu dram__bytes per launch: see profiles/r01_ncu_brute_c2.txt"}
+
+    # ---- end to end through the public API, host buffers (e2e)
+    e2e = None
+    if not args.no_e2e:
+        pa = torch.from_numpy(np.ascontiguousarray(A)).pin_memory()
+        pb = torch.from_numpy(np.ascontiguousarray(B)).pin_memory()
+        h2d = (pa.numel() + pb.numel()) * 8
+
+        def e2e_step():
+            Ad, Bd = D.DeviceMesh(pa, local), D.DeviceMesh(pb, local)
+            r = D.search_device(Ad, Bd, mode=mode, shard=shard, stream=stream)
+            return r
+
+        for _ in range(max(1, args.warmup // 2)):
+            e2e_step()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        d2h = 0
+        e0.record(stream)
+        for _ in range(args.steps):
+            r = e2e_step()
+            d2h += 32 + 40 * len(r.hits)
+        e1.record(stream)
+        barrier()
+        e_ms = max_over_ranks(e0.elapsed_time(e1))
+        e2e = {"value": total_pairs / (e_ms * 1e-3), "unit": UNIT, "ms_per_step": e_ms / args.steps,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h // args.steps,
+               "path": "device.search path: pinned host grids -> H2D -> mcx_pack -> mcx_search -> D2H hits"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        s = cpu_reference_sample(A, B, args.cpu_seconds)
+        cpu = {"value": s["value"], "unit": UNIT, "cores": s["threads"], "kind": "port",
+               "sample": f"C port of the SPEC all-pairs search, A triangles [0, {s['a_triangles']}) x all B "
+                         f"({s['pairs']:.3e} pairs, {s['seconds']:.1f} s, packing excluded)", "cpu": cpu_model()}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {**desc, "mode": args.mode, "parallelism": f"A-block cyclic shards x{world}, B replicated",
+                           "l2": "flushed between timed steps (256 MiB write, outside the events)"},
+                "search_wall_s": ms_per_step / 1e3, "hits": n_hits, "kernel_ms": kern_ms,
+                "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks,
+                "gpu_launches": launches, "gpu": props.name, "sms": sms}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

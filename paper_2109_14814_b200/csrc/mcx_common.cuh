@@ -70,6 +70,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// Non-coherent 16-byte load that the compiler cannot CSE (used to rematerialise
+// register-resident data instead of keeping it live across a rare slow path).
+__device__ __forceinline__ void ld_nc_v2(const double* p, double& x, double& y) {
+  asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "l"(p));
+}
+
 // ------------------------------------------------------- canonical FP64 solve
 // FMA-free, fixed association order; see oracle/canonical.py:solve_pairs.
 #define MCX_SING_RTOL 1e-12
@@ -94,47 +100,47 @@ __device__ __forceinline__ double dot4(const double c[4], const double x[4]) {
   return d;
 }
 
-__device__ __forceinline__ void load_geo(const double* __restrict__ g, double out[20]) {
-  const double2* p = reinterpret_cast<const double2*>(g);
-#pragma unroll
-  for (int k = 0; k < 10; ++k) {
-    const double2 v = __ldg(p + k);
-    out[2 * k] = v.x;
-    out[2 * k + 1] = v.y;
-  }
+__device__ __forceinline__ void ld4(const double* __restrict__ g, double o[4]) {
+  const double2 a = __ldg(reinterpret_cast<const double2*>(g));
+  const double2 b = __ldg(reinterpret_cast<const double2*>(g) + 1);
+  o[0] = a.x; o[1] = a.y; o[2] = b.x; o[3] = b.y;
 }
 
 // Returns 0 = miss, 1 = hit (sol = s, t, a, b), 2 = singular (gate).
+// Geometry is loaded in stages so the live set stays small (the op sequence is
+// fixed by the data dependences, not by the load order).
 __device__ __forceinline__ int solve_pair(const double* __restrict__ gA, const double* __restrict__ gB,
                                           double sol[4]) {
-  double A[20], B[20];
-  load_geo(gA, A);
-  load_geo(gB, B);
-  const double* p = A;
-  const double* e1 = A + 4;
-  const double* e2 = A + 8;
-  const double* Pa = A + 12;
-  const double* q = B;
-  const double* f1 = B + 4;
-  const double* f2 = B + 8;
-  const double* Qb = B + 12;
-  double r[4];
+  double r[4], p[4], q[4];
+  ld4(gA, p);
+  ld4(gB, q);
 #pragma unroll
   for (int c = 0; c < 4; ++c) r[c] = dsub(q[c], p[c]);
+  double Pa[6], Qb[6];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    Pa[k] = __ldg(gA + 12 + k);
+    Qb[k] = __ldg(gB + 12 + k);
+  }
   double D = dsub(dmul(Pa[0], Qb[5]), dmul(Pa[1], Qb[4]));
   D = dadd(D, dmul(Pa[2], Qb[3]));
   D = dadd(D, dmul(Pa[3], Qb[2]));
   D = dsub(D, dmul(Pa[4], Qb[1]));
   D = dadd(D, dmul(Pa[5], Qb[0]));
-  const double thr = dmul(dmul(A[18], B[18]), MCX_SING_RTOL);
+  const double thr = dmul(dmul(__ldg(gA + 18), __ldg(gB + 18)), MCX_SING_RTOL);
   if (fabs(D) <= thr) return 2;
   double g[4], h[4];
   contract(r, Qb, g);
   contract(r, Pa, h);
-  const double s = __ddiv_rn(dot4(g, e2), D);
-  const double t = __ddiv_rn(-dot4(g, e1), D);
-  const double a = __ddiv_rn(-dot4(h, f2), D);
-  const double b = __ddiv_rn(dot4(h, f1), D);
+  double x[4];
+  ld4(gA + 8, x);   // e2
+  const double s = __ddiv_rn(dot4(g, x), D);
+  ld4(gA + 4, x);   // e1
+  const double t = __ddiv_rn(-dot4(g, x), D);
+  ld4(gB + 8, x);   // f2
+  const double a = __ddiv_rn(-dot4(h, x), D);
+  ld4(gB + 4, x);   // f1
+  const double b = __ddiv_rn(dot4(h, x), D);
   if (s >= 0.0 && t >= 0.0 && a >= 0.0 && b >= 0.0 && dadd(s, t) <= 1.0 && dadd(a, b) <= 1.0) {
     sol[0] = s;
     sol[1] = t;

@@ -205,23 +205,33 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_brute_kernel(const
     }
   }
 
-  // ---- A triangles into registers (invalid slots can never overlap)
+  // ---- A triangles into registers (invalid slots can never overlap).  Reloaded
+  // (volatile, so never CSE'd) after every survivor flush: that makes the A boxes
+  // dead across the solve, so the rare slow path can use their registers and the
+  // hot loop keeps <= 128 registers (2 CTAs/SM) without spilling.
   double alo[R][4], ahi[R][4];
   uint32_t aidx[R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const uint64_t ia = a0 + (uint64_t)r * THREADS + tid;
-    aidx[r] = (uint32_t)ia;
-    if (ia < P.a_end) {
-      const double2* src = reinterpret_cast<const double2*>(P.boxA + ia);
-      double2 x0 = __ldg(src + 0), x1 = __ldg(src + 1), x2 = __ldg(src + 2), x3 = __ldg(src + 3);
-      alo[r][0] = x0.x; alo[r][1] = x0.y; alo[r][2] = x1.x; alo[r][3] = x1.y;
-      ahi[r][0] = x2.x; ahi[r][1] = x2.y; ahi[r][2] = x3.x; ahi[r][3] = x3.y;
-    } else {
+  for (int r = 0; r < R; ++r) aidx[r] = (uint32_t)(a0 + (uint64_t)r * THREADS + tid);
+  auto load_a = [&]() {
 #pragma unroll
-      for (int c = 0; c < 4; ++c) { alo[r][c] = __longlong_as_double(0x7ff0000000000000ll); ahi[r][c] = -alo[r][c]; }
+    for (int r = 0; r < R; ++r) {
+      if (aidx[r] < P.a_end) {
+        const double* src = reinterpret_cast<const double*>(P.boxA + aidx[r]);
+        ld_nc_v2(src + 0, alo[r][0], alo[r][1]);
+        ld_nc_v2(src + 2, alo[r][2], alo[r][3]);
+        ld_nc_v2(src + 4, ahi[r][0], ahi[r][1]);
+        ld_nc_v2(src + 6, ahi[r][2], ahi[r][3]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          alo[r][c] = __longlong_as_double(0x7ff0000000000000ll);
+          ahi[r][c] = -alo[r][c];
+        }
+      }
     }
-  }
+  };
+  load_a();
 
   uint2* q = S.queue[warp];
   int qn = 0;
@@ -234,7 +244,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_brute_kernel(const
     const uint64_t tb = b0 + (uint64_t)t * TILE;
     const int nvalid = (int)min((uint64_t)TILE, b1 - tb);
     const Box* tile = S.tile[s];
-#pragma unroll 2
+#pragma unroll 4
     for (int j = 0; j < nvalid; ++j) {
       const double2* bp = reinterpret_cast<const double2*>(tile + j);
       const double2 l01 = bp[0], l23 = bp[1], h01 = bp[2], h23 = bp[3];
@@ -256,9 +266,12 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_brute_kernel(const
           qn += __popc(m);
         }
         __syncwarp();
-        while (qn >= 32) {
-          qn -= 32;
-          flush_queue<KIND>(P, q + qn, 32, lane, n_pass, n_sing);
+        if (qn >= 32) {
+          do {
+            qn -= 32;
+            flush_queue<KIND>(P, q + qn, 32, lane, n_pass, n_sing);
+          } while (qn >= 32);
+          load_a();
         }
       }
     }
@@ -311,7 +324,8 @@ static int launch_brute_cfg(SearchParams P, uint64_t my_blocks, int device, cuda
   return MCX_OK;
 }
 
-// Variant selection (experiments: MCX_VARIANT=0..3; default 0).
+// Variant selection (MCX_VARIANT=0..3, for experiments; 0 = the tuned default:
+// R = 4, 256 threads, 2 CTAs/SM, 117 registers, no spills).
 static int variant_from_env() {
   const char* v = getenv("MCX_VARIANT");
   return v ? atoi(v) : 0;
@@ -320,10 +334,10 @@ static int variant_from_env() {
 template <int KIND>
 static int launch_brute(SearchParams P, uint64_t my_blocks, int device, cudaStream_t stream) {
   switch (variant_from_env()) {
-    case 1: return launch_brute_cfg<KIND, Cfg<4, 2>>(P, my_blocks, device, stream);
+    case 1: return launch_brute_cfg<KIND, Cfg<4, 1>>(P, my_blocks, device, stream);
     case 2: return launch_brute_cfg<KIND, Cfg<8, 1>>(P, my_blocks, device, stream);
     case 3: return launch_brute_cfg<KIND, Cfg<2, 1>>(P, my_blocks, device, stream);
-    default: return launch_brute_cfg<KIND, Cfg<4, 1>>(P, my_blocks, device, stream);
+    default: return launch_brute_cfg<KIND, Cfg<4, 2>>(P, my_blocks, device, stream);
   }
 }
 

@@ -60,18 +60,17 @@ class DeviceMesh:
         t = torch()
         _require_cuda(device)
         dev = t.device("cuda", device)
+        s = stream or t.cuda.current_stream(device)
+        _check_coords(coords)
         if isinstance(coords, np.ndarray):
-            _check_coords(coords)
             if not np.all(np.isfinite(coords)):
                 raise ConfigError("mesh coordinates must be finite (NaN/Inf would break the AABB contract)")
-            host = t.from_numpy(np.ascontiguousarray(coords, dtype=np.float64))
-            with t.cuda.device(device):
-                s = stream or t.cuda.current_stream(device)
-                with t.cuda.stream(s):
-                    self.coords = host.to(dev, non_blocking=True)
-        else:
-            _check_coords(coords)
-            self.coords = coords.to(dev, dtype=t.float64).contiguous()
+            coords = t.from_numpy(np.ascontiguousarray(coords, dtype=np.float64))
+        elif coords.device.type == "cpu" and not bool(t.isfinite(coords).all()):
+            raise ConfigError("mesh coordinates must be finite (NaN/Inf would break the AABB contract)")
+        with t.cuda.device(device), t.cuda.stream(s):
+            pinned = coords.device.type == "cpu" and coords.is_pinned()
+            self.coords = coords.to(dev, dtype=t.float64, non_blocking=pinned).contiguous()
         self.device = device
         _, self.M, self.N = (int(v) for v in self.coords.shape)
         self.n_tri = 2 * self.N * (self.M - 1)
@@ -80,7 +79,6 @@ class DeviceMesh:
         self.box = t.empty((self.n_tri, _lib.BOX_STRIDE), dtype=t.float64, device=dev)
         self.geo = t.empty((self.n_tri, _lib.GEO_STRIDE), dtype=t.float64, device=dev)
         L = _lib.load()
-        s = stream or t.cuda.current_stream(device)
         rc = L.mcx_pack(self.coords.data_ptr(), self.N, self.M, self.box.data_ptr(), self.geo.data_ptr(),
                         device, s.cuda_stream)
         _lib.check(rc, "mcx_pack")
@@ -254,3 +252,32 @@ def pair_candidates_device(coords_a, coords_b, device: int = 0, cap: int = 1 << 
 def ctypes_u64():
     import ctypes
     return ctypes.c_uint64(0)
+
+
+# ------------------------------------------------------------ multi-process helpers
+def shard_ranges(n_tri: int, rank: int, world: int, a_block: int | None = None):
+    """A-triangle ranges owned by ``rank`` under the kernel's cyclic block sharding
+    (block b of ``mcx_a_block()`` triangles → rank b mod world)."""
+    if not (0 <= rank < world):
+        raise ConfigError(f"rank {rank} outside world of {world}")
+    if a_block is None:
+        a_block = int(_lib.load().mcx_a_block())
+    nblk = (n_tri + a_block - 1) // a_block
+    return [(b * a_block, min((b + 1) * a_block, n_tri)) for b in range(rank, nblk, world)]
+
+
+def gather_hits(hits: np.ndarray, dst: int = 0, group=None):
+    """Gather every rank's (small) hit list to ``dst`` over torch.distributed and
+    return the merged, (iA, iB)-sorted list there (None on other ranks).  This is
+    result collection after the independent shard searches, not a data-path
+    collective; it works over gloo (CPU tests) and nccl."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    objs = [None] * world if rank == dst else None
+    dist.gather_object(np.ascontiguousarray(hits).tobytes(), objs, dst=dst, group=group)
+    if rank != dst:
+        return None
+    merged = np.concatenate([np.frombuffer(b, dtype=HIT_DTYPE) for b in objs]) if objs else np.zeros(0, HIT_DTYPE)
+    return merged[np.lexsort((merged["ib"], merged["ia"]))]

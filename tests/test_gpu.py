@@ -1,0 +1,214 @@
+"""GPU parity tests (B200): the CUDA path through the C ABI against the oracles.
+
+Bar: the sorted (iA, iB) hit set is bit-exact, and so are
+s, t, a, b (identical canonical IEEE op sequence), and the AABB-pass / singular
+counters equal the oracle's.  At full sizes parity uses the C oracle's exact
+sweep-and-prune (same predicate, only skips x-disjoint pairs) plus
+size-independent properties: partition / shard / variant invariance.
+"""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from oracle import canonical as O  # noqa: E402
+from oracle import serial as S  # noqa: E402
+from paper_2109_14814_b200 import _lib, device as D, isect  # noqa: E402
+from paper_2109_14814_b200.mesh import config_pair, manifold_like  # noqa: E402
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _bits(x):
+    return np.asarray(x, dtype=np.float64).view(np.uint64)
+
+
+def assert_same_hits(ref, hits, stats=None):
+    assert np.array_equal(ref["ia"], hits["ia"]), "iA differ"
+    assert np.array_equal(ref["ib"], hits["ib"]), "iB differ"
+    for f in "stab":
+        assert np.array_equal(_bits(ref[f]), _bits(hits[f])), f"{f} not bit-exact"
+    if stats is not None:
+        assert stats["n_aabb_pass"] == ref["n_aabb_pass"]
+        assert stats["n_singular"] == ref["n_singular"]
+        assert stats["n_hits"] == len(ref["ia"])
+
+
+@pytest.fixture(scope="module")
+def c1():
+    z = np.load(os.path.join(GOLD, "c1.npz"))
+    return z
+
+
+def test_device_pack_bit_exact(c1):
+    m = D.DeviceMesh(c1["A"], 0)
+    pk = O.pack(c1["A"])
+    box, geo = m.box.cpu().numpy(), m.geo.cpu().numpy()
+    assert np.array_equal(_bits(box[:, :4]), _bits(pk["lo"])) and np.array_equal(_bits(box[:, 4:]), _bits(pk["hi"]))
+    for k, sl in (("p", slice(0, 4)), ("e1", slice(4, 8)), ("e2", slice(8, 12)), ("P", slice(12, 18))):
+        assert np.array_equal(_bits(geo[:, sl]), _bits(pk[k])), k
+    assert np.array_equal(_bits(geo[:, 18]), _bits(pk["nrm"]))
+
+
+def test_golden_c1(c1):
+    r = D.search(c1["A"], c1["B"])
+    ref = {"ia": c1["ia"], "ib": c1["ib"], "n_aabb_pass": int(c1["n_aabb_pass"]),
+           "n_singular": int(c1["n_singular"])}
+    for f in "stab":
+        ref[f] = c1[f].view(np.float64)
+    assert_same_hits(ref, r.hits, r.stats)
+
+
+def test_golden_c4ii_exact_lattice():
+    z = np.load(os.path.join(GOLD, "c4ii.npz"))
+    r = D.search(z["A"], z["B"])
+    ref = {"ia": z["ia"], "ib": z["ib"], "n_aabb_pass": int(z["n_aabb_pass"]), "n_singular": int(z["n_singular"])}
+    for f in "stab":
+        ref[f] = z[f].view(np.float64)
+    assert_same_hits(ref, r.hits, r.stats)
+
+
+@pytest.mark.parametrize("name", ["C1", "C4i", "C4ii", "C4iii"])
+def test_parity_small(name, oracle_lib):
+    A, _, B, _ = config_pair(name)
+    ref = oracle_lib.search(A, B, sweep=True)
+    r = D.search(A, B)
+    assert_same_hits(ref, r.hits, r.stats)
+    assert r.stats["n_pairs"] == A.shape[2] * (A.shape[1] - 1) * 2 * B.shape[2] * (B.shape[1] - 1) * 2
+
+
+@pytest.mark.parametrize("variant", ["0", "1", "2", "3"])
+def test_kernel_variants_identical(variant, monkeypatch, oracle_lib):
+    monkeypatch.setenv("MCX_VARIANT", variant)
+    A, _, B, _ = config_pair("C4i")
+    ref = oracle_lib.search(A, B, sweep=True)
+    r = D.search(A, B)
+    assert_same_hits(ref, r.hits, r.stats)
+
+
+def test_parity_c2_full(oracle_lib):
+    """C2 (256×256 each, 1.7e10 pairs) against the C oracle's exact sweep-and-prune."""
+    A, _, B, _ = config_pair("C2")
+    ref = oracle_lib.search(A, B, sweep=True)
+    r = D.search(A, B)
+    assert_same_hits(ref, r.hits, r.stats)
+
+
+def test_parity_c5_reduced(oracle_lib):
+    """C5 at 1/8 scale: unbalanced 256×129 vs 32×17, hits concentrated in A's first columns."""
+    A, _, B, _ = config_pair("C5/8")
+    ref = oracle_lib.search(A, B, sweep=True)
+    r = D.search(A, B)
+    assert_same_hits(ref, r.hits, r.stats)
+    assert len(ref["ia"]) > 50
+
+
+@pytest.mark.parametrize("G", [2, 3, 8])
+def test_shard_invariance(G, oracle_lib):
+    """Cyclic A-block sharding (the multi-GPU partition) never changes the hit set."""
+    A, _, B, _ = config_pair("C4i")
+    Am, Bm = D.DeviceMesh(A, 0), D.DeviceMesh(B, 0)
+    full = D.search_device(Am, Bm)
+    parts = [D.search_device(Am, Bm, shard=(g, G)) for g in range(G)]
+    merged = D._merge(parts)
+    assert np.array_equal(merged.hits, full.hits)
+    assert sum(p.stats["n_pairs"] for p in parts) == full.stats["n_pairs"]
+    assert merged.stats["n_aabb_pass"] == full.stats["n_aabb_pass"]
+
+
+def test_a_range_partition():
+    A, _, B, _ = config_pair("C4iii")
+    Am, Bm = D.DeviceMesh(A, 0), D.DeviceMesh(B, 0)
+    full = D.search_device(Am, Bm)
+    cuts = [0, 1000, 4097, 4100, Am.n_tri]
+    parts = [D.search_device(Am, Bm, a_range=(a, b)) for a, b in zip(cuts[:-1], cuts[1:])]
+    assert np.array_equal(D._merge(parts).hits, full.hits)
+
+
+def test_capacity_regrow():
+    A, _, B, _ = config_pair("C4ii")  # 54k hits
+    Am, Bm = D.DeviceMesh(A, 0), D.DeviceMesh(B, 0)
+    D._Workspace.get(0).hits = None
+    r_small = D.search_device(Am, Bm, cap=7)
+    D._Workspace.get(0).hits = None
+    r_big = D.search_device(Am, Bm, cap=1 << 20)
+    assert len(r_small.hits) == len(r_big.hits) == 54201
+    assert np.array_equal(r_small.hits, r_big.hits)
+
+
+def test_swap_roles_symmetry():
+    """Searching B against A gives the transposed hit set (roles of s,t and a,b swap)."""
+    A, _, B, _ = config_pair("C1")
+    r1 = D.search(A, B)
+    r2 = D.search(B, A)
+    k1 = set(zip(r1.hits["ia"].tolist(), r1.hits["ib"].tolist()))
+    k2 = set(zip(r2.hits["ib"].tolist(), r2.hits["ia"].tolist()))
+    assert k1 == k2
+
+
+def test_disjoint_and_degenerate_inputs():
+    A, _ = manifold_like(32, 9, 1)
+    far = A + 100.0
+    r = D.search(A, far)
+    assert len(r.hits) == 0 and r.stats["n_aabb_pass"] == 0
+    # ragged sizes: A smaller than one block, B smaller than one tile, N odd
+    A2, _ = manifold_like(5, 2, 3)
+    B2, _ = manifold_like(7, 3, 3)
+    ref = O.search(A2, B2)
+    assert_same_hits(ref, D.search(A2, B2).hits)
+    # flat/degenerate triangles (all vertices identical) are singular, never hits
+    Z = np.zeros((4, 3, 4))
+    rz = D.search(Z, Z)
+    assert len(rz.hits) == 0 and rz.stats["n_singular"] == rz.stats["n_aabb_pass"] == (2 * 4 * 2) ** 2
+
+
+def test_multi_device_api_single_gpu():
+    """The in-process multi-GPU path (one host thread per device) with the same device twice."""
+    A, _, B, _ = config_pair("C4i")
+    r1 = D.search(A, B, devices=(0,))
+    r2 = D.search(A, B, devices=(0, 0))
+    assert np.array_equal(r1.hits, r2.hits)
+
+
+def test_find_intersections_records(oracle_lib):
+    A, sa, B, sb = config_pair("C1")
+    recs = isect.find_intersections(A, B)
+    ref = O.search(A, B)
+    hits = np.zeros(len(ref["ia"]), dtype=D.HIT_DTYPE)
+    for k in ("ia", "ib", "s", "t", "a", "b"):
+        hits[k] = ref[k]
+    want = isect.hits_to_records(A, sa, B, sb, hits)
+    assert [r.to_line() for r in recs] == [w.to_line() for w in want]
+
+
+@pytest.mark.parametrize("name", ["C1", "C4i"])
+def test_pair_candidates_spec_literal(name):
+    A, _, B, _ = config_pair(name)
+    want, _ = S.pair_candidates(A, B)
+    got = isect.pair_candidates(A, B)
+    assert np.array_equal(got, want.astype(np.uint64))
+
+
+def test_pair_candidates_small_exhaustive():
+    A, _ = manifold_like(16, 5, 11)
+    B = A + np.array([0.0, 0.0, 0.02, 0.0])[:, None, None]
+    want, _ = S.pair_candidates(A, B)
+    assert np.array_equal(isect.pair_candidates(A, B), want.astype(np.uint64))
+
+
+def test_nan_rejected():
+    A, _ = manifold_like(8, 3, 1)
+    A[0, 1, 2] = np.nan
+    with pytest.raises(Exception):
+        D.search(A, A)
+
+
+def test_bad_args_fail_loudly():
+    A, _, B, _ = config_pair("C1")
+    Am, Bm = D.DeviceMesh(A, 0), D.DeviceMesh(B, 0)
+    with pytest.raises(Exception):
+        D.search_device(Am, Bm, shard=(3, 2))
+    with pytest.raises(Exception):
+        D.search_device(Am, Bm, a_range=(10, 10 ** 9))

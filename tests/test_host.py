@@ -1,0 +1,189 @@
+"""CPU tests of the host side: the C ABI library's exports and struct layout, the
+reference-facing API's error behaviour, mesh / records I/O and record building."""
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from oracle import canonical as O
+from paper_2109_14814_b200 import _lib, errors, isect
+from paper_2109_14814_b200.mesh import (HalfLayer, ManifoldMesh, config_pair, half_layer, manifold_like,
+                                        read_mesh, write_mesh)
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "mcx.h")
+
+
+def _header_functions():
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:[a-z_0-9]+\s*\*?\s+)+\**(mcx_[a-z_]+)\s*\(", txt, re.M)))
+
+
+def test_library_exports_every_header_symbol():
+    L = _lib.load()  # loads without a GPU (cudart is linked statically)
+    funcs = _header_functions()
+    assert set(funcs) == set(_lib.EXPORTS)
+    for f in funcs:
+        assert hasattr(L, f), f
+    assert L.mcx_version() == 1
+    assert L.mcx_a_block() == 1024
+    assert isinstance(L.mcx_last_error(), bytes)
+
+
+def test_struct_layout_matches_header(tmp_path):
+    src = tmp_path / "layout.c"
+    src.write_text(
+        '#include <stdio.h>\n#include <stddef.h>\n#include "mcx.h"\n'
+        "int main(void){printf(\"%zu %zu %zu %zu %zu %zu %zu\\n\", sizeof(mcx_mesh_dev), sizeof(mcx_hit),"
+        " sizeof(mcx_stats), sizeof(mcx_opts), offsetof(mcx_opts, mode), offsetof(mcx_opts, workspace),"
+        " offsetof(mcx_hit, s));return 0;}\n")
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)], check=True)
+    got = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
+    want = [ctypes.sizeof(_lib.MeshDev), ctypes.sizeof(_lib.Hit), ctypes.sizeof(_lib.Stats), ctypes.sizeof(_lib.Opts),
+            _lib.Opts.mode.offset, _lib.Opts.workspace.offset, _lib.Hit.s.offset]
+    assert got == want
+
+
+def test_only_cuda_backend():
+    A, _ = manifold_like(8, 3, 1)
+    for bad in ("serial", "parallel", "cpu"):
+        with pytest.raises(errors.ConfigError):
+            isect.find_intersections(A, A, backend=bad)
+        with pytest.raises(errors.ConfigError):
+            isect.pair_candidates(A, A, backend=bad)
+
+
+def test_no_silent_cpu_fallback():
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    A, _ = manifold_like(8, 3, 1)
+    with pytest.raises(errors.BackendError):
+        isect.find_intersections(A, A)
+
+
+def test_error_hierarchy_exit_codes():
+    assert issubclass(errors.CapacityError, errors.BackendError)
+    assert issubclass(errors.BackendError, errors.ManiconnError)
+    assert errors.ConfigError("x").exit_code == 2
+    assert errors.NumericsError("x").exit_code == 3
+    assert errors.FileFormatError("x").exit_code == 4
+    e = errors.BackendError("boom", task=(3, "+", 2, "-"), status=2)
+    assert "layer pair (3, '+', 2, '-')" in str(e)
+
+
+def _mesh():
+    N, K, n_max, lam, D = 16, 3, 2, 2.0, 0.1
+    s = sorted({k * D / K for k in range(-K, K + 1)} | {sg * D * lam ** n for n in range(1, n_max + 1)
+                                                         for sg in (1, -1)} | {sg * D * lam ** n * 0.7
+                                                                               for n in range(1, n_max + 1) for sg in (1, -1)})
+    s = np.array(s)
+    coords, _ = manifold_like(N, len(s), 4)
+    return ManifoldMesh(coords=coords, s_values=s, kind="unstable", omega=1.3, lam=lam, D=D, n_max=n_max,
+                        boundary_cols=(0, len(s) - 1))
+
+
+def test_mnf1_roundtrip(tmp_path):
+    m = _mesh()
+    p = tmp_path / "m.mnf"
+    write_mesh(p, m)
+    r = read_mesh(p)
+    assert np.array_equal(r.coords, m.coords) and np.array_equal(r.s_values, m.s_values)
+    assert (r.kind, r.omega, r.lam, r.D, r.n_max, r.boundary_cols) == (m.kind, m.omega, m.lam, m.D, m.n_max,
+                                                                      m.boundary_cols)
+    raw = p.read_bytes()
+    (tmp_path / "bad").write_bytes(b"XXXX" + raw[4:])
+    with pytest.raises(errors.FileFormatError):
+        read_mesh(tmp_path / "bad")
+    (tmp_path / "trail").write_bytes(raw + b"\0")
+    with pytest.raises(errors.FileFormatError):
+        read_mesh(tmp_path / "trail")
+    (tmp_path / "trunc").write_bytes(raw[:100])
+    with pytest.raises(errors.FileFormatError):
+        read_mesh(tmp_path / "trunc")
+
+
+def test_half_layer_columns():
+    m = _mesh()
+    h = half_layer(m, 1, +1)
+    assert h.s_values[0] == pytest.approx(m.D) and h.s_values[-1] == pytest.approx(m.D * m.lam)
+    assert h.M >= 2 and h.n_triangles == 2 * m.N * (h.M - 1)
+    hn = half_layer(m, 2, -1)
+    assert hn.s_values[0] == pytest.approx(-m.D * m.lam ** 2) and hn.s_values[-1] == pytest.approx(-m.D * m.lam)
+    assert np.array_equal(h.coords, m.coords[:, h.col_range[0]:h.col_range[1] + 1])
+    with pytest.raises(errors.ConfigError):
+        half_layer(m, 3, +1)
+    with pytest.raises(errors.ConfigError):
+        HalfLayer(mesh=m, col_range=(2, 2))
+
+
+def test_from_planes_layout():
+    coords, s = manifold_like(6, 4, 2)
+    m = ManifoldMesh.from_planes(coords[0].T, coords[1].T, coords[2].T, coords[3].T, s)
+    assert np.array_equal(m.coords, coords)
+    # paper's storage: entry (i, k) of plane c at linear index i + N·k (column-major)
+    flat = m.coords[1].ravel()
+    assert flat[3 + 6 * 2] == m.plane(1)[3, 2]
+
+
+def test_records_from_oracle_hits(tmp_path):
+    A, sa, B, sb = config_pair("C1")
+    r = O.search(A, B)
+    hits = np.zeros(len(r["ia"]), dtype=[("ia", "<u4"), ("ib", "<u4"), ("s", "<f8"), ("t", "<f8"),
+                                         ("a", "<f8"), ("b", "<f8")])
+    for k in ("ia", "ib", "s", "t", "a", "b"):
+        hits[k] = r[k]
+    recs = isect.hits_to_records(A, sa, B, sb, hits, layer=(3, "+", 2, "-"))
+    assert len(recs) == 4
+    pts_o = O.hit_points(A, r["ia"], r["s"], r["t"])
+    gids = [rc.pair.gid for rc in recs]
+    assert gids == sorted(gids)
+    for rc in recs:
+        a, b, c, d = rc.bary
+        assert min(a, b, c, d) >= 0 and a + b <= 1 and c + d <= 1
+        n = np.nonzero((r["ia"] == rc.tri_index[0]) & (r["ib"] == rc.tri_index[1]))[0][0]
+        assert np.array_equal(rc.point, pts_o[n])
+        # the B side gives the same point within 1e-10·scale
+        pB = O.take(O.pack(B), np.array([rc.tri_index[1]]))
+        qpt = (pB["p"][0] + c * pB["e1"][0]) + d * pB["e2"][0]
+        assert np.max(np.abs(qpt - rc.point)) < 1e-10
+        # parameter estimates are inside the quad's parameter cell
+        thA = 2 * np.pi * np.arange(64) / 64
+        assert thA[rc.pair.i] - 1e-12 <= rc.params[0] <= thA[rc.pair.i] + 2 * np.pi / 64 + 1e-12
+        assert min(sa[rc.pair.k - 1], sa[rc.pair.k]) - 1e-12 <= rc.params[1] <= max(sa[rc.pair.k - 1], sa[rc.pair.k]) + 1e-12
+    p = tmp_path / "rec.txt"
+    isect.write_records(p, recs)
+    lines = p.read_text().splitlines()
+    assert len(lines) == 4 and all(len(ln.split()) == 17 for ln in lines)
+    back = isect.read_records(p)
+    for a, b in zip(recs, back):
+        assert np.array_equal(a.point, b.point) and a.bary == b.bary and a.params == b.params
+        assert a.pair.gid == b.pair.gid and a.layer == b.layer
+    (tmp_path / "bad.txt").write_text("1 + 2\n")
+    with pytest.raises(errors.FileFormatError):
+        isect.read_records(tmp_path / "bad.txt")
+
+
+def test_param_estimates_t2_vertices():
+    """The T² barycentric→(θ,s) map hits the T² vertices exactly (SPEC.md:499 design decision)."""
+    N, M = 8, 3
+    coords, s = manifold_like(N, M, 1)
+    i, k1 = 5, 1
+    tA = 2 * (i + N * k1) + 1
+    th = 2 * np.pi * np.arange(N) / N
+    for (x, y), want in (((0.0, 0.0), (th[i], s[k1 + 1])), ((1.0, 0.0), (th[i] + 2 * np.pi / N, s[k1])),
+                         ((0.0, 1.0), (th[i] + 2 * np.pi / N, s[k1 + 1]))):
+        hits = np.zeros(1, dtype=[("ia", "<u4"), ("ib", "<u4"), ("s", "<f8"), ("t", "<f8"), ("a", "<f8"), ("b", "<f8")])
+        hits["ia"], hits["ib"], hits["s"], hits["t"] = tA, 0, x, y
+        rc = isect.hits_to_records(coords, s, coords, s, hits, dedup=False)[0]
+        assert rc.params[0] == pytest.approx(want[0]) and rc.params[1] == pytest.approx(want[1])
+
+
+def test_dedup_within_tolerance():
+    pts = np.array([[0, 0, 0, 0], [5e-10, 0, 0, 0], [2e-9, 0, 0, 0], [1, 1, 1, 1], [1, 1, 1, 1 + 1e-10]], float)
+    keep = isect._dedup_mask(pts, 1e-9)
+    assert keep.tolist() == [True, False, True, True, False]

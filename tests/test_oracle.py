@@ -1,0 +1,268 @@
+"""CPU tests: the oracles against the SPEC's known answers and the golden fixtures.
+
+These pin the canonical arithmetic (oracle/canonical.py, oracle/mcx_oracle.c)
+before anything is compared with the GPU.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import canonical as O
+from oracle import exact as X
+from oracle import serial as S
+from paper_2109_14814_b200 import isect
+from paper_2109_14814_b200.mesh import config_pair, grid_points, manifold_like
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _bits(x):
+    return np.asarray(x, dtype=np.float64).view(np.uint64)
+
+
+# ------------------------------------------------------------ gid arithmetic
+def test_gid_examples():
+    assert isect.gid_to_cartesian(0, 7, 5, 4) == (0, 0, 0, 0)
+    assert isect.gid_to_cartesian(7, 7, 5, 4) == (0, 1, 0, 0)
+
+
+def test_gid_roundtrip_random():
+    rng = np.random.default_rng(5)
+    N1, N2, M1, M2 = 7, 5, 4, 6
+    g = rng.integers(0, N1 * N2 * (M1 - 1) * (M2 - 1), 100_000).astype(np.uint64)
+    i, j, k1, l1 = isect.gid_to_cartesian(g, N1, N2, M1)
+    assert np.all(i < N1) and np.all(j < N2) and np.all(k1 < M1 - 1) and np.all(l1 < M2 - 1)
+    assert np.array_equal(isect.cartesian_to_gid(i, j, k1, l1, N1, N2, M1), g)
+    # the oracle's independent restatement agrees
+    assert all(np.array_equal(a, b) for a, b in zip(S.gid_to_cartesian(g, N1, N2, M1), (i, j, k1, l1)))
+
+
+def test_gid_u64_at_paper_scale():
+    # PAPER's int gid overflows 2^31 at its own size; ours must not
+    N1, N2, M1, M2 = 1024, 2048, 35, 35
+    last = N1 * N2 * (M1 - 1) * (M2 - 1) - 1
+    assert last > 2 ** 31
+    assert isect.gid_to_cartesian(last, N1, N2, M1) == (N1 - 1, N2 - 1, M1 - 2, M2 - 2)
+    qi = isect.quad_index(last, N1, N2, M1, M2)
+    assert (qi.k, qi.l) == (M1 - 1, M2 - 1)
+    with pytest.raises(Exception):
+        isect.quad_index(last + 1, N1, N2, M1, M2)
+
+
+def test_pair_counts():  # SPEC.md:493, PAPER.md
+    with open(os.path.join(GOLD, "pair_counts.json")) as fh:
+        p = json.load(fh)["paper"]
+    assert isect.pair_counts(p["N1"], p["N2"], p["M1"], p["M2"]) == (p["quad_pairs"], p["triangle_pairs"])
+
+
+# ------------------------------------------------------------ AABB semantics
+def test_aabb_semantics():
+    lo = np.array([0.0, 0.0, 0.0, 0.0])
+    hi = np.array([1.0, 1.0, 1.0, 1.0])
+    assert O.aabb_overlap(lo, hi, lo, hi)  # self never rejected
+    assert not O.aabb_overlap(lo, hi, lo + [10, 0, 0, 0], hi + [10, 0, 0, 0])  # far translate rejected
+    assert O.aabb_overlap(lo, hi, lo + [1, 0, 0, 0], hi + [1, 0, 0, 0])  # touching: NOT rejected
+    assert not O.aabb_overlap(lo, hi, lo + [np.nextafter(1, 2), 0, 0, 0], hi + [2, 0, 0, 0])
+    for d in range(4):  # every coordinate separates, in both directions
+        off = np.zeros(4)
+        off[d] = 1.5
+        assert not O.aabb_overlap(lo, hi, lo + off, hi + off)
+        assert not O.aabb_overlap(lo + off, hi + off, lo, hi)
+
+
+# ------------------------------------------------------------ precise-test KATs
+def _solve_rows(rows):
+    A = {"p": rows[:, 0:4], "e1": rows[:, 4:8], "e2": rows[:, 8:12]}
+    B = {"p": rows[:, 12:16], "e1": rows[:, 16:20], "e2": rows[:, 20:24]}
+    for T in (A, B):
+        e1, e2 = T["e1"], T["e2"]
+        T["P"] = np.stack([e1[:, i] * e2[:, j] - e1[:, j] * e2[:, i] for i, j in O.BIV], axis=1)
+        n1 = ((e1[:, 0] * e1[:, 0] + e1[:, 1] * e1[:, 1]) + e1[:, 2] * e1[:, 2]) + e1[:, 3] * e1[:, 3]
+        n2 = ((e2[:, 0] * e2[:, 0] + e2[:, 1] * e2[:, 1]) + e2[:, 2] * e2[:, 2]) + e2[:, 3] * e2[:, 3]
+        T["nrm"] = np.sqrt(n1) * np.sqrt(n2)
+    return O.solve_pairs(A, B)
+
+
+def test_precise_kats():  # SPEC.md:466-468 against the exact Fraction oracle
+    z = np.load(os.path.join(GOLD, "kat_precise.npz"))
+    rows, exp, sing = z["rows"], z["expected"], z["singular"]
+    s, t, a, b, singular, hit = _solve_rows(rows)
+    assert np.array_equal(singular, sing)
+    assert not np.any(hit[sing])
+    got = np.stack([s, t, a, b], 1)[~sing]
+    want = exp[~sing]
+    # shared-vertex cases are exact integers: bit-exact (1, 0, 1, 0)
+    sv = np.all(want == np.array([1.0, 0.0, 1.0, 0.0]), axis=1)
+    assert sv.sum() >= 150
+    assert np.array_equal(got[sv], want[sv])
+    assert np.all(hit[~sing][sv])
+    # constructed crossings: interior, within a few ulp of the exact solution
+    assert np.allclose(got[~sv], want[~sv], rtol=0, atol=1e-15)
+    assert np.all(hit[~sing][~sv])
+
+
+def test_exact_solver_shared_vertex():
+    p, e1, e2 = np.array([0.0, 0, 0, 0]), np.array([1.0, 0, 0, 0]), np.array([0.0, 1, 0, 0])
+    q = np.array([1.0, -1, 0, -1])
+    f1 = p + e1 - q
+    f2 = np.array([0.0, 0, 1, 0])
+    assert X.solve_exact(p, e1, e2, q, f1, f2) == (1, 0, 1, 0)
+
+
+def test_bivector_determinant_matches_exact():
+    rng = np.random.default_rng(1)
+    for _ in range(50):
+        v = rng.integers(-9, 9, (4, 4)).astype(float)
+        e1, e2, f1, f2 = v
+        P = np.array([e1[i] * e2[j] - e1[j] * e2[i] for i, j in O.BIV])
+        Q = np.array([f1[i] * f2[j] - f1[j] * f2[i] for i, j in O.BIV])
+        D = P[0] * Q[5] - P[1] * Q[4] + P[2] * Q[3] + P[3] * Q[2] - P[4] * Q[1] + P[5] * Q[0]
+        assert D == float(X.det_exact(e1, e2, f1, f2))
+
+
+# ------------------------------------------------------------ mesh generator pins
+def test_theta_grid_matches_reference():
+    z = np.load(os.path.join(GOLD, "theta_grid.npz"))
+    for k in z.files:
+        assert np.array_equal(grid_points(int(k[1:])), z[k])
+
+
+def test_generator_resolution_independent():
+    A, _ = manifold_like(64, 33, 7)
+    B, _ = manifold_like(128, 65, 7)
+    assert np.allclose(A, B[:, ::2, ::2], atol=1e-12)
+
+
+# ------------------------------------------------------------ golden hit lists
+def _check_golden(z, r):
+    assert np.array_equal(r["ia"], z["ia"]) and np.array_equal(r["ib"], z["ib"])
+    for f in "stab":
+        assert np.array_equal(_bits(r[f]), z[f])
+    assert r["n_aabb_pass"] == int(z["n_aabb_pass"]) and r["n_singular"] == int(z["n_singular"])
+
+
+def test_golden_c1_numpy_oracle():
+    z = np.load(os.path.join(GOLD, "c1.npz"))
+    _check_golden(z, O.search(z["A"], z["B"]))
+    assert len(z["ia"]) == 4 and int(z["n_aabb_pass"]) == 438  # 438 survivors, 4 hits
+
+
+def test_golden_c4ii_exact_decisions():
+    """On the dyadic lattice the canonical arithmetic is exact: O1's decisions equal
+    the Fraction oracle's on every AABB-surviving pair (158,616 pairs)."""
+    z = np.load(os.path.join(GOLD, "c4ii.npz"))
+    pA, pB = O.pack(z["A"]), O.pack(z["B"])
+    ia, ib = z["surv_ia"].astype(np.int64), z["surv_ib"].astype(np.int64)
+    s, t, a, b, sing, hit = O.solve_pairs(O.take(pA, ia), O.take(pB, ib))
+    assert np.array_equal(hit, z["exact_accept"])
+    assert np.array_equal(sing, z["exact_singular"])
+    _check_golden(z, O.search(z["A"], z["B"]))
+
+
+def test_c_oracle_matches_numpy_oracle(oracle_lib):
+    z = np.load(os.path.join(GOLD, "c1.npz"))
+    for sweep in (False, True):
+        _check_golden(z, oracle_lib.search(z["A"], z["B"], sweep=sweep))
+    z = np.load(os.path.join(GOLD, "c4ii.npz"))
+    _check_golden(z, oracle_lib.search(z["A"], z["B"], sweep=True))
+
+
+@pytest.mark.parametrize("name", ["C4i", "C4iii"])
+def test_c_oracle_stress(oracle_lib, name):
+    A, _, B, _ = config_pair(name)
+    r1, r2 = O.search(A, B), oracle_lib.search(A, B, sweep=True)
+    for k in ("ia", "ib"):
+        assert np.array_equal(r1[k], r2[k])
+    for f in "stab":
+        assert np.array_equal(_bits(r1[f]), _bits(r2[f]))
+    assert (r1["n_aabb_pass"], r1["n_singular"]) == (r2["n_aabb_pass"], r2["n_singular"])
+
+
+def test_c_oracle_a_range_partition(oracle_lib):
+    A, _, B, _ = config_pair("C4i")
+    full = oracle_lib.search(A, B, sweep=True)
+    parts = [oracle_lib.search(A, B, a_range=(a0, min(a0 + 3000, 8064)), sweep=True) for a0 in range(0, 8064, 3000)]
+    ia = np.concatenate([p["ia"] for p in parts])
+    assert np.array_equal(ia, full["ia"])
+    assert sum(p["n_aabb_pass"] for p in parts) == full["n_aabb_pass"]
+
+
+def test_c_oracle_pack_matches_numpy(oracle_lib):
+    A, _, _, _ = config_pair("C1")
+    box, geo = oracle_lib.pack(A)
+    pk = O.pack(A)
+    assert np.array_equal(box[:, :4], pk["lo"]) and np.array_equal(box[:, 4:], pk["hi"])
+    for k, sl in (("p", slice(0, 4)), ("e1", slice(4, 8)), ("e2", slice(8, 12)), ("P", slice(12, 18))):
+        assert np.array_equal(geo[:, sl], pk[k])
+    assert np.array_equal(geo[:, 18], pk["nrm"])
+
+
+# ------------------------------------------------------------ SPEC-literal pipeline (O3)
+def test_moller_examples():
+    base = np.zeros((4, 2, 2))
+    base[0] = np.array([[0.0, 1.0], [0.0, 1.0]])  # x = θ index, y = s index: flat unit quad, z = 0
+    base[1] = np.array([[0.0, 0.0], [1.0, 1.0]])
+    VA = S.quad_vertices(base)
+    far = VA.copy()
+    far[..., 2] += 5.0  # all four vertices far above the plane
+    assert S.moller_reject_quads(VA, far)[0]
+    straddle = VA.copy()
+    straddle[:, :2, 2] += 1.0
+    straddle[:, 2:, 2] -= 1.0  # mixed signs both ways
+    assert not S.moller_reject_quads(VA, straddle)[0]
+
+
+def test_pair_candidates_exhaustive_small():
+    """(N1, N2, M1, M2) = (16, 16, 5, 5): survivor list equals brute-force evaluation of
+    both predicates over all 16·16·4·4 = 4,096 quad pairs (count corrected)."""
+    A, _ = manifold_like(16, 5, 11)
+    B, _ = manifold_like(16, 5, 11)
+    B = B + np.array([0.0, 0.0, 0.02, 0.0])[:, None, None]
+    gids, n_pass = S.pair_candidates(A, B)
+    VA, VB = S.quad_vertices(A), S.quad_vertices(B)
+    loA, hiA = S.quad_boxes(VA)
+    loB, hiB = S.quad_boxes(VB)
+    brute = []
+    for qa in range(VA.shape[0]):
+        for qb in range(VB.shape[0]):
+            if O.aabb_overlap(loA[qa], hiA[qa], loB[qb], hiB[qb]) and not S.moller_reject_quads(
+                    VA[qa:qa + 1], VB[qb:qb + 1])[0]:
+                brute.append(int(isect.cartesian_to_gid(qa % 16, qb % 16, qa // 16, qb // 16, 16, 16, 5)))
+    assert VA.shape[0] * VB.shape[0] == 4096
+    assert list(gids) == sorted(brute)
+    assert len(brute) > 0
+
+
+@pytest.mark.parametrize("name", ["C1", "C4i", "C4iii"])
+def test_spec_literal_subset_of_canonical(name):
+    """O3 (quad AABB + Möller + precise) ⊆ O1, equal on random meshes; on touching
+    geometry floating-point Möller drops some hits."""
+    A, _, B, _ = config_pair(name)
+    r1, r3 = O.search(A, B), S.find_intersections(A, B)
+    k1 = set(zip(r1["ia"].tolist(), r1["ib"].tolist()))
+    k3 = set(zip(r3["ia"].tolist(), r3["ib"].tolist()))
+    assert k3 <= k1
+    if name == "C1":
+        assert k3 == k1
+
+
+def test_rejection_soundness_random():
+    """No pair with an exact-oracle intersection is rejected by AABB or Möller."""
+    rng = np.random.default_rng(3)
+    bad = 0
+    for _ in range(2000):
+        g = rng.integers(-4, 5, (2, 4, 2, 2)).astype(float) / 4.0
+        VA, VB = S.quad_vertices(g[0]), S.quad_vertices(g[1])
+        loA, hiA = S.quad_boxes(VA)
+        loB, hiB = S.quad_boxes(VB)
+        rej = (not O.aabb_overlap(loA[0], hiA[0], loB[0], hiB[0])) or S.moller_reject_quads(VA, VB)[0]
+        if not rej:
+            continue
+        pa, pb = O.pack(g[0]), O.pack(g[1])
+        for ta in range(2):
+            for tb in range(2):
+                sol = X.solve_exact(pa["p"][ta], pa["e1"][ta], pa["e2"][ta], pb["p"][tb], pb["e1"][tb], pb["e2"][tb])
+                bad += X.accepted(sol)
+    assert bad == 0

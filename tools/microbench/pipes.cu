@@ -167,6 +167,62 @@ __global__ void k_iswar(const unsigned* in, void* outv, long long* cyc) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
 }
 
+
+// DSETP with B operands loaded from shared memory every iteration (like the search
+// inner loop): 4 LDS.128 + 4 chains x 8 DSETP per iteration.  Measures the DSETP
+// issue rate when ptxas cannot hoist the compares.
+__global__ void k_dsetp_smem(const double* in, void* outv, long long* cyc) {
+  unsigned* out = (unsigned*)outv;
+  __shared__ double2 sb[512][4];
+  for (int i = threadIdx.x; i < 512 * 4; i += blockDim.x) sb[i / 4][i % 4] = make_double2(in[i % 8] + i, in[(i + 1) % 8] - i);
+  double alo[4][4], ahi[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) { alo[r][c] = in[c] + threadIdx.x + r; ahi[r][c] = in[8 + c] + threadIdx.x * 2 + r; }
+  unsigned acc = 0;
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < ITERS / 512 * 8; ++it) {
+#pragma unroll 2
+    for (int j = 0; j < 512; ++j) {
+      const double2 l01 = sb[j][0], l23 = sb[j][1], h01 = sb[j][2], h23 = sb[j][3];
+      bool p[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        p[r] = (l01.x <= ahi[r][0]) & (alo[r][0] <= h01.x) & (l01.y <= ahi[r][1]) & (alo[r][1] <= h01.y) &
+               (l23.x <= ahi[r][2]) & (alo[r][2] <= h23.x) & (l23.y <= ahi[r][3]) & (alo[r][3] <= h23.y);
+      acc += (p[0] | p[1] | p[2] | p[3]) ? 1u : 0u;
+    }
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
+// DFMA with loop-carried dependence through 8 accumulators AND an smem operand.
+__global__ void k_dadd_chain(const double* in, void* outv, long long* cyc) {
+  double* out = (double*)outv;
+  double a[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) a[k] = in[k % 8] + threadIdx.x + k;
+  const double b = in[8];
+  __syncthreads();
+  long long t0 = clock64();
+  for (int i = 0; i < ITERS; ++i) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) a[k] = a[k] + b;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) a[k] = a[k] - b;
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+  double s = 0; for (int k = 0; k < 16; ++k) s += a[k];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 template <typename K, typename T>
 static int run(const char* name, K kern, const T* din, void* dout, long long* dcyc, int nsm, int threads,
                double lane_ops_per_thread, int repeats) {
@@ -196,8 +252,9 @@ static int run(const char* name, K kern, const T* din, void* dout, long long* dc
     double mean = 0; for (int i = 0; i < grid; ++i) mean += hcyc[i]; mean /= grid;
     clk_ghz = mean / (best_ms * 1e6);
   }
-  printf("{\"op\": \"%s\", \"lane_ops_per_clk_per_sm\": %.3f, \"occ\": %d, \"threads\": %d, \"ms\": %.3f, \"implied_ghz\": %.3f}\n",
-         name, best, occ, threads, best_ms, clk_ghz);
+  double total = (double)grid * threads * lane_ops_per_thread;
+  printf("{\"op\": \"%s\", \"lane_ops_per_clk_per_sm_clock64\": %.3f, \"lane_ops_per_s\": %.4e, \"per_sm_per_clk_at_1965\": %.2f, \"occ\": %d, \"threads\": %d, \"ms\": %.3f, \"implied_ghz\": %.3f}\n",
+         name, best, total / (best_ms * 1e-3), total / (best_ms * 1e-3) / nsm / 1.965e9, occ, threads, best_ms, clk_ghz);
   delete[] hcyc;
   return 0;
 }
@@ -221,6 +278,8 @@ int main() {
   CK(cudaMemcpy(df, hf, sizeof(hf), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(du, hu, sizeof(hu), cudaMemcpyHostToDevice));
   for (int threads : {256, 512}) {
+    run("dsetp_smem", k_dsetp_smem, dd, dout, dcyc, nsm, threads, 32.0 * (ITERS / 512 * 8) * 512, 3);
+    run("dadd", k_dadd_chain, dd, dout, dcyc, nsm, threads, 32.0 * ITERS, 3);
     run("dfma", k_dfma, dd, dout, dcyc, nsm, threads, 32.0 * ITERS, 3);
     run("dsetp", k_dsetp, dd, dout, dcyc, nsm, threads, 32.0 * ITERS, 3);
     run("fsetp", k_fsetp, df, dout, dcyc, nsm, threads, 32.0 * ITERS, 3);

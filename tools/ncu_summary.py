@@ -1,0 +1,65 @@
+"""Summarise ncu artefacts into the text files committed under profiles/.
+
+    python tools/ncu_summary.py rep  <file.ncu-rep>   # key metrics of each profiled kernel
+    python tools/ncu_summary.py list <launches.csv>   # per-kernel share of a launch list
+"""
+import csv
+import io
+import subprocess
+import sys
+from collections import defaultdict
+
+KEYS = [
+    "gpu__time_duration.sum", "sm__cycles_elapsed.avg.per_second", "launch__grid_size", "launch__block_size",
+    "launch__registers_per_thread", "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem",
+    "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__inst_executed.avg.per_cycle_active",
+    "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum", "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum",
+    "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum.pct_of_peak_sustained_elapsed",
+    "lts__t_sectors.sum", "lts__t_sectors.sum.per_second", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "dram__bytes_read.sum.per_second",
+]
+STALLS = "smsp__average_warps_issue_stalled_"
+
+
+def rep(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units = rows[0], rows[1]
+    for vals in rows[2:]:
+        name = vals[hdr.index("Kernel Name")] if "Kernel Name" in hdr else "?"
+        print(f"kernel: {name}")
+        for k in KEYS:
+            if k in hdr:
+                i = hdr.index(k)
+                print(f"  {k:70s} {vals[i]:>18s} {units[i]}")
+        st = [(h, vals[i]) for i, h in enumerate(hdr) if h.startswith(STALLS) and h.endswith("_per_issue_active.ratio")]
+        st = sorted(((float(v.replace(",", "")), h[len(STALLS):-len("_per_issue_active.ratio")]) for h, v in st
+                     if v not in ("", "n/a")), reverse=True)
+        print("  top stall reasons (warps stalled per issue):")
+        for v, h in st[:8]:
+            print(f"    {h:40s} {v:8.3f}")
+
+
+def launches(path):
+    rows = [r for r in csv.reader(open(path)) if len(r) > 5]
+    hdr = rows[0]
+    ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3, "s": 1e6}
+    agg = defaultdict(lambda: [0, 0.0])
+    for r in rows[1:]:
+        v = float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
+        agg[r[ki]][0] += 1
+        agg[r[ki]][1] += v
+    tot = sum(a[1] for a in agg.values())
+    print(f"{'launches':>8s} {'total_us':>14s} {'mean_us':>12s} {'share':>7s}  kernel")
+    for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        print(f"{n:8d} {t:14.1f} {t / n:12.1f} {100 * t / tot:6.2f}%  {k}")
+
+
+if __name__ == "__main__":
+    {"rep": rep, "list": launches}[sys.argv[1]](sys.argv[2])
