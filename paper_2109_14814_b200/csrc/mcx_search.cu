@@ -29,6 +29,8 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "../../include/mcx.h"
 #include "mcx_common.cuh"
 
@@ -91,13 +93,15 @@ constexpr int TILE = 512;            // B triangles per shared-memory tile
 constexpr int STAGES = 2;
 
 // Kernel variant: R A triangles per thread, MINB resident CTAs per SM (register cap).
-template <int R_, int MINB_>
+template <int R_, int MINB_, int JB_ = 1, int UNROLL_ = 2>
 struct Cfg {
   static constexpr int R = R_;
   static constexpr int MINB = MINB_;
+  static constexpr int JB = JB_;             // B triangles per warp vote
+  static constexpr int UNROLL = UNROLL_;     // inner-loop unroll
   static constexpr int THREADS = A_BLOCK / R_;
   static constexpr int WARPS = THREADS / 32;
-  static constexpr int QCAP = 32 * R_ + 32;  // per-warp survivor queue capacity
+  static constexpr int QCAP = 32 * R_ * JB_ + 32;  // per-warp survivor queue capacity
 };
 
 struct __align__(16) Box {
@@ -244,26 +248,32 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_brute_kernel(const
     const uint64_t tb = b0 + (uint64_t)t * TILE;
     const int nvalid = (int)min((uint64_t)TILE, b1 - tb);
     const Box* tile = S.tile[s];
-#pragma unroll 4
-    for (int j = 0; j < nvalid; ++j) {
-      const double2* bp = reinterpret_cast<const double2*>(tile + j);
-      const double2 l01 = bp[0], l23 = bp[1], h01 = bp[2], h23 = bp[3];
-      bool p[R];
+    // JB B triangles per warp vote: JB·R independent predicate chains in flight.
+    auto step = [&](int j, auto jb_c) {
+      constexpr int NJ = decltype(jb_c)::value;
+      bool p[NJ][R];
+      bool any = false;
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        p[r] = (l01.x <= ahi[r][0]) & (alo[r][0] <= h01.x) & (l01.y <= ahi[r][1]) & (alo[r][1] <= h01.y) &
-               (l23.x <= ahi[r][2]) & (alo[r][2] <= h23.x) & (l23.y <= ahi[r][3]) & (alo[r][3] <= h23.y);
-      }
-      bool any = p[0];
-#pragma unroll
-      for (int r = 1; r < R; ++r) any |= p[r];
-      if (__any_sync(0xffffffffu, any)) {
-        const uint32_t ib = (uint32_t)(tb + j);
+      for (int u = 0; u < NJ; ++u) {
+        const double2* bp = reinterpret_cast<const double2*>(tile + j + u);
+        const double2 l01 = bp[0], l23 = bp[1], h01 = bp[2], h23 = bp[3];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          const unsigned m = __ballot_sync(0xffffffffu, p[r]);
-          if (p[r]) q[qn + __popc(m & lt_mask)] = make_uint2(aidx[r], ib);
-          qn += __popc(m);
+          p[u][r] = (l01.x <= ahi[r][0]) & (alo[r][0] <= h01.x) & (l01.y <= ahi[r][1]) & (alo[r][1] <= h01.y) &
+                    (l23.x <= ahi[r][2]) & (alo[r][2] <= h23.x) & (l23.y <= ahi[r][3]) & (alo[r][3] <= h23.y);
+          any |= p[u][r];
+        }
+      }
+      if (__any_sync(0xffffffffu, any)) {
+#pragma unroll
+        for (int u = 0; u < NJ; ++u) {
+          const uint32_t ib = (uint32_t)(tb + j + u);
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const unsigned m = __ballot_sync(0xffffffffu, p[u][r]);
+            if (p[u][r]) q[qn + __popc(m & lt_mask)] = make_uint2(aidx[r], ib);
+            qn += __popc(m);
+          }
         }
         __syncwarp();
         if (qn >= 32) {
@@ -274,7 +284,11 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_brute_kernel(const
           load_a();
         }
       }
-    }
+    };
+    const int nmain = nvalid - nvalid % C::JB;
+#pragma unroll(C::UNROLL)
+    for (int j = 0; j < nmain; j += C::JB) step(j, std::integral_constant<int, C::JB>());
+    for (int j = nmain; j < nvalid; ++j) step(j, std::integral_constant<int, 1>());
     __syncthreads();  // every warp is done reading stage s
     if (tid == 0 && t + STAGES < ntiles) {
       const uint64_t nb = b0 + (uint64_t)(t + STAGES) * TILE;
@@ -334,10 +348,10 @@ static int variant_from_env() {
 template <int KIND>
 static int launch_brute(SearchParams P, uint64_t my_blocks, int device, cudaStream_t stream) {
   switch (variant_from_env()) {
-    case 1: return launch_brute_cfg<KIND, Cfg<4, 1>>(P, my_blocks, device, stream);
-    case 2: return launch_brute_cfg<KIND, Cfg<8, 1>>(P, my_blocks, device, stream);
-    case 3: return launch_brute_cfg<KIND, Cfg<2, 1>>(P, my_blocks, device, stream);
-    default: return launch_brute_cfg<KIND, Cfg<4, 2>>(P, my_blocks, device, stream);
+    case 1: return launch_brute_cfg<KIND, Cfg<4, 2, 1, 1>>(P, my_blocks, device, stream);
+    case 2: return launch_brute_cfg<KIND, Cfg<4, 2, 1, 4>>(P, my_blocks, device, stream);
+    case 3: return launch_brute_cfg<KIND, Cfg<4, 2, 1, 8>>(P, my_blocks, device, stream);
+    default: return launch_brute_cfg<KIND, Cfg<4, 2, 1, 2>>(P, my_blocks, device, stream);
   }
 }
 
