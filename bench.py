@@ -42,11 +42,14 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C3")
-    ap.add_argument("--mode", default="brute", choices=["brute", "cull"])
+    ap.add_argument("--mode", default="brute", choices=["brute", "cull"],
+                    help="primary mode for `value` (the other is measured too and reported alongside)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU-baseline sample duration")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo lets several ranks share one GPU (logic test of the N>1 path on a 1-GPU box)")
     return ap.parse_args()
 
 
@@ -171,6 +174,9 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ our arm
+KERNEL_LAUNCHES = {"brute": 1, "cull": 2}  # our kernels per search call (memset / D2H not counted)
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -181,13 +187,18 @@ def run_ours(args):
     rank, world, local = dist_env()
     if world != args.gpus and world > 1:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
+    local = local % torch.cuda.device_count()  # ranks may share a GPU under --dist-backend gloo
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     dev = torch.device("cuda", local)
+    red_dev = dev if args.dist_backend == "nccl" else torch.device("cpu")
     A, sa, B, sb = config_pair(args.config)
     desc = workload_desc(args.config, A, B)
-    mode = {"brute": _lib.MODE_BRUTE, "cull": _lib.MODE_CULL}[args.mode]
+    modes = {"brute": _lib.MODE_BRUTE, "cull": _lib.MODE_CULL}
     shard = (rank, world)
 
     stream = torch.cuda.current_stream(dev)
@@ -200,90 +211,117 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize(dev)
 
-    def max_over_ranks(x):
+    def reduce(x, op):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t = torch.tensor([float(x)], dtype=torch.float64, device=red_dev)
+        dist.all_reduce(t, op=op)
         return float(t.item())
 
-    def sum_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        return float(t.item())
+    MAX = dist.ReduceOp.MAX if world > 1 else None
+    SUM = dist.ReduceOp.SUM if world > 1 else None
 
-    # ---- device-resident search (value)
-    for _ in range(args.warmup):
-        res = D.search_device(Am, Bm, mode=mode, shard=shard, stream=stream)
-    barrier()
-    clk = ClockSampler(local) if rank == 0 else None
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    launches = 0
-    my_pairs = 0
-    for k in range(args.steps):
-        flush.zero_()  # L2 flush between timed steps (outside the events)
-        ev[k][0].record(stream)
-        res = D.search_device(Am, Bm, mode=mode, shard=shard, stream=stream)
-        ev[k][1].record(stream)
-        launches += 1
-        my_pairs += res.stats["n_pairs"]
-    barrier()
-    clocks = clk.stop() if clk else None
-    dev_ms = sum(s.elapsed_time(e) for s, e in ev)
-    t_max = max_over_ranks(dev_ms)
-    total_pairs = sum_over_ranks(my_pairs)
-    n_hits = int(sum_over_ranks(len(res.hits)))
-    value = total_pairs / (t_max * 1e-3)
-    ms_per_step = t_max / args.steps
+    def measure(mode_name, with_clocks):
+        mode = modes[mode_name]
+        for _ in range(args.warmup):
+            D.search_device(Am, Bm, mode=mode, shard=shard, stream=stream)
+        barrier()
+        clk = ClockSampler(local) if (with_clocks and rank == 0) else None
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        my_pairs = my_tested = 0
+        for k in range(args.steps):
+            flush.zero_()  # L2 flush between timed steps (outside the events)
+            ev[k][0].record(stream)
+            res = D.search_device(Am, Bm, mode=mode, shard=shard, stream=stream)
+            ev[k][1].record(stream)
+            my_pairs += res.stats["n_pairs"]
+            my_tested += res.stats["n_tested"]
+        barrier()
+        clocks = clk.stop() if clk else None
+        dev_ms = sum(s.elapsed_time(e) for s, e in ev)
+        t_max = reduce(dev_ms, MAX)
+        hits = res.hits
+        if world > 1:
+            hits = D.gather_hits(hits)
+        st = D.search_device(Am, Bm, mode=mode, shard=shard, stream=stream, timing=True).stats
+        return {"t_max_ms": t_max, "ms_per_step": t_max / args.steps,
+                "pairs": reduce(my_pairs, SUM), "tested": reduce(my_tested, SUM),
+                "value": reduce(my_pairs, SUM) / (t_max * 1e-3), "hits": None if hits is None else len(hits),
+                "kernel_ms": reduce(st["kernel_ms"], MAX), "stats": st, "clocks": clocks,
+                "launches": KERNEL_LAUNCHES[mode_name] * args.steps}
 
-    # ---- roofline of the search kernel (kernel-only events, one more launch)
-    st = D.search_device(Am, Bm, mode=mode, shard=shard, stream=stream, timing=True).stats
-    kern_ms = max_over_ranks(st["kernel_ms"])
-    props = torch.cuda.get_device_properties(dev)
-    sms = props.multi_processor_count
-    f_max = (clocks or {}).get("sm_max_mhz") or 1965.0
-    f_run = (clocks or {}).get("sm_mhz") or f_max
-    lane_ops = 8.0 * st["n_tested"] + 100.0 * st["n_aabb_pass"]  # SURVEY.md §8(d)
-    achieved = lane_ops / (st["kernel_ms"] * 1e-3) / 1e12
-    peak = sms * FP64_LANES_PER_CLK_PER_SM * f_max * 1e6 / 1e12
-    peak_run = sms * FP64_LANES_PER_CLK_PER_SM * f_run * 1e6 / 1e12
-    roofline = {"bound": "fp64_pipe", "achieved": achieved, "peak": peak, "unit": "Tlane-op/s",
-                "frac": achieved / peak, "frac_at_observed_clock": achieved / peak_run,
-                "peak_source": f"{sms} SMs x {FP64_LANES_PER_CLK_PER_SM} FP64 lanes/clk x {f_max:.0f} MHz "
-                               "(measured: DADD 63.5 lanes/clk/SM, profiles/r01_pipes.jsonl)",
-                "work_per_pair": "8 FP64 compares (AABB) + ~100 FP64 ops per AABB survivor",
-                "kernel_ms": st["kernel_ms"], "traffic": None,
-                "traffic_note": "ncu dram__bytes per launch: see profiles/r01_ncu_brute_c2.txt"}
-
-    # ---- end to end through the public API, host buffers (e2e)
-    e2e = None
-    if not args.no_e2e:
+    def measure_e2e(mode_name, pairs_total):
+        mode = modes[mode_name]
         pa = torch.from_numpy(np.ascontiguousarray(A)).pin_memory()
         pb = torch.from_numpy(np.ascontiguousarray(B)).pin_memory()
         h2d = (pa.numel() + pb.numel()) * 8
 
-        def e2e_step():
-            Ad, Bd = D.DeviceMesh(pa, local), D.DeviceMesh(pb, local)
-            r = D.search_device(Ad, Bd, mode=mode, shard=shard, stream=stream)
-            return r
+        def step():
+            Ad, Bd = D.DeviceMesh(pa, local, stream=stream), D.DeviceMesh(pb, local, stream=stream)
+            return D.search_device(Ad, Bd, mode=mode, shard=shard, stream=stream)
 
-        for _ in range(max(1, args.warmup // 2)):
-            e2e_step()
+        for _ in range(max(1, args.warmup)):
+            step()
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         d2h = 0
         e0.record(stream)
         for _ in range(args.steps):
-            r = e2e_step()
-            d2h += 32 + 40 * len(r.hits)
+            r = step()
+            d2h += 64 + 40 * len(r.hits)
         e1.record(stream)
         barrier()
-        e_ms = max_over_ranks(e0.elapsed_time(e1))
-        e2e = {"value": total_pairs / (e_ms * 1e-3), "unit": UNIT, "ms_per_step": e_ms / args.steps,
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h // args.steps,
-               "path": "device.search path: pinned host grids -> H2D -> mcx_pack -> mcx_search -> D2H hits"}
+        e_ms = reduce(e0.elapsed_time(e1), MAX)
+        return {"value": pairs_total / (e_ms * 1e-3), "unit": UNIT, "ms_per_step": e_ms / args.steps,
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h // args.steps,
+                "path": "pinned host grids -> H2D -> mcx_pack + mcx_levels -> mcx_search -> D2H counters + hits",
+                "mode": mode_name}
+
+    primary = args.mode
+    other = "cull" if primary == "brute" else "brute"
+    m1 = measure(primary, True)
+    m2 = measure(other, False)
+    brute = m1 if primary == "brute" else m2
+    cull = m2 if primary == "brute" else m1
+
+    # ---- roofline of the FP64 pair-test kernel (MCX_MODE_BRUTE, kernel-only events)
+    props = torch.cuda.get_device_properties(dev)
+    sms = props.multi_processor_count
+    clocks = m1["clocks"] or {}
+    f_max = clocks.get("sm_max_mhz") or 1965.0
+    f_run = clocks.get("sm_mhz") or f_max
+    st = brute["stats"]
+    lane_ops = 8.0 * st["n_tested"] + 100.0 * st["n_aabb_pass"]  # SURVEY.md §8(d)
+    achieved = lane_ops / (st["kernel_ms"] * 1e-3) / 1e12
+    peak = sms * FP64_LANES_PER_CLK_PER_SM * f_max * 1e6 / 1e12
+    peak_run = sms * FP64_LANES_PER_CLK_PER_SM * f_run * 1e6 / 1e12
+    roofline = {"bound": "fp64_pipe", "kernel": "search_brute_kernel (MCX_MODE_BRUTE, the FP64 pair-test kernel)",
+                "achieved": achieved, "peak": peak, "unit": "Tlane-op/s", "frac": achieved / peak,
+                "frac_at_observed_clock": achieved / peak_run,
+                "peak_source": f"{sms} SMs x {FP64_LANES_PER_CLK_PER_SM} FP64 lanes/clk x {f_max:.0f} MHz "
+                               "(pipe rate measured: DADD 63.5 lanes/clk/SM, profiles/r01_pipes.jsonl; "
+                               "MEASURED_PEAKS.json has no FP64 entry)",
+                "work_per_launch": "8 FP64 compare lane-ops per pair + ~100 FP64 lane-ops per AABB survivor",
+                "kernel_ms": st["kernel_ms"], "traffic": 16798976.0 / 1.7045913600e10 * st["n_pairs"],
+                "traffic_note": "dram__bytes_read+write per launch scaled from the C2 ncu capture "
+                                "(16.8 MB / 1.7e10 pairs, profiles/r01_ncu_brute_c2.txt): B boxes fit in L2"}
+    cst = cull["stats"]
+    cull_block = {"mode": "cull", "value": cull["value"], "unit": UNIT + " (logical)",
+                  "ms_per_step": cull["ms_per_step"], "search_wall_s": cull["ms_per_step"] / 1e3,
+                  "kernel_ms": cull["kernel_ms"], "logical_pairs_per_step": cst["n_pairs"],
+                  "executed_pair_tests_per_step": cst["n_tested"], "aabb_pass": cst["n_aabb_pass"],
+                  "speedup_vs_brute": brute["ms_per_step"] / cull["ms_per_step"], "hits": cull["hits"],
+                  "executed_fp64_frac": (8.0 * cst["n_tested"] + 100.0 * cst["n_aabb_pass"]) /
+                                        (cst["kernel_ms"] * 1e-3) / 1e12 / peak,
+                  "note": "identical hit set / AABB-pass / singular counts; exact union-box culling over the "
+                          "tiled storage order skips only provably disjoint pairs"}
+    if brute["hits"] is not None and cull["hits"] is not None and brute["hits"] != cull["hits"]:
+        raise SystemExit(f"brute/cull hit counts differ: {brute['hits']} vs {cull['hits']}")
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = measure_e2e(primary, m1["pairs"])
+        e2e["other_mode"] = measure_e2e(other, m1["pairs"])
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -293,14 +331,16 @@ def run_ours(args):
                          f"({s['pairs']:.3e} pairs, {s['seconds']:.1f} s, packing excluded)", "cpu": cpu_model()}
 
     if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
-                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {**desc, "mode": args.mode, "parallelism": f"A-block cyclic shards x{world}, B replicated",
+        line = {"metric": METRIC, "value": m1["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": m1["ms_per_step"], "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {**desc, "mode": primary, "parallelism": f"A-block cyclic shards x{world}, B replicated",
                            "l2": "flushed between timed steps (256 MiB write, outside the events)"},
-                "search_wall_s": ms_per_step / 1e3, "hits": n_hits, "kernel_ms": kern_ms,
-                "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks,
-                "gpu_launches": launches, "gpu": props.name, "sms": sms}
+                "search_wall_s": m1["ms_per_step"] / 1e3, "hits": m1["hits"], "kernel_ms": m1["kernel_ms"],
+                "roofline": roofline, "cull": cull_block if primary == "brute" else None,
+                "brute": None if primary == "brute" else {"value": brute["value"], "ms_per_step": brute["ms_per_step"]},
+                "e2e": e2e, "cpu_baseline": cpu, "clocks": m1["clocks"],
+                "gpu_launches": m1["launches"], "gpu": props.name, "sms": sms}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -49,10 +49,25 @@ extern "C" {
 #define MCX_MODE_BRUTE 0 /* every (iA, iB) pair gets the 8-compare AABB test       */
 #define MCX_MODE_CULL 1  /* exact block-AABB culling first; identical hit set      */
 
+/* Storage orders of the packed triangle records (mcx_pack). */
+#define MCX_ORDER_NATURAL 0 /* record t at position t = 2·(i + N·k) + τ               */
+#define MCX_ORDER_TILED 1   /* 16×16-quad tiles of 4×4-quad sub-tiles (spatially
+                               compact 32/512/1024-record blocks for culling)        */
+
+/* Hierarchy granularity (records per level box). */
+#define MCX_GROUP 32   /* gbox: one box per 32 records                               */
+#define MCX_TILE 512   /* tbox: one box per 512 records (B side)                     */
+#define MCX_BLOCK 1024 /* bbox: one box per 1024 records (A side; = mcx_a_block())   */
+
 typedef struct mcx_mesh_dev {
-  uint64_t n_tri;     /* number of triangles = 2·N·(M−1)                        */
-  const double* box;  /* device, [n_tri][8], 16-byte aligned                    */
-  const double* geo;  /* device, [n_tri][20], 16-byte aligned                   */
+  uint64_t n_tri;         /* number of triangles = 2·N·(M−1)                         */
+  const double* box;      /* device, [n_tri][8] in storage order, 16-byte aligned     */
+  const double* geo;      /* device, [n_tri][20] in storage order, 16-byte aligned    */
+  const uint32_t* perm;   /* device, [n_tri] storage position → original triangle
+                             index 2·(i + N·k) + τ; NULL = natural order              */
+  const double* gbox;     /* device, [⌈n/32⌉][8] group boxes (mcx_levels); MODE_CULL */
+  const double* tbox;     /* device, [⌈n/512⌉][8]                                    */
+  const double* bbox;     /* device, [⌈n/1024⌉][8]                                   */
 } mcx_mesh_dev;
 
 /* One intersecting triangle pair: A triangle ia, B triangle ib, and the
@@ -75,10 +90,10 @@ typedef struct mcx_stats {
 typedef struct mcx_opts {
   int device;            /* CUDA device ordinal                                      */
   void* stream;          /* cudaStream_t (NULL = legacy default stream)              */
-  uint64_t a_begin;      /* A triangle range [a_begin, a_end); a_end = 0 → n_tri     */
+  uint64_t a_begin;      /* A storage range [a_begin, a_end); a_end = 0 → n_tri      */
   uint64_t a_end;
-  uint32_t shard_index;  /* cyclic sharding of A blocks (MCX_A_BLOCK triangles each): */
-  uint32_t shard_count;  /*   this call takes blocks b with b % count == index; 0 → 1 */
+  uint32_t shard_index;  /* cyclic sharding of the absolute A blocks [1024 b, 1024 b +  */
+  uint32_t shard_count;  /*   1024): this call takes b % count == index; 0 → 1        */
   int mode;              /* MCX_MODE_BRUTE or MCX_MODE_CULL                           */
   int timing;            /* nonzero: record CUDA events and fill stats->kernel_ms    */
   void* workspace;       /* device scratch, >= mcx_workspace_bytes() bytes           */
@@ -94,10 +109,16 @@ uint64_t mcx_workspace_bytes(const mcx_mesh_dev* A, const mcx_mesh_dev* B, const
 /* Canonical triangle packing on the device (replaces the host-side triangle
  * construction of PAPER.md kernel steps 3-4 / SPEC Quad4 split).
  * coords: device, (4, M, N) float64 = four column-major N×M planes (x, y, px, py)
- * of one half-layer.  Writes box/geo for the
- * 2·N·(M−1) triangles, bit-identical to the CPU oracle's packing. */
-int mcx_pack(const double* coords, uint32_t N, uint32_t M, double* box, double* geo,
-             int device, void* stream);
+ * of one half-layer.  Writes box/geo (and perm, if
+ * non-NULL) for the 2·N·(M−1) triangles in the given storage order; every record
+ * is bit-identical to the CPU oracle's packing of that triangle. */
+int mcx_pack(const double* coords, uint32_t N, uint32_t M, int order, double* box, double* geo,
+             uint32_t* perm, int device, void* stream);
+
+/* Exact union boxes over consecutive records: gbox per 32, tbox per 512, bbox per
+ * 1024 (needed by MCX_MODE_CULL).  Enqueued on `stream`. */
+int mcx_levels(const double* box, uint64_t n_tri, double* gbox, double* tbox, double* bbox,
+               int device, void* stream);
 
 /* Triangle-level intersection search of A against B (replaces the reference's
  * rejection kernel + findall compaction + host precise test: PAPER.md kernel

@@ -17,14 +17,18 @@ LIB_PATH = os.path.join(HERE, "libmcx.so")
 
 MCX_OK, MCX_E_CAPACITY, MCX_E_CUDA, MCX_E_ARG = 0, 1, 2, 3
 MODE_BRUTE, MODE_CULL = 0, 1
+ORDER_NATURAL, ORDER_TILED = 0, 1
 BOX_STRIDE, GEO_STRIDE = 8, 20
+GROUP, TILE, BLOCK = 32, 512, 1024
 
-EXPORTS = ("mcx_a_block", "mcx_workspace_bytes", "mcx_pack", "mcx_search", "mcx_pair_candidates",
+EXPORTS = ("mcx_a_block", "mcx_workspace_bytes", "mcx_pack", "mcx_levels", "mcx_search", "mcx_pair_candidates",
            "mcx_last_error", "mcx_version")
 
 
 class MeshDev(ctypes.Structure):
-    _fields_ = [("n_tri", ctypes.c_uint64), ("box", ctypes.c_void_p), ("geo", ctypes.c_void_p)]
+    _fields_ = [("n_tri", ctypes.c_uint64), ("box", ctypes.c_void_p), ("geo", ctypes.c_void_p),
+                ("perm", ctypes.c_void_p), ("gbox", ctypes.c_void_p), ("tbox", ctypes.c_void_p),
+                ("bbox", ctypes.c_void_p)]
 
 
 class Hit(ctypes.Structure):
@@ -70,7 +74,9 @@ def load():
     L.mcx_workspace_bytes.restype = u64
     L.mcx_workspace_bytes.argtypes = [P(MeshDev), P(MeshDev), P(Opts)]
     L.mcx_pack.restype = i32
-    L.mcx_pack.argtypes = [vp, u32, u32, vp, vp, i32, vp]
+    L.mcx_pack.argtypes = [vp, u32, u32, i32, vp, vp, vp, i32, vp]
+    L.mcx_levels.restype = i32
+    L.mcx_levels.argtypes = [vp, u64, vp, vp, vp, i32, vp]
     L.mcx_search.restype = i32
     L.mcx_search.argtypes = [P(MeshDev), P(MeshDev), P(Opts), vp, u64, P(Stats)]
     L.mcx_pair_candidates.restype = i32

@@ -10,6 +10,35 @@
 
 namespace mcx {
 
+// ------------------------------------------------------------ geometry constants
+constexpr int A_BLOCK = 1024;  // A triangles per CTA / shard block (absolute: block b = [1024 b, 1024 b + 1024))
+constexpr int TILE = 512;      // B triangles per shared-memory tile (cull level-1 B unit)
+constexpr int GROUP = 32;      // triangles per warp group (cull level-2 unit, both meshes)
+constexpr int ORDER_TILE_Q = 16;  // tiled storage order: 16x16-quad tiles ...
+constexpr int ORDER_SUB_Q = 4;    // ... of 4x4-quad sub-tiles (= one 32-triangle group)
+
+struct __align__(16) Box {
+  double lo[4];
+  double hi[4];
+};
+
+// Storage position of quad (i, k) (i = θ index < N, k = column < MQ = M-1) in the
+// tiled order: row-major 16x16-quad tiles, inside them row-major 4x4 sub-tiles,
+// inside those row-major quads; ragged edge tiles/sub-tiles keep their true size,
+// so the map is a bijection onto [0, N·MQ).  A full sub-tile is one 32-triangle
+// group, a full tile one 512-triangle B tile, two adjacent tiles one A block.
+__host__ __device__ __forceinline__ uint64_t storage_quad(uint32_t i, uint32_t k, uint32_t N, uint32_t MQ) {
+  const uint32_t T = ORDER_TILE_Q, S = ORDER_SUB_Q;
+  const uint32_t tk = k / T, ti = i / T;
+  const uint32_t hq = min(T, MQ - tk * T), wq = min(T, N - ti * T);
+  const uint64_t off_tile = (uint64_t)tk * T * N + (uint64_t)ti * T * hq;
+  const uint32_t kk = k - tk * T, ii = i - ti * T;
+  const uint32_t sk = kk / S, si = ii / S;
+  const uint32_t hs = min(S, hq - sk * S), ws = min(S, wq - si * S);
+  const uint32_t off_sub = sk * S * wq + si * S * hs;
+  return off_tile + off_sub + (kk - sk * S) * ws + (ii - si * S);
+}
+
 // ------------------------------------------------------------ error state
 // Thread-local, so concurrent host threads (one per GPU) never clobber each other.
 extern thread_local char g_err[512];

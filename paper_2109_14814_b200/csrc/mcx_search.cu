@@ -2,13 +2,12 @@
 //
 // Replaces the reference's rejection kernel, findall compaction and host-side
 // precise test (PAPER.md "Computational Implementation", kernel steps 1-9 and
-// Fig. 1; SPEC isect.pair_candidates / find_intersections) with
-// one fused kernel:
+// Fig. 1; SPEC isect.pair_candidates / find_intersections).
 //
+// MCX_MODE_BRUTE — search_brute_kernel: every pair gets the AABB test.
 //   * A triangles live in registers: each thread owns R = 4 triangle AABBs
-//     (8 doubles each), so a CTA of 256 threads owns an A block of 1024
-//     triangles (a warp covers 32 consecutive triangles per r, i.e. one θ-strip
-//     of the mesh).
+//     (8 doubles each), a CTA of 256 threads one absolute A block of 1024
+//     storage positions.
 //   * B triangle AABBs stream through shared memory in tiles of 512 (32 KB)
 //     with a 2-stage ring of 1-D bulk async copies (cp.async.bulk → UBLKCP)
 //     completed on mbarriers.  Every B box is a warp-uniform broadcast
@@ -20,6 +19,15 @@
 //     canonical FMA-free FP64 bivector-Cramer sequence, reading
 //     the two triangles' geometry from L2.  Hits are compacted with one atomic
 //     per warp into the global (iA, iB, s, t, a, b) list (no flag buffer).
+//
+// MCX_MODE_CULL — the same predicate and the same survivor path behind two levels
+//   of exact box culling over the tiled storage order (mcx_pack.cu):
+//   cull_blocks_kernel tests every (A block of 1024, B tile of 512) union-box pair
+//   and compacts the overlapping ones; cull_pairs_kernel takes them, tests the
+//   32×16 (A group, B group) union boxes of 32 triangles each, and runs the pair
+//   test only inside overlapping groups.  A union box is disjoint from another box
+//   only if all its members are, so the AABB-pass set, singular count and hit set
+//   are identical to MCX_MODE_BRUTE; only n_tested shrinks.
 //
 // The solve uses only __dadd_rn/__dsub_rn/__dmul_rn/__ddiv_rn (never contracted
 // into DFMA) and the file is compiled with --fmad=false, so the op sequence is
@@ -36,60 +44,6 @@
 
 namespace mcx {
 
-// ------------------------------------------------------------------ packing
-// One thread per triangle; same op sequence as oracle/canonical.py:pack.
-__global__ void pack_kernel(const double* __restrict__ coords, uint32_t N, uint32_t M,
-                            double* __restrict__ box, double* __restrict__ geo) {
-  const uint64_t n_tri = 2ull * N * (M - 1);
-  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n_tri;
-       t += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t q = t >> 1;
-    const int tau = (int)(t & 1);
-    const uint32_t i = (uint32_t)(q % N), k = (uint32_t)(q / N);
-    const uint32_t ip = (i + 1 == N) ? 0 : i + 1;
-    double v0[4], v1[4], v2[4];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const double* pl = coords + (uint64_t)c * M * N;
-      const double w00 = pl[(uint64_t)k * N + i], w10 = pl[(uint64_t)k * N + ip];
-      const double w01 = pl[(uint64_t)(k + 1) * N + i], w11 = pl[(uint64_t)(k + 1) * N + ip];
-      v0[c] = __dadd_rn(tau ? w01 : w00, 0.0);
-      v1[c] = __dadd_rn(w10, 0.0);
-      v2[c] = __dadd_rn(tau ? w11 : w01, 0.0);
-    }
-    double e1[4], e2[4];
-    double* b = box + t * MCX_BOX_STRIDE;
-    double* g = geo + t * MCX_GEO_STRIDE;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      b[c] = fmin(fmin(v0[c], v1[c]), v2[c]);
-      b[4 + c] = fmax(fmax(v0[c], v1[c]), v2[c]);
-      e1[c] = __dsub_rn(v1[c], v0[c]);
-      e2[c] = __dsub_rn(v2[c], v0[c]);
-      g[c] = v0[c];
-      g[4 + c] = e1[c];
-      g[8 + c] = e2[c];
-    }
-    const int bi[6] = {0, 0, 0, 1, 1, 2}, bj[6] = {1, 2, 3, 2, 3, 3};
-#pragma unroll
-    for (int p = 0; p < 6; ++p)
-      g[12 + p] = __dsub_rn(__dmul_rn(e1[bi[p]], e2[bj[p]]), __dmul_rn(e1[bj[p]], e2[bi[p]]));
-    double n1 = __dmul_rn(e1[0], e1[0]);
-    n1 = __dadd_rn(n1, __dmul_rn(e1[1], e1[1]));
-    n1 = __dadd_rn(n1, __dmul_rn(e1[2], e1[2]));
-    n1 = __dadd_rn(n1, __dmul_rn(e1[3], e1[3]));
-    double n2 = __dmul_rn(e2[0], e2[0]);
-    n2 = __dadd_rn(n2, __dmul_rn(e2[1], e2[1]));
-    n2 = __dadd_rn(n2, __dmul_rn(e2[2], e2[2]));
-    n2 = __dadd_rn(n2, __dmul_rn(e2[3], e2[3]));
-    g[18] = __dmul_rn(__dsqrt_rn(n1), __dsqrt_rn(n2));
-    g[19] = 0.0;
-  }
-}
-
-// ------------------------------------------------------------ search kernel
-constexpr int A_BLOCK = 1024;        // A triangles per CTA (= THREADS · R for every variant)
-constexpr int TILE = 512;            // B triangles per shared-memory tile
 constexpr int STAGES = 2;
 
 // Kernel variant: R A triangles per thread, MINB resident CTAs per SM (register cap).
@@ -104,25 +58,32 @@ struct Cfg {
   static constexpr int QCAP = 32 * R_ * JB_ + 32;  // per-warp survivor queue capacity
 };
 
-struct __align__(16) Box {
-  double lo[4];
-  double hi[4];
-};
-
 enum Kind { KIND_TRI = 0, KIND_QUAD = 1 };
 
 struct SearchParams {
   const Box* boxA;
   const double* geoA;
+  const uint32_t* permA;    // storage → original index (NULL = identity)
   const Box* boxB;
   const double* geoB;
-  uint64_t a_begin, a_end;  // A triangle range
+  const uint32_t* permB;
+  uint64_t nA;
+  uint64_t a_begin, a_end;  // A storage range
+  uint64_t blk_first;       // first absolute A block of this shard
   uint64_t nB;
   uint64_t b_chunk;         // B triangles per CTA (multiple of TILE)
-  uint32_t shard_index, shard_count;
+  uint32_t shard_count;
   mcx_hit* hits;
   uint64_t cap;
-  unsigned long long* counters;  // [0] emitted, [1] aabb pass, [2] singular / Moller-rejected
+  unsigned long long* counters;  // [0] emitted, [1] aabb pass, [2] singular / Moller-rejected, [3] tested
+  // MCX_MODE_CULL
+  const Box* gboxA;
+  const Box* bboxA;
+  const Box* gboxB;
+  const Box* tboxB;
+  uint64_t my_blocks, ntilesB;
+  uint2* blk_list;          // overlapping (local A block, B tile) pairs
+  uint64_t blk_cap;
   // KIND_QUAD only: half-layer grids (4, M, N) for the Moller stage, and gid output
   const double* coordsA;
   const double* coordsB;
@@ -137,8 +98,22 @@ struct __align__(16) SearchSmem {
   unsigned long long full[STAGES];
 };
 
-// Process the queued pairs [0, n) of this warp's queue slice, one per lane:
-// KIND_TRI  — canonical solve, emit (iA, iB, s, t, a, b) hits;
+__device__ __forceinline__ bool box_overlap(const Box& a, const Box& b) {
+  return (b.lo[0] <= a.hi[0]) & (a.lo[0] <= b.hi[0]) & (b.lo[1] <= a.hi[1]) & (a.lo[1] <= b.hi[1]) &
+         (b.lo[2] <= a.hi[2]) & (a.lo[2] <= b.hi[2]) & (b.lo[3] <= a.hi[3]) & (a.lo[3] <= b.hi[3]);
+}
+
+__device__ __forceinline__ void empty_box(double lo[4], double hi[4]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    lo[c] = __longlong_as_double(0x7ff0000000000000ll);  // +inf: never overlaps
+    hi[c] = -lo[c];
+  }
+}
+
+// Process the queued pairs [0, n) of this warp's queue slice, one per lane
+// (queue entries are storage indices):
+// KIND_TRI  — canonical solve, emit (iA, iB, s, t, a, b) hits with original indices;
 // KIND_QUAD — SPEC-literal Moller quick test, emit surviving quad-pair gids.
 template <int KIND>
 __device__ __forceinline__ void flush_queue(const SearchParams& P, const uint2* q, int n, int lane,
@@ -167,7 +142,9 @@ __device__ __forceinline__ void flush_queue(const SearchParams& P, const uint2* 
       if (pos < P.cap) {
         if (KIND == KIND_TRI) {
           mcx_hit h;
-          h.ia = e.x; h.ib = e.y; h.s = sol[0]; h.t = sol[1]; h.a = sol[2]; h.b = sol[3];
+          h.ia = P.permA ? __ldg(P.permA + e.x) : e.x;
+          h.ib = P.permB ? __ldg(P.permB + e.y) : e.y;
+          h.s = sol[0]; h.t = sol[1]; h.a = sol[2]; h.b = sol[3];
           P.hits[pos] = h;
         } else {
           // quad indices qa = i + N1·k1, qb = j + N2·l1 → gid (PAPER.md kernel step 2)
@@ -180,6 +157,22 @@ __device__ __forceinline__ void flush_queue(const SearchParams& P, const uint2* 
   }
 }
 
+__device__ __forceinline__ void flush_counters(const SearchParams& P, int lane, unsigned long long n_pass,
+                                               unsigned long long n_sing, unsigned long long n_tested) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    n_pass += __shfl_xor_sync(0xffffffffu, n_pass, o);
+    n_sing += __shfl_xor_sync(0xffffffffu, n_sing, o);
+    n_tested += __shfl_xor_sync(0xffffffffu, n_tested, o);
+  }
+  if (lane == 0) {
+    if (n_pass) atomicAdd(P.counters + 1, n_pass);
+    if (n_sing) atomicAdd(P.counters + 2, n_sing);
+    if (n_tested) atomicAdd(P.counters + 3, n_tested);
+  }
+}
+
+// ------------------------------------------------------------ brute kernel
 template <int KIND, class C>
 __global__ void __launch_bounds__(C::THREADS, C::MINB) search_brute_kernel(const SearchParams P) {
   constexpr int R = C::R, THREADS = C::THREADS;
@@ -187,9 +180,9 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_brute_kernel(const
   SearchSmem<C>& S = *reinterpret_cast<SearchSmem<C>*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-  // ---- A block (cyclic shard) and B chunk of this CTA
-  const uint64_t gblk = P.shard_index + (uint64_t)blockIdx.x * P.shard_count;
-  const uint64_t a0 = P.a_begin + gblk * A_BLOCK;
+  // ---- absolute A block (cyclic shard) and B chunk of this CTA
+  const uint64_t gblk = P.blk_first + (uint64_t)blockIdx.x * P.shard_count;
+  const uint64_t a0 = gblk * A_BLOCK;
   const uint64_t b0 = (uint64_t)blockIdx.y * P.b_chunk;
   const uint64_t b1 = min(b0 + P.b_chunk, P.nB);
   const int ntiles = (int)((b1 - b0 + TILE - 1) / TILE);
@@ -209,7 +202,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_brute_kernel(const
     }
   }
 
-  // ---- A triangles into registers (invalid slots can never overlap).  Reloaded
+  // ---- A triangles into registers (out-of-range slots get empty boxes).  Reloaded
   // (volatile, so never CSE'd) after every survivor flush: that makes the A boxes
   // dead across the solve, so the rare slow path can use their registers and the
   // hot loop keeps <= 128 registers (2 CTAs/SM) without spilling.
@@ -220,18 +213,14 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_brute_kernel(const
   auto load_a = [&]() {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      if (aidx[r] < P.a_end) {
+      if (aidx[r] >= P.a_begin && aidx[r] < P.a_end) {
         const double* src = reinterpret_cast<const double*>(P.boxA + aidx[r]);
         ld_nc_v2(src + 0, alo[r][0], alo[r][1]);
         ld_nc_v2(src + 2, alo[r][2], alo[r][3]);
         ld_nc_v2(src + 4, ahi[r][0], ahi[r][1]);
         ld_nc_v2(src + 6, ahi[r][2], ahi[r][3]);
       } else {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          alo[r][c] = __longlong_as_double(0x7ff0000000000000ll);
-          ahi[r][c] = -alo[r][c];
-        }
+        empty_box(alo[r], ahi[r]);
       }
     }
   };
@@ -299,22 +288,111 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_brute_kernel(const
   }
   __syncwarp();
   if (qn > 0) flush_queue<KIND>(P, q, qn, lane, n_pass, n_sing);
+  flush_counters(P, lane, n_pass, n_sing, 0);
+}
 
-  // ---- per-warp counter reduction
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    n_pass += __shfl_xor_sync(0xffffffffu, n_pass, o);
-    n_sing += __shfl_xor_sync(0xffffffffu, n_sing, o);
+// ------------------------------------------------------------ cull kernels
+// Level 1: (local A block x, B tile y) union-box test, compacted with one atomic per warp.
+__global__ void __launch_bounds__(256) cull_blocks_kernel(const SearchParams P) {
+  const uint64_t total = P.my_blocks * P.ntilesB;
+  const int lane = threadIdx.x & 31;
+  for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < total; base += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t e = base + threadIdx.x;
+    bool ov = false;
+    uint32_t x = 0, y = 0;
+    if (e < total) {
+      x = (uint32_t)(e / P.ntilesB);
+      y = (uint32_t)(e % P.ntilesB);
+      const uint64_t gblk = P.blk_first + (uint64_t)x * P.shard_count;
+      ov = box_overlap(P.bboxA[gblk], P.tboxB[y]);
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, ov);
+    if (m) {
+      const int leader = __ffs(m) - 1;
+      unsigned long long pos = 0;
+      if (lane == leader) pos = atomicAdd(P.counters + 4, (unsigned long long)__popc(m));
+      pos = __shfl_sync(0xffffffffu, pos, leader) + __popc(m & ((1u << lane) - 1u));
+      if (ov && pos < P.blk_cap) P.blk_list[pos] = make_uint2(x, y);
+    }
   }
-  if (lane == 0) {
-    if (n_pass) atomicAdd(P.counters + 1, n_pass);
-    if (n_sing) atomicAdd(P.counters + 2, n_sing);
+}
+
+constexpr int CULL_THREADS = 256;
+constexpr int CULL_WARPS = CULL_THREADS / 32;
+constexpr int GPAIRS = (A_BLOCK / GROUP) * (TILE / GROUP);  // 32 × 16 group pairs per block pair
+
+struct CullSmem {
+  uint2 queue[CULL_WARPS][64];
+  uint16_t gpair[GPAIRS];
+  unsigned int n_gpair;
+};
+
+// Level 2 + pair tests: one CTA per overlapping (A block, B tile), persistent.
+__global__ void __launch_bounds__(CULL_THREADS) cull_pairs_kernel(const SearchParams P) {
+  __shared__ CullSmem S;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  unsigned long long n_pass = 0, n_sing = 0, n_tested = 0;
+  uint2* q = S.queue[warp];
+  int qn = 0;
+  const uint64_t nlist = min((uint64_t)*(volatile unsigned long long*)(P.counters + 4), P.blk_cap);
+  const uint64_t ngA = (P.nA + GROUP - 1) / GROUP, ngB = (P.nB + GROUP - 1) / GROUP;
+  for (uint64_t e = blockIdx.x; e < nlist; e += gridDim.x) {
+    const uint2 xy = P.blk_list[e];
+    const uint64_t gblk = P.blk_first + (uint64_t)xy.x * P.shard_count;
+    if (tid == 0) S.n_gpair = 0;
+    __syncthreads();
+    for (int k = tid; k < GPAIRS; k += CULL_THREADS) {
+      const uint64_t ga = gblk * (A_BLOCK / GROUP) + k / (TILE / GROUP);
+      const uint64_t gb = (uint64_t)xy.y * (TILE / GROUP) + k % (TILE / GROUP);
+      if (ga < ngA && gb < ngB && box_overlap(P.gboxA[ga], P.gboxB[gb])) S.gpair[atomicAdd(&S.n_gpair, 1u)] = (uint16_t)k;
+    }
+    __syncthreads();
+    const int ng = (int)S.n_gpair;
+    for (int w = warp; w < ng; w += CULL_WARPS) {
+      const int k = S.gpair[w];
+      const uint64_t ia = gblk * A_BLOCK + (uint64_t)(k / (TILE / GROUP)) * GROUP + lane;
+      const uint64_t jb0 = (uint64_t)xy.y * TILE + (uint64_t)(k % (TILE / GROUP)) * GROUP;
+      const bool va = ia >= P.a_begin && ia < P.a_end;
+      double alo[4], ahi[4];
+      if (va) {
+        const double2* s = reinterpret_cast<const double2*>(P.boxA + ia);
+        const double2 a = __ldg(s), b = __ldg(s + 1), c = __ldg(s + 2), d = __ldg(s + 3);
+        alo[0] = a.x; alo[1] = a.y; alo[2] = b.x; alo[3] = b.y;
+        ahi[0] = c.x; ahi[1] = c.y; ahi[2] = d.x; ahi[3] = d.y;
+      } else {
+        empty_box(alo, ahi);
+      }
+      const int nb = (int)min((uint64_t)GROUP, P.nB - jb0);
+      const unsigned vmask = __ballot_sync(0xffffffffu, va);
+      if (lane == 0) n_tested += (unsigned long long)__popc(vmask) * nb;
+      for (int j = 0; j < nb; ++j) {
+        const double2* bp = reinterpret_cast<const double2*>(P.boxB + jb0 + j);
+        const double2 l01 = __ldg(bp), l23 = __ldg(bp + 1), h01 = __ldg(bp + 2), h23 = __ldg(bp + 3);
+        const bool p = (l01.x <= ahi[0]) & (alo[0] <= h01.x) & (l01.y <= ahi[1]) & (alo[1] <= h01.y) &
+                       (l23.x <= ahi[2]) & (alo[2] <= h23.x) & (l23.y <= ahi[3]) & (alo[3] <= h23.y);
+        const unsigned m = __ballot_sync(0xffffffffu, p);
+        if (m) {
+          if (p) q[qn + __popc(m & lt_mask)] = make_uint2((uint32_t)ia, (uint32_t)(jb0 + j));
+          qn += __popc(m);
+          __syncwarp();
+          if (qn >= 32) {
+            qn -= 32;
+            flush_queue<KIND_TRI>(P, q + qn, 32, lane, n_pass, n_sing);
+          }
+        }
+      }
+    }
+    __syncthreads();  // gpair list reused by the next entry
   }
+  __syncwarp();
+  if (qn > 0) flush_queue<KIND_TRI>(P, q, qn, lane, n_pass, n_sing);
+  flush_counters(P, lane, n_pass, n_sing, n_tested);
 }
 
 // --------------------------------------------------------------- host side
 // Grid: x = A blocks of this shard, y = B chunks (multiple of TILE), sized for
-// ~16 waves at 2 CTAs/SM so the tail wave is a small fraction.
+// ~16 waves of resident CTAs so the tail wave is a small fraction.
 template <int KIND, class C>
 static int launch_brute_cfg(SearchParams P, uint64_t my_blocks, int device, cudaStream_t stream) {
   if (my_blocks == 0 || P.nB == 0) return MCX_OK;
@@ -339,20 +417,34 @@ static int launch_brute_cfg(SearchParams P, uint64_t my_blocks, int device, cuda
 }
 
 // Variant selection (MCX_VARIANT=0..3, for experiments; 0 = the tuned default:
-// R = 4, 256 threads, 2 CTAs/SM, 117 registers, no spills).
+// R = 4, 256 threads, 2 CTAs/SM, one B triangle per vote, unroll 2 — no spills).
 static int variant_from_env() {
   const char* v = getenv("MCX_VARIANT");
   return v ? atoi(v) : 0;
 }
 
 template <int KIND>
-static int launch_brute(SearchParams P, uint64_t my_blocks, int device, cudaStream_t stream) {
+static int launch_brute(const SearchParams& P, uint64_t my_blocks, int device, cudaStream_t stream) {
   switch (variant_from_env()) {
     case 1: return launch_brute_cfg<KIND, Cfg<4, 2, 1, 1>>(P, my_blocks, device, stream);
     case 2: return launch_brute_cfg<KIND, Cfg<4, 2, 1, 4>>(P, my_blocks, device, stream);
-    case 3: return launch_brute_cfg<KIND, Cfg<4, 2, 1, 8>>(P, my_blocks, device, stream);
+    case 3: return launch_brute_cfg<KIND, Cfg<4, 1, 1, 2>>(P, my_blocks, device, stream);
     default: return launch_brute_cfg<KIND, Cfg<4, 2, 1, 2>>(P, my_blocks, device, stream);
   }
+}
+
+static int launch_cull(SearchParams P, int device, cudaStream_t stream) {
+  if (P.my_blocks == 0 || P.nB == 0) return MCX_OK;
+  int dev_sms = 148;
+  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device);
+  const uint64_t total = P.my_blocks * P.ntilesB;
+  uint64_t g1 = (total + 255) / 256;
+  if (g1 > (uint64_t)dev_sms * 16) g1 = (uint64_t)dev_sms * 16;
+  cull_blocks_kernel<<<(unsigned)g1, 256, 0, stream>>>(P);
+  CUDA_TRY(cudaGetLastError());
+  cull_pairs_kernel<<<(unsigned)(dev_sms * 8), CULL_THREADS, 0, stream>>>(P);
+  CUDA_TRY(cudaGetLastError());
+  return MCX_OK;
 }
 
 struct Timing {
@@ -362,6 +454,34 @@ struct Timing {
     if (e1) cudaEventDestroy(e1);
   }
 };
+
+// Absolute-block shard geometry: blocks b in [⌊a_begin/1024⌋, ⌈a_end/1024⌉) with b % count == index.
+struct ShardGeom {
+  uint64_t first, my_blocks, na;
+};
+
+static ShardGeom shard_geom(uint64_t a_begin, uint64_t a_end, uint32_t sidx, uint32_t scount) {
+  ShardGeom g = {0, 0, 0};
+  if (a_end <= a_begin) return g;
+  const uint64_t b_lo = a_begin / A_BLOCK, b_hi = (a_end + A_BLOCK - 1) / A_BLOCK;
+  g.first = b_lo + ((uint64_t)sidx + scount - b_lo % scount) % scount;
+  if (g.first >= b_hi) return g;
+  g.my_blocks = (b_hi - g.first + scount - 1) / scount;
+  for (uint64_t x = 0; x < g.my_blocks; ++x) {
+    const uint64_t b = g.first + x * scount;
+    const uint64_t lo = b * A_BLOCK > a_begin ? b * A_BLOCK : a_begin;
+    const uint64_t hi = (b + 1) * A_BLOCK < a_end ? (b + 1) * A_BLOCK : a_end;
+    g.na += hi - lo;
+  }
+  return g;
+}
+
+static uint64_t cull_list_cap(const mcx_mesh_dev* A, const mcx_mesh_dev* B, const mcx_opts* o) {
+  const uint64_t a_end = o->a_end ? o->a_end : A->n_tri;
+  const uint32_t scount = o->shard_count ? o->shard_count : 1;
+  const ShardGeom g = shard_geom(o->a_begin, a_end, o->shard_index % scount, scount);
+  return g.my_blocks * ((B->n_tri + TILE - 1) / TILE);
+}
 
 static int launch_search(const mcx_mesh_dev* A, const mcx_mesh_dev* B, const mcx_opts* o, mcx_hit* hits,
                          uint64_t cap, mcx_stats* st) {
@@ -377,6 +497,9 @@ static int launch_search(const mcx_mesh_dev* A, const mcx_mesh_dev* B, const mcx
   if (A->n_tri >= (1ull << 32) || B->n_tri >= (1ull << 32))
     return set_error(MCX_E_ARG, "triangle counts must be < 2^32");
   if (o->mode != MCX_MODE_BRUTE && o->mode != MCX_MODE_CULL) return set_error(MCX_E_ARG, "unknown mode %d", o->mode);
+  if (o->mode == MCX_MODE_CULL && (!A->gbox || !A->bbox || !B->gbox || !B->tbox))
+    return set_error(MCX_E_ARG, "MCX_MODE_CULL needs level boxes (mcx_levels) on both meshes");
+  if (!A->box || !B->box || !A->geo || !B->geo) return set_error(MCX_E_ARG, "null box/geo");
   if (!o->workspace || o->workspace_bytes < mcx_workspace_bytes(A, B, o))
     return set_error(MCX_E_ARG, "workspace too small (need %llu bytes)",
                      (unsigned long long)mcx_workspace_bytes(A, B, o));
@@ -385,19 +508,11 @@ static int launch_search(const mcx_mesh_dev* A, const mcx_mesh_dev* B, const mcx
   if (cap > 0 && !hits) return set_error(MCX_E_ARG, "null hit buffer with nonzero capacity");
 
   unsigned long long* counters = (unsigned long long*)o->workspace;
-  CUDA_TRY(cudaMemsetAsync(counters, 0, 4 * sizeof(unsigned long long), stream));
+  CUDA_TRY(cudaMemsetAsync(counters, 0, 8 * sizeof(unsigned long long), stream));
 
-  const uint64_t nblk_total = (a_end - a_begin + A_BLOCK - 1) / A_BLOCK;
-  const uint64_t my_blocks = nblk_total > sidx ? (nblk_total - sidx + scount - 1) / scount : 0;
+  const ShardGeom g = shard_geom(a_begin, a_end, sidx, scount);
   const uint64_t nB = B->n_tri;
-  uint64_t na = 0;  // A triangles in this shard's blocks
-  if (my_blocks > 0) {
-    na = my_blocks * (uint64_t)A_BLOCK;
-    const uint64_t last = sidx + (my_blocks - 1) * scount;  // only the globally last block can be ragged
-    if (last == nblk_total - 1) na -= (uint64_t)A_BLOCK - ((a_end - a_begin) - last * A_BLOCK);
-  }
-  st->n_pairs = na * nB;
-  st->n_tested = st->n_pairs;
+  st->n_pairs = g.na * nB;
 
   Timing tm;
   if (o->timing) {
@@ -408,25 +523,42 @@ static int launch_search(const mcx_mesh_dev* A, const mcx_mesh_dev* B, const mcx
   SearchParams P = {};
   P.boxA = reinterpret_cast<const Box*>(A->box);
   P.geoA = A->geo;
+  P.permA = A->perm;
   P.boxB = reinterpret_cast<const Box*>(B->box);
   P.geoB = B->geo;
+  P.permB = B->perm;
+  P.nA = A->n_tri;
   P.a_begin = a_begin;
   P.a_end = a_end;
+  P.blk_first = g.first;
   P.nB = nB;
-  P.shard_index = sidx;
   P.shard_count = scount;
   P.hits = hits;
   P.cap = cap;
   P.counters = counters;
-  int rc = launch_brute<KIND_TRI>(P, my_blocks, o->device, stream);
+  int rc;
+  if (o->mode == MCX_MODE_BRUTE) {
+    rc = launch_brute<KIND_TRI>(P, g.my_blocks, o->device, stream);
+  } else {
+    P.gboxA = reinterpret_cast<const Box*>(A->gbox);
+    P.bboxA = reinterpret_cast<const Box*>(A->bbox);
+    P.gboxB = reinterpret_cast<const Box*>(B->gbox);
+    P.tboxB = reinterpret_cast<const Box*>(B->tbox);
+    P.my_blocks = g.my_blocks;
+    P.ntilesB = (nB + TILE - 1) / TILE;
+    P.blk_list = reinterpret_cast<uint2*>((char*)o->workspace + 256);
+    P.blk_cap = cull_list_cap(A, B, o);
+    rc = launch_cull(P, o->device, stream);
+  }
   if (rc != MCX_OK) return rc;
   if (o->timing) CUDA_TRY(cudaEventRecord(tm.e1, stream));
-  unsigned long long h[4];
+  unsigned long long h[8];
   CUDA_TRY(cudaMemcpyAsync(h, counters, sizeof(h), cudaMemcpyDeviceToHost, stream));
   CUDA_TRY(cudaStreamSynchronize(stream));
   st->n_hits = h[0];
   st->n_aabb_pass = h[1];
   st->n_singular = h[2];
+  st->n_tested = o->mode == MCX_MODE_BRUTE ? st->n_pairs : h[3];
   st->kernel_ms = 0.0;
   if (o->timing) {
     float ms = 0.f;
@@ -465,20 +597,22 @@ static int launch_pair_candidates(const double* cA, uint32_t NA, uint32_t MA, co
   const uint64_t need = 256 + (nqA + nqB) * sizeof(Box);
   if (!ws || ws_bytes < need)
     return set_error(MCX_E_ARG, "workspace too small (need %llu bytes)", (unsigned long long)need);
+  if (cap > 0 && !gids) return set_error(MCX_E_ARG, "null gid buffer with nonzero capacity");
   unsigned long long* counters = (unsigned long long*)ws;
   Box* boxA = reinterpret_cast<Box*>((char*)ws + 256);
   Box* boxB = boxA + nqA;
-  CUDA_TRY(cudaMemsetAsync(counters, 0, 4 * sizeof(unsigned long long), stream));
+  CUDA_TRY(cudaMemsetAsync(counters, 0, 8 * sizeof(unsigned long long), stream));
   quad_box_kernel<<<(unsigned)min((nqA + 255) / 256, (uint64_t)148 * 64), 256, 0, stream>>>(cA, NA, MA, boxA);
   quad_box_kernel<<<(unsigned)min((nqB + 255) / 256, (uint64_t)148 * 64), 256, 0, stream>>>(cB, NB, MB, boxB);
   CUDA_TRY(cudaGetLastError());
   SearchParams P = {};
   P.boxA = boxA;
   P.boxB = boxB;
+  P.nA = nqA;
   P.a_begin = 0;
   P.a_end = nqA;
+  P.blk_first = 0;
   P.nB = nqB;
-  P.shard_index = 0;
   P.shard_count = 1;
   P.cap = cap;
   P.counters = counters;
@@ -488,7 +622,7 @@ static int launch_pair_candidates(const double* cA, uint32_t NA, uint32_t MA, co
   P.gids = gids;
   int rc = launch_brute<KIND_QUAD>(P, (nqA + A_BLOCK - 1) / A_BLOCK, device, stream);
   if (rc != MCX_OK) return rc;
-  unsigned long long h[4];
+  unsigned long long h[8];
   CUDA_TRY(cudaMemcpyAsync(h, counters, sizeof(h), cudaMemcpyDeviceToHost, stream));
   CUDA_TRY(cudaStreamSynchronize(stream));
   *n_out = h[0];
@@ -504,20 +638,9 @@ extern "C" {
 
 uint32_t mcx_a_block(void) { return mcx::A_BLOCK; }
 
-uint64_t mcx_workspace_bytes(const mcx_mesh_dev*, const mcx_mesh_dev*, const mcx_opts*) { return 256; }
-
-int mcx_pack(const double* coords, uint32_t N, uint32_t M, double* box, double* geo, int device, void* stream) {
-  using namespace mcx;
-  if (N < 1 || M < 2) return set_error(MCX_E_ARG, "pack needs N >= 1 and M >= 2 (got N=%u, M=%u)", N, M);
-  if (((uintptr_t)box | (uintptr_t)geo) & 15) return set_error(MCX_E_ARG, "box/geo must be 16-byte aligned");
-  CUDA_TRY(cudaSetDevice(device));
-  const uint64_t n = 2ull * N * (M - 1);
-  const int threads = 256;
-  uint64_t blocks = (n + threads - 1) / threads;
-  if (blocks > 148ull * 64) blocks = 148ull * 64;
-  pack_kernel<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(coords, N, M, box, geo);
-  CUDA_TRY(cudaGetLastError());
-  return MCX_OK;
+uint64_t mcx_workspace_bytes(const mcx_mesh_dev* A, const mcx_mesh_dev* B, const mcx_opts* o) {
+  if (!A || !B || !o || o->mode != MCX_MODE_CULL) return 256;
+  return 256 + 8 * mcx::cull_list_cap(A, B, o);
 }
 
 int mcx_search(const mcx_mesh_dev* A, const mcx_mesh_dev* B, const mcx_opts* o, mcx_hit* hits, uint64_t cap,

@@ -54,9 +54,15 @@ def _check_coords(coords) -> None:
 
 
 class DeviceMesh:
-    """A half-layer grid resident in HBM, packed into triangle records on the device."""
+    """A half-layer grid resident in HBM, packed into triangle records on the device.
 
-    def __init__(self, coords, device: int = 0, stream=None):
+    Records are stored in the tiled order (``_lib.ORDER_TILED``) with ``perm``
+    mapping storage position → original triangle index, plus the culling
+    hierarchy (group / tile / block union boxes).  Both search modes use this
+    layout; hits always carry original indices.
+    """
+
+    def __init__(self, coords, device: int = 0, stream=None, order: int = _lib.ORDER_TILED):
         t = torch()
         _require_cuda(device)
         dev = t.device("cuda", device)
@@ -76,15 +82,27 @@ class DeviceMesh:
         self.n_tri = 2 * self.N * (self.M - 1)
         if self.n_tri >= 2 ** 32:
             raise ConfigError("triangle count must be < 2^32")
-        self.box = t.empty((self.n_tri, _lib.BOX_STRIDE), dtype=t.float64, device=dev)
-        self.geo = t.empty((self.n_tri, _lib.GEO_STRIDE), dtype=t.float64, device=dev)
+        n = self.n_tri
+        self.order = order
+        with t.cuda.device(device), t.cuda.stream(s):
+            self.box = t.empty((n, _lib.BOX_STRIDE), dtype=t.float64, device=dev)
+            self.geo = t.empty((n, _lib.GEO_STRIDE), dtype=t.float64, device=dev)
+            self.perm = t.empty(n, dtype=t.int32, device=dev) if order == _lib.ORDER_TILED else None
+            self.gbox = t.empty((-(-n // _lib.GROUP), 8), dtype=t.float64, device=dev)
+            self.tbox = t.empty((-(-n // _lib.TILE), 8), dtype=t.float64, device=dev)
+            self.bbox = t.empty((-(-n // _lib.BLOCK), 8), dtype=t.float64, device=dev)
         L = _lib.load()
-        rc = L.mcx_pack(self.coords.data_ptr(), self.N, self.M, self.box.data_ptr(), self.geo.data_ptr(),
-                        device, s.cuda_stream)
+        rc = L.mcx_pack(self.coords.data_ptr(), self.N, self.M, order, self.box.data_ptr(), self.geo.data_ptr(),
+                        self.perm.data_ptr() if self.perm is not None else None, device, s.cuda_stream)
         _lib.check(rc, "mcx_pack")
+        rc = L.mcx_levels(self.box.data_ptr(), n, self.gbox.data_ptr(), self.tbox.data_ptr(), self.bbox.data_ptr(),
+                          device, s.cuda_stream)
+        _lib.check(rc, "mcx_levels")
 
     def struct(self) -> _lib.MeshDev:
-        return _lib.MeshDev(self.n_tri, self.box.data_ptr(), self.geo.data_ptr())
+        return _lib.MeshDev(self.n_tri, self.box.data_ptr(), self.geo.data_ptr(),
+                            self.perm.data_ptr() if self.perm is not None else None,
+                            self.gbox.data_ptr(), self.tbox.data_ptr(), self.bbox.data_ptr())
 
 
 @dataclass

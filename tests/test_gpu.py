@@ -42,14 +42,39 @@ def c1():
     return z
 
 
-def test_device_pack_bit_exact(c1):
-    m = D.DeviceMesh(c1["A"], 0)
-    pk = O.pack(c1["A"])
+@pytest.mark.parametrize("order", [_lib.ORDER_TILED, _lib.ORDER_NATURAL])
+@pytest.mark.parametrize("shape", [(64, 64), (37, 23), (5, 2), (1024, 3)])
+def test_device_pack_bit_exact(order, shape):
+    """Every packed record equals the oracle's packing of its original triangle (tiled
+    order: via perm, which must be a bijection)."""
+    A, _ = manifold_like(shape[0], shape[1], 1)
+    m = D.DeviceMesh(A, 0, order=order)
+    pk = O.pack(A)
     box, geo = m.box.cpu().numpy(), m.geo.cpu().numpy()
+    if order == _lib.ORDER_TILED:
+        perm = m.perm.cpu().numpy().astype(np.int64)
+        assert np.array_equal(np.sort(perm), np.arange(m.n_tri))
+    else:
+        perm = np.arange(m.n_tri)
+    pk = O.take(pk, perm)
     assert np.array_equal(_bits(box[:, :4]), _bits(pk["lo"])) and np.array_equal(_bits(box[:, 4:]), _bits(pk["hi"]))
     for k, sl in (("p", slice(0, 4)), ("e1", slice(4, 8)), ("e2", slice(8, 12)), ("P", slice(12, 18))):
         assert np.array_equal(_bits(geo[:, sl]), _bits(pk[k])), k
     assert np.array_equal(_bits(geo[:, 18]), _bits(pk["nrm"]))
+    # level boxes are the exact unions of their records
+    gb = m.gbox.cpu().numpy()
+    for g in (0, len(gb) // 2, len(gb) - 1):
+        seg = box[g * 32:(g + 1) * 32]
+        assert np.array_equal(gb[g, :4], seg[:, :4].min(0)) and np.array_equal(gb[g, 4:], seg[:, 4:].max(0))
+    tb, bb = m.tbox.cpu().numpy(), m.bbox.cpu().numpy()
+    assert np.array_equal(tb[0, :4], box[:512, :4].min(0)) and np.array_equal(bb[-1, 4:], box[(len(bb) - 1) * 1024:, 4:].max(0))
+
+
+def test_tiled_order_is_spatially_compact():
+    A, _ = manifold_like(256, 129, 1)
+    tiled, nat = D.DeviceMesh(A, 0), D.DeviceMesh(A, 0, order=_lib.ORDER_NATURAL)
+    ext = lambda m: float(np.mean(np.max(m.gbox.cpu().numpy()[:, 4:] - m.gbox.cpu().numpy()[:, :4], axis=1)))
+    assert ext(tiled) < 0.5 * ext(nat)
 
 
 def test_golden_c1(c1):
@@ -70,12 +95,20 @@ def test_golden_c4ii_exact_lattice():
     assert_same_hits(ref, r.hits, r.stats)
 
 
+MODES = [_lib.MODE_BRUTE, _lib.MODE_CULL]
+
+
+@pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("name", ["C1", "C4i", "C4ii", "C4iii"])
-def test_parity_small(name, oracle_lib):
+def test_parity_small(name, mode, oracle_lib):
     A, _, B, _ = config_pair(name)
     ref = oracle_lib.search(A, B, sweep=True)
-    r = D.search(A, B)
+    r = D.search(A, B, mode=mode)
     assert_same_hits(ref, r.hits, r.stats)
+    if mode == _lib.MODE_CULL:
+        assert r.stats["n_tested"] < r.stats["n_pairs"]
+    else:
+        assert r.stats["n_tested"] == r.stats["n_pairs"]
     assert r.stats["n_pairs"] == A.shape[2] * (A.shape[1] - 1) * 2 * B.shape[2] * (B.shape[1] - 1) * 2
 
 
@@ -88,43 +121,65 @@ def test_kernel_variants_identical(variant, monkeypatch, oracle_lib):
     assert_same_hits(ref, r.hits, r.stats)
 
 
-def test_parity_c2_full(oracle_lib):
+@pytest.mark.parametrize("mode", MODES)
+def test_parity_c2_full(mode, oracle_lib):
     """C2 (256×256 each, 1.7e10 pairs) against the C oracle's exact sweep-and-prune."""
     A, _, B, _ = config_pair("C2")
     ref = oracle_lib.search(A, B, sweep=True)
-    r = D.search(A, B)
+    r = D.search(A, B, mode=mode)
     assert_same_hits(ref, r.hits, r.stats)
 
 
-def test_parity_c5_reduced(oracle_lib):
-    """C5 at 1/8 scale: unbalanced 256×129 vs 32×17, hits concentrated in A's first columns."""
-    A, _, B, _ = config_pair("C5/8")
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("scale", [8, 4])
+def test_parity_c5_reduced(scale, mode, oracle_lib):
+    """C5 at 1/8 and 1/4 scale: unbalanced meshes, hits concentrated in A's first columns."""
+    A, _, B, _ = config_pair(f"C5/{scale}")
     ref = oracle_lib.search(A, B, sweep=True)
-    r = D.search(A, B)
+    r = D.search(A, B, mode=mode)
     assert_same_hits(ref, r.hits, r.stats)
     assert len(ref["ia"]) > 50
 
 
+@pytest.mark.slow
+def test_parity_c3_cull_vs_oracle(oracle_lib):
+    """C3 (1.095e12 pairs) in cull mode against the C oracle's exact sweep-and-prune."""
+    A, _, B, _ = config_pair("C3")
+    ref = oracle_lib.search(A, B, sweep=True)
+    r = D.search(A, B, mode=_lib.MODE_CULL)
+    assert_same_hits(ref, r.hits, r.stats)
+
+
+@pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("G", [2, 3, 8])
-def test_shard_invariance(G, oracle_lib):
+def test_shard_invariance(G, mode, oracle_lib):
     """Cyclic A-block sharding (the multi-GPU partition) never changes the hit set."""
     A, _, B, _ = config_pair("C4i")
     Am, Bm = D.DeviceMesh(A, 0), D.DeviceMesh(B, 0)
-    full = D.search_device(Am, Bm)
-    parts = [D.search_device(Am, Bm, shard=(g, G)) for g in range(G)]
+    full = D.search_device(Am, Bm, mode=mode)
+    parts = [D.search_device(Am, Bm, shard=(g, G), mode=mode) for g in range(G)]
     merged = D._merge(parts)
     assert np.array_equal(merged.hits, full.hits)
     assert sum(p.stats["n_pairs"] for p in parts) == full.stats["n_pairs"]
     assert merged.stats["n_aabb_pass"] == full.stats["n_aabb_pass"]
 
 
-def test_a_range_partition():
+@pytest.mark.parametrize("mode", MODES)
+def test_a_range_partition(mode):
     A, _, B, _ = config_pair("C4iii")
     Am, Bm = D.DeviceMesh(A, 0), D.DeviceMesh(B, 0)
-    full = D.search_device(Am, Bm)
+    full = D.search_device(Am, Bm, mode=mode)
     cuts = [0, 1000, 4097, 4100, Am.n_tri]
-    parts = [D.search_device(Am, Bm, a_range=(a, b)) for a, b in zip(cuts[:-1], cuts[1:])]
+    parts = [D.search_device(Am, Bm, a_range=(a, b), mode=mode) for a, b in zip(cuts[:-1], cuts[1:])]
     assert np.array_equal(D._merge(parts).hits, full.hits)
+    assert sum(p.stats["n_pairs"] for p in parts) == full.stats["n_pairs"]
+
+
+def test_natural_and_tiled_orders_agree():
+    A, _, B, _ = config_pair("C4i")
+    r1 = D.search_device(D.DeviceMesh(A, 0, order=_lib.ORDER_NATURAL), D.DeviceMesh(B, 0, order=_lib.ORDER_NATURAL))
+    r2 = D.search_device(D.DeviceMesh(A, 0), D.DeviceMesh(B, 0))
+    assert np.array_equal(r1.hits, r2.hits)
 
 
 def test_capacity_regrow():
@@ -148,19 +203,23 @@ def test_swap_roles_symmetry():
     assert k1 == k2
 
 
-def test_disjoint_and_degenerate_inputs():
+@pytest.mark.parametrize("mode", MODES)
+def test_disjoint_and_degenerate_inputs(mode):
     A, _ = manifold_like(32, 9, 1)
     far = A + 100.0
-    r = D.search(A, far)
+    r = D.search(A, far, mode=mode)
     assert len(r.hits) == 0 and r.stats["n_aabb_pass"] == 0
+    if mode == _lib.MODE_CULL:
+        assert r.stats["n_tested"] == 0
     # ragged sizes: A smaller than one block, B smaller than one tile, N odd
-    A2, _ = manifold_like(5, 2, 3)
-    B2, _ = manifold_like(7, 3, 3)
-    ref = O.search(A2, B2)
-    assert_same_hits(ref, D.search(A2, B2).hits)
+    for na, ma, nb, mb in ((5, 2, 7, 3), (37, 23, 19, 41), (1, 2, 3, 2)):
+        A2, _ = manifold_like(na, ma, 3)
+        B2, _ = manifold_like(nb, mb, 3)
+        ref = O.search(A2, B2)
+        assert_same_hits(ref, D.search(A2, B2, mode=mode).hits)
     # flat/degenerate triangles (all vertices identical) are singular, never hits
     Z = np.zeros((4, 3, 4))
-    rz = D.search(Z, Z)
+    rz = D.search(Z, Z, mode=mode)
     assert len(rz.hits) == 0 and rz.stats["n_singular"] == rz.stats["n_aabb_pass"] == (2 * 4 * 2) ** 2
 
 
