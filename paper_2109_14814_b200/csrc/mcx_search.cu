@@ -47,8 +47,9 @@ namespace mcx {
 constexpr int STAGES = 2;
 
 // Kernel variant: R A triangles per thread, MINB resident CTAs per SM (register cap).
-template <int R_, int MINB_, int JB_ = 1, int UNROLL_ = 2>
+template <int R_, int MINB_, int JB_ = 1, int UNROLL_ = 2, int PF_ = 0>
 struct Cfg {
+  static constexpr int PF = PF_;             // prefetch the next B box before testing the current
   static constexpr int R = R_;
   static constexpr int MINB = MINB_;
   static constexpr int JB = JB_;             // B triangles per warp vote
@@ -274,10 +275,47 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_brute_kernel(const
         }
       }
     };
-    const int nmain = nvalid - nvalid % C::JB;
+    if constexpr (C::PF) {
+      // software-pipelined: the LDS of box j+1 is issued before the compares of box j
+      const double2* bp0 = reinterpret_cast<const double2*>(tile);
+      double2 n01 = bp0[0], n23 = bp0[1], m01 = bp0[2], m23 = bp0[3];
 #pragma unroll(C::UNROLL)
-    for (int j = 0; j < nmain; j += C::JB) step(j, std::integral_constant<int, C::JB>());
-    for (int j = nmain; j < nvalid; ++j) step(j, std::integral_constant<int, 1>());
+      for (int j = 0; j < nvalid; ++j) {
+        const double2 l01 = n01, l23 = n23, h01 = m01, h23 = m23;
+        const double2* bp = reinterpret_cast<const double2*>(tile + min(j + 1, nvalid - 1));
+        n01 = bp[0]; n23 = bp[1]; m01 = bp[2]; m23 = bp[3];
+        bool p[R];
+        bool any = false;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          p[r] = (l01.x <= ahi[r][0]) & (alo[r][0] <= h01.x) & (l01.y <= ahi[r][1]) & (alo[r][1] <= h01.y) &
+                 (l23.x <= ahi[r][2]) & (alo[r][2] <= h23.x) & (l23.y <= ahi[r][3]) & (alo[r][3] <= h23.y);
+          any |= p[r];
+        }
+        if (__any_sync(0xffffffffu, any)) {
+          const uint32_t ib = (uint32_t)(tb + j);
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const unsigned m = __ballot_sync(0xffffffffu, p[r]);
+            if (p[r]) q[qn + __popc(m & lt_mask)] = make_uint2(aidx[r], ib);
+            qn += __popc(m);
+          }
+          __syncwarp();
+          if (qn >= 32) {
+            do {
+              qn -= 32;
+              flush_queue<KIND>(P, q + qn, 32, lane, n_pass, n_sing);
+            } while (qn >= 32);
+            load_a();
+          }
+        }
+      }
+    } else {
+      const int nmain = nvalid - nvalid % C::JB;
+#pragma unroll(C::UNROLL)
+      for (int j = 0; j < nmain; j += C::JB) step(j, std::integral_constant<int, C::JB>());
+      for (int j = nmain; j < nvalid; ++j) step(j, std::integral_constant<int, 1>());
+    }
     __syncthreads();  // every warp is done reading stage s
     if (tid == 0 && t + STAGES < ntiles) {
       const uint64_t nb = b0 + (uint64_t)(t + STAGES) * TILE;
@@ -398,18 +436,35 @@ static int launch_brute_cfg(SearchParams P, uint64_t my_blocks, int device, cuda
   if (my_blocks == 0 || P.nB == 0) return MCX_OK;
   int dev_sms = 148;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device);
-  const uint64_t want = (uint64_t)dev_sms * C::MINB * 16;
-  uint64_t nchunk = (want + my_blocks - 1) / my_blocks;
-  const uint64_t max_chunks = (P.nB + TILE - 1) / TILE;
-  if (nchunk > max_chunks) nchunk = max_chunks;
-  if (nchunk < 1) nchunk = 1;
-  uint64_t chunk = (P.nB + nchunk - 1) / nchunk;
-  chunk = (chunk + TILE - 1) / TILE * TILE;
-  nchunk = (P.nB + chunk - 1) / chunk;
-  if (my_blocks > 0x7fffffffull || nchunk > 65535) return set_error(MCX_E_ARG, "grid too large");
-  P.b_chunk = chunk;
   const size_t smem = sizeof(SearchSmem<C>);
   CUDA_TRY(cudaFuncSetAttribute(search_brute_kernel<KIND, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = C::MINB;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, search_brute_kernel<KIND, C>, C::THREADS, smem));
+  const uint64_t slots = (uint64_t)dev_sms * (occ > 0 ? occ : 1);
+  // B chunk count: every CTA does the same work, so pick the count whose CTA total
+  // best fills whole waves of resident CTAs (the last partial wave idles the rest
+  // of the GPU), among counts giving >= 8 waves with chunks >= 16 tiles.
+  const uint64_t max_chunks = (P.nB + TILE - 1) / TILE;
+  uint64_t nchunk = 1, chunk = max_chunks * TILE;
+  const uint64_t min_ch = (my_blocks * max_chunks < 8 * slots) ? (uint64_t)TILE : 16 * (uint64_t)TILE;
+  double best = -1.0;
+  for (uint64_t c = 1; c <= max_chunks && c <= 4096; ++c) {
+    const uint64_t ch = ((P.nB + c - 1) / c + TILE - 1) / TILE * TILE;
+    const uint64_t nc = (P.nB + ch - 1) / ch;
+    if (nc != c) continue;
+    const uint64_t total = my_blocks * nc;
+    const bool enough = total >= 8 * slots || nc == max_chunks;
+    if (!enough && c < max_chunks && ch > min_ch) continue;
+    const double eff = (double)total / (double)(((total + slots - 1) / slots) * slots);
+    if (eff > best + 1e-3) {
+      best = eff;
+      nchunk = nc;
+      chunk = ch;
+    }
+    if (best > 0.995 || ch <= min_ch) break;
+  }
+  if (my_blocks > 0x7fffffffull || nchunk > 65535) return set_error(MCX_E_ARG, "grid too large");
+  P.b_chunk = chunk;
   dim3 grid((unsigned)my_blocks, (unsigned)nchunk);
   search_brute_kernel<KIND, C><<<grid, C::THREADS, smem, stream>>>(P);
   CUDA_TRY(cudaGetLastError());
@@ -417,7 +472,8 @@ static int launch_brute_cfg(SearchParams P, uint64_t my_blocks, int device, cuda
 }
 
 // Variant selection (MCX_VARIANT=0..3, for experiments; 0 = the tuned default:
-// R = 4, 256 threads, 2 CTAs/SM, one B triangle per vote, unroll 2 — no spills).
+// R = 4, 256 threads, 2 CTAs/SM, one B triangle per vote, next B box prefetched
+// from shared memory before the current one's compares, unroll 4 — no spills).
 static int variant_from_env() {
   const char* v = getenv("MCX_VARIANT");
   return v ? atoi(v) : 0;
@@ -426,10 +482,10 @@ static int variant_from_env() {
 template <int KIND>
 static int launch_brute(const SearchParams& P, uint64_t my_blocks, int device, cudaStream_t stream) {
   switch (variant_from_env()) {
-    case 1: return launch_brute_cfg<KIND, Cfg<4, 2, 1, 1>>(P, my_blocks, device, stream);
-    case 2: return launch_brute_cfg<KIND, Cfg<4, 2, 1, 4>>(P, my_blocks, device, stream);
-    case 3: return launch_brute_cfg<KIND, Cfg<4, 1, 1, 2>>(P, my_blocks, device, stream);
-    default: return launch_brute_cfg<KIND, Cfg<4, 2, 1, 2>>(P, my_blocks, device, stream);
+    case 1: return launch_brute_cfg<KIND, Cfg<4, 2, 1, 2, 0>>(P, my_blocks, device, stream);
+    case 2: return launch_brute_cfg<KIND, Cfg<4, 2, 1, 8, 1>>(P, my_blocks, device, stream);
+    case 3: return launch_brute_cfg<KIND, Cfg<4, 2, 1, 2, 1>>(P, my_blocks, device, stream);
+    default: return launch_brute_cfg<KIND, Cfg<4, 2, 1, 4, 1>>(P, my_blocks, device, stream);
   }
 }
 
