@@ -100,11 +100,22 @@ typedef struct mcx_opts {
   uint64_t workspace_bytes;
 } mcx_opts;
 
+/* One search task of a batch (e.g. one layer-pair of the reference's plan,
+ * SPEC.md:382-405): A's storage range [a_begin, a_end) (a_end = 0 → all)
+ * against all of B.  Both meshes must live on opts->device. */
+typedef struct mcx_task {
+  const mcx_mesh_dev* A;
+  const mcx_mesh_dev* B;
+  uint64_t a_begin;
+  uint64_t a_end;
+} mcx_task;
+
 /* A-block granularity of the kernel and of cyclic sharding. */
 uint32_t mcx_a_block(void);
 
-/* Device scratch the search needs for these meshes and options. */
+/* Device scratch the search needs for these meshes and options (16-byte aligned). */
 uint64_t mcx_workspace_bytes(const mcx_mesh_dev* A, const mcx_mesh_dev* B, const mcx_opts* opts);
+uint64_t mcx_batch_workspace_bytes(const mcx_task* tasks, uint32_t n_tasks, const mcx_opts* opts);
 
 /* Canonical triangle packing on the device (replaces the host-side triangle
  * construction of PAPER.md kernel steps 3-4 / SPEC Quad4 split).
@@ -128,6 +139,16 @@ int mcx_levels(const double* box, uint64_t n_tri, double* gbox, double* tbox, do
 int mcx_search(const mcx_mesh_dev* A, const mcx_mesh_dev* B, const mcx_opts* opts,
                mcx_hit* hits, uint64_t cap, mcx_stats* stats);
 
+/* Many searches in ONE launch per kernel (the reference's layer-pair task loop,
+ * SPEC.md:402, 504, run as one device job): every task's work units go into a
+ * single grid (brute) or a single flattened culling pass (cull).  Hits of all
+ * tasks share `hits` (up to cap); hit_task[k] (device, may be NULL) is the task
+ * index of hits[k]; stats[t] (host, n_tasks entries) gets task t's counters.
+ * opts->a_begin/a_end are ignored (per-task ranges are in the tasks).
+ * Synchronises opts->stream once, at the end. */
+int mcx_search_batch(const mcx_task* tasks, uint32_t n_tasks, const mcx_opts* opts,
+                     mcx_hit* hits, uint32_t* hit_task, uint64_t cap, mcx_stats* stats);
+
 /* Quad-pair candidate list of the SPEC-literal predicate: not aabb_reject (quad
  * boxes) and not moller_reject (PAPER.md kernel steps
  * 5-7).  A, B given as half-layer grids (device, (4, M, N)).  Writes up to cap
@@ -138,6 +159,7 @@ int mcx_pair_candidates(const double* coords_a, uint32_t NA, uint32_t MA,
                         const double* coords_b, uint32_t NB, uint32_t MB,
                         int device, void* stream, void* workspace, uint64_t workspace_bytes,
                         uint64_t* gids, uint64_t cap, uint64_t* n_out);
+/* workspace for mcx_pair_candidates: 1024 + 64·(N_A(M_A−1) + N_B(M_B−1)) bytes, 16-byte aligned. */
 
 const char* mcx_last_error(void);
 int mcx_version(void);

@@ -21,14 +21,19 @@ ORDER_NATURAL, ORDER_TILED = 0, 1
 BOX_STRIDE, GEO_STRIDE = 8, 20
 GROUP, TILE, BLOCK = 32, 512, 1024
 
-EXPORTS = ("mcx_a_block", "mcx_workspace_bytes", "mcx_pack", "mcx_levels", "mcx_search", "mcx_pair_candidates",
-           "mcx_last_error", "mcx_version")
+EXPORTS = ("mcx_a_block", "mcx_workspace_bytes", "mcx_batch_workspace_bytes", "mcx_pack", "mcx_levels",
+           "mcx_search", "mcx_search_batch", "mcx_pair_candidates", "mcx_last_error", "mcx_version")
 
 
 class MeshDev(ctypes.Structure):
     _fields_ = [("n_tri", ctypes.c_uint64), ("box", ctypes.c_void_p), ("geo", ctypes.c_void_p),
                 ("perm", ctypes.c_void_p), ("gbox", ctypes.c_void_p), ("tbox", ctypes.c_void_p),
                 ("bbox", ctypes.c_void_p)]
+
+
+class Task(ctypes.Structure):
+    _fields_ = [("A", ctypes.POINTER(MeshDev)), ("B", ctypes.POINTER(MeshDev)), ("a_begin", ctypes.c_uint64),
+                ("a_end", ctypes.c_uint64)]
 
 
 class Hit(ctypes.Structure):
@@ -73,6 +78,10 @@ def load():
     L.mcx_a_block.argtypes = []
     L.mcx_workspace_bytes.restype = u64
     L.mcx_workspace_bytes.argtypes = [P(MeshDev), P(MeshDev), P(Opts)]
+    L.mcx_batch_workspace_bytes.restype = u64
+    L.mcx_batch_workspace_bytes.argtypes = [P(Task), u32, P(Opts)]
+    L.mcx_search_batch.restype = i32
+    L.mcx_search_batch.argtypes = [P(Task), u32, P(Opts), vp, vp, u64, P(Stats)]
     L.mcx_pack.restype = i32
     L.mcx_pack.argtypes = [vp, u32, u32, i32, vp, vp, vp, i32, vp]
     L.mcx_levels.restype = i32

@@ -1,0 +1,77 @@
+"""Command line for the search stages of the reference pipeline.
+
+Only the two stages on the mesh-search path are provided, with the reference's
+flags and files:
+
+    python -m paper_2109_14814_b200.cli layers --umesh U.mnf --smesh S.mnf --nmax N --plan plan.txt
+    python -m paper_2109_14814_b200.cli intersect --umesh U.mnf --smesh S.mnf --plan plan.txt \
+        --backend cuda --out records.txt [--mode cull|brute]
+
+Meshes are MNF1 files, the plan is ``n1 sign1 n2 sign2 tof`` per
+line, records are ``n1 sign1 n2 sign2 gid x y px py a b c d theta_u
+s_u theta_s s_s``.  Exit codes: 0 ok, 2 config error,
+3 numerical / backend failure, 4 I/O error.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+
+from .errors import ConfigError, FileFormatError, ManiconnError
+
+
+def _parser():
+    ap = argparse.ArgumentParser(prog="maniconn-b200")
+    ap.add_argument("--log-level", default="warning")
+    sub = ap.add_subparsers(dest="cmd", required=True)
+    la = sub.add_parser("layers", help="enumerate the layer-pair plan")
+    la.add_argument("--umesh", required=True)
+    la.add_argument("--smesh", required=True)
+    la.add_argument("--nmax", type=int, required=True)
+    la.add_argument("--omega-p", type=float, default=1.0, help="perturbation frequency Ω_p for the TOF")
+    la.add_argument("--plan", required=True)
+    it = sub.add_parser("intersect", help="search every planned layer pair for mesh intersections")
+    it.add_argument("--umesh", required=True)
+    it.add_argument("--smesh", required=True)
+    it.add_argument("--plan", required=True)
+    it.add_argument("--backend", default="cuda")
+    it.add_argument("--mode", default="cull", choices=["cull", "brute"])
+    it.add_argument("--device", type=int, default=0)
+    it.add_argument("--out", required=True)
+    it.add_argument("--manifest", default=None, help="optional JSON with per-layer-pair counters")
+    return ap
+
+
+def main(argv=None) -> int:
+    from . import layers
+    from .isect import write_records
+    from .mesh import read_mesh
+
+    try:
+        args = _parser().parse_args(argv)
+    except SystemExit as exc:
+        return 2 if exc.code else 0
+    try:
+        if args.cmd == "layers":
+            u, s = read_mesh(args.umesh), read_mesh(args.smesh)
+            layers.write_plan(args.plan, layers.enumerate_layer_pairs(u, s, args.nmax, args.omega_p))
+            return 0
+        u, s = read_mesh(args.umesh), read_mesh(args.smesh)
+        plan = layers.read_plan(args.plan)
+        recs, stats = layers.search_plan(u, s, plan, backend=args.backend, mode=args.mode, device=args.device)
+        write_records(args.out, recs)
+        if args.manifest:
+            with open(args.manifest, "w") as fh:
+                json.dump({"records": len(recs), "tasks": stats}, fh, indent=1)
+        return 0
+    except OSError as exc:
+        print(f"error: {exc}", file=sys.stderr)
+        return 4
+    except (ConfigError, FileFormatError, ManiconnError) as exc:
+        print(f"error: {exc}", file=sys.stderr)
+        return getattr(exc, "exit_code", 1)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

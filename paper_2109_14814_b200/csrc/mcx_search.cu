@@ -38,6 +38,7 @@
 #include <stdlib.h>
 
 #include <type_traits>
+#include <vector>
 
 #include "../../include/mcx.h"
 #include "mcx_common.cuh"
@@ -61,7 +62,9 @@ struct Cfg {
 
 enum Kind { KIND_TRI = 0, KIND_QUAD = 1 };
 
-struct SearchParams {
+// Per-task parameters (one entry of the device task table; a single search is a
+// batch of one).  Pointers are device pointers.
+struct __align__(16) SearchParams {
   const Box* boxA;
   const double* geoA;
   const uint32_t* permA;    // storage → original index (NULL = identity)
@@ -71,26 +74,47 @@ struct SearchParams {
   uint64_t nA;
   uint64_t a_begin, a_end;  // A storage range
   uint64_t blk_first;       // first absolute A block of this shard
+  uint64_t my_blocks;       // A blocks of this shard
   uint64_t nB;
-  uint64_t b_chunk;         // B triangles per CTA (multiple of TILE)
-  uint32_t shard_count;
-  mcx_hit* hits;
-  uint64_t cap;
-  unsigned long long* counters;  // [0] emitted, [1] aabb pass, [2] singular / Moller-rejected, [3] tested
+  uint64_t b_chunk, nchunk; // brute: B triangles per CTA (multiple of TILE), chunks
+  uint64_t ntilesB;
+  uint32_t shard_count, task;
+  unsigned long long* counters;  // per task: [0] emitted, [1] aabb pass, [2] singular / Moller-rejected, [3] tested
   // MCX_MODE_CULL
   const Box* gboxA;
   const Box* bboxA;
   const Box* gboxB;
   const Box* tboxB;
-  uint64_t my_blocks, ntilesB;
-  uint2* blk_list;          // overlapping (local A block, B tile) pairs
-  uint64_t blk_cap;
-  // KIND_QUAD only: half-layer grids (4, M, N) for the Moller stage, and gid output
+  // KIND_QUAD only: half-layer grids (4, M, N) for the Moller stage
   const double* coordsA;
   const double* coordsB;
   uint32_t NA, MA, NB, MB;
-  uint64_t* gids;
 };
+
+// Whole-launch parameters: the task table and the shared outputs.
+struct Batch {
+  const SearchParams* tasks;
+  uint32_t n_tasks;
+  const uint64_t* prefix;        // [n_tasks + 1] exclusive prefix of per-task work units
+  mcx_hit* hits;                 // KIND_TRI output (original indices)
+  uint32_t* hit_task;            // task id of each hit (NULL: single task)
+  uint64_t* gids;                // KIND_QUAD output
+  uint64_t cap;
+  unsigned long long* emit;      // shared output position counter
+  uint4* blk_list;               // cull: overlapping (task, local A block, B tile)
+  uint64_t blk_cap;
+  unsigned long long* list_count;
+};
+
+// Task owning work unit u: the last t with prefix[t] <= u (n_tasks is small).
+__device__ __forceinline__ uint32_t find_task(const Batch& Bt, uint64_t u) {
+  uint32_t lo = 0, hi = Bt.n_tasks - 1;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi + 1) >> 1;
+    if (__ldg(Bt.prefix + mid) <= u) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
 
 template <class C>
 struct __align__(16) SearchSmem {
@@ -117,7 +141,7 @@ __device__ __forceinline__ void empty_box(double lo[4], double hi[4]) {
 // KIND_TRI  — canonical solve, emit (iA, iB, s, t, a, b) hits with original indices;
 // KIND_QUAD — SPEC-literal Moller quick test, emit surviving quad-pair gids.
 template <int KIND>
-__device__ __forceinline__ void flush_queue(const SearchParams& P, const uint2* q, int n, int lane,
+__device__ __forceinline__ void flush_queue(const SearchParams& P, const Batch& Bt, const uint2* q, int n, int lane,
                                             unsigned long long& n_pass, unsigned long long& n_sing) {
   const bool valid = lane < n;
   uint2 e = valid ? q[lane] : make_uint2(0, 0);
@@ -136,22 +160,26 @@ __device__ __forceinline__ void flush_queue(const SearchParams& P, const uint2* 
   if (hm) {
     const int leader = __ffs(hm) - 1;
     unsigned long long base = 0;
-    if (lane == leader) base = atomicAdd(P.counters + 0, (unsigned long long)__popc(hm));
+    if (lane == leader) {
+      base = atomicAdd(Bt.emit, (unsigned long long)__popc(hm));
+      atomicAdd(P.counters + 0, (unsigned long long)__popc(hm));
+    }
     base = __shfl_sync(0xffffffffu, base, leader);
     if (hit) {
       const unsigned long long pos = base + __popc(hm & ((1u << lane) - 1u));
-      if (pos < P.cap) {
+      if (pos < Bt.cap) {
         if (KIND == KIND_TRI) {
           mcx_hit h;
           h.ia = P.permA ? __ldg(P.permA + e.x) : e.x;
           h.ib = P.permB ? __ldg(P.permB + e.y) : e.y;
           h.s = sol[0]; h.t = sol[1]; h.a = sol[2]; h.b = sol[3];
-          P.hits[pos] = h;
+          Bt.hits[pos] = h;
+          if (Bt.hit_task) Bt.hit_task[pos] = P.task;
         } else {
           // quad indices qa = i + N1·k1, qb = j + N2·l1 → gid (PAPER.md kernel step 2)
           const uint64_t i = e.x % P.NA, k1 = e.x / P.NA, j = e.y % P.NB, l1 = e.y / P.NB;
           const uint64_t n12 = (uint64_t)P.NA * P.NB;
-          P.gids[pos] = i + (uint64_t)P.NA * j + n12 * k1 + n12 * (uint64_t)(P.MA - 1) * l1;
+          Bt.gids[pos] = i + (uint64_t)P.NA * j + n12 * k1 + n12 * (uint64_t)(P.MA - 1) * l1;
         }
       }
     }
@@ -175,16 +203,28 @@ __device__ __forceinline__ void flush_counters(const SearchParams& P, int lane, 
 
 // ------------------------------------------------------------ brute kernel
 template <int KIND, class C>
-__global__ void __launch_bounds__(C::THREADS, C::MINB) search_brute_kernel(const SearchParams P) {
+__global__ void __launch_bounds__(C::THREADS, C::MINB) search_brute_kernel(const Batch Bt) {
   constexpr int R = C::R, THREADS = C::THREADS;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   SearchSmem<C>& S = *reinterpret_cast<SearchSmem<C>*>(smem_raw);
+  __shared__ SearchParams Ps;
+  __shared__ uint64_t s_unit;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
+  // ---- task of this CTA (1-D grid over all tasks' (A block, B chunk) units)
+  if (tid == 0) {
+    const uint32_t t = find_task(Bt, blockIdx.x);
+    Ps = Bt.tasks[t];
+    s_unit = blockIdx.x - Bt.prefix[t];
+  }
+  __syncthreads();
+  const SearchParams& P = Ps;
+  const uint64_t unit = s_unit;
+
   // ---- absolute A block (cyclic shard) and B chunk of this CTA
-  const uint64_t gblk = P.blk_first + (uint64_t)blockIdx.x * P.shard_count;
+  const uint64_t gblk = P.blk_first + (unit / P.nchunk) * P.shard_count;
   const uint64_t a0 = gblk * A_BLOCK;
-  const uint64_t b0 = (uint64_t)blockIdx.y * P.b_chunk;
+  const uint64_t b0 = (unit % P.nchunk) * P.b_chunk;
   const uint64_t b1 = min(b0 + P.b_chunk, P.nB);
   const int ntiles = (int)((b1 - b0 + TILE - 1) / TILE);
 
@@ -269,7 +309,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_brute_kernel(const
         if (qn >= 32) {
           do {
             qn -= 32;
-            flush_queue<KIND>(P, q + qn, 32, lane, n_pass, n_sing);
+            flush_queue<KIND>(P, Bt, q + qn, 32, lane, n_pass, n_sing);
           } while (qn >= 32);
           load_a();
         }
@@ -304,7 +344,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_brute_kernel(const
           if (qn >= 32) {
             do {
               qn -= 32;
-              flush_queue<KIND>(P, q + qn, 32, lane, n_pass, n_sing);
+              flush_queue<KIND>(P, Bt, q + qn, 32, lane, n_pass, n_sing);
             } while (qn >= 32);
             load_a();
           }
@@ -325,22 +365,27 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_brute_kernel(const
     }
   }
   __syncwarp();
-  if (qn > 0) flush_queue<KIND>(P, q, qn, lane, n_pass, n_sing);
+  if (qn > 0) flush_queue<KIND>(P, Bt, q, qn, lane, n_pass, n_sing);
   flush_counters(P, lane, n_pass, n_sing, 0);
 }
 
 // ------------------------------------------------------------ cull kernels
-// Level 1: (local A block x, B tile y) union-box test, compacted with one atomic per warp.
-__global__ void __launch_bounds__(256) cull_blocks_kernel(const SearchParams P) {
-  const uint64_t total = P.my_blocks * P.ntilesB;
+// Level 1: (task, local A block x, B tile y) union-box tests over the flattened
+// unit space of all tasks, compacted with one atomic per warp.
+__global__ void __launch_bounds__(256) cull_blocks_kernel(const Batch Bt) {
+  const uint64_t total = Bt.prefix[Bt.n_tasks];
   const int lane = threadIdx.x & 31;
   for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < total; base += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t e = base + threadIdx.x;
     bool ov = false;
-    uint32_t x = 0, y = 0;
+    uint32_t t = 0, x = 0, y = 0;
     if (e < total) {
-      x = (uint32_t)(e / P.ntilesB);
-      y = (uint32_t)(e % P.ntilesB);
+      t = find_task(Bt, e);
+      const SearchParams& P = Bt.tasks[t];
+      const uint64_t u = e - __ldg(Bt.prefix + t);
+      const uint64_t ntiles = P.ntilesB;
+      x = (uint32_t)(u / ntiles);
+      y = (uint32_t)(u % ntiles);
       const uint64_t gblk = P.blk_first + (uint64_t)x * P.shard_count;
       ov = box_overlap(P.bboxA[gblk], P.tboxB[y]);
     }
@@ -348,9 +393,9 @@ __global__ void __launch_bounds__(256) cull_blocks_kernel(const SearchParams P) 
     if (m) {
       const int leader = __ffs(m) - 1;
       unsigned long long pos = 0;
-      if (lane == leader) pos = atomicAdd(P.counters + 4, (unsigned long long)__popc(m));
+      if (lane == leader) pos = atomicAdd(Bt.list_count, (unsigned long long)__popc(m));
       pos = __shfl_sync(0xffffffffu, pos, leader) + __popc(m & ((1u << lane) - 1u));
-      if (ov && pos < P.blk_cap) P.blk_list[pos] = make_uint2(x, y);
+      if (ov && pos < Bt.blk_cap) Bt.blk_list[pos] = make_uint4(t, x, y, 0);
     }
   }
 }
@@ -360,29 +405,46 @@ constexpr int CULL_WARPS = CULL_THREADS / 32;
 constexpr int GPAIRS = (A_BLOCK / GROUP) * (TILE / GROUP);  // 32 × 16 group pairs per block pair
 
 struct CullSmem {
+  SearchParams P;
   uint2 queue[CULL_WARPS][64];
   uint16_t gpair[GPAIRS];
   unsigned int n_gpair;
 };
 
-// Level 2 + pair tests: one CTA per overlapping (A block, B tile), persistent.
-__global__ void __launch_bounds__(CULL_THREADS) cull_pairs_kernel(const SearchParams P) {
+// Level 2 + pair tests: one CTA per overlapping (task, A block, B tile), persistent.
+__global__ void __launch_bounds__(CULL_THREADS) cull_pairs_kernel(const Batch Bt) {
   __shared__ CullSmem S;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
   unsigned long long n_pass = 0, n_sing = 0, n_tested = 0;
   uint2* q = S.queue[warp];
   int qn = 0;
-  const uint64_t nlist = min((uint64_t)*(volatile unsigned long long*)(P.counters + 4), P.blk_cap);
-  const uint64_t ngA = (P.nA + GROUP - 1) / GROUP, ngB = (P.nB + GROUP - 1) / GROUP;
+  uint32_t cur_task = 0xffffffffu;
+  const uint64_t nlist = min((uint64_t)*(volatile unsigned long long*)Bt.list_count, Bt.blk_cap);
   for (uint64_t e = blockIdx.x; e < nlist; e += gridDim.x) {
-    const uint2 xy = P.blk_list[e];
-    const uint64_t gblk = P.blk_first + (uint64_t)xy.x * P.shard_count;
+    const uint4 txy = Bt.blk_list[e];
+    if (txy.x != cur_task) {
+      // task switch: drain this warp's queue and counters against the old task first
+      if (cur_task != 0xffffffffu) {
+        __syncwarp();
+        if (qn > 0) flush_queue<KIND_TRI>(S.P, Bt, q, qn, lane, n_pass, n_sing);
+        qn = 0;
+        flush_counters(S.P, lane, n_pass, n_sing, n_tested);
+        n_pass = n_sing = n_tested = 0;
+      }
+      __syncthreads();
+      if (tid == 0) S.P = Bt.tasks[txy.x];
+      cur_task = txy.x;
+      __syncthreads();
+    }
+    const SearchParams& P = S.P;
+    const uint64_t gblk = P.blk_first + (uint64_t)txy.y * P.shard_count;
     if (tid == 0) S.n_gpair = 0;
     __syncthreads();
+    const uint64_t ngA = (P.nA + GROUP - 1) / GROUP, ngB = (P.nB + GROUP - 1) / GROUP;
     for (int k = tid; k < GPAIRS; k += CULL_THREADS) {
       const uint64_t ga = gblk * (A_BLOCK / GROUP) + k / (TILE / GROUP);
-      const uint64_t gb = (uint64_t)xy.y * (TILE / GROUP) + k % (TILE / GROUP);
+      const uint64_t gb = (uint64_t)txy.z * (TILE / GROUP) + k % (TILE / GROUP);
       if (ga < ngA && gb < ngB && box_overlap(P.gboxA[ga], P.gboxB[gb])) S.gpair[atomicAdd(&S.n_gpair, 1u)] = (uint16_t)k;
     }
     __syncthreads();
@@ -390,7 +452,7 @@ __global__ void __launch_bounds__(CULL_THREADS) cull_pairs_kernel(const SearchPa
     for (int w = warp; w < ng; w += CULL_WARPS) {
       const int k = S.gpair[w];
       const uint64_t ia = gblk * A_BLOCK + (uint64_t)(k / (TILE / GROUP)) * GROUP + lane;
-      const uint64_t jb0 = (uint64_t)xy.y * TILE + (uint64_t)(k % (TILE / GROUP)) * GROUP;
+      const uint64_t jb0 = (uint64_t)txy.z * TILE + (uint64_t)(k % (TILE / GROUP)) * GROUP;
       const bool va = ia >= P.a_begin && ia < P.a_end;
       double alo[4], ahi[4];
       if (va) {
@@ -416,43 +478,35 @@ __global__ void __launch_bounds__(CULL_THREADS) cull_pairs_kernel(const SearchPa
           __syncwarp();
           if (qn >= 32) {
             qn -= 32;
-            flush_queue<KIND_TRI>(P, q + qn, 32, lane, n_pass, n_sing);
+            flush_queue<KIND_TRI>(P, Bt, q + qn, 32, lane, n_pass, n_sing);
           }
         }
       }
     }
     __syncthreads();  // gpair list reused by the next entry
   }
-  __syncwarp();
-  if (qn > 0) flush_queue<KIND_TRI>(P, q, qn, lane, n_pass, n_sing);
-  flush_counters(P, lane, n_pass, n_sing, n_tested);
+  if (cur_task != 0xffffffffu) {
+    __syncwarp();
+    if (qn > 0) flush_queue<KIND_TRI>(S.P, Bt, q, qn, lane, n_pass, n_sing);
+    flush_counters(S.P, lane, n_pass, n_sing, n_tested);
+  }
 }
 
 // --------------------------------------------------------------- host side
-// Grid: x = A blocks of this shard, y = B chunks (multiple of TILE), sized for
-// ~16 waves of resident CTAs so the tail wave is a small fraction.
-template <int KIND, class C>
-static int launch_brute_cfg(SearchParams P, uint64_t my_blocks, int device, cudaStream_t stream) {
-  if (my_blocks == 0 || P.nB == 0) return MCX_OK;
-  int dev_sms = 148;
-  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device);
-  const size_t smem = sizeof(SearchSmem<C>);
-  CUDA_TRY(cudaFuncSetAttribute(search_brute_kernel<KIND, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int occ = C::MINB;
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, search_brute_kernel<KIND, C>, C::THREADS, smem));
-  const uint64_t slots = (uint64_t)dev_sms * (occ > 0 ? occ : 1);
-  // B chunk count: every CTA does the same work, so pick the count whose CTA total
-  // best fills whole waves of resident CTAs (the last partial wave idles the rest
-  // of the GPU), among counts giving >= 8 waves with chunks >= 16 tiles.
+// B chunk count for one task: every CTA of a task does the same work, so pick the
+// count whose CTA total best fills whole waves of resident CTAs (the last partial
+// wave idles the rest of the GPU), among counts giving >= 8 waves with chunks of
+// >= 16 tiles (1 tile for small problems).
+static void choose_chunks(SearchParams& P, uint64_t slots) {
   const uint64_t max_chunks = (P.nB + TILE - 1) / TILE;
   uint64_t nchunk = 1, chunk = max_chunks * TILE;
-  const uint64_t min_ch = (my_blocks * max_chunks < 8 * slots) ? (uint64_t)TILE : 16 * (uint64_t)TILE;
+  const uint64_t min_ch = (P.my_blocks * max_chunks < 8 * slots) ? (uint64_t)TILE : 16 * (uint64_t)TILE;
   double best = -1.0;
   for (uint64_t c = 1; c <= max_chunks && c <= 4096; ++c) {
     const uint64_t ch = ((P.nB + c - 1) / c + TILE - 1) / TILE * TILE;
     const uint64_t nc = (P.nB + ch - 1) / ch;
     if (nc != c) continue;
-    const uint64_t total = my_blocks * nc;
+    const uint64_t total = P.my_blocks * nc;
     const bool enough = total >= 8 * slots || nc == max_chunks;
     if (!enough && c < max_chunks && ch > min_ch) continue;
     const double eff = (double)total / (double)(((total + slots - 1) / slots) * slots);
@@ -463,42 +517,77 @@ static int launch_brute_cfg(SearchParams P, uint64_t my_blocks, int device, cuda
     }
     if (best > 0.995 || ch <= min_ch) break;
   }
-  if (my_blocks > 0x7fffffffull || nchunk > 65535) return set_error(MCX_E_ARG, "grid too large");
+  P.nchunk = nchunk;
   P.b_chunk = chunk;
-  dim3 grid((unsigned)my_blocks, (unsigned)nchunk);
-  search_brute_kernel<KIND, C><<<grid, C::THREADS, smem, stream>>>(P);
+}
+
+template <int KIND, class C>
+static int launch_brute_cfg(std::vector<SearchParams>& T, Batch Bt, std::vector<uint64_t>& prefix, void* dev_tab,
+                            int device, cudaStream_t stream) {
+  int dev_sms = 148;
+  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device);
+  const size_t smem = sizeof(SearchSmem<C>);
+  CUDA_TRY(cudaFuncSetAttribute(search_brute_kernel<KIND, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = C::MINB;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, search_brute_kernel<KIND, C>, C::THREADS, smem));
+  const uint64_t slots = (uint64_t)dev_sms * (occ > 0 ? occ : 1);
+  prefix.assign(T.size() + 1, 0);
+  for (size_t t = 0; t < T.size(); ++t) {
+    if (T[t].my_blocks && T[t].nB) choose_chunks(T[t], slots); else T[t].nchunk = 0;
+    prefix[t + 1] = prefix[t] + T[t].my_blocks * T[t].nchunk;
+  }
+  const uint64_t total = prefix.back();
+  if (total == 0) return MCX_OK;
+  if (total > 0x7fffffffull) return set_error(MCX_E_ARG, "grid too large");
+  const size_t tab = sizeof(SearchParams) * T.size();
+  CUDA_TRY(cudaMemcpyAsync(dev_tab, T.data(), tab, cudaMemcpyHostToDevice, stream));
+  CUDA_TRY(cudaMemcpyAsync((char*)dev_tab + tab, prefix.data(), sizeof(uint64_t) * prefix.size(),
+                           cudaMemcpyHostToDevice, stream));
+  Bt.tasks = reinterpret_cast<const SearchParams*>(dev_tab);
+  Bt.prefix = reinterpret_cast<const uint64_t*>((char*)dev_tab + tab);
+  search_brute_kernel<KIND, C><<<(unsigned)total, C::THREADS, smem, stream>>>(Bt);
   CUDA_TRY(cudaGetLastError());
   return MCX_OK;
 }
 
 // Variant selection (MCX_VARIANT=0..3, for experiments; 0 = the tuned default:
-// R = 4, 256 threads, 2 CTAs/SM, one B triangle per vote, next B box prefetched
-// from shared memory before the current one's compares, unroll 4 — no spills).
+// R = 4, 256 threads, 2 CTAs/SM, next B box prefetched from shared memory before
+// the current one's compares, unroll 4 — no spills).
 static int variant_from_env() {
   const char* v = getenv("MCX_VARIANT");
   return v ? atoi(v) : 0;
 }
 
 template <int KIND>
-static int launch_brute(const SearchParams& P, uint64_t my_blocks, int device, cudaStream_t stream) {
+static int launch_brute(std::vector<SearchParams>& T, const Batch& Bt, std::vector<uint64_t>& prefix, void* dev_tab,
+                        int device, cudaStream_t stream) {
   switch (variant_from_env()) {
-    case 1: return launch_brute_cfg<KIND, Cfg<4, 2, 1, 2, 0>>(P, my_blocks, device, stream);
-    case 2: return launch_brute_cfg<KIND, Cfg<4, 2, 1, 8, 1>>(P, my_blocks, device, stream);
-    case 3: return launch_brute_cfg<KIND, Cfg<4, 2, 1, 2, 1>>(P, my_blocks, device, stream);
-    default: return launch_brute_cfg<KIND, Cfg<4, 2, 1, 4, 1>>(P, my_blocks, device, stream);
+    case 1: return launch_brute_cfg<KIND, Cfg<4, 2, 1, 2, 0>>(T, Bt, prefix, dev_tab, device, stream);
+    case 2: return launch_brute_cfg<KIND, Cfg<4, 2, 1, 8, 1>>(T, Bt, prefix, dev_tab, device, stream);
+    case 3: return launch_brute_cfg<KIND, Cfg<4, 2, 1, 2, 1>>(T, Bt, prefix, dev_tab, device, stream);
+    default: return launch_brute_cfg<KIND, Cfg<4, 2, 1, 4, 1>>(T, Bt, prefix, dev_tab, device, stream);
   }
 }
 
-static int launch_cull(SearchParams P, int device, cudaStream_t stream) {
-  if (P.my_blocks == 0 || P.nB == 0) return MCX_OK;
+static int launch_cull(std::vector<SearchParams>& T, Batch Bt, std::vector<uint64_t>& prefix, void* dev_tab,
+                       int device, cudaStream_t stream) {
+  prefix.assign(T.size() + 1, 0);
+  for (size_t t = 0; t < T.size(); ++t) prefix[t + 1] = prefix[t] + T[t].my_blocks * (T[t].nB ? T[t].ntilesB : 0);
+  const uint64_t total = prefix.back();
+  if (total == 0) return MCX_OK;
+  const size_t tab = sizeof(SearchParams) * T.size();
+  CUDA_TRY(cudaMemcpyAsync(dev_tab, T.data(), tab, cudaMemcpyHostToDevice, stream));
+  CUDA_TRY(cudaMemcpyAsync((char*)dev_tab + tab, prefix.data(), sizeof(uint64_t) * prefix.size(),
+                           cudaMemcpyHostToDevice, stream));
+  Bt.tasks = reinterpret_cast<const SearchParams*>(dev_tab);
+  Bt.prefix = reinterpret_cast<const uint64_t*>((char*)dev_tab + tab);
   int dev_sms = 148;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device);
-  const uint64_t total = P.my_blocks * P.ntilesB;
   uint64_t g1 = (total + 255) / 256;
   if (g1 > (uint64_t)dev_sms * 16) g1 = (uint64_t)dev_sms * 16;
-  cull_blocks_kernel<<<(unsigned)g1, 256, 0, stream>>>(P);
+  cull_blocks_kernel<<<(unsigned)g1, 256, 0, stream>>>(Bt);
   CUDA_TRY(cudaGetLastError());
-  cull_pairs_kernel<<<(unsigned)(dev_sms * 8), CULL_THREADS, 0, stream>>>(P);
+  cull_pairs_kernel<<<(unsigned)(dev_sms * 8), CULL_THREADS, 0, stream>>>(Bt);
   CUDA_TRY(cudaGetLastError());
   return MCX_OK;
 }
@@ -532,96 +621,128 @@ static ShardGeom shard_geom(uint64_t a_begin, uint64_t a_end, uint32_t sidx, uin
   return g;
 }
 
-static uint64_t cull_list_cap(const mcx_mesh_dev* A, const mcx_mesh_dev* B, const mcx_opts* o) {
-  const uint64_t a_end = o->a_end ? o->a_end : A->n_tri;
-  const uint32_t scount = o->shard_count ? o->shard_count : 1;
-  const ShardGeom g = shard_geom(o->a_begin, a_end, o->shard_index % scount, scount);
-  return g.my_blocks * ((B->n_tri + TILE - 1) / TILE);
+// Workspace layout: [0, 64) shared counters (emit, list count); then 64 B of
+// counters per task; then the task table + prefix; then the cull block list.
+static uint64_t align16(uint64_t v) { return (v + 15) & ~15ull; }
+
+struct WsLayout {
+  uint64_t counters, table, list, total, list_cap;
+};
+
+static WsLayout ws_layout(const mcx_task* tasks, uint32_t n, const mcx_opts* o) {
+  WsLayout L;
+  L.counters = 64;
+  L.table = align16(64 + 64ull * n);
+  L.list = align16(L.table + sizeof(SearchParams) * n + 8ull * (n + 1));
+  L.list_cap = 0;
+  if (o && o->mode == MCX_MODE_CULL) {
+    const uint32_t scount = o->shard_count ? o->shard_count : 1;
+    for (uint32_t t = 0; t < n; ++t) {
+      const mcx_mesh_dev* A = tasks[t].A;
+      const mcx_mesh_dev* B = tasks[t].B;
+      if (!A || !B) continue;
+      const uint64_t a_end = tasks[t].a_end ? tasks[t].a_end : A->n_tri;
+      const ShardGeom g = shard_geom(tasks[t].a_begin, a_end, o->shard_index % scount, scount);
+      L.list_cap += g.my_blocks * ((B->n_tri + TILE - 1) / TILE);
+    }
+  }
+  L.total = L.list + 16 * L.list_cap;
+  return L;
 }
 
-static int launch_search(const mcx_mesh_dev* A, const mcx_mesh_dev* B, const mcx_opts* o, mcx_hit* hits,
-                         uint64_t cap, mcx_stats* st) {
+static int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mcx_hit* hits, uint32_t* hit_task,
+                        uint64_t cap, mcx_stats* st) {
+  if (!tasks || n == 0 || !o || !st) return set_error(MCX_E_ARG, "null argument or empty batch");
   cudaStream_t stream = (cudaStream_t)o->stream;
-  const uint64_t a_begin = o->a_begin;
-  const uint64_t a_end = o->a_end ? o->a_end : A->n_tri;
   const uint32_t scount = o->shard_count ? o->shard_count : 1;
   const uint32_t sidx = o->shard_index;
-  if (a_end > A->n_tri || a_begin > a_end)
-    return set_error(MCX_E_ARG, "A range [%llu, %llu) outside [0, %llu)", (unsigned long long)a_begin,
-                     (unsigned long long)a_end, (unsigned long long)A->n_tri);
   if (sidx >= scount) return set_error(MCX_E_ARG, "shard_index %u >= shard_count %u", sidx, scount);
-  if (A->n_tri >= (1ull << 32) || B->n_tri >= (1ull << 32))
-    return set_error(MCX_E_ARG, "triangle counts must be < 2^32");
   if (o->mode != MCX_MODE_BRUTE && o->mode != MCX_MODE_CULL) return set_error(MCX_E_ARG, "unknown mode %d", o->mode);
-  if (o->mode == MCX_MODE_CULL && (!A->gbox || !A->bbox || !B->gbox || !B->tbox))
-    return set_error(MCX_E_ARG, "MCX_MODE_CULL needs level boxes (mcx_levels) on both meshes");
-  if (!A->box || !B->box || !A->geo || !B->geo) return set_error(MCX_E_ARG, "null box/geo");
-  if (!o->workspace || o->workspace_bytes < mcx_workspace_bytes(A, B, o))
-    return set_error(MCX_E_ARG, "workspace too small (need %llu bytes)",
-                     (unsigned long long)mcx_workspace_bytes(A, B, o));
-  if (((uintptr_t)A->box | (uintptr_t)B->box | (uintptr_t)A->geo | (uintptr_t)B->geo) & 15)
-    return set_error(MCX_E_ARG, "box/geo pointers must be 16-byte aligned");
   if (cap > 0 && !hits) return set_error(MCX_E_ARG, "null hit buffer with nonzero capacity");
-
-  unsigned long long* counters = (unsigned long long*)o->workspace;
-  CUDA_TRY(cudaMemsetAsync(counters, 0, 8 * sizeof(unsigned long long), stream));
-
-  const ShardGeom g = shard_geom(a_begin, a_end, sidx, scount);
-  const uint64_t nB = B->n_tri;
-  st->n_pairs = g.na * nB;
-
+  const WsLayout L = ws_layout(tasks, n, o);
+  if (!o->workspace || o->workspace_bytes < L.total || ((uintptr_t)o->workspace & 15))
+    return set_error(MCX_E_ARG, "workspace too small or misaligned (need %llu bytes, 16-byte aligned)",
+                     (unsigned long long)L.total);
+  char* ws = (char*)o->workspace;
+  std::vector<SearchParams> T(n);
+  for (uint32_t t = 0; t < n; ++t) {
+    const mcx_mesh_dev* A = tasks[t].A;
+    const mcx_mesh_dev* B = tasks[t].B;
+    if (!A || !B) return set_error(MCX_E_ARG, "task %u: null mesh", t);
+    const uint64_t a_begin = tasks[t].a_begin;
+    const uint64_t a_end = tasks[t].a_end ? tasks[t].a_end : A->n_tri;
+    if (a_end > A->n_tri || a_begin > a_end)
+      return set_error(MCX_E_ARG, "task %u: A range [%llu, %llu) outside [0, %llu)", t, (unsigned long long)a_begin,
+                       (unsigned long long)a_end, (unsigned long long)A->n_tri);
+    if (A->n_tri >= (1ull << 32) || B->n_tri >= (1ull << 32))
+      return set_error(MCX_E_ARG, "task %u: triangle counts must be < 2^32", t);
+    if (!A->box || !B->box || !A->geo || !B->geo) return set_error(MCX_E_ARG, "task %u: null box/geo", t);
+    if (((uintptr_t)A->box | (uintptr_t)B->box | (uintptr_t)A->geo | (uintptr_t)B->geo) & 15)
+      return set_error(MCX_E_ARG, "task %u: box/geo pointers must be 16-byte aligned", t);
+    if (o->mode == MCX_MODE_CULL && (!A->gbox || !A->bbox || !B->gbox || !B->tbox))
+      return set_error(MCX_E_ARG, "task %u: MCX_MODE_CULL needs level boxes (mcx_levels) on both meshes", t);
+    const ShardGeom g = shard_geom(a_begin, a_end, sidx, scount);
+    SearchParams& P = T[t];
+    P = SearchParams{};
+    P.boxA = reinterpret_cast<const Box*>(A->box);
+    P.geoA = A->geo;
+    P.permA = A->perm;
+    P.boxB = reinterpret_cast<const Box*>(B->box);
+    P.geoB = B->geo;
+    P.permB = B->perm;
+    P.nA = A->n_tri;
+    P.a_begin = a_begin;
+    P.a_end = a_end;
+    P.blk_first = g.first;
+    P.my_blocks = g.my_blocks;
+    P.nB = B->n_tri;
+    P.ntilesB = (B->n_tri + TILE - 1) / TILE;
+    P.shard_count = scount;
+    P.task = t;
+    P.counters = reinterpret_cast<unsigned long long*>(ws + L.counters + 64ull * t);
+    P.gboxA = reinterpret_cast<const Box*>(A->gbox);
+    P.bboxA = reinterpret_cast<const Box*>(A->bbox);
+    P.gboxB = reinterpret_cast<const Box*>(B->gbox);
+    P.tboxB = reinterpret_cast<const Box*>(B->tbox);
+    st[t] = mcx_stats{};
+    st[t].n_pairs = g.na * B->n_tri;
+  }
+  CUDA_TRY(cudaMemsetAsync(ws, 0, L.counters + 64ull * n, stream));
+  Batch Bt = {};
+  Bt.n_tasks = n;
+  Bt.hits = hits;
+  Bt.hit_task = hit_task;
+  Bt.cap = cap;
+  Bt.emit = reinterpret_cast<unsigned long long*>(ws);
+  Bt.list_count = reinterpret_cast<unsigned long long*>(ws) + 1;
+  Bt.blk_list = reinterpret_cast<uint4*>(ws + L.list);
+  Bt.blk_cap = L.list_cap;
   Timing tm;
   if (o->timing) {
     CUDA_TRY(cudaEventCreate(&tm.e0));
     CUDA_TRY(cudaEventCreate(&tm.e1));
     CUDA_TRY(cudaEventRecord(tm.e0, stream));
   }
-  SearchParams P = {};
-  P.boxA = reinterpret_cast<const Box*>(A->box);
-  P.geoA = A->geo;
-  P.permA = A->perm;
-  P.boxB = reinterpret_cast<const Box*>(B->box);
-  P.geoB = B->geo;
-  P.permB = B->perm;
-  P.nA = A->n_tri;
-  P.a_begin = a_begin;
-  P.a_end = a_end;
-  P.blk_first = g.first;
-  P.nB = nB;
-  P.shard_count = scount;
-  P.hits = hits;
-  P.cap = cap;
-  P.counters = counters;
-  int rc;
-  if (o->mode == MCX_MODE_BRUTE) {
-    rc = launch_brute<KIND_TRI>(P, g.my_blocks, o->device, stream);
-  } else {
-    P.gboxA = reinterpret_cast<const Box*>(A->gbox);
-    P.bboxA = reinterpret_cast<const Box*>(A->bbox);
-    P.gboxB = reinterpret_cast<const Box*>(B->gbox);
-    P.tboxB = reinterpret_cast<const Box*>(B->tbox);
-    P.my_blocks = g.my_blocks;
-    P.ntilesB = (nB + TILE - 1) / TILE;
-    P.blk_list = reinterpret_cast<uint2*>((char*)o->workspace + 256);
-    P.blk_cap = cull_list_cap(A, B, o);
-    rc = launch_cull(P, o->device, stream);
-  }
+  std::vector<uint64_t> prefix;
+  const int rc = o->mode == MCX_MODE_BRUTE ? launch_brute<KIND_TRI>(T, Bt, prefix, ws + L.table, o->device, stream)
+                                           : launch_cull(T, Bt, prefix, ws + L.table, o->device, stream);
   if (rc != MCX_OK) return rc;
   if (o->timing) CUDA_TRY(cudaEventRecord(tm.e1, stream));
-  unsigned long long h[8];
-  CUDA_TRY(cudaMemcpyAsync(h, counters, sizeof(h), cudaMemcpyDeviceToHost, stream));
-  CUDA_TRY(cudaStreamSynchronize(stream));
-  st->n_hits = h[0];
-  st->n_aabb_pass = h[1];
-  st->n_singular = h[2];
-  st->n_tested = o->mode == MCX_MODE_BRUTE ? st->n_pairs : h[3];
-  st->kernel_ms = 0.0;
-  if (o->timing) {
-    float ms = 0.f;
-    CUDA_TRY(cudaEventElapsedTime(&ms, tm.e0, tm.e1));
-    st->kernel_ms = ms;
+  std::vector<unsigned long long> h(8 + 8ull * n);
+  CUDA_TRY(cudaMemcpyAsync(h.data(), ws, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, stream));
+  CUDA_TRY(cudaStreamSynchronize(stream));  // also keeps T / prefix alive until the copies are done
+  float ms = 0.f;
+  if (o->timing) CUDA_TRY(cudaEventElapsedTime(&ms, tm.e0, tm.e1));
+  for (uint32_t t = 0; t < n; ++t) {
+    const unsigned long long* c = h.data() + 8 + 8ull * t;
+    st[t].n_hits = c[0];
+    st[t].n_aabb_pass = c[1];
+    st[t].n_singular = c[2];
+    st[t].n_tested = o->mode == MCX_MODE_BRUTE ? st[t].n_pairs : c[3];
+    st[t].kernel_ms = ms;
   }
-  if (h[0] > cap) return set_error(MCX_E_CAPACITY, "hit capacity %llu < %llu hits", (unsigned long long)cap, h[0]);
+  if (h[0] > cap)
+    return set_error(MCX_E_CAPACITY, "hit capacity %llu < %llu hits", (unsigned long long)cap, h[0]);
   return MCX_OK;
 }
 
@@ -644,20 +765,24 @@ __global__ void quad_box_kernel(const double* __restrict__ coords, uint32_t N, u
   }
 }
 
+// pair_candidates workspace header: counters (128 B) + one task table entry + prefix.
+constexpr uint64_t PC_HEADER = 1024;
+static_assert(256 + sizeof(SearchParams) + 16 <= PC_HEADER, "pair_candidates header too small");
+
 static int launch_pair_candidates(const double* cA, uint32_t NA, uint32_t MA, const double* cB, uint32_t NB,
                                   uint32_t MB, int device, cudaStream_t stream, void* ws, uint64_t ws_bytes,
                                   uint64_t* gids, uint64_t cap, uint64_t* n_out) {
   if (NA < 1 || NB < 1 || MA < 2 || MB < 2) return set_error(MCX_E_ARG, "half-layers need >= 2 columns");
   const uint64_t nqA = (uint64_t)NA * (MA - 1), nqB = (uint64_t)NB * (MB - 1);
   if (nqA >= (1ull << 32) || nqB >= (1ull << 32)) return set_error(MCX_E_ARG, "quad counts must be < 2^32");
-  const uint64_t need = 256 + (nqA + nqB) * sizeof(Box);
-  if (!ws || ws_bytes < need)
-    return set_error(MCX_E_ARG, "workspace too small (need %llu bytes)", (unsigned long long)need);
+  const uint64_t need = PC_HEADER + (nqA + nqB) * sizeof(Box);
+  if (!ws || ws_bytes < need || ((uintptr_t)ws & 15))
+    return set_error(MCX_E_ARG, "workspace too small or misaligned (need %llu bytes)", (unsigned long long)need);
   if (cap > 0 && !gids) return set_error(MCX_E_ARG, "null gid buffer with nonzero capacity");
   unsigned long long* counters = (unsigned long long*)ws;
-  Box* boxA = reinterpret_cast<Box*>((char*)ws + 256);
+  Box* boxA = reinterpret_cast<Box*>((char*)ws + PC_HEADER);
   Box* boxB = boxA + nqA;
-  CUDA_TRY(cudaMemsetAsync(counters, 0, 8 * sizeof(unsigned long long), stream));
+  CUDA_TRY(cudaMemsetAsync(counters, 0, 16 * sizeof(unsigned long long), stream));
   quad_box_kernel<<<(unsigned)min((nqA + 255) / 256, (uint64_t)148 * 64), 256, 0, stream>>>(cA, NA, MA, boxA);
   quad_box_kernel<<<(unsigned)min((nqB + 255) / 256, (uint64_t)148 * 64), 256, 0, stream>>>(cB, NB, MB, boxB);
   CUDA_TRY(cudaGetLastError());
@@ -668,15 +793,22 @@ static int launch_pair_candidates(const double* cA, uint32_t NA, uint32_t MA, co
   P.a_begin = 0;
   P.a_end = nqA;
   P.blk_first = 0;
+  P.my_blocks = (nqA + A_BLOCK - 1) / A_BLOCK;
   P.nB = nqB;
+  P.ntilesB = (nqB + TILE - 1) / TILE;
   P.shard_count = 1;
-  P.cap = cap;
-  P.counters = counters;
+  P.counters = counters + 8;
   P.coordsA = cA;
   P.coordsB = cB;
   P.NA = NA; P.MA = MA; P.NB = NB; P.MB = MB;
-  P.gids = gids;
-  int rc = launch_brute<KIND_QUAD>(P, (nqA + A_BLOCK - 1) / A_BLOCK, device, stream);
+  Batch Bt = {};
+  Bt.n_tasks = 1;
+  Bt.gids = gids;
+  Bt.cap = cap;
+  Bt.emit = counters;
+  std::vector<SearchParams> T(1, P);
+  std::vector<uint64_t> prefix;
+  int rc = launch_brute<KIND_QUAD>(T, Bt, prefix, (char*)ws + 256, device, stream);
   if (rc != MCX_OK) return rc;
   unsigned long long h[8];
   CUDA_TRY(cudaMemcpyAsync(h, counters, sizeof(h), cudaMemcpyDeviceToHost, stream));
@@ -695,8 +827,13 @@ extern "C" {
 uint32_t mcx_a_block(void) { return mcx::A_BLOCK; }
 
 uint64_t mcx_workspace_bytes(const mcx_mesh_dev* A, const mcx_mesh_dev* B, const mcx_opts* o) {
-  if (!A || !B || !o || o->mode != MCX_MODE_CULL) return 256;
-  return 256 + 8 * mcx::cull_list_cap(A, B, o);
+  mcx_task t = {A, B, o ? o->a_begin : 0, o ? o->a_end : 0};
+  return mcx::ws_layout(&t, 1, o).total;
+}
+
+uint64_t mcx_batch_workspace_bytes(const mcx_task* tasks, uint32_t n_tasks, const mcx_opts* o) {
+  if (!tasks) return 0;
+  return mcx::ws_layout(tasks, n_tasks, o).total;
 }
 
 int mcx_search(const mcx_mesh_dev* A, const mcx_mesh_dev* B, const mcx_opts* o, mcx_hit* hits, uint64_t cap,
@@ -704,7 +841,16 @@ int mcx_search(const mcx_mesh_dev* A, const mcx_mesh_dev* B, const mcx_opts* o, 
   using namespace mcx;
   if (!A || !B || !o || !st) return set_error(MCX_E_ARG, "null argument");
   CUDA_TRY(cudaSetDevice(o->device));
-  return launch_search(A, B, o, hits, cap, st);
+  mcx_task t = {A, B, o->a_begin, o->a_end};
+  return launch_batch(&t, 1, o, hits, nullptr, cap, st);
+}
+
+int mcx_search_batch(const mcx_task* tasks, uint32_t n_tasks, const mcx_opts* o, mcx_hit* hits, uint32_t* hit_task,
+                     uint64_t cap, mcx_stats* stats) {
+  using namespace mcx;
+  if (!o) return set_error(MCX_E_ARG, "null options");
+  CUDA_TRY(cudaSetDevice(o->device));
+  return launch_batch(tasks, n_tasks, o, hits, hit_task, cap, stats);
 }
 
 int mcx_pair_candidates(const double* coords_a, uint32_t NA, uint32_t MA, const double* coords_b, uint32_t NB,

@@ -151,6 +151,12 @@ class _Workspace:
             self.ws = t.empty(nbytes, dtype=t.uint8, device=t.device("cuda", self.device))
         return self.ws
 
+    def task_buffer(self, cap: int):
+        t = torch()
+        if getattr(self, "tasks", None) is None or self.tasks.numel() < cap:
+            self.tasks = t.empty(max(cap, 1), dtype=t.int32, device=t.device("cuda", self.device))
+        return self.tasks
+
 
 def search_device(A: DeviceMesh, B: DeviceMesh, *, mode: int = _lib.MODE_BRUTE, a_range=None,
                   shard=(0, 1), cap: int = 1 << 16, timing: bool = False, stream=None, task=None,
@@ -187,6 +193,63 @@ def search_device(A: DeviceMesh, B: DeviceMesh, *, mode: int = _lib.MODE_BRUTE, 
     if sort and n:
         hits = hits[np.lexsort((hits["ib"], hits["ia"]))]
     return SearchResult(hits=hits, stats=st.as_dict())
+
+
+def search_batch(pairs, *, mode: int = _lib.MODE_BRUTE, shard=(0, 1), cap: int = 1 << 16, timing: bool = False,
+                 stream=None, task_ids=None):
+    """Many (A, B) DeviceMesh searches in one launch per kernel (mcx_search_batch).
+
+    ``pairs``: list of (A, B) or (A, B, (a_begin, a_end)).  Returns one
+    SearchResult per task, hits sorted by (ia, ib).
+    """
+    t = torch()
+    if not pairs:
+        return []
+    dev = pairs[0][0].device
+    for p in pairs:
+        if p[0].device != dev or p[1].device != dev:
+            raise ConfigError("all meshes of a batch must live on one device")
+    L = _lib.load()
+    s = stream or t.cuda.current_stream(dev)
+    W = _Workspace.get(dev)
+    n = len(pairs)
+    structs = [(p[0].struct(), p[1].struct()) for p in pairs]  # keep alive for the call
+    tasks = (_lib.Task * n)()
+    for k, (p, (As, Bs)) in enumerate(zip(pairs, structs)):
+        rng = p[2] if len(p) > 2 else (0, 0)
+        tasks[k] = _lib.Task(ctypes_pointer(As), ctypes_pointer(Bs), int(rng[0]), int(rng[1]))
+    opts = _lib.Opts(dev, s.cuda_stream, 0, 0, int(shard[0]), int(shard[1]), int(mode), int(timing), None, 0)
+    need = L.mcx_batch_workspace_bytes(tasks, n, opts)
+    ws = W.workspace(need)
+    opts.workspace = ws.data_ptr()
+    opts.workspace_bytes = ws.numel()
+    stats = (_lib.Stats * n)()
+    for _attempt in range(3):
+        buf = W.hit_buffer(cap)
+        cap_eff = buf.numel() // 5
+        tb = W.task_buffer(cap_eff)
+        rc = L.mcx_search_batch(tasks, n, opts, buf.data_ptr(), tb.data_ptr(), cap_eff, stats)
+        total = sum(int(stats[k].n_hits) for k in range(n))
+        if rc == _lib.MCX_E_CAPACITY:
+            cap = total + 1024
+            continue
+        _lib.check(rc, "mcx_search_batch", task=task_ids)
+        break
+    else:
+        raise CapacityError("hit buffer overflow persisted after regrowing", required=total, task=task_ids)
+    hits = buf[: total * 5].cpu().numpy().view(HIT_DTYPE).copy() if total else np.zeros(0, HIT_DTYPE)
+    owner = tb[:total].cpu().numpy() if total else np.zeros(0, np.int32)
+    out = []
+    for k in range(n):
+        h = hits[owner == k]
+        h = h[np.lexsort((h["ib"], h["ia"]))]
+        out.append(SearchResult(hits=h, stats=stats[k].as_dict()))
+    return out
+
+
+def ctypes_pointer(x):
+    import ctypes
+    return ctypes.pointer(x)
 
 
 def _merge(results) -> SearchResult:
@@ -250,7 +313,7 @@ def pair_candidates_device(coords_a, coords_b, device: int = 0, cap: int = 1 << 
         _, MA, NA = ca.shape
         _, MB, NB = cb.shape
         nq = NA * (MA - 1) + NB * (MB - 1)
-        ws = t.empty(256 + 64 * nq, dtype=t.uint8, device=dev)
+        ws = t.empty(1024 + 64 * nq, dtype=t.uint8, device=dev)  # include/mcx.h: 1024 + 64·quads
         s = t.cuda.current_stream(device)
         n_out = ctypes_u64()
         for _ in range(3):

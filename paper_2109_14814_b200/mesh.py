@@ -204,14 +204,17 @@ def read_mesh(path) -> ManifoldMesh:
 
 
 # ------------------------------------------------------------ synthetic generators
-def manifold_like(N: int, M: int, seed: int):
+def manifold_like(N: int, M: int, seed: int, s_values=None):
     """Smooth annulus-like sheet in 4D, frozen per SURVEY.md §8(d).
 
     Returns ``(coords (4, M, N), s_values (M,))``.  Draws do not depend on (N, M),
-    so one seed samples the same surface at any resolution.
+    so one seed samples the same surface at any resolution.  ``s_values``
+    (optional, length M) evaluates the surface at arbitrary s instead of
+    ``linspace(-1, 1, M)``.
     """
     theta = grid_points(N)
-    s = np.linspace(-1.0, 1.0, M)
+    s = np.linspace(-1.0, 1.0, M) if s_values is None else np.asarray(s_values, dtype=np.float64)
+    M = s.shape[0]
     rng = np.random.default_rng(seed)
     S = s[:, None]
     T = theta[None, :]
@@ -227,6 +230,33 @@ def manifold_like(N: int, M: int, seed: int):
         out[c] = acc
     out += 0.0  # canonicalise -0.0 to +0.0
     return out, s
+
+
+def layered_mesh(N: int, kind: str, n_max: int, lam: float, D: float, seed: int, K: int = 4,
+                 per_layer: int = 4) -> ManifoldMesh:
+    """Synthetic globalized mesh with layer bookkeeping.
+
+    s grid: the fundamental grid kD/K (k = −K..K) plus ``per_layer`` points per
+    layer on each side, with every layer boundary ±D·μ^n (μ = λ unstable, 1/λ
+    stable) a grid member, as globalization guarantees (PAPER.md "Discrete Mesh").
+    Coordinates: the frozen smooth surface of ``manifold_like`` at those s
+    (scaled to [-1, 1]).
+    """
+    mu = lam if kind == "unstable" else 1.0 / lam
+    if mu <= 1.0:
+        raise ConfigError("layers need |multiplier| > 1 in the growing direction")
+    sv = {k * D / K for k in range(-K, K + 1)}
+    for n in range(1, n_max + 1):
+        lo, hi = D * mu ** (n - 1), D * mu ** n
+        for j in range(per_layer + 1):
+            v = lo + (hi - lo) * j / per_layer
+            sv.add(v)
+            sv.add(-v)
+    s = np.array(sorted(sv))
+    coords, _ = manifold_like(N, len(s), seed, s_values=s / s.max())
+    bcols = tuple(int(np.argmin(np.abs(s - sg * D * mu ** n))) for n in range(0, n_max + 1) for sg in (-1, 1))
+    return ManifoldMesh(coords=coords, s_values=s, kind=kind, omega=1.0, lam=lam, D=D, n_max=n_max,
+                        boundary_cols=tuple(sorted(set(bcols))))
 
 
 def dyadic(coords: np.ndarray, bits: int = 8) -> np.ndarray:

@@ -271,3 +271,67 @@ def test_bad_args_fail_loudly():
         D.search_device(Am, Bm, shard=(3, 2))
     with pytest.raises(Exception):
         D.search_device(Am, Bm, a_range=(10, 10 ** 9))
+
+
+# ------------------------------------------------------------ batched tasks (one launch)
+@pytest.mark.parametrize("mode", MODES)
+def test_search_batch_equals_individual(mode):
+    meshes = {}
+    for name in ("C1", "C4i", "C4iii", "C5/8"):
+        A, _, B, _ = config_pair(name)
+        meshes[name] = (D.DeviceMesh(A, 0), D.DeviceMesh(B, 0))
+    pairs = [(*meshes["C1"],), (*meshes["C4i"],), (*meshes["C4iii"],), (*meshes["C5/8"],),
+             (*meshes["C4i"], (1000, 5000)), (meshes["C1"][1], meshes["C4i"][0])]
+    batch = D.search_batch(pairs, mode=mode)
+    for p, r in zip(pairs, batch):
+        single = D.search_device(p[0], p[1], mode=mode, a_range=p[2] if len(p) > 2 else None)
+        assert np.array_equal(r.hits, single.hits)
+        for k in ("n_pairs", "n_aabb_pass", "n_singular", "n_hits"):
+            assert r.stats[k] == single.stats[k], k
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_search_batch_sharded(mode):
+    A, _, B, _ = config_pair("C4i")
+    Am, Bm = D.DeviceMesh(A, 0), D.DeviceMesh(B, 0)
+    full = D.search_batch([(Am, Bm), (Bm, Am)], mode=mode)
+    parts = [D.search_batch([(Am, Bm), (Bm, Am)], mode=mode, shard=(g, 3)) for g in range(3)]
+    for t in range(2):
+        assert np.array_equal(D._merge([p[t] for p in parts]).hits, full[t].hits)
+
+
+@pytest.mark.parametrize("mode", ["cull", "brute"])
+def test_search_plan_matches_oracle(mode):
+    from paper_2109_14814_b200 import layers
+    from paper_2109_14814_b200.mesh import half_layer, layered_mesh
+    u = layered_mesh(96, "unstable", 3, 1.6, 0.1, 1)
+    s = layered_mesh(96, "stable", 3, 1 / 1.6, 0.1, 2)
+    plan = layers.enumerate_layer_pairs(u, s, 3)
+    recs, stats = layers.search_plan(u, s, plan, mode=mode)
+    want = []
+    for (n1, s1, n2, s2), tof in zip(plan.tasks, plan.tof):
+        hu, hs = half_layer(u, n1, 1 if s1 == "+" else -1), half_layer(s, n2, 1 if s2 == "+" else -1)
+        ca, cb = np.ascontiguousarray(hu.coords), np.ascontiguousarray(hs.coords)
+        ref = O.search(ca, cb)
+        h = np.zeros(len(ref["ia"]), dtype=D.HIT_DTYPE)
+        for k in ("ia", "ib", "s", "t", "a", "b"):
+            h[k] = ref[k]
+        want.extend(isect.hits_to_records(ca, hu.s_values, cb, hs.s_values, h, layer=(n1, s1, n2, s2), tof=tof))
+    assert [r.to_line() for r in recs] == [w.to_line() for w in want]
+    assert len(stats) == len(plan) == 20
+
+
+def test_cli_intersect(tmp_path):
+    from paper_2109_14814_b200 import cli, layers
+    from paper_2109_14814_b200.mesh import layered_mesh, write_mesh
+    u = layered_mesh(64, "unstable", 2, 1.6, 0.1, 1)
+    s = layered_mesh(64, "stable", 2, 1 / 1.6, 0.1, 2)
+    write_mesh(tmp_path / "u.mnf", u)
+    write_mesh(tmp_path / "s.mnf", s)
+    assert cli.main(["layers", "--umesh", str(tmp_path / "u.mnf"), "--smesh", str(tmp_path / "s.mnf"),
+                     "--nmax", "2", "--plan", str(tmp_path / "plan.txt")]) == 0
+    assert cli.main(["intersect", "--umesh", str(tmp_path / "u.mnf"), "--smesh", str(tmp_path / "s.mnf"),
+                     "--plan", str(tmp_path / "plan.txt"), "--backend", "cuda", "--out", str(tmp_path / "rec.txt"),
+                     "--manifest", str(tmp_path / "m.json")]) == 0
+    recs, _ = layers.search_plan(u, s, layers.read_plan(tmp_path / "plan.txt"))
+    assert (tmp_path / "rec.txt").read_text().splitlines() == [r.to_line() for r in recs]
