@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU-baseline sample duration")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-paper", action="store_true", help="skip the paper's 14-layer workload block")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo lets several ranks share one GPU (logic test of the N>1 path on a 1-GPU box)")
     return ap.parse_args()
@@ -323,6 +324,45 @@ def run_ours(args):
         e2e = measure_e2e(primary, m1["pairs"])
         e2e["other_mode"] = measure_e2e(other, m1["pairs"])
 
+    # ---- the paper's own benchmark shape: 14-layer search, 108 layer-pair tasks of
+    # N1 = 1024 x N2 = 2048 grids with 35 s-values per half-layer (PAPER.md "Computational
+    # Results": 2,424,307,712 quad pairs / 9,697,230,848 triangle pairs per task), one batch.
+    paper = None
+    if not args.no_paper:
+        from paper_2109_14814_b200.layers import enumerate_layer_pairs
+        from paper_2109_14814_b200.mesh import half_layer, layered_mesh
+        um = layered_mesh(1024, "unstable", 14, 1.6, 0.1, 1, K=17, per_layer=34)
+        sm = layered_mesh(2048, "stable", 14, 1 / 1.6, 0.1, 2, K=17, per_layer=34)
+        plan = enumerate_layer_pairs(um, sm, 14)
+        dm = {}
+
+        def half(mesh, key, n, sg):
+            if key not in dm:
+                dm[key] = D.DeviceMesh(np.ascontiguousarray(half_layer(mesh, n, 1 if sg == "+" else -1).coords), local)
+            return dm[key]
+
+        pairs = [(half(um, ("u", n1, s1), n1, s1), half(sm, ("s", n2, s2), n2, s2)) for n1, s1, n2, s2 in plan.tasks]
+        paper = {"workload": "synthetic layered meshes, U 1024 x S 2048 theta points, 14 layers, 35 s-values per "
+                             "half-layer, all 108 layer-pair tasks in one mcx_search_batch job",
+                 "tasks": len(pairs), "published": {"dgx_v100_full_search_s": 16.0, "laptop_full_search_s": 62.0,
+                                                    "dgx_v100_bbox_kernel_per_task_s": 0.03}}
+        for mname in ("brute", "cull"):
+            for _ in range(max(1, args.warmup)):
+                res = D.search_batch(pairs, mode=modes[mname], shard=shard, stream=stream)
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(args.steps):
+                res = D.search_batch(pairs, mode=modes[mname], shard=shard, stream=stream)
+            e1.record(stream)
+            barrier()
+            ms = reduce(e0.elapsed_time(e1), MAX) / args.steps
+            pairs_total = reduce(sum(r.stats["n_pairs"] for r in res), SUM)
+            paper[mname] = {"full_search_s": ms / 1e3, "pair_tests_per_s": pairs_total / (ms * 1e-3),
+                            "pairs": pairs_total, "executed_pair_tests": reduce(sum(r.stats["n_tested"] for r in res), SUM),
+                            "hits": reduce(sum(len(r.hits) for r in res), SUM),
+                            "speedup_vs_dgx_v100_full_search": 16.0 / (ms / 1e3)}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         s = cpu_reference_sample(A, B, args.cpu_seconds)
@@ -339,7 +379,7 @@ def run_ours(args):
                 "search_wall_s": m1["ms_per_step"] / 1e3, "hits": m1["hits"], "kernel_ms": m1["kernel_ms"],
                 "roofline": roofline, "cull": cull_block if primary == "brute" else None,
                 "brute": None if primary == "brute" else {"value": brute["value"], "ms_per_step": brute["ms_per_step"]},
-                "e2e": e2e, "cpu_baseline": cpu, "clocks": m1["clocks"],
+                "e2e": e2e, "cpu_baseline": cpu, "paper_workload": paper, "clocks": m1["clocks"],
                 "gpu_launches": m1["launches"], "gpu": props.name, "sms": sms}
         print(json.dumps(line), flush=True)
     if world > 1:
