@@ -68,6 +68,8 @@ typedef struct mcx_mesh_dev {
   const double* gbox;     /* device, [⌈n/32⌉][8] group boxes (mcx_levels); MODE_CULL */
   const double* tbox;     /* device, [⌈n/512⌉][8]                                    */
   const double* bbox;     /* device, [⌈n/1024⌉][8]                                   */
+  const uint32_t* status; /* device flag written by mcx_pack (nonzero: non-finite
+                             coordinates); checked by the searches; may be NULL      */
 } mcx_mesh_dev;
 
 /* One intersecting triangle pair: A triangle ia, B triangle ib, and the
@@ -122,9 +124,11 @@ uint64_t mcx_batch_workspace_bytes(const mcx_task* tasks, uint32_t n_tasks, cons
  * coords: device, (4, M, N) float64 = four column-major N×M planes (x, y, px, py)
  * of one half-layer.  Writes box/geo (and perm, if
  * non-NULL) for the 2·N·(M−1) triangles in the given storage order; every record
- * is bit-identical to the CPU oracle's packing of that triangle. */
+ * is bit-identical to the CPU oracle's packing of that triangle.  *status (device,
+ * may be NULL) becomes nonzero if any coordinate is NaN/Inf; searches given that
+ * mesh then fail with MCX_E_ARG (the AABB contract assumes finite inputs). */
 int mcx_pack(const double* coords, uint32_t N, uint32_t M, int order, double* box, double* geo,
-             uint32_t* perm, int device, void* stream);
+             uint32_t* perm, uint32_t* status, int device, void* stream);
 
 /* Exact union boxes over consecutive records: gbox per 32, tbox per 512, bbox per
  * 1024 (needed by MCX_MODE_CULL).  Enqueued on `stream`. */

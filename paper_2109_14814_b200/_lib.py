@@ -28,7 +28,7 @@ EXPORTS = ("mcx_a_block", "mcx_workspace_bytes", "mcx_batch_workspace_bytes", "m
 class MeshDev(ctypes.Structure):
     _fields_ = [("n_tri", ctypes.c_uint64), ("box", ctypes.c_void_p), ("geo", ctypes.c_void_p),
                 ("perm", ctypes.c_void_p), ("gbox", ctypes.c_void_p), ("tbox", ctypes.c_void_p),
-                ("bbox", ctypes.c_void_p)]
+                ("bbox", ctypes.c_void_p), ("status", ctypes.c_void_p)]
 
 
 class Task(ctypes.Structure):
@@ -83,7 +83,7 @@ def load():
     L.mcx_search_batch.restype = i32
     L.mcx_search_batch.argtypes = [P(Task), u32, P(Opts), vp, vp, u64, P(Stats)]
     L.mcx_pack.restype = i32
-    L.mcx_pack.argtypes = [vp, u32, u32, i32, vp, vp, vp, i32, vp]
+    L.mcx_pack.argtypes = [vp, u32, u32, i32, vp, vp, vp, vp, i32, vp]
     L.mcx_levels.restype = i32
     L.mcx_levels.argtypes = [vp, u64, vp, vp, vp, i32, vp]
     L.mcx_search.restype = i32

@@ -21,8 +21,10 @@
 namespace mcx {
 
 __global__ void pack_kernel(const double* __restrict__ coords, uint32_t N, uint32_t M, int tiled,
-                            double* __restrict__ box, double* __restrict__ geo, uint32_t* __restrict__ perm) {
+                            double* __restrict__ box, double* __restrict__ geo, uint32_t* __restrict__ perm,
+                            uint32_t* __restrict__ status) {
   const uint64_t n_tri = 2ull * N * (M - 1);
+  bool bad = false;
   for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n_tri;
        t += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t q = t >> 1;
@@ -34,25 +36,24 @@ __global__ void pack_kernel(const double* __restrict__ coords, uint32_t N, uint3
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const double* pl = coords + (uint64_t)c * M * N;
-      const double w00 = pl[(uint64_t)k * N + i], w10 = pl[(uint64_t)k * N + ip];
-      const double w01 = pl[(uint64_t)(k + 1) * N + i], w11 = pl[(uint64_t)(k + 1) * N + ip];
+      const double w00 = __ldg(pl + (uint64_t)k * N + i), w10 = __ldg(pl + (uint64_t)k * N + ip);
+      const double w01 = __ldg(pl + (uint64_t)(k + 1) * N + i), w11 = __ldg(pl + (uint64_t)(k + 1) * N + ip);
       v0[c] = __dadd_rn(tau ? w01 : w00, 0.0);  // canonicalise -0.0
       v1[c] = __dadd_rn(w10, 0.0);
       v2[c] = __dadd_rn(tau ? w11 : w01, 0.0);
+      bad |= !(isfinite(v0[c]) && isfinite(v1[c]) && isfinite(v2[c]));
     }
-    double e1[4], e2[4];
-    double* b = box + dst * MCX_BOX_STRIDE;
-    double* g = geo + dst * MCX_GEO_STRIDE;
+    double b[8], g[20];
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       b[c] = fmin(fmin(v0[c], v1[c]), v2[c]);
       b[4 + c] = fmax(fmax(v0[c], v1[c]), v2[c]);
-      e1[c] = __dsub_rn(v1[c], v0[c]);
-      e2[c] = __dsub_rn(v2[c], v0[c]);
       g[c] = v0[c];
-      g[4 + c] = e1[c];
-      g[8 + c] = e2[c];
+      g[4 + c] = __dsub_rn(v1[c], v0[c]);
+      g[8 + c] = __dsub_rn(v2[c], v0[c]);
     }
+    const double* e1 = g + 4;
+    const double* e2 = g + 8;
     const int bi[6] = {0, 0, 0, 1, 1, 2}, bj[6] = {1, 2, 3, 2, 3, 3};
 #pragma unroll
     for (int p = 0; p < 6; ++p)
@@ -67,58 +68,70 @@ __global__ void pack_kernel(const double* __restrict__ coords, uint32_t N, uint3
     n2 = __dadd_rn(n2, __dmul_rn(e2[3], e2[3]));
     g[18] = __dmul_rn(__dsqrt_rn(n1), __dsqrt_rn(n2));
     g[19] = 0.0;
+    // 16-byte vector stores (records are 64 / 160 B, 16-byte aligned)
+    double2* bo = reinterpret_cast<double2*>(box + dst * MCX_BOX_STRIDE);
+    double2* go = reinterpret_cast<double2*>(geo + dst * MCX_GEO_STRIDE);
+#pragma unroll
+    for (int v = 0; v < 4; ++v) bo[v] = make_double2(b[2 * v], b[2 * v + 1]);
+#pragma unroll
+    for (int v = 0; v < 10; ++v) go[v] = make_double2(g[2 * v], g[2 * v + 1]);
     if (perm) perm[dst] = (uint32_t)t;
   }
+  if (status && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(status, 1u);
 }
 
-// One warp per 32-triangle group: shuffle min/max reduction (exact).
-__global__ void group_box_kernel(const Box* __restrict__ box, uint64_t n, Box* __restrict__ gbox) {
-  const uint64_t ng = (n + GROUP - 1) / GROUP;
-  const int lane = threadIdx.x & 31;
-  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x / 32);
-  for (uint64_t g = blockIdx.x * (uint64_t)(blockDim.x / 32) + threadIdx.x / 32; g < ng; g += warps) {
-    const uint64_t t = g * GROUP + lane;
-    double lo[4], hi[4];
-    if (t < n) {
-      const double2* s = reinterpret_cast<const double2*>(box + t);
+// Culling hierarchy in one pass: one CTA per A block of 1024 records (= 2 B tiles
+// = 32 groups).  Each thread unions 4 consecutive records, 8 lanes form a group
+// (shuffle), the CTA's 32 group boxes give its 2 tile boxes and its block box.
+__global__ void __launch_bounds__(256) levels_kernel(const Box* __restrict__ box, uint64_t n, Box* __restrict__ gbox,
+                                                     Box* __restrict__ tbox, Box* __restrict__ bbox) {
+  __shared__ Box gsm[A_BLOCK / GROUP];
+  const uint64_t blk = blockIdx.x;
+  const int tid = threadIdx.x;
+  double lo[4], hi[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) { lo[c] = __longlong_as_double(0x7ff0000000000000ll); hi[c] = -lo[c]; }
+  const uint64_t r0 = blk * A_BLOCK + 4ull * tid;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    if (r0 + u < n) {
+      const double2* s = reinterpret_cast<const double2*>(box + r0 + u);
       const double2 a = __ldg(s), b = __ldg(s + 1), c = __ldg(s + 2), d = __ldg(s + 3);
-      lo[0] = a.x; lo[1] = a.y; lo[2] = b.x; lo[3] = b.y;
-      hi[0] = c.x; hi[1] = c.y; hi[2] = d.x; hi[3] = d.y;
-    } else {
-#pragma unroll
-      for (int c = 0; c < 4; ++c) { lo[c] = __longlong_as_double(0x7ff0000000000000ll); hi[c] = -lo[c]; }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        lo[c] = fmin(lo[c], __shfl_xor_sync(0xffffffffu, lo[c], o));
-        hi[c] = fmax(hi[c], __shfl_xor_sync(0xffffffffu, hi[c], o));
-      }
-    }
-    if (lane == 0) {
-      Box r;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) { r.lo[c] = lo[c]; r.hi[c] = hi[c]; }
-      gbox[g] = r;
+      lo[0] = fmin(lo[0], a.x); lo[1] = fmin(lo[1], a.y); lo[2] = fmin(lo[2], b.x); lo[3] = fmin(lo[3], b.y);
+      hi[0] = fmax(hi[0], c.x); hi[1] = fmax(hi[1], c.y); hi[2] = fmax(hi[2], d.x); hi[3] = fmax(hi[3], d.y);
     }
   }
-}
-
-// Union of `per` consecutive group boxes.
-__global__ void super_box_kernel(const Box* __restrict__ gbox, uint64_t ng, int per, Box* __restrict__ out) {
-  const uint64_t ns = (ng + per - 1) / per;
-  for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < ns; s += (uint64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+  for (int o = 1; o < 8; o <<= 1) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      lo[c] = fmin(lo[c], __shfl_xor_sync(0xffffffffu, lo[c], o));
+      hi[c] = fmax(hi[c], __shfl_xor_sync(0xffffffffu, hi[c], o));
+    }
+  }
+  const uint64_t ng = (n + GROUP - 1) / GROUP;
+  if ((tid & 7) == 0) {
     Box r;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) { r.lo[c] = __longlong_as_double(0x7ff0000000000000ll); r.hi[c] = -r.lo[c]; }
-    const uint64_t g1 = min(ng, (s + 1) * (uint64_t)per);
-    for (uint64_t g = s * per; g < g1; ++g) {
-      const Box b = gbox[g];
+    for (int c = 0; c < 4; ++c) { r.lo[c] = lo[c]; r.hi[c] = hi[c]; }
+    gsm[tid >> 3] = r;
+    const uint64_t g = blk * (A_BLOCK / GROUP) + (tid >> 3);
+    if (g < ng) gbox[g] = r;
+  }
+  __syncthreads();
+  if (tid < 3) {
+    const int g0 = tid == 2 ? 0 : tid * (TILE / GROUP);
+    const int g1 = tid == 2 ? A_BLOCK / GROUP : g0 + TILE / GROUP;
+    Box r = gsm[g0];
+    for (int g = g0 + 1; g < g1; ++g)
 #pragma unroll
-      for (int c = 0; c < 4; ++c) { r.lo[c] = fmin(r.lo[c], b.lo[c]); r.hi[c] = fmax(r.hi[c], b.hi[c]); }
+      for (int c = 0; c < 4; ++c) { r.lo[c] = fmin(r.lo[c], gsm[g].lo[c]); r.hi[c] = fmax(r.hi[c], gsm[g].hi[c]); }
+    if (tid == 2) {
+      bbox[blk] = r;
+    } else {
+      const uint64_t tt = blk * (A_BLOCK / TILE) + tid;
+      if (tt < (n + TILE - 1) / TILE) tbox[tt] = r;
     }
-    out[s] = r;
   }
 }
 
@@ -133,7 +146,7 @@ static unsigned grid_for(uint64_t work, int threads) {
 extern "C" {
 
 int mcx_pack(const double* coords, uint32_t N, uint32_t M, int order, double* box, double* geo, uint32_t* perm,
-             int device, void* stream) {
+             uint32_t* status, int device, void* stream) {
   using namespace mcx;
   if (N < 1 || M < 2) return set_error(MCX_E_ARG, "pack needs N >= 1 and M >= 2 (got N=%u, M=%u)", N, M);
   if (2ull * N * (M - 1) >= (1ull << 32)) return set_error(MCX_E_ARG, "triangle count must be < 2^32");
@@ -142,8 +155,9 @@ int mcx_pack(const double* coords, uint32_t N, uint32_t M, int order, double* bo
   if (((uintptr_t)box | (uintptr_t)geo) & 15) return set_error(MCX_E_ARG, "box/geo must be 16-byte aligned");
   CUDA_TRY(cudaSetDevice(device));
   const uint64_t n = 2ull * N * (M - 1);
+  if (status) CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(uint32_t), (cudaStream_t)stream));
   pack_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(coords, N, M, order == MCX_ORDER_TILED, box, geo,
-                                                                  perm);
+                                                                  perm, status);
   CUDA_TRY(cudaGetLastError());
   return MCX_OK;
 }
@@ -157,13 +171,10 @@ int mcx_levels(const double* box, uint64_t n_tri, double* gbox, double* tbox, do
   if (n_tri == 0) return MCX_OK;
   CUDA_TRY(cudaSetDevice(device));
   cudaStream_t s = (cudaStream_t)stream;
-  const uint64_t ng = (n_tri + GROUP - 1) / GROUP;
-  group_box_kernel<<<grid_for(ng * 32, 256), 256, 0, s>>>(reinterpret_cast<const Box*>(box), n_tri,
-                                                          reinterpret_cast<Box*>(gbox));
-  super_box_kernel<<<grid_for((ng + 15) / 16, 256), 256, 0, s>>>(reinterpret_cast<const Box*>(gbox), ng,
-                                                                 TILE / GROUP, reinterpret_cast<Box*>(tbox));
-  super_box_kernel<<<grid_for((ng + 31) / 32, 256), 256, 0, s>>>(reinterpret_cast<const Box*>(gbox), ng,
-                                                                 A_BLOCK / GROUP, reinterpret_cast<Box*>(bbox));
+  const uint64_t nb = (n_tri + A_BLOCK - 1) / A_BLOCK;
+  if (nb > 0x7fffffffull) return set_error(MCX_E_ARG, "too many records");
+  levels_kernel<<<(unsigned)nb, 256, 0, s>>>(reinterpret_cast<const Box*>(box), n_tri, reinterpret_cast<Box*>(gbox),
+                                             reinterpret_cast<Box*>(tbox), reinterpret_cast<Box*>(bbox));
   CUDA_TRY(cudaGetLastError());
   return MCX_OK;
 }

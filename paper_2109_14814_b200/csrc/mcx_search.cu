@@ -85,6 +85,8 @@ struct __align__(16) SearchParams {
   const Box* bboxA;
   const Box* gboxB;
   const Box* tboxB;
+  const uint32_t* statusA;  // mcx_pack non-finite flags (may be NULL)
+  const uint32_t* statusB;
   // KIND_QUAD only: half-layer grids (4, M, N) for the Moller stage
   const double* coordsA;
   const double* coordsB;
@@ -369,6 +371,17 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_brute_kernel(const
   flush_counters(P, lane, n_pass, n_sing, 0);
 }
 
+// OR of every task's input-mesh status flags (non-finite coordinates) into *flag.
+__global__ void status_kernel(const SearchParams* __restrict__ tasks, uint32_t n, unsigned long long* flag) {
+  unsigned v = 0;
+  for (uint32_t t = threadIdx.x; t < n; t += blockDim.x) {
+    if (tasks[t].statusA) v |= *tasks[t].statusA;
+    if (tasks[t].statusB) v |= *tasks[t].statusB;
+  }
+  v = __any_sync(0xffffffffu, v != 0);
+  if (threadIdx.x == 0 && v) atomicOr(flag, 1ull);
+}
+
 // ------------------------------------------------------------ cull kernels
 // Level 1: (task, local A block x, B tile y) union-box tests over the flattened
 // unit space of all tasks, compacted with one atomic per warp.
@@ -537,12 +550,12 @@ static int launch_brute_cfg(std::vector<SearchParams>& T, Batch Bt, std::vector<
     prefix[t + 1] = prefix[t] + T[t].my_blocks * T[t].nchunk;
   }
   const uint64_t total = prefix.back();
-  if (total == 0) return MCX_OK;
-  if (total > 0x7fffffffull) return set_error(MCX_E_ARG, "grid too large");
   const size_t tab = sizeof(SearchParams) * T.size();
   CUDA_TRY(cudaMemcpyAsync(dev_tab, T.data(), tab, cudaMemcpyHostToDevice, stream));
   CUDA_TRY(cudaMemcpyAsync((char*)dev_tab + tab, prefix.data(), sizeof(uint64_t) * prefix.size(),
                            cudaMemcpyHostToDevice, stream));
+  if (total == 0) return MCX_OK;
+  if (total > 0x7fffffffull) return set_error(MCX_E_ARG, "grid too large");
   Bt.tasks = reinterpret_cast<const SearchParams*>(dev_tab);
   Bt.prefix = reinterpret_cast<const uint64_t*>((char*)dev_tab + tab);
   search_brute_kernel<KIND, C><<<(unsigned)total, C::THREADS, smem, stream>>>(Bt);
@@ -574,11 +587,11 @@ static int launch_cull(std::vector<SearchParams>& T, Batch Bt, std::vector<uint6
   prefix.assign(T.size() + 1, 0);
   for (size_t t = 0; t < T.size(); ++t) prefix[t + 1] = prefix[t] + T[t].my_blocks * (T[t].nB ? T[t].ntilesB : 0);
   const uint64_t total = prefix.back();
-  if (total == 0) return MCX_OK;
   const size_t tab = sizeof(SearchParams) * T.size();
   CUDA_TRY(cudaMemcpyAsync(dev_tab, T.data(), tab, cudaMemcpyHostToDevice, stream));
   CUDA_TRY(cudaMemcpyAsync((char*)dev_tab + tab, prefix.data(), sizeof(uint64_t) * prefix.size(),
                            cudaMemcpyHostToDevice, stream));
+  if (total == 0) return MCX_OK;
   Bt.tasks = reinterpret_cast<const SearchParams*>(dev_tab);
   Bt.prefix = reinterpret_cast<const uint64_t*>((char*)dev_tab + tab);
   int dev_sms = 148;
@@ -704,6 +717,8 @@ static int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mc
     P.bboxA = reinterpret_cast<const Box*>(A->bbox);
     P.gboxB = reinterpret_cast<const Box*>(B->gbox);
     P.tboxB = reinterpret_cast<const Box*>(B->tbox);
+    P.statusA = A->status;
+    P.statusB = B->status;
     st[t] = mcx_stats{};
     st[t].n_pairs = g.na * B->n_tri;
   }
@@ -728,6 +743,9 @@ static int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mc
                                            : launch_cull(T, Bt, prefix, ws + L.table, o->device, stream);
   if (rc != MCX_OK) return rc;
   if (o->timing) CUDA_TRY(cudaEventRecord(tm.e1, stream));
+  status_kernel<<<1, 32, 0, stream>>>(reinterpret_cast<const SearchParams*>(ws + L.table), n,
+                                      reinterpret_cast<unsigned long long*>(ws) + 2);
+  CUDA_TRY(cudaGetLastError());
   std::vector<unsigned long long> h(8 + 8ull * n);
   CUDA_TRY(cudaMemcpyAsync(h.data(), ws, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, stream));
   CUDA_TRY(cudaStreamSynchronize(stream));  // also keeps T / prefix alive until the copies are done
@@ -741,6 +759,7 @@ static int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mc
     st[t].n_tested = o->mode == MCX_MODE_BRUTE ? st[t].n_pairs : c[3];
     st[t].kernel_ms = ms;
   }
+  if (h[2]) return set_error(MCX_E_ARG, "non-finite (NaN/Inf) coordinates in an input mesh (mcx_pack status)");
   if (h[0] > cap)
     return set_error(MCX_E_CAPACITY, "hit capacity %llu < %llu hits", (unsigned long long)cap, h[0]);
   return MCX_OK;

@@ -69,11 +69,9 @@ class DeviceMesh:
         s = stream or t.cuda.current_stream(device)
         _check_coords(coords)
         if isinstance(coords, np.ndarray):
-            if not np.all(np.isfinite(coords)):
-                raise ConfigError("mesh coordinates must be finite (NaN/Inf would break the AABB contract)")
             coords = t.from_numpy(np.ascontiguousarray(coords, dtype=np.float64))
-        elif coords.device.type == "cpu" and not bool(t.isfinite(coords).all()):
-            raise ConfigError("mesh coordinates must be finite (NaN/Inf would break the AABB contract)")
+        # NaN/Inf are detected on the device by mcx_pack (status flag) and reported
+        # by the search; no host-side pass over the coordinates.
         with t.cuda.device(device), t.cuda.stream(s):
             pinned = coords.device.type == "cpu" and coords.is_pinned()
             self.coords = coords.to(dev, dtype=t.float64, non_blocking=pinned).contiguous()
@@ -91,9 +89,11 @@ class DeviceMesh:
             self.gbox = t.empty((-(-n // _lib.GROUP), 8), dtype=t.float64, device=dev)
             self.tbox = t.empty((-(-n // _lib.TILE), 8), dtype=t.float64, device=dev)
             self.bbox = t.empty((-(-n // _lib.BLOCK), 8), dtype=t.float64, device=dev)
+            self.status = t.empty(1, dtype=t.int32, device=dev)
         L = _lib.load()
         rc = L.mcx_pack(self.coords.data_ptr(), self.N, self.M, order, self.box.data_ptr(), self.geo.data_ptr(),
-                        self.perm.data_ptr() if self.perm is not None else None, device, s.cuda_stream)
+                        self.perm.data_ptr() if self.perm is not None else None, self.status.data_ptr(), device,
+                        s.cuda_stream)
         _lib.check(rc, "mcx_pack")
         rc = L.mcx_levels(self.box.data_ptr(), n, self.gbox.data_ptr(), self.tbox.data_ptr(), self.bbox.data_ptr(),
                           device, s.cuda_stream)
@@ -102,7 +102,7 @@ class DeviceMesh:
     def struct(self) -> _lib.MeshDev:
         return _lib.MeshDev(self.n_tri, self.box.data_ptr(), self.geo.data_ptr(),
                             self.perm.data_ptr() if self.perm is not None else None,
-                            self.gbox.data_ptr(), self.tbox.data_ptr(), self.bbox.data_ptr())
+                            self.gbox.data_ptr(), self.tbox.data_ptr(), self.bbox.data_ptr(), self.status.data_ptr())
 
 
 @dataclass
@@ -264,9 +264,27 @@ def _merge(results) -> SearchResult:
     return SearchResult(hits=hits, stats=stats)
 
 
+def search_one(coords_a, coords_b, *, device: int = 0, mode: int = _lib.MODE_BRUTE, shard=(0, 1),
+               timing: bool = False, task=None, stream=None) -> SearchResult:
+    """Host grids → hits on one device: B is uploaded and packed on a side stream so
+    its H2D overlaps A's packing; then one search call.  Pinned CPU tensors give
+    asynchronous copies."""
+    t = torch()
+    with t.cuda.device(device):
+        main = stream or t.cuda.current_stream(device)
+        side = t.cuda.Stream(device)
+        side.wait_stream(main)
+        Bm = DeviceMesh(coords_b, device, stream=side)
+        ready = side.record_event()
+        Am = DeviceMesh(coords_a, device, stream=main)
+        main.wait_event(ready)
+        return search_device(Am, Bm, mode=mode, shard=shard, timing=timing, stream=main, task=task)
+
+
 def search(coords_a, coords_b, *, devices=(0,), mode: int = _lib.MODE_BRUTE, timing: bool = False,
            task=None) -> SearchResult:
-    """Host-to-host triangle search: upload, pack, search (sharded over ``devices``), gather, sort."""
+    """Host-to-host triangle search: upload, pack, search (sharded over ``devices``,
+    one host thread per GPU), gather, sort."""
     devices = list(devices)
     if not devices:
         raise ConfigError("devices must be non-empty")
@@ -278,12 +296,8 @@ def search(coords_a, coords_b, *, devices=(0,), mode: int = _lib.MODE_BRUTE, tim
 
     def run(rank: int):
         try:
-            d = devices[rank]
-            t = torch()
-            with t.cuda.device(d):
-                A = DeviceMesh(coords_a, d)
-                B = DeviceMesh(coords_b, d)
-                results[rank] = search_device(A, B, mode=mode, shard=(rank, G), timing=timing, task=task)
+            results[rank] = search_one(coords_a, coords_b, device=devices[rank], mode=mode, shard=(rank, G),
+                                       timing=timing, task=task)
         except Exception as exc:  # surfaced below with the task id
             errors[rank] = exc
 

@@ -257,11 +257,19 @@ def test_pair_candidates_small_exhaustive():
     assert np.array_equal(isect.pair_candidates(A, B), want.astype(np.uint64))
 
 
-def test_nan_rejected():
-    A, _ = manifold_like(8, 3, 1)
-    A[0, 1, 2] = np.nan
-    with pytest.raises(Exception):
-        D.search(A, A)
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("bad", [np.nan, np.inf, -np.inf])
+def test_non_finite_rejected(mode, bad):
+    """NaN/Inf inputs are flagged by the device packer and fail the search loudly."""
+    from paper_2109_14814_b200.errors import BackendError
+    A, _ = manifold_like(40, 7, 1)
+    B = A.copy()
+    B[2, 3, 17] = bad
+    with pytest.raises(BackendError, match="non-finite"):
+        D.search(A, B, mode=mode)
+    with pytest.raises(BackendError, match="non-finite"):
+        D.search_batch([(D.DeviceMesh(A, 0), D.DeviceMesh(A, 0)), (D.DeviceMesh(B, 0), D.DeviceMesh(A, 0))], mode=mode)
+    assert len(D.search(A, A, mode=mode).hits) > 0  # finite inputs still fine
 
 
 def test_bad_args_fail_loudly():
