@@ -165,6 +165,15 @@ int mcx_pair_candidates(const double* coords_a, uint32_t NA, uint32_t MA,
                         uint64_t* gids, uint64_t cap, uint64_t* n_out);
 /* workspace for mcx_pair_candidates: 1024 + 64·(N_A(M_A−1) + N_B(M_B−1)) bytes, 16-byte aligned. */
 
+/* Device-side record fields for hits:
+ * gid[k] (u64), point[k][4] = p + s·e1 + t·e2 from A's grid, params[k][4]
+ * = (θ_u, s_u, θ_s, s_s) per Eqs. (28)-(29) (T² by its vertex map), bit-identical to
+ * isect.hits_to_records.  coords_a: A's (4, MA, NA) grid; s_a/s_b: the half-layers'
+ * s-values (device).  Enqueued on `stream`. */
+int mcx_records(const mcx_hit* hits, uint64_t n, const double* coords_a, uint32_t NA, uint32_t MA,
+                const double* s_a, uint32_t NB, uint32_t MB, const double* s_b, uint64_t* gid,
+                double* point, double* params, int device, void* stream);
+
 const char* mcx_last_error(void);
 int mcx_version(void);
 

@@ -8,7 +8,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmcx.so")
-SOURCES = ["mcx_pack.cu", "mcx_search.cu"]
+SOURCES = ["mcx_pack.cu", "mcx_search.cu", "mcx_records.cu"]
 DEPS = SOURCES + ["mcx_common.cuh"]
 
 NVCC_FLAGS = [

@@ -344,6 +344,32 @@ def pair_candidates_device(coords_a, coords_b, device: int = 0, cap: int = 1 << 
     return np.sort(out)
 
 
+def record_fields_device(coords_a, s_a, coords_b, s_b, hits: np.ndarray, device: int = 0):
+    """gid / point / params of every hit computed on the device (mcx_records)."""
+    t = torch()
+    n = len(hits)
+    if n == 0:
+        return np.zeros(0, np.uint64), np.zeros((0, 4)), np.zeros((0, 4))
+    _require_cuda(device)
+    L = _lib.load()
+    dev = t.device("cuda", device)
+    ca = t.as_tensor(np.ascontiguousarray(coords_a, dtype=np.float64)).to(dev)
+    _, MA, NA = ca.shape
+    _, MB, NB = np.asarray(coords_b).shape
+    sa = t.as_tensor(np.ascontiguousarray(s_a, dtype=np.float64)).to(dev)
+    sb = t.as_tensor(np.ascontiguousarray(s_b, dtype=np.float64)).to(dev)
+    h = t.from_numpy(np.ascontiguousarray(hits).view(np.uint8)).to(dev)
+    gid = t.empty(n, dtype=t.int64, device=dev)
+    pts = t.empty((n, 4), dtype=t.float64, device=dev)
+    par = t.empty((n, 4), dtype=t.float64, device=dev)
+    with t.cuda.device(device):
+        s = t.cuda.current_stream(device)
+        rc = L.mcx_records(h.data_ptr(), n, ca.data_ptr(), NA, MA, sa.data_ptr(), NB, MB, sb.data_ptr(),
+                           gid.data_ptr(), pts.data_ptr(), par.data_ptr(), device, s.cuda_stream)
+    _lib.check(rc, "mcx_records")
+    return gid.cpu().numpy().view(np.uint64), pts.cpu().numpy(), par.cpu().numpy()
+
+
 def ctypes_u64():
     import ctypes
     return ctypes.c_uint64(0)

@@ -142,7 +142,7 @@ def _check_backend(backend: str):
 
 
 # ---------------------------------------------------------------- search API
-def search_hits(u_half, s_half, backend: str = "cuda", *, devices=(0,), mode: str = "brute",
+def search_hits(u_half, s_half, backend: str = "cuda", *, devices=(0,), mode: str = "cull",
                 timing: bool = False):
     """Triangle-level hits (iA, iB, s, t, a, b), sorted by (iA, iB), plus kernel stats."""
     _check_backend(backend)
@@ -160,9 +160,11 @@ def pair_candidates(u_half, s_half, backend: str = "cuda", *, device: int = 0) -
                                           task=_task(u_half, s_half))
 
 
-def hits_to_records(coords_a, s_a, coords_b, s_b, hits, layer=(0, "+", 0, "+"), tof=float("nan"),
-                    dedup: bool = True):
-    """Build sorted, deduplicated IntersectionRecords from triangle hits (host, tiny)."""
+def record_fields(coords_a, s_a, coords_b, s_b, hits):
+    """Host (NumPy) record fields for hits: (gid u64, point (n,4), params (n,4)).
+
+    Same op sequence as the device version (csrc/mcx_records.cu), bit-identical.
+    """
     _, MA, NA = coords_a.shape
     _, MB, NB = coords_b.shape
     ia = hits["ia"].astype(np.int64)
@@ -172,9 +174,7 @@ def hits_to_records(coords_a, s_a, coords_b, s_b, hits, layer=(0, "+", 0, "+"), 
     i, k1 = qa % NA, qa // NA
     j, l1 = qb % NB, qb // NB
     gid = cartesian_to_gid(i, j, k1, l1, NA, NB, MA)
-    order = np.lexsort((tauB, tauA, gid))
-    s, t, a, b = (hits[f][order] for f in ("s", "t", "a", "b"))
-    ia, i, k1, tauA, j, l1, tauB, gid = (x[order] for x in (ia, i, k1, tauA, j, l1, tauB, gid))
+    s, t, a, b = (hits[f] for f in ("s", "t", "a", "b"))
     # points p + s·e1 + t·e2 from A's grid (FMA-free, fixed order — SURVEY.md §7.3 step 8)
     W = np.transpose(coords_a, (1, 2, 0))
     ip = (i + 1) % NA
@@ -184,9 +184,8 @@ def hits_to_records(coords_a, s_a, coords_b, s_b, hits, layer=(0, "+", 0, "+"), 
     e1 = v10 - p
     e2 = np.where(T2, v11, v01) - p
     pts = (p + s[:, None] * e1) + t[:, None] * e2
-    thA, thB = grid_points(NA), grid_points(NB)
-    thA_n = np.append(thA, 2.0 * np.pi)  # θ_N = 2π at the wrap (eq. 28)
-    thB_n = np.append(thB, 2.0 * np.pi)
+    thA_n = np.append(grid_points(NA), 2.0 * np.pi)  # θ_N = 2π at the wrap (eq. 28)
+    thB_n = np.append(grid_points(NB), 2.0 * np.pi)
 
     def est(theta_n, sv, ii, kk, tau, x, y):
         th0, th1 = theta_n[ii], theta_n[ii + 1]
@@ -198,51 +197,81 @@ def hits_to_records(coords_a, s_a, coords_b, s_b, hits, layer=(0, "+", 0, "+"), 
         ss = np.where(tau == 0, (1 - y) * s0 + y * s1, (1 - x) * s1 + x * s0)
         return th, ss
 
-    thu, su = est(thA_n, s_a, i, k1, tauA, s, t)
-    ths, ss = est(thB_n, s_b, j, l1, tauB, a, b)
-    keep = np.ones(len(gid), dtype=bool)
-    if dedup and len(gid) > 1:
-        keep = _dedup_mask(pts, DEDUP_TOL)
+    thu, su = est(thA_n, np.asarray(s_a, dtype=np.float64), i, k1, tauA, s, t)
+    ths, ss = est(thB_n, np.asarray(s_b, dtype=np.float64), j, l1, tauB, a, b)
+    return gid.astype(np.uint64), pts, np.stack([thu, su, ths, ss], axis=1)
+
+
+def assemble_records(coords_a, coords_b, hits, gid, pts, params, layer=(0, "+", 0, "+"), tof=float("nan"),
+                     dedup: bool = True):
+    """Sort by (gid, τ_A, τ_B), deduplicate within 1e-9 and build records."""
+    _, MA, NA = coords_a.shape
+    _, MB, NB = coords_b.shape
+    ia = hits["ia"].astype(np.int64)
+    ib = hits["ib"].astype(np.int64)
+    order = np.lexsort((ib & 1, ia & 1, gid))
+    ia, ib, gid, pts, params = ia[order], ib[order], gid[order], pts[order], params[order]
+    bary = np.stack([hits[f][order] for f in ("s", "t", "a", "b")], axis=1)
+    keep = _dedup_mask(pts, DEDUP_TOL) if (dedup and len(gid) > 1) else np.ones(len(gid), dtype=bool)
     recs = []
     for n in np.nonzero(keep)[0]:
+        qa, qb = int(ia[n]) >> 1, int(ib[n]) >> 1
         recs.append(IntersectionRecord(
-            point=pts[n].copy(), bary=(float(s[n]), float(t[n]), float(a[n]), float(b[n])),
-            params=(float(thu[n]), float(su[n]), float(ths[n]), float(ss[n])),
-            pair=QuadIndex(int(gid[n]), int(i[n]), int(j[n]), int(k1[n]) + 1, int(l1[n]) + 1),
-            tri=(int(tauA[n]), int(tauB[n])), layer=layer, tof=tof, tri_index=(int(ia[n]), int(hits["ib"][order][n]))))
+            point=pts[n].copy(), bary=tuple(float(v) for v in bary[n]), params=tuple(float(v) for v in params[n]),
+            pair=QuadIndex(int(gid[n]), qa % NA, qb % NB, qa // NA + 1, qb // NB + 1),
+            tri=(int(ia[n]) & 1, int(ib[n]) & 1), layer=layer, tof=tof, tri_index=(int(ia[n]), int(ib[n]))))
     return recs
 
 
+def hits_to_records(coords_a, s_a, coords_b, s_b, hits, layer=(0, "+", 0, "+"), tof=float("nan"),
+                    dedup: bool = True):
+    """Build sorted, deduplicated IntersectionRecords from triangle hits (host path)."""
+    gid, pts, params = record_fields(coords_a, s_a, coords_b, s_b, hits)
+    return assemble_records(coords_a, coords_b, hits, gid, pts, params, layer=layer, tof=tof, dedup=dedup)
+
+
 def _dedup_mask(pts: np.ndarray, tol: float) -> np.ndarray:
-    """Greedy in record order: drop a record whose point is within tol (max-norm) of a kept one."""
-    keep = np.zeros(len(pts), dtype=bool)
-    cells: dict = {}
-    key = np.floor(pts / tol).astype(np.int64)
-    offs = np.array(np.meshgrid(*([[-1, 0, 1]] * 4), indexing="ij")).reshape(4, -1).T
-    for n in range(len(pts)):
-        dup = False
-        for o in offs:
-            for m in cells.get(tuple(key[n] + o), ()):
-                if np.max(np.abs(pts[m] - pts[n])) <= tol:
-                    dup = True
-                    break
-            if dup:
-                break
-        if not dup:
-            keep[n] = True
-            cells.setdefault(tuple(key[n]), []).append(n)
+    """Greedy in record order: drop a record whose point is within tol (max-norm) of a
+    KEPT earlier record.  Candidate pairs come from an x-sorted sweep (vectorised);
+    only records that have an earlier candidate are resolved in a Python loop."""
+    n = len(pts)
+    keep = np.ones(n, dtype=bool)
+    order = np.argsort(pts[:, 0], kind="stable")
+    xs = pts[order, 0]
+    hi = np.searchsorted(xs, xs + tol, side="right")
+    cnt = hi - np.arange(n) - 1
+    if cnt.sum() == 0:
+        return keep
+    src = np.repeat(np.arange(n), cnt)
+    dst = np.arange(cnt.sum()) - np.repeat(np.cumsum(cnt) - cnt, cnt) + src + 1
+    a, b = order[src], order[dst]
+    close = np.max(np.abs(pts[a] - pts[b]), axis=1) <= tol
+    a, b = a[close], b[close]
+    lo_, hi_ = np.minimum(a, b), np.maximum(a, b)  # record order: lo_ earlier
+    earlier = {}
+    for x, y in zip(lo_.tolist(), hi_.tolist()):
+        earlier.setdefault(y, []).append(x)
+    for y in sorted(earlier):
+        if any(keep[x] for x in earlier[y]):
+            keep[y] = False
     return keep
 
 
-def find_intersections(u_half, s_half, backend: str = "cuda", *, devices=(0,), mode: str = "brute",
+def record_fields_device(coords_a, s_a, coords_b, s_b, hits, device: int = 0):
+    """Device record fields (csrc/mcx_records.cu, §8(f) row 4) for host hit arrays."""
+    return _device.record_fields_device(coords_a, s_a, coords_b, s_b, hits, device=device)
+
+
+def find_intersections(u_half, s_half, backend: str = "cuda", *, devices=(0,), mode: str = "cull",
                        dedup: bool = True, tof: float = float("nan")):
     """All mesh intersections of two half-layers as IntersectionRecords."""
     _check_backend(backend)
     ca, cb = _coords(u_half), _coords(s_half)
     res = search_hits(ca, cb, backend, devices=devices, mode=mode)
     task = _task(u_half, s_half) or (0, "+", 0, "+")
-    return hits_to_records(ca, _svals(u_half, ca.shape[1]), cb, _svals(s_half, cb.shape[1]), res.hits,
-                           layer=task, tof=tof, dedup=dedup)
+    sa, sb = _svals(u_half, ca.shape[1]), _svals(s_half, cb.shape[1])
+    gid, pts, params = record_fields_device(ca, sa, cb, sb, res.hits, device=devices[0])
+    return assemble_records(ca, cb, res.hits, gid, pts, params, layer=task, tof=tof, dedup=dedup)
 
 
 # ---------------------------------------------------------------- records file

@@ -106,8 +106,9 @@ def search_plan(u_mesh: ManifoldMesh, s_mesh: ManifoldMesh, plan: LayerPairPlan,
     results = _device.search_batch(pairs, mode=m, task_ids=None)
     records, stats = [], []
     for res, (hu, hs, layer, tof) in zip(results, meta):
-        records.extend(isect.hits_to_records(np.ascontiguousarray(hu.coords), hu.s_values,
-                                             np.ascontiguousarray(hs.coords), hs.s_values, res.hits,
-                                             layer=layer, tof=tof, dedup=dedup))
+        ca, cb = np.ascontiguousarray(hu.coords), np.ascontiguousarray(hs.coords)
+        gid, pts, params = _device.record_fields_device(ca, hu.s_values, cb, hs.s_values, res.hits, device=device)
+        records.extend(isect.assemble_records(ca, cb, res.hits, gid, pts, params, layer=layer, tof=tof,
+                                              dedup=dedup))
         stats.append({"layer": layer, **res.stats})
     return records, stats

@@ -343,3 +343,23 @@ def test_cli_intersect(tmp_path):
                      "--manifest", str(tmp_path / "m.json")]) == 0
     recs, _ = layers.search_plan(u, s, layers.read_plan(tmp_path / "plan.txt"))
     assert (tmp_path / "rec.txt").read_text().splitlines() == [r.to_line() for r in recs]
+
+
+# ------------------------------------------------------------ device record fields (§8(f) row 4)
+@pytest.mark.parametrize("name", ["C1", "C4ii", "C5/4"])
+def test_device_record_fields_bit_exact(name):
+    A, sa, B, sb = config_pair(name)
+    hits = D.search(A, B, mode=_lib.MODE_CULL).hits
+    g1, p1, q1 = isect.record_fields(A, sa, B, sb, hits)
+    g2, p2, q2 = isect.record_fields_device(A, sa, B, sb, hits)
+    assert np.array_equal(g1, g2)
+    assert np.array_equal(_bits(p1), _bits(p2)) and np.array_equal(_bits(q1), _bits(q2))
+
+
+def test_find_intersections_device_records_equal_host():
+    A, sa, B, sb = config_pair("C4ii")
+    recs = isect.find_intersections(A, B)
+    hits = D.search(A, B).hits
+    want = isect.hits_to_records(A, np.linspace(-1.0, 1.0, A.shape[1]), B, np.linspace(-1.0, 1.0, B.shape[1]), hits)
+    assert [r.to_line() for r in recs] == [w.to_line() for w in want]
+    assert len(recs) < len(hits)  # shared-vertex hits collapse under the 1e-9 dedup

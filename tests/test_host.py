@@ -187,3 +187,14 @@ def test_dedup_within_tolerance():
     pts = np.array([[0, 0, 0, 0], [5e-10, 0, 0, 0], [2e-9, 0, 0, 0], [1, 1, 1, 1], [1, 1, 1, 1 + 1e-10]], float)
     keep = isect._dedup_mask(pts, 1e-9)
     assert keep.tolist() == [True, False, True, True, False]
+
+
+def test_dedup_greedy_chain():
+    """a~b, b~c, not a~c: the greedy rule keeps a, drops b, keeps c (record order)."""
+    pts = np.array([[0, 0, 0, 0], [8e-10, 0, 0, 0], [1.6e-9, 0, 0, 0]], float)
+    assert isect._dedup_mask(pts, 1e-9).tolist() == [True, False, True]
+    rng = np.random.default_rng(0)
+    base = rng.normal(size=(50, 4))
+    pts = np.concatenate([base, base + 1e-12, base[::-1]])
+    keep = isect._dedup_mask(pts, 1e-9)
+    assert keep.sum() == 50 and keep[:50].all()

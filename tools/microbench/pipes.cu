@@ -201,6 +201,81 @@ __global__ void k_dsetp_smem(const double* in, void* outv, long long* cyc) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
 }
 
+
+// FSETP with B operands from shared memory each iteration: 2 LDS.128 (8 floats) +
+// R chains x 8 FSETP — the FP32 conservative-prefilter variant of the inner loop.
+template <int R>
+__global__ void k_fsetp_smem(const double* in, void* outv, long long* cyc) {
+  unsigned* out = (unsigned*)outv;
+  __shared__ float4 sb[512][2];
+  for (int i = threadIdx.x; i < 512 * 2; i += blockDim.x)
+    sb[i / 2][i % 2] = make_float4(in[i % 8] + i, in[(i + 1) % 8] - i, in[(i + 2) % 8] + 0.5f * i, in[(i + 3) % 8]);
+  float alo[R][4], ahi[R][4];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) { alo[r][c] = in[c] + threadIdx.x + r; ahi[r][c] = in[8 + c] + threadIdx.x * 2 + r; }
+  unsigned acc = 0;
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < ITERS / 512 * 8; ++it) {
+#pragma unroll 4
+    for (int j = 0; j < 512; ++j) {
+      const float4 l = sb[j][0], h = sb[j][1];
+      bool any = false;
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        any |= (l.x <= ahi[r][0]) & (alo[r][0] <= h.x) & (l.y <= ahi[r][1]) & (alo[r][1] <= h.y) &
+               (l.z <= ahi[r][2]) & (alo[r][2] <= h.z) & (l.w <= ahi[r][3]) & (alo[r][3] <= h.w);
+      acc += __any_sync(0xffffffffu, any) ? 1u : 0u;
+    }
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
+
+// Mixed-pipe pair test: 4 DSETP (B.lo <= A.hi, FP64 pipe) + 4 FSETP (A.lo_rd <= B.hi_ru,
+// ALU pipe) per pair; B record = lo[4] double + hi[4] float (48 B = 3 LDS.128).
+template <int R>
+__global__ void k_mixed_smem(const double* in, void* outv, long long* cyc) {
+  unsigned* out = (unsigned*)outv;
+  struct __align__(16) MB { double lo[4]; float hi[4]; };
+  __shared__ MB sb[512];
+  for (int i = threadIdx.x; i < 512; i += blockDim.x) {
+    for (int c = 0; c < 4; ++c) { sb[i].lo[c] = in[c] + i * 1e-3; sb[i].hi[c] = (float)(in[4 + c] - i * 1e-3); }
+  }
+  double ahi[R][4];
+  float alo[R][4];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) { alo[r][c] = in[c] + threadIdx.x + r; ahi[r][c] = in[8 + c] + threadIdx.x * 2 + r; }
+  unsigned acc = 0;
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < ITERS / 512 * 8; ++it) {
+#pragma unroll 4
+    for (int j = 0; j < 512; ++j) {
+      const double2 l01 = *reinterpret_cast<const double2*>(&sb[j].lo[0]);
+      const double2 l23 = *reinterpret_cast<const double2*>(&sb[j].lo[2]);
+      const float4 h = *reinterpret_cast<const float4*>(&sb[j].hi[0]);
+      bool any = false;
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        any |= (l01.x <= ahi[r][0]) & (alo[r][0] <= h.x) & (l01.y <= ahi[r][1]) & (alo[r][1] <= h.y) &
+               (l23.x <= ahi[r][2]) & (alo[r][2] <= h.z) & (l23.y <= ahi[r][3]) & (alo[r][3] <= h.w);
+      acc += __any_sync(0xffffffffu, any) ? 1u : 0u;
+    }
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
 // DFMA with loop-carried dependence through 8 accumulators AND an smem operand.
 __global__ void k_dadd_chain(const double* in, void* outv, long long* cyc) {
   double* out = (double*)outv;
@@ -280,6 +355,11 @@ int main() {
   for (int threads : {256, 512}) {
     run("dsetp_smem", k_dsetp_smem, dd, dout, dcyc, nsm, threads, 32.0 * (ITERS / 512 * 8) * 512, 3);
     run("dadd", k_dadd_chain, dd, dout, dcyc, nsm, threads, 32.0 * ITERS, 3);
+    run("fsetp_smem_r4", k_fsetp_smem<4>, dd, dout, dcyc, nsm, threads, 32.0 * (ITERS / 512 * 8) * 512, 3);
+    run("mixed_smem_r4", k_mixed_smem<4>, dd, dout, dcyc, nsm, threads, 32.0 * (ITERS / 512 * 8) * 512, 3);
+    run("mixed_smem_r6", k_mixed_smem<6>, dd, dout, dcyc, nsm, threads, 48.0 * (ITERS / 512 * 8) * 512, 3);
+    run("mixed_smem_r8", k_mixed_smem<8>, dd, dout, dcyc, nsm, threads, 64.0 * (ITERS / 512 * 8) * 512, 3);
+    run("fsetp_smem_r8", k_fsetp_smem<8>, dd, dout, dcyc, nsm, threads, 64.0 * (ITERS / 512 * 8) * 512, 3);
     run("dfma", k_dfma, dd, dout, dcyc, nsm, threads, 32.0 * ITERS, 3);
     run("dsetp", k_dsetp, dd, dout, dcyc, nsm, threads, 32.0 * ITERS, 3);
     run("fsetp", k_fsetp, df, dout, dcyc, nsm, threads, 32.0 * ITERS, 3);
