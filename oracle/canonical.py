@@ -159,7 +159,7 @@ def solve_pairs(A: dict, B: dict):
     return s, t, a, b, singular, hit
 
 
-def search(coords_a, coords_b, chunk: int = 256, a_range=None, packed=None):
+def search(coords_a, coords_b, chunk: int = 0, a_range=None, packed=None):
     """All-pairs triangle search, CPU, single process.
 
     Returns dict: ``ia``, ``ib`` (uint32, sorted by (ia, ib)), ``s``, ``t``, ``a``,
@@ -169,6 +169,8 @@ def search(coords_a, coords_b, chunk: int = 256, a_range=None, packed=None):
     A = packed[0] if packed else pack(coords_a)
     B = packed[1] if packed else pack(coords_b)
     nA, nB = A["lo"].shape[0], B["lo"].shape[0]
+    if chunk <= 0:  # bound the (chunk, nB, 4) temporaries to ~2^22 elements
+        chunk = max(1, (1 << 22) // max(1, nB))
     a0, a1 = (0, nA) if a_range is None else a_range
     ia_l, ib_l = [], []
     for c0 in range(a0, a1, chunk):

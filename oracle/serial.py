@@ -96,9 +96,11 @@ def moller_reject_quads(VA, VB):
     return _side_reject(VA, VB) | _side_reject(VB, VA)
 
 
-def pair_candidates(coords_a, coords_b, chunk: int = 64):
+def pair_candidates(coords_a, coords_b, chunk: int = 0):
     """Sorted u64 gids with ¬aabb_reject ∧ ¬moller_reject, plus the AABB-pass count."""
     ca, cb = np.asarray(coords_a), np.asarray(coords_b)
+    if chunk <= 0:  # bound the (chunk, nB, 4) temporaries to ~2^24 elements
+        chunk = max(1, (1 << 22) // max(1, cb.shape[2] * (cb.shape[1] - 1)))
     _, MA, NA = ca.shape
     _, MB, NB = cb.shape
     VA, VB = quad_vertices(ca), quad_vertices(cb)

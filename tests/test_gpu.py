@@ -363,3 +363,17 @@ def test_find_intersections_device_records_equal_host():
     want = isect.hits_to_records(A, np.linspace(-1.0, 1.0, A.shape[1]), B, np.linspace(-1.0, 1.0, B.shape[1]), hits)
     assert [r.to_line() for r in recs] == [w.to_line() for w in want]
     assert len(recs) < len(hits)  # shared-vertex hits collapse under the 1e-9 dedup
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("kind", ["same", "tangent"])
+def test_parity_stress_large(kind, oracle_lib):
+    """Near-degenerate stress pairs at 512×257 (262k triangles each): B = A (shared edges and
+    vertices everywhere) and near-tangent sheets — both modes vs the C oracle's exact sweep."""
+    from paper_2109_14814_b200.mesh import stress_pair
+    A, B, _ = stress_pair(kind, N=512, M=257, seed=3)
+    ref = oracle_lib.search(A, B, sweep=True, cap=1 << 22)
+    for mode in MODES:
+        r = D.search(A, B, mode=mode)
+        assert_same_hits(ref, r.hits, r.stats)
+    assert len(ref["ia"]) > 1000

@@ -276,6 +276,56 @@ __global__ void k_mixed_smem(const double* in, void* outv, long long* cyc) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
 }
 
+
+// Mixed-pipe with ND FP64 compares (DSETP) + (8-ND) FP32 conservative compares (FSETP)
+// per pair.  B record: 4 doubles (lo) + 4 floats (hi) as before; the first ND compares
+// use doubles (4 lo-vs-hi + (ND-4) hi-vs-lo on doubles held in A registers).
+template <int R, int ND>
+__global__ void k_mixed2_smem(const double* in, void* outv, long long* cyc) {
+  unsigned* out = (unsigned*)outv;
+  struct __align__(16) MB { double lo[4]; double hi[2]; float hif[2]; float pad[2]; };
+  __shared__ MB sb[512];
+  for (int i = threadIdx.x; i < 512; i += blockDim.x) {
+    for (int c = 0; c < 4; ++c) sb[i].lo[c] = in[c] + i * 1e-3;
+    for (int c = 0; c < 2; ++c) { sb[i].hi[c] = in[4 + c] - i * 1e-3; sb[i].hif[c] = (float)(in[6 + c] - i * 1e-3); }
+  }
+  double ahi[R][4], alod[R][2];
+  float alof[R][2];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) ahi[r][c] = in[8 + c] + threadIdx.x * 2 + r;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) { alod[r][c] = in[c] + threadIdx.x + r; alof[r][c] = (float)(in[2 + c] + threadIdx.x + r); }
+  }
+  unsigned acc = 0;
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < ITERS / 512 * 8; ++it) {
+#pragma unroll 4
+    for (int j = 0; j < 512; ++j) {
+      const double2 l01 = *reinterpret_cast<const double2*>(&sb[j].lo[0]);
+      const double2 l23 = *reinterpret_cast<const double2*>(&sb[j].lo[2]);
+      const double2 h01 = *reinterpret_cast<const double2*>(&sb[j].hi[0]);
+      const float2 h23 = *reinterpret_cast<const float2*>(&sb[j].hif[0]);
+      bool any = false;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        bool p = (l01.x <= ahi[r][0]) & (l01.y <= ahi[r][1]) & (l23.x <= ahi[r][2]) & (l23.y <= ahi[r][3]);
+        if (ND >= 6) p = p & (alod[r][0] <= h01.x) & (alod[r][1] <= h01.y);
+        else { p = p & ((float)alod[r][0] <= (float)h01.x) & ((float)alod[r][1] <= (float)h01.y); }
+        p = p & (alof[r][0] <= h23.x) & (alof[r][1] <= h23.y);
+        any |= p;
+      }
+      acc += __any_sync(0xffffffffu, any) ? 1u : 0u;
+    }
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
 // DFMA with loop-carried dependence through 8 accumulators AND an smem operand.
 __global__ void k_dadd_chain(const double* in, void* outv, long long* cyc) {
   double* out = (double*)outv;
@@ -357,6 +407,8 @@ int main() {
     run("dadd", k_dadd_chain, dd, dout, dcyc, nsm, threads, 32.0 * ITERS, 3);
     run("fsetp_smem_r4", k_fsetp_smem<4>, dd, dout, dcyc, nsm, threads, 32.0 * (ITERS / 512 * 8) * 512, 3);
     run("mixed_smem_r4", k_mixed_smem<4>, dd, dout, dcyc, nsm, threads, 32.0 * (ITERS / 512 * 8) * 512, 3);
+    run("mixed2_r4_6d2f", k_mixed2_smem<4, 6>, dd, dout, dcyc, nsm, threads, 32.0 * (ITERS / 512 * 8) * 512, 3);
+    run("mixed2_r5_6d2f", k_mixed2_smem<5, 6>, dd, dout, dcyc, nsm, threads, 40.0 * (ITERS / 512 * 8) * 512, 3);
     run("mixed_smem_r6", k_mixed_smem<6>, dd, dout, dcyc, nsm, threads, 48.0 * (ITERS / 512 * 8) * 512, 3);
     run("mixed_smem_r8", k_mixed_smem<8>, dd, dout, dcyc, nsm, threads, 64.0 * (ITERS / 512 * 8) * 512, 3);
     run("fsetp_smem_r8", k_fsetp_smem<8>, dd, dout, dcyc, nsm, threads, 64.0 * (ITERS / 512 * 8) * 512, 3);
