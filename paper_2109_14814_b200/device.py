@@ -264,6 +264,18 @@ def _merge(results) -> SearchResult:
     return SearchResult(hits=hits, stats=stats)
 
 
+_SIDE_STREAMS: dict = {}
+
+
+def _side_stream(device: int):
+    """One persistent side stream per (thread, device): a fresh stream per call would
+    defeat the caching allocator (its blocks are cached per stream)."""
+    key = (threading.get_ident(), device)
+    if key not in _SIDE_STREAMS:
+        _SIDE_STREAMS[key] = torch().cuda.Stream(device)
+    return _SIDE_STREAMS[key]
+
+
 def search_one(coords_a, coords_b, *, device: int = 0, mode: int = _lib.MODE_BRUTE, shard=(0, 1),
                timing: bool = False, task=None, stream=None) -> SearchResult:
     """Host grids → hits on one device: B is uploaded and packed on a side stream so
@@ -272,7 +284,7 @@ def search_one(coords_a, coords_b, *, device: int = 0, mode: int = _lib.MODE_BRU
     t = torch()
     with t.cuda.device(device):
         main = stream or t.cuda.current_stream(device)
-        side = t.cuda.Stream(device)
+        side = _side_stream(device)
         side.wait_stream(main)
         Bm = DeviceMesh(coords_b, device, stream=side)
         ready = side.record_event()

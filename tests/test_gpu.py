@@ -376,4 +376,4 @@ def test_parity_stress_large(kind, oracle_lib):
     for mode in MODES:
         r = D.search(A, B, mode=mode)
         assert_same_hits(ref, r.hits, r.stats)
-    assert len(ref["ia"]) > 1000
+    assert len(ref["ia"]) > (1000 if kind == "same" else 100)
