@@ -367,6 +367,23 @@ def run_ours(args):
                              "half-layer, all 108 layer-pair tasks in one mcx_search_batch job",
                  "tasks": len(pairs), "published": {"dgx_v100_full_search_s": 16.0, "laptop_full_search_s": 62.0,
                                                     "dgx_v100_bbox_kernel_per_task_s": 0.03}}
+        # the paper's own GPU stage per task: quad-level bbox + Moller candidates (pair_candidates)
+        if rank == 0:
+            hu = np.ascontiguousarray(half_layer(um, 14, 1).coords)
+            hs = np.ascontiguousarray(half_layer(sm, 14, 1).coords)
+            D.pair_candidates_device(hu, hs, device=local)
+            barrier()
+            t0 = time.perf_counter()
+            reps = 5
+            for _ in range(reps):
+                cand = D.pair_candidates_device(hu, hs, device=local)
+            torch.cuda.synchronize(dev)
+            dt = (time.perf_counter() - t0) / reps
+            nq = (hu.shape[2] * (hu.shape[1] - 1)) * (hs.shape[2] * (hs.shape[1] - 1))
+            paper["pair_candidates_one_task"] = {
+                "task": "(U14+, S14+) quad pairs, SPEC-literal bbox + Moller + compaction, host-to-host call",
+                "quad_pairs": nq, "seconds": dt, "quad_pairs_per_s": nq / dt, "candidates": int(len(cand)),
+                "speedup_vs_dgx_v100_bbox_kernel": 0.03 / dt}
         for mname in ("brute", "cull"):
             for _ in range(max(1, args.warmup)):
                 res = D.search_batch(pairs, mode=modes[mname], shard=shard, stream=stream)

@@ -377,3 +377,18 @@ def test_parity_stress_large(kind, oracle_lib):
         r = D.search(A, B, mode=mode)
         assert_same_hits(ref, r.hits, r.stats)
     assert len(ref["ia"]) > (1000 if kind == "same" else 100)
+
+
+def test_c_host_example():
+    """The C ABI driven from plain C (no Python/torch): brute and cull agree."""
+    import subprocess
+    d = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools", "c_example")
+    subprocess.run(["make", "-s", "-C", d], check=True)
+    out = subprocess.run([os.path.join(d, "mcx_example"), "200", "65"], capture_output=True, text=True, check=True)
+    rows = [ln.split() for ln in out.stdout.strip().splitlines()]
+    assert [r[0] for r in rows] == ["brute", "cull"]
+    brute, cull = rows
+    assert brute[1] == cull[1]                      # logical pairs
+    assert brute[2] == brute[1] and int(cull[2]) < int(cull[1])  # executed tests
+    assert brute[3:7] == cull[3:7]                  # aabb pass, singular, hits, checksum
+    assert int(brute[5]) > 0
