@@ -324,9 +324,12 @@ def run_ours(args):
                                "(pipe rate measured: DADD 63.5 lanes/clk/SM, profiles/r01_pipes.jsonl; "
                                "MEASURED_PEAKS.json has no FP64 entry)",
                 "work_per_launch": "8 FP64 compare lane-ops per pair + ~100 FP64 lane-ops per AABB survivor",
-                "kernel_ms": st["kernel_ms"], "traffic": 16798976.0 / 1.7045913600e10 * st["n_pairs"],
-                "traffic_note": "dram__bytes_read+write per launch scaled from the C2 ncu capture "
-                                "(16.8 MB / 1.7e10 pairs, profiles/r01_ncu_brute_c2.txt): B boxes fit in L2"}
+                "kernel_ms": st["kernel_ms"],
+                "traffic": (2140494000.0 + 14626304.0) if args.config == "C3" else None,
+                "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum of one C3 launch, ncu --set full "
+                                "(profiles/r01_ncu_brute_c3.txt): 2.16 GB vs 68 GB of algorithmic L2->SMEM tile "
+                                "traffic; B's 67 MB of boxes are re-read from HBM ~32x per launch (L2 is split "
+                                "over two dies) at ~4 GB/s - negligible against the FP64 bound"}
     cst = cull["stats"]
     cull_block = {"mode": "cull", "value": cull["value"], "unit": UNIT + " (logical)",
                   "ms_per_step": cull["ms_per_step"], "search_wall_s": cull["ms_per_step"] / 1e3,
