@@ -165,6 +165,19 @@ int mcx_pair_candidates(const double* coords_a, uint32_t NA, uint32_t MA,
                         uint64_t* gids, uint64_t cap, uint64_t* n_out);
 /* workspace for mcx_pair_candidates: 1024 + 64·(N_A(M_A−1) + N_B(M_B−1)) bytes, 16-byte aligned. */
 
+/* The same SPEC-literal candidate list from packed meshes (mcx_pack + mcx_levels of the
+ * two grids, any storage order) with exact union-box culling: quads are record pairs,
+ * the quad box is the union of its two triangle boxes (= the SPEC quad AABB), the
+ * Moller stage reads the grids.  Identical gid set and counters to
+ * mcx_pair_candidates; stats: n_pairs = quad pairs, n_tested = quad-box tests run,
+ * n_aabb_pass = quad-AABB survivors, n_singular = Moller rejections, n_hits =
+ * candidates.  opts->mode is ignored (always culls); sharding applies. */
+int mcx_pair_candidates_mesh(const mcx_mesh_dev* A, const double* coords_a, uint32_t NA, uint32_t MA,
+                             const mcx_mesh_dev* B, const double* coords_b, uint32_t NB, uint32_t MB,
+                             const mcx_opts* opts, uint64_t* gids, uint64_t cap, mcx_stats* stats);
+uint64_t mcx_pair_candidates_mesh_workspace_bytes(const mcx_mesh_dev* A, const mcx_mesh_dev* B,
+                                                  const mcx_opts* opts);
+
 /* Device-side record fields for hits:
  * gid[k] (u64), point[k][4] = p + s·e1 + t·e2 from A's grid, params[k][4]
  * = (θ_u, s_u, θ_s, s_s) per Eqs. (28)-(29) (T² by its vertex map), bit-identical to

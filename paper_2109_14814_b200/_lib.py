@@ -22,7 +22,8 @@ BOX_STRIDE, GEO_STRIDE = 8, 20
 GROUP, TILE, BLOCK = 32, 512, 1024
 
 EXPORTS = ("mcx_a_block", "mcx_workspace_bytes", "mcx_batch_workspace_bytes", "mcx_pack", "mcx_levels",
-           "mcx_search", "mcx_search_batch", "mcx_pair_candidates", "mcx_records", "mcx_last_error", "mcx_version")
+           "mcx_search", "mcx_search_batch", "mcx_pair_candidates", "mcx_pair_candidates_mesh",
+           "mcx_pair_candidates_mesh_workspace_bytes", "mcx_records", "mcx_last_error", "mcx_version")
 
 
 class MeshDev(ctypes.Structure):
@@ -90,6 +91,11 @@ def load():
     L.mcx_search.argtypes = [P(MeshDev), P(MeshDev), P(Opts), vp, u64, P(Stats)]
     L.mcx_pair_candidates.restype = i32
     L.mcx_pair_candidates.argtypes = [vp, u32, u32, vp, u32, u32, i32, vp, vp, u64, vp, u64, P(u64)]
+    L.mcx_pair_candidates_mesh.restype = i32
+    L.mcx_pair_candidates_mesh.argtypes = [P(MeshDev), vp, u32, u32, P(MeshDev), vp, u32, u32, P(Opts), vp, u64,
+                                           P(Stats)]
+    L.mcx_pair_candidates_mesh_workspace_bytes.restype = u64
+    L.mcx_pair_candidates_mesh_workspace_bytes.argtypes = [P(MeshDev), P(MeshDev), P(Opts)]
     L.mcx_records.restype = i32
     L.mcx_records.argtypes = [vp, u64, vp, u32, u32, vp, u32, u32, vp, vp, vp, vp, i32, vp]
     L.mcx_last_error.restype = ctypes.c_char_p

@@ -425,6 +425,11 @@ struct CullSmem {
 };
 
 // Level 2 + pair tests: one CTA per overlapping (task, A block, B tile), persistent.
+// KIND_TRI: one A triangle per lane against the 32 B triangles of a group.
+// KIND_QUAD: quads are record pairs (2s, 2s+1 = T¹, T² of one quad), quad box = union
+// of the two triangle boxes (= the SPEC's quad AABB); lane = (A quad l & 15, half of
+// the B group's 16 quads); survivors go through the SPEC-literal Moller stage.
+template <int KIND>
 __global__ void __launch_bounds__(CULL_THREADS) cull_pairs_kernel(const Batch Bt) {
   __shared__ CullSmem S;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -440,7 +445,7 @@ __global__ void __launch_bounds__(CULL_THREADS) cull_pairs_kernel(const Batch Bt
       // task switch: drain this warp's queue and counters against the old task first
       if (cur_task != 0xffffffffu) {
         __syncwarp();
-        if (qn > 0) flush_queue<KIND_TRI>(S.P, Bt, q, qn, lane, n_pass, n_sing);
+        if (qn > 0) flush_queue<KIND>(S.P, Bt, q, qn, lane, n_pass, n_sing);
         qn = 0;
         flush_counters(S.P, lane, n_pass, n_sing, n_tested);
         n_pass = n_sing = n_tested = 0;
@@ -464,34 +469,82 @@ __global__ void __launch_bounds__(CULL_THREADS) cull_pairs_kernel(const Batch Bt
     const int ng = (int)S.n_gpair;
     for (int w = warp; w < ng; w += CULL_WARPS) {
       const int k = S.gpair[w];
-      const uint64_t ia = gblk * A_BLOCK + (uint64_t)(k / (TILE / GROUP)) * GROUP + lane;
+      const uint64_t ga0 = gblk * A_BLOCK + (uint64_t)(k / (TILE / GROUP)) * GROUP;
       const uint64_t jb0 = (uint64_t)txy.z * TILE + (uint64_t)(k % (TILE / GROUP)) * GROUP;
-      const bool va = ia >= P.a_begin && ia < P.a_end;
-      double alo[4], ahi[4];
-      if (va) {
-        const double2* s = reinterpret_cast<const double2*>(P.boxA + ia);
-        const double2 a = __ldg(s), b = __ldg(s + 1), c = __ldg(s + 2), d = __ldg(s + 3);
-        alo[0] = a.x; alo[1] = a.y; alo[2] = b.x; alo[3] = b.y;
-        ahi[0] = c.x; ahi[1] = c.y; ahi[2] = d.x; ahi[3] = d.y;
+      if constexpr (KIND == KIND_TRI) {
+        const uint64_t ia = ga0 + lane;
+        const bool va = ia >= P.a_begin && ia < P.a_end;
+        double alo[4], ahi[4];
+        if (va) {
+          const double2* s = reinterpret_cast<const double2*>(P.boxA + ia);
+          const double2 a = __ldg(s), b = __ldg(s + 1), c = __ldg(s + 2), d = __ldg(s + 3);
+          alo[0] = a.x; alo[1] = a.y; alo[2] = b.x; alo[3] = b.y;
+          ahi[0] = c.x; ahi[1] = c.y; ahi[2] = d.x; ahi[3] = d.y;
+        } else {
+          empty_box(alo, ahi);
+        }
+        const int nb = (int)min((uint64_t)GROUP, P.nB - jb0);
+        const unsigned vmask = __ballot_sync(0xffffffffu, va);
+        if (lane == 0) n_tested += (unsigned long long)__popc(vmask) * nb;
+        for (int j = 0; j < nb; ++j) {
+          const double2* bp = reinterpret_cast<const double2*>(P.boxB + jb0 + j);
+          const double2 l01 = __ldg(bp), l23 = __ldg(bp + 1), h01 = __ldg(bp + 2), h23 = __ldg(bp + 3);
+          const bool p = (l01.x <= ahi[0]) & (alo[0] <= h01.x) & (l01.y <= ahi[1]) & (alo[1] <= h01.y) &
+                         (l23.x <= ahi[2]) & (alo[2] <= h23.x) & (l23.y <= ahi[3]) & (alo[3] <= h23.y);
+          const unsigned m = __ballot_sync(0xffffffffu, p);
+          if (m) {
+            if (p) q[qn + __popc(m & lt_mask)] = make_uint2((uint32_t)ia, (uint32_t)(jb0 + j));
+            qn += __popc(m);
+            __syncwarp();
+            if (qn >= 32) {
+              qn -= 32;
+              flush_queue<KIND>(P, Bt, q + qn, 32, lane, n_pass, n_sing);
+            }
+          }
+        }
       } else {
+        const uint64_t ra = ga0 + 2 * (uint64_t)(lane & 15);  // T¹ record of this lane's A quad
+        const bool va = ra + 1 < P.nA;
+        double alo[4], ahi[4];
         empty_box(alo, ahi);
-      }
-      const int nb = (int)min((uint64_t)GROUP, P.nB - jb0);
-      const unsigned vmask = __ballot_sync(0xffffffffu, va);
-      if (lane == 0) n_tested += (unsigned long long)__popc(vmask) * nb;
-      for (int j = 0; j < nb; ++j) {
-        const double2* bp = reinterpret_cast<const double2*>(P.boxB + jb0 + j);
-        const double2 l01 = __ldg(bp), l23 = __ldg(bp + 1), h01 = __ldg(bp + 2), h23 = __ldg(bp + 3);
-        const bool p = (l01.x <= ahi[0]) & (alo[0] <= h01.x) & (l01.y <= ahi[1]) & (alo[1] <= h01.y) &
-                       (l23.x <= ahi[2]) & (alo[2] <= h23.x) & (l23.y <= ahi[3]) & (alo[3] <= h23.y);
-        const unsigned m = __ballot_sync(0xffffffffu, p);
-        if (m) {
-          if (p) q[qn + __popc(m & lt_mask)] = make_uint2((uint32_t)ia, (uint32_t)(jb0 + j));
-          qn += __popc(m);
-          __syncwarp();
-          if (qn >= 32) {
-            qn -= 32;
-            flush_queue<KIND_TRI>(P, Bt, q + qn, 32, lane, n_pass, n_sing);
+        if (va) {
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const Box bx = P.boxA[ra + u];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) { alo[c] = fmin(alo[c], bx.lo[c]); ahi[c] = fmax(ahi[c], bx.hi[c]); }
+          }
+        }
+        const uint32_t qa = va ? (P.permA ? __ldg(P.permA + ra) >> 1 : (uint32_t)(ra >> 1)) : 0u;
+        for (int jj = 0; jj < (GROUP / 2) / 2; ++jj) {
+          const uint64_t rb = jb0 + 2 * (uint64_t)((lane >> 4) * ((GROUP / 2) / 2) + jj);  // T¹ record of B quad
+          const bool vb = rb + 1 < P.nB;
+          bool p = false;
+          if (vb && va) {
+            double blo[4], bhi[4];
+            empty_box(blo, bhi);
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const Box bx = P.boxB[rb + u];
+#pragma unroll
+              for (int c = 0; c < 4; ++c) { blo[c] = fmin(blo[c], bx.lo[c]); bhi[c] = fmax(bhi[c], bx.hi[c]); }
+            }
+            ++n_tested;
+            p = (blo[0] <= ahi[0]) & (alo[0] <= bhi[0]) & (blo[1] <= ahi[1]) & (alo[1] <= bhi[1]) &
+                (blo[2] <= ahi[2]) & (alo[2] <= bhi[2]) & (blo[3] <= ahi[3]) & (alo[3] <= bhi[3]);
+          }
+          const unsigned m = __ballot_sync(0xffffffffu, p);
+          if (m) {
+            if (p) {
+              const uint32_t qb = P.permB ? __ldg(P.permB + rb) >> 1 : (uint32_t)(rb >> 1);
+              q[qn + __popc(m & lt_mask)] = make_uint2(qa, qb);
+            }
+            qn += __popc(m);
+            __syncwarp();
+            if (qn >= 32) {
+              qn -= 32;
+              flush_queue<KIND>(P, Bt, q + qn, 32, lane, n_pass, n_sing);
+            }
           }
         }
       }
@@ -500,7 +553,7 @@ __global__ void __launch_bounds__(CULL_THREADS) cull_pairs_kernel(const Batch Bt
   }
   if (cur_task != 0xffffffffu) {
     __syncwarp();
-    if (qn > 0) flush_queue<KIND_TRI>(S.P, Bt, q, qn, lane, n_pass, n_sing);
+    if (qn > 0) flush_queue<KIND>(S.P, Bt, q, qn, lane, n_pass, n_sing);
     flush_counters(S.P, lane, n_pass, n_sing, n_tested);
   }
 }
@@ -582,6 +635,7 @@ static int launch_brute(std::vector<SearchParams>& T, const Batch& Bt, std::vect
   }
 }
 
+template <int KIND>
 static int launch_cull(std::vector<SearchParams>& T, Batch Bt, std::vector<uint64_t>& prefix, void* dev_tab,
                        int device, cudaStream_t stream) {
   prefix.assign(T.size() + 1, 0);
@@ -600,7 +654,7 @@ static int launch_cull(std::vector<SearchParams>& T, Batch Bt, std::vector<uint6
   if (g1 > (uint64_t)dev_sms * 16) g1 = (uint64_t)dev_sms * 16;
   cull_blocks_kernel<<<(unsigned)g1, 256, 0, stream>>>(Bt);
   CUDA_TRY(cudaGetLastError());
-  cull_pairs_kernel<<<(unsigned)(dev_sms * 8), CULL_THREADS, 0, stream>>>(Bt);
+  cull_pairs_kernel<KIND><<<(unsigned)(dev_sms * 8), CULL_THREADS, 0, stream>>>(Bt);
   CUDA_TRY(cudaGetLastError());
   return MCX_OK;
 }
@@ -740,7 +794,7 @@ static int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mc
   }
   std::vector<uint64_t> prefix;
   const int rc = o->mode == MCX_MODE_BRUTE ? launch_brute<KIND_TRI>(T, Bt, prefix, ws + L.table, o->device, stream)
-                                           : launch_cull(T, Bt, prefix, ws + L.table, o->device, stream);
+                                           : launch_cull<KIND_TRI>(T, Bt, prefix, ws + L.table, o->device, stream);
   if (rc != MCX_OK) return rc;
   if (o->timing) CUDA_TRY(cudaEventRecord(tm.e1, stream));
   status_kernel<<<1, 32, 0, stream>>>(reinterpret_cast<const SearchParams*>(ws + L.table), n,
@@ -837,6 +891,94 @@ static int launch_pair_candidates(const double* cA, uint32_t NA, uint32_t MA, co
   return MCX_OK;
 }
 
+// SPEC-literal pair_candidates over packed meshes with exact culling (quads = record
+// pairs); same survivor set and counters as launch_pair_candidates.
+static int launch_pair_candidates_mesh(const mcx_mesh_dev* A, const double* cA, uint32_t NA, uint32_t MA,
+                                       const mcx_mesh_dev* B, const double* cB, uint32_t NB, uint32_t MB,
+                                       const mcx_opts* o, uint64_t* gids, uint64_t cap, mcx_stats* st) {
+  if (!A || !B || !cA || !cB || !o || !st) return set_error(MCX_E_ARG, "null argument");
+  if (A->n_tri != 2ull * NA * (MA - 1) || B->n_tri != 2ull * NB * (MB - 1))
+    return set_error(MCX_E_ARG, "mesh record counts do not match the grids");
+  if (!A->gbox || !A->bbox || !B->gbox || !B->tbox) return set_error(MCX_E_ARG, "meshes need level boxes");
+  if (cap > 0 && !gids) return set_error(MCX_E_ARG, "null gid buffer with nonzero capacity");
+  const uint32_t scount = o->shard_count ? o->shard_count : 1;
+  if (o->shard_index >= scount) return set_error(MCX_E_ARG, "shard_index >= shard_count");
+  mcx_opts oc = *o;
+  oc.mode = MCX_MODE_CULL;
+  mcx_task t = {A, B, 0, 0};
+  const WsLayout L = ws_layout(&t, 1, &oc);
+  if (!o->workspace || o->workspace_bytes < L.total || ((uintptr_t)o->workspace & 15))
+    return set_error(MCX_E_ARG, "workspace too small or misaligned (need %llu bytes)", (unsigned long long)L.total);
+  cudaStream_t stream = (cudaStream_t)o->stream;
+  char* ws = (char*)o->workspace;
+  const ShardGeom g = shard_geom(0, A->n_tri, o->shard_index, scount);
+  std::vector<SearchParams> T(1);
+  SearchParams& P = T[0];
+  P = SearchParams{};
+  P.boxA = reinterpret_cast<const Box*>(A->box);
+  P.permA = A->perm;
+  P.boxB = reinterpret_cast<const Box*>(B->box);
+  P.permB = B->perm;
+  P.nA = A->n_tri;
+  P.a_begin = 0;
+  P.a_end = A->n_tri;
+  P.blk_first = g.first;
+  P.my_blocks = g.my_blocks;
+  P.nB = B->n_tri;
+  P.ntilesB = (B->n_tri + TILE - 1) / TILE;
+  P.shard_count = scount;
+  P.counters = reinterpret_cast<unsigned long long*>(ws + L.counters);
+  P.gboxA = reinterpret_cast<const Box*>(A->gbox);
+  P.bboxA = reinterpret_cast<const Box*>(A->bbox);
+  P.gboxB = reinterpret_cast<const Box*>(B->gbox);
+  P.tboxB = reinterpret_cast<const Box*>(B->tbox);
+  P.statusA = A->status;
+  P.statusB = B->status;
+  P.coordsA = cA;
+  P.coordsB = cB;
+  P.NA = NA; P.MA = MA; P.NB = NB; P.MB = MB;
+  *st = mcx_stats{};
+  st->n_pairs = (g.na / 2) * (B->n_tri / 2);  // quad pairs
+  CUDA_TRY(cudaMemsetAsync(ws, 0, L.counters + 64, stream));
+  Batch Bt = {};
+  Bt.n_tasks = 1;
+  Bt.gids = gids;
+  Bt.cap = cap;
+  Bt.emit = reinterpret_cast<unsigned long long*>(ws);
+  Bt.list_count = reinterpret_cast<unsigned long long*>(ws) + 1;
+  Bt.blk_list = reinterpret_cast<uint4*>(ws + L.list);
+  Bt.blk_cap = L.list_cap;
+  Timing tm;
+  if (o->timing) {
+    CUDA_TRY(cudaEventCreate(&tm.e0));
+    CUDA_TRY(cudaEventCreate(&tm.e1));
+    CUDA_TRY(cudaEventRecord(tm.e0, stream));
+  }
+  std::vector<uint64_t> prefix;
+  const int rc = launch_cull<KIND_QUAD>(T, Bt, prefix, ws + L.table, o->device, stream);
+  if (rc != MCX_OK) return rc;
+  if (o->timing) CUDA_TRY(cudaEventRecord(tm.e1, stream));
+  status_kernel<<<1, 32, 0, stream>>>(reinterpret_cast<const SearchParams*>(ws + L.table), 1,
+                                      reinterpret_cast<unsigned long long*>(ws) + 2);
+  CUDA_TRY(cudaGetLastError());
+  unsigned long long h[16];
+  CUDA_TRY(cudaMemcpyAsync(h, ws, sizeof(h), cudaMemcpyDeviceToHost, stream));
+  CUDA_TRY(cudaStreamSynchronize(stream));
+  const unsigned long long* c = h + 8;
+  st->n_hits = c[0];
+  st->n_aabb_pass = c[1];
+  st->n_singular = c[2];  // Moller-rejected quad pairs
+  st->n_tested = c[3];
+  if (o->timing) {
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, tm.e0, tm.e1));
+    st->kernel_ms = ms;
+  }
+  if (h[2]) return set_error(MCX_E_ARG, "non-finite (NaN/Inf) coordinates in an input mesh (mcx_pack status)");
+  if (c[0] > cap) return set_error(MCX_E_CAPACITY, "candidate capacity %llu < %llu", (unsigned long long)cap, c[0]);
+  return MCX_OK;
+}
+
 thread_local char g_err[512] = "";
 
 }  // namespace mcx
@@ -880,6 +1022,23 @@ int mcx_pair_candidates(const double* coords_a, uint32_t NA, uint32_t MA, const 
   CUDA_TRY(cudaSetDevice(device));
   return launch_pair_candidates(coords_a, NA, MA, coords_b, NB, MB, device, (cudaStream_t)stream, workspace,
                                 workspace_bytes, gids, cap, n_out);
+}
+
+int mcx_pair_candidates_mesh(const mcx_mesh_dev* A, const double* coords_a, uint32_t NA, uint32_t MA,
+                             const mcx_mesh_dev* B, const double* coords_b, uint32_t NB, uint32_t MB,
+                             const mcx_opts* opts, uint64_t* gids, uint64_t cap, mcx_stats* stats) {
+  using namespace mcx;
+  if (!opts) return set_error(MCX_E_ARG, "null options");
+  CUDA_TRY(cudaSetDevice(opts->device));
+  return launch_pair_candidates_mesh(A, coords_a, NA, MA, B, coords_b, NB, MB, opts, gids, cap, stats);
+}
+
+uint64_t mcx_pair_candidates_mesh_workspace_bytes(const mcx_mesh_dev* A, const mcx_mesh_dev* B, const mcx_opts* o) {
+  if (!A || !B || !o) return 0;
+  mcx_opts oc = *o;
+  oc.mode = MCX_MODE_CULL;
+  mcx_task t = {A, B, 0, 0};
+  return mcx::ws_layout(&t, 1, &oc).total;
 }
 
 const char* mcx_last_error(void) { return mcx::g_err; }

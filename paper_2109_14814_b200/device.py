@@ -382,6 +382,36 @@ def record_fields_device(coords_a, s_a, coords_b, s_b, hits: np.ndarray, device:
     return gid.cpu().numpy().view(np.uint64), pts.cpu().numpy(), par.cpu().numpy()
 
 
+def pair_candidates_mesh(A: DeviceMesh, B: DeviceMesh, *, shard=(0, 1), cap: int = 1 << 16, stream=None,
+                         task=None, timing: bool = False):
+    """SPEC-literal quad-pair candidates from packed meshes with exact culling
+    (mcx_pair_candidates_mesh).  Returns (sorted u64 gids, stats)."""
+    t = torch()
+    if A.device != B.device:
+        raise ConfigError("A and B must live on the same device")
+    L = _lib.load()
+    s = stream or t.cuda.current_stream(A.device)
+    W = _Workspace.get(A.device)
+    opts = _lib.Opts(A.device, s.cuda_stream, 0, 0, int(shard[0]), int(shard[1]), _lib.MODE_CULL, int(timing),
+                     None, 0)
+    As, Bs = A.struct(), B.struct()
+    ws = W.workspace(L.mcx_pair_candidates_mesh_workspace_bytes(As, Bs, opts))
+    opts.workspace, opts.workspace_bytes = ws.data_ptr(), ws.numel()
+    st = _lib.Stats()
+    dev = t.device("cuda", A.device)
+    for _ in range(3):
+        gids = t.empty(max(cap, 1), dtype=t.int64, device=dev)
+        rc = L.mcx_pair_candidates_mesh(As, A.coords.data_ptr(), A.N, A.M, Bs, B.coords.data_ptr(), B.N, B.M, opts,
+                                        gids.data_ptr(), cap, st)
+        if rc == _lib.MCX_E_CAPACITY:
+            cap = int(st.n_hits) + 1024
+            continue
+        _lib.check(rc, "mcx_pair_candidates_mesh", task=task)
+        break
+    n = int(st.n_hits)
+    return np.sort(gids[:n].cpu().numpy().view(np.uint64)), st.as_dict()
+
+
 def ctypes_u64():
     import ctypes
     return ctypes.c_uint64(0)

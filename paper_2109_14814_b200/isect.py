@@ -153,11 +153,22 @@ def search_hits(u_half, s_half, backend: str = "cuda", *, devices=(0,), mode: st
                           task=_task(u_half, s_half))
 
 
-def pair_candidates(u_half, s_half, backend: str = "cuda", *, device: int = 0) -> np.ndarray:
-    """Sorted u64 gids with ¬aabb_reject ∧ ¬moller_reject."""
+def pair_candidates(u_half, s_half, backend: str = "cuda", *, device: int = 0, mode: str = "cull") -> np.ndarray:
+    """Sorted u64 gids with ¬aabb_reject ∧ ¬moller_reject.
+
+    ``mode="cull"`` (default) runs the quad tests only inside overlapping union boxes
+    of the packed meshes; ``"brute"`` tests every quad pair.  Same result.
+    """
     _check_backend(backend)
-    return _device.pair_candidates_device(_coords(u_half), _coords(s_half), device=device,
-                                          task=_task(u_half, s_half))
+    if mode == "brute":
+        return _device.pair_candidates_device(_coords(u_half), _coords(s_half), device=device,
+                                              task=_task(u_half, s_half))
+    if mode != "cull":
+        raise ConfigError(f"mode must be 'brute' or 'cull', got {mode!r}")
+    A = _device.DeviceMesh(_coords(u_half), device)
+    B = _device.DeviceMesh(_coords(s_half), device)
+    gids, _ = _device.pair_candidates_mesh(A, B, task=_task(u_half, s_half))
+    return gids
 
 
 def record_fields(coords_a, s_a, coords_b, s_b, hits):

@@ -242,19 +242,36 @@ def test_find_intersections_records(oracle_lib):
     assert [r.to_line() for r in recs] == [w.to_line() for w in want]
 
 
-@pytest.mark.parametrize("name", ["C1", "C4i"])
-def test_pair_candidates_spec_literal(name):
+@pytest.mark.parametrize("mode", ["brute", "cull"])
+@pytest.mark.parametrize("name", ["C1", "C4i", "C4iii", "C5/8"])
+def test_pair_candidates_spec_literal(name, mode):
     A, _, B, _ = config_pair(name)
     want, _ = S.pair_candidates(A, B)
-    got = isect.pair_candidates(A, B)
+    got = isect.pair_candidates(A, B, mode=mode)
     assert np.array_equal(got, want.astype(np.uint64))
 
 
-def test_pair_candidates_small_exhaustive():
+@pytest.mark.parametrize("mode", ["brute", "cull"])
+def test_pair_candidates_small_exhaustive(mode):
     A, _ = manifold_like(16, 5, 11)
     B = A + np.array([0.0, 0.0, 0.02, 0.0])[:, None, None]
     want, _ = S.pair_candidates(A, B)
-    assert np.array_equal(isect.pair_candidates(A, B), want.astype(np.uint64))
+    assert np.array_equal(isect.pair_candidates(A, B, mode=mode), want.astype(np.uint64))
+
+
+def test_pair_candidates_mesh_counters_and_shards():
+    A, _, B, _ = config_pair("C4i")
+    want, n_pass = S.pair_candidates(A, B)
+    Am, Bm = D.DeviceMesh(A, 0), D.DeviceMesh(B, 0)
+    gids, st = D.pair_candidates_mesh(Am, Bm)
+    assert np.array_equal(gids, want.astype(np.uint64))
+    assert st["n_aabb_pass"] == n_pass and st["n_hits"] == len(want)
+    assert st["n_pairs"] == (Am.n_tri // 2) * (Bm.n_tri // 2) and st["n_tested"] < st["n_pairs"]
+    parts = [D.pair_candidates_mesh(Am, Bm, shard=(g, 3))[0] for g in range(3)]
+    assert np.array_equal(np.sort(np.concatenate(parts)), gids)
+    nat = D.pair_candidates_mesh(D.DeviceMesh(A, 0, order=_lib.ORDER_NATURAL),
+                                 D.DeviceMesh(B, 0, order=_lib.ORDER_NATURAL))[0]
+    assert np.array_equal(nat, gids)
 
 
 @pytest.mark.parametrize("mode", MODES)
