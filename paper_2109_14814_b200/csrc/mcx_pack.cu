@@ -149,7 +149,7 @@ int mcx_pack(const double* coords, uint32_t N, uint32_t M, int order, double* bo
              uint32_t* status, int device, void* stream) {
   using namespace mcx;
   if (N < 1 || M < 2) return set_error(MCX_E_ARG, "pack needs N >= 1 and M >= 2 (got N=%u, M=%u)", N, M);
-  if (2ull * N * (M - 1) >= (1ull << 32)) return set_error(MCX_E_ARG, "triangle count must be < 2^32");
+  if (2ull * N * (M - 1) >= (1ull << 31)) return set_error(MCX_E_ARG, "triangle count must be < 2^31");
   if (order != MCX_ORDER_NATURAL && order != MCX_ORDER_TILED) return set_error(MCX_E_ARG, "unknown order %d", order);
   if (!coords || !box || !geo) return set_error(MCX_E_ARG, "null buffer");
   if (((uintptr_t)box | (uintptr_t)geo) & 15) return set_error(MCX_E_ARG, "box/geo must be 16-byte aligned");

@@ -741,8 +741,8 @@ static int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mc
     if (a_end > A->n_tri || a_begin > a_end)
       return set_error(MCX_E_ARG, "task %u: A range [%llu, %llu) outside [0, %llu)", t, (unsigned long long)a_begin,
                        (unsigned long long)a_end, (unsigned long long)A->n_tri);
-    if (A->n_tri >= (1ull << 32) || B->n_tri >= (1ull << 32))
-      return set_error(MCX_E_ARG, "task %u: triangle counts must be < 2^32", t);
+    if (A->n_tri >= (1ull << 31) || B->n_tri >= (1ull << 31))
+      return set_error(MCX_E_ARG, "task %u: triangle counts must be < 2^31", t);
     if (!A->box || !B->box || !A->geo || !B->geo) return set_error(MCX_E_ARG, "task %u: null box/geo", t);
     if (((uintptr_t)A->box | (uintptr_t)B->box | (uintptr_t)A->geo | (uintptr_t)B->geo) & 15)
       return set_error(MCX_E_ARG, "task %u: box/geo pointers must be 16-byte aligned", t);
@@ -847,7 +847,7 @@ static int launch_pair_candidates(const double* cA, uint32_t NA, uint32_t MA, co
                                   uint64_t* gids, uint64_t cap, uint64_t* n_out) {
   if (NA < 1 || NB < 1 || MA < 2 || MB < 2) return set_error(MCX_E_ARG, "half-layers need >= 2 columns");
   const uint64_t nqA = (uint64_t)NA * (MA - 1), nqB = (uint64_t)NB * (MB - 1);
-  if (nqA >= (1ull << 32) || nqB >= (1ull << 32)) return set_error(MCX_E_ARG, "quad counts must be < 2^32");
+  if (nqA >= (1ull << 31) || nqB >= (1ull << 31)) return set_error(MCX_E_ARG, "quad counts must be < 2^31");
   const uint64_t need = PC_HEADER + (nqA + nqB) * sizeof(Box);
   if (!ws || ws_bytes < need || ((uintptr_t)ws & 15))
     return set_error(MCX_E_ARG, "workspace too small or misaligned (need %llu bytes)", (unsigned long long)need);

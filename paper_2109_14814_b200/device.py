@@ -78,8 +78,8 @@ class DeviceMesh:
         self.device = device
         _, self.M, self.N = (int(v) for v in self.coords.shape)
         self.n_tri = 2 * self.N * (self.M - 1)
-        if self.n_tri >= 2 ** 32:
-            raise ConfigError("triangle count must be < 2^32")
+        if self.n_tri >= 2 ** 31:
+            raise ConfigError("triangle count must be < 2^31")
         n = self.n_tri
         self.order = order
         with t.cuda.device(device), t.cuda.stream(s):
