@@ -409,3 +409,30 @@ def test_c_host_example():
     assert brute[2] == brute[1] and int(cull[2]) < int(cull[1])  # executed tests
     assert brute[3:7] == cull[3:7]                  # aabb pass, singular, hits, checksum
     assert int(brute[5]) > 0
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("case", ["cross5", "cross6", "adversarial"])
+def test_acceptance6_exact_oracle(case, mode):
+    """SPEC acceptance 6: on synthetic meshes of (N1, N2, M1, M2) = (32, 32, 9, 9) the hit set
+    equals a brute-force all-pairs EXACT (fractions) precise-test oracle.  Dyadic lattice
+    inputs make the exact answer well defined at touching configurations."""
+    from oracle import exact as X
+    from paper_2109_14814_b200.mesh import dyadic, stress_pair
+    if case == "adversarial":
+        A, B, _ = stress_pair("dyadic", N=32, M=9, seed=4)
+    else:
+        seed = int(case[-1])
+        A = dyadic(manifold_like(32, 9, seed)[0])
+        B = dyadic(manifold_like(32, 9, seed + 10)[0])
+    pA, pB = O.pack(A), O.pack(B)
+    ov = O.aabb_overlap(pA["lo"][:, None], pA["hi"][:, None], pB["lo"][None], pB["hi"][None])
+    want = set()
+    for a, b in zip(*np.nonzero(ov)):
+        sol = X.solve_exact(pA["p"][a], pA["e1"][a], pA["e2"][a], pB["p"][b], pB["e1"][b], pB["e2"][b])
+        if X.accepted(sol):
+            want.add((int(a), int(b)))
+    r = D.search(A, B, mode=mode)
+    got = set(zip(r.hits["ia"].tolist(), r.hits["ib"].tolist()))
+    assert got == want
+    assert r.stats["n_aabb_pass"] == int(ov.sum())

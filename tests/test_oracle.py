@@ -266,3 +266,36 @@ def test_rejection_soundness_random():
                 sol = X.solve_exact(pa["p"][ta], pa["e1"][ta], pa["e2"][ta], pb["p"][tb], pb["e1"][tb], pb["e2"][tb])
                 bad += X.accepted(sol)
     assert bad == 0
+
+
+def test_rejection_soundness_million_pairs():
+    """SPEC acceptance 6: 0 soundness violations over 1e6 randomized quad pairs — no pair
+    rejected by quad AABB or Möller has an intersecting triangle pair.  Coordinates are
+    on a coarse dyadic lattice, where the canonical solve is exact (see
+    test_golden_c4ii_exact_decisions), so the check is an exact one."""
+    rng = np.random.default_rng(2026)
+    n = 1_000_000
+    rejected_total = checked = 0
+    for c0 in range(0, n, 200_000):
+        m = 200_000
+        base = rng.integers(-8, 9, (2, m, 1, 4)).astype(float) / 8.0
+        VA = base[0] + rng.integers(-2, 3, (m, 4, 4)) / 16.0
+        VB = base[1] + rng.integers(-2, 3, (m, 4, 4)) / 16.0
+        loA, hiA = S.quad_boxes(VA)
+        loB, hiB = S.quad_boxes(VB)
+        rej = (~O.aabb_overlap(loA, hiA, loB, hiB)) | S.moller_reject_quads(VA, VB)
+        rejected_total += int(rej.sum())
+        idx = np.nonzero(rej)[0]
+        for ta, (o, u, w) in enumerate(((0, 1, 2), (2, 1, 3))):
+            for tb, (o2, u2, w2) in enumerate(((0, 1, 2), (2, 1, 3))):
+                def tri(V, oo, uu, ww):
+                    p = V[idx, oo] + 0.0
+                    e1, e2 = V[idx, uu] - p, V[idx, ww] - p
+                    P = np.stack([e1[:, i] * e2[:, j] - e1[:, j] * e2[:, i] for i, j in O.BIV], axis=1)
+                    n1 = ((e1[:, 0] * e1[:, 0] + e1[:, 1] * e1[:, 1]) + e1[:, 2] * e1[:, 2]) + e1[:, 3] * e1[:, 3]
+                    n2 = ((e2[:, 0] * e2[:, 0] + e2[:, 1] * e2[:, 1]) + e2[:, 2] * e2[:, 2]) + e2[:, 3] * e2[:, 3]
+                    return {"p": p, "e1": e1, "e2": e2, "P": P, "nrm": np.sqrt(n1) * np.sqrt(n2)}
+                *_, hit = O.solve_pairs(tri(VA, o, u, w), tri(VB, o2, u2, w2))
+                assert not hit.any(), f"{int(hit.sum())} rejected pairs intersect (T{ta + 1}, T{tb + 1})"
+                checked += idx.size
+    assert rejected_total > 0.5 * n and checked == 4 * rejected_total
