@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_brute_kernel(const
         }
       }
     };
-    if constexpr (C::PF) {
+    if constexpr (C::PF == 1) {
       // software-pipelined: the LDS of box j+1 is issued before the compares of box j
       const double2* bp0 = reinterpret_cast<const double2*>(tile);
       double2 n01 = bp0[0], n23 = bp0[1], m01 = bp0[2], m23 = bp0[3];
