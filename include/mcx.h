@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define MCX_ABI_VERSION 1
+#define MCX_ABI_VERSION 2
 
 #define MCX_OK 0
 #define MCX_E_CAPACITY 1
@@ -48,6 +48,9 @@ extern "C" {
 /* Search modes. */
 #define MCX_MODE_BRUTE 0 /* every (iA, iB) pair gets the 8-compare AABB test       */
 #define MCX_MODE_CULL 1  /* exact block-AABB culling first; identical hit set      */
+#define MCX_MODE_PREFILTER 2 /* every pair tested, first by a conservative 8-byte
+                                quantised-box integer test (fma + alu pipes), the
+                                rare passes by the exact FP64 test; identical hit set */
 
 /* Storage orders of the packed triangle records (mcx_pack). */
 #define MCX_ORDER_NATURAL 0 /* record t at position t = 2·(i + N·k) + τ               */
@@ -87,6 +90,8 @@ typedef struct mcx_stats {
   uint64_t n_singular;  /* solved pairs rejected by the singular gate */
   uint64_t n_hits;      /* accepted pairs (may exceed the hit capacity)            */
   double kernel_ms;     /* device time of the search kernels (CUDA events)         */
+  uint64_t n_exact_tests; /* exact FP64 box tests run (MCX_MODE_PREFILTER: pairs the
+                             quantised test passed; otherwise == n_tested)           */
 } mcx_stats;
 
 typedef struct mcx_opts {
@@ -96,7 +101,7 @@ typedef struct mcx_opts {
   uint64_t a_end;
   uint32_t shard_index;  /* cyclic sharding of the absolute A blocks [1024 b, 1024 b +  */
   uint32_t shard_count;  /*   1024): this call takes b % count == index; 0 → 1        */
-  int mode;              /* MCX_MODE_BRUTE or MCX_MODE_CULL                           */
+  int mode;              /* MCX_MODE_BRUTE, MCX_MODE_CULL or MCX_MODE_PREFILTER       */
   int timing;            /* nonzero: record CUDA events and fill stats->kernel_ms    */
   void* workspace;       /* device scratch, >= mcx_workspace_bytes() bytes           */
   uint64_t workspace_bytes;

@@ -15,8 +15,10 @@ from .errors import BackendError, CapacityError
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libmcx.so")
 
+ABI_VERSION = 2  # include/mcx.h MCX_ABI_VERSION
 MCX_OK, MCX_E_CAPACITY, MCX_E_CUDA, MCX_E_ARG = 0, 1, 2, 3
-MODE_BRUTE, MODE_CULL = 0, 1
+MODE_BRUTE, MODE_CULL, MODE_PREFILTER = 0, 1, 2
+MODE_NAMES = {"brute": MODE_BRUTE, "cull": MODE_CULL, "prefilter": MODE_PREFILTER}
 ORDER_NATURAL, ORDER_TILED = 0, 1
 BOX_STRIDE, GEO_STRIDE = 8, 20
 GROUP, TILE, BLOCK = 32, 512, 1024
@@ -44,7 +46,8 @@ class Hit(ctypes.Structure):
 
 class Stats(ctypes.Structure):
     _fields_ = [("n_pairs", ctypes.c_uint64), ("n_tested", ctypes.c_uint64), ("n_aabb_pass", ctypes.c_uint64),
-                ("n_singular", ctypes.c_uint64), ("n_hits", ctypes.c_uint64), ("kernel_ms", ctypes.c_double)]
+                ("n_singular", ctypes.c_uint64), ("n_hits", ctypes.c_uint64), ("kernel_ms", ctypes.c_double),
+                ("n_exact_tests", ctypes.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -102,6 +105,8 @@ def load():
     L.mcx_last_error.argtypes = []
     L.mcx_version.restype = i32
     L.mcx_version.argtypes = []
+    if L.mcx_version() != ABI_VERSION:
+        raise BackendError(f"{LIB_PATH} has ABI version {L.mcx_version()}, expected {ABI_VERSION}: rebuild it")
     _lib = L
     return L
 

@@ -5,7 +5,7 @@ flags and files:
 
     python -m paper_2109_14814_b200.cli layers --umesh U.mnf --smesh S.mnf --nmax N --plan plan.txt
     python -m paper_2109_14814_b200.cli intersect --umesh U.mnf --smesh S.mnf --plan plan.txt \
-        --backend cuda --out records.txt [--mode cull|brute]
+        --backend cuda --out records.txt [--mode cull|brute|prefilter]
 
 Meshes are MNF1 files, the plan is ``n1 sign1 n2 sign2 tof`` per
 line, records are ``n1 sign1 n2 sign2 gid x y px py a b c d theta_u
@@ -36,7 +36,7 @@ def _parser():
     it.add_argument("--smesh", required=True)
     it.add_argument("--plan", required=True)
     it.add_argument("--backend", default="cuda")
-    it.add_argument("--mode", default="cull", choices=["cull", "brute"])
+    it.add_argument("--mode", default="cull", choices=["cull", "brute", "prefilter"])
     it.add_argument("--device", type=int, default=0)
     it.add_argument("--out", required=True)
     it.add_argument("--manifest", default=None, help="optional JSON with per-layer-pair counters")

@@ -37,6 +37,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <algorithm>
 #include <type_traits>
 #include <vector>
 
@@ -91,6 +92,10 @@ struct __align__(16) SearchParams {
   const double* coordsA;
   const double* coordsB;
   uint32_t NA, MA, NB, MB;
+  // MCX_MODE_PREFILTER only: 8-byte quantised boxes (storage order) and the task's frame
+  uint2* qA;
+  uint2* qB;
+  long long* qframe;  // [8] ordered keys: min lo[4], max hi[4] over both meshes
 };
 
 // Whole-launch parameters: the task table and the shared outputs.
@@ -106,6 +111,7 @@ struct Batch {
   uint4* blk_list;               // cull: overlapping (task, local A block, B tile)
   uint64_t blk_cap;
   unsigned long long* list_count;
+  uint32_t neg1;                 // 0xffffffff, a runtime operand so the SWAR subtract stays an IMAD
 };
 
 // Task owning work unit u: the last t with prefix[t] <= u (n_tasks is small).
@@ -369,6 +375,260 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_brute_kernel(const
   __syncwarp();
   if (qn > 0) flush_queue<KIND>(P, Bt, q, qn, lane, n_pass, n_sing);
   flush_counters(P, lane, n_pass, n_sing, 0);
+}
+
+// ------------------------------------------------------------ prefilter mode
+// MCX_MODE_PREFILTER: every pair is tested, but first by a conservative integer
+// test on 8-byte quantised boxes that runs on the fma + alu pipes instead of the
+// FP64 pipe; only pairs it cannot reject get the exact FP64 box test (and then
+// the canonical solve), so the AABB-pass / singular / hit sets are exactly those
+// of MCX_MODE_BRUTE.
+//
+// Quantisation (per task, one frame for both meshes): for coordinate c,
+// f_c(x) = (x − o_c)·κ_c with o_c = min lo_c, κ_c = 127 / (max hi_c − o_c), both in
+// RN double arithmetic, so f_c is monotone non-decreasing; qlo = clamp(⌊f(lo)⌋),
+// qhi = clamp(⌈f(hi)⌉) to [0, 127].  Then A.lo_c ≤ B.hi_c ⇒ qloA_c ≤ qhiB_c (and
+// likewise for the other 7 compares): the quantised test never rejects a pair the
+// exact test keeps, whatever the frame (a degenerate frame gives κ = 0, q = 0: no
+// rejection).  Record layout ("L form", 2 words of 4 bytes, byte c = coordinate c):
+// word0 = qlo_c, word1 = 127 − qhi_c.  An A record is turned into the "H form"
+// H0 = (0x7F7F7F7F − word1) | G, H1 = (0x7F7F7F7F − word0) | G, G = 0x80808080;
+// then byte c of H0 − L_B0 is 128 + qhiA_c − qloB_c ∈ [1, 255] (no borrow between
+// bytes) and has its guard bit set iff qloB_c ≤ qhiA_c, and H1 − L_B1 likewise
+// tests qloA_c ≤ qhiB_c.  A pair passes iff all 8 guard bits of the two
+// differences are set: 2 IMAD (fma pipe) + 1 LOP3 + 1 ISETP (alu) per pair instead
+// of 8 DSETP on the 64-lane/clk FP64 pipe.
+constexpr int QR = 16;                   // A records per thread
+constexpr int Q_THREADS = A_BLOCK / QR;  // 64 threads = 2 warps, 512 A records per warp
+constexpr int Q_WARPS = Q_THREADS / 32;
+constexpr int QTILE = 1024;              // B records per shared-memory stage (8 KB)
+constexpr int Q_QCAP = 64;
+constexpr unsigned QG = 0x80808080u;
+constexpr unsigned Q7F = 0x7F7F7F7Fu;
+
+struct __align__(16) QSmem {
+  uint2 tile[STAGES][QTILE];
+  uint2 queue[Q_WARPS][Q_QCAP];
+  unsigned long long full[STAGES];
+};
+
+// Order-preserving map of finite doubles onto signed 64-bit keys (for atomicMin/Max).
+__device__ __forceinline__ long long okey(double x) {
+  const long long b = __double_as_longlong(x);
+  return b >= 0 ? b : b ^ 0x7fffffffffffffffll;
+}
+__device__ __forceinline__ double okey_inv(long long k) {
+  return __longlong_as_double(k >= 0 ? k : k ^ 0x7fffffffffffffffll);
+}
+
+// a − b computed as b·(−1) + a on the fma pipe (m1 = 0xffffffff at run time).
+__device__ __forceinline__ unsigned imad_sub(unsigned a, unsigned m1, unsigned b) {
+  unsigned r;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(b), "r"(m1), "r"(a));
+  return r;
+}
+
+__device__ __forceinline__ uint2 ld_nc_u2(const uint2* p) {
+  uint2 v;
+  asm volatile("ld.global.nc.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  return v;
+}
+
+__global__ void qframe_init_kernel(const Batch Bt) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= Bt.n_tasks) return;
+  long long* f = Bt.tasks[t].qframe;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    f[c] = 0x7fffffffffffffffll;
+    f[4 + c] = (long long)0x8000000000000000ull;
+  }
+}
+
+// Union box of A and B per task (blockIdx.y = task): warp min/max, 8 atomics per warp.
+__global__ void __launch_bounds__(256) qbounds_kernel(const Batch Bt) {
+  const SearchParams& P = Bt.tasks[blockIdx.y];
+  const Box* boxA = P.boxA;
+  const Box* boxB = P.boxB;
+  const uint64_t nA = P.nA, n = nA + P.nB;
+  double lo[4], hi[4];
+  empty_box(lo, hi);
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x) {
+    const double2* b = reinterpret_cast<const double2*>(k < nA ? boxA + k : boxB + (k - nA));
+    const double2 l01 = __ldg(b), l23 = __ldg(b + 1), h01 = __ldg(b + 2), h23 = __ldg(b + 3);
+    lo[0] = fmin(lo[0], l01.x); lo[1] = fmin(lo[1], l01.y); lo[2] = fmin(lo[2], l23.x); lo[3] = fmin(lo[3], l23.y);
+    hi[0] = fmax(hi[0], h01.x); hi[1] = fmax(hi[1], h01.y); hi[2] = fmax(hi[2], h23.x); hi[3] = fmax(hi[3], h23.y);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      lo[c] = fmin(lo[c], __shfl_xor_sync(0xffffffffu, lo[c], o));
+      hi[c] = fmax(hi[c], __shfl_xor_sync(0xffffffffu, hi[c], o));
+    }
+  if ((threadIdx.x & 31) == 0 && lo[0] <= hi[0]) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      atomicMin(P.qframe + c, okey(lo[c]));
+      atomicMax(P.qframe + 4 + c, okey(hi[c]));
+    }
+  }
+}
+
+// Quantised L-form records of A and B per task (blockIdx.y = task).
+__global__ void __launch_bounds__(256) quant_kernel(const Batch Bt) {
+  const SearchParams& P = Bt.tasks[blockIdx.y];
+  double o[4], kap[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    o[c] = okey_inv(P.qframe[c]);
+    const double e = __dsub_rn(okey_inv(P.qframe[4 + c]), o[c]);
+    double k = (e > 0.0) ? __ddiv_rn(127.0, e) : 0.0;  // e NaN/inf/<=0 → no quantisation
+    if (!(k < 1.0e300)) k = 0.0;
+    kap[c] = k;
+  }
+  const Box* boxA = P.boxA;
+  const Box* boxB = P.boxB;
+  const uint64_t nA = P.nA, n = nA + P.nB;
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x) {
+    const double* b = reinterpret_cast<const double*>(k < nA ? boxA + k : boxB + (k - nA));
+    unsigned w0 = 0, w1 = 0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      unsigned ql = 0, qh = 0;
+      if (kap[c] > 0.0) {
+        const double fl = floor(__dmul_rn(__dsub_rn(__ldg(b + c), o[c]), kap[c]));
+        const double fh = ceil(__dmul_rn(__dsub_rn(__ldg(b + 4 + c), o[c]), kap[c]));
+        ql = (unsigned)fmin(fmax(fl, 0.0), 127.0);
+        qh = (unsigned)fmin(fmax(fh, 0.0), 127.0);
+      }
+      w0 |= ql << (8 * c);
+      w1 |= (127u - qh) << (8 * c);
+    }
+    if (k < nA) P.qA[k] = make_uint2(w0, w1);
+    else P.qB[k - nA] = make_uint2(w0, w1);
+  }
+}
+
+template <int UNROLL>
+__global__ void __launch_bounds__(Q_THREADS) search_prefilter_kernel(const Batch Bt) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  QSmem& S = *reinterpret_cast<QSmem*>(smem_raw);
+  __shared__ SearchParams Ps;
+  __shared__ uint64_t s_unit;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    const uint32_t t = find_task(Bt, blockIdx.x);
+    Ps = Bt.tasks[t];
+    s_unit = blockIdx.x - Bt.prefix[t];
+  }
+  __syncthreads();
+  const SearchParams& P = Ps;
+  const uint64_t unit = s_unit;
+  const uint64_t gblk = P.blk_first + (unit / P.nchunk) * P.shard_count;
+  const uint64_t a0 = gblk * A_BLOCK;
+  const uint64_t b0 = (unit % P.nchunk) * P.b_chunk;
+  const uint64_t b1 = min(b0 + P.b_chunk, P.nB);
+  const int ntiles = (int)((b1 - b0 + QTILE - 1) / QTILE);
+  const unsigned m1 = Bt.neg1;
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&S.full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int s = 0; s < STAGES && s < ntiles; ++s) {
+      const uint64_t tb = b0 + (uint64_t)s * QTILE;
+      const uint32_t bytes = (uint32_t)((min((uint64_t)QTILE, b1 - tb) * sizeof(uint2) + 15) & ~15ull);
+      mbar_arrive_expect_tx(&S.full[s], bytes);
+      bulk_g2s(&S.tile[s][0], P.qB + tb, bytes, &S.full[s]);
+    }
+  }
+
+  // A records of this thread: warp w covers the 512 storage positions a0 + 512 w + [0, 512)
+  const uint32_t abase = (uint32_t)(a0 + (uint64_t)warp * (QR * 32) + lane);
+  unsigned h0[QR], h1[QR];
+  auto load_a = [&]() {
+#pragma unroll
+    for (int r = 0; r < QR; ++r) {
+      const uint32_t ia = abase + r * 32;
+      if (ia >= P.a_begin && ia < P.a_end) {
+        const uint2 l = ld_nc_u2(P.qA + ia);
+        h0[r] = (Q7F - l.y) | QG;
+        h1[r] = (Q7F - l.x) | QG;
+      } else {
+        h0[r] = Q7F;  // guard bits clear in every byte of H0 − L_B0: never passes
+        h1[r] = Q7F;
+      }
+    }
+  };
+  load_a();
+
+  uint2* q = S.queue[warp];
+  int qn = 0;
+  unsigned long long n_pass = 0, n_sing = 0, n_exact = 0;
+  const unsigned lt_mask = (1u << lane) - 1u;
+
+  for (int t = 0; t < ntiles; ++t) {
+    const int s = t % STAGES;
+    mbar_wait(&S.full[s], (uint32_t)((t / STAGES) & 1));
+    const uint64_t tb = b0 + (uint64_t)t * QTILE;
+    const int nvalid = (int)min((uint64_t)QTILE, b1 - tb);
+    const uint2* tile = S.tile[s];
+#pragma unroll(UNROLL)
+    for (int j = 0; j < nvalid; ++j) {
+      const uint2 bq = tile[j];
+      bool any = false;
+#pragma unroll
+      for (int r = 0; r < QR; ++r) {
+        const unsigned x0 = imad_sub(h0[r], m1, bq.x), x1 = imad_sub(h1[r], m1, bq.y);
+        any |= ((x0 & x1 & QG) == QG);
+      }
+      if (__any_sync(0xffffffffu, any)) {
+        // rare: exact FP64 box test for every quantised pass of this B record, from L1/L2
+        const uint32_t ib = (uint32_t)(tb + j);
+        const double2* bp = reinterpret_cast<const double2*>(P.boxB + ib);
+        const double2 l01 = __ldg(bp), l23 = __ldg(bp + 1), g01 = __ldg(bp + 2), g23 = __ldg(bp + 3);
+        for (int r = 0; r < QR; ++r) {
+          const uint32_t ia = abase + r * 32;
+          bool p = false;
+          if (ia >= P.a_begin && ia < P.a_end) {
+            const uint2 l = ld_nc_u2(P.qA + ia);
+            const unsigned x0 = imad_sub((Q7F - l.y) | QG, m1, bq.x), x1 = imad_sub((Q7F - l.x) | QG, m1, bq.y);
+            if ((x0 & x1 & QG) == QG) {
+              ++n_exact;
+              const double2* ap = reinterpret_cast<const double2*>(P.boxA + ia);
+              const double2 a01 = __ldg(ap), a23 = __ldg(ap + 1), c01 = __ldg(ap + 2), c23 = __ldg(ap + 3);
+              p = (l01.x <= c01.x) & (a01.x <= g01.x) & (l01.y <= c01.y) & (a01.y <= g01.y) &
+                  (l23.x <= c23.x) & (a23.x <= g23.x) & (l23.y <= c23.y) & (a23.y <= g23.y);
+            }
+          }
+          const unsigned m = __ballot_sync(0xffffffffu, p);
+          if (m) {
+            if (p) q[qn + __popc(m & lt_mask)] = make_uint2(ia, ib);
+            qn += __popc(m);
+            __syncwarp();
+            if (qn >= 32) {
+              qn -= 32;
+              flush_queue<KIND_TRI>(P, Bt, q + qn, 32, lane, n_pass, n_sing);
+            }
+          }
+        }
+        load_a();
+      }
+    }
+    __syncthreads();  // every warp is done reading stage s
+    if (tid == 0 && t + STAGES < ntiles) {
+      const uint64_t nb = b0 + (uint64_t)(t + STAGES) * QTILE;
+      const uint32_t bytes = (uint32_t)((min((uint64_t)QTILE, b1 - nb) * sizeof(uint2) + 15) & ~15ull);
+      mbar_arrive_expect_tx(&S.full[s], bytes);
+      bulk_g2s(&S.tile[s][0], P.qB + nb, bytes, &S.full[s]);
+    }
+  }
+  __syncwarp();
+  if (qn > 0) flush_queue<KIND_TRI>(P, Bt, q, qn, lane, n_pass, n_sing);
+  flush_counters(P, lane, n_pass, n_sing, n_exact);
 }
 
 // OR of every task's input-mesh status flags (non-finite coordinates) into *flag.
@@ -659,6 +919,50 @@ static int launch_cull(std::vector<SearchParams>& T, Batch Bt, std::vector<uint6
   return MCX_OK;
 }
 
+// MCX_MODE_PREFILTER: frame init → union bounds → quantise → prefilter search.
+static int launch_prefilter(std::vector<SearchParams>& T, Batch Bt, std::vector<uint64_t>& prefix, void* dev_tab,
+                            int device, cudaStream_t stream) {
+  int dev_sms = 148;
+  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device);
+  constexpr int UNROLL = 4;
+  const size_t smem = sizeof(QSmem);
+  CUDA_TRY(cudaFuncSetAttribute(search_prefilter_kernel<UNROLL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+  int occ = 1;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, search_prefilter_kernel<UNROLL>, Q_THREADS, smem));
+  const uint64_t slots = (uint64_t)dev_sms * (occ > 0 ? occ : 1);
+  prefix.assign(T.size() + 1, 0);
+  uint64_t max_records = 0;
+  for (size_t t = 0; t < T.size(); ++t) {
+    if (T[t].my_blocks && T[t].nB) choose_chunks(T[t], slots); else T[t].nchunk = 0;
+    prefix[t + 1] = prefix[t] + T[t].my_blocks * T[t].nchunk;
+    if (T[t].nchunk) max_records = std::max<uint64_t>(max_records, T[t].nA + T[t].nB);
+  }
+  const uint64_t total = prefix.back();
+  const size_t tab = sizeof(SearchParams) * T.size();
+  CUDA_TRY(cudaMemcpyAsync(dev_tab, T.data(), tab, cudaMemcpyHostToDevice, stream));
+  CUDA_TRY(cudaMemcpyAsync((char*)dev_tab + tab, prefix.data(), sizeof(uint64_t) * prefix.size(),
+                           cudaMemcpyHostToDevice, stream));
+  if (total == 0) return MCX_OK;
+  if (total > 0x7fffffffull) return set_error(MCX_E_ARG, "grid too large");
+  if (T.size() > 65535) return set_error(MCX_E_ARG, "MCX_MODE_PREFILTER supports at most 65535 tasks per batch");
+  Bt.tasks = reinterpret_cast<const SearchParams*>(dev_tab);
+  Bt.prefix = reinterpret_cast<const uint64_t*>((char*)dev_tab + tab);
+  Bt.neg1 = 0xffffffffu;
+  const unsigned n = (unsigned)T.size();
+  qframe_init_kernel<<<(n + 127) / 128, 128, 0, stream>>>(Bt);
+  // ~4 records per thread, at most 8 blocks per SM in total across the tasks
+  uint64_t gx = (max_records + 1023) / 1024;
+  const uint64_t gcap = std::max<uint64_t>(1, (uint64_t)dev_sms * 8 / n);
+  if (gx > gcap) gx = gcap;
+  const dim3 grid((unsigned)gx, n);
+  qbounds_kernel<<<grid, 256, 0, stream>>>(Bt);
+  quant_kernel<<<grid, 256, 0, stream>>>(Bt);
+  search_prefilter_kernel<UNROLL><<<(unsigned)total, Q_THREADS, smem, stream>>>(Bt);
+  CUDA_TRY(cudaGetLastError());
+  return MCX_OK;
+}
+
 struct Timing {
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   ~Timing() {
@@ -694,7 +998,14 @@ static uint64_t align16(uint64_t v) { return (v + 15) & ~15ull; }
 
 struct WsLayout {
   uint64_t counters, table, list, total, list_cap;
+  uint64_t quant;  // MCX_MODE_PREFILTER: per task 64 B frame + quantised A and B records
 };
+
+// Bytes of one task's quantisation area: frame, then A's and B's 8-byte records,
+// each padded so the 16-byte-rounded bulk copy of a tail tile stays inside.
+static uint64_t quant_task_bytes(uint64_t nA, uint64_t nB) {
+  return 64 + align16(8 * (nA + 2)) + align16(8 * (nB + 2));
+}
 
 static WsLayout ws_layout(const mcx_task* tasks, uint32_t n, const mcx_opts* o) {
   WsLayout L;
@@ -713,7 +1024,12 @@ static WsLayout ws_layout(const mcx_task* tasks, uint32_t n, const mcx_opts* o) 
       L.list_cap += g.my_blocks * ((B->n_tri + TILE - 1) / TILE);
     }
   }
-  L.total = L.list + 16 * L.list_cap;
+  L.quant = align16(L.list + 16 * L.list_cap);
+  L.total = L.quant;
+  if (o && o->mode == MCX_MODE_PREFILTER) {
+    for (uint32_t t = 0; t < n; ++t)
+      if (tasks[t].A && tasks[t].B) L.total += quant_task_bytes(tasks[t].A->n_tri, tasks[t].B->n_tri);
+  }
   return L;
 }
 
@@ -724,13 +1040,15 @@ static int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mc
   const uint32_t scount = o->shard_count ? o->shard_count : 1;
   const uint32_t sidx = o->shard_index;
   if (sidx >= scount) return set_error(MCX_E_ARG, "shard_index %u >= shard_count %u", sidx, scount);
-  if (o->mode != MCX_MODE_BRUTE && o->mode != MCX_MODE_CULL) return set_error(MCX_E_ARG, "unknown mode %d", o->mode);
+  if (o->mode != MCX_MODE_BRUTE && o->mode != MCX_MODE_CULL && o->mode != MCX_MODE_PREFILTER)
+    return set_error(MCX_E_ARG, "unknown mode %d", o->mode);
   if (cap > 0 && !hits) return set_error(MCX_E_ARG, "null hit buffer with nonzero capacity");
   const WsLayout L = ws_layout(tasks, n, o);
   if (!o->workspace || o->workspace_bytes < L.total || ((uintptr_t)o->workspace & 15))
     return set_error(MCX_E_ARG, "workspace too small or misaligned (need %llu bytes, 16-byte aligned)",
                      (unsigned long long)L.total);
   char* ws = (char*)o->workspace;
+  uint64_t qoff = L.quant;
   std::vector<SearchParams> T(n);
   for (uint32_t t = 0; t < n; ++t) {
     const mcx_mesh_dev* A = tasks[t].A;
@@ -773,6 +1091,12 @@ static int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mc
     P.tboxB = reinterpret_cast<const Box*>(B->tbox);
     P.statusA = A->status;
     P.statusB = B->status;
+    if (o->mode == MCX_MODE_PREFILTER) {
+      P.qframe = reinterpret_cast<long long*>(ws + qoff);
+      P.qA = reinterpret_cast<uint2*>(ws + qoff + 64);
+      P.qB = reinterpret_cast<uint2*>(ws + qoff + 64 + align16(8 * (A->n_tri + 2)));
+      qoff += quant_task_bytes(A->n_tri, B->n_tri);
+    }
     st[t] = mcx_stats{};
     st[t].n_pairs = g.na * B->n_tri;
   }
@@ -794,7 +1118,8 @@ static int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mc
   }
   std::vector<uint64_t> prefix;
   const int rc = o->mode == MCX_MODE_BRUTE ? launch_brute<KIND_TRI>(T, Bt, prefix, ws + L.table, o->device, stream)
-                                           : launch_cull<KIND_TRI>(T, Bt, prefix, ws + L.table, o->device, stream);
+                 : o->mode == MCX_MODE_CULL ? launch_cull<KIND_TRI>(T, Bt, prefix, ws + L.table, o->device, stream)
+                                            : launch_prefilter(T, Bt, prefix, ws + L.table, o->device, stream);
   if (rc != MCX_OK) return rc;
   if (o->timing) CUDA_TRY(cudaEventRecord(tm.e1, stream));
   status_kernel<<<1, 32, 0, stream>>>(reinterpret_cast<const SearchParams*>(ws + L.table), n,
@@ -810,7 +1135,8 @@ static int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mc
     st[t].n_hits = c[0];
     st[t].n_aabb_pass = c[1];
     st[t].n_singular = c[2];
-    st[t].n_tested = o->mode == MCX_MODE_BRUTE ? st[t].n_pairs : c[3];
+    st[t].n_tested = o->mode == MCX_MODE_CULL ? c[3] : st[t].n_pairs;
+    st[t].n_exact_tests = o->mode == MCX_MODE_BRUTE ? st[t].n_pairs : c[3];
     st[t].kernel_ms = ms;
   }
   if (h[2]) return set_error(MCX_E_ARG, "non-finite (NaN/Inf) coordinates in an input mesh (mcx_pack status)");
@@ -969,6 +1295,7 @@ static int launch_pair_candidates_mesh(const mcx_mesh_dev* A, const double* cA, 
   st->n_aabb_pass = c[1];
   st->n_singular = c[2];  // Moller-rejected quad pairs
   st->n_tested = c[3];
+  st->n_exact_tests = c[3];
   if (o->timing) {
     float ms = 0.f;
     CUDA_TRY(cudaEventElapsedTime(&ms, tm.e0, tm.e1));

@@ -146,9 +146,9 @@ def search_hits(u_half, s_half, backend: str = "cuda", *, devices=(0,), mode: st
                 timing: bool = False):
     """Triangle-level hits (iA, iB, s, t, a, b), sorted by (iA, iB), plus kernel stats."""
     _check_backend(backend)
-    m = {"brute": _lib.MODE_BRUTE, "cull": _lib.MODE_CULL}.get(mode)
+    m = _lib.MODE_NAMES.get(mode)
     if m is None:
-        raise ConfigError(f"mode must be 'brute' or 'cull', got {mode!r}")
+        raise ConfigError(f"mode must be one of {sorted(_lib.MODE_NAMES)}, got {mode!r}")
     return _device.search(_coords(u_half), _coords(s_half), devices=devices, mode=m, timing=timing,
                           task=_task(u_half, s_half))
 

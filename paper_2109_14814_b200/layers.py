@@ -86,9 +86,9 @@ def search_plan(u_mesh: ManifoldMesh, s_mesh: ManifoldMesh, plan: LayerPairPlan,
     and the per-task counters (the RunManifest's survivor/hit counts).
     """
     isect._check_backend(backend)
-    m = {"brute": _lib.MODE_BRUTE, "cull": _lib.MODE_CULL}.get(mode)
+    m = _lib.MODE_NAMES.get(mode)
     if m is None:
-        raise ConfigError(f"mode must be 'brute' or 'cull', got {mode!r}")
+        raise ConfigError(f"mode must be one of {sorted(_lib.MODE_NAMES)}, got {mode!r}")
     halves = {}
 
     def get(mesh, key, n, s):

@@ -95,7 +95,7 @@ def test_golden_c4ii_exact_lattice():
     assert_same_hits(ref, r.hits, r.stats)
 
 
-MODES = [_lib.MODE_BRUTE, _lib.MODE_CULL]
+MODES = [_lib.MODE_BRUTE, _lib.MODE_CULL, _lib.MODE_PREFILTER]
 
 
 @pytest.mark.parametrize("mode", MODES)
@@ -397,14 +397,15 @@ def test_parity_stress_large(kind, oracle_lib):
 
 
 def test_c_host_example():
-    """The C ABI driven from plain C (no Python/torch): brute and cull agree."""
+    """The C ABI driven from plain C (no Python/torch): brute, cull and prefilter agree."""
     import subprocess
     d = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools", "c_example")
     subprocess.run(["make", "-s", "-C", d], check=True)
     out = subprocess.run([os.path.join(d, "mcx_example"), "200", "65"], capture_output=True, text=True, check=True)
     rows = [ln.split() for ln in out.stdout.strip().splitlines()]
-    assert [r[0] for r in rows] == ["brute", "cull"]
-    brute, cull = rows
+    assert [r[0] for r in rows] == ["brute", "cull", "prefilter"]
+    brute, cull, pre = rows
+    assert pre[1:7] == brute[1:7]
     assert brute[1] == cull[1]                      # logical pairs
     assert brute[2] == brute[1] and int(cull[2]) < int(cull[1])  # executed tests
     assert brute[3:7] == cull[3:7]                  # aabb pass, singular, hits, checksum
@@ -436,3 +437,39 @@ def test_acceptance6_exact_oracle(case, mode):
     got = set(zip(r.hits["ia"].tolist(), r.hits["ib"].tolist()))
     assert got == want
     assert r.stats["n_aabb_pass"] == int(ov.sum())
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C4i"])
+def test_prefilter_counts(name):
+    """MCX_MODE_PREFILTER: every pair is tested (n_tested == n_pairs); the exact FP64 box
+    test runs only on quantised passes, a superset of the exact AABB passes."""
+    A, _, B, _ = config_pair(name)
+    Am, Bm = D.DeviceMesh(A, 0), D.DeviceMesh(B, 0)
+    rb = D.search_device(Am, Bm, mode=_lib.MODE_BRUTE)
+    rp = D.search_device(Am, Bm, mode=_lib.MODE_PREFILTER)
+    assert_same_hits(rb.hits, rp.hits)
+    sp = rp.stats
+    assert sp["n_tested"] == sp["n_pairs"] == rb.stats["n_pairs"]
+    assert sp["n_aabb_pass"] == rb.stats["n_aabb_pass"] and sp["n_singular"] == rb.stats["n_singular"]
+    assert sp["n_aabb_pass"] <= sp["n_exact_tests"] < sp["n_pairs"]
+    assert rb.stats["n_exact_tests"] == rb.stats["n_pairs"]
+
+
+def test_prefilter_frames_exact(oracle_lib):
+    """Quantisation frames that make the integer test weak or degenerate never change
+    the result: a far outlier column (coarse frame), a constant coordinate (κ = 0),
+    huge magnitudes (frame extent overflows to inf → κ = 0), tiny magnitudes."""
+    A, _, B, _ = config_pair("C4iii")
+    cases = []
+    A1 = A.copy(); A1[:, -1, :] += 1.0e6  # one far column in A
+    cases.append((A1, B))
+    A2 = A.copy(); B2 = B.copy(); A2[3] = 0.25; B2[3] = 0.25  # py constant on both meshes
+    cases.append((A2, B2))
+    cases.append((A * 1.0e300, B * 1.0e300))
+    A4 = A.copy(); A4[0, 0, 0] = -1.7e308; B4 = B.copy(); B4[1, 0, 0] = 1.7e308  # extent overflows
+    cases.append((A4, B4))
+    cases.append((A * 1.0e-300, B * 1.0e-300))
+    for Ax, Bx in cases:
+        ref = oracle_lib.search(Ax, Bx, sweep=True)
+        r = D.search(Ax, Bx, mode=_lib.MODE_PREFILTER)
+        assert_same_hits(ref, r.hits, r.stats)

@@ -28,7 +28,7 @@ def test_library_exports_every_header_symbol():
     assert set(funcs) == set(_lib.EXPORTS)
     for f in funcs:
         assert hasattr(L, f), f
-    assert L.mcx_version() == 1
+    assert L.mcx_version() == 2
     assert L.mcx_a_block() == 1024
     assert isinstance(L.mcx_last_error(), bytes)
 

@@ -95,8 +95,9 @@ int main(int argc, char** argv) {
   mcx_hit* dhits;
   CK(cudaMalloc((void**)&dhits, sizeof(mcx_hit) * cap));
   mcx_hit* hh = (mcx_hit*)malloc(sizeof(mcx_hit) * cap);
-  const int modes[2] = {MCX_MODE_BRUTE, MCX_MODE_CULL};
-  for (int mi = 0; mi < 2; ++mi) {
+  const int modes[3] = {MCX_MODE_BRUTE, MCX_MODE_CULL, MCX_MODE_PREFILTER};
+  const char* names[3] = {"brute", "cull", "prefilter"};
+  for (int mi = 0; mi < 3; ++mi) {
     mcx_opts o = {0};
     o.device = 0;
     o.mode = modes[mi];
@@ -108,7 +109,7 @@ int main(int argc, char** argv) {
     CK(cudaMemcpy(hh, dhits, sizeof(mcx_hit) * st.n_hits, cudaMemcpyDeviceToHost));
     unsigned long long sum = 0;
     for (uint64_t h = 0; h < st.n_hits; ++h) sum += (unsigned long long)hh[h].ia * 1000003ull + hh[h].ib;
-    printf("%s %llu %llu %llu %llu %llu %llu %.3f\n", mi ? "cull" : "brute", (unsigned long long)st.n_pairs,
+    printf("%s %llu %llu %llu %llu %llu %llu %.3f\n", names[mi], (unsigned long long)st.n_pairs,
            (unsigned long long)st.n_tested, (unsigned long long)st.n_aabb_pass, (unsigned long long)st.n_singular,
            (unsigned long long)st.n_hits, sum, st.kernel_ms);
     CK(cudaFree(o.workspace));

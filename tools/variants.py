@@ -8,7 +8,7 @@ from oracle import c_oracle as C
 
 cfgs = sys.argv[1].split(",") if len(sys.argv) > 1 else ["C3"]
 variants = sys.argv[2].split(",") if len(sys.argv) > 2 else ["0", "1", "2", "3"]
-mode = _lib.MODE_CULL if (len(sys.argv) > 3 and sys.argv[3] == "cull") else _lib.MODE_BRUTE
+mode = _lib.MODE_NAMES[sys.argv[3] if len(sys.argv) > 3 else "brute"]
 A, _, B, _ = config_pair("C4i")
 ref = C.search(A, B, sweep=True)
 Am, Bm = D.DeviceMesh(A, 0), D.DeviceMesh(B, 0)
@@ -27,7 +27,7 @@ for name in cfgs:
         ts = [D.search_device(Am, Bm, mode=mode, timing=True).stats for _ in range(3)]
         st = min(ts, key=lambda s: s["kernel_ms"])
         ms = st["kernel_ms"]
-        print(json.dumps({"cfg": name, "variant": v, "mode": "cull" if mode else "brute", "ms": ms,
+        print(json.dumps({"cfg": name, "variant": v, "mode": sys.argv[3] if len(sys.argv) > 3 else "brute", "exact_tests": st["n_exact_tests"], "ms": ms,
                           "pairs_per_s": st["n_pairs"] / ms * 1e3, "tested": st["n_tested"],
                           "lane_ops_T": (8 * st["n_tested"] + 100 * st["n_aabb_pass"]) / ms / 1e9,
                           "frac": (8 * st["n_tested"] + 100 * st["n_aabb_pass"]) / ms / 1e9 / 18.61248,
