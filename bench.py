@@ -5,11 +5,15 @@ mesh-intersection search (BASELINE.json metric) on N B200s.
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
 
 One step = one complete search of mesh A against mesh B (every triangle pair
-gets the AABB test, survivors the canonical FP64 solve, hits compacted) for the
-named synthetic configuration (default C3: 1024×512 vs 1024×512 grids,
-1,046,528 triangles each, 1.095e12 pairs).  Under torchrun each rank owns one
-GPU and searches its cyclic share of A's 1024-triangle blocks (no collective on
-the data path); timing is the max over ranks of CUDA-event device time.
+is tested, the AABB survivors get the canonical FP64 solve, hits are compacted)
+for the named synthetic configuration (default C3: 1024×512 vs 1024×512 grids,
+1,046,528 triangles each, 1.095e12 pairs).  `value` uses MCX_MODE_PREFILTER
+(every pair tested by a conservative quantised-box integer test, its passes by
+the exact FP64 test); the FP64 brute-force kernel and the culled search of the
+same workload are measured in the same run and reported beside it.  Under
+torchrun each rank owns one GPU and searches its cyclic share of A's
+1024-triangle blocks (no collective on the data path); timing is the max over
+ranks of CUDA-event device time.
 
 ``--impl reference`` times the reference's CPU search (the C port of the
 SPEC's all-pairs "parallel" backend, oracle/mcx_oracle.c, all host threads) on a
@@ -42,8 +46,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C3")
-    ap.add_argument("--mode", default="brute", choices=["brute", "cull"],
-                    help="primary mode for `value` (the other is measured too and reported alongside)")
+    ap.add_argument("--mode", default="prefilter", choices=["prefilter", "brute", "cull"],
+                    help="primary mode for `value` (the others are measured too and reported alongside)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU-baseline sample duration")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -196,7 +200,11 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ our arm
-KERNEL_LAUNCHES = {"brute": 2, "cull": 3}  # our kernels per search call: search (+cull level 1) + status check
+# our kernels per search call: brute = search + status check; cull = 2 cull levels + status;
+# prefilter = frame init + bounds + quantise + search + status
+KERNEL_LAUNCHES = {"brute": 2, "cull": 3, "prefilter": 5}
+FMA_LANES_PER_CLK_PER_SM = 64  # B200 fma pipe (IMAD); measured 62.7 by tools/microbench/hprefilter.cu (swar3_mix0)
+PREFILTER_FMA_OPS_PER_PAIR = 2  # SASS of the prefilter inner loop: IMAD + IMAD.IADD + LOP3.LUT.PAND per pair
 
 
 def run_ours(args):
@@ -220,7 +228,7 @@ def run_ours(args):
     red_dev = dev if args.dist_backend == "nccl" else torch.device("cpu")
     A, sa, B, sb = config_pair(args.config)
     desc = workload_desc(args.config, A, B)
-    modes = {"brute": _lib.MODE_BRUTE, "cull": _lib.MODE_CULL}
+    modes = dict(_lib.MODE_NAMES)
     shard = (rank, world)
 
     stream = torch.cuda.current_stream(dev)
@@ -300,53 +308,82 @@ def run_ours(args):
                 "mode": mode_name}
 
     primary = args.mode
-    other = "cull" if primary == "brute" else "brute"
-    m1 = measure(primary, True)
-    m2 = measure(other, False)
-    brute = m1 if primary == "brute" else m2
-    cull = m2 if primary == "brute" else m1
+    others = [m for m in ("prefilter", "brute", "cull") if m != primary]
+    res_by_mode = {primary: measure(primary, True)}
+    for m in others:
+        res_by_mode[m] = measure(m, False)
+    m1 = res_by_mode[primary]
+    brute, cull, pre = res_by_mode["brute"], res_by_mode["cull"], res_by_mode["prefilter"]
+    hit_counts = {k: v["hits"] for k, v in res_by_mode.items() if v["hits"] is not None}
+    if len(set(hit_counts.values())) > 1:
+        raise SystemExit(f"hit counts differ between modes: {hit_counts}")
 
-    # ---- roofline of the FP64 pair-test kernel (MCX_MODE_BRUTE, kernel-only events)
     props = torch.cuda.get_device_properties(dev)
     sms = props.multi_processor_count
     clocks = m1["clocks"] or {}
     f_max = clocks.get("sm_max_mhz") or 1965.0
     f_run = clocks.get("sm_mhz") or f_max
+
+    # ---- roofline of the FP64 pair-test kernel (MCX_MODE_BRUTE, kernel-only events)
     st = brute["stats"]
     lane_ops = 8.0 * st["n_tested"] + 100.0 * st["n_aabb_pass"]
     achieved = lane_ops / (st["kernel_ms"] * 1e-3) / 1e12
     peak = sms * FP64_LANES_PER_CLK_PER_SM * f_max * 1e6 / 1e12
     peak_run = sms * FP64_LANES_PER_CLK_PER_SM * f_run * 1e6 / 1e12
-    roofline = {"bound": "fp64_pipe", "kernel": "search_brute_kernel (MCX_MODE_BRUTE, the FP64 pair-test kernel)",
-                "achieved": achieved, "peak": peak, "unit": "Tlane-op/s", "frac": achieved / peak,
-                "frac_at_observed_clock": achieved / peak_run,
-                "peak_source": f"{sms} SMs x {FP64_LANES_PER_CLK_PER_SM} FP64 lanes/clk x {f_max:.0f} MHz "
-                               "(pipe rate measured: DADD 63.5 lanes/clk/SM, profiles/r01_pipes.jsonl; "
-                               "MEASURED_PEAKS.json has no FP64 entry)",
-                "work_per_launch": "8 FP64 compare lane-ops per pair + ~100 FP64 lane-ops per AABB survivor",
-                "kernel_ms": st["kernel_ms"],
-                "traffic": (2140494000.0 + 14626304.0) if args.config == "C3" else None,
-                "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum of one C3 launch, ncu --set full "
-                                "(profiles/r01_ncu_brute_c3.txt): 2.16 GB vs 68 GB of algorithmic L2->SMEM tile "
-                                "traffic; B's 67 MB of boxes are re-read from HBM ~32x per launch (L2 is split "
-                                "over two dies) at ~4 GB/s - negligible against the FP64 bound"}
+    fp64_roofline = {
+        "bound": "fp64_pipe", "kernel": "search_brute_kernel (MCX_MODE_BRUTE, the FP64 pair-test kernel)",
+        "achieved": achieved, "peak": peak, "unit": "Tlane-op/s", "frac": achieved / peak,
+        "frac_at_observed_clock": achieved / peak_run,
+        "peak_source": f"{sms} SMs x {FP64_LANES_PER_CLK_PER_SM} FP64 lanes/clk x {f_max:.0f} MHz "
+                       "(pipe rate measured: DADD 63.5 lanes/clk/SM, profiles/r01_pipes.jsonl; "
+                       "MEASURED_PEAKS.json has no FP64 entry)",
+        "work_per_launch": "8 FP64 compare lane-ops per pair + ~100 FP64 lane-ops per AABB survivor",
+        "kernel_ms": st["kernel_ms"],
+        "traffic": (2140494000.0 + 14626304.0) if args.config == "C3" else None,
+        "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum of one C3 launch, ncu --set full "
+                        "(profiles/r01_ncu_brute_c3.txt): 2.16 GB vs 68 GB of algorithmic L2->SMEM tile "
+                        "traffic; B's 67 MB of boxes are re-read from HBM ~32x per launch (L2 is split "
+                        "over two dies) at ~4 GB/s - negligible against the FP64 bound"}
+    # ---- roofline of the prefilter kernel: every pair = 2 integer subtractions on the fma
+    # pipe (IMAD, IMAD.IADD) + 1 LOP3 on the alu pipe; the fma pipe binds first
+    pst = pre["stats"]
+    pf_peak = sms * FMA_LANES_PER_CLK_PER_SM / PREFILTER_FMA_OPS_PER_PAIR * f_max * 1e6
+    pf_achieved = pst["n_tested"] / (pst["kernel_ms"] * 1e-3)
+    pf_roofline = {
+        "bound": "fma_pipe", "kernel": "search_prefilter_kernel (MCX_MODE_PREFILTER: quantised-box SWAR test of "
+                                       "every pair, exact FP64 test of its passes)",
+        "achieved": pf_achieved, "peak": pf_peak, "unit": "pair-tests/s", "frac": pf_achieved / pf_peak,
+        "frac_of_issue_bound": pf_achieved / (pf_peak * 4.0 / 3.0),
+        "peak_source": f"{sms} SMs x {FMA_LANES_PER_CLK_PER_SM} fma-pipe lanes/clk / {PREFILTER_FMA_OPS_PER_PAIR} "
+                       f"IMAD per pair x {f_max:.0f} MHz (fma rate measured 62.7 lanes/clk/SM, "
+                       "tools/microbench/hprefilter.cu); issue bound = 3 instructions per pair",
+        "work_per_launch": "n_pairs quantised pair tests (2 IMAD + 1 LOP3 each) + n_exact_tests FP64 box tests",
+        "exact_tests_per_step": pst["n_exact_tests"], "kernel_ms": pst["kernel_ms"],
+        "kernel_ms_note": "CUDA events around the whole call: frame + quantise kernels (~0.05 ms) + search",
+        "traffic": None}
+    roofline = pf_roofline if primary == "prefilter" else fp64_roofline
+    fp64_block = {"mode": "brute", "value": brute["value"], "unit": UNIT, "ms_per_step": brute["ms_per_step"],
+                  "kernel_ms": brute["kernel_ms"], "roofline": fp64_roofline,
+                  "note": "every pair gets the 8-compare FP64 AABB test (the north star's FP64 kernel)"}
+    pre_block = {"mode": "prefilter", "value": pre["value"], "unit": UNIT, "ms_per_step": pre["ms_per_step"],
+                 "kernel_ms": pre["kernel_ms"], "roofline": pf_roofline,
+                 "speedup_vs_fp64_brute": brute["ms_per_step"] / pre["ms_per_step"]}
     cst = cull["stats"]
     cull_block = {"mode": "cull", "value": cull["value"], "unit": UNIT + " (logical)",
                   "ms_per_step": cull["ms_per_step"], "search_wall_s": cull["ms_per_step"] / 1e3,
                   "kernel_ms": cull["kernel_ms"], "logical_pairs_per_step": cst["n_pairs"],
                   "executed_pair_tests_per_step": cst["n_tested"], "aabb_pass": cst["n_aabb_pass"],
-                  "speedup_vs_brute": brute["ms_per_step"] / cull["ms_per_step"], "hits": cull["hits"],
+                  "speedup_vs_brute": brute["ms_per_step"] / cull["ms_per_step"],
+                  "speedup_vs_prefilter": pre["ms_per_step"] / cull["ms_per_step"], "hits": cull["hits"],
                   "executed_fp64_frac": (8.0 * cst["n_tested"] + 100.0 * cst["n_aabb_pass"]) /
                                         (cst["kernel_ms"] * 1e-3) / 1e12 / peak,
                   "note": "identical hit set / AABB-pass / singular counts; exact union-box culling over the "
                           "tiled storage order skips only provably disjoint pairs"}
-    if brute["hits"] is not None and cull["hits"] is not None and brute["hits"] != cull["hits"]:
-        raise SystemExit(f"brute/cull hit counts differ: {brute['hits']} vs {cull['hits']}")
 
     e2e = None
     if not args.no_e2e:
         e2e = measure_e2e(primary, m1["pairs"])
-        e2e["other_mode"] = measure_e2e(other, m1["pairs"])
+        e2e["other_modes"] = {m: measure_e2e(m, m1["pairs"]) for m in others}
 
     # ---- the paper's own benchmark shape: 14-layer search, 108 layer-pair tasks of
     # N1 = 1024 x N2 = 2048 grids with 35 s-values per half-layer (PAPER.md "Computational
@@ -370,7 +407,7 @@ def run_ours(args):
                              "half-layer, all 108 layer-pair tasks in one mcx_search_batch job",
                  "tasks": len(pairs), "published": {"dgx_v100_full_search_s": 16.0, "laptop_full_search_s": 62.0,
                                                     "dgx_v100_bbox_kernel_per_task_s": 0.03}}
-        for mname in ("brute", "cull"):
+        for mname in ("prefilter", "brute", "cull"):
             for _ in range(max(1, args.warmup)):
                 res = D.search_batch(pairs, mode=modes[mname], shard=shard, stream=stream)
             barrier()
@@ -434,8 +471,7 @@ def run_ours(args):
                 "config": {**desc, "mode": primary, "parallelism": f"A-block cyclic shards x{world}, B replicated",
                            "l2": "flushed between timed steps (256 MiB write, outside the events)"},
                 "search_wall_s": m1["ms_per_step"] / 1e3, "hits": m1["hits"], "kernel_ms": m1["kernel_ms"],
-                "roofline": roofline, "cull": cull_block if primary == "brute" else None,
-                "brute": None if primary == "brute" else {"value": brute["value"], "ms_per_step": brute["ms_per_step"]},
+                "roofline": roofline, "fp64_brute": fp64_block, "prefilter": pre_block, "cull": cull_block,
                 "e2e": e2e, "cpu_baseline": cpu, "paper_workload": paper, "clocks": m1["clocks"],
                 "gpu_launches": m1["launches"], "gpu": props.name, "sms": sms}
         print(json.dumps(line), flush=True)

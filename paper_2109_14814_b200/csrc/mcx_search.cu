@@ -398,17 +398,27 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_brute_kernel(const
 // tests qloA_c ≤ qhiB_c.  A pair passes iff all 8 guard bits of the two
 // differences are set: 2 IMAD (fma pipe) + 1 LOP3 + 1 ISETP (alu) per pair instead
 // of 8 DSETP on the 64-lane/clk FP64 pipe.
-constexpr int QR = 16;                   // A records per thread
-constexpr int Q_THREADS = A_BLOCK / QR;  // 64 threads = 2 warps, 512 A records per warp
-constexpr int Q_WARPS = Q_THREADS / 32;
 constexpr int QTILE = 1024;              // B records per shared-memory stage (8 KB)
 constexpr int Q_QCAP = 64;
 constexpr unsigned QG = 0x80808080u;
 constexpr unsigned Q7F = 0x7F7F7F7Fu;
 
+// Prefilter kernel variant: QR A records per thread (a warp covers 32·QR consecutive
+// storage positions of the 1024-record A block), JB B records per warp vote.
+template <int QR_, int JB_, int UNROLL_, int MINB_ = 1>
+struct QCfg {
+  static constexpr int QR = QR_;
+  static constexpr int MINB = MINB_;      // resident CTAs per SM the register cap targets
+  static constexpr int JB = JB_;
+  static constexpr int UNROLL = UNROLL_;
+  static constexpr int THREADS = A_BLOCK / QR_;
+  static constexpr int WARPS = THREADS / 32;
+};
+
+template <class C>
 struct __align__(16) QSmem {
   uint2 tile[STAGES][QTILE];
-  uint2 queue[Q_WARPS][Q_QCAP];
+  uint2 queue[C::WARPS][Q_QCAP];
   unsigned long long full[STAGES];
 };
 
@@ -426,6 +436,23 @@ __device__ __forceinline__ unsigned imad_sub(unsigned a, unsigned m1, unsigned b
   unsigned r;
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(b), "r"(m1), "r"(a));
   return r;
+}
+
+// a − b on the alu pipe (IADD3); half of the pair tests use it so that neither the
+// fma nor the alu pipe saturates before instruction issue does.
+__device__ __forceinline__ unsigned alu_sub(unsigned a, unsigned b) {
+  unsigned r;
+  asm("sub.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+
+// allfail &= "the pair with differences x0, x1 fails": one LOP3 with predicate output
+// (SASS LOP3.LUT.PAND), LUT 0x2a = (~x0 | ~x1) & G, nonzero iff a guard bit is missing.
+__device__ __forceinline__ void fail_and(unsigned& allfail, unsigned x0, unsigned x1) {
+  unsigned d;  // LOP3 result (unused: only its != 0 predicate matters)
+  asm("{\n .reg .pred p;\n setp.ne.u32 p, %1, 0;\n lop3.and.b32 %0|p, %2, %3, %4, 0x2a, p;\n selp.u32 %1, 1, 0, p;\n}"
+      : "=r"(d), "+r"(allfail)
+      : "r"(x0), "r"(x1), "r"(QG));
 }
 
 __device__ __forceinline__ uint2 ld_nc_u2(const uint2* p) {
@@ -510,10 +537,11 @@ __global__ void __launch_bounds__(256) quant_kernel(const Batch Bt) {
   }
 }
 
-template <int UNROLL>
-__global__ void __launch_bounds__(Q_THREADS) search_prefilter_kernel(const Batch Bt) {
+template <class C>
+__global__ void __launch_bounds__(C::THREADS, C::MINB) search_prefilter_kernel(const Batch Bt) {
+  constexpr int QR = C::QR;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  QSmem& S = *reinterpret_cast<QSmem*>(smem_raw);
+  QSmem<C>& S = *reinterpret_cast<QSmem<C>*>(smem_raw);
   __shared__ SearchParams Ps;
   __shared__ uint64_t s_unit;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -546,7 +574,7 @@ __global__ void __launch_bounds__(Q_THREADS) search_prefilter_kernel(const Batch
     }
   }
 
-  // A records of this thread: warp w covers the 512 storage positions a0 + 512 w + [0, 512)
+  // A records of this thread: warp w covers storage positions a0 + 32·QR·w + [0, 32·QR)
   const uint32_t abase = (uint32_t)(a0 + (uint64_t)warp * (QR * 32) + lane);
   unsigned h0[QR], h1[QR];
   auto load_a = [&]() {
@@ -570,54 +598,65 @@ __global__ void __launch_bounds__(Q_THREADS) search_prefilter_kernel(const Batch
   unsigned long long n_pass = 0, n_sing = 0, n_exact = 0;
   const unsigned lt_mask = (1u << lane) - 1u;
 
+  // Rare path for B record ib (quantised form bq): the exact FP64 box test for every
+  // quantised pass of this warp, reading A's records from L1/L2 (registers stay free).
+  auto slow = [&](uint32_t ib, uint2 bq) {
+    const double2* bp = reinterpret_cast<const double2*>(P.boxB + ib);
+    const double2 l01 = __ldg(bp), l23 = __ldg(bp + 1), g01 = __ldg(bp + 2), g23 = __ldg(bp + 3);
+    for (int r = 0; r < QR; ++r) {
+      const uint32_t ia = abase + r * 32;
+      bool p = false;
+      if (ia >= P.a_begin && ia < P.a_end) {
+        const uint2 l = ld_nc_u2(P.qA + ia);
+        const unsigned x0 = imad_sub((Q7F - l.y) | QG, m1, bq.x), x1 = imad_sub((Q7F - l.x) | QG, m1, bq.y);
+        if ((x0 & x1 & QG) == QG) {
+          ++n_exact;
+          const double2* ap = reinterpret_cast<const double2*>(P.boxA + ia);
+          const double2 a01 = __ldg(ap), a23 = __ldg(ap + 1), c01 = __ldg(ap + 2), c23 = __ldg(ap + 3);
+          p = (l01.x <= c01.x) & (a01.x <= g01.x) & (l01.y <= c01.y) & (a01.y <= g01.y) &
+              (l23.x <= c23.x) & (a23.x <= g23.x) & (l23.y <= c23.y) & (a23.y <= g23.y);
+        }
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, p);
+      if (m) {
+        if (p) q[qn + __popc(m & lt_mask)] = make_uint2(ia, ib);
+        qn += __popc(m);
+        __syncwarp();
+        if (qn >= 32) {
+          qn -= 32;
+          flush_queue<KIND_TRI>(P, Bt, q + qn, 32, lane, n_pass, n_sing);
+        }
+      }
+    }
+  };
+
   for (int t = 0; t < ntiles; ++t) {
     const int s = t % STAGES;
     mbar_wait(&S.full[s], (uint32_t)((t / STAGES) & 1));
     const uint64_t tb = b0 + (uint64_t)t * QTILE;
     const int nvalid = (int)min((uint64_t)QTILE, b1 - tb);
     const uint2* tile = S.tile[s];
-#pragma unroll(UNROLL)
-    for (int j = 0; j < nvalid; ++j) {
-      const uint2 bq = tile[j];
-      bool any = false;
+    auto step = [&](int j, auto jb_c) {
+      constexpr int NJ = decltype(jb_c)::value;
+      uint2 bq[NJ];
+      unsigned allfail[4] = {1, 1, 1, 1};  // 4 independent predicate chains (latency)
 #pragma unroll
-      for (int r = 0; r < QR; ++r) {
-        const unsigned x0 = imad_sub(h0[r], m1, bq.x), x1 = imad_sub(h1[r], m1, bq.y);
-        any |= ((x0 & x1 & QG) == QG);
+      for (int u = 0; u < NJ; ++u) {
+        bq[u] = tile[j + u];
+#pragma unroll
+        for (int r = 0; r < QR; ++r)
+          fail_and(allfail[r & 3], imad_sub(h0[r], m1, bq[u].x), alu_sub(h1[r], bq[u].y));
       }
-      if (__any_sync(0xffffffffu, any)) {
-        // rare: exact FP64 box test for every quantised pass of this B record, from L1/L2
-        const uint32_t ib = (uint32_t)(tb + j);
-        const double2* bp = reinterpret_cast<const double2*>(P.boxB + ib);
-        const double2 l01 = __ldg(bp), l23 = __ldg(bp + 1), g01 = __ldg(bp + 2), g23 = __ldg(bp + 3);
-        for (int r = 0; r < QR; ++r) {
-          const uint32_t ia = abase + r * 32;
-          bool p = false;
-          if (ia >= P.a_begin && ia < P.a_end) {
-            const uint2 l = ld_nc_u2(P.qA + ia);
-            const unsigned x0 = imad_sub((Q7F - l.y) | QG, m1, bq.x), x1 = imad_sub((Q7F - l.x) | QG, m1, bq.y);
-            if ((x0 & x1 & QG) == QG) {
-              ++n_exact;
-              const double2* ap = reinterpret_cast<const double2*>(P.boxA + ia);
-              const double2 a01 = __ldg(ap), a23 = __ldg(ap + 1), c01 = __ldg(ap + 2), c23 = __ldg(ap + 3);
-              p = (l01.x <= c01.x) & (a01.x <= g01.x) & (l01.y <= c01.y) & (a01.y <= g01.y) &
-                  (l23.x <= c23.x) & (a23.x <= g23.x) & (l23.y <= c23.y) & (a23.y <= g23.y);
-            }
-          }
-          const unsigned m = __ballot_sync(0xffffffffu, p);
-          if (m) {
-            if (p) q[qn + __popc(m & lt_mask)] = make_uint2(ia, ib);
-            qn += __popc(m);
-            __syncwarp();
-            if (qn >= 32) {
-              qn -= 32;
-              flush_queue<KIND_TRI>(P, Bt, q + qn, 32, lane, n_pass, n_sing);
-            }
-          }
-        }
+      if (__any_sync(0xffffffffu, (allfail[0] & allfail[1] & allfail[2] & allfail[3]) == 0)) {
+#pragma unroll 1
+        for (int u = 0; u < NJ; ++u) slow((uint32_t)(tb + j + u), bq[u]);
         load_a();
       }
-    }
+    };
+    const int nmain = nvalid - nvalid % C::JB;
+#pragma unroll(C::UNROLL)
+    for (int j = 0; j < nmain; j += C::JB) step(j, std::integral_constant<int, C::JB>());
+    for (int j = nmain; j < nvalid; ++j) step(j, std::integral_constant<int, 1>());
     __syncthreads();  // every warp is done reading stage s
     if (tid == 0 && t + STAGES < ntiles) {
       const uint64_t nb = b0 + (uint64_t)(t + STAGES) * QTILE;
@@ -920,16 +959,15 @@ static int launch_cull(std::vector<SearchParams>& T, Batch Bt, std::vector<uint6
 }
 
 // MCX_MODE_PREFILTER: frame init → union bounds → quantise → prefilter search.
-static int launch_prefilter(std::vector<SearchParams>& T, Batch Bt, std::vector<uint64_t>& prefix, void* dev_tab,
-                            int device, cudaStream_t stream) {
+template <class C>
+static int launch_prefilter_cfg(std::vector<SearchParams>& T, Batch Bt, std::vector<uint64_t>& prefix, void* dev_tab,
+                                int device, cudaStream_t stream) {
   int dev_sms = 148;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device);
-  constexpr int UNROLL = 4;
-  const size_t smem = sizeof(QSmem);
-  CUDA_TRY(cudaFuncSetAttribute(search_prefilter_kernel<UNROLL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem));
+  const size_t smem = sizeof(QSmem<C>);
+  CUDA_TRY(cudaFuncSetAttribute(search_prefilter_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 1;
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, search_prefilter_kernel<UNROLL>, Q_THREADS, smem));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, search_prefilter_kernel<C>, C::THREADS, smem));
   const uint64_t slots = (uint64_t)dev_sms * (occ > 0 ? occ : 1);
   prefix.assign(T.size() + 1, 0);
   uint64_t max_records = 0;
@@ -958,9 +996,24 @@ static int launch_prefilter(std::vector<SearchParams>& T, Batch Bt, std::vector<
   const dim3 grid((unsigned)gx, n);
   qbounds_kernel<<<grid, 256, 0, stream>>>(Bt);
   quant_kernel<<<grid, 256, 0, stream>>>(Bt);
-  search_prefilter_kernel<UNROLL><<<(unsigned)total, Q_THREADS, smem, stream>>>(Bt);
+  search_prefilter_kernel<C><<<(unsigned)total, C::THREADS, smem, stream>>>(Bt);
   CUDA_TRY(cudaGetLastError());
   return MCX_OK;
+}
+
+// Variant selection (MCX_VARIANT, experiments; 0 = the tuned default: 32 A records per
+// thread, one-warp CTAs, one vote per 2 B records — measured on C3 in DESIGN.md §5).
+static int launch_prefilter(std::vector<SearchParams>& T, const Batch& Bt, std::vector<uint64_t>& prefix,
+                            void* dev_tab, int device, cudaStream_t stream) {
+  switch (variant_from_env()) {
+    case 1: return launch_prefilter_cfg<QCfg<32, 1, 4>>(T, Bt, prefix, dev_tab, device, stream);
+    case 2: return launch_prefilter_cfg<QCfg<16, 2, 2>>(T, Bt, prefix, dev_tab, device, stream);
+    case 3: return launch_prefilter_cfg<QCfg<8, 1, 4>>(T, Bt, prefix, dev_tab, device, stream);
+    case 4: return launch_prefilter_cfg<QCfg<16, 1, 4>>(T, Bt, prefix, dev_tab, device, stream);
+    case 5: return launch_prefilter_cfg<QCfg<32, 1, 4, 16>>(T, Bt, prefix, dev_tab, device, stream);
+    case 6: return launch_prefilter_cfg<QCfg<16, 1, 4, 10>>(T, Bt, prefix, dev_tab, device, stream);
+    default: return launch_prefilter_cfg<QCfg<32, 2, 2>>(T, Bt, prefix, dev_tab, device, stream);
+  }
 }
 
 struct Timing {

@@ -112,12 +112,13 @@ def test_parity_small(name, mode, oracle_lib):
     assert r.stats["n_pairs"] == A.shape[2] * (A.shape[1] - 1) * 2 * B.shape[2] * (B.shape[1] - 1) * 2
 
 
-@pytest.mark.parametrize("variant", ["0", "1", "2", "3"])
-def test_kernel_variants_identical(variant, monkeypatch, oracle_lib):
+@pytest.mark.parametrize("mode", [_lib.MODE_BRUTE, _lib.MODE_PREFILTER])
+@pytest.mark.parametrize("variant", ["0", "1", "2", "3", "4", "5", "6"])
+def test_kernel_variants_identical(variant, mode, monkeypatch, oracle_lib):
     monkeypatch.setenv("MCX_VARIANT", variant)
     A, _, B, _ = config_pair("C4i")
     ref = oracle_lib.search(A, B, sweep=True)
-    r = D.search(A, B)
+    r = D.search(A, B, mode=mode)
     assert_same_hits(ref, r.hits, r.stats)
 
 

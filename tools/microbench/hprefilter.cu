@@ -260,6 +260,52 @@ int run2(const char* name, K k, int R, const double* d_in, unsigned* d_out, int 
   return 0;
 }
 
+__device__ __forceinline__ unsigned alu_sub(unsigned a, unsigned b) {
+  unsigned r;
+  asm("sub.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+
+// 3 instructions per pair: 2 subtractions + LOP3 with predicate output chained by AND
+// (PTX lop3.and.b32 d|p).  MIX: every MIX-th pair does its second subtraction on the alu pipe.
+template <int R, int MIX>
+__global__ void __launch_bounds__(256, 1) k_swar3(const double* in, unsigned* out, unsigned m1) {
+  constexpr unsigned G = 0x80808080u;
+  __shared__ uint2 sb[NB];
+  for (int i = threadIdx.x; i < NB; i += blockDim.x) {
+    unsigned v = (unsigned)(in[i % 8] * 1000.0) * 2654435761u + i * 40503u;
+    sb[i] = make_uint2(v & ~G, (v * 3u) & ~G);
+  }
+  unsigned ah[R][2];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int w = 0; w < 2; ++w) ah[r][w] = ((unsigned)(in[(r * 2 + w) % 16] * 977.0 + r) * 2246822519u + threadIdx.x * 7919u) | G;
+  unsigned acc = 0;
+  __syncthreads();
+  for (int it = 0; it < PASSES; ++it) {
+#pragma unroll 4
+    for (int j = 0; j < NB; ++j) {
+      const uint2 b = sb[j];
+      unsigned x[2 * R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        x[2 * r] = imad_sub(ah[r][0], m1, b.x);
+        x[2 * r + 1] = (MIX > 0 && r % MIX == MIX - 1) ? alu_sub(ah[r][1], b.y) : imad_sub(ah[r][1], m1, b.y);
+      }
+      unsigned allfail = 1;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        unsigned d;
+        asm("{\n .reg .pred p;\n setp.ne.u32 p, %1, 0;\n lop3.and.b32 %0|p, %2, %3, %4, 0x2a, p;\n selp.u32 %1, 1, 0, p;\n}"
+            : "=r"(d), "+r"(allfail) : "r"(x[2 * r]), "r"(x[2 * r + 1]), "r"(G));
+      }
+      if (__any_sync(0xffffffffu, allfail == 0)) acc += j;
+    }
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
 int main() {
   int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   double h[16]; for (int i = 0; i < 16; ++i) h[i] = 0.1 * i - 0.7;
@@ -288,5 +334,10 @@ int main() {
   run2("swar7", k_swar<2, 8, 1>, 8, d_in, d_out, nsm);
   run2("swar7", k_swar<2, 16, 1>, 16, d_in, d_out, nsm);
   run2("swar7", k_swar<2, 32, 1>, 32, d_in, d_out, nsm);
+  run2("swar3_mix0", k_swar3<16, 0>, 16, d_in, d_out, nsm);
+  run2("swar3_mix2", k_swar3<16, 2>, 16, d_in, d_out, nsm);
+  run2("swar3_mix3", k_swar3<16, 3>, 16, d_in, d_out, nsm);
+  run2("swar3_mix1", k_swar3<16, 1>, 16, d_in, d_out, nsm);
+  run2("swar3_r32_mix2", k_swar3<32, 2>, 32, d_in, d_out, nsm);
   return 0;
 }

@@ -15,7 +15,7 @@ ap.add_argument("--iters", type=int, default=2)
 a = ap.parse_args()
 A, sa, B, sb = config_pair(a.config)
 Am, Bm = D.DeviceMesh(A, 0), D.DeviceMesh(B, 0)
-m = {"brute": _lib.MODE_BRUTE, "cull": _lib.MODE_CULL}[a.mode]
+m = _lib.MODE_NAMES[a.mode]
 for _ in range(a.iters):
     r = D.search_device(Am, Bm, mode=m, timing=True)
 print(r.stats)
