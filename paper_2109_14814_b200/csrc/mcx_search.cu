@@ -92,10 +92,9 @@ struct __align__(16) SearchParams {
   const double* coordsA;
   const double* coordsB;
   uint32_t NA, MA, NB, MB;
-  // MCX_MODE_PREFILTER only: 8-byte quantised boxes (storage order) and the task's frame
-  uint2* qA;
-  uint2* qB;
-  long long* qframe;  // [8] ordered keys: min lo[4], max hi[4] over both meshes
+  // MCX_MODE_PREFILTER only: conservative fp32 boxes {lo_rd[4]}, {hi_ru[4]} per record
+  float4* fA;
+  float4* fB;
 };
 
 // Whole-launch parameters: the task table and the shared outputs.
@@ -111,7 +110,7 @@ struct Batch {
   uint4* blk_list;               // cull: overlapping (task, local A block, B tile)
   uint64_t blk_cap;
   unsigned long long* list_count;
-  uint32_t neg1;                 // 0xffffffff, a runtime operand so the SWAR subtract stays an IMAD
+  uint32_t neg1;                 // 0xffffffff, a runtime operand so the packed subtract stays an IMAD
 };
 
 // Task owning work unit u: the last t with prefix[t] <= u (n_tasks is small).
@@ -379,57 +378,33 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_brute_kernel(const
 
 // ------------------------------------------------------------ prefilter mode
 // MCX_MODE_PREFILTER: every pair is tested, but first by a conservative integer
-// test on 8-byte quantised boxes that runs on the fma + alu pipes instead of the
-// FP64 pipe; only pairs it cannot reject get the exact FP64 box test (and then
-// the canonical solve), so the AABB-pass / singular / hit sets are exactly those
-// of MCX_MODE_BRUTE.
-//
-// Quantisation (per task, one frame for both meshes): for coordinate c,
-// f_c(x) = (x − o_c)·κ_c with o_c = min lo_c, κ_c = 127 / (max hi_c − o_c), both in
-// RN double arithmetic, so f_c is monotone non-decreasing; qlo = clamp(⌊f(lo)⌋),
-// qhi = clamp(⌈f(hi)⌉) to [0, 127].  Then A.lo_c ≤ B.hi_c ⇒ qloA_c ≤ qhiB_c (and
-// likewise for the other 7 compares): the quantised test never rejects a pair the
-// exact test keeps, whatever the frame (a degenerate frame gives κ = 0, q = 0: no
-// rejection).  Record layout ("L form", 2 words of 4 bytes, byte c = coordinate c):
-// word0 = qlo_c, word1 = 127 − qhi_c.  An A record is turned into the "H form"
-// H0 = (0x7F7F7F7F − word1) | G, H1 = (0x7F7F7F7F − word0) | G, G = 0x80808080;
-// then byte c of H0 − L_B0 is 128 + qhiA_c − qloB_c ∈ [1, 255] (no borrow between
-// bytes) and has its guard bit set iff qloB_c ≤ qhiA_c, and H1 − L_B1 likewise
-// tests qloA_c ≤ qhiB_c.  A pair passes iff all 8 guard bits of the two
-// differences are set: 2 IMAD (fma pipe) + 1 LOP3 + 1 ISETP (alu) per pair instead
-// of 8 DSETP on the 64-lane/clk FP64 pipe.
-constexpr int QTILE = 1024;              // B records per shared-memory stage (8 KB)
+// test on quantised boxes that runs on the fma + alu pipes instead of the FP64 pipe
+// (64 lanes/clk/SM on B200, 8 DSETP per pair); only pairs it cannot reject get the
+// exact FP64 box test and then the canonical solve, so the AABB-pass / singular /
+// hit sets are exactly those of MCX_MODE_BRUTE.
+//   * fp32 boxes rounded outwards (lo toward −∞, hi toward +∞) are computed once per
+//     call (fbox_kernel).  Every later step is a monotone fp32 function of them, so
+//     A.lo ≤ B.hi ⇒ qlo_A ≤ qhi_B: the quantised test only ever keeps extra pairs.
+//   * Frame = union box of the CTA's own A block (1024 records): o_c = min lo_c,
+//     κ_c = 6 / (max hi_c − o_c) (0 if the extent is 0 or not finite);
+//     q(x) = clamp(⌊(x − o)·κ⌋ or ⌈·⌉, 0, 6).  3 bits per bound suffice in a frame
+//     that small, so all 8 compares of a pair fit ONE 32-bit word of eight 4-bit
+//     fields (value 0..6 + guard bit 3).
+//   * B words: nibble c = qlo_c, nibble 4+c = 6 − qhi_c.  A B record whose fp32 box
+//     misses the frame cannot overlap any record of the block: it gets nibble 0 = 7,
+//     which fails against every A word because qhi_A ≤ 6.
+//   * A words: nibble c = 8 + qhi_c, nibble 4+c = 14 − qlo_c.  H − L then has, per
+//     nibble, 8 + qhi_A − qlo_B ∈ [1, 15] (no borrow between nibbles) — guard bit
+//     set iff qlo_B ≤ qhi_A — and 8 + qhi_B − qlo_A.  Invalid A slots: 0x77777777.
+//   * Pair test = IMAD (L·(−1) + H, fma pipe) + LOP3.LUT.PAND (~x & G, alu pipe,
+//     predicate output ANDed into one of 4 "all fail" chains): 2 instructions,
+//     balanced across the two pipes.  One warp vote per JB B records.
+//   * B records reach shared memory as fp32 boxes (bulk copies, 8 KB stages); the
+//     CTA quantises each tile into its frame (~1/50 of the test work) before testing.
+//   * On a vote the warp re-tests that B record against its A words (kept in shared
+//     memory) and runs the exact FP64 box test on the quantised passes from L1/L2;
+//     survivors are queued and solved exactly like the FP64 kernel.
 constexpr int Q_QCAP = 64;
-constexpr unsigned QG = 0x80808080u;
-constexpr unsigned Q7F = 0x7F7F7F7Fu;
-
-// Prefilter kernel variant: QR A records per thread (a warp covers 32·QR consecutive
-// storage positions of the 1024-record A block), JB B records per warp vote.
-template <int QR_, int JB_, int UNROLL_, int MINB_ = 1>
-struct QCfg {
-  static constexpr int QR = QR_;
-  static constexpr int MINB = MINB_;      // resident CTAs per SM the register cap targets
-  static constexpr int JB = JB_;
-  static constexpr int UNROLL = UNROLL_;
-  static constexpr int THREADS = A_BLOCK / QR_;
-  static constexpr int WARPS = THREADS / 32;
-};
-
-template <class C>
-struct __align__(16) QSmem {
-  uint2 tile[STAGES][QTILE];
-  uint2 queue[C::WARPS][Q_QCAP];
-  unsigned long long full[STAGES];
-};
-
-// Order-preserving map of finite doubles onto signed 64-bit keys (for atomicMin/Max).
-__device__ __forceinline__ long long okey(double x) {
-  const long long b = __double_as_longlong(x);
-  return b >= 0 ? b : b ^ 0x7fffffffffffffffll;
-}
-__device__ __forceinline__ double okey_inv(long long k) {
-  return __longlong_as_double(k >= 0 ? k : k ^ 0x7fffffffffffffffll);
-}
 
 // a − b computed as b·(−1) + a on the fma pipe (m1 = 0xffffffff at run time).
 __device__ __forceinline__ unsigned imad_sub(unsigned a, unsigned m1, unsigned b) {
@@ -438,110 +413,70 @@ __device__ __forceinline__ unsigned imad_sub(unsigned a, unsigned m1, unsigned b
   return r;
 }
 
-// a − b on the alu pipe (IADD3); half of the pair tests use it so that neither the
-// fma nor the alu pipe saturates before instruction issue does.
-__device__ __forceinline__ unsigned alu_sub(unsigned a, unsigned b) {
-  unsigned r;
-  asm("sub.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
-  return r;
-}
+constexpr int FTILE = 256;  // B records per stage (256 × 32 B = 8 KB)
+constexpr unsigned G4 = 0x88888888u;
 
-// allfail &= "the pair with differences x0, x1 fails": one LOP3 with predicate output
-// (SASS LOP3.LUT.PAND), LUT 0x2a = (~x0 | ~x1) & G, nonzero iff a guard bit is missing.
-__device__ __forceinline__ void fail_and(unsigned& allfail, unsigned x0, unsigned x1) {
+template <int QR_, int JB_, int UNROLL_, int MINB_ = 1>
+struct LCfg {
+  static constexpr int QR = QR_;
+  static constexpr int JB = JB_;
+  static constexpr int UNROLL = UNROLL_;
+  static constexpr int MINB = MINB_;
+  static constexpr int THREADS = A_BLOCK / QR_;
+  static constexpr int WARPS = THREADS / 32;
+  static_assert(WARPS >= 1 && THREADS % 32 == 0, "QR must leave whole warps in a 1024-record block");
+};
+
+template <class C>
+struct __align__(16) LSmem {
+  float4 tile[STAGES][FTILE][2];
+  unsigned qt[FTILE];
+  uint2 queue[C::WARPS][Q_QCAP];
+  float frame[C::WARPS][8];
+  float fr[16];
+  unsigned aw[C::WARPS][C::QR][32];  // the A words, reloaded from here after a slow path
+  unsigned long long full[STAGES];
+};
+
+// allfail &= "x has a guard bit clear" (LOP3 LUT 0x0a = ~x & G4).
+__device__ __forceinline__ void fail_and1(unsigned& allfail, unsigned x) {
   unsigned d;  // LOP3 result (unused: only its != 0 predicate matters)
-  asm("{\n .reg .pred p;\n setp.ne.u32 p, %1, 0;\n lop3.and.b32 %0|p, %2, %3, %4, 0x2a, p;\n selp.u32 %1, 1, 0, p;\n}"
+  asm("{\n .reg .pred p;\n setp.ne.u32 p, %1, 0;\n lop3.and.b32 %0|p, %2, %2, %3, 0x0a, p;\n selp.u32 %1, 1, 0, p;\n}"
       : "=r"(d), "+r"(allfail)
-      : "r"(x0), "r"(x1), "r"(QG));
+      : "r"(x), "r"(G4));
 }
 
-__device__ __forceinline__ uint2 ld_nc_u2(const uint2* p) {
-  uint2 v;
-  asm volatile("ld.global.nc.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
-  return v;
-}
-
-__global__ void qframe_init_kernel(const Batch Bt) {
-  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= Bt.n_tasks) return;
-  long long* f = Bt.tasks[t].qframe;
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    f[c] = 0x7fffffffffffffffll;
-    f[4 + c] = (long long)0x8000000000000000ull;
-  }
-}
-
-// Union box of A and B per task (blockIdx.y = task): warp min/max, 8 atomics per warp.
-__global__ void __launch_bounds__(256) qbounds_kernel(const Batch Bt) {
+// Conservative fp32 boxes of A and B per task (blockIdx.y = task).
+__global__ void __launch_bounds__(256) fbox_kernel(const Batch Bt) {
   const SearchParams& P = Bt.tasks[blockIdx.y];
   const Box* boxA = P.boxA;
   const Box* boxB = P.boxB;
   const uint64_t nA = P.nA, n = nA + P.nB;
-  double lo[4], hi[4];
-  empty_box(lo, hi);
   for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x) {
     const double2* b = reinterpret_cast<const double2*>(k < nA ? boxA + k : boxB + (k - nA));
     const double2 l01 = __ldg(b), l23 = __ldg(b + 1), h01 = __ldg(b + 2), h23 = __ldg(b + 3);
-    lo[0] = fmin(lo[0], l01.x); lo[1] = fmin(lo[1], l01.y); lo[2] = fmin(lo[2], l23.x); lo[3] = fmin(lo[3], l23.y);
-    hi[0] = fmax(hi[0], h01.x); hi[1] = fmax(hi[1], h01.y); hi[2] = fmax(hi[2], h23.x); hi[3] = fmax(hi[3], h23.y);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      lo[c] = fmin(lo[c], __shfl_xor_sync(0xffffffffu, lo[c], o));
-      hi[c] = fmax(hi[c], __shfl_xor_sync(0xffffffffu, hi[c], o));
-    }
-  if ((threadIdx.x & 31) == 0 && lo[0] <= hi[0]) {
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      atomicMin(P.qframe + c, okey(lo[c]));
-      atomicMax(P.qframe + 4 + c, okey(hi[c]));
-    }
+    const float4 lo = make_float4(__double2float_rd(l01.x), __double2float_rd(l01.y), __double2float_rd(l23.x),
+                                  __double2float_rd(l23.y));
+    const float4 hi = make_float4(__double2float_ru(h01.x), __double2float_ru(h01.y), __double2float_ru(h23.x),
+                                  __double2float_ru(h23.y));
+    float4* dst = k < nA ? P.fA + 2 * k : P.fB + 2 * (k - nA);
+    dst[0] = lo;
+    dst[1] = hi;
   }
 }
 
-// Quantised L-form records of A and B per task (blockIdx.y = task).
-__global__ void __launch_bounds__(256) quant_kernel(const Batch Bt) {
-  const SearchParams& P = Bt.tasks[blockIdx.y];
-  double o[4], kap[4];
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    o[c] = okey_inv(P.qframe[c]);
-    const double e = __dsub_rn(okey_inv(P.qframe[4 + c]), o[c]);
-    double k = (e > 0.0) ? __ddiv_rn(127.0, e) : 0.0;  // e NaN/inf/<=0 → no quantisation
-    if (!(k < 1.0e300)) k = 0.0;
-    kap[c] = k;
-  }
-  const Box* boxA = P.boxA;
-  const Box* boxB = P.boxB;
-  const uint64_t nA = P.nA, n = nA + P.nB;
-  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x) {
-    const double* b = reinterpret_cast<const double*>(k < nA ? boxA + k : boxB + (k - nA));
-    unsigned w0 = 0, w1 = 0;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      unsigned ql = 0, qh = 0;
-      if (kap[c] > 0.0) {
-        const double fl = floor(__dmul_rn(__dsub_rn(__ldg(b + c), o[c]), kap[c]));
-        const double fh = ceil(__dmul_rn(__dsub_rn(__ldg(b + 4 + c), o[c]), kap[c]));
-        ql = (unsigned)fmin(fmax(fl, 0.0), 127.0);
-        qh = (unsigned)fmin(fmax(fh, 0.0), 127.0);
-      }
-      w0 |= ql << (8 * c);
-      w1 |= (127u - qh) << (8 * c);
-    }
-    if (k < nA) P.qA[k] = make_uint2(w0, w1);
-    else P.qB[k - nA] = make_uint2(w0, w1);
-  }
+__device__ __forceinline__ unsigned qfloor(float x, float o, float k) {
+  return (unsigned)__float2int_rd(fminf(fmaxf(__fmul_rn(__fsub_rn(x, o), k), 0.f), 6.f));
+}
+__device__ __forceinline__ unsigned qceil(float x, float o, float k) {
+  return (unsigned)__float2int_ru(fminf(fmaxf(__fmul_rn(__fsub_rn(x, o), k), 0.f), 6.f));
 }
 
 template <class C>
-__global__ void __launch_bounds__(C::THREADS, C::MINB) search_prefilter_kernel(const Batch Bt) {
+__global__ void __launch_bounds__(C::THREADS, C::MINB) search_local_kernel(const Batch Bt) {
   constexpr int QR = C::QR;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  QSmem<C>& S = *reinterpret_cast<QSmem<C>*>(smem_raw);
+  LSmem<C>& S = *reinterpret_cast<LSmem<C>*>(smem_raw);
   __shared__ SearchParams Ps;
   __shared__ uint64_t s_unit;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -557,7 +492,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_prefilter_kernel(c
   const uint64_t a0 = gblk * A_BLOCK;
   const uint64_t b0 = (unit % P.nchunk) * P.b_chunk;
   const uint64_t b1 = min(b0 + P.b_chunk, P.nB);
-  const int ntiles = (int)((b1 - b0 + QTILE - 1) / QTILE);
+  const int ntiles = (int)((b1 - b0 + FTILE - 1) / FTILE);
   const unsigned m1 = Bt.neg1;
 
   if (tid == 0) {
@@ -567,29 +502,72 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_prefilter_kernel(c
   __syncthreads();
   if (tid == 0) {
     for (int s = 0; s < STAGES && s < ntiles; ++s) {
-      const uint64_t tb = b0 + (uint64_t)s * QTILE;
-      const uint32_t bytes = (uint32_t)((min((uint64_t)QTILE, b1 - tb) * sizeof(uint2) + 15) & ~15ull);
+      const uint64_t tb = b0 + (uint64_t)s * FTILE;
+      const uint32_t bytes = (uint32_t)(min((uint64_t)FTILE, b1 - tb) * 32);
       mbar_arrive_expect_tx(&S.full[s], bytes);
-      bulk_g2s(&S.tile[s][0], P.qB + tb, bytes, &S.full[s]);
+      bulk_g2s(&S.tile[s][0][0], P.fB + 2 * tb, bytes, &S.full[s]);
     }
   }
 
-  // A records of this thread: warp w covers storage positions a0 + 32·QR·w + [0, 32·QR)
+  // ---- frame of the block: union of the CTA's valid A records (all warps)
   const uint32_t abase = (uint32_t)(a0 + (uint64_t)warp * (QR * 32) + lane);
-  unsigned h0[QR], h1[QR];
+  float lo[4], hi[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) { lo[c] = __int_as_float(0x7f800000); hi[c] = -lo[c]; }
+#pragma unroll 4
+  for (int r = 0; r < QR; ++r) {
+    const uint32_t ia = abase + r * 32;
+    if (ia >= P.a_begin && ia < P.a_end) {
+      const float4 l = __ldg(P.fA + 2 * (uint64_t)ia), h = __ldg(P.fA + 2 * (uint64_t)ia + 1);
+      lo[0] = fminf(lo[0], l.x); lo[1] = fminf(lo[1], l.y); lo[2] = fminf(lo[2], l.z); lo[3] = fminf(lo[3], l.w);
+      hi[0] = fmaxf(hi[0], h.x); hi[1] = fmaxf(hi[1], h.y); hi[2] = fmaxf(hi[2], h.z); hi[3] = fmaxf(hi[3], h.w);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      lo[c] = fminf(lo[c], __shfl_xor_sync(0xffffffffu, lo[c], o));
+      hi[c] = fmaxf(hi[c], __shfl_xor_sync(0xffffffffu, hi[c], o));
+    }
+  if (lane == 0) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) { S.frame[warp][c] = lo[c]; S.frame[warp][4 + c] = hi[c]; }
+  }
+  __syncthreads();
+  // frame parameters in shared memory: fr[0..3] = o_c, fr[4..7] = κ_c, fr[8..11] = lo_c, fr[12..15] = hi_c
+  if (tid < 4) {
+    const int c = tid;
+    float l = S.frame[0][c], h = S.frame[0][4 + c];
+    for (int w = 1; w < C::WARPS; ++w) { l = fminf(l, S.frame[w][c]); h = fmaxf(h, S.frame[w][4 + c]); }
+    const float e = __fsub_rn(h, l);
+    float k = (e > 0.f && e < 3.0e38f) ? __fdiv_rn(6.f, e) : 0.f;  // also 0 for an empty block (l > h)
+    if (!(k < 3.0e38f)) k = 0.f;
+    S.fr[c] = (k > 0.f) ? l : 0.f;
+    S.fr[4 + c] = k;
+    S.fr[8 + c] = l;
+    S.fr[12 + c] = h;
+  }
+  __syncthreads();
+
+  // ---- A words in registers
+  auto a_word = [&](uint32_t ia) -> unsigned {
+    const float* fr = S.fr;
+    const float4 l = __ldg(P.fA + 2 * (uint64_t)ia), h = __ldg(P.fA + 2 * (uint64_t)ia + 1);
+    return ((8u + qceil(h.x, fr[0], fr[4])) << 0) | ((8u + qceil(h.y, fr[1], fr[5])) << 4) |
+           ((8u + qceil(h.z, fr[2], fr[6])) << 8) | ((8u + qceil(h.w, fr[3], fr[7])) << 12) |
+           ((14u - qfloor(l.x, fr[0], fr[4])) << 16) | ((14u - qfloor(l.y, fr[1], fr[5])) << 20) |
+           ((14u - qfloor(l.z, fr[2], fr[6])) << 24) | ((14u - qfloor(l.w, fr[3], fr[7])) << 28);
+  };
+  for (int r = 0; r < QR; ++r) {
+    const uint32_t ia = abase + r * 32;
+    S.aw[warp][r][lane] = (ia >= P.a_begin && ia < P.a_end) ? a_word(ia) : 0x77777777u;  // all guards clear
+  }
+  __syncwarp();
+  unsigned hw[QR];
   auto load_a = [&]() {
 #pragma unroll
-    for (int r = 0; r < QR; ++r) {
-      const uint32_t ia = abase + r * 32;
-      if (ia >= P.a_begin && ia < P.a_end) {
-        const uint2 l = ld_nc_u2(P.qA + ia);
-        h0[r] = (Q7F - l.y) | QG;
-        h1[r] = (Q7F - l.x) | QG;
-      } else {
-        h0[r] = Q7F;  // guard bits clear in every byte of H0 − L_B0: never passes
-        h1[r] = Q7F;
-      }
-    }
+    for (int r = 0; r < QR; ++r) hw[r] = *(volatile unsigned*)&S.aw[warp][r][lane];
   };
   load_a();
 
@@ -598,24 +576,18 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_prefilter_kernel(c
   unsigned long long n_pass = 0, n_sing = 0, n_exact = 0;
   const unsigned lt_mask = (1u << lane) - 1u;
 
-  // Rare path for B record ib (quantised form bq): the exact FP64 box test for every
-  // quantised pass of this warp, reading A's records from L1/L2 (registers stay free).
-  auto slow = [&](uint32_t ib, uint2 bq) {
+  auto slow = [&](uint32_t ib, unsigned bw) {
     const double2* bp = reinterpret_cast<const double2*>(P.boxB + ib);
     const double2 l01 = __ldg(bp), l23 = __ldg(bp + 1), g01 = __ldg(bp + 2), g23 = __ldg(bp + 3);
     for (int r = 0; r < QR; ++r) {
       const uint32_t ia = abase + r * 32;
       bool p = false;
-      if (ia >= P.a_begin && ia < P.a_end) {
-        const uint2 l = ld_nc_u2(P.qA + ia);
-        const unsigned x0 = imad_sub((Q7F - l.y) | QG, m1, bq.x), x1 = imad_sub((Q7F - l.x) | QG, m1, bq.y);
-        if ((x0 & x1 & QG) == QG) {
-          ++n_exact;
-          const double2* ap = reinterpret_cast<const double2*>(P.boxA + ia);
-          const double2 a01 = __ldg(ap), a23 = __ldg(ap + 1), c01 = __ldg(ap + 2), c23 = __ldg(ap + 3);
-          p = (l01.x <= c01.x) & (a01.x <= g01.x) & (l01.y <= c01.y) & (a01.y <= g01.y) &
-              (l23.x <= c23.x) & (a23.x <= g23.x) & (l23.y <= c23.y) & (a23.y <= g23.y);
-        }
+      if (((S.aw[warp][r][lane] - bw) & G4) == G4) {  // quantised pass (invalid slots never pass)
+        ++n_exact;
+        const double2* ap = reinterpret_cast<const double2*>(P.boxA + ia);
+        const double2 a01 = __ldg(ap), a23 = __ldg(ap + 1), c01 = __ldg(ap + 2), c23 = __ldg(ap + 3);
+        p = (l01.x <= c01.x) & (a01.x <= g01.x) & (l01.y <= c01.y) & (a01.y <= g01.y) &
+            (l23.x <= c23.x) & (a23.x <= g23.x) & (l23.y <= c23.y) & (a23.y <= g23.y);
       }
       const unsigned m = __ballot_sync(0xffffffffu, p);
       if (m) {
@@ -633,23 +605,36 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_prefilter_kernel(c
   for (int t = 0; t < ntiles; ++t) {
     const int s = t % STAGES;
     mbar_wait(&S.full[s], (uint32_t)((t / STAGES) & 1));
-    const uint64_t tb = b0 + (uint64_t)t * QTILE;
-    const int nvalid = (int)min((uint64_t)QTILE, b1 - tb);
-    const uint2* tile = S.tile[s];
+    const uint64_t tb = b0 + (uint64_t)t * FTILE;
+    const int nvalid = (int)min((uint64_t)FTILE, b1 - tb);
+    // quantise this tile's B records into the block frame (all threads)
+    for (int j = tid; j < nvalid; j += C::THREADS) {
+      const float* fr = S.fr;
+      const float4 l = S.tile[s][j][0], h = S.tile[s][j][1];
+      const bool in = (l.x <= fr[12]) & (fr[8] <= h.x) & (l.y <= fr[13]) & (fr[9] <= h.y) & (l.z <= fr[14]) &
+                      (fr[10] <= h.z) & (l.w <= fr[15]) & (fr[11] <= h.w);
+      unsigned w = 7u;  // misses the frame: nibble 0 = 7 fails against every A word
+      if (in)
+        w = qfloor(l.x, fr[0], fr[4]) | (qfloor(l.y, fr[1], fr[5]) << 4) | (qfloor(l.z, fr[2], fr[6]) << 8) |
+            (qfloor(l.w, fr[3], fr[7]) << 12) | ((6u - qceil(h.x, fr[0], fr[4])) << 16) |
+            ((6u - qceil(h.y, fr[1], fr[5])) << 20) | ((6u - qceil(h.z, fr[2], fr[6])) << 24) |
+            ((6u - qceil(h.w, fr[3], fr[7])) << 28);
+      S.qt[j] = w;
+    }
+    __syncthreads();
     auto step = [&](int j, auto jb_c) {
       constexpr int NJ = decltype(jb_c)::value;
-      uint2 bq[NJ];
-      unsigned allfail[4] = {1, 1, 1, 1};  // 4 independent predicate chains (latency)
+      unsigned bw[NJ];
+      unsigned allfail[4] = {1, 1, 1, 1};
 #pragma unroll
       for (int u = 0; u < NJ; ++u) {
-        bq[u] = tile[j + u];
+        bw[u] = S.qt[j + u];
 #pragma unroll
-        for (int r = 0; r < QR; ++r)
-          fail_and(allfail[r & 3], imad_sub(h0[r], m1, bq[u].x), alu_sub(h1[r], bq[u].y));
+        for (int r = 0; r < QR; ++r) fail_and1(allfail[r & 3], imad_sub(hw[r], m1, bw[u]));
       }
       if (__any_sync(0xffffffffu, (allfail[0] & allfail[1] & allfail[2] & allfail[3]) == 0)) {
 #pragma unroll 1
-        for (int u = 0; u < NJ; ++u) slow((uint32_t)(tb + j + u), bq[u]);
+        for (int u = 0; u < NJ; ++u) slow((uint32_t)(tb + j + u), S.qt[j + u]);
         load_a();
       }
     };
@@ -657,12 +642,12 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_prefilter_kernel(c
 #pragma unroll(C::UNROLL)
     for (int j = 0; j < nmain; j += C::JB) step(j, std::integral_constant<int, C::JB>());
     for (int j = nmain; j < nvalid; ++j) step(j, std::integral_constant<int, 1>());
-    __syncthreads();  // every warp is done reading stage s
+    __syncthreads();  // every warp is done reading stage s and qt
     if (tid == 0 && t + STAGES < ntiles) {
-      const uint64_t nb = b0 + (uint64_t)(t + STAGES) * QTILE;
-      const uint32_t bytes = (uint32_t)((min((uint64_t)QTILE, b1 - nb) * sizeof(uint2) + 15) & ~15ull);
+      const uint64_t nb = b0 + (uint64_t)(t + STAGES) * FTILE;
+      const uint32_t bytes = (uint32_t)(min((uint64_t)FTILE, b1 - nb) * 32);
       mbar_arrive_expect_tx(&S.full[s], bytes);
-      bulk_g2s(&S.tile[s][0], P.qB + nb, bytes, &S.full[s]);
+      bulk_g2s(&S.tile[s][0][0], P.fB + 2 * nb, bytes, &S.full[s]);
     }
   }
   __syncwarp();
@@ -861,11 +846,11 @@ __global__ void __launch_bounds__(CULL_THREADS) cull_pairs_kernel(const Batch Bt
 // B chunk count for one task: every CTA of a task does the same work, so pick the
 // count whose CTA total best fills whole waves of resident CTAs (the last partial
 // wave idles the rest of the GPU), among counts giving >= 8 waves with chunks of
-// >= 16 tiles (1 tile for small problems).
-static void choose_chunks(SearchParams& P, uint64_t slots) {
+// >= min_tiles tiles (1 tile for small problems).
+static void choose_chunks(SearchParams& P, uint64_t slots, uint64_t min_tiles = 16) {
   const uint64_t max_chunks = (P.nB + TILE - 1) / TILE;
   uint64_t nchunk = 1, chunk = max_chunks * TILE;
-  const uint64_t min_ch = (P.my_blocks * max_chunks < 8 * slots) ? (uint64_t)TILE : 16 * (uint64_t)TILE;
+  const uint64_t min_ch = (P.my_blocks * max_chunks < 8 * slots) ? (uint64_t)TILE : min_tiles * (uint64_t)TILE;
   double best = -1.0;
   for (uint64_t c = 1; c <= max_chunks && c <= 4096; ++c) {
     const uint64_t ch = ((P.nB + c - 1) / c + TILE - 1) / TILE * TILE;
@@ -958,21 +943,21 @@ static int launch_cull(std::vector<SearchParams>& T, Batch Bt, std::vector<uint6
   return MCX_OK;
 }
 
-// MCX_MODE_PREFILTER: frame init → union bounds → quantise → prefilter search.
+// MCX_MODE_PREFILTER: conservative fp32 boxes → prefilter search.
 template <class C>
-static int launch_prefilter_cfg(std::vector<SearchParams>& T, Batch Bt, std::vector<uint64_t>& prefix, void* dev_tab,
-                                int device, cudaStream_t stream) {
+static int launch_local_cfg(std::vector<SearchParams>& T, Batch Bt, std::vector<uint64_t>& prefix, void* dev_tab,
+                            int device, cudaStream_t stream) {
   int dev_sms = 148;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device);
-  const size_t smem = sizeof(QSmem<C>);
-  CUDA_TRY(cudaFuncSetAttribute(search_prefilter_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const size_t smem = sizeof(LSmem<C>);
+  CUDA_TRY(cudaFuncSetAttribute(search_local_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 1;
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, search_prefilter_kernel<C>, C::THREADS, smem));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, search_local_kernel<C>, C::THREADS, smem));
   const uint64_t slots = (uint64_t)dev_sms * (occ > 0 ? occ : 1);
   prefix.assign(T.size() + 1, 0);
   uint64_t max_records = 0;
   for (size_t t = 0; t < T.size(); ++t) {
-    if (T[t].my_blocks && T[t].nB) choose_chunks(T[t], slots); else T[t].nchunk = 0;
+    if (T[t].my_blocks && T[t].nB) choose_chunks(T[t], slots, 2); else T[t].nchunk = 0;
     prefix[t + 1] = prefix[t] + T[t].my_blocks * T[t].nchunk;
     if (T[t].nchunk) max_records = std::max<uint64_t>(max_records, T[t].nA + T[t].nB);
   }
@@ -988,31 +973,26 @@ static int launch_prefilter_cfg(std::vector<SearchParams>& T, Batch Bt, std::vec
   Bt.prefix = reinterpret_cast<const uint64_t*>((char*)dev_tab + tab);
   Bt.neg1 = 0xffffffffu;
   const unsigned n = (unsigned)T.size();
-  qframe_init_kernel<<<(n + 127) / 128, 128, 0, stream>>>(Bt);
-  // ~4 records per thread, at most 8 blocks per SM in total across the tasks
   uint64_t gx = (max_records + 1023) / 1024;
   const uint64_t gcap = std::max<uint64_t>(1, (uint64_t)dev_sms * 8 / n);
   if (gx > gcap) gx = gcap;
-  const dim3 grid((unsigned)gx, n);
-  qbounds_kernel<<<grid, 256, 0, stream>>>(Bt);
-  quant_kernel<<<grid, 256, 0, stream>>>(Bt);
-  search_prefilter_kernel<C><<<(unsigned)total, C::THREADS, smem, stream>>>(Bt);
+  fbox_kernel<<<dim3((unsigned)gx, n), 256, 0, stream>>>(Bt);
+  search_local_kernel<C><<<(unsigned)total, C::THREADS, smem, stream>>>(Bt);
   CUDA_TRY(cudaGetLastError());
   return MCX_OK;
 }
 
-// Variant selection (MCX_VARIANT, experiments; 0 = the tuned default: 32 A records per
-// thread, one-warp CTAs, one vote per 2 B records — measured on C3 in DESIGN.md §5).
+// Variant selection (MCX_VARIANT, experiments; 0 = the tuned default: 16 A records per
+// thread, 2-warp CTAs, one vote per 8 B records — measured in DESIGN.md §5).
 static int launch_prefilter(std::vector<SearchParams>& T, const Batch& Bt, std::vector<uint64_t>& prefix,
                             void* dev_tab, int device, cudaStream_t stream) {
   switch (variant_from_env()) {
-    case 1: return launch_prefilter_cfg<QCfg<32, 1, 4>>(T, Bt, prefix, dev_tab, device, stream);
-    case 2: return launch_prefilter_cfg<QCfg<16, 2, 2>>(T, Bt, prefix, dev_tab, device, stream);
-    case 3: return launch_prefilter_cfg<QCfg<8, 1, 4>>(T, Bt, prefix, dev_tab, device, stream);
-    case 4: return launch_prefilter_cfg<QCfg<16, 1, 4>>(T, Bt, prefix, dev_tab, device, stream);
-    case 5: return launch_prefilter_cfg<QCfg<32, 1, 4, 16>>(T, Bt, prefix, dev_tab, device, stream);
-    case 6: return launch_prefilter_cfg<QCfg<16, 1, 4, 10>>(T, Bt, prefix, dev_tab, device, stream);
-    default: return launch_prefilter_cfg<QCfg<32, 2, 2>>(T, Bt, prefix, dev_tab, device, stream);
+    case 1: return launch_local_cfg<LCfg<32, 2, 2>>(T, Bt, prefix, dev_tab, device, stream);
+    case 2: return launch_local_cfg<LCfg<32, 4, 1>>(T, Bt, prefix, dev_tab, device, stream);
+    case 3: return launch_local_cfg<LCfg<32, 8, 1>>(T, Bt, prefix, dev_tab, device, stream);
+    case 4: return launch_local_cfg<LCfg<16, 4, 1>>(T, Bt, prefix, dev_tab, device, stream);
+    case 5: return launch_local_cfg<LCfg<8, 4, 1>>(T, Bt, prefix, dev_tab, device, stream);
+    default: return launch_local_cfg<LCfg<16, 8, 1>>(T, Bt, prefix, dev_tab, device, stream);
   }
 }
 
@@ -1051,13 +1031,12 @@ static uint64_t align16(uint64_t v) { return (v + 15) & ~15ull; }
 
 struct WsLayout {
   uint64_t counters, table, list, total, list_cap;
-  uint64_t quant;  // MCX_MODE_PREFILTER: per task 64 B frame + quantised A and B records
+  uint64_t quant;  // MCX_MODE_PREFILTER: per task conservative fp32 boxes of A and B
 };
 
-// Bytes of one task's quantisation area: frame, then A's and B's 8-byte records,
-// each padded so the 16-byte-rounded bulk copy of a tail tile stays inside.
+// Bytes of one task's prefilter area: A's and B's conservative fp32 boxes (32 B each).
 static uint64_t quant_task_bytes(uint64_t nA, uint64_t nB) {
-  return 64 + align16(8 * (nA + 2)) + align16(8 * (nB + 2));
+  return 32 * (nA + nB);
 }
 
 static WsLayout ws_layout(const mcx_task* tasks, uint32_t n, const mcx_opts* o) {
@@ -1145,9 +1124,8 @@ static int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mc
     P.statusA = A->status;
     P.statusB = B->status;
     if (o->mode == MCX_MODE_PREFILTER) {
-      P.qframe = reinterpret_cast<long long*>(ws + qoff);
-      P.qA = reinterpret_cast<uint2*>(ws + qoff + 64);
-      P.qB = reinterpret_cast<uint2*>(ws + qoff + 64 + align16(8 * (A->n_tri + 2)));
+      P.fA = reinterpret_cast<float4*>(ws + qoff);
+      P.fB = P.fA + 2 * A->n_tri;
       qoff += quant_task_bytes(A->n_tri, B->n_tri);
     }
     st[t] = mcx_stats{};
