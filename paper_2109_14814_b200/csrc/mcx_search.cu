@@ -396,9 +396,11 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_brute_kernel(const
 //   * A words: nibble c = 8 + qhi_c, nibble 4+c = 14 − qlo_c.  H − L then has, per
 //     nibble, 8 + qhi_A − qlo_B ∈ [1, 15] (no borrow between nibbles) — guard bit
 //     set iff qlo_B ≤ qhi_A — and 8 + qhi_B − qlo_A.  Invalid A slots: 0x77777777.
-//   * Pair test = IMAD (L·(−1) + H, fma pipe) + LOP3.LUT.PAND (~x & G, alu pipe,
-//     predicate output ANDed into one of 4 "all fail" chains): 2 instructions,
-//     balanced across the two pipes.  One warp vote per JB B records.
+//   * Pair test = IMAD (L·(−1) + H, fma pipe) + half a LOP3.LUT.PAND (alu pipe): one
+//     LOP3 with LUT ~x_a & ~x_b & G per two A words, predicate output ANDed into one of
+//     4 "all fail" chains — "both fail at a common guard position", a conservative
+//     "both fail".  1.5 instructions per pair; the fma pipe (IMAD, 64 lanes/clk/SM)
+//     binds.  One warp vote per JB B records.
 //   * B records reach shared memory as fp32 boxes (bulk copies, 8 KB stages); the
 //     CTA quantises each tile into its frame (~1/50 of the test work) before testing.
 //   * On a vote the warp re-tests that B record against its A words (kept in shared
@@ -416,8 +418,9 @@ __device__ __forceinline__ unsigned imad_sub(unsigned a, unsigned m1, unsigned b
 constexpr int FTILE = 256;  // B records per stage (256 × 32 B = 8 KB)
 constexpr unsigned G4 = 0x88888888u;
 
-template <int QR_, int JB_, int UNROLL_, int MINB_ = 1>
+template <int QR_, int JB_, int UNROLL_, int MINB_ = 1, bool PAIR2_ = false>
 struct LCfg {
+  static constexpr bool PAIR2 = PAIR2_;  // one LOP3 for two pair tests (conservative "both fail")
   static constexpr int QR = QR_;
   static constexpr int JB = JB_;
   static constexpr int UNROLL = UNROLL_;
@@ -437,6 +440,17 @@ struct __align__(16) LSmem {
   unsigned aw[C::WARPS][C::QR][32];  // the A words, reloaded from here after a slow path
   unsigned long long full[STAGES];
 };
+
+// allfail &= "x_a and x_b have a guard bit clear at a common position" (LOP3 LUT 0x02 =
+// ~x_a & ~x_b & G4): true only if both pairs fail, so it is a conservative "both fail"
+// (a pass of either clears it; two fails at different positions give a spurious vote,
+// which the slow path resolves).  One alu instruction per two pair tests.
+__device__ __forceinline__ void fail_and2(unsigned& allfail, unsigned xa, unsigned xb) {
+  unsigned d;  // LOP3 result (unused: only its != 0 predicate matters)
+  asm("{\n .reg .pred p;\n setp.ne.u32 p, %1, 0;\n lop3.and.b32 %0|p, %2, %3, %4, 0x02, p;\n selp.u32 %1, 1, 0, p;\n}"
+      : "=r"(d), "+r"(allfail)
+      : "r"(xa), "r"(xb), "r"(G4));
+}
 
 // allfail &= "x has a guard bit clear" (LOP3 LUT 0x0a = ~x & G4).
 __device__ __forceinline__ void fail_and1(unsigned& allfail, unsigned x) {
@@ -629,8 +643,14 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_local_kernel(const
 #pragma unroll
       for (int u = 0; u < NJ; ++u) {
         bw[u] = S.qt[j + u];
+        if constexpr (C::PAIR2) {
 #pragma unroll
-        for (int r = 0; r < QR; ++r) fail_and1(allfail[r & 3], imad_sub(hw[r], m1, bw[u]));
+          for (int r = 0; r < QR; r += 2)
+            fail_and2(allfail[(r >> 1) & 3], imad_sub(hw[r], m1, bw[u]), imad_sub(hw[r + 1], m1, bw[u]));
+        } else {
+#pragma unroll
+          for (int r = 0; r < QR; ++r) fail_and1(allfail[r & 3], imad_sub(hw[r], m1, bw[u]));
+        }
       }
       if (__any_sync(0xffffffffu, (allfail[0] & allfail[1] & allfail[2] & allfail[3]) == 0)) {
 #pragma unroll 1
@@ -983,7 +1003,8 @@ static int launch_local_cfg(std::vector<SearchParams>& T, Batch Bt, std::vector<
 }
 
 // Variant selection (MCX_VARIANT, experiments; 0 = the tuned default: 16 A records per
-// thread, 2-warp CTAs, one vote per 8 B records — measured in DESIGN.md §5).
+// thread, 2-warp CTAs, one vote per 8 B records, one LOP3 per two pair tests —
+// measured in DESIGN.md §5).
 static int launch_prefilter(std::vector<SearchParams>& T, const Batch& Bt, std::vector<uint64_t>& prefix,
                             void* dev_tab, int device, cudaStream_t stream) {
   switch (variant_from_env()) {
@@ -992,7 +1013,10 @@ static int launch_prefilter(std::vector<SearchParams>& T, const Batch& Bt, std::
     case 3: return launch_local_cfg<LCfg<32, 8, 1>>(T, Bt, prefix, dev_tab, device, stream);
     case 4: return launch_local_cfg<LCfg<16, 4, 1>>(T, Bt, prefix, dev_tab, device, stream);
     case 5: return launch_local_cfg<LCfg<8, 4, 1>>(T, Bt, prefix, dev_tab, device, stream);
-    default: return launch_local_cfg<LCfg<16, 8, 1>>(T, Bt, prefix, dev_tab, device, stream);
+    case 6: return launch_local_cfg<LCfg<16, 8, 1>>(T, Bt, prefix, dev_tab, device, stream);
+    case 7: return launch_local_cfg<LCfg<32, 8, 1, 1, true>>(T, Bt, prefix, dev_tab, device, stream);
+    case 8: return launch_local_cfg<LCfg<16, 4, 1, 1, true>>(T, Bt, prefix, dev_tab, device, stream);
+    default: return launch_local_cfg<LCfg<16, 8, 1, 1, true>>(T, Bt, prefix, dev_tab, device, stream);
   }
 }
 
