@@ -48,9 +48,10 @@ extern "C" {
 /* Search modes. */
 #define MCX_MODE_BRUTE 0 /* every (iA, iB) pair gets the 8-compare AABB test       */
 #define MCX_MODE_CULL 1  /* exact block-AABB culling first; identical hit set      */
-#define MCX_MODE_PREFILTER 2 /* every pair tested, first by a conservative 8-byte
-                                quantised-box integer test (fma + alu pipes), the
-                                rare passes by the exact FP64 test; identical hit set */
+#define MCX_MODE_PREFILTER 2 /* every pair tested, first by a conservative packed-
+                                integer test on 3-bit quantised boxes (fma + alu
+                                pipes), its rare passes by the exact FP64 test;
+                                identical hit set                                   */
 
 /* Storage orders of the packed triangle records (mcx_pack). */
 #define MCX_ORDER_NATURAL 0 /* record t at position t = 2·(i + N·k) + τ               */
