@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-paper", action="store_true", help="skip the paper's 14-layer workload block")
+    ap.add_argument("--no-c5", action="store_true", help="skip the configs[4] (C5hd) hit-compaction / balance block")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo lets several ranks share one GPU (logic test of the N>1 path on a 1-GPU box)")
     return ap.parse_args()
@@ -457,6 +458,33 @@ def run_ours(args):
                          "quad_box_tests": int(pst["n_tested"]), "same_candidates": bool(np.array_equal(cand, cand2)),
                          "path": "packed meshes -> mcx_pair_candidates_mesh (exact union-box culling)"}}
 
+    # ---- configs[4]: unbalanced high-hit-density pair (C5hd: 4.2M x 65k triangles, 13,226
+    # hits clustered in A's first quarter) - hit compaction, and the 8-GPU cyclic partition's
+    # balance measured shard by shard on this GPU (world == 1 only)
+    c5 = None
+    if world == 1 and not args.no_c5:
+        A5, _, B5, _ = config_pair("C5hd")
+        A5m, B5m = D.DeviceMesh(A5, local), D.DeviceMesh(B5, local)
+        c5 = {"workload": workload_desc("C5hd", A5, B5)["workload"] + " (configs[4], high-hit-density variant)"}
+        for mname in ("prefilter", "brute", "cull"):
+            for _ in range(max(1, args.warmup)):
+                D.search_device(A5m, B5m, mode=modes[mname], stream=stream)
+            ts = [D.search_device(A5m, B5m, mode=modes[mname], stream=stream, timing=True) for _ in range(args.steps)]
+            ms = statistics.median(r.stats["kernel_ms"] for r in ts)
+            c5[mname] = {"kernel_ms": ms, "pair_tests_per_s": ts[0].stats["n_pairs"] / (ms * 1e-3),
+                         "hits": int(ts[0].stats["n_hits"]), "aabb_pass": int(ts[0].stats["n_aabb_pass"])}
+        shards = []
+        for g in range(8):
+            r = D.search_device(A5m, B5m, mode=modes["prefilter"], shard=(g, 8), stream=stream, timing=True)
+            shards.append({"kernel_ms": r.stats["kernel_ms"], "hits": int(r.stats["n_hits"]),
+                           "aabb_pass": int(r.stats["n_aabb_pass"])})
+        kms = [x["kernel_ms"] for x in shards]
+        hs = [x["hits"] for x in shards]
+        c5["prefilter_8_cyclic_shards"] = {
+            "per_shard": shards, "time_max_over_mean": max(kms) / statistics.mean(kms),
+            "hits_max_over_mean": max(hs) / statistics.mean(hs), "hits_total": sum(hs),
+            "note": "the 8-GPU partition (A blocks dealt cyclically) run shard by shard on one GPU"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         s = cpu_reference_sample(A, B, args.cpu_seconds)
@@ -473,7 +501,7 @@ def run_ours(args):
                            "l2": "flushed between timed steps (256 MiB write, outside the events)"},
                 "search_wall_s": m1["ms_per_step"] / 1e3, "hits": m1["hits"], "kernel_ms": m1["kernel_ms"],
                 "roofline": roofline, "fp64_brute": fp64_block, "prefilter": pre_block, "cull": cull_block,
-                "e2e": e2e, "cpu_baseline": cpu, "paper_workload": paper, "clocks": m1["clocks"],
+                "e2e": e2e, "cpu_baseline": cpu, "paper_workload": paper, "c5_unbalanced": c5, "clocks": m1["clocks"],
                 "gpu_launches": m1["launches"], "gpu": props.name, "sms": sms}
         print(json.dumps(line), flush=True)
     if world > 1:

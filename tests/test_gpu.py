@@ -474,3 +474,33 @@ def test_prefilter_frames_exact(oracle_lib):
         ref = oracle_lib.search(Ax, Bx, sweep=True)
         r = D.search(Ax, Bx, mode=_lib.MODE_PREFILTER)
         assert_same_hits(ref, r.hits, r.stats)
+
+
+@pytest.fixture(scope="module")
+def c5hd(oracle_lib):
+    A, _, B, _ = config_pair("C5hd")
+    return A, B, oracle_lib.search(A, B, sweep=True), D.DeviceMesh(A, 0), D.DeviceMesh(B, 0)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_parity_c5hd_full(mode, c5hd):
+    """configs[4] at full scale, high-hit-density variant: 4.2M × 65k triangles,
+    13,226 hits clustered in A's first quarter — hit compaction under load."""
+    A, B, ref, Am, Bm = c5hd
+    assert len(ref["ia"]) == 13226
+    assert_same_hits(ref, D.search_device(Am, Bm, mode=mode).hits)
+    r = D.search(A, B, mode=mode)
+    assert_same_hits(ref, r.hits, r.stats)
+
+
+@pytest.mark.parametrize("mode", [_lib.MODE_PREFILTER, _lib.MODE_CULL])
+def test_c5hd_cyclic_shards_balance_hits(mode, c5hd):
+    """8 cyclic A-block shards (the 8-GPU partition, run one after another here): their
+    union is the full hit set and the clustered hits spread evenly over the shards."""
+    A, B, ref, Am, Bm = c5hd
+    parts = [D.search_device(Am, Bm, shard=(g, 8), mode=mode).hits for g in range(8)]
+    got = np.concatenate(parts)
+    got = got[np.lexsort((got["ib"], got["ia"]))]
+    assert_same_hits(ref, got)
+    counts = np.array([len(p) for p in parts])
+    assert counts.max() <= 1.5 * counts.mean(), counts
