@@ -131,6 +131,12 @@ def cpu_model():
     return "unknown"
 
 
+def bench_config(desc, mode, world):
+    """The `config` object both arms print (same workload, same keys)."""
+    return {**desc, "mode": mode, "parallelism": f"A-block cyclic shards x{world}, B replicated",
+            "l2": "flushed between timed steps (256 MiB write, outside the events)"}
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -153,9 +159,11 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": desc["pairs_per_step"] / v * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {**desc, "mode": "brute"},
+            "config": bench_config(desc, args.mode, world),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": s["threads"], "kind": "port",
-                             "sample": sample, "cpu": cpu_model()},
+                             "sample": sample, "cpu": cpu_model(),
+                             "algorithm": "the SPEC's all-pairs search (every pair through the FP64 AABB test, "
+                                          "canonical solve of the passes), C port, OpenMP over A"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "search_wall_s_extrapolated": desc["pairs_per_step"] / v}
     print(json.dumps(line), flush=True)
@@ -497,8 +505,7 @@ def run_ours(args):
         line = {"metric": METRIC, "value": m1["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": m1["ms_per_step"], "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {**desc, "mode": primary, "parallelism": f"A-block cyclic shards x{world}, B replicated",
-                           "l2": "flushed between timed steps (256 MiB write, outside the events)"},
+                "config": bench_config(desc, primary, world),
                 "search_wall_s": m1["ms_per_step"] / 1e3, "hits": m1["hits"], "kernel_ms": m1["kernel_ms"],
                 "roofline": roofline, "fp64_brute": fp64_block, "prefilter": pre_block, "cull": cull_block,
                 "e2e": e2e, "cpu_baseline": cpu, "paper_workload": paper, "c5_unbalanced": c5, "clocks": m1["clocks"],
