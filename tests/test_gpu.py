@@ -142,13 +142,21 @@ def test_parity_c5_reduced(scale, mode, oracle_lib):
     assert len(ref["ia"]) > 50
 
 
-@pytest.mark.slow
-def test_parity_c3_cull_vs_oracle(oracle_lib):
-    """C3 (1.095e12 pairs) in cull mode against the C oracle's exact sweep-and-prune."""
+@pytest.fixture(scope="module")
+def c3_ref(oracle_lib):
     A, _, B, _ = config_pair("C3")
-    ref = oracle_lib.search(A, B, sweep=True)
-    r = D.search(A, B, mode=_lib.MODE_CULL)
+    return A, B, oracle_lib.search(A, B, sweep=True)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("mode", MODES)
+def test_parity_c3_vs_oracle(mode, c3_ref):
+    """C3 (1M x 1M triangles, 1.095e12 pairs: the north-star size) in every mode against
+    the C oracle's exact sweep-and-prune: hit set, solution bits and counters."""
+    A, B, ref = c3_ref
+    r = D.search(A, B, mode=mode)
     assert_same_hits(ref, r.hits, r.stats)
+    assert r.stats["n_pairs"] == 1046528 * 1046528
 
 
 @pytest.mark.parametrize("mode", MODES)
