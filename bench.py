@@ -369,8 +369,11 @@ def run_ours(args):
                        "(128 and 85 pairs/clk/SM)",
         "work_per_launch": "n_pairs quantised pair tests (1 IMAD + 1/2 LOP3 each) + n_exact_tests FP64 box tests",
         "exact_tests_per_step": pst["n_exact_tests"], "kernel_ms": pst["kernel_ms"],
-        "kernel_ms_note": "CUDA events around the whole call: fp32 box kernel (~0.04 ms) + search",
-        "traffic": None}
+        "kernel_ms_note": "CUDA events around the whole call: fp32 box kernel (~0.03 ms) + search",
+        "traffic": (68652288.0 + 3390464.0) if args.config == "C3" else None,
+        "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum of one C3 launch, ncu --set full "
+                        "(profiles/r01_ncu_prefilter_c3.txt): B's 33 MB of fp32 boxes + A's, read ~once; the "
+                        "1.1e12 pair tests touch only registers and shared memory"}
     roofline = pf_roofline if primary == "prefilter" else fp64_roofline
     fp64_block = {"mode": "brute", "value": brute["value"], "unit": UNIT, "ms_per_step": brute["ms_per_step"],
                   "kernel_ms": brute["kernel_ms"], "roofline": fp64_roofline,
