@@ -385,7 +385,8 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_brute_kernel(const
 //   * fp32 boxes rounded outwards (lo toward −∞, hi toward +∞) are computed once per
 //     call (fbox_kernel).  Every later step is a monotone fp32 function of them, so
 //     A.lo ≤ B.hi ⇒ qlo_A ≤ qhi_B: the quantised test only ever keeps extra pairs.
-//   * Frame = union box of the CTA's own A block (1024 records): o_c = min lo_c,
+//   * Frame = union box of the warp's own 512 A records (a 16×16-quad tile of the
+//     tiled storage order; LCfg::WFRAME, else the CTA's 1024): o_c = min lo_c,
 //     κ_c = 6 / (max hi_c − o_c) (0 if the extent is 0 or not finite);
 //     q(x) = clamp(⌊(x − o)·κ⌋ or ⌈·⌉, 0, 6).  3 bits per bound suffice in a frame
 //     that small, so all 8 compares of a pair fit ONE 32-bit word of eight 4-bit
@@ -418,9 +419,10 @@ __device__ __forceinline__ unsigned imad_sub(unsigned a, unsigned m1, unsigned b
 constexpr int FTILE = 256;  // B records per stage (256 × 32 B = 8 KB)
 constexpr unsigned G4 = 0x88888888u;
 
-template <int QR_, int JB_, int UNROLL_, int MINB_ = 1, bool PAIR2_ = false>
+template <int QR_, int JB_, int UNROLL_, int MINB_ = 1, bool PAIR2_ = false, bool WFRAME_ = false>
 struct LCfg {
-  static constexpr bool PAIR2 = PAIR2_;  // one LOP3 for two pair tests (conservative "both fail")
+  static constexpr bool PAIR2 = PAIR2_;    // one LOP3 for two pair tests (conservative "both fail")
+  static constexpr bool WFRAME = WFRAME_;  // one frame per warp (its 32·QR A records) instead of per CTA
   static constexpr int QR = QR_;
   static constexpr int JB = JB_;
   static constexpr int UNROLL = UNROLL_;
@@ -428,15 +430,16 @@ struct LCfg {
   static constexpr int THREADS = A_BLOCK / QR_;
   static constexpr int WARPS = THREADS / 32;
   static_assert(WARPS >= 1 && THREADS % 32 == 0, "QR must leave whole warps in a 1024-record block");
+  static constexpr int NF = WFRAME ? WARPS : 1;  // frames (and quantised B tiles) per CTA
 };
 
 template <class C>
 struct __align__(16) LSmem {
   float4 tile[STAGES][FTILE][2];
-  unsigned qt[FTILE];
+  unsigned qt[C::NF][FTILE];
   uint2 queue[C::WARPS][Q_QCAP];
   float frame[C::WARPS][8];
-  float fr[16];
+  float fr[C::NF][16];
   unsigned aw[C::WARPS][C::QR][32];  // the A words, reloaded from here after a slow path
   unsigned long long full[STAGES];
 };
@@ -550,23 +553,25 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_local_kernel(const
   }
   __syncthreads();
   // frame parameters in shared memory: fr[0..3] = o_c, fr[4..7] = κ_c, fr[8..11] = lo_c, fr[12..15] = hi_c
-  if (tid < 4) {
-    const int c = tid;
-    float l = S.frame[0][c], h = S.frame[0][4 + c];
-    for (int w = 1; w < C::WARPS; ++w) { l = fminf(l, S.frame[w][c]); h = fmaxf(h, S.frame[w][4 + c]); }
+  const int fi = C::WFRAME ? warp : 0;  // this warp's frame / quantised B tile
+  if ((C::WFRAME ? lane : tid) < 4) {
+    const int c = C::WFRAME ? lane : tid;
+    float l = S.frame[fi][c], h = S.frame[fi][4 + c];
+    if (!C::WFRAME)
+      for (int w = 1; w < C::WARPS; ++w) { l = fminf(l, S.frame[w][c]); h = fmaxf(h, S.frame[w][4 + c]); }
     const float e = __fsub_rn(h, l);
-    float k = (e > 0.f && e < 3.0e38f) ? __fdiv_rn(6.f, e) : 0.f;  // also 0 for an empty block (l > h)
+    float k = (e > 0.f && e < 3.0e38f) ? __fdiv_rn(6.f, e) : 0.f;  // also 0 for an empty frame (l > h)
     if (!(k < 3.0e38f)) k = 0.f;
-    S.fr[c] = (k > 0.f) ? l : 0.f;
-    S.fr[4 + c] = k;
-    S.fr[8 + c] = l;
-    S.fr[12 + c] = h;
+    S.fr[fi][c] = (k > 0.f) ? l : 0.f;
+    S.fr[fi][4 + c] = k;
+    S.fr[fi][8 + c] = l;
+    S.fr[fi][12 + c] = h;
   }
   __syncthreads();
 
   // ---- A words in registers
   auto a_word = [&](uint32_t ia) -> unsigned {
-    const float* fr = S.fr;
+    const float* fr = S.fr[fi];
     const float4 l = __ldg(P.fA + 2 * (uint64_t)ia), h = __ldg(P.fA + 2 * (uint64_t)ia + 1);
     return ((8u + qceil(h.x, fr[0], fr[4])) << 0) | ((8u + qceil(h.y, fr[1], fr[5])) << 4) |
            ((8u + qceil(h.z, fr[2], fr[6])) << 8) | ((8u + qceil(h.w, fr[3], fr[7])) << 12) |
@@ -621,9 +626,9 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_local_kernel(const
     mbar_wait(&S.full[s], (uint32_t)((t / STAGES) & 1));
     const uint64_t tb = b0 + (uint64_t)t * FTILE;
     const int nvalid = (int)min((uint64_t)FTILE, b1 - tb);
-    // quantise this tile's B records into the block frame (all threads)
-    for (int j = tid; j < nvalid; j += C::THREADS) {
-      const float* fr = S.fr;
+    // quantise this tile's B records into the frame (per CTA: all threads; per warp: its lanes)
+    for (int j = C::WFRAME ? lane : tid; j < nvalid; j += C::WFRAME ? 32 : C::THREADS) {
+      const float* fr = S.fr[fi];
       const float4 l = S.tile[s][j][0], h = S.tile[s][j][1];
       const bool in = (l.x <= fr[12]) & (fr[8] <= h.x) & (l.y <= fr[13]) & (fr[9] <= h.y) & (l.z <= fr[14]) &
                       (fr[10] <= h.z) & (l.w <= fr[15]) & (fr[11] <= h.w);
@@ -633,7 +638,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_local_kernel(const
             (qfloor(l.w, fr[3], fr[7]) << 12) | ((6u - qceil(h.x, fr[0], fr[4])) << 16) |
             ((6u - qceil(h.y, fr[1], fr[5])) << 20) | ((6u - qceil(h.z, fr[2], fr[6])) << 24) |
             ((6u - qceil(h.w, fr[3], fr[7])) << 28);
-      S.qt[j] = w;
+      S.qt[fi][j] = w;
     }
     __syncthreads();
     auto step = [&](int j, auto jb_c) {
@@ -642,7 +647,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_local_kernel(const
       unsigned allfail[4] = {1, 1, 1, 1};
 #pragma unroll
       for (int u = 0; u < NJ; ++u) {
-        bw[u] = S.qt[j + u];
+        bw[u] = S.qt[fi][j + u];
         if constexpr (C::PAIR2) {
 #pragma unroll
           for (int r = 0; r < QR; r += 2)
@@ -654,7 +659,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_local_kernel(const
       }
       if (__any_sync(0xffffffffu, (allfail[0] & allfail[1] & allfail[2] & allfail[3]) == 0)) {
 #pragma unroll 1
-        for (int u = 0; u < NJ; ++u) slow((uint32_t)(tb + j + u), S.qt[j + u]);
+        for (int u = 0; u < NJ; ++u) slow((uint32_t)(tb + j + u), S.qt[fi][j + u]);
         load_a();
       }
     };
@@ -1003,8 +1008,8 @@ static int launch_local_cfg(std::vector<SearchParams>& T, Batch Bt, std::vector<
 }
 
 // Variant selection (MCX_VARIANT, experiments; 0 = the tuned default: 16 A records per
-// thread, 2-warp CTAs, one vote per 8 B records, one LOP3 per two pair tests —
-// measured in DESIGN.md §5).
+// thread, 2-warp CTAs, one frame per warp, one vote per 8 B records, one LOP3 per two
+// pair tests — measured in DESIGN.md §5).
 static int launch_prefilter(std::vector<SearchParams>& T, const Batch& Bt, std::vector<uint64_t>& prefix,
                             void* dev_tab, int device, cudaStream_t stream) {
   switch (variant_from_env()) {
@@ -1016,7 +1021,10 @@ static int launch_prefilter(std::vector<SearchParams>& T, const Batch& Bt, std::
     case 6: return launch_local_cfg<LCfg<16, 8, 1>>(T, Bt, prefix, dev_tab, device, stream);
     case 7: return launch_local_cfg<LCfg<32, 8, 1, 1, true>>(T, Bt, prefix, dev_tab, device, stream);
     case 8: return launch_local_cfg<LCfg<16, 4, 1, 1, true>>(T, Bt, prefix, dev_tab, device, stream);
-    default: return launch_local_cfg<LCfg<16, 8, 1, 1, true>>(T, Bt, prefix, dev_tab, device, stream);
+    case 9: return launch_local_cfg<LCfg<16, 8, 1, 1, true>>(T, Bt, prefix, dev_tab, device, stream);
+    case 10: return launch_local_cfg<LCfg<8, 8, 1, 1, true, true>>(T, Bt, prefix, dev_tab, device, stream);
+    case 11: return launch_local_cfg<LCfg<8, 8, 1, 1, true>>(T, Bt, prefix, dev_tab, device, stream);
+    default: return launch_local_cfg<LCfg<16, 8, 1, 1, true, true>>(T, Bt, prefix, dev_tab, device, stream);
   }
 }
 
