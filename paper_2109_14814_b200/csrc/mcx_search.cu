@@ -1008,7 +1008,7 @@ static int launch_local_cfg(std::vector<SearchParams>& T, Batch Bt, std::vector<
 }
 
 // Variant selection (MCX_VARIANT, experiments; 0 = the tuned default: 16 A records per
-// thread, 2-warp CTAs, one frame per warp, one vote per 8 B records, one LOP3 per two
+// thread, 2-warp CTAs, one frame per warp, one vote per 16 B records, one LOP3 per two
 // pair tests — measured in DESIGN.md §5).
 static int launch_prefilter(std::vector<SearchParams>& T, const Batch& Bt, std::vector<uint64_t>& prefix,
                             void* dev_tab, int device, cudaStream_t stream) {
@@ -1024,7 +1024,12 @@ static int launch_prefilter(std::vector<SearchParams>& T, const Batch& Bt, std::
     case 9: return launch_local_cfg<LCfg<16, 8, 1, 1, true>>(T, Bt, prefix, dev_tab, device, stream);
     case 10: return launch_local_cfg<LCfg<8, 8, 1, 1, true, true>>(T, Bt, prefix, dev_tab, device, stream);
     case 11: return launch_local_cfg<LCfg<8, 8, 1, 1, true>>(T, Bt, prefix, dev_tab, device, stream);
-    default: return launch_local_cfg<LCfg<16, 8, 1, 1, true, true>>(T, Bt, prefix, dev_tab, device, stream);
+    case 12: return launch_local_cfg<LCfg<16, 8, 1, 1, true, true>>(T, Bt, prefix, dev_tab, device, stream);
+    case 13: return launch_local_cfg<LCfg<16, 8, 2, 1, true, true>>(T, Bt, prefix, dev_tab, device, stream);
+    case 14: return launch_local_cfg<LCfg<16, 4, 2, 1, true, true>>(T, Bt, prefix, dev_tab, device, stream);
+    case 15: return launch_local_cfg<LCfg<16, 32, 1, 1, true, true>>(T, Bt, prefix, dev_tab, device, stream);
+    case 16: return launch_local_cfg<LCfg<32, 16, 1, 1, true, true>>(T, Bt, prefix, dev_tab, device, stream);
+    default: return launch_local_cfg<LCfg<16, 16, 1, 1, true, true>>(T, Bt, prefix, dev_tab, device, stream);
   }
 }
 
