@@ -1013,22 +1013,12 @@ static int launch_local_cfg(std::vector<SearchParams>& T, Batch Bt, std::vector<
 static int launch_prefilter(std::vector<SearchParams>& T, const Batch& Bt, std::vector<uint64_t>& prefix,
                             void* dev_tab, int device, cudaStream_t stream) {
   switch (variant_from_env()) {
-    case 1: return launch_local_cfg<LCfg<32, 2, 2>>(T, Bt, prefix, dev_tab, device, stream);
-    case 2: return launch_local_cfg<LCfg<32, 4, 1>>(T, Bt, prefix, dev_tab, device, stream);
-    case 3: return launch_local_cfg<LCfg<32, 8, 1>>(T, Bt, prefix, dev_tab, device, stream);
-    case 4: return launch_local_cfg<LCfg<16, 4, 1>>(T, Bt, prefix, dev_tab, device, stream);
-    case 5: return launch_local_cfg<LCfg<8, 4, 1>>(T, Bt, prefix, dev_tab, device, stream);
-    case 6: return launch_local_cfg<LCfg<16, 8, 1>>(T, Bt, prefix, dev_tab, device, stream);
-    case 7: return launch_local_cfg<LCfg<32, 8, 1, 1, true>>(T, Bt, prefix, dev_tab, device, stream);
-    case 8: return launch_local_cfg<LCfg<16, 4, 1, 1, true>>(T, Bt, prefix, dev_tab, device, stream);
-    case 9: return launch_local_cfg<LCfg<16, 8, 1, 1, true>>(T, Bt, prefix, dev_tab, device, stream);
-    case 10: return launch_local_cfg<LCfg<8, 8, 1, 1, true, true>>(T, Bt, prefix, dev_tab, device, stream);
-    case 11: return launch_local_cfg<LCfg<8, 8, 1, 1, true>>(T, Bt, prefix, dev_tab, device, stream);
-    case 12: return launch_local_cfg<LCfg<16, 8, 1, 1, true, true>>(T, Bt, prefix, dev_tab, device, stream);
-    case 13: return launch_local_cfg<LCfg<16, 8, 2, 1, true, true>>(T, Bt, prefix, dev_tab, device, stream);
-    case 14: return launch_local_cfg<LCfg<16, 4, 2, 1, true, true>>(T, Bt, prefix, dev_tab, device, stream);
-    case 15: return launch_local_cfg<LCfg<16, 32, 1, 1, true, true>>(T, Bt, prefix, dev_tab, device, stream);
-    case 16: return launch_local_cfg<LCfg<32, 16, 1, 1, true, true>>(T, Bt, prefix, dev_tab, device, stream);
+    case 1: return launch_local_cfg<LCfg<16, 8, 1, 1, true, true>>(T, Bt, prefix, dev_tab, device, stream);
+    case 2: return launch_local_cfg<LCfg<16, 32, 1, 1, true, true>>(T, Bt, prefix, dev_tab, device, stream);
+    case 3: return launch_local_cfg<LCfg<32, 16, 1, 1, true, true>>(T, Bt, prefix, dev_tab, device, stream);
+    case 4: return launch_local_cfg<LCfg<16, 8, 1, 1, true>>(T, Bt, prefix, dev_tab, device, stream);   // CTA frame
+    case 5: return launch_local_cfg<LCfg<16, 8, 1>>(T, Bt, prefix, dev_tab, device, stream);            // 1 LOP3/pair
+    case 6: return launch_local_cfg<LCfg<8, 8, 1, 1, true, true>>(T, Bt, prefix, dev_tab, device, stream);
     default: return launch_local_cfg<LCfg<16, 16, 1, 1, true, true>>(T, Bt, prefix, dev_tab, device, stream);
   }
 }
