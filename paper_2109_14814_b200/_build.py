@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmcx.so")
 SOURCES = ["mcx_pack.cu", "mcx_search.cu", "mcx_records.cu"]
-DEPS = SOURCES + ["mcx_common.cuh"]
+DEPS = SOURCES + ["mcx_common.cuh", "mcx_search.cuh", "mcx_prefilter.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

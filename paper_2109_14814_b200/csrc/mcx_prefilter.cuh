@@ -1,0 +1,369 @@
+// mcx_prefilter.cuh — MCX_MODE_PREFILTER: every pair tested by a conservative
+// packed-integer test on quantised boxes (fma + alu pipes), its passes by the exact
+// FP64 test.  Included by mcx_search.cu (one translation unit).
+#pragma once
+#include "mcx_search.cuh"
+
+namespace mcx {
+
+// ------------------------------------------------------------ prefilter mode
+// MCX_MODE_PREFILTER: every pair is tested, but first by a conservative integer
+// test on quantised boxes that runs on the fma + alu pipes instead of the FP64 pipe
+// (64 lanes/clk/SM on B200, 8 DSETP per pair); only pairs it cannot reject get the
+// exact FP64 box test and then the canonical solve, so the AABB-pass / singular /
+// hit sets are exactly those of MCX_MODE_BRUTE.
+//   * fp32 boxes rounded outwards (lo toward −∞, hi toward +∞) are computed once per
+//     call (fbox_kernel).  Every later step is a monotone fp32 function of them, so
+//     A.lo ≤ B.hi ⇒ qlo_A ≤ qhi_B: the quantised test only ever keeps extra pairs.
+//   * Frame = union box of the warp's own 512 A records (a 16×16-quad tile of the
+//     tiled storage order; LCfg::WFRAME, else the CTA's 1024): o_c = min lo_c,
+//     κ_c = 6 / (max hi_c − o_c) (0 if the extent is 0 or not finite);
+//     q(x) = clamp(⌊(x − o)·κ⌋ or ⌈·⌉, 0, 6).  3 bits per bound suffice in a frame
+//     that small, so all 8 compares of a pair fit ONE 32-bit word of eight 4-bit
+//     fields (value 0..6 + guard bit 3).
+//   * B words: nibble c = qlo_c, nibble 4+c = 6 − qhi_c.  A B record whose fp32 box
+//     misses the frame cannot overlap any record of the block: it gets nibble 0 = 7,
+//     which fails against every A word because qhi_A ≤ 6.
+//   * A words: nibble c = 8 + qhi_c, nibble 4+c = 14 − qlo_c.  H − L then has, per
+//     nibble, 8 + qhi_A − qlo_B ∈ [1, 15] (no borrow between nibbles) — guard bit
+//     set iff qlo_B ≤ qhi_A — and 8 + qhi_B − qlo_A.  Invalid A slots: 0x77777777.
+//   * Pair test = IMAD (L·(−1) + H, fma pipe) + half a LOP3.LUT.PAND (alu pipe): one
+//     LOP3 with LUT ~x_a & ~x_b & G per two A words, predicate output ANDed into one of
+//     4 "all fail" chains — "both fail at a common guard position", a conservative
+//     "both fail".  1.5 instructions per pair; the fma pipe (IMAD, 64 lanes/clk/SM)
+//     binds.  One warp vote per JB B records.
+//   * B records reach shared memory as fp32 boxes (bulk copies, 8 KB stages); the
+//     CTA quantises each tile into its frame (~1/50 of the test work) before testing.
+//   * On a vote the warp re-tests that B record against its A words (kept in shared
+//     memory) and runs the exact FP64 box test on the quantised passes from L1/L2;
+//     survivors are queued and solved exactly like the FP64 kernel.
+constexpr int Q_QCAP = 64;
+
+// a − b computed as b·(−1) + a on the fma pipe (m1 = 0xffffffff at run time).
+__device__ __forceinline__ unsigned imad_sub(unsigned a, unsigned m1, unsigned b) {
+  unsigned r;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(b), "r"(m1), "r"(a));
+  return r;
+}
+
+constexpr int FTILE = 256;  // B records per stage (256 × 32 B = 8 KB)
+constexpr unsigned G4 = 0x88888888u;
+
+template <int QR_, int JB_, int UNROLL_, int MINB_ = 1, bool PAIR2_ = false, bool WFRAME_ = false>
+struct LCfg {
+  static constexpr bool PAIR2 = PAIR2_;    // one LOP3 for two pair tests (conservative "both fail")
+  static constexpr bool WFRAME = WFRAME_;  // one frame per warp (its 32·QR A records) instead of per CTA
+  static constexpr int QR = QR_;
+  static constexpr int JB = JB_;
+  static constexpr int UNROLL = UNROLL_;
+  static constexpr int MINB = MINB_;
+  static constexpr int THREADS = A_BLOCK / QR_;
+  static constexpr int WARPS = THREADS / 32;
+  static_assert(WARPS >= 1 && THREADS % 32 == 0, "QR must leave whole warps in a 1024-record block");
+  static constexpr int NF = WFRAME ? WARPS : 1;  // frames (and quantised B tiles) per CTA
+};
+
+template <class C>
+struct __align__(16) LSmem {
+  float4 tile[STAGES][FTILE][2];
+  unsigned qt[C::NF][FTILE];
+  uint2 queue[C::WARPS][Q_QCAP];
+  float frame[C::WARPS][8];
+  float fr[C::NF][16];
+  unsigned aw[C::WARPS][C::QR][32];  // the A words, reloaded from here after a slow path
+  unsigned long long full[STAGES];
+};
+
+// allfail &= "x_a and x_b have a guard bit clear at a common position" (LOP3 LUT 0x02 =
+// ~x_a & ~x_b & G4): true only if both pairs fail, so it is a conservative "both fail"
+// (a pass of either clears it; two fails at different positions give a spurious vote,
+// which the slow path resolves).  One alu instruction per two pair tests.
+__device__ __forceinline__ void fail_and2(unsigned& allfail, unsigned xa, unsigned xb) {
+  // the LOP3 result register d is unused: only its != 0 predicate matters
+  asm("{\n .reg .pred p;\n .reg .b32 d;\n setp.ne.u32 p, %0, 0;\n lop3.and.b32 d|p, %1, %2, %3, 0x02, p;\n"
+      " selp.u32 %0, 1, 0, p;\n}"
+      : "+r"(allfail)
+      : "r"(xa), "r"(xb), "r"(G4));
+}
+
+// allfail &= "x has a guard bit clear" (LOP3 LUT 0x0a = ~x & G4).
+__device__ __forceinline__ void fail_and1(unsigned& allfail, unsigned x) {
+  asm("{\n .reg .pred p;\n .reg .b32 d;\n setp.ne.u32 p, %0, 0;\n lop3.and.b32 d|p, %1, %1, %2, 0x0a, p;\n"
+      " selp.u32 %0, 1, 0, p;\n}"
+      : "+r"(allfail)
+      : "r"(x), "r"(G4));
+}
+
+// Conservative fp32 boxes of A and B per task (blockIdx.y = task).
+__global__ void __launch_bounds__(256) fbox_kernel(const Batch Bt) {
+  const SearchParams& P = Bt.tasks[blockIdx.y];
+  const Box* boxA = P.boxA;
+  const Box* boxB = P.boxB;
+  const uint64_t nA = P.nA, n = nA + P.nB;
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x) {
+    const double2* b = reinterpret_cast<const double2*>(k < nA ? boxA + k : boxB + (k - nA));
+    const double2 l01 = __ldg(b), l23 = __ldg(b + 1), h01 = __ldg(b + 2), h23 = __ldg(b + 3);
+    const float4 lo = make_float4(__double2float_rd(l01.x), __double2float_rd(l01.y), __double2float_rd(l23.x),
+                                  __double2float_rd(l23.y));
+    const float4 hi = make_float4(__double2float_ru(h01.x), __double2float_ru(h01.y), __double2float_ru(h23.x),
+                                  __double2float_ru(h23.y));
+    float4* dst = k < nA ? P.fA + 2 * k : P.fB + 2 * (k - nA);
+    dst[0] = lo;
+    dst[1] = hi;
+  }
+}
+
+__device__ __forceinline__ unsigned qfloor(float x, float o, float k) {
+  return (unsigned)__float2int_rd(fminf(fmaxf(__fmul_rn(__fsub_rn(x, o), k), 0.f), 6.f));
+}
+__device__ __forceinline__ unsigned qceil(float x, float o, float k) {
+  return (unsigned)__float2int_ru(fminf(fmaxf(__fmul_rn(__fsub_rn(x, o), k), 0.f), 6.f));
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::THREADS, C::MINB) search_local_kernel(const Batch Bt) {
+  constexpr int QR = C::QR;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  LSmem<C>& S = *reinterpret_cast<LSmem<C>*>(smem_raw);
+  __shared__ SearchParams Ps;
+  __shared__ uint64_t s_unit;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    const uint32_t t = find_task(Bt, blockIdx.x);
+    Ps = Bt.tasks[t];
+    s_unit = blockIdx.x - Bt.prefix[t];
+  }
+  __syncthreads();
+  const SearchParams& P = Ps;
+  const uint64_t unit = s_unit;
+  const uint64_t gblk = P.blk_first + (unit / P.nchunk) * P.shard_count;
+  const uint64_t a0 = gblk * A_BLOCK;
+  const uint64_t b0 = (unit % P.nchunk) * P.b_chunk;
+  const uint64_t b1 = min(b0 + P.b_chunk, P.nB);
+  const int ntiles = (int)((b1 - b0 + FTILE - 1) / FTILE);
+  const unsigned m1 = Bt.neg1;
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&S.full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int s = 0; s < STAGES && s < ntiles; ++s) {
+      const uint64_t tb = b0 + (uint64_t)s * FTILE;
+      const uint32_t bytes = (uint32_t)(min((uint64_t)FTILE, b1 - tb) * 32);
+      mbar_arrive_expect_tx(&S.full[s], bytes);
+      bulk_g2s(&S.tile[s][0][0], P.fB + 2 * tb, bytes, &S.full[s]);
+    }
+  }
+
+  // ---- frame of the block: union of the CTA's valid A records (all warps)
+  const uint32_t abase = (uint32_t)(a0 + (uint64_t)warp * (QR * 32) + lane);
+  float lo[4], hi[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) { lo[c] = __int_as_float(0x7f800000); hi[c] = -lo[c]; }
+#pragma unroll 4
+  for (int r = 0; r < QR; ++r) {
+    const uint32_t ia = abase + r * 32;
+    if (ia >= P.a_begin && ia < P.a_end) {
+      const float4 l = __ldg(P.fA + 2 * (uint64_t)ia), h = __ldg(P.fA + 2 * (uint64_t)ia + 1);
+      lo[0] = fminf(lo[0], l.x); lo[1] = fminf(lo[1], l.y); lo[2] = fminf(lo[2], l.z); lo[3] = fminf(lo[3], l.w);
+      hi[0] = fmaxf(hi[0], h.x); hi[1] = fmaxf(hi[1], h.y); hi[2] = fmaxf(hi[2], h.z); hi[3] = fmaxf(hi[3], h.w);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      lo[c] = fminf(lo[c], __shfl_xor_sync(0xffffffffu, lo[c], o));
+      hi[c] = fmaxf(hi[c], __shfl_xor_sync(0xffffffffu, hi[c], o));
+    }
+  if (lane == 0) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) { S.frame[warp][c] = lo[c]; S.frame[warp][4 + c] = hi[c]; }
+  }
+  __syncthreads();
+  // frame parameters in shared memory: fr[0..3] = o_c, fr[4..7] = κ_c, fr[8..11] = lo_c, fr[12..15] = hi_c
+  const int fi = C::WFRAME ? warp : 0;  // this warp's frame / quantised B tile
+  if ((C::WFRAME ? lane : tid) < 4) {
+    const int c = C::WFRAME ? lane : tid;
+    float l = S.frame[fi][c], h = S.frame[fi][4 + c];
+    if (!C::WFRAME)
+      for (int w = 1; w < C::WARPS; ++w) { l = fminf(l, S.frame[w][c]); h = fmaxf(h, S.frame[w][4 + c]); }
+    const float e = __fsub_rn(h, l);
+    float k = (e > 0.f && e < 3.0e38f) ? __fdiv_rn(6.f, e) : 0.f;  // also 0 for an empty frame (l > h)
+    if (!(k < 3.0e38f)) k = 0.f;
+    S.fr[fi][c] = (k > 0.f) ? l : 0.f;
+    S.fr[fi][4 + c] = k;
+    S.fr[fi][8 + c] = l;
+    S.fr[fi][12 + c] = h;
+  }
+  __syncthreads();
+
+  // ---- A words in registers
+  auto a_word = [&](uint32_t ia) -> unsigned {
+    const float* fr = S.fr[fi];
+    const float4 l = __ldg(P.fA + 2 * (uint64_t)ia), h = __ldg(P.fA + 2 * (uint64_t)ia + 1);
+    return ((8u + qceil(h.x, fr[0], fr[4])) << 0) | ((8u + qceil(h.y, fr[1], fr[5])) << 4) |
+           ((8u + qceil(h.z, fr[2], fr[6])) << 8) | ((8u + qceil(h.w, fr[3], fr[7])) << 12) |
+           ((14u - qfloor(l.x, fr[0], fr[4])) << 16) | ((14u - qfloor(l.y, fr[1], fr[5])) << 20) |
+           ((14u - qfloor(l.z, fr[2], fr[6])) << 24) | ((14u - qfloor(l.w, fr[3], fr[7])) << 28);
+  };
+  for (int r = 0; r < QR; ++r) {
+    const uint32_t ia = abase + r * 32;
+    S.aw[warp][r][lane] = (ia >= P.a_begin && ia < P.a_end) ? a_word(ia) : 0x77777777u;  // all guards clear
+  }
+  __syncwarp();
+  unsigned hw[QR];
+  auto load_a = [&]() {
+#pragma unroll
+    for (int r = 0; r < QR; ++r) hw[r] = *(volatile unsigned*)&S.aw[warp][r][lane];
+  };
+  load_a();
+
+  uint2* q = S.queue[warp];
+  int qn = 0;
+  unsigned long long n_pass = 0, n_sing = 0, n_exact = 0;
+  const unsigned lt_mask = (1u << lane) - 1u;
+
+  auto slow = [&](uint32_t ib, unsigned bw) {
+    const double2* bp = reinterpret_cast<const double2*>(P.boxB + ib);
+    const double2 l01 = __ldg(bp), l23 = __ldg(bp + 1), g01 = __ldg(bp + 2), g23 = __ldg(bp + 3);
+    for (int r = 0; r < QR; ++r) {
+      const uint32_t ia = abase + r * 32;
+      bool p = false;
+      if (((S.aw[warp][r][lane] - bw) & G4) == G4) {  // quantised pass (invalid slots never pass)
+        ++n_exact;
+        const double2* ap = reinterpret_cast<const double2*>(P.boxA + ia);
+        const double2 a01 = __ldg(ap), a23 = __ldg(ap + 1), c01 = __ldg(ap + 2), c23 = __ldg(ap + 3);
+        p = (l01.x <= c01.x) & (a01.x <= g01.x) & (l01.y <= c01.y) & (a01.y <= g01.y) &
+            (l23.x <= c23.x) & (a23.x <= g23.x) & (l23.y <= c23.y) & (a23.y <= g23.y);
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, p);
+      if (m) {
+        if (p) q[qn + __popc(m & lt_mask)] = make_uint2(ia, ib);
+        qn += __popc(m);
+        __syncwarp();
+        if (qn >= 32) {
+          qn -= 32;
+          flush_queue<KIND_TRI>(P, Bt, q + qn, 32, lane, n_pass, n_sing);
+        }
+      }
+    }
+  };
+
+  for (int t = 0; t < ntiles; ++t) {
+    const int s = t % STAGES;
+    mbar_wait(&S.full[s], (uint32_t)((t / STAGES) & 1));
+    const uint64_t tb = b0 + (uint64_t)t * FTILE;
+    const int nvalid = (int)min((uint64_t)FTILE, b1 - tb);
+    // quantise this tile's B records into the frame (per CTA: all threads; per warp: its lanes)
+    for (int j = C::WFRAME ? lane : tid; j < nvalid; j += C::WFRAME ? 32 : C::THREADS) {
+      const float* fr = S.fr[fi];
+      const float4 l = S.tile[s][j][0], h = S.tile[s][j][1];
+      const bool in = (l.x <= fr[12]) & (fr[8] <= h.x) & (l.y <= fr[13]) & (fr[9] <= h.y) & (l.z <= fr[14]) &
+                      (fr[10] <= h.z) & (l.w <= fr[15]) & (fr[11] <= h.w);
+      unsigned w = 7u;  // misses the frame: nibble 0 = 7 fails against every A word
+      if (in)
+        w = qfloor(l.x, fr[0], fr[4]) | (qfloor(l.y, fr[1], fr[5]) << 4) | (qfloor(l.z, fr[2], fr[6]) << 8) |
+            (qfloor(l.w, fr[3], fr[7]) << 12) | ((6u - qceil(h.x, fr[0], fr[4])) << 16) |
+            ((6u - qceil(h.y, fr[1], fr[5])) << 20) | ((6u - qceil(h.z, fr[2], fr[6])) << 24) |
+            ((6u - qceil(h.w, fr[3], fr[7])) << 28);
+      S.qt[fi][j] = w;
+    }
+    __syncthreads();
+    auto step = [&](int j, auto jb_c) {
+      constexpr int NJ = decltype(jb_c)::value;
+      unsigned bw[NJ];
+      unsigned allfail[4] = {1, 1, 1, 1};
+#pragma unroll
+      for (int u = 0; u < NJ; ++u) {
+        bw[u] = S.qt[fi][j + u];
+        if constexpr (C::PAIR2) {
+#pragma unroll
+          for (int r = 0; r < QR; r += 2)
+            fail_and2(allfail[(r >> 1) & 3], imad_sub(hw[r], m1, bw[u]), imad_sub(hw[r + 1], m1, bw[u]));
+        } else {
+#pragma unroll
+          for (int r = 0; r < QR; ++r) fail_and1(allfail[r & 3], imad_sub(hw[r], m1, bw[u]));
+        }
+      }
+      if (__any_sync(0xffffffffu, (allfail[0] & allfail[1] & allfail[2] & allfail[3]) == 0)) {
+#pragma unroll 1
+        for (int u = 0; u < NJ; ++u) slow((uint32_t)(tb + j + u), S.qt[fi][j + u]);
+        load_a();
+      }
+    };
+    const int nmain = nvalid - nvalid % C::JB;
+#pragma unroll(C::UNROLL)
+    for (int j = 0; j < nmain; j += C::JB) step(j, std::integral_constant<int, C::JB>());
+    for (int j = nmain; j < nvalid; ++j) step(j, std::integral_constant<int, 1>());
+    __syncthreads();  // every warp is done reading stage s and qt
+    if (tid == 0 && t + STAGES < ntiles) {
+      const uint64_t nb = b0 + (uint64_t)(t + STAGES) * FTILE;
+      const uint32_t bytes = (uint32_t)(min((uint64_t)FTILE, b1 - nb) * 32);
+      mbar_arrive_expect_tx(&S.full[s], bytes);
+      bulk_g2s(&S.tile[s][0][0], P.fB + 2 * nb, bytes, &S.full[s]);
+    }
+  }
+  __syncwarp();
+  if (qn > 0) flush_queue<KIND_TRI>(P, Bt, q, qn, lane, n_pass, n_sing);
+  flush_counters(P, lane, n_pass, n_sing, n_exact);
+}
+
+// MCX_MODE_PREFILTER: conservative fp32 boxes → prefilter search.
+template <class C>
+static int launch_local_cfg(std::vector<SearchParams>& T, Batch Bt, std::vector<uint64_t>& prefix, void* dev_tab,
+                            int device, cudaStream_t stream) {
+  int dev_sms = 148;
+  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device);
+  const size_t smem = sizeof(LSmem<C>);
+  CUDA_TRY(cudaFuncSetAttribute(search_local_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 1;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, search_local_kernel<C>, C::THREADS, smem));
+  const uint64_t slots = (uint64_t)dev_sms * (occ > 0 ? occ : 1);
+  prefix.assign(T.size() + 1, 0);
+  uint64_t max_records = 0;
+  for (size_t t = 0; t < T.size(); ++t) {
+    if (T[t].my_blocks && T[t].nB) choose_chunks(T[t], slots, 2); else T[t].nchunk = 0;
+    prefix[t + 1] = prefix[t] + T[t].my_blocks * T[t].nchunk;
+    if (T[t].nchunk) max_records = std::max<uint64_t>(max_records, T[t].nA + T[t].nB);
+  }
+  const uint64_t total = prefix.back();
+  const size_t tab = sizeof(SearchParams) * T.size();
+  CUDA_TRY(cudaMemcpyAsync(dev_tab, T.data(), tab, cudaMemcpyHostToDevice, stream));
+  CUDA_TRY(cudaMemcpyAsync((char*)dev_tab + tab, prefix.data(), sizeof(uint64_t) * prefix.size(),
+                           cudaMemcpyHostToDevice, stream));
+  if (total == 0) return MCX_OK;
+  if (total > 0x7fffffffull) return set_error(MCX_E_ARG, "grid too large");
+  if (T.size() > 65535) return set_error(MCX_E_ARG, "MCX_MODE_PREFILTER supports at most 65535 tasks per batch");
+  Bt.tasks = reinterpret_cast<const SearchParams*>(dev_tab);
+  Bt.prefix = reinterpret_cast<const uint64_t*>((char*)dev_tab + tab);
+  Bt.neg1 = 0xffffffffu;
+  const unsigned n = (unsigned)T.size();
+  uint64_t gx = (max_records + 1023) / 1024;
+  const uint64_t gcap = std::max<uint64_t>(1, (uint64_t)dev_sms * 8 / n);
+  if (gx > gcap) gx = gcap;
+  fbox_kernel<<<dim3((unsigned)gx, n), 256, 0, stream>>>(Bt);
+  search_local_kernel<C><<<(unsigned)total, C::THREADS, smem, stream>>>(Bt);
+  CUDA_TRY(cudaGetLastError());
+  return MCX_OK;
+}
+
+// Variant selection (MCX_VARIANT, experiments; 0 = the tuned default: 16 A records per
+// thread, 2-warp CTAs, one frame per warp, one vote per 16 B records, one LOP3 per two
+// pair tests — measured in DESIGN.md §5).
+static int launch_prefilter(std::vector<SearchParams>& T, const Batch& Bt, std::vector<uint64_t>& prefix,
+                            void* dev_tab, int device, cudaStream_t stream) {
+  switch (variant_from_env()) {
+    case 1: return launch_local_cfg<LCfg<16, 8, 1, 1, true, true>>(T, Bt, prefix, dev_tab, device, stream);
+    case 2: return launch_local_cfg<LCfg<16, 32, 1, 1, true, true>>(T, Bt, prefix, dev_tab, device, stream);
+    case 3: return launch_local_cfg<LCfg<32, 16, 1, 1, true, true>>(T, Bt, prefix, dev_tab, device, stream);
+    case 4: return launch_local_cfg<LCfg<16, 8, 1, 1, true>>(T, Bt, prefix, dev_tab, device, stream);   // CTA frame
+    case 5: return launch_local_cfg<LCfg<16, 8, 1>>(T, Bt, prefix, dev_tab, device, stream);            // 1 LOP3/pair
+    case 6: return launch_local_cfg<LCfg<8, 8, 1, 1, true, true>>(T, Bt, prefix, dev_tab, device, stream);
+    default: return launch_local_cfg<LCfg<16, 16, 1, 1, true, true>>(T, Bt, prefix, dev_tab, device, stream);
+  }
+}
+
+}  // namespace mcx

@@ -1,0 +1,216 @@
+// mcx_search.cuh — types and device/host helpers shared by the search kernels
+// (mcx_search.cu: FP64 brute force + culling; mcx_prefilter.cuh: prefilter mode).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdlib.h>
+
+#include <algorithm>
+#include <type_traits>
+#include <vector>
+
+#include "../../include/mcx.h"
+#include "mcx_common.cuh"
+
+namespace mcx {
+
+constexpr int STAGES = 2;
+
+// Kernel variant: R A triangles per thread, MINB resident CTAs per SM (register cap).
+template <int R_, int MINB_, int JB_ = 1, int UNROLL_ = 2, int PF_ = 0>
+struct Cfg {
+  static constexpr int PF = PF_;             // prefetch the next B box before testing the current
+  static constexpr int R = R_;
+  static constexpr int MINB = MINB_;
+  static constexpr int JB = JB_;             // B triangles per warp vote
+  static constexpr int UNROLL = UNROLL_;     // inner-loop unroll
+  static constexpr int THREADS = A_BLOCK / R_;
+  static constexpr int WARPS = THREADS / 32;
+  static constexpr int QCAP = 32 * R_ * JB_ + 32;  // per-warp survivor queue capacity
+};
+
+enum Kind { KIND_TRI = 0, KIND_QUAD = 1 };
+
+// Per-task parameters (one entry of the device task table; a single search is a
+// batch of one).  Pointers are device pointers.
+struct __align__(16) SearchParams {
+  const Box* boxA;
+  const double* geoA;
+  const uint32_t* permA;    // storage → original index (NULL = identity)
+  const Box* boxB;
+  const double* geoB;
+  const uint32_t* permB;
+  uint64_t nA;
+  uint64_t a_begin, a_end;  // A storage range
+  uint64_t blk_first;       // first absolute A block of this shard
+  uint64_t my_blocks;       // A blocks of this shard
+  uint64_t nB;
+  uint64_t b_chunk, nchunk; // brute: B triangles per CTA (multiple of TILE), chunks
+  uint64_t ntilesB;
+  uint32_t shard_count, task;
+  unsigned long long* counters;  // per task: [0] emitted, [1] aabb pass, [2] singular / Moller-rejected, [3] tested
+  // MCX_MODE_CULL
+  const Box* gboxA;
+  const Box* bboxA;
+  const Box* gboxB;
+  const Box* tboxB;
+  const uint32_t* statusA;  // mcx_pack non-finite flags (may be NULL)
+  const uint32_t* statusB;
+  // KIND_QUAD only: half-layer grids (4, M, N) for the Moller stage
+  const double* coordsA;
+  const double* coordsB;
+  uint32_t NA, MA, NB, MB;
+  // MCX_MODE_PREFILTER only: conservative fp32 boxes {lo_rd[4]}, {hi_ru[4]} per record
+  float4* fA;
+  float4* fB;
+};
+
+// Whole-launch parameters: the task table and the shared outputs.
+struct Batch {
+  const SearchParams* tasks;
+  uint32_t n_tasks;
+  const uint64_t* prefix;        // [n_tasks + 1] exclusive prefix of per-task work units
+  mcx_hit* hits;                 // KIND_TRI output (original indices)
+  uint32_t* hit_task;            // task id of each hit (NULL: single task)
+  uint64_t* gids;                // KIND_QUAD output
+  uint64_t cap;
+  unsigned long long* emit;      // shared output position counter
+  uint4* blk_list;               // cull: overlapping (task, local A block, B tile)
+  uint64_t blk_cap;
+  unsigned long long* list_count;
+  uint32_t neg1;                 // 0xffffffff, a runtime operand so the packed subtract stays an IMAD
+};
+
+// Task owning work unit u: the last t with prefix[t] <= u (n_tasks is small).
+__device__ __forceinline__ uint32_t find_task(const Batch& Bt, uint64_t u) {
+  uint32_t lo = 0, hi = Bt.n_tasks - 1;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi + 1) >> 1;
+    if (__ldg(Bt.prefix + mid) <= u) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+template <class C>
+struct __align__(16) SearchSmem {
+  Box tile[STAGES][TILE];
+  uint2 queue[C::WARPS][C::QCAP];
+  unsigned long long full[STAGES];
+};
+
+__device__ __forceinline__ bool box_overlap(const Box& a, const Box& b) {
+  return (b.lo[0] <= a.hi[0]) & (a.lo[0] <= b.hi[0]) & (b.lo[1] <= a.hi[1]) & (a.lo[1] <= b.hi[1]) &
+         (b.lo[2] <= a.hi[2]) & (a.lo[2] <= b.hi[2]) & (b.lo[3] <= a.hi[3]) & (a.lo[3] <= b.hi[3]);
+}
+
+__device__ __forceinline__ void empty_box(double lo[4], double hi[4]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    lo[c] = __longlong_as_double(0x7ff0000000000000ll);  // +inf: never overlaps
+    hi[c] = -lo[c];
+  }
+}
+
+// Process the queued pairs [0, n) of this warp's queue slice, one per lane
+// (queue entries are storage indices):
+// KIND_TRI  — canonical solve, emit (iA, iB, s, t, a, b) hits with original indices;
+// KIND_QUAD — SPEC-literal Moller quick test, emit surviving quad-pair gids.
+template <int KIND>
+__device__ __forceinline__ void flush_queue(const SearchParams& P, const Batch& Bt, const uint2* q, int n, int lane,
+                                            unsigned long long& n_pass, unsigned long long& n_sing) {
+  const bool valid = lane < n;
+  uint2 e = valid ? q[lane] : make_uint2(0, 0);
+  __syncwarp();
+  double sol[4];
+  int rc = 0;
+  if (KIND == KIND_TRI) {
+    if (valid) rc = solve_pair(P.geoA + (uint64_t)e.x * MCX_GEO_STRIDE, P.geoB + (uint64_t)e.y * MCX_GEO_STRIDE, sol);
+  } else {
+    if (valid) rc = moller_reject(P.coordsA, P.NA, P.MA, e.x, P.coordsB, P.NB, P.MB, e.y) ? 2 : 1;
+  }
+  n_pass += valid ? 1 : 0;
+  n_sing += (rc == 2) ? 1 : 0;
+  const bool hit = (rc == 1);
+  const unsigned hm = __ballot_sync(0xffffffffu, hit);
+  if (hm) {
+    const int leader = __ffs(hm) - 1;
+    unsigned long long base = 0;
+    if (lane == leader) {
+      base = atomicAdd(Bt.emit, (unsigned long long)__popc(hm));
+      atomicAdd(P.counters + 0, (unsigned long long)__popc(hm));
+    }
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (hit) {
+      const unsigned long long pos = base + __popc(hm & ((1u << lane) - 1u));
+      if (pos < Bt.cap) {
+        if (KIND == KIND_TRI) {
+          mcx_hit h;
+          h.ia = P.permA ? __ldg(P.permA + e.x) : e.x;
+          h.ib = P.permB ? __ldg(P.permB + e.y) : e.y;
+          h.s = sol[0]; h.t = sol[1]; h.a = sol[2]; h.b = sol[3];
+          Bt.hits[pos] = h;
+          if (Bt.hit_task) Bt.hit_task[pos] = P.task;
+        } else {
+          // quad indices qa = i + N1·k1, qb = j + N2·l1 → gid (PAPER.md kernel step 2)
+          const uint64_t i = e.x % P.NA, k1 = e.x / P.NA, j = e.y % P.NB, l1 = e.y / P.NB;
+          const uint64_t n12 = (uint64_t)P.NA * P.NB;
+          Bt.gids[pos] = i + (uint64_t)P.NA * j + n12 * k1 + n12 * (uint64_t)(P.MA - 1) * l1;
+        }
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void flush_counters(const SearchParams& P, int lane, unsigned long long n_pass,
+                                               unsigned long long n_sing, unsigned long long n_tested) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    n_pass += __shfl_xor_sync(0xffffffffu, n_pass, o);
+    n_sing += __shfl_xor_sync(0xffffffffu, n_sing, o);
+    n_tested += __shfl_xor_sync(0xffffffffu, n_tested, o);
+  }
+  if (lane == 0) {
+    if (n_pass) atomicAdd(P.counters + 1, n_pass);
+    if (n_sing) atomicAdd(P.counters + 2, n_sing);
+    if (n_tested) atomicAdd(P.counters + 3, n_tested);
+  }
+}
+
+// --------------------------------------------------------------- host side
+// B chunk count for one task: every CTA of a task does the same work, so pick the
+// count whose CTA total best fills whole waves of resident CTAs (the last partial
+// wave idles the rest of the GPU), among counts giving >= 8 waves with chunks of
+// >= min_tiles tiles (1 tile for small problems).
+static void choose_chunks(SearchParams& P, uint64_t slots, uint64_t min_tiles = 16) {
+  const uint64_t max_chunks = (P.nB + TILE - 1) / TILE;
+  uint64_t nchunk = 1, chunk = max_chunks * TILE;
+  const uint64_t min_ch = (P.my_blocks * max_chunks < 8 * slots) ? (uint64_t)TILE : min_tiles * (uint64_t)TILE;
+  double best = -1.0;
+  for (uint64_t c = 1; c <= max_chunks && c <= 4096; ++c) {
+    const uint64_t ch = ((P.nB + c - 1) / c + TILE - 1) / TILE * TILE;
+    const uint64_t nc = (P.nB + ch - 1) / ch;
+    if (nc != c) continue;
+    const uint64_t total = P.my_blocks * nc;
+    const bool enough = total >= 8 * slots || nc == max_chunks;
+    if (!enough && c < max_chunks && ch > min_ch) continue;
+    const double eff = (double)total / (double)(((total + slots - 1) / slots) * slots);
+    if (eff > best + 1e-3) {
+      best = eff;
+      nchunk = nc;
+      chunk = ch;
+    }
+    if (best > 0.995 || ch <= min_ch) break;
+  }
+  P.nchunk = nchunk;
+  P.b_chunk = chunk;
+}
+
+// Variant selection (MCX_VARIANT=0..3, for experiments; 0 = the tuned default:
+// R = 4, 256 threads, 2 CTAs/SM, next B box prefetched from shared memory before
+// the current one's compares, unroll 4 — no spills).
+static int variant_from_env() {
+  const char* v = getenv("MCX_VARIANT");
+  return v ? atoi(v) : 0;
+}
+
+}  // namespace mcx
