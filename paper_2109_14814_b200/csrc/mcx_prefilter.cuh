@@ -94,22 +94,16 @@ __device__ __forceinline__ void fail_and1(unsigned& allfail, unsigned x) {
       : "r"(x), "r"(G4));
 }
 
-// Conservative fp32 boxes of A and B per task (blockIdx.y = task).
+// Conservative fp32 boxes of every distinct mesh of the batch (blockIdx.y = job).
 __global__ void __launch_bounds__(256) fbox_kernel(const Batch Bt) {
-  const SearchParams& P = Bt.tasks[blockIdx.y];
-  const Box* boxA = P.boxA;
-  const Box* boxB = P.boxB;
-  const uint64_t nA = P.nA, n = nA + P.nB;
-  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x) {
-    const double2* b = reinterpret_cast<const double2*>(k < nA ? boxA + k : boxB + (k - nA));
+  const FboxJob J = Bt.fjobs[blockIdx.y];
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < J.n; k += (uint64_t)gridDim.x * blockDim.x) {
+    const double2* b = reinterpret_cast<const double2*>(J.src + k);
     const double2 l01 = __ldg(b), l23 = __ldg(b + 1), h01 = __ldg(b + 2), h23 = __ldg(b + 3);
-    const float4 lo = make_float4(__double2float_rd(l01.x), __double2float_rd(l01.y), __double2float_rd(l23.x),
-                                  __double2float_rd(l23.y));
-    const float4 hi = make_float4(__double2float_ru(h01.x), __double2float_ru(h01.y), __double2float_ru(h23.x),
-                                  __double2float_ru(h23.y));
-    float4* dst = k < nA ? P.fA + 2 * k : P.fB + 2 * (k - nA);
-    dst[0] = lo;
-    dst[1] = hi;
+    J.dst[2 * k] = make_float4(__double2float_rd(l01.x), __double2float_rd(l01.y), __double2float_rd(l23.x),
+                               __double2float_rd(l23.y));
+    J.dst[2 * k + 1] = make_float4(__double2float_ru(h01.x), __double2float_ru(h01.y), __double2float_ru(h23.x),
+                                   __double2float_ru(h23.y));
   }
 }
 
@@ -314,7 +308,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_local_kernel(const
 // MCX_MODE_PREFILTER: conservative fp32 boxes → prefilter search.
 template <class C>
 static int launch_local_cfg(std::vector<SearchParams>& T, Batch Bt, std::vector<uint64_t>& prefix, void* dev_tab,
-                            int device, cudaStream_t stream) {
+                            const std::vector<FboxJob>& jobs, void* dev_jobs, int device, cudaStream_t stream) {
   int dev_sms = 148;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device);
   const size_t smem = sizeof(LSmem<C>);
@@ -323,11 +317,9 @@ static int launch_local_cfg(std::vector<SearchParams>& T, Batch Bt, std::vector<
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, search_local_kernel<C>, C::THREADS, smem));
   const uint64_t slots = (uint64_t)dev_sms * (occ > 0 ? occ : 1);
   prefix.assign(T.size() + 1, 0);
-  uint64_t max_records = 0;
   for (size_t t = 0; t < T.size(); ++t) {
     if (T[t].my_blocks && T[t].nB) choose_chunks(T[t], slots, 2); else T[t].nchunk = 0;
     prefix[t + 1] = prefix[t] + T[t].my_blocks * T[t].nchunk;
-    if (T[t].nchunk) max_records = std::max<uint64_t>(max_records, T[t].nA + T[t].nB);
   }
   const uint64_t total = prefix.back();
   const size_t tab = sizeof(SearchParams) * T.size();
@@ -336,11 +328,16 @@ static int launch_local_cfg(std::vector<SearchParams>& T, Batch Bt, std::vector<
                            cudaMemcpyHostToDevice, stream));
   if (total == 0) return MCX_OK;
   if (total > 0x7fffffffull) return set_error(MCX_E_ARG, "grid too large");
-  if (T.size() > 65535) return set_error(MCX_E_ARG, "MCX_MODE_PREFILTER supports at most 65535 tasks per batch");
+  if (jobs.size() > 65535) return set_error(MCX_E_ARG, "MCX_MODE_PREFILTER supports at most 65535 meshes per batch");
   Bt.tasks = reinterpret_cast<const SearchParams*>(dev_tab);
   Bt.prefix = reinterpret_cast<const uint64_t*>((char*)dev_tab + tab);
   Bt.neg1 = 0xffffffffu;
-  const unsigned n = (unsigned)T.size();
+  Bt.fjobs = reinterpret_cast<const FboxJob*>(dev_jobs);
+  Bt.n_fjobs = (uint32_t)jobs.size();
+  CUDA_TRY(cudaMemcpyAsync(dev_jobs, jobs.data(), sizeof(FboxJob) * jobs.size(), cudaMemcpyHostToDevice, stream));
+  uint64_t max_records = 0;
+  for (const FboxJob& j : jobs) max_records = std::max<uint64_t>(max_records, j.n);
+  const unsigned n = (unsigned)jobs.size();
   uint64_t gx = (max_records + 1023) / 1024;
   const uint64_t gcap = std::max<uint64_t>(1, (uint64_t)dev_sms * 8 / n);
   if (gx > gcap) gx = gcap;
@@ -354,15 +351,16 @@ static int launch_local_cfg(std::vector<SearchParams>& T, Batch Bt, std::vector<
 // thread, 2-warp CTAs, one frame per warp, one vote per 16 B records, one LOP3 per two
 // pair tests — measured in DESIGN.md §5).
 static int launch_prefilter(std::vector<SearchParams>& T, const Batch& Bt, std::vector<uint64_t>& prefix,
-                            void* dev_tab, int device, cudaStream_t stream) {
+                            void* dev_tab, const std::vector<FboxJob>& jobs, void* dev_jobs, int device,
+                            cudaStream_t stream) {
   switch (variant_from_env()) {
-    case 1: return launch_local_cfg<LCfg<16, 8, 1, 1, true, true>>(T, Bt, prefix, dev_tab, device, stream);
-    case 2: return launch_local_cfg<LCfg<16, 32, 1, 1, true, true>>(T, Bt, prefix, dev_tab, device, stream);
-    case 3: return launch_local_cfg<LCfg<32, 16, 1, 1, true, true>>(T, Bt, prefix, dev_tab, device, stream);
-    case 4: return launch_local_cfg<LCfg<16, 8, 1, 1, true>>(T, Bt, prefix, dev_tab, device, stream);   // CTA frame
-    case 5: return launch_local_cfg<LCfg<16, 8, 1>>(T, Bt, prefix, dev_tab, device, stream);            // 1 LOP3/pair
-    case 6: return launch_local_cfg<LCfg<8, 8, 1, 1, true, true>>(T, Bt, prefix, dev_tab, device, stream);
-    default: return launch_local_cfg<LCfg<16, 16, 1, 1, true, true>>(T, Bt, prefix, dev_tab, device, stream);
+    case 1: return launch_local_cfg<LCfg<16, 8, 1, 1, true, true>>(T, Bt, prefix, dev_tab, jobs, dev_jobs, device, stream);
+    case 2: return launch_local_cfg<LCfg<16, 32, 1, 1, true, true>>(T, Bt, prefix, dev_tab, jobs, dev_jobs, device, stream);
+    case 3: return launch_local_cfg<LCfg<32, 16, 1, 1, true, true>>(T, Bt, prefix, dev_tab, jobs, dev_jobs, device, stream);
+    case 4: return launch_local_cfg<LCfg<16, 8, 1, 1, true>>(T, Bt, prefix, dev_tab, jobs, dev_jobs, device, stream);   // CTA frame
+    case 5: return launch_local_cfg<LCfg<16, 8, 1>>(T, Bt, prefix, dev_tab, jobs, dev_jobs, device, stream);            // 1 LOP3/pair
+    case 6: return launch_local_cfg<LCfg<8, 8, 1, 1, true, true>>(T, Bt, prefix, dev_tab, jobs, dev_jobs, device, stream);
+    default: return launch_local_cfg<LCfg<16, 16, 1, 1, true, true>>(T, Bt, prefix, dev_tab, jobs, dev_jobs, device, stream);
   }
 }
 

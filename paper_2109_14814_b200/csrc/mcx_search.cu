@@ -506,12 +506,20 @@ static uint64_t align16(uint64_t v) { return (v + 15) & ~15ull; }
 
 struct WsLayout {
   uint64_t counters, table, list, total, list_cap;
-  uint64_t quant;  // MCX_MODE_PREFILTER: per task conservative fp32 boxes of A and B
+  uint64_t jobs, quant;  // MCX_MODE_PREFILTER: fp32-box job table, then the boxes of each distinct mesh
 };
 
-// Bytes of one task's prefilter area: A's and B's conservative fp32 boxes (32 B each).
-static uint64_t quant_task_bytes(uint64_t nA, uint64_t nB) {
-  return 32 * (nA + nB);
+// MCX_MODE_PREFILTER: the distinct meshes of a batch (by box pointer, in order of
+// first appearance), each converted to conservative fp32 boxes once per call.
+static void distinct_meshes(const mcx_task* tasks, uint32_t n, std::vector<const mcx_mesh_dev*>& out) {
+  out.clear();
+  for (uint32_t t = 0; t < n; ++t)
+    for (const mcx_mesh_dev* m : {tasks[t].A, tasks[t].B}) {
+      if (!m) continue;
+      bool seen = false;
+      for (const mcx_mesh_dev* x : out) seen |= (x->box == m->box);
+      if (!seen) out.push_back(m);
+    }
 }
 
 static WsLayout ws_layout(const mcx_task* tasks, uint32_t n, const mcx_opts* o) {
@@ -531,11 +539,15 @@ static WsLayout ws_layout(const mcx_task* tasks, uint32_t n, const mcx_opts* o) 
       L.list_cap += g.my_blocks * ((B->n_tri + TILE - 1) / TILE);
     }
   }
-  L.quant = align16(L.list + 16 * L.list_cap);
-  L.total = L.quant;
+  L.jobs = align16(L.list + 16 * L.list_cap);
+  L.quant = L.jobs;
+  L.total = L.jobs;
   if (o && o->mode == MCX_MODE_PREFILTER) {
-    for (uint32_t t = 0; t < n; ++t)
-      if (tasks[t].A && tasks[t].B) L.total += quant_task_bytes(tasks[t].A->n_tri, tasks[t].B->n_tri);
+    std::vector<const mcx_mesh_dev*> ms;
+    distinct_meshes(tasks, n, ms);
+    L.quant = align16(L.jobs + sizeof(FboxJob) * ms.size());
+    L.total = L.quant;
+    for (const mcx_mesh_dev* m : ms) L.total += 32 * m->n_tri;
   }
   return L;
 }
@@ -555,7 +567,21 @@ static int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mc
     return set_error(MCX_E_ARG, "workspace too small or misaligned (need %llu bytes, 16-byte aligned)",
                      (unsigned long long)L.total);
   char* ws = (char*)o->workspace;
-  uint64_t qoff = L.quant;
+  std::vector<const mcx_mesh_dev*> meshes;
+  std::vector<FboxJob> jobs;
+  if (o->mode == MCX_MODE_PREFILTER) {
+    distinct_meshes(tasks, n, meshes);
+    uint64_t off = L.quant;
+    for (const mcx_mesh_dev* m : meshes) {
+      jobs.push_back(FboxJob{reinterpret_cast<const Box*>(m->box), reinterpret_cast<float4*>(ws + off), m->n_tri});
+      off += 32 * m->n_tri;
+    }
+  }
+  auto fbox_of = [&](const mcx_mesh_dev* m) -> float4* {
+    for (size_t k = 0; k < meshes.size(); ++k)
+      if (meshes[k]->box == m->box) return jobs[k].dst;
+    return nullptr;
+  };
   std::vector<SearchParams> T(n);
   for (uint32_t t = 0; t < n; ++t) {
     const mcx_mesh_dev* A = tasks[t].A;
@@ -599,9 +625,8 @@ static int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mc
     P.statusA = A->status;
     P.statusB = B->status;
     if (o->mode == MCX_MODE_PREFILTER) {
-      P.fA = reinterpret_cast<float4*>(ws + qoff);
-      P.fB = P.fA + 2 * A->n_tri;
-      qoff += quant_task_bytes(A->n_tri, B->n_tri);
+      P.fA = fbox_of(A);
+      P.fB = fbox_of(B);
     }
     st[t] = mcx_stats{};
     st[t].n_pairs = g.na * B->n_tri;
@@ -625,7 +650,8 @@ static int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mc
   std::vector<uint64_t> prefix;
   const int rc = o->mode == MCX_MODE_BRUTE ? launch_brute<KIND_TRI>(T, Bt, prefix, ws + L.table, o->device, stream)
                  : o->mode == MCX_MODE_CULL ? launch_cull<KIND_TRI>(T, Bt, prefix, ws + L.table, o->device, stream)
-                                            : launch_prefilter(T, Bt, prefix, ws + L.table, o->device, stream);
+                                            : launch_prefilter(T, Bt, prefix, ws + L.table, jobs, ws + L.jobs,
+                                                               o->device, stream);
   if (rc != MCX_OK) return rc;
   if (o->timing) CUDA_TRY(cudaEventRecord(tm.e1, stream));
   status_kernel<<<1, 32, 0, stream>>>(reinterpret_cast<const SearchParams*>(ws + L.table), n,

@@ -65,6 +65,13 @@ struct __align__(16) SearchParams {
   float4* fB;
 };
 
+// MCX_MODE_PREFILTER: conservative fp32 boxes of one distinct mesh of the batch.
+struct FboxJob {
+  const Box* src;
+  float4* dst;  // [n][2]: lo rounded toward −∞, hi toward +∞
+  uint64_t n;
+};
+
 // Whole-launch parameters: the task table and the shared outputs.
 struct Batch {
   const SearchParams* tasks;
@@ -79,6 +86,8 @@ struct Batch {
   uint64_t blk_cap;
   unsigned long long* list_count;
   uint32_t neg1;                 // 0xffffffff, a runtime operand so the packed subtract stays an IMAD
+  const struct FboxJob* fjobs;   // MCX_MODE_PREFILTER: one fp32-box conversion per distinct mesh
+  uint32_t n_fjobs;
 };
 
 // Task owning work unit u: the last t with prefix[t] <= u (n_tasks is small).

@@ -315,7 +315,8 @@ def test_search_batch_equals_individual(mode):
         A, _, B, _ = config_pair(name)
         meshes[name] = (D.DeviceMesh(A, 0), D.DeviceMesh(B, 0))
     pairs = [(*meshes["C1"],), (*meshes["C4i"],), (*meshes["C4iii"],), (*meshes["C5/8"],),
-             (*meshes["C4i"], (1000, 5000)), (meshes["C1"][1], meshes["C4i"][0])]
+             (*meshes["C4i"], (1000, 5000)), (meshes["C1"][1], meshes["C4i"][0]),
+             (meshes["C4i"][0], meshes["C4i"][0])]  # meshes shared across tasks and within one
     batch = D.search_batch(pairs, mode=mode)
     for p, r in zip(pairs, batch):
         single = D.search_device(p[0], p[1], mode=mode, a_range=p[2] if len(p) > 2 else None)
@@ -334,7 +335,7 @@ def test_search_batch_sharded(mode):
         assert np.array_equal(D._merge([p[t] for p in parts]).hits, full[t].hits)
 
 
-@pytest.mark.parametrize("mode", ["cull", "brute"])
+@pytest.mark.parametrize("mode", ["cull", "brute", "prefilter"])
 def test_search_plan_matches_oracle(mode):
     from paper_2109_14814_b200 import layers
     from paper_2109_14814_b200.mesh import half_layer, layered_mesh
