@@ -32,8 +32,9 @@ namespace mcx {
 //     4 "all fail" chains — "both fail at a common guard position", a conservative
 //     "both fail".  1.5 instructions per pair; the fma pipe (IMAD, 64 lanes/clk/SM)
 //     binds.  One warp vote per JB B records.
-//   * B records reach shared memory as fp32 boxes (bulk copies, 8 KB stages); the
-//     CTA quantises each tile into its frame (~1/50 of the test work) before testing.
+//   * B records reach shared memory as fp32 boxes (bulk copies, 8 KB stages); each
+//     warp quantises each tile into its own frame (~1/20 of the test work) before
+//     testing it.
 //   * On a vote the warp re-tests that B record against its A words (kept in shared
 //     memory) and runs the exact FP64 box test on the quantised passes from L1/L2;
 //     survivors are queued and solved exactly like the FP64 kernel.
