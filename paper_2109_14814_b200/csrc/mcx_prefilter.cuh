@@ -47,11 +47,22 @@ __device__ __forceinline__ unsigned imad_sub(unsigned a, unsigned m1, unsigned b
   return r;
 }
 
+// xa = ha − l with borrow-out, xb = hb − l − borrow.  H > L always holds (every H
+// nibble ≥ 7 ≥ every L nibble, H ≠ L), so the borrow is 0 and xb = hb − l; the chain
+// only makes ptxas put the first subtraction on the alu pipe (IADD3 with carry-out).
+__device__ __forceinline__ void sub2_cc(unsigned& xa, unsigned& xb, unsigned ha, unsigned hb, unsigned l) {
+  asm("sub.cc.u32 %0, %2, %4;\n subc.u32 %1, %3, %4;" : "=r"(xa), "=r"(xb) : "r"(ha), "r"(hb), "r"(l));
+}
+
 constexpr int FTILE = 256;  // B records per stage (256 × 32 B = 8 KB)
 constexpr unsigned G4 = 0x88888888u;
 
-template <int QR_, int JB_, int UNROLL_, int MINB_ = 1, bool PAIR2_ = false, bool WFRAME_ = false>
+template <int QR_, int JB_, int UNROLL_, int MINB_ = 1, bool PAIR2_ = false, bool WFRAME_ = false, int SUBMIX_ = 0>
 struct LCfg {
+  // subtractions not forced onto the fma pipe: 0 none; 1 / 2: the second of every other /
+  // every pair left to ptxas as plain C (it still picks IMAD.IADD); 3 / 4: one / two of every
+  // 16 pairs through a borrow chain, whose first subtraction must be an alu IADD3
+  static constexpr int SUBMIX = SUBMIX_;
   static constexpr bool PAIR2 = PAIR2_;    // one LOP3 for two pair tests (conservative "both fail")
   static constexpr bool WFRAME = WFRAME_;  // one frame per warp (its 32·QR A records) instead of per CTA
   static constexpr int QR = QR_;
@@ -276,8 +287,17 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_local_kernel(const
         bw[u] = S.qt[fi][j + u];
         if constexpr (C::PAIR2) {
 #pragma unroll
-          for (int r = 0; r < QR; r += 2)
-            fail_and2(allfail[(r >> 1) & 3], imad_sub(hw[r], m1, bw[u]), imad_sub(hw[r + 1], m1, bw[u]));
+          for (int r = 0; r < QR; r += 2) {
+            const bool plain = (C::SUBMIX == 2) || (C::SUBMIX == 1 && (r & 3) == 2);
+            if (C::SUBMIX >= 3 && (r & (C::SUBMIX == 3 ? 7 : 3)) == (C::SUBMIX == 3 ? 6 : 2)) {
+              unsigned xa, xb;  // borrow chain: the first subtraction must be an alu IADD3
+              sub2_cc(xa, xb, hw[r], hw[r + 1], bw[u]);
+              fail_and2(allfail[(r >> 1) & 3], xa, xb);
+            } else {
+              fail_and2(allfail[(r >> 1) & 3], imad_sub(hw[r], m1, bw[u]),
+                        plain ? hw[r + 1] - bw[u] : imad_sub(hw[r + 1], m1, bw[u]));
+            }
+          }
         } else {
 #pragma unroll
           for (int r = 0; r < QR; ++r) fail_and1(allfail[r & 3], imad_sub(hw[r], m1, bw[u]));
@@ -350,7 +370,7 @@ static int launch_local_cfg(std::vector<SearchParams>& T, Batch Bt, std::vector<
 
 // Variant selection (MCX_VARIANT, experiments; 0 = the tuned default: 16 A records per
 // thread, 2-warp CTAs, one frame per warp, one vote per 16 B records, one LOP3 per two
-// pair tests — measured in DESIGN.md §5).
+// pair tests, 1 of 16 subtractions on the alu pipe — measured in DESIGN.md §5).
 static int launch_prefilter(std::vector<SearchParams>& T, const Batch& Bt, std::vector<uint64_t>& prefix,
                             void* dev_tab, const std::vector<FboxJob>& jobs, void* dev_jobs, int device,
                             cudaStream_t stream) {
@@ -361,7 +381,11 @@ static int launch_prefilter(std::vector<SearchParams>& T, const Batch& Bt, std::
     case 4: return launch_local_cfg<LCfg<16, 8, 1, 1, true>>(T, Bt, prefix, dev_tab, jobs, dev_jobs, device, stream);   // CTA frame
     case 5: return launch_local_cfg<LCfg<16, 8, 1>>(T, Bt, prefix, dev_tab, jobs, dev_jobs, device, stream);            // 1 LOP3/pair
     case 6: return launch_local_cfg<LCfg<8, 8, 1, 1, true, true>>(T, Bt, prefix, dev_tab, jobs, dev_jobs, device, stream);
-    default: return launch_local_cfg<LCfg<16, 16, 1, 1, true, true>>(T, Bt, prefix, dev_tab, jobs, dev_jobs, device, stream);
+    case 7: return launch_local_cfg<LCfg<16, 16, 1, 1, true, true, 1>>(T, Bt, prefix, dev_tab, jobs, dev_jobs, device, stream);
+    case 8: return launch_local_cfg<LCfg<16, 16, 1, 1, true, true, 2>>(T, Bt, prefix, dev_tab, jobs, dev_jobs, device, stream);
+    case 9: return launch_local_cfg<LCfg<16, 16, 1, 1, true, true>>(T, Bt, prefix, dev_tab, jobs, dev_jobs, device, stream);
+    case 10: return launch_local_cfg<LCfg<16, 16, 1, 1, true, true, 4>>(T, Bt, prefix, dev_tab, jobs, dev_jobs, device, stream);
+    default: return launch_local_cfg<LCfg<16, 16, 1, 1, true, true, 3>>(T, Bt, prefix, dev_tab, jobs, dev_jobs, device, stream);
   }
 }
 
