@@ -330,28 +330,12 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_local_kernel(const
 template <class C>
 static int launch_local_cfg(std::vector<SearchParams>& T, Batch Bt, std::vector<uint64_t>& prefix, void* dev_tab,
                             const std::vector<FboxJob>& jobs, void* dev_jobs, int device, cudaStream_t stream) {
-  int dev_sms = 148;
-  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device);
   const size_t smem = sizeof(LSmem<C>);
-  CUDA_TRY(cudaFuncSetAttribute(search_local_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int occ = 1;
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, search_local_kernel<C>, C::THREADS, smem));
-  const uint64_t slots = (uint64_t)dev_sms * (occ > 0 ? occ : 1);
-  prefix.assign(T.size() + 1, 0);
-  for (size_t t = 0; t < T.size(); ++t) {
-    if (T[t].my_blocks && T[t].nB) choose_chunks(T[t], slots, 2); else T[t].nchunk = 0;
-    prefix[t + 1] = prefix[t] + T[t].my_blocks * T[t].nchunk;
-  }
-  const uint64_t total = prefix.back();
-  const size_t tab = sizeof(SearchParams) * T.size();
-  CUDA_TRY(cudaMemcpyAsync(dev_tab, T.data(), tab, cudaMemcpyHostToDevice, stream));
-  CUDA_TRY(cudaMemcpyAsync((char*)dev_tab + tab, prefix.data(), sizeof(uint64_t) * prefix.size(),
-                           cudaMemcpyHostToDevice, stream));
-  if (total == 0) return MCX_OK;
-  if (total > 0x7fffffffull) return set_error(MCX_E_ARG, "grid too large");
+  uint64_t slots = 0, total = 0;
+  int rc = resident_slots(search_local_kernel<C>, C::THREADS, smem, device, &slots);
+  if (rc == MCX_OK) rc = upload_plan(T, Bt, prefix, dev_tab, slots, 2, stream, &total);
+  if (rc != MCX_OK || total == 0) return rc;
   if (jobs.size() > 65535) return set_error(MCX_E_ARG, "MCX_MODE_PREFILTER supports at most 65535 meshes per batch");
-  Bt.tasks = reinterpret_cast<const SearchParams*>(dev_tab);
-  Bt.prefix = reinterpret_cast<const uint64_t*>((char*)dev_tab + tab);
   Bt.neg1 = 0xffffffffu;
   Bt.fjobs = reinterpret_cast<const FboxJob*>(dev_jobs);
   Bt.n_fjobs = (uint32_t)jobs.size();
@@ -359,8 +343,8 @@ static int launch_local_cfg(std::vector<SearchParams>& T, Batch Bt, std::vector<
   uint64_t max_records = 0;
   for (const FboxJob& j : jobs) max_records = std::max<uint64_t>(max_records, j.n);
   const unsigned n = (unsigned)jobs.size();
-  uint64_t gx = (max_records + 1023) / 1024;
-  const uint64_t gcap = std::max<uint64_t>(1, (uint64_t)dev_sms * 8 / n);
+  uint64_t gx = (max_records + 1023) / 1024;  // ~4 records per thread, ~2 blocks per search slot overall
+  const uint64_t gcap = std::max<uint64_t>(1, 2 * slots / n);
   if (gx > gcap) gx = gcap;
   fbox_kernel<<<dim3((unsigned)gx, n), 256, 0, stream>>>(Bt);
   search_local_kernel<C><<<(unsigned)total, C::THREADS, smem, stream>>>(Bt);

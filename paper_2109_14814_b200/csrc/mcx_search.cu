@@ -410,27 +410,11 @@ __global__ void __launch_bounds__(CULL_THREADS) cull_pairs_kernel(const Batch Bt
 template <int KIND, class C>
 static int launch_brute_cfg(std::vector<SearchParams>& T, Batch Bt, std::vector<uint64_t>& prefix, void* dev_tab,
                             int device, cudaStream_t stream) {
-  int dev_sms = 148;
-  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device);
   const size_t smem = sizeof(SearchSmem<C>);
-  CUDA_TRY(cudaFuncSetAttribute(search_brute_kernel<KIND, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int occ = C::MINB;
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, search_brute_kernel<KIND, C>, C::THREADS, smem));
-  const uint64_t slots = (uint64_t)dev_sms * (occ > 0 ? occ : 1);
-  prefix.assign(T.size() + 1, 0);
-  for (size_t t = 0; t < T.size(); ++t) {
-    if (T[t].my_blocks && T[t].nB) choose_chunks(T[t], slots); else T[t].nchunk = 0;
-    prefix[t + 1] = prefix[t] + T[t].my_blocks * T[t].nchunk;
-  }
-  const uint64_t total = prefix.back();
-  const size_t tab = sizeof(SearchParams) * T.size();
-  CUDA_TRY(cudaMemcpyAsync(dev_tab, T.data(), tab, cudaMemcpyHostToDevice, stream));
-  CUDA_TRY(cudaMemcpyAsync((char*)dev_tab + tab, prefix.data(), sizeof(uint64_t) * prefix.size(),
-                           cudaMemcpyHostToDevice, stream));
-  if (total == 0) return MCX_OK;
-  if (total > 0x7fffffffull) return set_error(MCX_E_ARG, "grid too large");
-  Bt.tasks = reinterpret_cast<const SearchParams*>(dev_tab);
-  Bt.prefix = reinterpret_cast<const uint64_t*>((char*)dev_tab + tab);
+  uint64_t slots = 0, total = 0;
+  int rc = resident_slots(search_brute_kernel<KIND, C>, C::THREADS, smem, device, &slots);
+  if (rc == MCX_OK) rc = upload_plan(T, Bt, prefix, dev_tab, slots, 16, stream, &total);
+  if (rc != MCX_OK || total == 0) return rc;
   search_brute_kernel<KIND, C><<<(unsigned)total, C::THREADS, smem, stream>>>(Bt);
   CUDA_TRY(cudaGetLastError());
   return MCX_OK;

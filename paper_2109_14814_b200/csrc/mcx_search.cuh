@@ -214,6 +214,39 @@ static void choose_chunks(SearchParams& P, uint64_t slots, uint64_t min_tiles = 
   P.b_chunk = chunk;
 }
 
+// Chunk every task for `slots` resident CTAs, build the per-task prefix of work units
+// and upload the task table + prefix to dev_tab (stream-ordered).  *total = CTAs to
+// launch; Bt's table pointers are set.  Shared by the brute and prefilter launchers.
+static int upload_plan(std::vector<SearchParams>& T, Batch& Bt, std::vector<uint64_t>& prefix, void* dev_tab,
+                       uint64_t slots, uint64_t min_tiles, cudaStream_t stream, uint64_t* total) {
+  prefix.assign(T.size() + 1, 0);
+  for (size_t t = 0; t < T.size(); ++t) {
+    if (T[t].my_blocks && T[t].nB) choose_chunks(T[t], slots, min_tiles); else T[t].nchunk = 0;
+    prefix[t + 1] = prefix[t] + T[t].my_blocks * T[t].nchunk;
+  }
+  *total = prefix.back();
+  const size_t tab = sizeof(SearchParams) * T.size();
+  CUDA_TRY(cudaMemcpyAsync(dev_tab, T.data(), tab, cudaMemcpyHostToDevice, stream));
+  CUDA_TRY(cudaMemcpyAsync((char*)dev_tab + tab, prefix.data(), sizeof(uint64_t) * prefix.size(),
+                           cudaMemcpyHostToDevice, stream));
+  if (*total > 0x7fffffffull) return set_error(MCX_E_ARG, "grid too large");
+  Bt.tasks = reinterpret_cast<const SearchParams*>(dev_tab);
+  Bt.prefix = reinterpret_cast<const uint64_t*>((char*)dev_tab + tab);
+  return MCX_OK;
+}
+
+// Resident CTAs of `kernel` on the whole device (at least one per SM).
+template <class K>
+static int resident_slots(K kernel, int threads, size_t smem, int device, uint64_t* slots) {
+  int dev_sms = 148;
+  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device);
+  CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 1;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem));
+  *slots = (uint64_t)dev_sms * (occ > 0 ? occ : 1);
+  return MCX_OK;
+}
+
 // Variant selection (MCX_VARIANT=0..3, for experiments; 0 = the tuned default:
 // R = 4, 256 threads, 2 CTAs/SM, next B box prefetched from shared memory before
 // the current one's compares, unroll 4 — no spills).
