@@ -472,6 +472,24 @@ def run_ours(args):
                          "quad_box_tests": int(pst["n_tested"]), "same_candidates": bool(np.array_equal(cand, cand2)),
                          "path": "packed meshes -> mcx_pair_candidates_mesh (exact union-box culling)"}}
 
+    # ---- the 8-GPU partition of the headline workload, run shard by shard on this GPU
+    # (world == 1 only): per-shard device time of the primary mode; the max over shards is
+    # what an 8-GPU run's max-over-ranks timing would see for the kernel alone
+    shards8 = None
+    if world == 1 and not args.no_c5:
+        mode = modes[primary]
+        ms8 = []
+        for g in range(8):
+            D.search_device(Am, Bm, mode=mode, shard=(g, 8), stream=stream)
+            ms8.append(min(D.search_device(Am, Bm, mode=mode, shard=(g, 8), stream=stream, timing=True)
+                           .stats["kernel_ms"] for _ in range(2)))
+        shards8 = {"mode": primary, "per_shard_kernel_ms": ms8, "max_over_mean": max(ms8) / statistics.mean(ms8),
+                   "sum_over_unsharded": sum(ms8) / m1["kernel_ms"],
+                   "pairs_per_s_if_8_gpus": desc["pairs_per_step"] / (max(ms8) * 1e-3),
+                   "note": "NOT a multi-GPU measurement: the 8 cyclic A-block shards of this workload timed one "
+                           "after another on one GPU (kernel events); the last field is the pair rate 8 GPUs "
+                           "would reach if each ran its shard as fast, with no host or copy overhead"}
+
     # ---- configs[4]: unbalanced high-hit-density pair (C5hd: 4.2M x 65k triangles, 13,226
     # hits clustered in A's first quarter) - hit compaction, and the 8-GPU cyclic partition's
     # balance measured shard by shard on this GPU (world == 1 only)
@@ -514,7 +532,7 @@ def run_ours(args):
                 "config": bench_config(desc, primary, world),
                 "search_wall_s": m1["ms_per_step"] / 1e3, "hits": m1["hits"], "kernel_ms": m1["kernel_ms"],
                 "roofline": roofline, "fp64_brute": fp64_block, "prefilter": pre_block, "cull": cull_block,
-                "e2e": e2e, "cpu_baseline": cpu, "paper_workload": paper, "c5_unbalanced": c5, "clocks": m1["clocks"],
+                "e2e": e2e, "cpu_baseline": cpu, "paper_workload": paper, "c5_unbalanced": c5, "shards8": shards8, "clocks": m1["clocks"],
                 "gpu_launches": m1["launches"], "gpu": props.name, "sms": sms}
         print(json.dumps(line), flush=True)
     if world > 1:
