@@ -513,3 +513,30 @@ def test_c5hd_cyclic_shards_balance_hits(mode, c5hd):
     assert_same_hits(ref, got)
     counts = np.array([len(p) for p in parts])
     assert counts.max() <= 1.5 * counts.mean(), counts
+
+
+@pytest.mark.parametrize("case", range(24))
+def test_random_meshes_all_modes(case, oracle_lib):
+    """Randomised parity sweep: random grid shapes (ragged, odd, tiny, tall), surfaces,
+    affine scalings (1e-8 .. 1e8), translations and near-coincident copies, each
+    searched in all three modes against the C oracle's exact sweep."""
+    rng = np.random.default_rng(1000 + case)
+    na, ma = int(rng.integers(1, 160)), int(rng.integers(2, 70))
+    nb, mb = int(rng.integers(1, 160)), int(rng.integers(2, 70))
+    A, _ = manifold_like(na, ma, int(rng.integers(0, 50)))
+    kind = case % 3
+    if kind == 0:    # independent surfaces
+        B, _ = manifold_like(nb, mb, int(rng.integers(0, 50)))
+    elif kind == 1:  # the same surface resampled, slightly perturbed (dense contacts)
+        B, _ = manifold_like(nb, mb, 7)
+        A, _ = manifold_like(na, ma, 7)
+        B = B + rng.normal(0, 1e-3, (4, 1, 1))
+    else:            # a copy of A shifted by a fraction of a cell (many touching boxes)
+        B = A + rng.normal(0, 1e-2, (4, 1, 1))
+    scale = 10.0 ** rng.uniform(-8, 8)
+    shift = rng.normal(0, 10, (4, 1, 1)) * scale
+    A, B = A * scale + shift + 0.0, B * scale + shift + 0.0
+    ref = oracle_lib.search(A, B, sweep=True)
+    for mode in MODES:
+        r = D.search(A, B, mode=mode)
+        assert_same_hits(ref, r.hits, r.stats)
