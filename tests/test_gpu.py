@@ -7,6 +7,7 @@ sweep-and-prune (same predicate, only skips x-disjoint pairs) plus
 size-independent properties: partition / shard / variant invariance.
 """
 import os
+import sys
 
 import numpy as np
 import pytest
@@ -540,3 +541,18 @@ def test_random_meshes_all_modes(case, oracle_lib):
     for mode in MODES:
         r = D.search(A, B, mode=mode)
         assert_same_hits(ref, r.hits, r.stats)
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck", "initcheck"])
+def test_compute_sanitizer_clean(tool):
+    """Every libmcx kernel (pack, levels, three search modes, batches, shards, the
+    capacity-regrow path, pair_candidates, records) under compute-sanitizer: no errors."""
+    import shutil
+    import subprocess
+    exe = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([exe, "--tool", tool, "--error-exitcode", "7", sys.executable,
+                          os.path.join(root, "tools", "sanitize_run.py")],
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
+    assert "sanitize workload ok" in out.stdout
