@@ -214,9 +214,9 @@ class ClockSampler:
 KERNEL_LAUNCHES = {"brute": 2, "cull": 3, "prefilter": 3}
 INT_LANES_PER_CLK_PER_SM = 64  # B200 fma-heavy (IMAD) and alu (LOP3) pipes, each; IMAD measured 62.7 lanes/clk/SM
                                # (tools/microbench/hprefilter.cu swar3_mix0); issue: 4 SMSP x 32 = 128 lanes/clk/SM
-# SASS of the prefilter inner loop, per 16 pair tests: 14 IMAD + 1 IMAD.X (fma-heavy pipe),
-# 1 IADD3 + 8 LOP3.LUT.PAND (alu pipe)
-PREFILTER_IMAD_PER_PAIR = 15.0 / 16.0
+# SASS of the prefilter inner loop, per 16 pair tests: 12 IMAD + 2 IMAD.X (fma-heavy pipe),
+# 2 IADD3 + 8 LOP3.LUT.PAND (alu pipe)
+PREFILTER_IMAD_PER_PAIR = 14.0 / 16.0
 
 
 def run_ours(args):
@@ -356,8 +356,8 @@ def run_ours(args):
                         "(profiles/r01_ncu_brute_c3.txt): 2.16 GB vs 68 GB of algorithmic L2->SMEM tile "
                         "traffic; B's 67 MB of boxes are re-read from HBM ~32x per launch (L2 is split "
                         "over two dies) at ~4 GB/s - negligible against the FP64 bound"}
-    # ---- roofline of the prefilter kernel: every pair = 15/16 IMAD-class op (fma-heavy pipe,
-    # 64 lanes/clk/SM = the bound) + 1/16 IADD3 + 1/2 LOP3 (alu pipe); issue: 1.5 instructions per pair
+    # ---- roofline of the prefilter kernel: every pair = 14/16 IMAD-class op (fma-heavy pipe,
+    # 64 lanes/clk/SM = the bound) + 2/16 IADD3 + 1/2 LOP3 (alu pipe); issue: 1.5 instructions per pair
     pst = pre["stats"]
     pf_peak = sms * INT_LANES_PER_CLK_PER_SM / PREFILTER_IMAD_PER_PAIR * f_max * 1e6
     pf_achieved = pst["n_tested"] / (pst["kernel_ms"] * 1e-3)
@@ -368,8 +368,8 @@ def run_ours(args):
         "peak_source": f"{sms} SMs x {INT_LANES_PER_CLK_PER_SM} IMAD lanes/clk (fma-heavy pipe) / "
                        f"{PREFILTER_IMAD_PER_PAIR:.4f} IMAD-class ops per pair x {f_max:.0f} MHz (IMAD rate "
                        "measured 62.7 lanes/clk/SM, tools/microbench/hprefilter.cu); the alu pipe and issue "
-                       "bind later (114 and 85 pairs/clk/SM)",
-        "work_per_launch": "n_pairs quantised pair tests (15/16 IMAD + 1/16 IADD3 + 1/2 LOP3 each) + "
+                       "bind later (102 and 85 pairs/clk/SM)",
+        "work_per_launch": "n_pairs quantised pair tests (14/16 IMAD + 2/16 IADD3 + 1/2 LOP3 each) + "
                            "n_exact_tests FP64 box tests",
         "exact_tests_per_step": pst["n_exact_tests"], "kernel_ms": pst["kernel_ms"],
         "kernel_ms_note": "CUDA events around the whole call: fp32 box kernel (~0.03 ms) + search",

@@ -60,8 +60,8 @@ constexpr unsigned G4 = 0x88888888u;
 template <int QR_, int JB_, int UNROLL_, int MINB_ = 1, bool PAIR2_ = false, bool WFRAME_ = false, int SUBMIX_ = 0>
 struct LCfg {
   // subtractions not forced onto the fma pipe: 0 none; 1 / 2: the second of every other /
-  // every pair left to ptxas as plain C (it still picks IMAD.IADD); 3 / 4: one / two of every
-  // 16 pairs through a borrow chain, whose first subtraction must be an alu IADD3
+  // every pair left to ptxas as plain C (it still picks IMAD.IADD); 3 / 4: two / four of every
+  // 16 pairs in borrow chains, whose first subtraction must be an alu IADD3
   static constexpr int SUBMIX = SUBMIX_;
   static constexpr bool PAIR2 = PAIR2_;    // one LOP3 for two pair tests (conservative "both fail")
   static constexpr bool WFRAME = WFRAME_;  // one frame per warp (its 32·QR A records) instead of per CTA
@@ -354,7 +354,7 @@ static int launch_local_cfg(std::vector<SearchParams>& T, Batch Bt, std::vector<
 
 // Variant selection (MCX_VARIANT, experiments; 0 = the tuned default: 16 A records per
 // thread, 2-warp CTAs, one frame per warp, one vote per 16 B records, one LOP3 per two
-// pair tests, 1 of 16 subtractions on the alu pipe — measured in DESIGN.md §5).
+// pair tests, 2 of 16 subtractions on the alu pipe — measured in DESIGN.md §5).
 static int launch_prefilter(std::vector<SearchParams>& T, const Batch& Bt, std::vector<uint64_t>& prefix,
                             void* dev_tab, const std::vector<FboxJob>& jobs, void* dev_jobs, int device,
                             cudaStream_t stream) {
