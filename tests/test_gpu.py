@@ -371,6 +371,12 @@ def test_cli_intersect(tmp_path):
                      "--manifest", str(tmp_path / "m.json")]) == 0
     recs, _ = layers.search_plan(u, s, layers.read_plan(tmp_path / "plan.txt"))
     assert (tmp_path / "rec.txt").read_text().splitlines() == [r.to_line() for r in recs]
+    for mode in ("brute", "prefilter"):  # every search mode writes the identical records file
+        out = tmp_path / f"rec_{mode}.txt"
+        assert cli.main(["intersect", "--umesh", str(tmp_path / "u.mnf"), "--smesh", str(tmp_path / "s.mnf"),
+                         "--plan", str(tmp_path / "plan.txt"), "--backend", "cuda", "--out", str(out),
+                         "--mode", mode]) == 0
+        assert out.read_text() == (tmp_path / "rec.txt").read_text()
 
 
 # ------------------------------------------------------------ device record fields (§8(f) row 4)
