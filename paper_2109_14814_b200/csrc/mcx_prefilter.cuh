@@ -232,14 +232,24 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_local_kernel(const
   unsigned long long n_pass = 0, n_sing = 0, n_exact = 0;
   const unsigned lt_mask = (1u << lane) - 1u;
 
+  // Rare path for B record ib (word bw): the lane's quantised passes as a bit mask over
+  // its A slots, then the exact FP64 box test for them only, one pass per lane per round.
   auto slow = [&](uint32_t ib, unsigned bw) {
+    unsigned msk = 0;
+#pragma unroll
+    for (int r = 0; r < QR; ++r)  // invalid A slots never pass
+      msk |= (((S.aw[warp][r][lane] - bw) & G4) == G4) ? (1u << r) : 0u;
+    if (!__any_sync(0xffffffffu, msk != 0)) return;  // a spurious vote of the paired LOP3 test
     const double2* bp = reinterpret_cast<const double2*>(P.boxB + ib);
     const double2 l01 = __ldg(bp), l23 = __ldg(bp + 1), g01 = __ldg(bp + 2), g23 = __ldg(bp + 3);
-    for (int r = 0; r < QR; ++r) {
-      const uint32_t ia = abase + r * 32;
+    while (__any_sync(0xffffffffu, msk != 0)) {
       bool p = false;
-      if (((S.aw[warp][r][lane] - bw) & G4) == G4) {  // quantised pass (invalid slots never pass)
+      uint32_t ia = 0;
+      if (msk) {
+        const int r = __ffs(msk) - 1;
+        msk &= msk - 1;
         ++n_exact;
+        ia = abase + r * 32;
         const double2* ap = reinterpret_cast<const double2*>(P.boxA + ia);
         const double2 a01 = __ldg(ap), a23 = __ldg(ap + 1), c01 = __ldg(ap + 2), c23 = __ldg(ap + 3);
         p = (l01.x <= c01.x) & (a01.x <= g01.x) & (l01.y <= c01.y) & (a01.y <= g01.y) &
