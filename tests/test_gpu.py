@@ -192,13 +192,14 @@ def test_natural_and_tiled_orders_agree():
     assert np.array_equal(r1.hits, r2.hits)
 
 
-def test_capacity_regrow():
+@pytest.mark.parametrize("mode", MODES)
+def test_capacity_regrow(mode):
     A, _, B, _ = config_pair("C4ii")  # 54k hits
     Am, Bm = D.DeviceMesh(A, 0), D.DeviceMesh(B, 0)
     D._Workspace.get(0).hits = None
-    r_small = D.search_device(Am, Bm, cap=7)
+    r_small = D.search_device(Am, Bm, cap=7, mode=mode)
     D._Workspace.get(0).hits = None
-    r_big = D.search_device(Am, Bm, cap=1 << 20)
+    r_big = D.search_device(Am, Bm, cap=1 << 20, mode=mode)
     assert len(r_small.hits) == len(r_big.hits) == 54201
     assert np.array_equal(r_small.hits, r_big.hits)
 
