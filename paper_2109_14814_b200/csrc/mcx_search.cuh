@@ -190,13 +190,13 @@ __device__ __forceinline__ void flush_counters(const SearchParams& P, int lane, 
 // count whose CTA total best fills whole waves of resident CTAs (the last partial
 // wave idles the rest of the GPU), among counts giving >= 8 waves with chunks of
 // >= min_tiles tiles (1 tile for small problems).
-static void choose_chunks(SearchParams& P, uint64_t slots, uint64_t min_tiles = 16) {
-  const uint64_t max_chunks = (P.nB + TILE - 1) / TILE;
-  uint64_t nchunk = 1, chunk = max_chunks * TILE;
-  const uint64_t min_ch = (P.my_blocks * max_chunks < 8 * slots) ? (uint64_t)TILE : min_tiles * (uint64_t)TILE;
+static void choose_chunks(SearchParams& P, uint64_t slots, uint64_t min_tiles = 16, uint64_t tile = TILE) {
+  const uint64_t max_chunks = (P.nB + tile - 1) / tile;
+  uint64_t nchunk = 1, chunk = max_chunks * tile;
+  const uint64_t min_ch = (P.my_blocks * max_chunks < 8 * slots) ? tile : min_tiles * tile;
   double best = -1.0;
   for (uint64_t c = 1; c <= max_chunks && c <= 4096; ++c) {
-    const uint64_t ch = ((P.nB + c - 1) / c + TILE - 1) / TILE * TILE;
+    const uint64_t ch = ((P.nB + c - 1) / c + tile - 1) / tile * tile;
     const uint64_t nc = (P.nB + ch - 1) / ch;
     if (nc != c) continue;
     const uint64_t total = P.my_blocks * nc;
@@ -218,10 +218,11 @@ static void choose_chunks(SearchParams& P, uint64_t slots, uint64_t min_tiles = 
 // and upload the task table + prefix to dev_tab (stream-ordered).  *total = CTAs to
 // launch; Bt's table pointers are set.  Shared by the brute and prefilter launchers.
 static int upload_plan(std::vector<SearchParams>& T, Batch& Bt, std::vector<uint64_t>& prefix, void* dev_tab,
-                       uint64_t slots, uint64_t min_tiles, cudaStream_t stream, uint64_t* total) {
+                       uint64_t slots, uint64_t min_tiles, cudaStream_t stream, uint64_t* total,
+                       uint64_t tile = TILE) {
   prefix.assign(T.size() + 1, 0);
   for (size_t t = 0; t < T.size(); ++t) {
-    if (T[t].my_blocks && T[t].nB) choose_chunks(T[t], slots, min_tiles); else T[t].nchunk = 0;
+    if (T[t].my_blocks && T[t].nB) choose_chunks(T[t], slots, min_tiles, tile); else T[t].nchunk = 0;
     prefix[t + 1] = prefix[t] + T[t].my_blocks * T[t].nchunk;
   }
   *total = prefix.back();
