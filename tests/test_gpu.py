@@ -563,3 +563,16 @@ def test_compute_sanitizer_clean(tool):
                          capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
     assert "sanitize workload ok" in out.stdout
+
+
+@pytest.mark.slow
+def test_parity_4m_x_4m_vs_oracle(oracle_lib):
+    """Beyond the BASELINE sizes: 4.2M x 4.2M triangles (1.76e13 pairs) in prefilter and
+    cull mode against the C oracle's exact sweep."""
+    A, _ = manifold_like(2048, 1025, 1)
+    B, _ = manifold_like(2048, 1025, 2)
+    ref = oracle_lib.search(A, B, sweep=True)
+    Am, Bm = D.DeviceMesh(A, 0), D.DeviceMesh(B, 0)
+    for mode in (_lib.MODE_PREFILTER, _lib.MODE_CULL):
+        r = D.search_device(Am, Bm, mode=mode)
+        assert_same_hits(ref, r.hits, r.stats)

@@ -17,12 +17,15 @@ def shapes():
         yield name, A, B
     A, _ = manifold_like(512, 257, 3)
     yield "dense-self-512x257", A, A
+    A, _ = manifold_like(2048, 1025, 1)  # 4.2M x 4.2M triangles, 1.76e13 pairs (beyond configs)
+    B, _ = manifold_like(2048, 1025, 2)
+    yield "4Mx4M", A, B
 
 
 for name, A, B in shapes():
     Am, Bm = D.DeviceMesh(A, 0), D.DeviceMesh(B, 0)
     hits = None
-    for mode in ("brute", "prefilter", "cull"):
+    for mode in (("prefilter", "cull") if name == "4Mx4M" else ("brute", "prefilter", "cull")):
         m = _lib.MODE_NAMES[mode]
         D.search_device(Am, Bm, mode=m)
         runs = [D.search_device(Am, Bm, mode=m, timing=True) for _ in range(5)]
