@@ -17,11 +17,15 @@ python tools/mode_table.py > "$out/r01_modes.jsonl"
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file "$out/launches.csv" \
     python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-c5 > /dev/null
 python tools/ncu_summary.py list "$out/launches.csv" > "$out/r01_launches_bench_c3.txt"
-for m in prefilter brute cull; do
-  ncu --set full --import-source on --clock-control none -k regex:"search_|cull_|fbox|pack|levels" -c 4 \
-      -o "$out/ncu_$m" python tools/profile_run.py --config C3 --mode $m --iters 1 > /dev/null
-  python tools/ncu_summary.py rep "$out/ncu_$m.ncu-rep" > "$out/r01_ncu_${m}_c3.txt"
-done
+ncu_rep() {  # name, kernel regex, launch count, mode
+  ncu --set full --import-source on --clock-control none -k regex:"$2" -c "$3" \
+      -o "$out/ncu_$1" python tools/profile_run.py --config C3 --mode "$4" --iters 1 > /dev/null
+  python tools/ncu_summary.py rep "$out/ncu_$1.ncu-rep" > "$out/r01_ncu_$1_c3.txt"
+}
+ncu_rep prefilter "search_local|fbox" 2 prefilter
+ncu_rep brute "search_brute" 1 brute
+ncu_rep cull "cull_" 2 cull
+ncu_rep pack "pack_kernel|levels_kernel" 2 cull
 make -C tools/microbench > /dev/null 2>&1 || nvcc -gencode arch=compute_100a,code=sm_100a -O3 \
     -o tools/microbench/hprefilter tools/microbench/hprefilter.cu
 tools/microbench/hprefilter > "$out/r01_microbench_pairtest.jsonl"
