@@ -185,11 +185,16 @@ def test_a_range_partition(mode):
     assert sum(p.stats["n_pairs"] for p in parts) == full.stats["n_pairs"]
 
 
-def test_natural_and_tiled_orders_agree():
-    A, _, B, _ = config_pair("C4i")
-    r1 = D.search_device(D.DeviceMesh(A, 0, order=_lib.ORDER_NATURAL), D.DeviceMesh(B, 0, order=_lib.ORDER_NATURAL))
-    r2 = D.search_device(D.DeviceMesh(A, 0), D.DeviceMesh(B, 0))
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("name", ["C4i", "C5/8"])
+def test_natural_and_tiled_orders_agree(name, mode):
+    A, _, B, _ = config_pair(name)
+    r1 = D.search_device(D.DeviceMesh(A, 0, order=_lib.ORDER_NATURAL), D.DeviceMesh(B, 0, order=_lib.ORDER_NATURAL),
+                         mode=mode)
+    r2 = D.search_device(D.DeviceMesh(A, 0), D.DeviceMesh(B, 0), mode=_lib.MODE_BRUTE)
     assert np.array_equal(r1.hits, r2.hits)
+    r3 = D.search_device(D.DeviceMesh(A, 0, order=_lib.ORDER_NATURAL), D.DeviceMesh(B, 0), mode=mode)  # mixed
+    assert np.array_equal(r3.hits, r2.hits)
 
 
 @pytest.mark.parametrize("mode", MODES)
