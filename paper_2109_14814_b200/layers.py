@@ -16,7 +16,7 @@ import numpy as np
 
 from . import _lib, device as _device, isect
 from .errors import ConfigError, FileFormatError
-from .mesh import HalfLayer, ManifoldMesh, half_layer
+from .mesh import ManifoldMesh, half_layer
 
 
 @dataclass

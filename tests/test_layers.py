@@ -1,7 +1,6 @@
 """Layer-pair plan: enumeration counts, TOF, plan file, CLI."""
 import math
 
-import numpy as np
 import pytest
 
 from paper_2109_14814_b200 import cli, errors, layers

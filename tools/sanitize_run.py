@@ -9,7 +9,7 @@ import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2109_14814_b200 import _lib, device as D  # noqa: E402
-from paper_2109_14814_b200.mesh import config_pair, manifold_like  # noqa: E402
+from paper_2109_14814_b200.mesh import manifold_like  # noqa: E402
 
 A, sa = manifold_like(48, 21, 3)
 B, sb = manifold_like(40, 19, 3)
