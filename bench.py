@@ -214,9 +214,9 @@ class ClockSampler:
 KERNEL_LAUNCHES = {"brute": 2, "cull": 3, "prefilter": 3}
 INT_LANES_PER_CLK_PER_SM = 64  # B200 fma-heavy (IMAD) and alu (LOP3) pipes, each; IMAD measured 62.7 lanes/clk/SM
                                # (tools/microbench/hprefilter.cu swar3_mix0); issue: 4 SMSP x 32 = 128 lanes/clk/SM
-# SASS of the prefilter inner loop, per 16 pair tests: 12 IMAD + 2 IMAD.X (fma-heavy pipe),
-# 2 IADD3 + 8 LOP3.LUT.PAND (alu pipe)
-PREFILTER_IMAD_PER_PAIR = 14.0 / 16.0
+# SASS of the prefilter inner loop, per 16 pair tests: 8 IMAD + 4 IMAD.X (fma-heavy pipe),
+# 4 IADD3 + 8 LOP3.LUT.PAND (alu pipe) - 24 instructions, balanced over the two pipes
+PREFILTER_IMAD_PER_PAIR = 12.0 / 16.0
 
 
 def run_ours(args):
@@ -356,20 +356,21 @@ def run_ours(args):
                         "(profiles/r01_ncu_brute_c3.txt): 2.16 GB vs 68 GB of algorithmic L2->SMEM tile "
                         "traffic; B's 67 MB of boxes are re-read from HBM ~32x per launch (L2 is split "
                         "over two dies) at ~4 GB/s - negligible against the FP64 bound"}
-    # ---- roofline of the prefilter kernel: every pair = 14/16 IMAD-class op (fma-heavy pipe,
-    # 64 lanes/clk/SM = the bound) + 2/16 IADD3 + 1/2 LOP3 (alu pipe); issue: 1.5 instructions per pair
+    # ---- roofline of the prefilter kernel: every pair = 12/16 IMAD-class op (fma-heavy pipe,
+    # 64 lanes/clk/SM) + 4/16 IADD3 + 1/2 LOP3 (alu pipe, 64 lanes/clk/SM): 1.5 instructions per
+    # pair, so the fma pipe, the alu pipe and instruction issue all bind at 85.3 pairs/clk/SM
     pst = pre["stats"]
     pf_peak = sms * INT_LANES_PER_CLK_PER_SM / PREFILTER_IMAD_PER_PAIR * f_max * 1e6
     pf_achieved = pst["n_tested"] / (pst["kernel_ms"] * 1e-3)
     pf_roofline = {
-        "bound": "fma_pipe", "kernel": "search_local_kernel (MCX_MODE_PREFILTER: quantised-box packed integer "
-                                       "test of every pair, exact FP64 test of its passes)",
+        "bound": "int_pipes+issue", "kernel": "search_local_kernel (MCX_MODE_PREFILTER: quantised-box packed "
+                                              "integer test of every pair, exact FP64 test of its passes)",
         "achieved": pf_achieved, "peak": pf_peak, "unit": "pair-tests/s", "frac": pf_achieved / pf_peak,
         "peak_source": f"{sms} SMs x {INT_LANES_PER_CLK_PER_SM} IMAD lanes/clk (fma-heavy pipe) / "
                        f"{PREFILTER_IMAD_PER_PAIR:.4f} IMAD-class ops per pair x {f_max:.0f} MHz (IMAD rate "
-                       "measured 62.7 lanes/clk/SM, tools/microbench/hprefilter.cu); the alu pipe and issue "
-                       "bind later (102 and 85 pairs/clk/SM)",
-        "work_per_launch": "n_pairs quantised pair tests (14/16 IMAD + 2/16 IADD3 + 1/2 LOP3 each) + "
+                       "measured 62.7 lanes/clk/SM, tools/microbench/hprefilter.cu); the alu pipe (12/16 per "
+                       "pair) and issue (1.5 instructions per pair, 4 SMSP x 32 lanes/clk) bind at the same rate",
+        "work_per_launch": "n_pairs quantised pair tests (12/16 IMAD + 4/16 IADD3 + 1/2 LOP3 each) + "
                            "n_exact_tests FP64 box tests",
         "exact_tests_per_step": pst["n_exact_tests"], "kernel_ms": pst["kernel_ms"],
         "kernel_ms_note": "CUDA events around the whole call: fp32 box kernel (~0.03 ms) + search",

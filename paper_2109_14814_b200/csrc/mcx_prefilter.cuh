@@ -57,12 +57,11 @@ __device__ __forceinline__ void sub2_cc(unsigned& xa, unsigned& xb, unsigned ha,
 constexpr int FTILE = 256;  // B records per stage (256 × 32 B = 8 KB)
 constexpr unsigned G4 = 0x88888888u;
 
-template <int QR_, int JB_, int UNROLL_, int MINB_ = 1, bool PAIR2_ = false, bool WFRAME_ = false, int SUBMIX_ = 0>
+template <int QR_, int JB_, int UNROLL_, int MINB_ = 1, bool PAIR2_ = false, bool WFRAME_ = false, int CHAINS_ = 0>
 struct LCfg {
-  // subtractions not forced onto the fma pipe: 0 none; 1 / 2: the second of every other /
-  // every pair left to ptxas as plain C (it still picks IMAD.IADD); 3 / 4: two / four of every
-  // 16 pairs in borrow chains, whose first subtraction must be an alu IADD3
-  static constexpr int SUBMIX = SUBMIX_;
+  // pairs of A slots (of every 8) whose two subtractions form a borrow chain, so that ptxas
+  // must put the first on the alu pipe (IADD3 with carry-out) instead of the fma pipe
+  static constexpr int CHAINS = CHAINS_;
   static constexpr bool PAIR2 = PAIR2_;    // one LOP3 for two pair tests (conservative "both fail")
   static constexpr bool WFRAME = WFRAME_;  // one frame per warp (its 32·QR A records) instead of per CTA
   static constexpr int QR = QR_;
@@ -298,14 +297,13 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_local_kernel(const
         if constexpr (C::PAIR2) {
 #pragma unroll
           for (int r = 0; r < QR; r += 2) {
-            const bool plain = (C::SUBMIX == 2) || (C::SUBMIX == 1 && (r & 3) == 2);
-            if (C::SUBMIX >= 3 && (r & (C::SUBMIX == 3 ? 7 : 3)) == (C::SUBMIX == 3 ? 6 : 2)) {
+            const int st = (r >> 1) & 7;  // chains spread evenly over the 8 slot pairs
+            if (((st + 1) * C::CHAINS) / 8 != (st * C::CHAINS) / 8) {
               unsigned xa, xb;  // borrow chain: the first subtraction must be an alu IADD3
               sub2_cc(xa, xb, hw[r], hw[r + 1], bw[u]);
               fail_and2(allfail[(r >> 1) & 3], xa, xb);
             } else {
-              fail_and2(allfail[(r >> 1) & 3], imad_sub(hw[r], m1, bw[u]),
-                        plain ? hw[r + 1] - bw[u] : imad_sub(hw[r + 1], m1, bw[u]));
+              fail_and2(allfail[(r >> 1) & 3], imad_sub(hw[r], m1, bw[u]), imad_sub(hw[r + 1], m1, bw[u]));
             }
           }
         } else {
@@ -368,19 +366,21 @@ static int launch_local_cfg(std::vector<SearchParams>& T, Batch Bt, std::vector<
 static int launch_prefilter(std::vector<SearchParams>& T, const Batch& Bt, std::vector<uint64_t>& prefix,
                             void* dev_tab, const std::vector<FboxJob>& jobs, void* dev_jobs, int device,
                             cudaStream_t stream) {
+#define MCX_LOCAL(...) launch_local_cfg<LCfg<__VA_ARGS__>>(T, Bt, prefix, dev_tab, jobs, dev_jobs, device, stream)
   switch (variant_from_env()) {
-    case 1: return launch_local_cfg<LCfg<16, 8, 1, 1, true, true>>(T, Bt, prefix, dev_tab, jobs, dev_jobs, device, stream);
-    case 2: return launch_local_cfg<LCfg<16, 32, 1, 1, true, true>>(T, Bt, prefix, dev_tab, jobs, dev_jobs, device, stream);
-    case 3: return launch_local_cfg<LCfg<32, 16, 1, 1, true, true>>(T, Bt, prefix, dev_tab, jobs, dev_jobs, device, stream);
-    case 4: return launch_local_cfg<LCfg<16, 8, 1, 1, true>>(T, Bt, prefix, dev_tab, jobs, dev_jobs, device, stream);   // CTA frame
-    case 5: return launch_local_cfg<LCfg<16, 8, 1>>(T, Bt, prefix, dev_tab, jobs, dev_jobs, device, stream);            // 1 LOP3/pair
-    case 6: return launch_local_cfg<LCfg<8, 8, 1, 1, true, true>>(T, Bt, prefix, dev_tab, jobs, dev_jobs, device, stream);
-    case 7: return launch_local_cfg<LCfg<16, 16, 1, 1, true, true, 1>>(T, Bt, prefix, dev_tab, jobs, dev_jobs, device, stream);
-    case 8: return launch_local_cfg<LCfg<16, 16, 1, 1, true, true, 2>>(T, Bt, prefix, dev_tab, jobs, dev_jobs, device, stream);
-    case 9: return launch_local_cfg<LCfg<16, 16, 1, 1, true, true>>(T, Bt, prefix, dev_tab, jobs, dev_jobs, device, stream);
-    case 10: return launch_local_cfg<LCfg<16, 16, 1, 1, true, true, 4>>(T, Bt, prefix, dev_tab, jobs, dev_jobs, device, stream);
-    default: return launch_local_cfg<LCfg<16, 16, 1, 1, true, true, 3>>(T, Bt, prefix, dev_tab, jobs, dev_jobs, device, stream);
+    case 1: return MCX_LOCAL(16, 16, 1, 8, true, true, 2);
+    case 2: return MCX_LOCAL(16, 16, 1, 8, true, true, 3);
+    case 3: return MCX_LOCAL(16, 16, 1, 8, true, true, 5);
+    case 4: return MCX_LOCAL(16, 16, 1, 8, true, true, 6);
+    case 5: return MCX_LOCAL(16, 16, 1, 1, true, true, 2);  // 6 CTAs/SM (150 registers)
+    case 6: return MCX_LOCAL(16, 8, 1, 8, true, true, 4);
+    case 7: return MCX_LOCAL(32, 16, 1, 4, true, true, 4);
+    case 8: return MCX_LOCAL(16, 8, 1, 1, true);            // one frame per CTA
+    case 9: return MCX_LOCAL(16, 8, 1);                     // one LOP3 per pair test
+    case 10: return MCX_LOCAL(8, 8, 1, 1, true, true);
+    default: return MCX_LOCAL(16, 16, 1, 8, true, true, 4);
   }
+#undef MCX_LOCAL
 }
 
 }  // namespace mcx
