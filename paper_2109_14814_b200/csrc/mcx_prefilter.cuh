@@ -361,8 +361,8 @@ static int launch_local_cfg(std::vector<SearchParams>& T, Batch Bt, std::vector<
 }
 
 // Variant selection (MCX_VARIANT, experiments; 0 = the tuned default: 16 A records per
-// thread, 2-warp CTAs, one frame per warp, one vote per 16 B records, one LOP3 per two
-// pair tests, 2 of 16 subtractions on the alu pipe — measured in DESIGN.md §5).
+// thread, 2-warp CTAs, 8 CTAs/SM, one frame per warp, one vote per 64 B records, one
+// LOP3 per two pair tests, 4 of 16 subtractions on the alu pipe — DESIGN.md §5).
 static int launch_prefilter(std::vector<SearchParams>& T, const Batch& Bt, std::vector<uint64_t>& prefix,
                             void* dev_tab, const std::vector<FboxJob>& jobs, void* dev_jobs, int device,
                             cudaStream_t stream) {
@@ -378,7 +378,9 @@ static int launch_prefilter(std::vector<SearchParams>& T, const Batch& Bt, std::
     case 8: return MCX_LOCAL(16, 8, 1, 1, true);            // one frame per CTA
     case 9: return MCX_LOCAL(16, 8, 1);                     // one LOP3 per pair test
     case 10: return MCX_LOCAL(8, 8, 1, 1, true, true);
-    default: return MCX_LOCAL(16, 16, 1, 8, true, true, 4);
+    case 11: return MCX_LOCAL(16, 32, 1, 8, true, true, 4);
+    case 12: return MCX_LOCAL(16, 16, 1, 8, true, true, 4);
+    default: return MCX_LOCAL(16, 64, 1, 8, true, true, 4);
   }
 #undef MCX_LOCAL
 }
