@@ -286,7 +286,8 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_local_kernel(const
             ((6u - qceil(h.w, fr[3], fr[7])) << 28);
       S.qt[fi][j] = w;
     }
-    __syncthreads();
+    if constexpr (C::WFRAME) __syncwarp();  // each warp reads only the words it wrote
+    else __syncthreads();
     auto step = [&](int j, auto jb_c) {
       constexpr int NJ = decltype(jb_c)::value;
       unsigned bw[NJ];
