@@ -58,7 +58,7 @@ class DeviceMesh:
 
     Records are stored in the tiled order (``_lib.ORDER_TILED``) with ``perm``
     mapping storage position → original triangle index, plus the culling
-    hierarchy (group / tile / block union boxes).  Both search modes use this
+    hierarchy (group / tile / block union boxes).  All search modes use this
     layout; hits always carry original indices.
     """
 

@@ -409,7 +409,7 @@ def test_find_intersections_device_records_equal_host():
 @pytest.mark.parametrize("kind", ["same", "tangent"])
 def test_parity_stress_large(kind, oracle_lib):
     """Near-degenerate stress pairs at 512×257 (262k triangles each): B = A (shared edges and
-    vertices everywhere) and near-tangent sheets — both modes vs the C oracle's exact sweep."""
+    vertices everywhere) and near-tangent sheets — every mode vs the C oracle's exact sweep."""
     from paper_2109_14814_b200.mesh import stress_pair
     A, B, _ = stress_pair(kind, N=512, M=257, seed=3)
     ref = oracle_lib.search(A, B, sweep=True, cap=1 << 22)
