@@ -42,6 +42,7 @@
 
 #include <algorithm>
 #include <type_traits>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/mcx.h"
@@ -495,15 +496,15 @@ struct WsLayout {
 
 // MCX_MODE_PREFILTER: the distinct meshes of a batch (by box pointer, in order of
 // first appearance), each converted to conservative fp32 boxes once per call.
-static void distinct_meshes(const mcx_task* tasks, uint32_t n, std::vector<const mcx_mesh_dev*>& out) {
+static void distinct_meshes(const mcx_task* tasks, uint32_t n, std::vector<const mcx_mesh_dev*>& out,
+                            std::unordered_map<const double*, size_t>* index = nullptr) {
+  std::unordered_map<const double*, size_t> local;
+  std::unordered_map<const double*, size_t>& idx = index ? *index : local;
   out.clear();
+  idx.clear();
   for (uint32_t t = 0; t < n; ++t)
-    for (const mcx_mesh_dev* m : {tasks[t].A, tasks[t].B}) {
-      if (!m) continue;
-      bool seen = false;
-      for (const mcx_mesh_dev* x : out) seen |= (x->box == m->box);
-      if (!seen) out.push_back(m);
-    }
+    for (const mcx_mesh_dev* m : {tasks[t].A, tasks[t].B})
+      if (m && idx.emplace(m->box, out.size()).second) out.push_back(m);
 }
 
 static WsLayout ws_layout(const mcx_task* tasks, uint32_t n, const mcx_opts* o) {
@@ -552,20 +553,17 @@ static int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mc
                      (unsigned long long)L.total);
   char* ws = (char*)o->workspace;
   std::vector<const mcx_mesh_dev*> meshes;
+  std::unordered_map<const double*, size_t> mesh_index;
   std::vector<FboxJob> jobs;
   if (o->mode == MCX_MODE_PREFILTER) {
-    distinct_meshes(tasks, n, meshes);
+    distinct_meshes(tasks, n, meshes, &mesh_index);
     uint64_t off = L.quant;
     for (const mcx_mesh_dev* m : meshes) {
       jobs.push_back(FboxJob{reinterpret_cast<const Box*>(m->box), reinterpret_cast<float4*>(ws + off), m->n_tri});
       off += 32 * m->n_tri;
     }
   }
-  auto fbox_of = [&](const mcx_mesh_dev* m) -> float4* {
-    for (size_t k = 0; k < meshes.size(); ++k)
-      if (meshes[k]->box == m->box) return jobs[k].dst;
-    return nullptr;
-  };
+  auto fbox_of = [&](const mcx_mesh_dev* m) -> float4* { return jobs[mesh_index.at(m->box)].dst; };
   std::vector<SearchParams> T(n);
   for (uint32_t t = 0; t < n; ++t) {
     const mcx_mesh_dev* A = tasks[t].A;
