@@ -342,7 +342,7 @@ static int launch_local_cfg(std::vector<SearchParams>& T, Batch Bt, std::vector<
   const size_t smem = sizeof(LSmem<C>);
   uint64_t slots = 0, total = 0;
   int rc = resident_slots(search_local_kernel<C>, C::THREADS, smem, device, &slots);
-  if (rc == MCX_OK) rc = upload_plan(T, Bt, prefix, dev_tab, slots, 4, stream, &total, FTILE);
+  if (rc == MCX_OK) rc = upload_plan(T, Bt, prefix, dev_tab, slots, 8, stream, &total, FTILE);
   if (rc != MCX_OK || total == 0) return rc;
   if (jobs.size() > 65535) return set_error(MCX_E_ARG, "MCX_MODE_PREFILTER supports at most 65535 meshes per batch");
   Bt.neg1 = 0xffffffffu;
