@@ -525,6 +525,16 @@ def run_ours(args):
                "sample": f"C port of the SPEC all-pairs search, A triangles [0, {s['a_triangles']}) x all B "
                          f"({s['pairs']:.3e} pairs, {s['seconds']:.1f} s, packing excluded)", "cpu": cpu_model(),
                "spec_literal_serial": cpu_spec_literal_sample(A, B)}
+        # the culling counterpart on the CPU: the C oracle's exact x-sweep-and-prune over the
+        # whole workload (all threads, packing included) - the CPU analogue of `cull`
+        from oracle import c_oracle
+        t0 = time.perf_counter()
+        rs = c_oracle.search(A, B, sweep=True)
+        sw = time.perf_counter() - t0
+        cpu["sweep_and_prune_full_search"] = {
+            "seconds": sw, "hits": int(len(rs["ia"])), "threads": c_oracle.max_threads(),
+            "vs_gpu_cull_step": sw / (cull["ms_per_step"] * 1e-3),
+            "note": "exact CPU culling search of the full workload (C oracle x-sweep), packing included"}
 
     if rank == 0:
         line = {"metric": METRIC, "value": m1["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
