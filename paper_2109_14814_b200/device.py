@@ -100,9 +100,18 @@ class DeviceMesh:
         _lib.check(rc, "mcx_levels")
 
     def struct(self) -> _lib.MeshDev:
-        return _lib.MeshDev(self.n_tri, self.box.data_ptr(), self.geo.data_ptr(),
-                            self.perm.data_ptr() if self.perm is not None else None,
-                            self.gbox.data_ptr(), self.tbox.data_ptr(), self.bbox.data_ptr(), self.status.data_ptr())
+        """The mcx_mesh_dev view of this mesh (built once: the buffers never move)."""
+        if getattr(self, "_struct", None) is None:
+            self._struct = _lib.MeshDev(self.n_tri, self.box.data_ptr(), self.geo.data_ptr(),
+                                        self.perm.data_ptr() if self.perm is not None else None,
+                                        self.gbox.data_ptr(), self.tbox.data_ptr(), self.bbox.data_ptr(),
+                                        self.status.data_ptr())
+            self._struct_ptr = ctypes_pointer(self._struct)
+        return self._struct
+
+    def struct_ptr(self):
+        self.struct()
+        return self._struct_ptr
 
 
 @dataclass
@@ -213,11 +222,12 @@ def search_batch(pairs, *, mode: int = _lib.MODE_BRUTE, shard=(0, 1), cap: int =
     s = stream or t.cuda.current_stream(dev)
     W = _Workspace.get(dev)
     n = len(pairs)
-    structs = [(p[0].struct(), p[1].struct()) for p in pairs]  # keep alive for the call
     tasks = (_lib.Task * n)()
-    for k, (p, (As, Bs)) in enumerate(zip(pairs, structs)):
-        rng = p[2] if len(p) > 2 else (0, 0)
-        tasks[k] = _lib.Task(ctypes_pointer(As), ctypes_pointer(Bs), int(rng[0]), int(rng[1]))
+    for k, p in enumerate(pairs):  # mesh structs are cached on the DeviceMesh (kept alive by it)
+        t_k = tasks[k]
+        t_k.A, t_k.B = p[0].struct_ptr(), p[1].struct_ptr()
+        if len(p) > 2:
+            t_k.a_begin, t_k.a_end = int(p[2][0]), int(p[2][1])
     opts = _lib.Opts(dev, s.cuda_stream, 0, 0, int(shard[0]), int(shard[1]), int(mode), int(timing), None, 0)
     need = L.mcx_batch_workspace_bytes(tasks, n, opts)
     ws = W.workspace(need)
@@ -239,12 +249,11 @@ def search_batch(pairs, *, mode: int = _lib.MODE_BRUTE, shard=(0, 1), cap: int =
         raise CapacityError("hit buffer overflow persisted after regrowing", required=total, task=task_ids)
     hits = buf[: total * 5].cpu().numpy().view(HIT_DTYPE).copy() if total else np.zeros(0, HIT_DTYPE)
     owner = tb[:total].cpu().numpy() if total else np.zeros(0, np.int32)
-    out = []
-    for k in range(n):
-        h = hits[owner == k]
-        h = h[np.lexsort((h["ib"], h["ia"]))]
-        out.append(SearchResult(hits=h, stats=stats[k].as_dict()))
-    return out
+    # one sort by (task, ia, ib), then split at the task boundaries (O(hits log hits), not O(tasks x hits))
+    order = np.lexsort((hits["ib"], hits["ia"], owner))
+    hits, owner = hits[order], owner[order]
+    cuts = np.searchsorted(owner, np.arange(n + 1))
+    return [SearchResult(hits=hits[cuts[k]:cuts[k + 1]].copy(), stats=stats[k].as_dict()) for k in range(n)]
 
 
 def ctypes_pointer(x):
