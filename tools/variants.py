@@ -29,6 +29,8 @@ for name in cfgs:
         ms = st["kernel_ms"]
         print(json.dumps({"cfg": name, "variant": v, "mode": sys.argv[3] if len(sys.argv) > 3 else "brute", "exact_tests": st["n_exact_tests"], "ms": ms,
                           "pairs_per_s": st["n_pairs"] / ms * 1e3, "tested": st["n_tested"],
-                          "lane_ops_T": (8 * st["n_tested"] + 100 * st["n_aabb_pass"]) / ms / 1e9,
-                          "frac": (8 * st["n_tested"] + 100 * st["n_aabb_pass"]) / ms / 1e9 / 18.61248,
+                          # FP64-pipe lane-ops and fraction of the 18.6 T lane-op/s peak: meaningful for
+                          # the FP64 kernels (brute, cull) only
+                          "fp64_lane_ops_T": (8 * st["n_exact_tests"] + 100 * st["n_aabb_pass"]) / ms / 1e9,
+                          "fp64_frac": (8 * st["n_exact_tests"] + 100 * st["n_aabb_pass"]) / ms / 1e9 / 18.61248,
                           "hits": int(st["n_hits"]), "pass": int(st["n_aabb_pass"])}), flush=True)
