@@ -581,3 +581,28 @@ def test_parity_4m_x_4m_vs_oracle(oracle_lib):
     for mode in (_lib.MODE_PREFILTER, _lib.MODE_CULL):
         r = D.search_device(Am, Bm, mode=mode)
         assert_same_hits(ref, r.hits, r.stats)
+
+
+def test_bench_json_contract():
+    """bench.py (our arm) on a small config: one JSON line with the keys the driver reads."""
+    import json
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--config", "C2", "--steps", "3",
+                          "--warmup", "3", "--no-cpu-baseline", "--no-paper", "--no-c5"],
+                         capture_output=True, text=True, check=True, timeout=600, cwd=root).stdout
+    lines = [ln for ln in out.strip().splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "clocks", "gpu_launches"):
+        assert k in d, k
+    assert d["steps"] == 3 and d["warmup"] == 3 and d["n_gpus"] == 1 and d["value"] > 0
+    assert d["config"]["pairs_per_step"] == 130560 * 130560 and "workload" in d["config"]
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert k in d["roofline"], k
+    assert 0 < d["roofline"]["frac"] < 1.2
+    for k in ("value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"):
+        assert k in d["e2e"], k
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["gpu_launches"] > 0
+    assert d["hits"] == d["cull"]["hits"] == 4
