@@ -8,8 +8,9 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmcx.so")
-SOURCES = ["mcx_pack.cu", "mcx_search.cu", "mcx_records.cu"]
-DEPS = SOURCES + ["mcx_common.cuh", "mcx_search.cuh", "mcx_prefilter.cuh"]
+SOURCES = ["mcx_pack.cu", "mcx_search.cu", "mcx_records.cu", "mcx_runtime.cu"]
+DEPS = SOURCES + ["mcx_common.cuh", "mcx_search.cuh", "mcx_prefilter.cuh", "mcx_records.cuh", "mcx_format.cuh",
+                  "mcx_internal.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -39,6 +39,28 @@ __host__ __device__ __forceinline__ uint64_t storage_quad(uint32_t i, uint32_t k
   return off_tile + off_sub + (kk - sk * S) * ws + (ii - si * S);
 }
 
+// Inverse of storage_quad: storage quad index sq → (i, k).  Every tile row but the
+// last holds T·N quads, every tile of a row but the last T·hq, and so on down to the
+// 4×4 sub-tiles, so each level's index is a plain division by the full-size stride.
+__host__ __device__ __forceinline__ void quad_of_storage(uint64_t sq, uint32_t N, uint32_t MQ, uint32_t& i,
+                                                         uint32_t& k) {
+  const uint32_t T = ORDER_TILE_Q, S = ORDER_SUB_Q;
+  const uint32_t tk = (uint32_t)(sq / ((uint64_t)T * N));
+  uint32_t r = (uint32_t)(sq - (uint64_t)tk * T * N);
+  const uint32_t hq = min(T, MQ - tk * T);
+  const uint32_t ti = r / (T * hq);
+  r -= ti * T * hq;
+  const uint32_t wq = min(T, N - ti * T);
+  const uint32_t sk = r / (S * wq);
+  r -= sk * S * wq;
+  const uint32_t hs = min(S, hq - sk * S);
+  const uint32_t si = r / (S * hs);
+  r -= si * S * hs;
+  const uint32_t ws = min(S, wq - si * S);
+  i = ti * T + si * S + r % ws;
+  k = tk * T + sk * S + r / ws;
+}
+
 // ------------------------------------------------------------ error state
 // Thread-local, so concurrent host threads (one per GPU) never clobber each other.
 extern thread_local char g_err[512];
@@ -50,6 +72,18 @@ inline int set_error(int code, const char* fmt, ...) {
   va_end(ap);
   return code;
 }
+
+// Saves the calling thread's current device and restores it on scope exit, so no
+// entry point leaves the caller's device switched (include/mcx.h conventions).
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = false;
+  DeviceGuard() { ok = cudaGetDevice(&prev) == cudaSuccess; }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (ok && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
 
 #define CUDA_TRY(expr)                                                                        \
   do {                                                                                        \
@@ -99,6 +133,20 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// 1-D bulk async copy shared → global (SASS: UBLKCP), tracked by a bulk group.  The
+// shared data must be made visible to the async proxy first (fence_proxy_async).
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_commit_and_wait_read() {
+  asm volatile("cp.async.bulk.commit_group;\n cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
 // Non-coherent 16-byte load that the compiler cannot CSE (used to rematerialise
 // register-resident data instead of keeping it live across a rare slow path).
 __device__ __forceinline__ void ld_nc_v2(const double* p, double& x, double& y) {
@@ -106,12 +154,88 @@ __device__ __forceinline__ void ld_nc_v2(const double* p, double& x, double& y) 
 }
 
 // ------------------------------------------------------- canonical FP64 solve
-// FMA-free, fixed association order; see oracle/canonical.py:solve_pairs.
+// FMA-free, fixed association order; see oracle/canonical.py:pack / solve_pairs.
 #define MCX_SING_RTOL 1e-12
 
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+
+// Vertices of original triangle t = 2·(i + N·k) + τ of a (4, M, N) grid, −0.0
+// canonicalised (x + 0.0): T¹ = (v00, v10, v01), T² = (v01, v10, v11), i + 1 mod N
+// (the packing origin is the first vertex).  Used
+// by pack_kernel for the boxes and by the solve, so both see identical vertices.
+__device__ __forceinline__ void tri_verts(const double* __restrict__ c, uint32_t N, uint32_t M, uint32_t t,
+                                          double v0[4], double v1[4], double v2[4]) {
+  const uint32_t q = t >> 1, tau = t & 1;
+  const uint32_t i = q % N, k = q / N;
+  const uint32_t ip = (i + 1 == N) ? 0 : i + 1;
+  const uint64_t r0 = (uint64_t)k * N, r1 = r0 + N;
+  const uint64_t plane = (uint64_t)M * N;
+#pragma unroll
+  for (int d = 0; d < 4; ++d) {
+    const double* pl = c + d * plane;
+    v0[d] = dadd(__ldg(pl + (tau ? r1 : r0) + i), 0.0);
+    v1[d] = dadd(__ldg(pl + r0 + ip), 0.0);
+    v2[d] = dadd(__ldg(pl + r1 + (tau ? ip : i)), 0.0);
+  }
+}
+
+// Vertex addressing of original triangle t for the solve.  The solve reads vertices
+// through non-CSE-able loads and re-derives an edge each time it needs one: the
+// values (and bits) are those of the packing, v + 0.0 then v1 − v0, while the live
+// register set stays small enough for the hot loops around it.
+struct TriRef {
+  const double* c;
+  uint32_t plane, o[3];  // plane stride; offsets of v0, v1, v2 within a plane (N·M < 2^32)
+};
+
+__device__ __forceinline__ TriRef tri_ref(const double* c, uint32_t N, uint32_t M, uint32_t t) {
+  const uint32_t q = t >> 1, tau = t & 1;
+  const uint32_t i = q % N, k = q / N;
+  const uint32_t ip = (i + 1 == N) ? 0 : i + 1;
+  const uint32_t r0 = k * N, r1 = r0 + N;
+  TriRef T;
+  T.c = c;
+  T.plane = M * N;
+  T.o[0] = (tau ? r1 : r0) + i;
+  T.o[1] = r0 + ip;
+  T.o[2] = r1 + (tau ? ip : i);
+  return T;
+}
+
+__device__ __forceinline__ double ld_vol(const double* p) {
+  double x;
+  asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(x) : "l"(p));
+  return x;
+}
+
+__device__ __forceinline__ double vert(const TriRef& T, int v, int d) {
+  return dadd(ld_vol(T.c + ((uint64_t)d * T.plane + T.o[v])), 0.0);
+}
+
+// e = v_which − v0 (which = 1: e1, 2: e2), the packing's edge.
+__device__ __forceinline__ void edge(const TriRef& T, int which, double e[4]) {
+#pragma unroll
+  for (int d = 0; d < 4; ++d) e[d] = dsub(vert(T, which, d), vert(T, 0, d));
+}
+
+// P = e1∧e2 (order 01, 02, 03, 12, 13, 23) and nrm = ‖e1‖·‖e2‖, left-to-right sums.
+__device__ __forceinline__ void biv_norm(const TriRef& T, double P[6], double& nrm) {
+  double e1[4], e2[4];
+  edge(T, 1, e1);
+  edge(T, 2, e2);
+  const int bi[6] = {0, 0, 0, 1, 1, 2}, bj[6] = {1, 2, 3, 2, 3, 3};
+#pragma unroll
+  for (int p = 0; p < 6; ++p) P[p] = dsub(dmul(e1[bi[p]], e2[bj[p]]), dmul(e1[bj[p]], e2[bi[p]]));
+  double n1 = dmul(e1[0], e1[0]), n2 = dmul(e2[0], e2[0]);
+#pragma unroll
+  for (int d = 1; d < 4; ++d) {
+    n1 = dadd(n1, dmul(e1[d], e1[d]));
+    n2 = dadd(n2, dmul(e2[d], e2[d]));
+  }
+  nrm = dmul(__dsqrt_rn(n1), __dsqrt_rn(n2));
+}
 
 // g_j = Σ_i r_i K_ij for the antisymmetric K of bivector B (order 01,02,03,12,13,23)
 __device__ __forceinline__ void contract(const double r[4], const double B[6], double c[4]) {
@@ -129,46 +253,37 @@ __device__ __forceinline__ double dot4(const double c[4], const double x[4]) {
   return d;
 }
 
-__device__ __forceinline__ void ld4(const double* __restrict__ g, double o[4]) {
-  const double2 a = __ldg(reinterpret_cast<const double2*>(g));
-  const double2 b = __ldg(reinterpret_cast<const double2*>(g) + 1);
-  o[0] = a.x; o[1] = a.y; o[2] = b.x; o[3] = b.y;
-}
-
-// Returns 0 = miss, 1 = hit (sol = s, t, a, b), 2 = singular (gate).
-// Geometry is loaded in stages so the live set stays small (the op sequence is
-// fixed by the data dependences, not by the load order).
-__device__ __forceinline__ int solve_pair(const double* __restrict__ gA, const double* __restrict__ gB,
-                                          double sol[4]) {
-  double r[4], p[4], q[4];
-  ld4(gA, p);
-  ld4(gB, q);
+// The precise test of original triangles ta of grid A and tb of
+// grid B.  Returns 0 = miss, 1 = hit (sol = s, t, a, b), 2 = singular (gate,
+// SPEC.md:464).  Only AABB survivors get here (1e-7..1e-3 of the pairs), so the
+// triangle geometry is rebuilt from the grids (L1/L2) instead of being stored.
+__device__ __forceinline__ int solve_tri(const double* __restrict__ cA, uint32_t NA, uint32_t MA, uint32_t ta,
+                                         const double* __restrict__ cB, uint32_t NB, uint32_t MB, uint32_t tb,
+                                         double sol[4]) {
+  const TriRef A = tri_ref(cA, NA, MA, ta), B = tri_ref(cB, NB, MB, tb);
+  double Pa[6], Qb[6], nA, nB;
+  biv_norm(A, Pa, nA);
+  biv_norm(B, Qb, nB);
+  double r[4];
 #pragma unroll
-  for (int c = 0; c < 4; ++c) r[c] = dsub(q[c], p[c]);
-  double Pa[6], Qb[6];
-#pragma unroll
-  for (int k = 0; k < 6; ++k) {
-    Pa[k] = __ldg(gA + 12 + k);
-    Qb[k] = __ldg(gB + 12 + k);
-  }
+  for (int c = 0; c < 4; ++c) r[c] = dsub(vert(B, 0, c), vert(A, 0, c));
   double D = dsub(dmul(Pa[0], Qb[5]), dmul(Pa[1], Qb[4]));
   D = dadd(D, dmul(Pa[2], Qb[3]));
   D = dadd(D, dmul(Pa[3], Qb[2]));
   D = dsub(D, dmul(Pa[4], Qb[1]));
   D = dadd(D, dmul(Pa[5], Qb[0]));
-  const double thr = dmul(dmul(__ldg(gA + 18), __ldg(gB + 18)), MCX_SING_RTOL);
+  const double thr = dmul(dmul(nA, nB), MCX_SING_RTOL);
   if (fabs(D) <= thr) return 2;
-  double g[4], h[4];
+  double g[4], h[4], x[4];
   contract(r, Qb, g);
   contract(r, Pa, h);
-  double x[4];
-  ld4(gA + 8, x);   // e2
+  edge(A, 2, x);
   const double s = __ddiv_rn(dot4(g, x), D);
-  ld4(gA + 4, x);   // e1
+  edge(A, 1, x);
   const double t = __ddiv_rn(-dot4(g, x), D);
-  ld4(gB + 8, x);   // f2
+  edge(B, 2, x);
   const double a = __ddiv_rn(-dot4(h, x), D);
-  ld4(gB + 4, x);   // f1
+  edge(B, 1, x);
   const double b = __ddiv_rn(dot4(h, x), D);
   if (s >= 0.0 && t >= 0.0 && a >= 0.0 && b >= 0.0 && dadd(s, t) <= 1.0 && dadd(a, b) <= 1.0) {
     sol[0] = s;

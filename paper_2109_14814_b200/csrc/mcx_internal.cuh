@@ -1,0 +1,19 @@
+// mcx_internal.cuh — entry points shared between the translation units of libmcx.so
+// (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/mcx.h"
+
+namespace mcx {
+
+// mcx_pack.cu: the fused pack + levels kernel, enqueued on `stream` (device current).
+int pack_enqueue(const double* coords, uint32_t N, uint32_t M, int order, double* box, uint32_t* perm, double* gbox,
+                 double* tbox, double* bbox, uint32_t* status, cudaStream_t stream);
+
+// mcx_search.cu: a batch of searches (device current); synchronises o->stream.
+int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mcx_hit* hits, uint32_t* hit_task,
+                 uint64_t cap, mcx_stats* st);
+
+}  // namespace mcx

@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_local_kernel(const
 
   uint2* q = S.queue[warp];
   int qn = 0;
-  unsigned long long n_pass = 0, n_sing = 0, n_exact = 0;
+  unsigned long long n_exact = 0;
   const unsigned lt_mask = (1u << lane) - 1u;
 
   // Rare path for B record ib (word bw): the lane's quantised passes as a bit mask over
@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_local_kernel(const
         __syncwarp();
         if (qn >= 32) {
           qn -= 32;
-          flush_queue<KIND_TRI>(P, Bt, q + qn, 32, lane, n_pass, n_sing);
+          flush_queue(P, Bt, q + qn, 32, lane);
         }
       }
     }
@@ -331,13 +331,13 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_local_kernel(const
     }
   }
   __syncwarp();
-  if (qn > 0) flush_queue<KIND_TRI>(P, Bt, q, qn, lane, n_pass, n_sing);
-  flush_counters(P, lane, n_pass, n_sing, n_exact);
+  if (qn > 0) flush_queue(P, Bt, q, qn, lane);
+  flush_tested(P, lane, n_exact);
 }
 
 // MCX_MODE_PREFILTER: conservative fp32 boxes → prefilter search.
 template <class C>
-static int launch_local_cfg(std::vector<SearchParams>& T, Batch Bt, std::vector<uint64_t>& prefix, void* dev_tab,
+static int launch_local_cfg(std::vector<SearchParams>& T, Batch& Bt, std::vector<uint64_t>& prefix, void* dev_tab,
                             const std::vector<FboxJob>& jobs, void* dev_jobs, int device, cudaStream_t stream) {
   const size_t smem = sizeof(LSmem<C>);
   uint64_t slots = 0, total = 0;
@@ -364,7 +364,7 @@ static int launch_local_cfg(std::vector<SearchParams>& T, Batch Bt, std::vector<
 // Variant selection (MCX_VARIANT, experiments; 0 = the tuned default: 16 A records per
 // thread, 2-warp CTAs, 8 CTAs/SM, one frame per warp, one vote per 64 B records, one
 // LOP3 per two pair tests, 4 of 16 subtractions on the alu pipe — DESIGN.md §5).
-static int launch_prefilter(std::vector<SearchParams>& T, const Batch& Bt, std::vector<uint64_t>& prefix,
+static int launch_prefilter(std::vector<SearchParams>& T, Batch& Bt, std::vector<uint64_t>& prefix,
                             void* dev_tab, const std::vector<FboxJob>& jobs, void* dev_jobs, int device,
                             cudaStream_t stream) {
 #define MCX_LOCAL(...) launch_local_cfg<LCfg<__VA_ARGS__>>(T, Bt, prefix, dev_tab, jobs, dev_jobs, device, stream)

@@ -1,0 +1,665 @@
+// mcx_runtime.cu — the host-to-host runtime of libmcx.so: the reference's
+// find_intersections and layer-pair task loop as one
+// call per job, everything after the H2D copy on the device.
+//
+//   mcx_mesh_load      H2D of a half-layer grid + s-values, fused pack (mcx_pack.cu)
+//   mcx_intersect      1. batched search of all jobs (mcx_search.cu: box tests →
+//                         candidate compaction → precise test), hits stay in HBM
+//                      2. record keys: gid, τ_A, τ_B per hit
+//                      3. sort by (job, gid, τ_A, τ_B)  (CUB radix sort: stable,
+//                         LSD — (gid, τ) first, then job)
+//                      4. record fields in that order (mcx_records.cuh: point,
+//                         Eqs. 28-29 estimates), 128-byte mcx_record each
+//                      5. 1e-9 dedup: close pairs from an x-sorted
+//                         window scan, then the greedy rule resolved in rounds
+//                      6. compaction of the kept records and the "%.17g" records
+//                         text (mcx_format.cuh), both in record order
+//                      7. D2H of the records and the text into pinned host memory
+//   mcx_find_intersections   load A (stream 0) and B (stream 1, overlapping A's
+//                      packing), mcx_intersect, release.
+//
+// Dedup contract (identical to isect._dedup_mask on the host): in record order, a
+// record is dropped iff some KEPT earlier record of the same job has a point within
+// 1e-9 in every coordinate (|fl(p − q)| ≤ 1e-9).  The greedy rule is resolved in
+// rounds: a record with a kept close predecessor is dropped; a record whose close
+// predecessors are all dropped is kept; the smallest undecided record is decided in
+// every round, so the rounds terminate and give the sequential answer.
+//
+// Device memory comes from a per-context CUDA memory pool (stream-ordered
+// cudaMallocFromPoolAsync, release threshold "never"), so repeated calls reuse it.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+#include <vector>
+
+#include "../../include/mcx.h"
+#include "mcx_common.cuh"
+#include "mcx_format.cuh"
+#include "mcx_internal.cuh"
+#include "mcx_records.cuh"
+
+#define MCX_DEDUP_TOL 1e-9
+
+namespace mcx {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+struct HostBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+// Per-job parameters of the records stage (device table).
+struct JobDev {
+  const double* cA;
+  const double* sA;
+  const double* sB;
+  uint32_t NA, MA, NB, MB;
+  int32_t n1, sign1, n2, sign2;
+};
+
+}  // namespace mcx
+
+struct mcx_context {
+  int device = 0;
+  cudaStream_t s0 = nullptr, s1 = nullptr;
+  cudaEvent_t ev = nullptr;
+  cudaMemPool_t pool = nullptr;
+  mcx::DevBuf ws, hits, hit_task, jobs, k0, k1, v0, v1, recs, recs_out, state, blocked, pairs, lens, offs, cub,
+      text, small;
+  mcx::HostBuf h_recs, h_text, h_small;
+  uint64_t cand_cap = MCX_DEFAULT_CAND_CAP, hit_cap = 1 << 16, pair_cap = 1 << 12;
+};
+
+struct mcx_mesh {
+  mcx_context* ctx = nullptr;
+  double *coords = nullptr, *s_values = nullptr, *box = nullptr, *gbox = nullptr, *tbox = nullptr, *bbox = nullptr;
+  uint32_t *perm = nullptr, *status = nullptr;
+  mcx_mesh_dev view{};
+};
+
+namespace mcx {
+
+static int ensure(mcx_context* c, DevBuf& b, size_t bytes, cudaStream_t s) {
+  if (b.bytes >= bytes && b.p) return MCX_OK;
+  if (b.p) CUDA_TRY(cudaFreeAsync(b.p, s));
+  b.p = nullptr;
+  b.bytes = 0;
+  const size_t nb = std::max<size_t>(bytes + bytes / 2, 256);
+  CUDA_TRY(cudaMallocFromPoolAsync(&b.p, nb, c->pool, s));
+  b.bytes = nb;
+  return MCX_OK;
+}
+
+static int ensure_host(HostBuf& b, size_t bytes) {
+  if (b.bytes >= bytes && b.p) return MCX_OK;
+  if (b.p) CUDA_TRY(cudaFreeHost(b.p));
+  b.p = nullptr;
+  b.bytes = 0;
+  const size_t nb = std::max<size_t>(bytes + bytes / 2, 4096);
+  CUDA_TRY(cudaMallocHost(&b.p, nb));
+  b.bytes = nb;
+  return MCX_OK;
+}
+
+static void release(mcx_context* c, DevBuf& b, cudaStream_t s) {
+  if (b.p) cudaFreeAsync(b.p, s);
+  b.p = nullptr;
+  b.bytes = 0;
+}
+
+static int bits_for(uint64_t v) {  // bits to represent every value in [0, v]
+  int b = 0;
+  while (b < 64 && (v >> b)) ++b;
+  return b;
+}
+
+// ------------------------------------------------------------------ kernels
+// 2. sort key of hit k: gid << 2 | τ_A << 1 | τ_B (job sorted in a second, stable pass)
+__global__ void key_kernel(const mcx_hit* __restrict__ hits, const uint32_t* __restrict__ hit_task, uint64_t n,
+                           const JobDev* __restrict__ jobs, uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x) {
+    const mcx_hit H = hits[k];
+    const JobDev& J = jobs[hit_task ? hit_task[k] : 0];
+    const uint32_t qa = H.ia >> 1, qb = H.ib >> 1;
+    const uint64_t i = qa % J.NA, k1 = qa / J.NA, j = qb % J.NB, l1 = qb / J.NB;
+    const uint64_t n12 = (uint64_t)J.NA * J.NB;
+    const uint64_t gid = i + (uint64_t)J.NA * j + n12 * k1 + n12 * (uint64_t)(J.MA - 1) * l1;
+    keys[k] = gid << 2 | (uint64_t)(H.ia & 1) << 1 | (H.ib & 1);
+    vals[k] = (uint32_t)k;
+  }
+}
+
+// job of the hit at each sorted position (second sort pass key)
+__global__ void task_key_kernel(const uint32_t* __restrict__ order, const uint32_t* __restrict__ hit_task, uint64_t n,
+                                uint64_t* __restrict__ keys) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n; r += (uint64_t)gridDim.x * blockDim.x)
+    keys[r] = hit_task[order[r]];
+}
+
+// 4. record r = fields of hit order[r]; xkey for the dedup sweep (order-preserving bits of x)
+__global__ void record_kernel(const mcx_hit* __restrict__ hits, const uint32_t* __restrict__ hit_task,
+                              const uint32_t* __restrict__ order, uint64_t n, const JobDev* __restrict__ jobs,
+                              mcx_record* __restrict__ recs, uint64_t* __restrict__ xkeys, uint32_t* __restrict__ xvals) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n; r += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = order[r];
+    const mcx_hit H = hits[k];
+    const uint32_t task = hit_task ? hit_task[k] : 0;
+    const JobDev& J = jobs[task];
+    mcx_record R;
+    record_fields(H, J.cA, J.NA, J.MA, J.sA, J.NB, J.MB, J.sB, R.gid, R.point, R.params);
+    R.ia = H.ia;
+    R.ib = H.ib;
+    R.bary[0] = H.s; R.bary[1] = H.t; R.bary[2] = H.a; R.bary[3] = H.b;
+    R.task = task;
+    R.pad[0] = R.pad[1] = R.pad[2] = 0;
+    recs[r] = R;
+    if (xkeys) {
+      uint64_t u = __double_as_longlong(R.point[0]);
+      xkeys[r] = (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+      xvals[r] = (uint32_t)r;
+    }
+  }
+}
+
+__global__ void xtask_key_kernel(const uint32_t* __restrict__ xorder, const mcx_record* __restrict__ recs, uint64_t n,
+                                 uint64_t* __restrict__ keys) {
+  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n; p += (uint64_t)gridDim.x * blockDim.x)
+    keys[p] = recs[xorder[p]].task;
+}
+
+// 5a. close pairs: from each position of the (job, x)-sorted order, scan forward while
+// the job matches and fl(x' − x) ≤ tol (monotone in the scan); test the other 3 coords.
+__global__ void close_pairs_kernel(const uint32_t* __restrict__ xorder, const mcx_record* __restrict__ recs,
+                                   uint64_t n, uint2* __restrict__ pairs, uint64_t cap,
+                                   unsigned long long* __restrict__ count, uint8_t* __restrict__ state) {
+  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n; p += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t r = xorder[p];
+    const mcx_record& R = recs[r];
+    for (uint64_t q = p + 1; q < n; ++q) {
+      const uint32_t r2 = xorder[q];
+      const mcx_record& S = recs[r2];
+      if (S.task != R.task) break;
+      if (!(fabs(dsub(S.point[0], R.point[0])) <= MCX_DEDUP_TOL)) break;
+      if (fabs(dsub(S.point[1], R.point[1])) <= MCX_DEDUP_TOL && fabs(dsub(S.point[2], R.point[2])) <= MCX_DEDUP_TOL &&
+          fabs(dsub(S.point[3], R.point[3])) <= MCX_DEDUP_TOL) {
+        const uint32_t e = min(r, r2), l = max(r, r2);
+        const unsigned long long pos = atomicAdd(count, 1ull);
+        if (pos < cap) pairs[pos] = make_uint2(e, l);
+        state[l] = 0;  // has a close predecessor: undecided
+      }
+    }
+  }
+}
+
+// 5b. greedy resolution in rounds (one CTA; close pairs are few).  state: 1 kept,
+// 2 dropped, 0 undecided.
+__global__ void __launch_bounds__(1024) resolve_kernel(const uint2* __restrict__ pairs, uint64_t np,
+                                                       uint8_t* __restrict__ state, uint8_t* __restrict__ blocked) {
+  for (int round = 0;; ++round) {
+    for (uint64_t k = threadIdx.x; k < np; k += blockDim.x) {  // a kept predecessor drops it
+      const uint2 e = pairs[k];
+      if (state[e.y] == 0 && state[e.x] == 1) state[e.y] = 2;
+    }
+    __syncthreads();
+    for (uint64_t k = threadIdx.x; k < np; k += blockDim.x) {  // an undecided predecessor blocks it
+      const uint2 e = pairs[k];
+      if (state[e.y] == 0 && state[e.x] != 2) blocked[e.y] = 1;
+    }
+    __syncthreads();
+    bool left = false;
+    for (uint64_t k = threadIdx.x; k < np; k += blockDim.x) {  // all predecessors dropped: keep
+      const uint2 e = pairs[k];
+      if (state[e.y] == 0 && !blocked[e.y]) state[e.y] = 1;
+    }
+    __syncthreads();
+    for (uint64_t k = threadIdx.x; k < np; k += blockDim.x) {
+      const uint2 e = pairs[k];
+      blocked[e.y] = 0;
+      left |= state[e.y] == 0;
+    }
+    if (!__syncthreads_or(left)) break;
+  }
+}
+
+// 6. text lengths of the kept records (0 for dropped ones), then the text itself
+__global__ void line_len_kernel(const mcx_record* __restrict__ recs, const uint8_t* __restrict__ state, uint64_t n,
+                                const JobDev* __restrict__ jobs, uint32_t* __restrict__ lens,
+                                uint8_t* __restrict__ flags) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n; r += (uint64_t)gridDim.x * blockDim.x) {
+    const bool keep = !state || state[r] == 1;
+    flags[r] = keep;
+    if (!lens) continue;
+    const mcx_record& R = recs[r];
+    const JobDev& J = jobs[R.task];
+    lens[r] = keep ? (uint32_t)fmt::fmt_record_line(nullptr, J.n1, J.sign1, J.n2, J.sign2, R.gid, R.point, R.bary,
+                                                    R.params)
+                   : 0u;
+  }
+}
+
+__global__ void line_write_kernel(const mcx_record* __restrict__ recs, const uint8_t* __restrict__ flags, uint64_t n,
+                                  const JobDev* __restrict__ jobs, const uint64_t* __restrict__ incl,
+                                  const uint32_t* __restrict__ lens, char* __restrict__ text) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n; r += (uint64_t)gridDim.x * blockDim.x) {
+    if (!flags[r]) continue;
+    const mcx_record& R = recs[r];
+    const JobDev& J = jobs[R.task];
+    fmt::fmt_record_line(text + (incl[r] - lens[r]), J.n1, J.sign1, J.n2, J.sign2, R.gid, R.point, R.bary, R.params);
+  }
+}
+
+static unsigned grid_of(uint64_t n) {
+  uint64_t b = (n + 255) / 256;
+  return (unsigned)std::min<uint64_t>(std::max<uint64_t>(b, 1), 148ull * 16);
+}
+
+// Steps 2-7 for n hits already in c->hits (hit_task: c->hit_task or null for one job).
+static int postprocess(mcx_context* c, uint64_t n, const uint32_t* hit_task, const std::vector<JobDev>& jobs,
+                       const mcx_find_opts* fo, const mcx_record** records, uint64_t* n_records, const char** text,
+                       uint64_t* text_bytes) {
+  cudaStream_t s = c->s0;
+  *records = nullptr;
+  *n_records = 0;
+  if (text) *text = nullptr;
+  if (text_bytes) *text_bytes = 0;
+  if (n == 0) return MCX_OK;
+  if (n > 0xffffffffull) return set_error(MCX_E_ARG, "more than 2^32 hits in one call");
+  int rc = ensure(c, c->jobs, sizeof(JobDev) * jobs.size(), s);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(c->jobs.p, jobs.data(), sizeof(JobDev) * jobs.size(), cudaMemcpyHostToDevice, s));
+  const JobDev* J = (const JobDev*)c->jobs.p;
+  const mcx_hit* H = (const mcx_hit*)c->hits.p;
+  if ((rc = ensure(c, c->k0, 8 * n, s)) || (rc = ensure(c, c->k1, 8 * n, s)) || (rc = ensure(c, c->v0, 4 * n, s)) ||
+      (rc = ensure(c, c->v1, 4 * n, s)) || (rc = ensure(c, c->recs, sizeof(mcx_record) * n, s)) ||
+      (rc = ensure(c, c->recs_out, sizeof(mcx_record) * n, s)) || (rc = ensure(c, c->state, n, s)) ||
+      (rc = ensure(c, c->blocked, n, s)) || (rc = ensure(c, c->lens, 4 * n, s)) ||
+      (rc = ensure(c, c->offs, 8 * n, s)) || (rc = ensure(c, c->small, 64, s)))
+    return rc;
+  uint64_t max_gid = 0;
+  for (const JobDev& j : jobs) max_gid = std::max<uint64_t>(max_gid, (uint64_t)j.NA * (j.MA - 1) * j.NB * (j.MB - 1));
+  const int key_bits = bits_for(max_gid) + 2;
+  if (key_bits > 64) return set_error(MCX_E_ARG, "gid range too large for a 64-bit sort key");
+  const int task_bits = std::max(1, bits_for(jobs.size() - 1));
+  const int ni = (int)n;
+  // 2-3: sort hits by (gid, τ_A, τ_B), then stably by job
+  key_kernel<<<grid_of(n), 256, 0, s>>>(H, hit_task, n, J, (uint64_t*)c->k0.p, (uint32_t*)c->v0.p);
+  CUDA_TRY(cudaGetLastError());
+  cub::DoubleBuffer<uint64_t> keys((uint64_t*)c->k0.p, (uint64_t*)c->k1.p);
+  cub::DoubleBuffer<uint32_t> vals((uint32_t*)c->v0.p, (uint32_t*)c->v1.p);
+  auto sort_pairs = [&](int bits) -> int {
+    size_t tmp = 0;
+    CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, vals, ni, 0, bits, s));
+    int r = ensure(c, c->cub, tmp, s);
+    if (r) return r;
+    tmp = c->cub.bytes;
+    CUDA_TRY(cub::DeviceRadixSort::SortPairs(c->cub.p, tmp, keys, vals, ni, 0, bits, s));
+    return MCX_OK;
+  };
+  if ((rc = sort_pairs(key_bits))) return rc;
+  if (hit_task && jobs.size() > 1) {
+    task_key_kernel<<<grid_of(n), 256, 0, s>>>(vals.Current(), hit_task, n, keys.Current());
+    CUDA_TRY(cudaGetLastError());
+    if ((rc = sort_pairs(task_bits))) return rc;
+  }
+  // 4: records in sorted order (+ x keys for the dedup sweep)
+  mcx_record* R = (mcx_record*)c->recs.p;
+  const uint32_t* order = vals.Current();
+  const bool dedup = fo->dedup && n > 1;
+  uint64_t* xk = (keys.Current() == (uint64_t*)c->k0.p) ? (uint64_t*)c->k1.p : (uint64_t*)c->k0.p;
+  uint32_t* xv = (order == (const uint32_t*)c->v0.p) ? (uint32_t*)c->v1.p : (uint32_t*)c->v0.p;
+  record_kernel<<<grid_of(n), 256, 0, s>>>(H, hit_task, order, n, J, R, dedup ? xk : nullptr, xv);
+  CUDA_TRY(cudaGetLastError());
+  uint8_t* state = (uint8_t*)c->state.p;
+  unsigned long long* pair_count = (unsigned long long*)c->small.p;
+  if (dedup) {
+    // 5: (job, x) order of the records, close pairs, greedy resolution
+    cub::DoubleBuffer<uint64_t> xkeys(xk, xk == (uint64_t*)c->k0.p ? (uint64_t*)c->k1.p : (uint64_t*)c->k0.p);
+    cub::DoubleBuffer<uint32_t> xvals(xv, xv == (uint32_t*)c->v0.p ? (uint32_t*)c->v1.p : (uint32_t*)c->v0.p);
+    keys = xkeys;
+    vals = xvals;
+    if ((rc = sort_pairs(64))) return rc;
+    if (jobs.size() > 1) {
+      xtask_key_kernel<<<grid_of(n), 256, 0, s>>>(vals.Current(), R, n, keys.Current());
+      CUDA_TRY(cudaGetLastError());
+      if ((rc = sort_pairs(task_bits))) return rc;
+    }
+    for (int attempt = 0; attempt < 3; ++attempt) {
+      if ((rc = ensure(c, c->pairs, 8 * c->pair_cap, s))) return rc;
+      CUDA_TRY(cudaMemsetAsync(state, 1, n, s));
+      CUDA_TRY(cudaMemsetAsync(c->blocked.p, 0, n, s));
+      CUDA_TRY(cudaMemsetAsync(pair_count, 0, 8, s));
+      close_pairs_kernel<<<grid_of(n), 256, 0, s>>>(vals.Current(), R, n, (uint2*)c->pairs.p, c->pair_cap, pair_count,
+                                                     state);
+      CUDA_TRY(cudaGetLastError());
+      unsigned long long np = 0;
+      CUDA_TRY(cudaMemcpyAsync(&np, pair_count, 8, cudaMemcpyDeviceToHost, s));
+      CUDA_TRY(cudaStreamSynchronize(s));
+      if (np > c->pair_cap) {
+        c->pair_cap = np + 1024;
+        continue;
+      }
+      if (np) resolve_kernel<<<1, 1024, 0, s>>>((const uint2*)c->pairs.p, np, state, (uint8_t*)c->blocked.p);
+      CUDA_TRY(cudaGetLastError());
+      break;
+    }
+  }
+  // 6: flags (+ text lengths), inclusive scan of the lengths, compaction, text
+  uint8_t* flags = (uint8_t*)c->blocked.p;  // reused: resolution is done
+  const bool want_text = fo->text && text && text_bytes;
+  line_len_kernel<<<grid_of(n), 256, 0, s>>>(R, dedup ? state : nullptr, n, J, want_text ? (uint32_t*)c->lens.p : nullptr,
+                                             flags);
+  CUDA_TRY(cudaGetLastError());
+  unsigned long long* n_sel = pair_count + 1;
+  {
+    size_t tmp = 0;
+    CUDA_TRY(cub::DeviceSelect::Flagged(nullptr, tmp, R, flags, (mcx_record*)c->recs_out.p, n_sel, ni, s));
+    if ((rc = ensure(c, c->cub, tmp, s))) return rc;
+    tmp = c->cub.bytes;
+    CUDA_TRY(cub::DeviceSelect::Flagged(c->cub.p, tmp, R, flags, (mcx_record*)c->recs_out.p, n_sel, ni, s));
+  }
+  uint64_t* incl = (uint64_t*)c->offs.p;
+  if (want_text) {
+    size_t tmp = 0;
+    const uint32_t* lens = (const uint32_t*)c->lens.p;
+    CUDA_TRY(cub::DeviceScan::InclusiveSum(nullptr, tmp, lens, incl, ni, s));
+    if ((rc = ensure(c, c->cub, tmp, s))) return rc;
+    tmp = c->cub.bytes;
+    CUDA_TRY(cub::DeviceScan::InclusiveSum(c->cub.p, tmp, lens, incl, ni, s));
+  }
+  ensure_host(c->h_small, 64);
+  uint64_t* hs = (uint64_t*)c->h_small.p;
+  CUDA_TRY(cudaMemcpyAsync(hs, n_sel, 8, cudaMemcpyDeviceToHost, s));
+  if (want_text) CUDA_TRY(cudaMemcpyAsync(hs + 1, incl + n - 1, 8, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  const uint64_t kept = hs[0], tbytes = want_text ? hs[1] : 0;
+  if (want_text) {
+    if ((rc = ensure(c, c->text, tbytes + 1, s))) return rc;
+    line_write_kernel<<<grid_of(n), 256, 0, s>>>(R, flags, n, J, incl, (const uint32_t*)c->lens.p, (char*)c->text.p);
+    CUDA_TRY(cudaGetLastError());
+  }
+  // 7: D2H into pinned context memory
+  if ((rc = ensure_host(c->h_recs, sizeof(mcx_record) * kept))) return rc;
+  CUDA_TRY(cudaMemcpyAsync(c->h_recs.p, c->recs_out.p, sizeof(mcx_record) * kept, cudaMemcpyDeviceToHost, s));
+  if (want_text) {
+    if ((rc = ensure_host(c->h_text, tbytes + 1))) return rc;
+    CUDA_TRY(cudaMemcpyAsync(c->h_text.p, c->text.p, tbytes, cudaMemcpyDeviceToHost, s));
+  }
+  CUDA_TRY(cudaStreamSynchronize(s));
+  *records = (const mcx_record*)c->h_recs.p;
+  *n_records = kept;
+  if (want_text) {
+    ((char*)c->h_text.p)[tbytes] = 0;
+    *text = (const char*)c->h_text.p;
+    *text_bytes = tbytes;
+  }
+  return MCX_OK;
+}
+
+static JobDev job_of(const mcx_mesh* A, const mcx_mesh* B, mcx_layer L) {
+  JobDev j;
+  j.cA = A->coords;
+  j.sA = A->s_values;
+  j.sB = B->s_values;
+  j.NA = A->view.N;
+  j.MA = A->view.M;
+  j.NB = B->view.N;
+  j.MB = B->view.M;
+  j.n1 = L.n1;
+  j.sign1 = L.sign1;
+  j.n2 = L.n2;
+  j.sign2 = L.sign2;
+  return j;
+}
+
+static int check_find_opts(const mcx_find_opts* fo) {
+  if (!fo) return set_error(MCX_E_ARG, "null find options");
+  if (fo->mode != MCX_MODE_BRUTE && fo->mode != MCX_MODE_CULL && fo->mode != MCX_MODE_PREFILTER)
+    return set_error(MCX_E_ARG, "unknown mode %d", fo->mode);
+  if (fo->pipeline != MCX_PIPE_TRIANGLE && fo->pipeline != MCX_PIPE_SPEC)
+    return set_error(MCX_E_ARG, "unknown pipeline %d", fo->pipeline);
+  return MCX_OK;
+}
+
+// Steps 1-7 for jobs whose meshes are resident (device current, all work on c->s0).
+static int intersect(mcx_context* c, const mcx_job* jobs, uint32_t n_jobs, const mcx_find_opts* fo,
+                     const mcx_record** records, uint64_t* n_records, const char** text, uint64_t* text_bytes,
+                     mcx_stats* stats) {
+  int rc = check_find_opts(fo);
+  if (rc) return rc;
+  if (!jobs || n_jobs == 0 || !records || !n_records || !stats) return set_error(MCX_E_ARG, "null argument");
+  std::vector<mcx_task> tasks(n_jobs);
+  std::vector<JobDev> jd(n_jobs);
+  for (uint32_t t = 0; t < n_jobs; ++t) {
+    if (!jobs[t].A || !jobs[t].B) return set_error(MCX_E_ARG, "job %u: null mesh", t);
+    if (jobs[t].A->ctx != c || jobs[t].B->ctx != c) return set_error(MCX_E_ARG, "job %u: mesh of another context", t);
+    tasks[t] = mcx_task{&jobs[t].A->view, &jobs[t].B->view, 0, 0};
+    jd[t] = job_of(jobs[t].A, jobs[t].B, jobs[t].layer);
+  }
+  mcx_opts o{};
+  o.device = c->device;
+  o.stream = c->s0;
+  o.shard_index = fo->shard_index;
+  o.shard_count = fo->shard_count;
+  o.mode = fo->mode;
+  o.pipeline = fo->pipeline;
+  uint64_t total = 0;
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    o.cand_cap = c->cand_cap;
+    const uint64_t wsb = mcx_batch_workspace_bytes(tasks.data(), n_jobs, &o);
+    if ((rc = ensure(c, c->ws, wsb, c->s0)) || (rc = ensure(c, c->hits, sizeof(mcx_hit) * c->hit_cap, c->s0)) ||
+        (rc = ensure(c, c->hit_task, 4 * c->hit_cap, c->s0)))
+      return rc;
+    o.workspace = c->ws.p;
+    o.workspace_bytes = c->ws.bytes;
+    rc = launch_batch(tasks.data(), n_jobs, &o, (mcx_hit*)c->hits.p, (uint32_t*)c->hit_task.p, c->hit_cap, stats);
+    total = 0;
+    uint64_t cands = 0;
+    for (uint32_t t = 0; t < n_jobs; ++t) {
+      total += stats[t].n_hits;
+      cands += stats[t].n_aabb_pass;
+    }
+    if (rc == MCX_E_CAPACITY) {
+      if (cands > c->cand_cap) c->cand_cap = cands + 1024;
+      if (total > c->hit_cap) c->hit_cap = total + 1024;
+      continue;
+    }
+    if (rc) return rc;
+    break;
+  }
+  if (rc) return rc;
+  return postprocess(c, total, n_jobs > 1 ? (const uint32_t*)c->hit_task.p : nullptr, jd, fo, records, n_records,
+                     text, text_bytes);
+}
+
+static int load_mesh(mcx_context* c, const double* coords, uint32_t N, uint32_t M, const double* s_values,
+                     cudaStream_t s, mcx_mesh** out) {
+  if (!coords || !s_values || !out) return set_error(MCX_E_ARG, "null argument");
+  if (N < 1 || M < 2) return set_error(MCX_E_ARG, "a half-layer needs N >= 1 and M >= 2 (SPEC.md:473)");
+  const uint64_t n = 2ull * N * (M - 1);
+  if (n >= (1ull << 31)) return set_error(MCX_E_ARG, "triangle count must be < 2^31");
+  mcx_mesh* m = new mcx_mesh();
+  m->ctx = c;
+  auto alloc = [&](void** p, size_t bytes) -> int {
+    CUDA_TRY(cudaMallocFromPoolAsync(p, std::max<size_t>(bytes, 16), c->pool, s));
+    return MCX_OK;
+  };
+  int rc = MCX_OK;
+  if ((rc = alloc((void**)&m->coords, 32ull * N * M)) || (rc = alloc((void**)&m->s_values, 8ull * M)) ||
+      (rc = alloc((void**)&m->box, 64 * n)) || (rc = alloc((void**)&m->perm, 4 * n)) ||
+      (rc = alloc((void**)&m->gbox, 64 * ((n + GROUP - 1) / GROUP))) ||
+      (rc = alloc((void**)&m->tbox, 64 * ((n + TILE - 1) / TILE))) ||
+      (rc = alloc((void**)&m->bbox, 64 * ((n + A_BLOCK - 1) / A_BLOCK))) || (rc = alloc((void**)&m->status, 16))) {
+    mcx_mesh_free(m);
+    return rc;
+  }
+  cudaError_t e = cudaMemcpyAsync(m->coords, coords, 32ull * N * M, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(m->s_values, s_values, 8ull * M, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) {
+    mcx_mesh_free(m);
+    return set_error(MCX_E_CUDA, "mesh upload: %s", cudaGetErrorString(e));
+  }
+  rc = pack_enqueue(m->coords, N, M, MCX_ORDER_TILED, m->box, m->perm, m->gbox, m->tbox, m->bbox, m->status, s);
+  if (rc) {
+    mcx_mesh_free(m);
+    return rc;
+  }
+  m->view = mcx_mesh_dev{n, m->coords, N, M, m->box, m->perm, m->gbox, m->tbox, m->bbox, m->status};
+  *out = m;
+  return MCX_OK;
+}
+
+}  // namespace mcx
+
+extern "C" {
+
+int mcx_context_create(int device, mcx_context** out) {
+  using namespace mcx;
+  if (!out) return set_error(MCX_E_ARG, "null argument");
+  *out = nullptr;
+  DeviceGuard guard;
+  CUDA_TRY(cudaSetDevice(device));
+  mcx_context* c = new mcx_context();
+  c->device = device;
+  cudaMemPoolProps props{};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = device;
+  cudaError_t e = cudaMemPoolCreate(&c->pool, &props);
+  if (e == cudaSuccess) {
+    uint64_t keep = ~0ull;  // never hand memory back between calls
+    e = cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->s0, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->s1, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev, cudaEventDisableTiming);
+  if (e != cudaSuccess) {
+    mcx_context_destroy(c);
+    return set_error(MCX_E_CUDA, "context creation: %s", cudaGetErrorString(e));
+  }
+  *out = c;
+  return MCX_OK;
+}
+
+int mcx_context_destroy(mcx_context* c) {
+  using namespace mcx;
+  if (!c) return MCX_OK;
+  DeviceGuard guard;
+  cudaSetDevice(c->device);
+  if (c->s0) {
+    for (DevBuf* b : {&c->ws, &c->hits, &c->hit_task, &c->jobs, &c->k0, &c->k1, &c->v0, &c->v1, &c->recs, &c->recs_out,
+                      &c->state, &c->blocked, &c->pairs, &c->lens, &c->offs, &c->cub, &c->text, &c->small})
+      release(c, *b, c->s0);
+    cudaStreamSynchronize(c->s0);
+  }
+  for (HostBuf* b : {&c->h_recs, &c->h_text, &c->h_small})
+    if (b->p) cudaFreeHost(b->p);
+  if (c->ev) cudaEventDestroy(c->ev);
+  if (c->s0) cudaStreamDestroy(c->s0);
+  if (c->s1) cudaStreamDestroy(c->s1);
+  if (c->pool) cudaMemPoolDestroy(c->pool);
+  delete c;
+  return MCX_OK;
+}
+
+int mcx_mesh_load(mcx_context* c, const double* coords, uint32_t N, uint32_t M, const double* s_values,
+                  mcx_mesh** mesh) {
+  using namespace mcx;
+  if (!c) return set_error(MCX_E_ARG, "null context");
+  DeviceGuard guard;
+  CUDA_TRY(cudaSetDevice(c->device));
+  int rc = load_mesh(c, coords, N, M, s_values, c->s0, mesh);
+  if (rc == MCX_OK) CUDA_TRY(cudaStreamSynchronize(c->s0));
+  return rc;
+}
+
+int mcx_mesh_free(mcx_mesh* m) {
+  using namespace mcx;
+  if (!m) return MCX_OK;
+  mcx_context* c = m->ctx;
+  DeviceGuard guard;
+  cudaSetDevice(c->device);
+  for (void* p : {(void*)m->coords, (void*)m->s_values, (void*)m->box, (void*)m->perm, (void*)m->gbox, (void*)m->tbox,
+                  (void*)m->bbox, (void*)m->status})
+    if (p) cudaFreeAsync(p, c->s0);
+  delete m;
+  return MCX_OK;
+}
+
+const mcx_mesh_dev* mcx_mesh_view(const mcx_mesh* m) { return m ? &m->view : nullptr; }
+
+int mcx_intersect(mcx_context* c, const mcx_job* jobs, uint32_t n_jobs, const mcx_find_opts* fo,
+                  const mcx_record** records, uint64_t* n_records, const char** text, uint64_t* text_bytes,
+                  mcx_stats* stats) {
+  using namespace mcx;
+  if (!c) return set_error(MCX_E_ARG, "null context");
+  DeviceGuard guard;
+  CUDA_TRY(cudaSetDevice(c->device));
+  return intersect(c, jobs, n_jobs, fo, records, n_records, text, text_bytes, stats);
+}
+
+int mcx_find_intersections(mcx_context* c, const double* coords_a, uint32_t NA, uint32_t MA, const double* s_a,
+                           const double* coords_b, uint32_t NB, uint32_t MB, const double* s_b, mcx_layer layer,
+                           const mcx_find_opts* fo, const mcx_record** records, uint64_t* n_records,
+                           const char** text, uint64_t* text_bytes, mcx_stats* stats) {
+  using namespace mcx;
+  if (!c) return set_error(MCX_E_ARG, "null context");
+  int rc = check_find_opts(fo);
+  if (rc) return rc;
+  DeviceGuard guard;
+  CUDA_TRY(cudaSetDevice(c->device));
+  mcx_mesh *A = nullptr, *B = nullptr;
+  // A on stream 0; B's copy on stream 1 overlaps A's packing; stream 0 waits for B.
+  rc = load_mesh(c, coords_a, NA, MA, s_a, c->s0, &A);
+  if (rc == MCX_OK) rc = load_mesh(c, coords_b, NB, MB, s_b, c->s1, &B);
+  if (rc == MCX_OK) {
+    cudaError_t e = cudaEventRecord(c->ev, c->s1);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c->s0, c->ev, 0);
+    if (e != cudaSuccess) rc = set_error(MCX_E_CUDA, "stream join: %s", cudaGetErrorString(e));
+  }
+  if (rc == MCX_OK) {
+    mcx_job j{A, B, layer};
+    rc = intersect(c, &j, 1, fo, records, n_records, text, text_bytes, stats);
+  }
+  mcx_mesh_free(A);  // stream-ordered on s0, after everything above
+  mcx_mesh_free(B);
+  return rc;
+}
+
+int mcx_finish_hits(mcx_context* c, const mcx_hit* hits, uint64_t n_hits, const mcx_mesh* A, const mcx_mesh* B,
+                    mcx_layer layer, const mcx_find_opts* fo, const mcx_record** records, uint64_t* n_records,
+                    const char** text, uint64_t* text_bytes) {
+  using namespace mcx;
+  if (!c || !A || !B || !records || !n_records || (n_hits && !hits)) return set_error(MCX_E_ARG, "null argument");
+  if (A->ctx != c || B->ctx != c) return set_error(MCX_E_ARG, "mesh of another context");
+  int rc = check_find_opts(fo);
+  if (rc) return rc;
+  DeviceGuard guard;
+  CUDA_TRY(cudaSetDevice(c->device));
+  if ((rc = ensure(c, c->hits, sizeof(mcx_hit) * std::max<uint64_t>(n_hits, 1), c->s0))) return rc;
+  if (n_hits) CUDA_TRY(cudaMemcpyAsync(c->hits.p, hits, sizeof(mcx_hit) * n_hits, cudaMemcpyHostToDevice, c->s0));
+  // validate the indices on the device before any record reads the grids
+  const uint64_t nA = A->view.n_tri, nB = B->view.n_tri;
+  for (uint64_t k = 0; k < n_hits; ++k)
+    if (hits[k].ia >= nA || hits[k].ib >= nB)
+      return set_error(MCX_E_ARG, "hit %llu: triangle index outside the meshes", (unsigned long long)k);
+  std::vector<JobDev> jd(1, job_of(A, B, layer));
+  return postprocess(c, n_hits, nullptr, jd, fo, records, n_records, text, text_bytes);
+}
+
+int mcx_format_g17(double v, char* out) {
+  if (!out) return mcx::set_error(MCX_E_ARG, "null buffer");
+  const int n = mcx::fmt::fmt_g17(v, out);
+  out[n] = 0;
+  return n;
+}
+
+}  // extern "C"

@@ -16,8 +16,8 @@
 //     SPEC.md:442-450 (touching boxes are not rejected).
 //   * Rare survivors are pushed by warp ballot into a per-warp shared-memory
 //     queue; when 32 are queued the warp solves them lane-parallel with the
-//     canonical FMA-free FP64 bivector-Cramer sequence, reading
-//     the two triangles' geometry from L2.  Hits are compacted with one atomic
+//     canonical FMA-free FP64 bivector-Cramer sequence, rebuilding
+//     the two triangles' geometry from the grids (L1/L2) with the packing's ops.  Hits are compacted with one atomic
 //     per warp into the global (iA, iB, s, t, a, b) list (no flag buffer).
 //
 // MCX_MODE_PREFILTER — mcx_prefilter.cuh: every pair tested by a conservative packed-
@@ -31,6 +31,10 @@
 //   test only inside overlapping groups.  A union box is disjoint from another box
 //   only if all its members are, so the AABB-pass set, singular count and hit set
 //   are identical to MCX_MODE_BRUTE; only n_tested shrinks.
+//
+// MCX_PIPE_SPEC — the SPEC's literal pipeline on the culling
+//   kernels: quads are record pairs, quad-box survivors go through the SPEC-literal
+//   Moller test and its candidates through the 4 triangle-pair precise tests.
 //
 // The solve uses only __dadd_rn/__dsub_rn/__dmul_rn/__ddiv_rn (never contracted
 // into DFMA) and the file is compiled with --fmad=false, so the op sequence is
@@ -49,6 +53,7 @@
 #include "mcx_common.cuh"
 #include "mcx_search.cuh"
 #include "mcx_prefilter.cuh"
+#include "mcx_internal.cuh"
 
 namespace mcx {
 
@@ -94,10 +99,9 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_brute_kernel(const
     }
   }
 
-  // ---- A triangles into registers (out-of-range slots get empty boxes).  Reloaded
-  // (volatile, so never CSE'd) after every survivor flush: that makes the A boxes
-  // dead across the solve, so the rare slow path can use their registers and the
-  // hot loop keeps <= 128 registers (2 CTAs/SM) without spilling.
+  // ---- A triangles into registers (out-of-range slots get empty boxes).  A survivor
+  // flush only appends to the candidate list (the precise test is solve_kernel's),
+  // so the boxes stay live across it and the hot loop fits 2 CTAs/SM.
   double alo[R][4], ahi[R][4];
   uint32_t aidx[R];
 #pragma unroll
@@ -120,7 +124,6 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_brute_kernel(const
 
   uint2* q = S.queue[warp];
   int qn = 0;
-  unsigned long long n_pass = 0, n_sing = 0;
   const unsigned lt_mask = (1u << lane) - 1u;
 
   for (int t = 0; t < ntiles; ++t) {
@@ -160,9 +163,8 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_brute_kernel(const
         if (qn >= 32) {
           do {
             qn -= 32;
-            flush_queue<KIND>(P, Bt, q + qn, 32, lane, n_pass, n_sing);
+            flush_queue(P, Bt, q + qn, 32, lane);
           } while (qn >= 32);
-          load_a();
         }
       }
     };
@@ -195,9 +197,8 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_brute_kernel(const
           if (qn >= 32) {
             do {
               qn -= 32;
-              flush_queue<KIND>(P, Bt, q + qn, 32, lane, n_pass, n_sing);
+              flush_queue(P, Bt, q + qn, 32, lane);
             } while (qn >= 32);
-            load_a();
           }
         }
       }
@@ -216,8 +217,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_brute_kernel(const
     }
   }
   __syncwarp();
-  if (qn > 0) flush_queue<KIND>(P, Bt, q, qn, lane, n_pass, n_sing);
-  flush_counters(P, lane, n_pass, n_sing, 0);
+  if (qn > 0) flush_queue(P, Bt, q, qn, lane);
 }
 
 // OR of every task's input-mesh status flags (non-finite coordinates) into *flag.
@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(CULL_THREADS) cull_pairs_kernel(const Batch Bt
   __shared__ CullSmem S;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
-  unsigned long long n_pass = 0, n_sing = 0, n_tested = 0;
+  unsigned long long n_tested = 0;
   uint2* q = S.queue[warp];
   int qn = 0;
   uint32_t cur_task = 0xffffffffu;
@@ -294,10 +294,10 @@ __global__ void __launch_bounds__(CULL_THREADS) cull_pairs_kernel(const Batch Bt
       // task switch: drain this warp's queue and counters against the old task first
       if (cur_task != 0xffffffffu) {
         __syncwarp();
-        if (qn > 0) flush_queue<KIND>(S.P, Bt, q, qn, lane, n_pass, n_sing);
+        if (qn > 0) flush_queue(S.P, Bt, q, qn, lane);
         qn = 0;
-        flush_counters(S.P, lane, n_pass, n_sing, n_tested);
-        n_pass = n_sing = n_tested = 0;
+        flush_tested(S.P, lane, n_tested);
+        n_tested = 0;
       }
       __syncthreads();
       if (tid == 0) S.P = Bt.tasks[txy.x];
@@ -347,13 +347,13 @@ __global__ void __launch_bounds__(CULL_THREADS) cull_pairs_kernel(const Batch Bt
             __syncwarp();
             if (qn >= 32) {
               qn -= 32;
-              flush_queue<KIND>(P, Bt, q + qn, 32, lane, n_pass, n_sing);
+              flush_queue(P, Bt, q + qn, 32, lane);
             }
           }
         }
       } else {
         const uint64_t ra = ga0 + 2 * (uint64_t)(lane & 15);  // T¹ record of this lane's A quad
-        const bool va = ra + 1 < P.nA;
+        const bool va = ra >= P.a_begin && ra + 2 <= P.a_end;
         double alo[4], ahi[4];
         empty_box(alo, ahi);
         if (va) {
@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(CULL_THREADS) cull_pairs_kernel(const Batch Bt
             __syncwarp();
             if (qn >= 32) {
               qn -= 32;
-              flush_queue<KIND>(P, Bt, q + qn, 32, lane, n_pass, n_sing);
+              flush_queue(P, Bt, q + qn, 32, lane);
             }
           }
         }
@@ -402,14 +402,14 @@ __global__ void __launch_bounds__(CULL_THREADS) cull_pairs_kernel(const Batch Bt
   }
   if (cur_task != 0xffffffffu) {
     __syncwarp();
-    if (qn > 0) flush_queue<KIND>(S.P, Bt, q, qn, lane, n_pass, n_sing);
-    flush_counters(S.P, lane, n_pass, n_sing, n_tested);
+    if (qn > 0) flush_queue(S.P, Bt, q, qn, lane);
+    flush_tested(S.P, lane, n_tested);
   }
 }
 
 // --------------------------------------------------------------- host side
 template <int KIND, class C>
-static int launch_brute_cfg(std::vector<SearchParams>& T, Batch Bt, std::vector<uint64_t>& prefix, void* dev_tab,
+static int launch_brute_cfg(std::vector<SearchParams>& T, Batch& Bt, std::vector<uint64_t>& prefix, void* dev_tab,
                             int device, cudaStream_t stream) {
   const size_t smem = sizeof(SearchSmem<C>);
   uint64_t slots = 0, total = 0;
@@ -422,7 +422,7 @@ static int launch_brute_cfg(std::vector<SearchParams>& T, Batch Bt, std::vector<
 }
 
 template <int KIND>
-static int launch_brute(std::vector<SearchParams>& T, const Batch& Bt, std::vector<uint64_t>& prefix, void* dev_tab,
+static int launch_brute(std::vector<SearchParams>& T, Batch& Bt, std::vector<uint64_t>& prefix, void* dev_tab,
                         int device, cudaStream_t stream) {
   switch (variant_from_env()) {
     case 1: return launch_brute_cfg<KIND, Cfg<4, 2, 1, 2, 0>>(T, Bt, prefix, dev_tab, device, stream);
@@ -433,7 +433,7 @@ static int launch_brute(std::vector<SearchParams>& T, const Batch& Bt, std::vect
 }
 
 template <int KIND>
-static int launch_cull(std::vector<SearchParams>& T, Batch Bt, std::vector<uint64_t>& prefix, void* dev_tab,
+static int launch_cull(std::vector<SearchParams>& T, Batch& Bt, std::vector<uint64_t>& prefix, void* dev_tab,
                        int device, cudaStream_t stream) {
   prefix.assign(T.size() + 1, 0);
   for (size_t t = 0; t < T.size(); ++t) prefix[t + 1] = prefix[t] + T[t].my_blocks * (T[t].nB ? T[t].ntilesB : 0);
@@ -452,6 +452,16 @@ static int launch_cull(std::vector<SearchParams>& T, Batch Bt, std::vector<uint6
   cull_blocks_kernel<<<(unsigned)g1, 256, 0, stream>>>(Bt);
   CUDA_TRY(cudaGetLastError());
   cull_pairs_kernel<KIND><<<(unsigned)(dev_sms * 8), CULL_THREADS, 0, stream>>>(Bt);
+  CUDA_TRY(cudaGetLastError());
+  return MCX_OK;
+}
+
+// Stage 3 over the candidate list the sweep kernels compacted (count read on the device).
+template <int KIND>
+static int launch_solve(const Batch& Bt, int device, cudaStream_t stream) {
+  int dev_sms = 148;
+  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device);
+  solve_kernel<KIND><<<(unsigned)(dev_sms * 4), 256, 0, stream>>>(Bt);
   CUDA_TRY(cudaGetLastError());
   return MCX_OK;
 }
@@ -490,7 +500,7 @@ static ShardGeom shard_geom(uint64_t a_begin, uint64_t a_end, uint32_t sidx, uin
 static uint64_t align16(uint64_t v) { return (v + 15) & ~15ull; }
 
 struct WsLayout {
-  uint64_t counters, table, list, total, list_cap;
+  uint64_t counters, table, list, total, list_cap, cand, cand_cap;
   uint64_t jobs, quant;  // MCX_MODE_PREFILTER: fp32-box job table, then the boxes of each distinct mesh
 };
 
@@ -513,7 +523,7 @@ static WsLayout ws_layout(const mcx_task* tasks, uint32_t n, const mcx_opts* o) 
   L.table = align16(64 + 64ull * n);
   L.list = align16(L.table + sizeof(SearchParams) * n + 8ull * (n + 1));
   L.list_cap = 0;
-  if (o && o->mode == MCX_MODE_CULL) {
+  if (o && (o->mode == MCX_MODE_CULL || o->pipeline == MCX_PIPE_SPEC)) {
     const uint32_t scount = o->shard_count ? o->shard_count : 1;
     for (uint32_t t = 0; t < n; ++t) {
       const mcx_mesh_dev* A = tasks[t].A;
@@ -524,7 +534,9 @@ static WsLayout ws_layout(const mcx_task* tasks, uint32_t n, const mcx_opts* o) 
       L.list_cap += g.my_blocks * ((B->n_tri + TILE - 1) / TILE);
     }
   }
-  L.jobs = align16(L.list + 16 * L.list_cap);
+  L.cand = align16(L.list + 16 * L.list_cap);
+  L.cand_cap = (o && o->cand_cap) ? o->cand_cap : MCX_DEFAULT_CAND_CAP;
+  L.jobs = align16(L.cand + 16 * L.cand_cap);
   L.quant = L.jobs;
   L.total = L.jobs;
   if (o && o->mode == MCX_MODE_PREFILTER) {
@@ -537,7 +549,7 @@ static WsLayout ws_layout(const mcx_task* tasks, uint32_t n, const mcx_opts* o) 
   return L;
 }
 
-static int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mcx_hit* hits, uint32_t* hit_task,
+int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mcx_hit* hits, uint32_t* hit_task,
                         uint64_t cap, mcx_stats* st) {
   if (!tasks || n == 0 || !o || !st) return set_error(MCX_E_ARG, "null argument or empty batch");
   cudaStream_t stream = (cudaStream_t)o->stream;
@@ -546,6 +558,15 @@ static int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mc
   if (sidx >= scount) return set_error(MCX_E_ARG, "shard_index %u >= shard_count %u", sidx, scount);
   if (o->mode != MCX_MODE_BRUTE && o->mode != MCX_MODE_CULL && o->mode != MCX_MODE_PREFILTER)
     return set_error(MCX_E_ARG, "unknown mode %d", o->mode);
+  if (o->pipeline != MCX_PIPE_TRIANGLE && o->pipeline != MCX_PIPE_SPEC)
+    return set_error(MCX_E_ARG, "unknown pipeline %d", o->pipeline);
+  if (o->pipeline == MCX_PIPE_SPEC && o->mode != MCX_MODE_CULL)
+    return set_error(MCX_E_ARG, "MCX_PIPE_SPEC runs on the culling kernels only (mode MCX_MODE_CULL)");
+  const bool spec = o->pipeline == MCX_PIPE_SPEC;
+  if (spec)
+    for (uint32_t t = 0; t < n; ++t)
+      if ((tasks[t].a_begin | tasks[t].a_end) & 1)
+        return set_error(MCX_E_ARG, "task %u: MCX_PIPE_SPEC needs an A range of whole quads (even bounds)", t);
   if (cap > 0 && !hits) return set_error(MCX_E_ARG, "null hit buffer with nonzero capacity");
   const WsLayout L = ws_layout(tasks, n, o);
   if (!o->workspace || o->workspace_bytes < L.total || ((uintptr_t)o->workspace & 15))
@@ -576,20 +597,23 @@ static int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mc
                        (unsigned long long)a_end, (unsigned long long)A->n_tri);
     if (A->n_tri >= (1ull << 31) || B->n_tri >= (1ull << 31))
       return set_error(MCX_E_ARG, "task %u: triangle counts must be < 2^31", t);
-    if (!A->box || !B->box || !A->geo || !B->geo) return set_error(MCX_E_ARG, "task %u: null box/geo", t);
-    if (((uintptr_t)A->box | (uintptr_t)B->box | (uintptr_t)A->geo | (uintptr_t)B->geo) & 15)
-      return set_error(MCX_E_ARG, "task %u: box/geo pointers must be 16-byte aligned", t);
+    if (!A->box || !B->box || !A->coords || !B->coords) return set_error(MCX_E_ARG, "task %u: null box/coords", t);
+    if (((uintptr_t)A->box | (uintptr_t)B->box) & 15)
+      return set_error(MCX_E_ARG, "task %u: box pointers must be 16-byte aligned", t);
+    if (A->M < 2 || B->M < 2 || A->n_tri != 2ull * A->N * (A->M - 1) || B->n_tri != 2ull * B->N * (B->M - 1))
+      return set_error(MCX_E_ARG, "task %u: n_tri does not match the N x M grid", t);
     if (o->mode == MCX_MODE_CULL && (!A->gbox || !A->bbox || !B->gbox || !B->tbox))
-      return set_error(MCX_E_ARG, "task %u: MCX_MODE_CULL needs level boxes (mcx_levels) on both meshes", t);
+      return set_error(MCX_E_ARG, "task %u: MCX_MODE_CULL needs level boxes (mcx_pack) on both meshes", t);
     const ShardGeom g = shard_geom(a_begin, a_end, sidx, scount);
     SearchParams& P = T[t];
     P = SearchParams{};
     P.boxA = reinterpret_cast<const Box*>(A->box);
-    P.geoA = A->geo;
     P.permA = A->perm;
     P.boxB = reinterpret_cast<const Box*>(B->box);
-    P.geoB = B->geo;
     P.permB = B->perm;
+    P.coordsA = A->coords;
+    P.coordsB = B->coords;
+    P.NA = A->N; P.MA = A->M; P.NB = B->N; P.MB = B->M;
     P.nA = A->n_tri;
     P.a_begin = a_begin;
     P.a_end = a_end;
@@ -611,7 +635,7 @@ static int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mc
       P.fB = fbox_of(B);
     }
     st[t] = mcx_stats{};
-    st[t].n_pairs = g.na * B->n_tri;
+    st[t].n_pairs = spec ? (g.na / 2) * (B->n_tri / 2) : g.na * B->n_tri;
   }
   CUDA_TRY(cudaMemsetAsync(ws, 0, L.counters + 64ull * n, stream));
   Batch Bt = {};
@@ -623,6 +647,9 @@ static int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mc
   Bt.list_count = reinterpret_cast<unsigned long long*>(ws) + 1;
   Bt.blk_list = reinterpret_cast<uint4*>(ws + L.list);
   Bt.blk_cap = L.list_cap;
+  Bt.cand = reinterpret_cast<uint4*>(ws + L.cand);
+  Bt.cand_cap = L.cand_cap;
+  Bt.cand_count = reinterpret_cast<unsigned long long*>(ws) + 3;
   Timing tm;
   if (o->timing) {
     CUDA_TRY(cudaEventCreate(&tm.e0));
@@ -630,11 +657,16 @@ static int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mc
     CUDA_TRY(cudaEventRecord(tm.e0, stream));
   }
   std::vector<uint64_t> prefix;
-  const int rc = o->mode == MCX_MODE_BRUTE ? launch_brute<KIND_TRI>(T, Bt, prefix, ws + L.table, o->device, stream)
+  int rc = spec ? launch_cull<KIND_SPEC>(T, Bt, prefix, ws + L.table, o->device, stream)
+                 : o->mode == MCX_MODE_BRUTE ? launch_brute<KIND_TRI>(T, Bt, prefix, ws + L.table, o->device, stream)
                  : o->mode == MCX_MODE_CULL ? launch_cull<KIND_TRI>(T, Bt, prefix, ws + L.table, o->device, stream)
                                             : launch_prefilter(T, Bt, prefix, ws + L.table, jobs, ws + L.jobs,
                                                                o->device, stream);
   if (rc != MCX_OK) return rc;
+  if (Bt.tasks) {  // no work units → no table, no candidates
+    rc = spec ? launch_solve<KIND_SPEC>(Bt, o->device, stream) : launch_solve<KIND_TRI>(Bt, o->device, stream);
+    if (rc != MCX_OK) return rc;
+  }
   if (o->timing) CUDA_TRY(cudaEventRecord(tm.e1, stream));
   status_kernel<<<1, 32, 0, stream>>>(reinterpret_cast<const SearchParams*>(ws + L.table), n,
                                       reinterpret_cast<unsigned long long*>(ws) + 2);
@@ -651,9 +683,13 @@ static int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mc
     st[t].n_singular = c[2];
     st[t].n_tested = o->mode == MCX_MODE_CULL ? c[3] : st[t].n_pairs;
     st[t].n_exact_tests = o->mode == MCX_MODE_BRUTE ? st[t].n_pairs : c[3];
+    st[t].n_candidates = spec ? c[4] : c[1];
     st[t].kernel_ms = ms;
   }
   if (h[2]) return set_error(MCX_E_ARG, "non-finite (NaN/Inf) coordinates in an input mesh (mcx_pack status)");
+  if (h[3] > L.cand_cap)
+    return set_error(MCX_E_CAPACITY, "candidate capacity %llu < %llu box-test survivors (opts->cand_cap)",
+                     (unsigned long long)L.cand_cap, h[3]);
   if (h[0] > cap)
     return set_error(MCX_E_CAPACITY, "hit capacity %llu < %llu hits", (unsigned long long)cap, h[0]);
   return MCX_OK;
@@ -684,13 +720,14 @@ static_assert(256 + sizeof(SearchParams) + 16 <= PC_HEADER, "pair_candidates hea
 
 static int launch_pair_candidates(const double* cA, uint32_t NA, uint32_t MA, const double* cB, uint32_t NB,
                                   uint32_t MB, int device, cudaStream_t stream, void* ws, uint64_t ws_bytes,
-                                  uint64_t* gids, uint64_t cap, uint64_t* n_out) {
+                                  uint64_t* gids, uint64_t cap, mcx_stats* st) {
   if (NA < 1 || NB < 1 || MA < 2 || MB < 2) return set_error(MCX_E_ARG, "half-layers need >= 2 columns");
   const uint64_t nqA = (uint64_t)NA * (MA - 1), nqB = (uint64_t)NB * (MB - 1);
   if (nqA >= (1ull << 31) || nqB >= (1ull << 31)) return set_error(MCX_E_ARG, "quad counts must be < 2^31");
   const uint64_t need = PC_HEADER + (nqA + nqB) * sizeof(Box);
-  if (!ws || ws_bytes < need || ((uintptr_t)ws & 15))
-    return set_error(MCX_E_ARG, "workspace too small or misaligned (need %llu bytes)", (unsigned long long)need);
+  if (!ws || ws_bytes < need + 16 || ((uintptr_t)ws & 15))
+    return set_error(MCX_E_ARG, "workspace too small or misaligned (need %llu bytes + 16 per candidate)",
+                     (unsigned long long)need);
   if (cap > 0 && !gids) return set_error(MCX_E_ARG, "null gid buffer with nonzero capacity");
   unsigned long long* counters = (unsigned long long*)ws;
   Box* boxA = reinterpret_cast<Box*>((char*)ws + PC_HEADER);
@@ -719,26 +756,40 @@ static int launch_pair_candidates(const double* cA, uint32_t NA, uint32_t MA, co
   Bt.gids = gids;
   Bt.cap = cap;
   Bt.emit = counters;
+  Bt.cand_count = counters + 3;
+  Bt.cand = reinterpret_cast<uint4*>((char*)ws + need);
+  Bt.cand_cap = (ws_bytes - need) / 16;
   std::vector<SearchParams> T(1, P);
   std::vector<uint64_t> prefix;
   int rc = launch_brute<KIND_QUAD>(T, Bt, prefix, (char*)ws + 256, device, stream);
+  if (rc == MCX_OK && Bt.tasks) rc = launch_solve<KIND_QUAD>(Bt, device, stream);
   if (rc != MCX_OK) return rc;
-  unsigned long long h[8];
+  unsigned long long h[16];
   CUDA_TRY(cudaMemcpyAsync(h, counters, sizeof(h), cudaMemcpyDeviceToHost, stream));
   CUDA_TRY(cudaStreamSynchronize(stream));
-  *n_out = h[0];
+  *st = mcx_stats{};
+  st->n_pairs = nqA * nqB;
+  st->n_tested = st->n_exact_tests = nqA * nqB;
+  st->n_aabb_pass = h[8 + 1];
+  st->n_singular = h[8 + 2];  // Moller-rejected quad pairs
+  st->n_hits = st->n_candidates = h[8 + 0];
+  if (h[3] > Bt.cand_cap)
+    return set_error(MCX_E_CAPACITY, "workspace holds %llu quad-box survivors, %llu needed (16 B each)",
+                     (unsigned long long)Bt.cand_cap, h[3]);
   if (h[0] > cap) return set_error(MCX_E_CAPACITY, "candidate capacity %llu < %llu", (unsigned long long)cap, h[0]);
   return MCX_OK;
 }
 
 // SPEC-literal pair_candidates over packed meshes with exact culling (quads = record
 // pairs); same survivor set and counters as launch_pair_candidates.
-static int launch_pair_candidates_mesh(const mcx_mesh_dev* A, const double* cA, uint32_t NA, uint32_t MA,
-                                       const mcx_mesh_dev* B, const double* cB, uint32_t NB, uint32_t MB,
-                                       const mcx_opts* o, uint64_t* gids, uint64_t cap, mcx_stats* st) {
-  if (!A || !B || !cA || !cB || !o || !st) return set_error(MCX_E_ARG, "null argument");
-  if (A->n_tri != 2ull * NA * (MA - 1) || B->n_tri != 2ull * NB * (MB - 1))
+static int launch_pair_candidates_mesh(const mcx_mesh_dev* A, const mcx_mesh_dev* B, const mcx_opts* o, uint64_t* gids,
+                                       uint64_t cap, mcx_stats* st) {
+  if (!A || !B || !o || !st) return set_error(MCX_E_ARG, "null argument");
+  if (!A->coords || !B->coords || !A->box || !B->box) return set_error(MCX_E_ARG, "null mesh buffer");
+  if (A->M < 2 || B->M < 2 || A->n_tri != 2ull * A->N * (A->M - 1) || B->n_tri != 2ull * B->N * (B->M - 1))
     return set_error(MCX_E_ARG, "mesh record counts do not match the grids");
+  const double *cA = A->coords, *cB = B->coords;
+  const uint32_t NA = A->N, MA = A->M, NB = B->N, MB = B->M;
   if (!A->gbox || !A->bbox || !B->gbox || !B->tbox) return set_error(MCX_E_ARG, "meshes need level boxes");
   if (cap > 0 && !gids) return set_error(MCX_E_ARG, "null gid buffer with nonzero capacity");
   const uint32_t scount = o->shard_count ? o->shard_count : 1;
@@ -788,6 +839,9 @@ static int launch_pair_candidates_mesh(const mcx_mesh_dev* A, const double* cA, 
   Bt.list_count = reinterpret_cast<unsigned long long*>(ws) + 1;
   Bt.blk_list = reinterpret_cast<uint4*>(ws + L.list);
   Bt.blk_cap = L.list_cap;
+  Bt.cand = reinterpret_cast<uint4*>(ws + L.cand);
+  Bt.cand_cap = L.cand_cap;
+  Bt.cand_count = reinterpret_cast<unsigned long long*>(ws) + 3;
   Timing tm;
   if (o->timing) {
     CUDA_TRY(cudaEventCreate(&tm.e0));
@@ -795,7 +849,8 @@ static int launch_pair_candidates_mesh(const mcx_mesh_dev* A, const double* cA, 
     CUDA_TRY(cudaEventRecord(tm.e0, stream));
   }
   std::vector<uint64_t> prefix;
-  const int rc = launch_cull<KIND_QUAD>(T, Bt, prefix, ws + L.table, o->device, stream);
+  int rc = launch_cull<KIND_QUAD>(T, Bt, prefix, ws + L.table, o->device, stream);
+  if (rc == MCX_OK && Bt.tasks) rc = launch_solve<KIND_QUAD>(Bt, o->device, stream);
   if (rc != MCX_OK) return rc;
   if (o->timing) CUDA_TRY(cudaEventRecord(tm.e1, stream));
   status_kernel<<<1, 32, 0, stream>>>(reinterpret_cast<const SearchParams*>(ws + L.table), 1,
@@ -810,12 +865,16 @@ static int launch_pair_candidates_mesh(const mcx_mesh_dev* A, const double* cA, 
   st->n_singular = c[2];  // Moller-rejected quad pairs
   st->n_tested = c[3];
   st->n_exact_tests = c[3];
+  st->n_candidates = c[0];
   if (o->timing) {
     float ms = 0.f;
     CUDA_TRY(cudaEventElapsedTime(&ms, tm.e0, tm.e1));
     st->kernel_ms = ms;
   }
   if (h[2]) return set_error(MCX_E_ARG, "non-finite (NaN/Inf) coordinates in an input mesh (mcx_pack status)");
+  if (h[3] > L.cand_cap)
+    return set_error(MCX_E_CAPACITY, "candidate-list capacity %llu < %llu quad-box survivors (opts->cand_cap)",
+                     (unsigned long long)L.cand_cap, h[3]);
   if (c[0] > cap) return set_error(MCX_E_CAPACITY, "candidate capacity %llu < %llu", (unsigned long long)cap, c[0]);
   return MCX_OK;
 }
@@ -842,6 +901,7 @@ int mcx_search(const mcx_mesh_dev* A, const mcx_mesh_dev* B, const mcx_opts* o, 
                mcx_stats* st) {
   using namespace mcx;
   if (!A || !B || !o || !st) return set_error(MCX_E_ARG, "null argument");
+  DeviceGuard guard;
   CUDA_TRY(cudaSetDevice(o->device));
   mcx_task t = {A, B, o->a_begin, o->a_end};
   return launch_batch(&t, 1, o, hits, nullptr, cap, st);
@@ -851,27 +911,29 @@ int mcx_search_batch(const mcx_task* tasks, uint32_t n_tasks, const mcx_opts* o,
                      uint64_t cap, mcx_stats* stats) {
   using namespace mcx;
   if (!o) return set_error(MCX_E_ARG, "null options");
+  DeviceGuard guard;
   CUDA_TRY(cudaSetDevice(o->device));
   return launch_batch(tasks, n_tasks, o, hits, hit_task, cap, stats);
 }
 
 int mcx_pair_candidates(const double* coords_a, uint32_t NA, uint32_t MA, const double* coords_b, uint32_t NB,
                         uint32_t MB, int device, void* stream, void* workspace, uint64_t workspace_bytes,
-                        uint64_t* gids, uint64_t cap, uint64_t* n_out) {
+                        uint64_t* gids, uint64_t cap, mcx_stats* stats) {
   using namespace mcx;
-  if (!coords_a || !coords_b || !n_out) return set_error(MCX_E_ARG, "null argument");
+  if (!coords_a || !coords_b || !stats) return set_error(MCX_E_ARG, "null argument");
+  DeviceGuard guard;
   CUDA_TRY(cudaSetDevice(device));
   return launch_pair_candidates(coords_a, NA, MA, coords_b, NB, MB, device, (cudaStream_t)stream, workspace,
-                                workspace_bytes, gids, cap, n_out);
+                                workspace_bytes, gids, cap, stats);
 }
 
-int mcx_pair_candidates_mesh(const mcx_mesh_dev* A, const double* coords_a, uint32_t NA, uint32_t MA,
-                             const mcx_mesh_dev* B, const double* coords_b, uint32_t NB, uint32_t MB,
-                             const mcx_opts* opts, uint64_t* gids, uint64_t cap, mcx_stats* stats) {
+int mcx_pair_candidates_mesh(const mcx_mesh_dev* A, const mcx_mesh_dev* B, const mcx_opts* opts, uint64_t* gids,
+                             uint64_t cap, mcx_stats* stats) {
   using namespace mcx;
   if (!opts) return set_error(MCX_E_ARG, "null options");
+  DeviceGuard guard;
   CUDA_TRY(cudaSetDevice(opts->device));
-  return launch_pair_candidates_mesh(A, coords_a, NA, MA, B, coords_b, NB, MB, opts, gids, cap, stats);
+  return launch_pair_candidates_mesh(A, B, opts, gids, cap, stats);
 }
 
 uint64_t mcx_pair_candidates_mesh_workspace_bytes(const mcx_mesh_dev* A, const mcx_mesh_dev* B, const mcx_opts* o) {

@@ -29,16 +29,20 @@ struct Cfg {
   static constexpr int QCAP = 32 * R_ * JB_ + 32;  // per-warp survivor queue capacity
 };
 
-enum Kind { KIND_TRI = 0, KIND_QUAD = 1 };
+// What a box-test survivor (candidate) is and what the solve stage does with it:
+//  KIND_TRI  — (storage A record, storage B record): precise test → triangle hit;
+//  KIND_QUAD — (A quad, B quad), original quad indices: Moller → quad-pair gid
+//              (SPEC pair_candidates);
+//  KIND_SPEC — (A quad, B quad): Moller, then the 4 triangle-pair precise tests of
+//              each candidate → triangle hits (SPEC find_intersections).
+enum Kind { KIND_TRI = 0, KIND_QUAD = 1, KIND_SPEC = 2 };
 
 // Per-task parameters (one entry of the device task table; a single search is a
 // batch of one).  Pointers are device pointers.
 struct __align__(16) SearchParams {
   const Box* boxA;
-  const double* geoA;
   const uint32_t* permA;    // storage → original index (NULL = identity)
   const Box* boxB;
-  const double* geoB;
   const uint32_t* permB;
   uint64_t nA;
   uint64_t a_begin, a_end;  // A storage range
@@ -48,7 +52,9 @@ struct __align__(16) SearchParams {
   uint64_t b_chunk, nchunk; // brute: B triangles per CTA (multiple of TILE), chunks
   uint64_t ntilesB;
   uint32_t shard_count, task;
-  unsigned long long* counters;  // per task: [0] emitted, [1] aabb pass, [2] singular / Moller-rejected, [3] tested
+  // per task: [0] emitted, [1] aabb pass, [2] singular (KIND_QUAD: Moller-rejected), [3] tested,
+  // [4] KIND_SPEC: Moller survivors (candidates)
+  unsigned long long* counters;
   // MCX_MODE_CULL
   const Box* gboxA;
   const Box* bboxA;
@@ -56,7 +62,7 @@ struct __align__(16) SearchParams {
   const Box* tboxB;
   const uint32_t* statusA;  // mcx_pack non-finite flags (may be NULL)
   const uint32_t* statusB;
-  // KIND_QUAD only: half-layer grids (4, M, N) for the Moller stage
+  // half-layer grids (4, M, N): the solve rebuilds triangle geometry from them; Moller
   const double* coordsA;
   const double* coordsB;
   uint32_t NA, MA, NB, MB;
@@ -82,6 +88,9 @@ struct Batch {
   uint64_t* gids;                // KIND_QUAD output
   uint64_t cap;
   unsigned long long* emit;      // shared output position counter
+  uint4* cand;                   // box-test survivors {A index, B index, task, 0} (compacted)
+  uint64_t cand_cap;
+  unsigned long long* cand_count;
   uint4* blk_list;               // cull: overlapping (task, local A block, B tile)
   uint64_t blk_cap;
   unsigned long long* list_count;
@@ -120,69 +129,117 @@ __device__ __forceinline__ void empty_box(double lo[4], double hi[4]) {
   }
 }
 
-// Process the queued pairs [0, n) of this warp's queue slice, one per lane
-// (queue entries are storage indices):
-// KIND_TRI  — canonical solve, emit (iA, iB, s, t, a, b) hits with original indices;
-// KIND_QUAD — SPEC-literal Moller quick test, emit surviving quad-pair gids.
-template <int KIND>
-__device__ __forceinline__ void flush_queue(const SearchParams& P, const Batch& Bt, const uint2* q, int n, int lane,
-                                            unsigned long long& n_pass, unsigned long long& n_sing) {
-  const bool valid = lane < n;
-  uint2 e = valid ? q[lane] : make_uint2(0, 0);
-  __syncwarp();
-  double sol[4];
-  int rc = 0;
-  if (KIND == KIND_TRI) {
-    if (valid) rc = solve_pair(P.geoA + (uint64_t)e.x * MCX_GEO_STRIDE, P.geoB + (uint64_t)e.y * MCX_GEO_STRIDE, sol);
-  } else {
-    if (valid) rc = moller_reject(P.coordsA, P.NA, P.MA, e.x, P.coordsB, P.NB, P.MB, e.y) ? 2 : 1;
+// Stage 2 (compaction, Fig. 1): append this warp's queued box-test
+// survivors [0, n) to the global candidate list — one atomic per 32 survivors,
+// one coalesced 16-byte store per lane.  The count keeps running past cand_cap so
+// the host learns the exact size to regrow to.
+__device__ __forceinline__ void flush_queue(const SearchParams& P, const Batch& Bt, const uint2* q, int n,
+                                            int lane) {
+  unsigned long long base = 0;
+  if (lane == 0) {
+    base = atomicAdd(Bt.cand_count, (unsigned long long)n);
+    atomicAdd(P.counters + 1, (unsigned long long)n);
   }
-  n_pass += valid ? 1 : 0;
-  n_sing += (rc == 2) ? 1 : 0;
-  const bool hit = (rc == 1);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (lane < n && base + lane < Bt.cand_cap) {
+    const uint2 e = q[lane];
+    Bt.cand[base + lane] = make_uint4(e.x, e.y, P.task, 0u);
+  }
+  __syncwarp();
+}
+
+// Append this warp's accepted triangle hits (ballot + one atomic per warp for the
+// output position; per-lane task counters, hits are rare).
+__device__ __forceinline__ void emit_hits(const Batch& Bt, bool hit, uint32_t ia, uint32_t ib, const double sol[4],
+                                          uint32_t task, unsigned long long* task_counters, int lane) {
   const unsigned hm = __ballot_sync(0xffffffffu, hit);
-  if (hm) {
-    const int leader = __ffs(hm) - 1;
-    unsigned long long base = 0;
-    if (lane == leader) {
-      base = atomicAdd(Bt.emit, (unsigned long long)__popc(hm));
-      atomicAdd(P.counters + 0, (unsigned long long)__popc(hm));
+  if (!hm) return;
+  const int leader = __ffs(hm) - 1;
+  unsigned long long base = 0;
+  if (lane == leader) base = atomicAdd(Bt.emit, (unsigned long long)__popc(hm));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (hit) {
+    atomicAdd(task_counters + 0, 1ull);
+    const unsigned long long pos = base + __popc(hm & ((1u << lane) - 1u));
+    if (pos < Bt.cap) {
+      mcx_hit h;
+      h.ia = ia;
+      h.ib = ib;
+      h.s = sol[0]; h.t = sol[1]; h.a = sol[2]; h.b = sol[3];
+      Bt.hits[pos] = h;
+      if (Bt.hit_task) Bt.hit_task[pos] = task;
     }
-    base = __shfl_sync(0xffffffffu, base, leader);
-    if (hit) {
-      const unsigned long long pos = base + __popc(hm & ((1u << lane) - 1u));
-      if (pos < Bt.cap) {
-        if (KIND == KIND_TRI) {
-          mcx_hit h;
-          h.ia = P.permA ? __ldg(P.permA + e.x) : e.x;
-          h.ib = P.permB ? __ldg(P.permB + e.y) : e.y;
-          h.s = sol[0]; h.t = sol[1]; h.a = sol[2]; h.b = sol[3];
-          Bt.hits[pos] = h;
-          if (Bt.hit_task) Bt.hit_task[pos] = P.task;
-        } else {
-          // quad indices qa = i + N1·k1, qb = j + N2·l1 → gid (PAPER.md kernel step 2)
-          const uint64_t i = e.x % P.NA, k1 = e.x / P.NA, j = e.y % P.NB, l1 = e.y / P.NB;
-          const uint64_t n12 = (uint64_t)P.NA * P.NB;
-          Bt.gids[pos] = i + (uint64_t)P.NA * j + n12 * k1 + n12 * (uint64_t)(P.MA - 1) * l1;
+  }
+}
+
+// Stage 3 (the precise test, PAPER.md "Precise Test"): one
+// thread per candidate at full occupancy, apart from the compare-bound sweep kernels
+// so their register budget holds only the box tests.
+template <int KIND>
+__global__ void __launch_bounds__(256) solve_kernel(const Batch Bt) {
+  const uint64_t n = min((uint64_t)*(volatile unsigned long long*)Bt.cand_count, Bt.cand_cap);
+  const int lane = threadIdx.x & 31;
+  for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < n; base += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = base + threadIdx.x;
+    const bool valid = k < n;
+    const uint4 c = valid ? Bt.cand[k] : make_uint4(0u, 0u, 0u, 0u);
+    const SearchParams& P = Bt.tasks[c.z];
+    if (KIND == KIND_TRI) {
+      double sol[4];
+      int rc = 0;
+      uint32_t ia = 0, ib = 0;
+      if (valid) {
+        ia = P.permA ? __ldg(P.permA + c.x) : c.x;
+        ib = P.permB ? __ldg(P.permB + c.y) : c.y;
+        rc = solve_tri(P.coordsA, P.NA, P.MA, ia, P.coordsB, P.NB, P.MB, ib, sol);
+        if (rc == 2) atomicAdd(P.counters + 2, 1ull);
+      }
+      emit_hits(Bt, rc == 1, ia, ib, sol, c.z, P.counters, lane);
+    } else if (KIND == KIND_QUAD) {
+      const bool cand = valid && !moller_reject(P.coordsA, P.NA, P.MA, c.x, P.coordsB, P.NB, P.MB, c.y);
+      if (valid && !cand) atomicAdd(P.counters + 2, 1ull);
+      const unsigned hm = __ballot_sync(0xffffffffu, cand);
+      if (hm) {
+        const int leader = __ffs(hm) - 1;
+        unsigned long long pos0 = 0;
+        if (lane == leader) pos0 = atomicAdd(Bt.emit, (unsigned long long)__popc(hm));
+        pos0 = __shfl_sync(0xffffffffu, pos0, leader);
+        const unsigned long long pos = pos0 + __popc(hm & ((1u << lane) - 1u));
+        if (cand) {
+          atomicAdd(P.counters + 0, 1ull);
+          atomicAdd(P.counters + 4, 1ull);
+          if (pos < Bt.cap) {
+            // quad indices qa = i + N1·k1, qb = j + N2·l1 → gid (PAPER.md kernel step 2)
+            const uint64_t i = c.x % P.NA, k1 = c.x / P.NA, j = c.y % P.NB, l1 = c.y / P.NB;
+            const uint64_t n12 = (uint64_t)P.NA * P.NB;
+            Bt.gids[pos] = i + (uint64_t)P.NA * j + n12 * k1 + n12 * (uint64_t)(P.MA - 1) * l1;
+          }
         }
+      }
+    } else {
+      // KIND_SPEC: "for each surviving gid, runs all 4 triangle-pair precise tests"
+      const bool cand = valid && !moller_reject(P.coordsA, P.NA, P.MA, c.x, P.coordsB, P.NB, P.MB, c.y);
+      if (cand) atomicAdd(P.counters + 4, 1ull);
+#pragma unroll 1
+      for (int v = 0; v < 4; ++v) {
+        const uint32_t ia = 2 * c.x + (v >> 1), ib = 2 * c.y + (v & 1);
+        double sol[4];
+        int rc = 0;
+        if (cand) {
+          rc = solve_tri(P.coordsA, P.NA, P.MA, ia, P.coordsB, P.NB, P.MB, ib, sol);
+          if (rc == 2) atomicAdd(P.counters + 2, 1ull);
+        }
+        emit_hits(Bt, rc == 1, ia, ib, sol, c.z, P.counters, lane);
       }
     }
   }
 }
 
-__device__ __forceinline__ void flush_counters(const SearchParams& P, int lane, unsigned long long n_pass,
-                                               unsigned long long n_sing, unsigned long long n_tested) {
+// Per-task count of executed box tests (cull: pair tests; prefilter: exact FP64 box tests).
+__device__ __forceinline__ void flush_tested(const SearchParams& P, int lane, unsigned long long n_tested) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    n_pass += __shfl_xor_sync(0xffffffffu, n_pass, o);
-    n_sing += __shfl_xor_sync(0xffffffffu, n_sing, o);
-    n_tested += __shfl_xor_sync(0xffffffffu, n_tested, o);
-  }
-  if (lane == 0) {
-    if (n_pass) atomicAdd(P.counters + 1, n_pass);
-    if (n_sing) atomicAdd(P.counters + 2, n_sing);
-    if (n_tested) atomicAdd(P.counters + 3, n_tested);
-  }
+  for (int o = 16; o > 0; o >>= 1) n_tested += __shfl_xor_sync(0xffffffffu, n_tested, o);
+  if (lane == 0 && n_tested) atomicAdd(P.counters + 3, n_tested);
 }
 
 // --------------------------------------------------------------- host side

@@ -2,11 +2,12 @@
 search calls through the C ABI, capacity handling and multi-GPU sharding.
 
 HBM layout per mesh (DESIGN.md §Data layout):
-  coords  (4, M, N) f64  — the half-layer grid as uploaded (32·N·M bytes)
+  coords  (4, M, N) f64  — the half-layer grid as uploaded (32·N·M bytes); the
+                           precise test rebuilds survivor triangles from it
   box     (n, 8)    f64  — per-triangle AABB lo[4], hi[4] (64 B/tri), the only
-                           array the hot loop streams
-  geo     (n, 20)   f64  — origin, edges, bivector, norm (160 B/tri), read only
-                           for AABB survivors
+                           array the hot loops stream
+  perm    (n,)      u32  — storage position → original triangle index
+  gbox/tbox/bbox         — union boxes per 32 / 512 / 1024 records (culling)
 Hits come back as (iA, iB, s, t, a, b) records of 40 B.
 
 Multi-GPU: A's triangle range is cut into blocks of
@@ -17,6 +18,7 @@ and the host concatenates and sorts the small hit lists.  No collective.
 from __future__ import annotations
 
 import threading
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 
 import numpy as np
@@ -54,11 +56,11 @@ def _check_coords(coords) -> None:
 
 
 class DeviceMesh:
-    """A half-layer grid resident in HBM, packed into triangle records on the device.
+    """A half-layer grid resident in HBM, packed into triangle boxes on the device.
 
-    Records are stored in the tiled order (``_lib.ORDER_TILED``) with ``perm``
-    mapping storage position → original triangle index, plus the culling
-    hierarchy (group / tile / block union boxes).  All search modes use this
+    One ``mcx_pack`` call writes the boxes in the tiled order (``_lib.ORDER_TILED``)
+    with ``perm`` mapping storage position → original triangle index, plus the
+    culling hierarchy (group / tile / block union boxes).  All search modes use this
     layout; hits always carry original indices.
     """
 
@@ -66,43 +68,39 @@ class DeviceMesh:
         t = torch()
         _require_cuda(device)
         dev = t.device("cuda", device)
-        s = stream or t.cuda.current_stream(device)
         _check_coords(coords)
         if isinstance(coords, np.ndarray):
             coords = t.from_numpy(np.ascontiguousarray(coords, dtype=np.float64))
+        self.device = device
+        L = _lib.load()
         # NaN/Inf are detected on the device by mcx_pack (status flag) and reported
         # by the search; no host-side pass over the coordinates.
-        with t.cuda.device(device), t.cuda.stream(s):
-            pinned = coords.device.type == "cpu" and coords.is_pinned()
-            self.coords = coords.to(dev, dtype=t.float64, non_blocking=pinned).contiguous()
-        self.device = device
-        _, self.M, self.N = (int(v) for v in self.coords.shape)
-        self.n_tri = 2 * self.N * (self.M - 1)
-        if self.n_tri >= 2 ** 31:
-            raise ConfigError("triangle count must be < 2^31")
-        n = self.n_tri
-        self.order = order
-        with t.cuda.device(device), t.cuda.stream(s):
-            self.box = t.empty((n, _lib.BOX_STRIDE), dtype=t.float64, device=dev)
-            self.geo = t.empty((n, _lib.GEO_STRIDE), dtype=t.float64, device=dev)
-            self.perm = t.empty(n, dtype=t.int32, device=dev) if order == _lib.ORDER_TILED else None
-            self.gbox = t.empty((-(-n // _lib.GROUP), 8), dtype=t.float64, device=dev)
-            self.tbox = t.empty((-(-n // _lib.TILE), 8), dtype=t.float64, device=dev)
-            self.bbox = t.empty((-(-n // _lib.BLOCK), 8), dtype=t.float64, device=dev)
-            self.status = t.empty(1, dtype=t.int32, device=dev)
-        L = _lib.load()
-        rc = L.mcx_pack(self.coords.data_ptr(), self.N, self.M, order, self.box.data_ptr(), self.geo.data_ptr(),
-                        self.perm.data_ptr() if self.perm is not None else None, self.status.data_ptr(), device,
-                        s.cuda_stream)
+        with t.cuda.device(device):
+            s = stream or t.cuda.current_stream(device)
+            with t.cuda.stream(s):
+                pinned = coords.device.type == "cpu" and coords.is_pinned()
+                self.coords = coords.to(dev, dtype=t.float64, non_blocking=pinned).contiguous()
+                _, self.M, self.N = (int(v) for v in self.coords.shape)
+                self.n_tri = 2 * self.N * (self.M - 1)
+                if self.n_tri >= 2 ** 31:
+                    raise ConfigError("triangle count must be < 2^31")
+                n = self.n_tri
+                self.order = order
+                self.box = t.empty((n, _lib.BOX_STRIDE), dtype=t.float64, device=dev)
+                self.perm = t.empty(n, dtype=t.int32, device=dev) if order == _lib.ORDER_TILED else None
+                self.gbox = t.empty((-(-n // _lib.GROUP), 8), dtype=t.float64, device=dev)
+                self.tbox = t.empty((-(-n // _lib.TILE), 8), dtype=t.float64, device=dev)
+                self.bbox = t.empty((-(-n // _lib.BLOCK), 8), dtype=t.float64, device=dev)
+                self.status = t.empty(1, dtype=t.int32, device=dev)
+            rc = L.mcx_pack(self.coords.data_ptr(), self.N, self.M, order, self.box.data_ptr(),
+                            self.perm.data_ptr() if self.perm is not None else None, self.gbox.data_ptr(),
+                            self.tbox.data_ptr(), self.bbox.data_ptr(), self.status.data_ptr(), device, s.cuda_stream)
         _lib.check(rc, "mcx_pack")
-        rc = L.mcx_levels(self.box.data_ptr(), n, self.gbox.data_ptr(), self.tbox.data_ptr(), self.bbox.data_ptr(),
-                          device, s.cuda_stream)
-        _lib.check(rc, "mcx_levels")
 
     def struct(self) -> _lib.MeshDev:
         """The mcx_mesh_dev view of this mesh (built once: the buffers never move)."""
         if getattr(self, "_struct", None) is None:
-            self._struct = _lib.MeshDev(self.n_tri, self.box.data_ptr(), self.geo.data_ptr(),
+            self._struct = _lib.MeshDev(self.n_tri, self.coords.data_ptr(), self.N, self.M, self.box.data_ptr(),
                                         self.perm.data_ptr() if self.perm is not None else None,
                                         self.gbox.data_ptr(), self.tbox.data_ptr(), self.bbox.data_ptr(),
                                         self.status.data_ptr())
@@ -147,6 +145,7 @@ class _Workspace:
         self.device = device
         self.ws = t.empty(1 << 16, dtype=t.uint8, device=t.device("cuda", device))
         self.hits = None
+        self.cand_cap = _lib.DEFAULT_CAND_CAP
 
     def hit_buffer(self, cap: int):
         t = torch()
@@ -167,37 +166,51 @@ class _Workspace:
         return self.tasks
 
 
+def _grow_for(rc, stats_list, cap, cand_cap):
+    """After MCX_E_CAPACITY: the new (hit cap, candidate cap) from the exact counts."""
+    hits = sum(int(st.n_hits) for st in stats_list)
+    cands = sum(int(st.n_aabb_pass) for st in stats_list)
+    if cands > cand_cap:
+        cand_cap = cands + 1024
+    if hits > cap:
+        cap = hits + 1024
+    return cap, cand_cap
+
+
 def search_device(A: DeviceMesh, B: DeviceMesh, *, mode: int = _lib.MODE_BRUTE, a_range=None,
                   shard=(0, 1), cap: int = 1 << 16, timing: bool = False, stream=None, task=None,
-                  sort: bool = True) -> SearchResult:
-    """Run one search call on A.device; grows the hit buffer and reruns on overflow."""
+                  sort: bool = True, pipeline: int = _lib.PIPE_TRIANGLE) -> SearchResult:
+    """Run one search call on A.device; grows the hit / candidate buffers and reruns on overflow."""
     t = torch()
     if A.device != B.device:
         raise ConfigError("A and B must live on the same device")
     L = _lib.load()
-    s = stream or t.cuda.current_stream(A.device)
     W = _Workspace.get(A.device)
     a0, a1 = (0, 0) if a_range is None else (int(a_range[0]), int(a_range[1]))
-    opts = _lib.Opts(A.device, s.cuda_stream, a0, a1, int(shard[0]), int(shard[1]), int(mode), int(timing), None, 0)
     As, Bs = A.struct(), B.struct()
-    need = L.mcx_workspace_bytes(As, Bs, opts)
-    ws = W.workspace(need)
-    opts.workspace = ws.data_ptr()
-    opts.workspace_bytes = ws.numel()
     st = _lib.Stats()
-    for _attempt in range(3):
-        buf = W.hit_buffer(cap)
-        cap_eff = buf.numel() // 5
-        rc = L.mcx_search(As, Bs, opts, buf.data_ptr(), cap_eff, st)
-        if rc == _lib.MCX_E_CAPACITY:
-            cap = int(st.n_hits) + 1024
-            continue
-        _lib.check(rc, "mcx_search", task=task)
-        break
-    else:
-        raise CapacityError("hit buffer overflow persisted after regrowing", required=int(st.n_hits), task=task)
-    n = int(st.n_hits)
-    raw = buf[: n * 5].cpu().numpy() if n else np.zeros(0)
+    cand_cap = W.cand_cap
+    with t.cuda.device(A.device):
+        s = stream or t.cuda.current_stream(A.device)
+        for _attempt in range(4):
+            opts = _lib.Opts(A.device, s.cuda_stream, a0, a1, int(shard[0]), int(shard[1]), int(mode), int(timing),
+                             None, 0, int(pipeline), cand_cap)
+            ws = W.workspace(L.mcx_workspace_bytes(As, Bs, opts))
+            opts.workspace, opts.workspace_bytes = ws.data_ptr(), ws.numel()
+            buf = W.hit_buffer(cap)
+            cap_eff = buf.numel() // 5
+            rc = L.mcx_search(As, Bs, opts, buf.data_ptr(), cap_eff, st)
+            if rc == _lib.MCX_E_CAPACITY:
+                cap, cand_cap = _grow_for(rc, [st], cap_eff, cand_cap)
+                W.cand_cap = max(W.cand_cap, cand_cap)
+                continue
+            _lib.check(rc, "mcx_search", task=task)
+            break
+        else:
+            raise CapacityError("hit / candidate buffer overflow persisted after regrowing", required=int(st.n_hits),
+                                task=task)
+        n = int(st.n_hits)
+        raw = buf[: n * 5].cpu().numpy() if n else np.zeros(0)
     hits = raw.view(HIT_DTYPE).copy() if n else np.zeros(0, HIT_DTYPE)
     if sort and n:
         hits = hits[np.lexsort((hits["ib"], hits["ia"]))]
@@ -205,11 +218,12 @@ def search_device(A: DeviceMesh, B: DeviceMesh, *, mode: int = _lib.MODE_BRUTE, 
 
 
 def search_batch(pairs, *, mode: int = _lib.MODE_BRUTE, shard=(0, 1), cap: int = 1 << 16, timing: bool = False,
-                 stream=None, task_ids=None):
+                 stream=None, task_ids=None, pipeline: int = _lib.PIPE_TRIANGLE):
     """Many (A, B) DeviceMesh searches in one launch per kernel (mcx_search_batch).
 
     ``pairs``: list of (A, B) or (A, B, (a_begin, a_end)).  Returns one
-    SearchResult per task, hits sorted by (ia, ib).
+    SearchResult per task, hits sorted by (ia, ib).  ``task_ids`` (optional, one per
+    pair) tags errors with the failing layer pair.
     """
     t = torch()
     if not pairs:
@@ -219,7 +233,6 @@ def search_batch(pairs, *, mode: int = _lib.MODE_BRUTE, shard=(0, 1), cap: int =
         if p[0].device != dev or p[1].device != dev:
             raise ConfigError("all meshes of a batch must live on one device")
     L = _lib.load()
-    s = stream or t.cuda.current_stream(dev)
     W = _Workspace.get(dev)
     n = len(pairs)
     tasks = (_lib.Task * n)()
@@ -228,32 +241,47 @@ def search_batch(pairs, *, mode: int = _lib.MODE_BRUTE, shard=(0, 1), cap: int =
         t_k.A, t_k.B = p[0].struct_ptr(), p[1].struct_ptr()
         if len(p) > 2:
             t_k.a_begin, t_k.a_end = int(p[2][0]), int(p[2][1])
-    opts = _lib.Opts(dev, s.cuda_stream, 0, 0, int(shard[0]), int(shard[1]), int(mode), int(timing), None, 0)
-    need = L.mcx_batch_workspace_bytes(tasks, n, opts)
-    ws = W.workspace(need)
-    opts.workspace = ws.data_ptr()
-    opts.workspace_bytes = ws.numel()
     stats = (_lib.Stats * n)()
-    for _attempt in range(3):
-        buf = W.hit_buffer(cap)
-        cap_eff = buf.numel() // 5
-        tb = W.task_buffer(cap_eff)
-        rc = L.mcx_search_batch(tasks, n, opts, buf.data_ptr(), tb.data_ptr(), cap_eff, stats)
+    cand_cap = W.cand_cap
+    with t.cuda.device(dev):
+        s = stream or t.cuda.current_stream(dev)
+        for _attempt in range(4):
+            opts = _lib.Opts(dev, s.cuda_stream, 0, 0, int(shard[0]), int(shard[1]), int(mode), int(timing), None, 0,
+                             int(pipeline), cand_cap)
+            ws = W.workspace(L.mcx_batch_workspace_bytes(tasks, n, opts))
+            opts.workspace, opts.workspace_bytes = ws.data_ptr(), ws.numel()
+            buf = W.hit_buffer(cap)
+            cap_eff = buf.numel() // 5
+            tb = W.task_buffer(cap_eff)
+            rc = L.mcx_search_batch(tasks, n, opts, buf.data_ptr(), tb.data_ptr(), cap_eff, stats)
+            if rc == _lib.MCX_E_CAPACITY:
+                cap, cand_cap = _grow_for(rc, list(stats), cap_eff, cand_cap)
+                W.cand_cap = max(W.cand_cap, cand_cap)
+                continue
+            if rc != _lib.MCX_OK:
+                _raise_for_task(rc, "mcx_search_batch", pairs, stats, task_ids)
+            break
+        else:
+            raise CapacityError("hit / candidate buffer overflow persisted after regrowing",
+                                required=sum(int(x.n_hits) for x in stats), task=task_ids)
         total = sum(int(stats[k].n_hits) for k in range(n))
-        if rc == _lib.MCX_E_CAPACITY:
-            cap = total + 1024
-            continue
-        _lib.check(rc, "mcx_search_batch", task=task_ids)
-        break
-    else:
-        raise CapacityError("hit buffer overflow persisted after regrowing", required=total, task=task_ids)
-    hits = buf[: total * 5].cpu().numpy().view(HIT_DTYPE).copy() if total else np.zeros(0, HIT_DTYPE)
-    owner = tb[:total].cpu().numpy() if total else np.zeros(0, np.int32)
+        hits = buf[: total * 5].cpu().numpy().view(HIT_DTYPE).copy() if total else np.zeros(0, HIT_DTYPE)
+        owner = tb[:total].cpu().numpy() if total else np.zeros(0, np.int32)
     # one sort by (task, ia, ib), then split at the task boundaries (O(hits log hits), not O(tasks x hits))
     order = np.lexsort((hits["ib"], hits["ia"], owner))
     hits, owner = hits[order], owner[order]
     cuts = np.searchsorted(owner, np.arange(n + 1))
     return [SearchResult(hits=hits[cuts[k]:cuts[k + 1]].copy(), stats=stats[k].as_dict()) for k in range(n)]
+
+
+def _raise_for_task(rc, what, pairs, stats, task_ids):
+    """A failed batch names the layer pair it failed on when that is knowable: a
+    non-finite mesh is found from the per-mesh status flags."""
+    if rc == _lib.MCX_E_ARG and task_ids is not None:
+        for k, p in enumerate(pairs):
+            if int(p[0].status.item()) or int(p[1].status.item()):
+                _lib.check(rc, what, task=task_ids[k])
+    _lib.check(rc, what, task=task_ids)
 
 
 def ctypes_pointer(x):
@@ -274,19 +302,40 @@ def _merge(results) -> SearchResult:
 
 
 _SIDE_STREAMS: dict = {}
+_POOLS: dict = {}
+_POOLS_LOCK = threading.Lock()
 
 
 def _side_stream(device: int):
     """One persistent side stream per (thread, device): a fresh stream per call would
-    defeat the caching allocator (its blocks are cached per stream)."""
+    defeat the caching allocator (its blocks are cached per stream).  Multi-GPU calls
+    run on the per-device worker threads (_device_pool), so the set stays bounded."""
     key = (threading.get_ident(), device)
     if key not in _SIDE_STREAMS:
         _SIDE_STREAMS[key] = torch().cuda.Stream(device)
     return _SIDE_STREAMS[key]
 
 
+def _device_pool(device: int) -> ThreadPoolExecutor:
+    """One persistent worker thread per GPU: per-thread workspaces and side streams are
+    created once per device instead of once per call."""
+    with _POOLS_LOCK:
+        if device not in _POOLS:
+            _POOLS[device] = ThreadPoolExecutor(max_workers=1, thread_name_prefix=f"mcx-gpu{device}")
+        return _POOLS[device]
+
+
+def run_on_devices(fn, devices):
+    """fn(rank) for every rank, each on its device's worker thread (ctypes releases the
+    GIL, so the GPUs run concurrently); re-raises the first error."""
+    if len(devices) == 1:
+        return [fn(0)]
+    futs = [_device_pool(d).submit(fn, r) for r, d in enumerate(devices)]
+    return [f.result() for f in futs]
+
+
 def search_one(coords_a, coords_b, *, device: int = 0, mode: int = _lib.MODE_BRUTE, shard=(0, 1),
-               timing: bool = False, task=None, stream=None) -> SearchResult:
+               timing: bool = False, task=None, stream=None, pipeline: int = _lib.PIPE_TRIANGLE) -> SearchResult:
     """Host grids → hits on one device: B is uploaded and packed on a side stream so
     its H2D overlaps A's packing; then one search call.  Pinned CPU tensors give
     asynchronous copies."""
@@ -299,45 +348,27 @@ def search_one(coords_a, coords_b, *, device: int = 0, mode: int = _lib.MODE_BRU
         ready = side.record_event()
         Am = DeviceMesh(coords_a, device, stream=main)
         main.wait_event(ready)
-        return search_device(Am, Bm, mode=mode, shard=shard, timing=timing, stream=main, task=task)
+        return search_device(Am, Bm, mode=mode, shard=shard, timing=timing, stream=main, task=task,
+                             pipeline=pipeline)
 
 
 def search(coords_a, coords_b, *, devices=(0,), mode: int = _lib.MODE_BRUTE, timing: bool = False,
-           task=None) -> SearchResult:
+           task=None, pipeline: int = _lib.PIPE_TRIANGLE) -> SearchResult:
     """Host-to-host triangle search: upload, pack, search (sharded over ``devices``,
-    one host thread per GPU), gather, sort."""
+    one persistent host thread per GPU), gather, sort."""
     devices = list(devices)
     if not devices:
         raise ConfigError("devices must be non-empty")
     for d in devices:
         _require_cuda(d)
     G = len(devices)
-    results = [None] * G
-    errors = [None] * G
-
-    def run(rank: int):
-        try:
-            results[rank] = search_one(coords_a, coords_b, device=devices[rank], mode=mode, shard=(rank, G),
-                                       timing=timing, task=task)
-        except Exception as exc:  # surfaced below with the task id
-            errors[rank] = exc
-
-    if G == 1:
-        run(0)
-    else:
-        threads = [threading.Thread(target=run, args=(r,)) for r in range(G)]
-        for th in threads:
-            th.start()
-        for th in threads:
-            th.join()
-    for e in errors:
-        if e is not None:
-            raise e
+    results = run_on_devices(lambda r: search_one(coords_a, coords_b, device=devices[r], mode=mode, shard=(r, G),
+                                                  timing=timing, task=task, pipeline=pipeline), devices)
     return _merge(results)
 
 
 def pair_candidates_device(coords_a, coords_b, device: int = 0, cap: int = 1 << 16, task=None) -> np.ndarray:
-    """Sorted u64 quad-pair gids surviving ¬aabb_reject ∧ ¬moller_reject."""
+    """Sorted u64 quad-pair gids surviving ¬aabb_reject ∧ ¬moller_reject, brute force."""
     t = torch()
     _require_cuda(device)
     L = _lib.load()
@@ -348,19 +379,25 @@ def pair_candidates_device(coords_a, coords_b, device: int = 0, cap: int = 1 << 
         _, MA, NA = ca.shape
         _, MB, NB = cb.shape
         nq = NA * (MA - 1) + NB * (MB - 1)
-        ws = t.empty(1024 + 64 * nq, dtype=t.uint8, device=dev)  # include/mcx.h: 1024 + 64·quads
         s = t.cuda.current_stream(device)
-        n_out = ctypes_u64()
-        for _ in range(3):
+        st = _lib.Stats()
+        n_cand = 1 << 16
+        for _ in range(4):
+            # include/mcx.h: 1024 + 64·quads + 16 per quad-AABB survivor
+            ws = t.empty(1024 + 64 * nq + 16 * n_cand, dtype=t.uint8, device=dev)
             gids = t.empty(max(cap, 1), dtype=t.int64, device=dev)
             rc = L.mcx_pair_candidates(ca.data_ptr(), NA, MA, cb.data_ptr(), NB, MB, device, s.cuda_stream,
-                                       ws.data_ptr(), ws.numel(), gids.data_ptr(), cap, n_out)
+                                       ws.data_ptr(), ws.numel(), gids.data_ptr(), cap, st)
             if rc == _lib.MCX_E_CAPACITY:
-                cap = int(n_out.value) + 1024
+                n_cand = max(n_cand, int(st.n_aabb_pass) + 1024)
+                cap = max(cap, int(st.n_hits) + 1024)
                 continue
             _lib.check(rc, "mcx_pair_candidates", task=task)
             break
-        n = int(n_out.value)
+        else:
+            raise CapacityError("candidate buffer overflow persisted after regrowing", required=int(st.n_hits),
+                                task=task)
+        n = int(st.n_hits)
         out = gids[:n].cpu().numpy().view(np.uint64)
     return np.sort(out)
 
@@ -374,21 +411,21 @@ def record_fields_device(coords_a, s_a, coords_b, s_b, hits: np.ndarray, device:
     _require_cuda(device)
     L = _lib.load()
     dev = t.device("cuda", device)
-    ca = t.as_tensor(np.ascontiguousarray(coords_a, dtype=np.float64)).to(dev)
-    _, MA, NA = ca.shape
-    _, MB, NB = np.asarray(coords_b).shape
-    sa = t.as_tensor(np.ascontiguousarray(s_a, dtype=np.float64)).to(dev)
-    sb = t.as_tensor(np.ascontiguousarray(s_b, dtype=np.float64)).to(dev)
-    h = t.from_numpy(np.ascontiguousarray(hits).view(np.uint8)).to(dev)
-    gid = t.empty(n, dtype=t.int64, device=dev)
-    pts = t.empty((n, 4), dtype=t.float64, device=dev)
-    par = t.empty((n, 4), dtype=t.float64, device=dev)
     with t.cuda.device(device):
+        ca = t.as_tensor(np.ascontiguousarray(coords_a, dtype=np.float64)).to(dev)
+        _, MA, NA = ca.shape
+        _, MB, NB = np.asarray(coords_b).shape
+        sa = t.as_tensor(np.ascontiguousarray(s_a, dtype=np.float64)).to(dev)
+        sb = t.as_tensor(np.ascontiguousarray(s_b, dtype=np.float64)).to(dev)
+        h = t.from_numpy(np.ascontiguousarray(hits).view(np.uint8)).to(dev)
+        gid = t.empty(n, dtype=t.int64, device=dev)
+        pts = t.empty((n, 4), dtype=t.float64, device=dev)
+        par = t.empty((n, 4), dtype=t.float64, device=dev)
         s = t.cuda.current_stream(device)
         rc = L.mcx_records(h.data_ptr(), n, ca.data_ptr(), NA, MA, sa.data_ptr(), NB, MB, sb.data_ptr(),
                            gid.data_ptr(), pts.data_ptr(), par.data_ptr(), device, s.cuda_stream)
-    _lib.check(rc, "mcx_records")
-    return gid.cpu().numpy().view(np.uint64), pts.cpu().numpy(), par.cpu().numpy()
+        _lib.check(rc, "mcx_records")
+        return gid.cpu().numpy().view(np.uint64), pts.cpu().numpy(), par.cpu().numpy()
 
 
 def pair_candidates_mesh(A: DeviceMesh, B: DeviceMesh, *, shard=(0, 1), cap: int = 1 << 16, stream=None,
@@ -399,26 +436,31 @@ def pair_candidates_mesh(A: DeviceMesh, B: DeviceMesh, *, shard=(0, 1), cap: int
     if A.device != B.device:
         raise ConfigError("A and B must live on the same device")
     L = _lib.load()
-    s = stream or t.cuda.current_stream(A.device)
     W = _Workspace.get(A.device)
-    opts = _lib.Opts(A.device, s.cuda_stream, 0, 0, int(shard[0]), int(shard[1]), _lib.MODE_CULL, int(timing),
-                     None, 0)
     As, Bs = A.struct(), B.struct()
-    ws = W.workspace(L.mcx_pair_candidates_mesh_workspace_bytes(As, Bs, opts))
-    opts.workspace, opts.workspace_bytes = ws.data_ptr(), ws.numel()
     st = _lib.Stats()
     dev = t.device("cuda", A.device)
-    for _ in range(3):
-        gids = t.empty(max(cap, 1), dtype=t.int64, device=dev)
-        rc = L.mcx_pair_candidates_mesh(As, A.coords.data_ptr(), A.N, A.M, Bs, B.coords.data_ptr(), B.N, B.M, opts,
-                                        gids.data_ptr(), cap, st)
-        if rc == _lib.MCX_E_CAPACITY:
-            cap = int(st.n_hits) + 1024
-            continue
-        _lib.check(rc, "mcx_pair_candidates_mesh", task=task)
-        break
-    n = int(st.n_hits)
-    return np.sort(gids[:n].cpu().numpy().view(np.uint64)), st.as_dict()
+    cand_cap = W.cand_cap
+    with t.cuda.device(A.device):
+        s = stream or t.cuda.current_stream(A.device)
+        for _ in range(4):
+            opts = _lib.Opts(A.device, s.cuda_stream, 0, 0, int(shard[0]), int(shard[1]), _lib.MODE_CULL, int(timing),
+                             None, 0, _lib.PIPE_TRIANGLE, cand_cap)
+            ws = W.workspace(L.mcx_pair_candidates_mesh_workspace_bytes(As, Bs, opts))
+            opts.workspace, opts.workspace_bytes = ws.data_ptr(), ws.numel()
+            gids = t.empty(max(cap, 1), dtype=t.int64, device=dev)
+            rc = L.mcx_pair_candidates_mesh(As, Bs, opts, gids.data_ptr(), cap, st)
+            if rc == _lib.MCX_E_CAPACITY:
+                cap, cand_cap = _grow_for(rc, [st], cap, cand_cap)
+                W.cand_cap = max(W.cand_cap, cand_cap)
+                continue
+            _lib.check(rc, "mcx_pair_candidates_mesh", task=task)
+            break
+        else:
+            raise CapacityError("candidate buffer overflow persisted after regrowing", required=int(st.n_hits),
+                                task=task)
+        n = int(st.n_hits)
+        return np.sort(gids[:n].cpu().numpy().view(np.uint64)), st.as_dict()
 
 
 def ctypes_u64():

@@ -142,15 +142,25 @@ def _check_backend(backend: str):
 
 
 # ---------------------------------------------------------------- search API
-def search_hits(u_half, s_half, backend: str = "cuda", *, devices=(0,), mode: str = "cull",
-                timing: bool = False):
-    """Triangle-level hits (iA, iB, s, t, a, b), sorted by (iA, iB), plus kernel stats."""
-    _check_backend(backend)
+def _mode_pipeline(mode: str, pipeline: str):
     m = _lib.MODE_NAMES.get(mode)
     if m is None:
         raise ConfigError(f"mode must be one of {sorted(_lib.MODE_NAMES)}, got {mode!r}")
+    p = _lib.PIPELINE_NAMES.get(pipeline)
+    if p is None:
+        raise ConfigError(f"pipeline must be one of {sorted(_lib.PIPELINE_NAMES)}, got {pipeline!r}")
+    if p == _lib.PIPE_SPEC and m != _lib.MODE_CULL:
+        raise ConfigError("pipeline='spec' runs on the culling kernels (mode='cull')")
+    return m, p
+
+
+def search_hits(u_half, s_half, backend: str = "cuda", *, devices=(0,), mode: str = "cull",
+                pipeline: str = "triangle", timing: bool = False):
+    """Triangle-level hits (iA, iB, s, t, a, b), sorted by (iA, iB), plus kernel stats."""
+    _check_backend(backend)
+    m, p = _mode_pipeline(mode, pipeline)
     return _device.search(_coords(u_half), _coords(s_half), devices=devices, mode=m, timing=timing,
-                          task=_task(u_half, s_half))
+                          task=_task(u_half, s_half), pipeline=p)
 
 
 def pair_candidates(u_half, s_half, backend: str = "cuda", *, device: int = 0, mode: str = "cull") -> np.ndarray:
@@ -242,14 +252,16 @@ def hits_to_records(coords_a, s_a, coords_b, s_b, hits, layer=(0, "+", 0, "+"), 
 
 
 def _dedup_mask(pts: np.ndarray, tol: float) -> np.ndarray:
-    """Greedy in record order: drop a record whose point is within tol (max-norm) of a
-    KEPT earlier record.  Candidate pairs come from an x-sorted sweep (vectorised);
-    only records that have an earlier candidate are resolved in a Python loop."""
+    """Greedy in record order: drop a record whose point is within tol of a KEPT
+    earlier record in every coordinate (|fl(p_c − q_c)| ≤ tol; the device runtime
+    implements the same rule, csrc/mcx_runtime.cu).  Candidate pairs come from an
+    x-sorted sweep with a 2·tol window (a superset, filtered exactly below); only
+    records that have an earlier candidate are resolved in a Python loop."""
     n = len(pts)
     keep = np.ones(n, dtype=bool)
     order = np.argsort(pts[:, 0], kind="stable")
     xs = pts[order, 0]
-    hi = np.searchsorted(xs, xs + tol, side="right")
+    hi = np.searchsorted(xs, xs + 2.0 * tol, side="right")
     cnt = hi - np.arange(n) - 1
     if cnt.sum() == 0:
         return keep
@@ -273,16 +285,58 @@ def record_fields_device(coords_a, s_a, coords_b, s_b, hits, device: int = 0):
     return _device.record_fields_device(coords_a, s_a, coords_b, s_b, hits, device=device)
 
 
+def records_to_objects(recs, NA: int, NB: int, layer=(0, "+", 0, "+"), tof: float = float("nan")):
+    """IntersectionRecords from the runtime's record array (runtime.RECORD_DTYPE)."""
+    out = []
+    ia = recs["ia"].astype(np.int64)
+    ib = recs["ib"].astype(np.int64)
+    qa, qb = ia >> 1, ib >> 1
+    for n in range(len(recs)):
+        out.append(IntersectionRecord(
+            point=recs["point"][n].copy(), bary=tuple(float(v) for v in recs["bary"][n]),
+            params=tuple(float(v) for v in recs["params"][n]),
+            pair=QuadIndex(int(recs["gid"][n]), int(qa[n] % NA), int(qb[n] % NB), int(qa[n] // NA) + 1,
+                           int(qb[n] // NB) + 1),
+            tri=(int(ia[n]) & 1, int(ib[n]) & 1), layer=layer, tof=tof, tri_index=(int(ia[n]), int(ib[n]))))
+    return out
+
+
 def find_intersections(u_half, s_half, backend: str = "cuda", *, devices=(0,), mode: str = "cull",
-                       dedup: bool = True, tof: float = float("nan")):
-    """All mesh intersections of two half-layers as IntersectionRecords."""
+                       pipeline: str = "spec", dedup: bool = True, tof: float = float("nan")):
+    """All mesh intersections of two half-layers as IntersectionRecords.
+
+    ``pipeline="spec"`` (default) is the SPEC's literal pipeline — quad AABB + Möller
+    survivors, then the 4 triangle-pair precise tests of each — so the records equal
+    the reference's serial backend's record for record.
+    ``pipeline="triangle"`` tests every triangle pair's boxes (no Möller), which also
+    keeps the touching hits floating-point Möller can drop.
+
+    One GPU: one ``mcx_find_intersections`` call — upload, pack, search, records,
+    (gid, τ_A, τ_B) sort and dedup all on the device.  Several GPUs: A's blocks are
+    sharded over ``devices``, the hit lists gathered, and the records stage runs on
+    ``devices[0]`` (``mcx_finish_hits``).
+    """
+    from . import runtime
     _check_backend(backend)
+    m, p = _mode_pipeline(mode, pipeline)
     ca, cb = _coords(u_half), _coords(s_half)
-    res = search_hits(ca, cb, backend, devices=devices, mode=mode)
-    task = _task(u_half, s_half) or (0, "+", 0, "+")
+    layer = _task(u_half, s_half) or (0, "+", 0, "+")
     sa, sb = _svals(u_half, ca.shape[1]), _svals(s_half, cb.shape[1])
-    gid, pts, params = record_fields_device(ca, sa, cb, sb, res.hits, device=devices[0])
-    return assemble_records(ca, cb, res.hits, gid, pts, params, layer=task, tof=tof, dedup=dedup)
+    devices = list(devices)
+    if not devices:
+        raise ConfigError("devices must be non-empty")
+    ctx = runtime.context(devices[0])
+    if len(devices) == 1:
+        recs, _, _ = ctx.find(ca, sa, cb, sb, layer, mode=m, pipeline=p, dedup=dedup, task=_task(u_half, s_half))
+    else:
+        res = _device.search(ca, cb, devices=devices, mode=m, task=_task(u_half, s_half), pipeline=p)
+        A, B = ctx.mesh(ca, sa), ctx.mesh(cb, sb)
+        try:
+            recs, _ = ctx.finish_hits(res.hits, A, B, layer, dedup=dedup)
+        finally:
+            A.free()
+            B.free()
+    return records_to_objects(recs, ca.shape[2], cb.shape[2], layer=layer, tof=tof)
 
 
 # ---------------------------------------------------------------- records file

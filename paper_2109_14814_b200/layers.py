@@ -2,10 +2,13 @@
 reference's intersection stage dispatches to ``isect``.
 
 Only the bookkeeping on the search path is here: ``enumerate_layer_pairs``
-(SPEC.md:382-390), the plan text file ``n1 sign1 n2 sign2 tof``, and
-``search_plan``, which runs every task of a plan as ONE batched device job
-(``mcx_search_batch``: one launch per kernel for all tasks, §8(f) row 3), each
-distinct half-layer uploaded and packed once.
+(with the ``--include-core`` extension of SPEC.md:398), the plan
+text file ``n1 sign1 n2 sign2 tof``, and ``search_plan``, which runs
+a plan as ONE batched device job per GPU (``mcx_intersect``: one launch per kernel
+for all of the GPU's tasks, §8(f) row 3), each distinct half-layer uploaded and
+packed once, records sorted / deduplicated / formatted on the device.  With several
+GPUs the tasks are dealt out whole (they are independent) by a
+deterministic longest-first assignment, one host thread per GPU.
 """
 from __future__ import annotations
 
@@ -14,7 +17,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import _lib, device as _device, isect
+from . import _lib, device as _device, isect, runtime
 from .errors import ConfigError, FileFormatError
 from .mesh import ManifoldMesh, half_layer
 
@@ -30,15 +33,24 @@ class LayerPairPlan:
         return len(self.tasks)
 
 
-def enumerate_layer_pairs(u_mesh: ManifoldMesh, s_mesh: ManifoldMesh, n_max: int, omega_p: float = 1.0):
+def enumerate_layer_pairs(u_mesh: ManifoldMesh, s_mesh: ManifoldMesh, n_max: int, omega_p: float = 1.0,
+                          include_core: bool = False):
     """Pairs (U_n, S_n) and (U_n, S_{n−1}) for n = 1..n_max over all four sign
     combinations; (U_1, S_0) is skipped because layers start at 1 (SPEC.md:382-390,
-    design decision).  Counts: n_max = 1 → 4, 2 → 12, 5 → 36, i.e. 4·(2·n_max − 1)."""
+    design decision).  Counts: n_max = 1 → 4, 2 → 12, 5 → 36, i.e. 4·(2·n_max − 1).
+
+    ``include_core`` re-enables the fundamental-domain cores |s| < D as
+    layer 0 (one half-layer per mesh, sign '+'): the same family extended to n = 0 adds
+    (U_0, S_0) and (U_1^±, S_0), three tasks, listed first."""
     if n_max < 1:
         raise ConfigError("n_max must be >= 1")
     if n_max > u_mesh.n_max or n_max > s_mesh.n_max:
         raise ConfigError(f"meshes are globalized to n_max = {u_mesh.n_max}/{s_mesh.n_max} < {n_max}")
     plan = LayerPairPlan()
+    if include_core:
+        for task in ((0, "+", 0, "+"), (1, "+", 0, "+"), (1, "-", 0, "+")):
+            plan.tasks.append(task)
+            plan.tof.append(2.0 * math.pi * (task[0] + task[2]) / omega_p)
     for n in range(1, n_max + 1):
         for n2 in (n, n - 1):
             if n2 < 1:
@@ -56,6 +68,9 @@ def write_plan(path, plan: LayerPairPlan) -> None:
             fh.write(f"{n1} {s1} {n2} {s2} {tof:.17g}\n")
 
 
+_SIGNS = ("+", "-")
+
+
 def read_plan(path) -> LayerPairPlan:
     plan = LayerPairPlan()
     with open(path) as fh:
@@ -63,8 +78,8 @@ def read_plan(path) -> LayerPairPlan:
             f = line.split()
             if not f:
                 continue
-            if len(f) != 5 or f[1] not in "+-" or f[3] not in "+-":
-                raise FileFormatError(f"{path}:{ln}: expected 'n1 sign1 n2 sign2 tof'")
+            if len(f) != 5 or f[1] not in _SIGNS or f[3] not in _SIGNS:
+                raise FileFormatError(f"{path}:{ln}: expected 'n1 sign1 n2 sign2 tof' with signs '+' / '-'")
             try:
                 plan.tasks.append((int(f[0]), f[1], int(f[2]), f[3]))
                 plan.tof.append(float(f[4]))
@@ -77,38 +92,94 @@ def _sign(s: str) -> int:
     return 1 if s == "+" else -1
 
 
-def search_plan(u_mesh: ManifoldMesh, s_mesh: ManifoldMesh, plan: LayerPairPlan, backend: str = "cuda", *,
-                mode: str = "cull", device: int = 0, dedup: bool = True):
-    """Run every layer-pair task of ``plan`` as one batched device job.
+def assign_tasks(costs, n_devices: int):
+    """Deterministic longest-processing-time-first assignment of whole tasks to GPUs
+    (ties by task index).  Returns one sorted task-index list per device."""
+    load = [0.0] * n_devices
+    out = [[] for _ in range(n_devices)]
+    for k in sorted(range(len(costs)), key=lambda k: (-costs[k], k)):
+        d = min(range(n_devices), key=lambda d: (load[d], d))
+        out[d].append(k)
+        load[d] += costs[k]
+    return [sorted(o) for o in out]
 
-    Returns ``(records, per_task_stats)``: records of all tasks in plan order (each
-    task's records sorted by gid and deduplicated as ``find_intersections`` does),
-    and the per-task counters (the RunManifest's survivor/hit counts).
+
+@dataclass
+class PlanResult:
+    records: list      # IntersectionRecords of all tasks, plan order
+    stats: list        # per task: counters (+ "layer", "device")
+    text: bytes = b""  # the records file body (SPEC.md:507), when requested
+
+    def __iter__(self):  # records, stats = search_plan(...)
+        return iter((self.records, self.stats))
+
+
+def _halves(u_mesh, s_mesh, plan):
+    halves = {}
+    for (n1, s1, n2, s2) in plan.tasks:
+        for key, mesh, n, sg in ((("u", n1, s1), u_mesh, n1, s1), (("s", n2, s2), s_mesh, n2, s2)):
+            if key not in halves:
+                halves[key] = half_layer(mesh, n, _sign(sg))
+    return halves
+
+
+def search_plan(u_mesh: ManifoldMesh, s_mesh: ManifoldMesh, plan: LayerPairPlan, backend: str = "cuda", *,
+                mode: str = "cull", pipeline: str = "spec", device: int = 0, devices=None, dedup: bool = True,
+                text: bool = False) -> PlanResult:
+    """Run every layer-pair task of ``plan``.
+
+    Per GPU one ``mcx_intersect`` call over its tasks: the distinct half-layers it
+    needs are uploaded and packed once, every task's search runs in one batched
+    launch, and records come back sorted by (gid, τ_A, τ_B) and deduplicated per task
+    exactly as ``isect.find_intersections`` returns them.  ``devices`` deals whole tasks
+    over several GPUs (one host thread each); the result is in plan order either way.
     """
     isect._check_backend(backend)
-    m = _lib.MODE_NAMES.get(mode)
-    if m is None:
-        raise ConfigError(f"mode must be one of {sorted(_lib.MODE_NAMES)}, got {mode!r}")
-    halves = {}
+    m, p = isect._mode_pipeline(mode, pipeline)
+    devices = list(devices) if devices is not None else [device]
+    if not devices:
+        raise ConfigError("devices must be non-empty")
+    halves = _halves(u_mesh, s_mesh, plan)
+    costs = [halves[("u", n1, s1)].n_triangles * halves[("s", n2, s2)].n_triangles
+             for (n1, s1, n2, s2) in plan.tasks]
+    parts = assign_tasks(costs, len(devices))
 
-    def get(mesh, key, n, s):
-        if key not in halves:
-            h = half_layer(mesh, n, _sign(s))
-            halves[key] = (h, _device.DeviceMesh(np.ascontiguousarray(h.coords), device))
-        return halves[key]
+    def run(rank):
+        mine = parts[rank]
+        if not mine:
+            return [], b"", []
+        ctx = runtime.context(devices[rank])
+        meshes = {}
+        try:
+            jobs = []
+            for k in mine:
+                n1, s1, n2, s2 = plan.tasks[k]
+                for key in (("u", n1, s1), ("s", n2, s2)):
+                    if key not in meshes:
+                        h = halves[key]
+                        meshes[key] = ctx.mesh(np.ascontiguousarray(h.coords), h.s_values)
+                jobs.append((meshes[("u", n1, s1)], meshes[("s", n2, s2)], plan.tasks[k]))
+            return ctx.intersect(jobs, mode=m, pipeline=p, dedup=dedup, text=text,
+                                 task_ids=[plan.tasks[k] for k in mine])
+        finally:
+            for mesh in meshes.values():
+                mesh.free()
 
-    pairs, meta = [], []
-    for (n1, s1, n2, s2), tof in zip(plan.tasks, plan.tof):
-        hu, du = get(u_mesh, ("u", n1, s1), n1, s1)
-        hs, ds = get(s_mesh, ("s", n2, s2), n2, s2)
-        pairs.append((du, ds))
-        meta.append((hu, hs, (n1, s1, n2, s2), tof))
-    results = _device.search_batch(pairs, mode=m, task_ids=None)
-    records, stats = [], []
-    for res, (hu, hs, layer, tof) in zip(results, meta):
-        ca, cb = np.ascontiguousarray(hu.coords), np.ascontiguousarray(hs.coords)
-        gid, pts, params = _device.record_fields_device(ca, hu.s_values, cb, hs.s_values, res.hits, device=device)
-        records.extend(isect.assemble_records(ca, cb, res.hits, gid, pts, params, layer=layer, tof=tof,
-                                              dedup=dedup))
-        stats.append({"layer": layer, **res.stats})
-    return records, stats
+    outs = _device.run_on_devices(run, devices)
+    per_task = [None] * len(plan)
+    for rank, (recs, txt, stats) in enumerate(outs):
+        mine = parts[rank]
+        lines = txt.split(b"\n")[:-1] if txt else []
+        cut = np.searchsorted(recs["task"], np.arange(len(mine) + 1)) if len(recs) else np.zeros(len(mine) + 1, int)
+        for j, k in enumerate(mine):
+            seg = recs[cut[j]:cut[j + 1]]
+            body = b"".join(l + b"\n" for l in lines[cut[j]:cut[j + 1]]) if text else b""
+            per_task[k] = (seg, body, {"layer": plan.tasks[k], "device": devices[rank], **stats[j]})
+    records, stats, chunks = [], [], []
+    for k, (seg, body, st) in enumerate(per_task):
+        n1, s1, n2, s2 = plan.tasks[k]
+        hu, hs = halves[("u", n1, s1)], halves[("s", n2, s2)]
+        records.extend(isect.records_to_objects(seg, hu.N, hs.N, layer=plan.tasks[k], tof=plan.tof[k]))
+        stats.append(st)
+        chunks.append(body)
+    return PlanResult(records=records, stats=stats, text=b"".join(chunks))

@@ -142,16 +142,23 @@ def half_layer(mesh: ManifoldMesh, n: int, sign: int) -> HalfLayer:
 
     Unstable: s ∈ sign·[Dλ^(n−1), Dλ^n]; stable: s ∈ sign·[D/λ^(n−1), D/λ^n].
     Endpoints must be members of ``s_values`` within 1e-12 (layer boundaries are
-    grid members by construction, PAPER.md "Discrete Mesh").
+    grid members by construction, PAPER.md "Discrete Mesh").  ``n = 0`` is the
+    fundamental-domain core s ∈ [−D, D] (one half-layer, sign +), searched only
+    with ``--include-core`` (SPEC.md:398).
     """
-    if not (1 <= n <= mesh.n_max):
-        raise ConfigError(f"layer index n={n} out of range 1..{mesh.n_max}")
-    if sign not in (1, -1):
-        raise ConfigError(f"sign must be +1 or -1, got {sign}")
-    lam = mesh.lam if mesh.kind == "unstable" else 1.0 / mesh.lam
-    e0 = sign * mesh.D * lam ** (n - 1)
-    e1 = sign * mesh.D * lam ** n
-    lo, hi = min(e0, e1), max(e0, e1)
+    if n == 0:
+        if sign != 1:
+            raise ConfigError("the core (n = 0) is one half-layer, sign '+'")
+        lo, hi = -mesh.D, mesh.D
+    else:
+        if not (1 <= n <= mesh.n_max):
+            raise ConfigError(f"layer index n={n} out of range 1..{mesh.n_max}")
+        if sign not in (1, -1):
+            raise ConfigError(f"sign must be +1 or -1, got {sign}")
+        lam = mesh.lam if mesh.kind == "unstable" else 1.0 / mesh.lam
+        e0 = sign * mesh.D * lam ** (n - 1)
+        e1 = sign * mesh.D * lam ** n
+        lo, hi = min(e0, e1), max(e0, e1)
     s = mesh.s_values
     tol = 1e-12 * max(1.0, abs(hi))
     k_lo = int(np.argmin(np.abs(s - lo)))

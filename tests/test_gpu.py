@@ -44,14 +44,15 @@ def c1():
 
 
 @pytest.mark.parametrize("order", [_lib.ORDER_TILED, _lib.ORDER_NATURAL])
-@pytest.mark.parametrize("shape", [(64, 64), (37, 23), (5, 2), (1024, 3)])
+@pytest.mark.parametrize("shape", [(64, 64), (37, 23), (5, 2), (1024, 3), (33, 50)])
 def test_device_pack_bit_exact(order, shape):
-    """Every packed record equals the oracle's packing of its original triangle (tiled
-    order: via perm, which must be a bijection)."""
+    """Every packed box equals the oracle's box of its original triangle (tiled order:
+    via perm, which must be a bijection), and the level boxes written by the same
+    pass are the exact unions of their records."""
     A, _ = manifold_like(shape[0], shape[1], 1)
     m = D.DeviceMesh(A, 0, order=order)
     pk = O.pack(A)
-    box, geo = m.box.cpu().numpy(), m.geo.cpu().numpy()
+    box = m.box.cpu().numpy()
     if order == _lib.ORDER_TILED:
         perm = m.perm.cpu().numpy().astype(np.int64)
         assert np.array_equal(np.sort(perm), np.arange(m.n_tri))
@@ -59,16 +60,23 @@ def test_device_pack_bit_exact(order, shape):
         perm = np.arange(m.n_tri)
     pk = O.take(pk, perm)
     assert np.array_equal(_bits(box[:, :4]), _bits(pk["lo"])) and np.array_equal(_bits(box[:, 4:]), _bits(pk["hi"]))
-    for k, sl in (("p", slice(0, 4)), ("e1", slice(4, 8)), ("e2", slice(8, 12)), ("P", slice(12, 18))):
-        assert np.array_equal(_bits(geo[:, sl]), _bits(pk[k])), k
-    assert np.array_equal(_bits(geo[:, 18]), _bits(pk["nrm"]))
-    # level boxes are the exact unions of their records
-    gb = m.gbox.cpu().numpy()
-    for g in (0, len(gb) // 2, len(gb) - 1):
-        seg = box[g * 32:(g + 1) * 32]
-        assert np.array_equal(gb[g, :4], seg[:, :4].min(0)) and np.array_equal(gb[g, 4:], seg[:, 4:].max(0))
-    tb, bb = m.tbox.cpu().numpy(), m.bbox.cpu().numpy()
-    assert np.array_equal(tb[0, :4], box[:512, :4].min(0)) and np.array_equal(bb[-1, 4:], box[(len(bb) - 1) * 1024:, 4:].max(0))
+    n = m.n_tri
+    for lev, size in ((m.gbox, 32), (m.tbox, 512), (m.bbox, 1024)):
+        lb = lev.cpu().numpy()
+        assert len(lb) == -(-n // size)
+        for g in range(len(lb)):
+            seg = box[g * size:(g + 1) * size]
+            assert np.array_equal(lb[g, :4], seg[:, :4].min(0)) and np.array_equal(lb[g, 4:], seg[:, 4:].max(0))
+
+
+def test_tiled_pack_requires_perm():
+    A, _ = manifold_like(16, 5, 1)
+    t = D.torch()
+    c = t.from_numpy(A).cuda()
+    box = t.empty((2 * 16 * 4, 8), dtype=t.float64, device="cuda")
+    rc = _lib.load().mcx_pack(c.data_ptr(), 16, 5, _lib.ORDER_TILED, box.data_ptr(), None, None, None, None, None, 0,
+                              None)
+    assert rc == _lib.MCX_E_ARG and "perm" in _lib.last_error()
 
 
 def test_tiled_order_is_spatially_compact():
@@ -249,7 +257,7 @@ def test_multi_device_api_single_gpu():
 
 def test_find_intersections_records(oracle_lib):
     A, sa, B, sb = config_pair("C1")
-    recs = isect.find_intersections(A, B)
+    recs = isect.find_intersections(A, B, pipeline="triangle")
     ref = O.search(A, B)
     hits = np.zeros(len(ref["ia"]), dtype=D.HIT_DTYPE)
     for k in ("ia", "ib", "s", "t", "a", "b"):
@@ -342,25 +350,29 @@ def test_search_batch_sharded(mode):
         assert np.array_equal(D._merge([p[t] for p in parts]).hits, full[t].hits)
 
 
-@pytest.mark.parametrize("mode", ["cull", "brute", "prefilter"])
-def test_search_plan_matches_oracle(mode):
+@pytest.mark.parametrize("mode,pipeline", [("cull", "triangle"), ("brute", "triangle"), ("prefilter", "triangle"),
+                                           ("cull", "spec")])
+def test_search_plan_matches_oracle(mode, pipeline):
     from paper_2109_14814_b200 import layers
     from paper_2109_14814_b200.mesh import half_layer, layered_mesh
     u = layered_mesh(96, "unstable", 3, 1.6, 0.1, 1)
     s = layered_mesh(96, "stable", 3, 1 / 1.6, 0.1, 2)
     plan = layers.enumerate_layer_pairs(u, s, 3)
-    recs, stats = layers.search_plan(u, s, plan, mode=mode)
+    res = layers.search_plan(u, s, plan, mode=mode, pipeline=pipeline, text=True)
+    recs, stats = res
     want = []
     for (n1, s1, n2, s2), tof in zip(plan.tasks, plan.tof):
         hu, hs = half_layer(u, n1, 1 if s1 == "+" else -1), half_layer(s, n2, 1 if s2 == "+" else -1)
         ca, cb = np.ascontiguousarray(hu.coords), np.ascontiguousarray(hs.coords)
-        ref = O.search(ca, cb)
+        ref = O.search(ca, cb) if pipeline == "triangle" else S.find_intersections(ca, cb)
         h = np.zeros(len(ref["ia"]), dtype=D.HIT_DTYPE)
         for k in ("ia", "ib", "s", "t", "a", "b"):
             h[k] = ref[k]
         want.extend(isect.hits_to_records(ca, hu.s_values, cb, hs.s_values, h, layer=(n1, s1, n2, s2), tof=tof))
     assert [r.to_line() for r in recs] == [w.to_line() for w in want]
+    assert res.text == "".join(w.to_line() + "\n" for w in want).encode()  # device-formatted records file
     assert len(stats) == len(plan) == 20
+    assert len(want) > 0
 
 
 def test_cli_intersect(tmp_path):
@@ -377,12 +389,17 @@ def test_cli_intersect(tmp_path):
                      "--manifest", str(tmp_path / "m.json")]) == 0
     recs, _ = layers.search_plan(u, s, layers.read_plan(tmp_path / "plan.txt"))
     assert (tmp_path / "rec.txt").read_text().splitlines() == [r.to_line() for r in recs]
-    for mode in ("brute", "prefilter"):  # every search mode writes the identical records file
+    tri = None
+    for mode in ("cull", "brute", "prefilter"):  # every search mode writes the identical records file
         out = tmp_path / f"rec_{mode}.txt"
         assert cli.main(["intersect", "--umesh", str(tmp_path / "u.mnf"), "--smesh", str(tmp_path / "s.mnf"),
                          "--plan", str(tmp_path / "plan.txt"), "--backend", "cuda", "--out", str(out),
-                         "--mode", mode]) == 0
-        assert out.read_text() == (tmp_path / "rec.txt").read_text()
+                         "--mode", mode, "--pipeline", "triangle", "--devices", "0,0"]) == 0
+        tri = tri or out.read_text()
+        assert out.read_text() == tri
+    assert cli.main(["intersect", "--umesh", str(tmp_path / "u.mnf"), "--smesh", str(tmp_path / "s.mnf"),
+                     "--plan", str(tmp_path / "plan.txt"), "--backend", "cuda", "--out", str(tmp_path / "x"),
+                     "--mode", "brute"]) == 2  # the spec pipeline runs on the culling kernels only
 
 
 # ------------------------------------------------------------ device record fields (§8(f) row 4)
@@ -398,7 +415,7 @@ def test_device_record_fields_bit_exact(name):
 
 def test_find_intersections_device_records_equal_host():
     A, sa, B, sb = config_pair("C4ii")
-    recs = isect.find_intersections(A, B)
+    recs = isect.find_intersections(A, B, pipeline="triangle")
     hits = D.search(A, B).hits
     want = isect.hits_to_records(A, np.linspace(-1.0, 1.0, A.shape[1]), B, np.linspace(-1.0, 1.0, B.shape[1]), hits)
     assert [r.to_line() for r in recs] == [w.to_line() for w in want]
@@ -426,8 +443,10 @@ def test_c_host_example():
     subprocess.run(["make", "-s", "-C", d], check=True)
     out = subprocess.run([os.path.join(d, "mcx_example"), "200", "65"], capture_output=True, text=True, check=True)
     rows = [ln.split() for ln in out.stdout.strip().splitlines()]
-    assert [r[0] for r in rows] == ["brute", "cull", "prefilter"]
-    brute, cull, pre = rows
+    assert [r[0] for r in rows] == ["brute", "cull", "prefilter", "runtime"]
+    brute, cull, pre, rt = rows
+    assert rt[1] == rt[2] == brute[5] and rt[4] == brute[6]  # host runtime: same hits, one record each
+    assert int(rt[3]) > 0
     assert pre[1:7] == brute[1:7]
     assert brute[1] == cull[1]                      # logical pairs
     assert brute[2] == brute[1] and int(cull[2]) < int(cull[1])  # executed tests
@@ -606,3 +625,156 @@ def test_bench_json_contract():
         assert k in d["e2e"], k
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["gpu_launches"] > 0
     assert d["hits"] == d["cull"]["hits"] == 4
+
+
+# ------------------------------------------------------------ SPEC-literal pipeline on the GPU
+def _as_hits(ref):
+    h = np.zeros(len(ref["ia"]), dtype=D.HIT_DTYPE)
+    for k in ("ia", "ib", "s", "t", "a", "b"):
+        h[k] = ref[k]
+    return h
+
+
+@pytest.mark.parametrize("name", ["C1", "C4i", "C4ii", "C4iii", "C5/8", "C5/4"])
+def test_spec_pipeline_records_equal_serial_backend(name):
+    """find_intersections(pipeline="spec") on the GPU equals the SPEC-literal serial
+    backend (oracle/serial.py: quad AABB + Moller + 4 precise tests per survivor) record
+    for record, text byte for byte."""
+    A, sa, B, sb = config_pair(name)
+    want = isect.hits_to_records(A, sa, B, sb, _as_hits(S.find_intersections(A, B)))
+    from paper_2109_14814_b200 import runtime
+    recs, text, st = runtime.context(0).find(A, sa, B, sb, mode=_lib.MODE_CULL, pipeline=_lib.PIPE_SPEC, text=True)
+    got = isect.records_to_objects(recs, A.shape[2], B.shape[2])
+    assert [r.to_line() for r in got] == [w.to_line() for w in want]
+    assert text == "".join(w.to_line() + "\n" for w in want).encode()
+    gids, n_pass = S.pair_candidates(A, B)
+    assert st["n_candidates"] == len(gids) and st["n_aabb_pass"] == n_pass
+    assert [r.to_line() for r in isect.find_intersections(A, B)] == [w.to_line() for w in want]  # the default
+
+
+def test_spec_pipeline_acceptance_set():
+    """(N1, N2, M1, M2) = (32, 32, 9, 9) dyadic meshes (SPEC acceptance 6 sizes): spec pipeline
+    hits equal the serial backend's, and are a subset of the exact all-pairs answer."""
+    from oracle import exact as X
+    from paper_2109_14814_b200.mesh import dyadic
+    for seed in (5, 6):
+        A = dyadic(manifold_like(32, 9, seed)[0])
+        B = dyadic(manifold_like(32, 9, seed + 10)[0])
+        ref = S.find_intersections(A, B)
+        r = D.search(A, B, mode=_lib.MODE_CULL, pipeline=_lib.PIPE_SPEC)
+        assert_same_hits(ref, r.hits)
+        pA, pB = O.pack(A), O.pack(B)
+        for a, b in zip(r.hits["ia"], r.hits["ib"]):
+            sol = X.solve_exact(pA["p"][a], pA["e1"][a], pA["e2"][a], pB["p"][b], pB["e1"][b], pB["e2"][b])
+            assert X.accepted(sol)
+
+
+# ------------------------------------------------------------ device records pipeline (§8(f) row 4)
+@pytest.mark.parametrize("name", ["C1", "C4i", "C4ii", "C5/8"])
+@pytest.mark.parametrize("dedup", [True, False])
+def test_runtime_records_and_text_equal_host(name, dedup):
+    """Device records (fields, (gid, τ_A, τ_B) order, 1e-9 dedup) and the device-formatted
+    records text equal the host path (isect.hits_to_records + to_line) byte for byte."""
+    from paper_2109_14814_b200 import runtime
+    A, sa, B, sb = config_pair(name)
+    hits = D.search(A, B, mode=_lib.MODE_CULL).hits
+    want = isect.hits_to_records(A, sa, B, sb, hits, layer=(3, "-", 2, "+"), dedup=dedup)
+    recs, text, st = runtime.context(0).find(A, sa, B, sb, (3, "-", 2, "+"), mode=_lib.MODE_CULL,
+                                             pipeline=_lib.PIPE_TRIANGLE, dedup=dedup, text=True)
+    got = isect.records_to_objects(recs, A.shape[2], B.shape[2], layer=(3, "-", 2, "+"))
+    assert [r.to_line() for r in got] == [w.to_line() for w in want]
+    assert text == "".join(w.to_line() + "\n" for w in want).encode()
+    assert st["n_hits"] == len(hits)
+
+
+def test_runtime_batch_and_finish_hits():
+    """mcx_intersect over several resident jobs equals one find per job; mcx_finish_hits
+    (host hit list, e.g. gathered from several GPUs) equals find."""
+    from paper_2109_14814_b200 import runtime
+    ctx = runtime.context(0)
+    cfgs = [config_pair(n) for n in ("C1", "C4ii", "C5/8")]
+    meshes = [(ctx.mesh(A, sa), ctx.mesh(B, sb)) for A, sa, B, sb in cfgs]
+    layers_ = [(1, "+", 1, "-"), (2, "-", 1, "+"), (0, "+", 0, "+")]
+    jobs = [(ma, mb, L) for (ma, mb), L in zip(meshes, layers_)]
+    recs, text, stats = ctx.intersect(jobs, pipeline=_lib.PIPE_TRIANGLE, text=True)
+    parts, ptext = [], b""
+    for (A, sa, B, sb), L in zip(cfgs, layers_):
+        r, t, _ = ctx.find(A, sa, B, sb, L, pipeline=_lib.PIPE_TRIANGLE, text=True)
+        parts.append(r)
+        ptext += t
+    assert text == ptext
+    cat = np.concatenate(parts)
+    for f in ("gid", "ia", "ib"):
+        assert np.array_equal(recs[f], cat[f])
+    assert np.array_equal(recs["task"], np.repeat(np.arange(3), [len(p) for p in parts]))
+    A, sa, B, sb = cfgs[2]
+    hits = D.search(A, B, devices=(0, 0), mode=_lib.MODE_CULL).hits
+    r2, t2 = ctx.finish_hits(hits, meshes[2][0], meshes[2][1], layers_[2], text=True)
+    assert t2 == ctx.find(A, sa, B, sb, layers_[2], pipeline=_lib.PIPE_TRIANGLE, text=True)[1]
+    for ma, mb in meshes:
+        ma.free()
+        mb.free()
+
+
+@pytest.mark.slow
+def test_runtime_dense_records_equal_host():
+    """Dense cases: C5hd (13,226 hits) and a 512×257 mesh against itself (every triangle
+    touches its neighbours): device records and text equal the host path."""
+    from paper_2109_14814_b200 import runtime
+    for name in ("C5hd", "dense-self"):
+        if name == "C5hd":
+            A, sa, B, sb = config_pair("C5hd")
+        else:
+            A, sa = manifold_like(512, 257, 3)
+            B, sb = A, sa
+        hits = D.search(A, B, mode=_lib.MODE_CULL).hits
+        want = isect.hits_to_records(A, sa, B, sb, hits)
+        recs, text, _ = runtime.context(0).find(A, sa, B, sb, mode=_lib.MODE_CULL, pipeline=_lib.PIPE_TRIANGLE,
+                                                text=True)
+        assert text == "".join(w.to_line() + "\n" for w in want).encode(), name
+        assert len(recs) == len(want) and len(hits) > 10000
+
+
+def test_search_plan_multi_device_equals_single():
+    from paper_2109_14814_b200 import layers
+    from paper_2109_14814_b200.mesh import layered_mesh
+    u = layered_mesh(64, "unstable", 3, 1.6, 0.1, 1)
+    s = layered_mesh(64, "stable", 3, 1 / 1.6, 0.1, 2)
+    plan = layers.enumerate_layer_pairs(u, s, 3, include_core=True)
+    a = layers.search_plan(u, s, plan, text=True)
+    b = layers.search_plan(u, s, plan, devices=(0, 0, 0), text=True)
+    assert a.text == b.text and len(a.records) == len(b.records) > 0
+    assert [x["layer"] for x in b.stats] == plan.tasks
+
+
+def test_concurrent_host_threads_one_device():
+    """Two host threads searching concurrently on one device (contexts and workspaces are
+    per thread; SPEC.md:504 tasks run concurrently) get the single-thread results."""
+    import threading
+    A, sa, B, sb = config_pair("C4i")
+    ref = D.search(A, B, mode=_lib.MODE_CULL).hits
+    out = [None] * 4
+    from paper_2109_14814_b200 import runtime
+
+    def work(k):
+        if k % 2:
+            out[k] = D.search(A, B, mode=_lib.MODE_PREFILTER).hits
+        else:
+            out[k] = runtime.context(0).find(A, sa, B, sb, pipeline=_lib.PIPE_TRIANGLE, dedup=False)[0]
+    th = [threading.Thread(target=work, args=(k,)) for k in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for k in range(4):
+        o = out[k]
+        assert np.array_equal(np.sort(o["ia"].astype(np.int64) << 32 | o["ib"]), np.sort(ref["ia"].astype(np.int64) << 32 | ref["ib"]))
+
+
+def test_device_guard_preserves_current_device():
+    t = D.torch()
+    before = t.cuda.current_device()
+    A, sa, B, sb = config_pair("C1")
+    isect.find_intersections(A, B, devices=(0,))
+    D.search(A, B, devices=(0,))
+    assert t.cuda.current_device() == before

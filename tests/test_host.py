@@ -4,6 +4,7 @@ import ctypes
 import os
 import re
 import subprocess
+import sys
 
 import numpy as np
 import pytest
@@ -19,7 +20,7 @@ HEADER = os.path.join(ROOT, "include", "mcx.h")
 
 def _header_functions():
     txt = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:[a-z_0-9]+\s*\*?\s+)+\**(mcx_[a-z_]+)\s*\(", txt, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:[a-z_0-9]+\s*\*?\s+)+\**(mcx_[a-z_0-9]+)\s*\(", txt, re.M)))
 
 
 def test_library_exports_every_header_symbol():
@@ -28,24 +29,55 @@ def test_library_exports_every_header_symbol():
     assert set(funcs) == set(_lib.EXPORTS)
     for f in funcs:
         assert hasattr(L, f), f
-    assert L.mcx_version() == 2
+    assert L.mcx_version() == 3
     assert L.mcx_a_block() == 1024
     assert isinstance(L.mcx_last_error(), bytes)
 
 
+LAYOUT = [  # (C expression, ctypes value)
+    ("sizeof(mcx_mesh_dev)", ctypes.sizeof(_lib.MeshDev)), ("offsetof(mcx_mesh_dev, N)", _lib.MeshDev.N.offset),
+    ("offsetof(mcx_mesh_dev, box)", _lib.MeshDev.box.offset), ("offsetof(mcx_mesh_dev, status)", _lib.MeshDev.status.offset),
+    ("sizeof(mcx_hit)", ctypes.sizeof(_lib.Hit)), ("offsetof(mcx_hit, s)", _lib.Hit.s.offset),
+    ("sizeof(mcx_stats)", ctypes.sizeof(_lib.Stats)), ("offsetof(mcx_stats, n_candidates)", _lib.Stats.n_candidates.offset),
+    ("sizeof(mcx_opts)", ctypes.sizeof(_lib.Opts)), ("offsetof(mcx_opts, mode)", _lib.Opts.mode.offset),
+    ("offsetof(mcx_opts, workspace)", _lib.Opts.workspace.offset), ("offsetof(mcx_opts, pipeline)", _lib.Opts.pipeline.offset),
+    ("offsetof(mcx_opts, cand_cap)", _lib.Opts.cand_cap.offset),
+    ("sizeof(mcx_task)", ctypes.sizeof(_lib.Task)), ("sizeof(mcx_record)", ctypes.sizeof(_lib.Record)),
+    ("offsetof(mcx_record, point)", _lib.Record.point.offset), ("offsetof(mcx_record, params)", _lib.Record.params.offset),
+    ("offsetof(mcx_record, task)", _lib.Record.task.offset), ("sizeof(mcx_layer)", ctypes.sizeof(_lib.Layer)),
+    ("sizeof(mcx_job)", ctypes.sizeof(_lib.Job)), ("offsetof(mcx_job, layer)", _lib.Job.layer.offset),
+    ("sizeof(mcx_find_opts)", ctypes.sizeof(_lib.FindOpts)),
+    ("offsetof(mcx_find_opts, shard_count)", _lib.FindOpts.shard_count.offset),
+]
+
+
 def test_struct_layout_matches_header(tmp_path):
     src = tmp_path / "layout.c"
-    src.write_text(
-        '#include <stdio.h>\n#include <stddef.h>\n#include "mcx.h"\n'
-        "int main(void){printf(\"%zu %zu %zu %zu %zu %zu %zu\\n\", sizeof(mcx_mesh_dev), sizeof(mcx_hit),"
-        " sizeof(mcx_stats), sizeof(mcx_opts), offsetof(mcx_opts, mode), offsetof(mcx_opts, workspace),"
-        " offsetof(mcx_hit, s));return 0;}\n")
+    body = "".join(f'printf("%zu\\n", (size_t)({expr}));' for expr, _ in LAYOUT)
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "mcx.h"\nint main(void){' + body + "return 0;}\n")
     exe = tmp_path / "layout"
     subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)], check=True)
     got = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
-    want = [ctypes.sizeof(_lib.MeshDev), ctypes.sizeof(_lib.Hit), ctypes.sizeof(_lib.Stats), ctypes.sizeof(_lib.Opts),
-            _lib.Opts.mode.offset, _lib.Opts.workspace.offset, _lib.Hit.s.offset]
-    assert got == want
+    assert got == [v for _, v in LAYOUT]
+
+
+def test_device_formatter_matches_python_g17():
+    """mcx_format_g17 is the host build of the device records formatter (mcx_format.cuh):
+    it must print every double exactly like Python's f"{v:.17g}" (SPEC.md:507 records)."""
+    L = _lib.load()
+    rng = np.random.default_rng(7)
+    vals = [0.0, -0.0, np.inf, -np.inf, np.nan, 1e16, 1e17, 0.0001, 1e-5, 0.1, 2.0 ** 60, 5e-324,
+            1.7976931348623157e308, 1e-310, 6.283185307179586, 123456789012345650.0]
+    for e in range(-324, 309, 7):
+        x = float(f"1e{e}")
+        vals += [x, np.nextafter(x, 0.0), np.nextafter(x, np.inf)]
+    vals += list(rng.integers(0, 2 ** 64, size=20000, dtype=np.uint64).view(np.float64))
+    vals += list(rng.normal(size=20000)) + list(rng.uniform(0, 1, 20000))
+    buf = ctypes.create_string_buffer(64)
+    for v in vals:
+        n = L.mcx_format_g17(float(v), buf)
+        assert buf.value.decode() == f"{float(v):.17g}", repr(v)
+        assert n == len(buf.value)
 
 
 def test_only_cuda_backend():
@@ -69,11 +101,40 @@ def test_no_silent_cpu_fallback():
 def test_error_hierarchy_exit_codes():
     assert issubclass(errors.CapacityError, errors.BackendError)
     assert issubclass(errors.BackendError, errors.ManiconnError)
-    assert errors.ConfigError("x").exit_code == 2
-    assert errors.NumericsError("x").exit_code == 3
-    assert errors.FileFormatError("x").exit_code == 4
+    assert errors.exit_code(errors.ConfigError("x")) == 2
+    assert errors.exit_code(errors.NumericsError("x")) == 3
+    assert errors.exit_code(errors.SingularSystemError("x", condition=1e13)) == 3
+    assert errors.exit_code(errors.FileFormatError("x")) == 4
+    assert errors.exit_code(errors.BackendError("x")) == 3
     e = errors.BackendError("boom", task=(3, "+", 2, "-"), status=2)
     assert "layer pair (3, '+', 2, '-')" in str(e)
+
+
+REF_SRC = "/root/reference/pkg/src"
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_SRC), reason="reference sources not present (GPU box)")
+def test_errors_are_the_reference_classes_when_importable():
+    """With the reference package on the path, a reference caller's except clauses catch
+    this backend's errors: the shared classes ARE maniconn.errors' (errors.py:4-53)."""
+    code = (
+        "import maniconn.errors as R\n"
+        "from paper_2109_14814_b200 import errors as E, isect\n"
+        "assert E.REFERENCE_CLASSES\n"
+        "for n in ('ManiconnError', 'ConfigError', 'NumericsError', 'SingularSystemError', 'FileFormatError'):\n"
+        "    assert getattr(E, n) is getattr(R, n), n\n"
+        "assert issubclass(E.BackendError, R.ManiconnError) and issubclass(E.CapacityError, R.ManiconnError)\n"
+        "import numpy as np\n"
+        "try:\n"
+        "    isect.find_intersections(np.zeros((4, 3, 8)), np.zeros((4, 3, 8)), backend='serial')\n"
+        "except R.ConfigError:\n"
+        "    pass\n"
+        "else:\n"
+        "    raise SystemExit('not caught')\n"
+        "print('ok')\n")
+    env = dict(os.environ, PYTHONPATH=os.pathsep.join([REF_SRC, ROOT, os.environ.get("PYTHONPATH", "")]))
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, cwd=ROOT)
+    assert out.returncode == 0 and out.stdout.strip() == "ok", out.stderr
 
 
 def _mesh():

@@ -2,11 +2,14 @@
  * Minimal C host for the C ABI (include/mcx.h): no Python, no torch.
  *
  * Builds a synthetic pair of half-layer grids on the host, uploads them with
- * cudaMalloc/cudaMemcpy, packs them on the device (mcx_pack + mcx_levels), runs
- * the search in both modes (mcx_search) and prints one line per mode:
- *   mode n_pairs n_tested n_aabb_pass n_singular n_hits checksum
+ * cudaMalloc/cudaMemcpy, packs them on the device (mcx_pack), runs the search in
+ * every mode (mcx_search) and prints one line per mode:
+ *   mode n_pairs n_tested n_aabb_pass n_singular n_hits checksum kernel_ms
  * The checksum is an order-independent sum over hits of (ia * 1000003 + ib), so the
- * two modes must print the same hit count and checksum.
+ * modes must print the same hit count and checksum.  Then the host-to-host runtime
+ * (mcx_context_create + mcx_find_intersections from the host grids) prints
+ *   runtime n_hits n_records text_bytes checksum
+ * with the same checksum over the (deduplicated) records' triangle pairs.
  *
  * Build (tools/c_example/Makefile): gcc + libcudart + libmcx.so.
  */
@@ -50,7 +53,7 @@ static void grid(double* c, uint32_t N, uint32_t M, double phase) {
 }
 
 typedef struct {
-  double *coords, *box, *geo, *gbox, *tbox, *bbox;
+  double *coords, *box, *gbox, *tbox, *bbox;
   uint32_t *perm, *status;
   mcx_mesh_dev dev;
 } mesh_t;
@@ -60,17 +63,17 @@ static void upload(mesh_t* m, const double* host, uint32_t N, uint32_t M) {
   CK(cudaMalloc((void**)&m->coords, sizeof(double) * 4 * N * M));
   CK(cudaMemcpy(m->coords, host, sizeof(double) * 4 * N * M, cudaMemcpyHostToDevice));
   CK(cudaMalloc((void**)&m->box, sizeof(double) * MCX_BOX_STRIDE * n));
-  CK(cudaMalloc((void**)&m->geo, sizeof(double) * MCX_GEO_STRIDE * n));
   CK(cudaMalloc((void**)&m->perm, sizeof(uint32_t) * n));
   CK(cudaMalloc((void**)&m->status, sizeof(uint32_t)));
   CK(cudaMalloc((void**)&m->gbox, sizeof(double) * 8 * ((n + MCX_GROUP - 1) / MCX_GROUP)));
   CK(cudaMalloc((void**)&m->tbox, sizeof(double) * 8 * ((n + MCX_TILE - 1) / MCX_TILE)));
   CK(cudaMalloc((void**)&m->bbox, sizeof(double) * 8 * ((n + MCX_BLOCK - 1) / MCX_BLOCK)));
-  MK(mcx_pack(m->coords, N, M, MCX_ORDER_TILED, m->box, m->geo, m->perm, m->status, 0, NULL));
-  MK(mcx_levels(m->box, n, m->gbox, m->tbox, m->bbox, 0, NULL));
+  MK(mcx_pack(m->coords, N, M, MCX_ORDER_TILED, m->box, m->perm, m->gbox, m->tbox, m->bbox, m->status, 0, NULL));
   m->dev.n_tri = n;
+  m->dev.coords = m->coords;
+  m->dev.N = N;
+  m->dev.M = M;
   m->dev.box = m->box;
-  m->dev.geo = m->geo;
   m->dev.perm = m->perm;
   m->dev.gbox = m->gbox;
   m->dev.tbox = m->tbox;
@@ -114,5 +117,22 @@ int main(int argc, char** argv) {
            (unsigned long long)st.n_hits, sum, st.kernel_ms);
     CK(cudaFree(o.workspace));
   }
+  /* the host-to-host runtime: host grids in, records + records text out */
+  double* sv = (double*)malloc(sizeof(double) * M);
+  for (uint32_t k = 0; k < M; ++k) sv[k] = -1.0 + 2.0 * k / (M - 1);
+  mcx_context* ctx = NULL;
+  MK(mcx_context_create(0, &ctx));
+  mcx_find_opts fo = {MCX_MODE_CULL, MCX_PIPE_TRIANGLE, 0, 1, 0, 0}; /* no dedup: one record per hit */
+  mcx_layer layer = {1, 1, 1, -1};
+  const mcx_record* recs = NULL;
+  const char* text = NULL;
+  uint64_t n_recs = 0, n_text = 0;
+  mcx_stats st;
+  MK(mcx_find_intersections(ctx, ha, N, M, sv, hb, N, M, sv, layer, &fo, &recs, &n_recs, &text, &n_text, &st));
+  unsigned long long sum = 0;
+  for (uint64_t r = 0; r < n_recs; ++r) sum += (unsigned long long)recs[r].ia * 1000003ull + recs[r].ib;
+  printf("runtime %llu %llu %llu %llu\n", (unsigned long long)st.n_hits, (unsigned long long)n_recs,
+         (unsigned long long)n_text, sum);
+  MK(mcx_context_destroy(ctx));
   return 0;
 }
