@@ -215,42 +215,35 @@ MCX_HD int fmt_g17(double v, char* o) {
 }
 
 // One records-file line: "n1 sign1 n2 sign2 gid x y px py a b c d
-// theta_u s_u theta_s s_s\n" — the 12 doubles with fmt_g17.  o == nullptr: length only.
+// theta_u s_u theta_s s_s\n" — the 12 doubles with fmt_g17.  Each field is formatted
+// into a local buffer and then copied to o (o == nullptr: length only); writing the
+// fields straight through a pointer that may be local or global lost the stores in
+// device code, so the two address spaces never mix here.
 MCX_HD int fmt_record_line(char* o, int n1, int sign1, int n2, int sign2, uint64_t gid, const double* point,
                            const double* bary, const double* params) {
-  char tmp[48];
-  char* w = o ? o : tmp;
+  char f[32];
   int n = 0;
-  auto put_int = [&](int x) {
-    char* dst = o ? w + n : tmp;
-    int k = 0;
-    if (x < 0) {
-      dst[k++] = '-';
-      x = -x;
+  for (int field = 0; field < 17; ++field) {
+    int k;
+    if (field == 0 || field == 2) {
+      const int x = field == 0 ? n1 : n2;
+      k = 0;
+      if (x < 0) f[k++] = '-';
+      k += put_u64(f + k, (uint64_t)(x < 0 ? -(int64_t)x : x));
+    } else if (field == 1 || field == 3) {
+      f[0] = (field == 1 ? sign1 : sign2) >= 0 ? '+' : '-';
+      k = 1;
+    } else if (field == 4) {
+      k = put_u64(f, gid);
+    } else {
+      const int c = field - 5;
+      k = fmt_g17(c < 4 ? point[c] : (c < 8 ? bary[c - 4] : params[c - 8]), f);
     }
-    k += put_u64(dst + k, (uint64_t)x);
+    f[k++] = field == 16 ? '\n' : ' ';
+    if (o)
+      for (int i = 0; i < k; ++i) o[n + i] = f[i];
     n += k;
-  };
-  auto put_ch = [&](char c) {
-    if (o) w[n] = c;
-    ++n;
-  };
-  put_int(n1);
-  put_ch(' ');
-  put_ch(sign1 >= 0 ? '+' : '-');
-  put_ch(' ');
-  put_int(n2);
-  put_ch(' ');
-  put_ch(sign2 >= 0 ? '+' : '-');
-  put_ch(' ');
-  n += put_u64(o ? w + n : tmp, gid);
-  const double* src[3] = {point, bary, params};
-  for (int f = 0; f < 3; ++f)
-    for (int c = 0; c < 4; ++c) {
-      put_ch(' ');
-      n += fmt_g17(src[f][c], o ? w + n : tmp);
-    }
-  put_ch('\n');
+  }
   return n;
 }
 
