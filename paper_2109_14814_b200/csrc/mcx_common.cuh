@@ -5,6 +5,7 @@
 #include <stdarg.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <string.h>
 
 #include "../../include/mcx.h"
 
@@ -92,6 +93,36 @@ struct DeviceGuard {
       return ::mcx::set_error(MCX_E_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #expr,          \
                               cudaGetErrorString(_e));                                        \
   } while (0)
+
+// Pinned host staging for the small table uploads of a search.  A pageable source
+// makes cudaMemcpyAsync stage the copy and wait for the stream's earlier work, which
+// serialises the host with the GPU on a latency-critical path; the host runtime
+// (mcx_runtime.cu) installs a context-owned pinned buffer for the duration of a call.
+struct HostStage {
+  char* p = nullptr;
+  size_t cap = 0, used = 0;
+};
+extern thread_local HostStage* g_stage;
+
+struct StageScope {
+  HostStage* prev;
+  explicit StageScope(HostStage* s) : prev(g_stage) {
+    if (s) s->used = 0;
+    g_stage = s;
+  }
+  ~StageScope() { g_stage = prev; }
+};
+
+inline cudaError_t h2d_async(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  HostStage* st = g_stage;
+  if (st && st->p && st->used + bytes <= st->cap) {
+    char* q = st->p + st->used;
+    memcpy(q, src, bytes);
+    st->used += (bytes + 15) & ~(size_t)15;
+    return cudaMemcpyAsync(dst, q, bytes, cudaMemcpyHostToDevice, s);
+  }
+  return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
+}
 
 // ------------------------------------------------------- mbarrier + bulk copy
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

@@ -8,9 +8,11 @@
 
 namespace mcx {
 
-// mcx_pack.cu: the fused pack + levels kernel, enqueued on `stream` (device current).
+// mcx_pack.cu: the fused pack + levels kernel over 1024-record blocks [b0, b1) (b1 = 0:
+// all), enqueued on `stream` (device current); pack_blocks = the block count.
+uint64_t pack_blocks(uint32_t N, uint32_t M);
 int pack_enqueue(const double* coords, uint32_t N, uint32_t M, int order, double* box, uint32_t* perm, double* gbox,
-                 double* tbox, double* bbox, uint32_t* status, cudaStream_t stream);
+                 double* tbox, double* bbox, uint32_t* status, cudaStream_t stream, uint64_t b0, uint64_t b1);
 
 // mcx_search.cu: a batch of searches (device current); synchronises o->stream.
 int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mcx_hit* hits, uint32_t* hit_task,

@@ -33,18 +33,18 @@ struct PackSmem {
   Box gsm[A_BLOCK / GROUP];
 };
 
-__global__ void __launch_bounds__(PACK_THREADS) pack_kernel(const double* __restrict__ coords, uint32_t N,
-                                                            uint32_t M, int tiled, Box* __restrict__ box,
-                                                            uint32_t* __restrict__ perm, Box* __restrict__ gbox,
-                                                            Box* __restrict__ tbox, Box* __restrict__ bbox,
-                                                            uint32_t* __restrict__ status) {
+__global__ void __launch_bounds__(PACK_THREADS, 3) pack_kernel(const double* __restrict__ coords, uint32_t N,
+                                                               uint32_t M, int tiled, Box* __restrict__ box,
+                                                               uint32_t* __restrict__ perm, Box* __restrict__ gbox,
+                                                               Box* __restrict__ tbox, Box* __restrict__ bbox,
+                                                               uint32_t* __restrict__ status, uint32_t blk0) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   PackSmem& S = *reinterpret_cast<PackSmem*>(smem_raw);
   const uint32_t MQ = M - 1;
   const uint64_t nq = (uint64_t)N * MQ;
   const uint64_t n = 2 * nq;
   const int tid = threadIdx.x, lane = tid & 31;
-  const uint64_t blk = blockIdx.x;
+  const uint64_t blk = blk0 + blockIdx.x;
   const uint64_t sq = blk * PACK_THREADS + tid;  // storage quad of this thread
   const bool valid = sq < nq;
   bool bad = false;
@@ -63,21 +63,33 @@ __global__ void __launch_bounds__(PACK_THREADS) pack_kernel(const double* __rest
       k = (uint32_t)(sq / N);
     }
     const uint32_t t0 = 2 * (i + N * k);
+    // the quad's 4 vertices once (16 loads, all issued before use): T¹ = (v00, v10,
+    // v01), T² = (v01, v10, v11) — the vertex sets of tri_verts, −0.0 canonicalised
+    const uint32_t ip = (i + 1 == N) ? 0 : i + 1;
+    const uint64_t r0 = (uint64_t)k * N, r1 = r0 + N, plane = (uint64_t)M * N;
+    double w00[4], w10[4], w01[4], w11[4];
 #pragma unroll
-    for (int tau = 0; tau < 2; ++tau) {
-      double v0[4], v1[4], v2[4];
-      tri_verts(coords, N, M, t0 + tau, v0, v1, v2);
-      Box b;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        bad |= !(isfinite(v0[c]) && isfinite(v1[c]) && isfinite(v2[c]));
-        b.lo[c] = fmin(fmin(v0[c], v1[c]), v2[c]);
-        b.hi[c] = fmax(fmax(v0[c], v1[c]), v2[c]);
-        qlo[c] = fmin(qlo[c], b.lo[c]);
-        qhi[c] = fmax(qhi[c], b.hi[c]);
-      }
-      S.box[2 * tid + tau] = b;
+    for (int c = 0; c < 4; ++c) {
+      const double* pl = coords + c * plane;
+      w00[c] = __ldg(pl + r0 + i);
+      w10[c] = __ldg(pl + r0 + ip);
+      w01[c] = __ldg(pl + r1 + i);
+      w11[c] = __ldg(pl + r1 + ip);
     }
+    Box b1, b2;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const double a = dadd(w00[c], 0.0), b = dadd(w10[c], 0.0), d = dadd(w01[c], 0.0), e = dadd(w11[c], 0.0);
+      bad |= !(isfinite(a) && isfinite(b) && isfinite(d) && isfinite(e));
+      b1.lo[c] = fmin(fmin(a, b), d);
+      b1.hi[c] = fmax(fmax(a, b), d);
+      b2.lo[c] = fmin(fmin(d, b), e);
+      b2.hi[c] = fmax(fmax(d, b), e);
+      qlo[c] = fmin(b1.lo[c], b2.lo[c]);
+      qhi[c] = fmax(b1.hi[c], b2.hi[c]);
+    }
+    S.box[2 * tid] = b1;
+    S.box[2 * tid + 1] = b2;
     if (perm) reinterpret_cast<uint2*>(perm)[sq] = make_uint2(t0, t0 + 1);
   }
   if (status && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status, 1u);
@@ -187,9 +199,12 @@ __global__ void __launch_bounds__(256) levels_kernel(const Box* __restrict__ box
   }
 }
 
-// Enqueue the fused pack on `stream` (device already current).
+uint64_t pack_blocks(uint32_t N, uint32_t M) { return (2ull * N * (M - 1) + A_BLOCK - 1) / A_BLOCK; }
+
+// Enqueue the fused pack of blocks [b0, b1) (b1 = 0: all) on `stream` (device already
+// current).  The status flag is cleared by the launch that starts at block 0.
 int pack_enqueue(const double* coords, uint32_t N, uint32_t M, int order, double* box, uint32_t* perm, double* gbox,
-                 double* tbox, double* bbox, uint32_t* status, cudaStream_t stream) {
+                 double* tbox, double* bbox, uint32_t* status, cudaStream_t stream, uint64_t b0, uint64_t b1) {
   if (N < 1 || M < 2) return set_error(MCX_E_ARG, "pack needs N >= 1 and M >= 2 (got N=%u, M=%u)", N, M);
   if (2ull * N * (M - 1) >= (1ull << 31)) return set_error(MCX_E_ARG, "triangle count must be < 2^31");
   if (order != MCX_ORDER_NATURAL && order != MCX_ORDER_TILED) return set_error(MCX_E_ARG, "unknown order %d", order);
@@ -201,14 +216,16 @@ int pack_enqueue(const double* coords, uint32_t N, uint32_t M, int order, double
   if (perm && ((uintptr_t)perm & 7)) return set_error(MCX_E_ARG, "perm must be 8-byte aligned");
   if ((gbox != nullptr) != (tbox != nullptr) || (gbox != nullptr) != (bbox != nullptr))
     return set_error(MCX_E_ARG, "gbox, tbox and bbox must be given together");
-  const uint64_t n = 2ull * N * (M - 1);
-  const uint64_t nblk = (n + A_BLOCK - 1) / A_BLOCK;
+  const uint64_t nblk = pack_blocks(N, M);
+  if (b1 == 0 || b1 > nblk) b1 = nblk;
+  if (b0 >= b1) return MCX_OK;
   static_assert(sizeof(PackSmem) <= 227 * 1024, "pack smem");
   CUDA_TRY(cudaFuncSetAttribute(pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PackSmem)));
-  if (status) CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(uint32_t), stream));
-  pack_kernel<<<(unsigned)nblk, PACK_THREADS, sizeof(PackSmem), stream>>>(
+  CUDA_TRY(cudaFuncSetAttribute(pack_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  if (status && b0 == 0) CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(uint32_t), stream));
+  pack_kernel<<<(unsigned)(b1 - b0), PACK_THREADS, sizeof(PackSmem), stream>>>(
       coords, N, M, order == MCX_ORDER_TILED, reinterpret_cast<Box*>(box), perm, reinterpret_cast<Box*>(gbox),
-      reinterpret_cast<Box*>(tbox), reinterpret_cast<Box*>(bbox), status);
+      reinterpret_cast<Box*>(tbox), reinterpret_cast<Box*>(bbox), status, (uint32_t)b0);
   CUDA_TRY(cudaGetLastError());
   return MCX_OK;
 }
@@ -222,7 +239,7 @@ int mcx_pack(const double* coords, uint32_t N, uint32_t M, int order, double* bo
   using namespace mcx;
   DeviceGuard guard;
   CUDA_TRY(cudaSetDevice(device));
-  return pack_enqueue(coords, N, M, order, box, perm, gbox, tbox, bbox, status, (cudaStream_t)stream);
+  return pack_enqueue(coords, N, M, order, box, perm, gbox, tbox, bbox, status, (cudaStream_t)stream, 0, 0);
 }
 
 int mcx_levels(const double* box, uint64_t n_tri, double* gbox, double* tbox, double* bbox, int device,

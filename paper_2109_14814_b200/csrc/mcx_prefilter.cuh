@@ -348,7 +348,7 @@ static int launch_local_cfg(std::vector<SearchParams>& T, Batch& Bt, std::vector
   Bt.neg1 = 0xffffffffu;
   Bt.fjobs = reinterpret_cast<const FboxJob*>(dev_jobs);
   Bt.n_fjobs = (uint32_t)jobs.size();
-  CUDA_TRY(cudaMemcpyAsync(dev_jobs, jobs.data(), sizeof(FboxJob) * jobs.size(), cudaMemcpyHostToDevice, stream));
+  CUDA_TRY(h2d_async(dev_jobs, jobs.data(), sizeof(FboxJob) * jobs.size(), stream));
   uint64_t max_records = 0;
   for (const FboxJob& j : jobs) max_records = std::max<uint64_t>(max_records, j.n);
   const unsigned n = (unsigned)jobs.size();

@@ -76,6 +76,7 @@ struct mcx_context {
   mcx::DevBuf ws, hits, hit_task, jobs, k0, k1, v0, v1, recs, recs_out, state, blocked, pairs, lens, offs, cub,
       text, small;
   mcx::HostBuf h_recs, h_text, h_small;
+  mcx::HostStage stage;  // pinned staging of the per-call tables
   uint64_t cand_cap = MCX_DEFAULT_CAND_CAP, hit_cap = 1 << 16, pair_cap = 1 << 12;
 };
 
@@ -257,6 +258,180 @@ __global__ void line_write_kernel(const mcx_record* __restrict__ recs, const uin
   }
 }
 
+// ------------------------------------------------------------------ small hit counts
+// Steps 2-6 in ONE single-CTA kernel for n ≤ SMALL_N hits (the common case: a handful
+// to a few hundred intersections per layer pair): bitonic sort of the (job, gid, τ_A,
+// τ_B) keys in shared memory, records, the 1e-9 dedup (all earlier records of the job
+// scanned; ≤ SMALL_K close predecessors each, else the general path reruns it), the
+// greedy rule resolved in rounds, and block-scan compaction of records and text.
+// Keys are unique ((gid, τ) ↔ (iA, iB) within a job), so sort stability is moot.
+constexpr int SMALL_N = 1024;
+constexpr int SMALL_K = 8;
+constexpr int REC_LINE_MAX = 352;  // ≥ the longest records line (349 bytes)
+
+struct SmallOut {
+  unsigned long long kept, text_bytes, overflow;
+};
+
+// exclusive block prefix sum of v over 1024 threads (returns the total in *tot)
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* warp_sums, uint32_t* tot) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sums[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = warp_sums[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    warp_sums[lane] = w;  // inclusive over warps
+  }
+  __syncthreads();
+  const uint32_t base = warp ? warp_sums[warp - 1] : 0u;
+  *tot = warp_sums[31];
+  __syncthreads();
+  return base + x - v;
+}
+
+__global__ void __launch_bounds__(1024) post_small_kernel(const mcx_hit* __restrict__ hits,
+                                                          const uint32_t* __restrict__ hit_task, uint32_t n,
+                                                          const JobDev* __restrict__ jobs, int gid_shift, int dedup,
+                                                          int want_text, mcx_record* __restrict__ recs,
+                                                          mcx_record* __restrict__ out, char* __restrict__ text,
+                                                          SmallOut* __restrict__ res) {
+  __shared__ unsigned long long key[SMALL_N];
+  __shared__ uint16_t idx[SMALL_N];
+  __shared__ uint16_t nb[SMALL_N][SMALL_K];
+  __shared__ uint8_t nnb[SMALL_N], state[SMALL_N];
+  __shared__ uint32_t warp_sums[32];
+  __shared__ int overflow;
+  const int tid = threadIdx.x;
+  uint32_t P = 1;
+  while (P < n) P <<= 1;
+  if (tid == 0) overflow = 0;
+  for (uint32_t k = tid; k < P; k += blockDim.x) {
+    unsigned long long kk = ~0ull;
+    if (k < n) {
+      const mcx_hit H = hits[k];
+      const uint32_t t = hit_task ? hit_task[k] : 0u;
+      const JobDev& J = jobs[t];
+      const uint32_t qa = H.ia >> 1, qb = H.ib >> 1;
+      const uint64_t i = qa % J.NA, k1 = qa / J.NA, j = qb % J.NB, l1 = qb / J.NB;
+      const uint64_t n12 = (uint64_t)J.NA * J.NB;
+      const uint64_t gid = i + (uint64_t)J.NA * j + n12 * k1 + n12 * (uint64_t)(J.MA - 1) * l1;
+      kk = ((unsigned long long)t << gid_shift) | gid << 2 | (uint64_t)(H.ia & 1) << 1 | (H.ib & 1);
+    }
+    key[k] = kk;
+    idx[k] = (uint16_t)k;
+  }
+  __syncthreads();
+  for (uint32_t k = 2; k <= P; k <<= 1)
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = tid; i < P; i += blockDim.x) {
+        const uint32_t l = i ^ j;
+        if (l > i) {
+          const bool up = (i & k) == 0;
+          if ((key[i] > key[l]) == up) {
+            const unsigned long long tk = key[i];
+            key[i] = key[l];
+            key[l] = tk;
+            const uint16_t ti = idx[i];
+            idx[i] = idx[l];
+            idx[l] = ti;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  const uint32_t r = tid;  // one record per thread (n ≤ 1024 = blockDim)
+  const bool valid = r < n;
+  if (valid) {
+    const uint32_t k = idx[r];
+    const mcx_hit H = hits[k];
+    const uint32_t t = hit_task ? hit_task[k] : 0u;
+    const JobDev& J = jobs[t];
+    mcx_record R;
+    record_fields(H, J.cA, J.NA, J.MA, J.sA, J.NB, J.MB, J.sB, R.gid, R.point, R.params);
+    R.ia = H.ia;
+    R.ib = H.ib;
+    R.bary[0] = H.s; R.bary[1] = H.t; R.bary[2] = H.a; R.bary[3] = H.b;
+    R.task = t;
+    R.pad[0] = R.pad[1] = R.pad[2] = 0;
+    recs[r] = R;
+  }
+  __syncthreads();  // records visible (global, L1 of this SM)
+  // dedup: close predecessors of r within its job (records of a job are contiguous)
+  uint8_t cnt = 0;
+  if (valid && dedup) {
+    const mcx_record& R = recs[r];
+    for (int e = (int)r - 1; e >= 0; --e) {
+      const mcx_record& E = recs[e];
+      if (E.task != R.task) break;
+      if (fabs(dsub(R.point[0], E.point[0])) <= MCX_DEDUP_TOL && fabs(dsub(R.point[1], E.point[1])) <= MCX_DEDUP_TOL &&
+          fabs(dsub(R.point[2], E.point[2])) <= MCX_DEDUP_TOL && fabs(dsub(R.point[3], E.point[3])) <= MCX_DEDUP_TOL) {
+        if (cnt < SMALL_K) nb[r][cnt] = (uint16_t)e;
+        ++cnt;
+      }
+    }
+    if (cnt > SMALL_K) overflow = 1;
+  }
+  if (valid) {
+    nnb[r] = cnt;
+    state[r] = cnt ? 0 : 1;
+  }
+  __syncthreads();
+  if (overflow) {
+    if (tid == 0) res->overflow = 1;
+    return;
+  }
+  if (dedup) {
+    for (;;) {  // decisions are monotone, so racing reads only delay them
+      bool left = false;
+      if (valid && state[r] == 0) {
+        bool kept_pred = false, all_dropped = true;
+        for (int q = 0; q < nnb[r]; ++q) {
+          const uint8_t st = state[nb[r][q]];
+          kept_pred |= st == 1;
+          all_dropped &= st == 2;
+        }
+        if (kept_pred) state[r] = 2;
+        else if (all_dropped) state[r] = 1;
+        else left = true;
+      }
+      if (!__syncthreads_or(left)) break;
+    }
+  }
+  const bool keep = valid && state[r] == 1;
+  uint32_t total;
+  const uint32_t pos = block_excl_scan(keep ? 1u : 0u, warp_sums, &total);
+  if (keep) out[pos] = recs[r];
+  uint32_t len = 0;
+  if (keep && want_text) {
+    const mcx_record& R = recs[r];
+    const JobDev& J = jobs[R.task];
+    len = (uint32_t)fmt::fmt_record_line(nullptr, J.n1, J.sign1, J.n2, J.sign2, R.gid, R.point, R.bary, R.params);
+  }
+  uint32_t tbytes = 0;
+  const uint32_t off = block_excl_scan(len, warp_sums, &tbytes);
+  if (len) {
+    const mcx_record& R = recs[r];
+    const JobDev& J = jobs[R.task];
+    fmt::fmt_record_line(text + off, J.n1, J.sign1, J.n2, J.sign2, R.gid, R.point, R.bary, R.params);
+  }
+  if (tid == 0) {
+    res->kept = total;
+    res->text_bytes = tbytes;
+    res->overflow = 0;
+  }
+}
+
 static unsigned grid_of(uint64_t n) {
   uint64_t b = (n + 255) / 256;
   return (unsigned)std::min<uint64_t>(std::max<uint64_t>(b, 1), 148ull * 16);
@@ -275,9 +450,45 @@ static int postprocess(mcx_context* c, uint64_t n, const uint32_t* hit_task, con
   if (n > 0xffffffffull) return set_error(MCX_E_ARG, "more than 2^32 hits in one call");
   int rc = ensure(c, c->jobs, sizeof(JobDev) * jobs.size(), s);
   if (rc) return rc;
-  CUDA_TRY(cudaMemcpyAsync(c->jobs.p, jobs.data(), sizeof(JobDev) * jobs.size(), cudaMemcpyHostToDevice, s));
+  CUDA_TRY(h2d_async(c->jobs.p, jobs.data(), sizeof(JobDev) * jobs.size(), s));
   const JobDev* J = (const JobDev*)c->jobs.p;
   const mcx_hit* H = (const mcx_hit*)c->hits.p;
+  {
+    uint64_t mg = 0;
+    for (const JobDev& j : jobs) mg = std::max<uint64_t>(mg, (uint64_t)j.NA * (j.MA - 1) * j.NB * (j.MB - 1));
+    const int shift = bits_for(mg) + 2, tb = std::max(1, bits_for(jobs.size() - 1));
+    if (n <= (uint64_t)SMALL_N && shift + tb <= 64) {
+      const bool want_text = fo->text && text && text_bytes;
+      if ((rc = ensure(c, c->recs, sizeof(mcx_record) * n, s)) ||
+          (rc = ensure(c, c->recs_out, sizeof(mcx_record) * n, s)) || (rc = ensure(c, c->small, 64, s)) ||
+          (want_text && (rc = ensure(c, c->text, (size_t)REC_LINE_MAX * n, s))) ||
+          (rc = ensure_host(c->h_recs, sizeof(mcx_record) * n)) || (rc = ensure_host(c->h_small, 64)) ||
+          (want_text && (rc = ensure_host(c->h_text, (size_t)REC_LINE_MAX * n + 1))))
+        return rc;
+      post_small_kernel<<<1, 1024, 0, s>>>(H, hit_task, (uint32_t)n, J, shift, fo->dedup ? 1 : 0, want_text ? 1 : 0,
+                                           (mcx_record*)c->recs.p, (mcx_record*)c->recs_out.p, (char*)c->text.p,
+                                           (SmallOut*)c->small.p);
+      CUDA_TRY(cudaGetLastError());
+      // upper-bound copies: no sync needed to learn the exact sizes first
+      CUDA_TRY(cudaMemcpyAsync(c->h_small.p, c->small.p, sizeof(SmallOut), cudaMemcpyDeviceToHost, s));
+      CUDA_TRY(cudaMemcpyAsync(c->h_recs.p, c->recs_out.p, sizeof(mcx_record) * n, cudaMemcpyDeviceToHost, s));
+      if (want_text)
+        CUDA_TRY(cudaMemcpyAsync(c->h_text.p, c->text.p, (size_t)REC_LINE_MAX * n, cudaMemcpyDeviceToHost, s));
+      CUDA_TRY(cudaStreamSynchronize(s));
+      const SmallOut* so = (const SmallOut*)c->h_small.p;
+      if (!so->overflow) {
+        *records = (const mcx_record*)c->h_recs.p;
+        *n_records = so->kept;
+        if (want_text) {
+          ((char*)c->h_text.p)[so->text_bytes] = 0;
+          *text = (const char*)c->h_text.p;
+          *text_bytes = so->text_bytes;
+        }
+        return MCX_OK;
+      }
+      // more than SMALL_K close predecessors somewhere: the general path below
+    }
+  }
   if ((rc = ensure(c, c->k0, 8 * n, s)) || (rc = ensure(c, c->k1, 8 * n, s)) || (rc = ensure(c, c->v0, 4 * n, s)) ||
       (rc = ensure(c, c->v1, 4 * n, s)) || (rc = ensure(c, c->recs, sizeof(mcx_record) * n, s)) ||
       (rc = ensure(c, c->recs_out, sizeof(mcx_record) * n, s)) || (rc = ensure(c, c->state, n, s)) ||
@@ -436,6 +647,11 @@ static int intersect(mcx_context* c, const mcx_job* jobs, uint32_t n_jobs, const
   int rc = check_find_opts(fo);
   if (rc) return rc;
   if (!jobs || n_jobs == 0 || !records || !n_records || !stats) return set_error(MCX_E_ARG, "null argument");
+  if (!c->stage.p) {
+    CUDA_TRY(cudaMallocHost((void**)&c->stage.p, 1 << 20));
+    c->stage.cap = 1 << 20;
+  }
+  StageScope scope(&c->stage);
   std::vector<mcx_task> tasks(n_jobs);
   std::vector<JobDev> jd(n_jobs);
   for (uint32_t t = 0; t < n_jobs; ++t) {
@@ -501,13 +717,30 @@ static int load_mesh(mcx_context* c, const double* coords, uint32_t N, uint32_t 
     mcx_mesh_free(m);
     return rc;
   }
-  cudaError_t e = cudaMemcpyAsync(m->coords, coords, 32ull * N * M, cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(m->s_values, s_values, 8ull * M, cudaMemcpyHostToDevice, s);
-  if (e != cudaSuccess) {
-    mcx_mesh_free(m);
-    return set_error(MCX_E_CUDA, "mesh upload: %s", cudaGetErrorString(e));
+  cudaError_t e = cudaMemcpyAsync(m->s_values, s_values, 8ull * M, cudaMemcpyHostToDevice, s);
+  // Upload and pack pipelined over chunks of whole 16-column tile rows: the blocks of
+  // the tile rows a chunk completes are packed while the next chunk is copied, so only
+  // the last chunk's packing follows the last byte of the H2D copy.
+  const uint32_t MQ = M - 1, ntr = (MQ + ORDER_TILE_Q - 1) / ORDER_TILE_Q;
+  const uint64_t nblk = pack_blocks(N, M), plane = (uint64_t)N * M * 8;
+  const uint32_t nch = n >= (1u << 18) ? std::min<uint32_t>(4, ntr) : 1;
+  uint64_t b_done = 0;
+  uint32_t col_done = 0;
+  for (uint32_t j = 0; j < nch && e == cudaSuccess && rc == MCX_OK; ++j) {
+    const bool last = j + 1 == nch;
+    const uint32_t tr1 = (uint32_t)((uint64_t)ntr * (j + 1) / nch);
+    const uint32_t col1 = last ? M : std::min<uint32_t>(M, ORDER_TILE_Q * tr1 + 1);
+    if (col1 > col_done)
+      e = cudaMemcpy2DAsync(m->coords + (uint64_t)col_done * N, plane, coords + (uint64_t)col_done * N, plane,
+                            (uint64_t)(col1 - col_done) * N * 8, 4, cudaMemcpyHostToDevice, s);
+    const uint64_t b1 = last ? nblk : 2ull * N * std::min<uint32_t>(MQ, ORDER_TILE_Q * tr1) / A_BLOCK;
+    if (e == cudaSuccess && b1 > b_done)  // (b1 = 0 would mean "all blocks" to pack_enqueue)
+      rc = pack_enqueue(m->coords, N, M, MCX_ORDER_TILED, m->box, m->perm, m->gbox, m->tbox, m->bbox, m->status, s,
+                        b_done, b1);
+    b_done = std::max(b_done, b1);
+    col_done = col1;
   }
-  rc = pack_enqueue(m->coords, N, M, MCX_ORDER_TILED, m->box, m->perm, m->gbox, m->tbox, m->bbox, m->status, s);
+  if (e != cudaSuccess) rc = set_error(MCX_E_CUDA, "mesh upload: %s", cudaGetErrorString(e));
   if (rc) {
     mcx_mesh_free(m);
     return rc;
@@ -562,6 +795,7 @@ int mcx_context_destroy(mcx_context* c) {
   }
   for (HostBuf* b : {&c->h_recs, &c->h_text, &c->h_small})
     if (b->p) cudaFreeHost(b->p);
+  if (c->stage.p) cudaFreeHost(c->stage.p);
   if (c->ev) cudaEventDestroy(c->ev);
   if (c->s0) cudaStreamDestroy(c->s0);
   if (c->s1) cudaStreamDestroy(c->s1);

@@ -439,9 +439,8 @@ static int launch_cull(std::vector<SearchParams>& T, Batch& Bt, std::vector<uint
   for (size_t t = 0; t < T.size(); ++t) prefix[t + 1] = prefix[t] + T[t].my_blocks * (T[t].nB ? T[t].ntilesB : 0);
   const uint64_t total = prefix.back();
   const size_t tab = sizeof(SearchParams) * T.size();
-  CUDA_TRY(cudaMemcpyAsync(dev_tab, T.data(), tab, cudaMemcpyHostToDevice, stream));
-  CUDA_TRY(cudaMemcpyAsync((char*)dev_tab + tab, prefix.data(), sizeof(uint64_t) * prefix.size(),
-                           cudaMemcpyHostToDevice, stream));
+  CUDA_TRY(h2d_async(dev_tab, T.data(), tab, stream));
+  CUDA_TRY(h2d_async((char*)dev_tab + tab, prefix.data(), sizeof(uint64_t) * prefix.size(), stream));
   if (total == 0) return MCX_OK;
   Bt.tasks = reinterpret_cast<const SearchParams*>(dev_tab);
   Bt.prefix = reinterpret_cast<const uint64_t*>((char*)dev_tab + tab);
@@ -880,6 +879,7 @@ static int launch_pair_candidates_mesh(const mcx_mesh_dev* A, const mcx_mesh_dev
 }
 
 thread_local char g_err[512] = "";
+thread_local HostStage* g_stage = nullptr;
 
 }  // namespace mcx
 

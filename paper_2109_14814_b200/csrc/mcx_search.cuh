@@ -284,9 +284,8 @@ static int upload_plan(std::vector<SearchParams>& T, Batch& Bt, std::vector<uint
   }
   *total = prefix.back();
   const size_t tab = sizeof(SearchParams) * T.size();
-  CUDA_TRY(cudaMemcpyAsync(dev_tab, T.data(), tab, cudaMemcpyHostToDevice, stream));
-  CUDA_TRY(cudaMemcpyAsync((char*)dev_tab + tab, prefix.data(), sizeof(uint64_t) * prefix.size(),
-                           cudaMemcpyHostToDevice, stream));
+  CUDA_TRY(h2d_async(dev_tab, T.data(), tab, stream));
+  CUDA_TRY(h2d_async((char*)dev_tab + tab, prefix.data(), sizeof(uint64_t) * prefix.size(), stream));
   if (*total > 0x7fffffffull) return set_error(MCX_E_ARG, "grid too large");
   Bt.tasks = reinterpret_cast<const SearchParams*>(dev_tab);
   Bt.prefix = reinterpret_cast<const uint64_t*>((char*)dev_tab + tab);
