@@ -107,6 +107,18 @@ MCX_HD uint32_t pow10u(int k) {  // k in [0, 9]
 
 // round-half-even(|v| · 10^k) for finite v = m·2^e2 (m > 0)
 MCX_HD uint64_t scaled_round(uint64_t m, int e2, int k) {
+  // Fast path in 128-bit registers for the usual magnitudes (2m·10^k and its shift fit):
+  // no local-memory big integer.  Same exact arithmetic, so the same digits.
+  if (k >= 0 && k <= 22 && e2 > -127 && e2 <= 0) {
+    unsigned __int128 q = (unsigned __int128)(2 * m);
+    for (int r = 0; r < k; ++r) q *= 10u;  // 2m·10^k < 2^54 · 10^22 < 2^128
+    const int sh = -e2;
+    const bool sticky = sh && (q & (((unsigned __int128)1 << sh) - 1)) != 0;
+    q >>= sh;
+    uint64_t d = (uint64_t)(q >> 1);
+    if (((uint64_t)q & 1) && (sticky || (d & 1))) ++d;
+    return d;
+  }
   Big N;
   big_set(N, m);
   big_shl(N, 1);  // one extra bit: the half
@@ -214,32 +226,38 @@ MCX_HD int fmt_g17(double v, char* o) {
   return n;
 }
 
-// One records-file line: "n1 sign1 n2 sign2 gid x y px py a b c d
-// theta_u s_u theta_s s_s\n" — the 12 doubles with fmt_g17.  Each field is formatted
-// into a local buffer and then copied to o (o == nullptr: length only); writing the
-// fields straight through a pointer that may be local or global lost the stores in
-// device code, so the two address spaces never mix here.
+// Field f (0..16) of a records-file line: n1 sign1 n2 sign2 gid x y px
+// py a b c d theta_u s_u theta_s s_s, written to o (≤ 24 bytes, no separator).
+MCX_HD int fmt_field(char* o, int f, int n1, int sign1, int n2, int sign2, uint64_t gid, const double* point,
+                     const double* bary, const double* params) {
+  if (f == 0 || f == 2) {
+    const int x = f == 0 ? n1 : n2;
+    int k = 0;
+    if (x < 0) o[k++] = '-';
+    return k + put_u64(o + k, (uint64_t)(x < 0 ? -(int64_t)x : x));
+  }
+  if (f == 1 || f == 3) {
+    o[0] = (f == 1 ? sign1 : sign2) >= 0 ? '+' : '-';
+    return 1;
+  }
+  if (f == 4) return put_u64(o, gid);
+  const int c = f - 5;
+  return fmt_g17(c < 4 ? point[c] : (c < 8 ? bary[c - 4] : params[c - 8]), o);
+}
+
+constexpr int LINE_FIELDS = 17;
+
+// One records-file line: the 17 fields separated by ' ' and ended by '\n'.  Each field
+// is formatted into a local buffer and then copied to o (o == nullptr: length only);
+// writing the fields straight through a pointer that may be local or global lost the
+// stores in device code, so the two address spaces never mix here.
 MCX_HD int fmt_record_line(char* o, int n1, int sign1, int n2, int sign2, uint64_t gid, const double* point,
                            const double* bary, const double* params) {
   char f[32];
   int n = 0;
-  for (int field = 0; field < 17; ++field) {
-    int k;
-    if (field == 0 || field == 2) {
-      const int x = field == 0 ? n1 : n2;
-      k = 0;
-      if (x < 0) f[k++] = '-';
-      k += put_u64(f + k, (uint64_t)(x < 0 ? -(int64_t)x : x));
-    } else if (field == 1 || field == 3) {
-      f[0] = (field == 1 ? sign1 : sign2) >= 0 ? '+' : '-';
-      k = 1;
-    } else if (field == 4) {
-      k = put_u64(f, gid);
-    } else {
-      const int c = field - 5;
-      k = fmt_g17(c < 4 ? point[c] : (c < 8 ? bary[c - 4] : params[c - 8]), f);
-    }
-    f[k++] = field == 16 ? '\n' : ' ';
+  for (int field = 0; field < LINE_FIELDS; ++field) {
+    int k = fmt_field(f, field, n1, sign1, n2, sign2, gid, point, bary, params);
+    f[k++] = field == LINE_FIELDS - 1 ? '\n' : ' ';
     if (o)
       for (int i = 0; i < k; ++i) o[n + i] = f[i];
     n += k;

@@ -14,8 +14,12 @@ uint64_t pack_blocks(uint32_t N, uint32_t M);
 int pack_enqueue(const double* coords, uint32_t N, uint32_t M, int order, double* box, uint32_t* perm, double* gbox,
                  double* tbox, double* bbox, uint32_t* status, cudaStream_t stream, uint64_t b0, uint64_t b1);
 
-// mcx_search.cu: a batch of searches (device current); synchronises o->stream.
+// mcx_search.cu: a batch of searches (device current).  h_counters == nullptr:
+// synchronises o->stream and fills the stats.  Otherwise the workspace header (8 + 8·n
+// u64s) is copied to h_counters (pinned) asynchronously, only stats[t].n_pairs is set,
+// and the caller synchronises and calls batch_stats (requires o->timing == 0).
 int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mcx_hit* hits, uint32_t* hit_task,
-                 uint64_t cap, mcx_stats* st);
+                 uint64_t cap, mcx_stats* st, unsigned long long* h_counters);
+int batch_stats(const unsigned long long* h, uint32_t n, const mcx_opts* o, uint64_t cap, mcx_stats* st, float ms);
 
 }  // namespace mcx

@@ -31,7 +31,11 @@
 #include <stdint.h>
 #include <string.h>
 
+#include <stdio.h>
+#include <stdlib.h>
+
 #include <algorithm>
+#include <chrono>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
@@ -74,8 +78,9 @@ struct mcx_context {
   cudaEvent_t ev = nullptr;
   cudaMemPool_t pool = nullptr;
   mcx::DevBuf ws, hits, hit_task, jobs, k0, k1, v0, v1, recs, recs_out, state, blocked, pairs, lens, offs, cub,
-      text, small;
-  mcx::HostBuf h_recs, h_text, h_small;
+      text, small, flen;
+  mcx::HostBuf h_recs, h_text, h_small, h_counters;
+  mcx::HostBuf h_map;    // mapped pinned memory the small-path kernel writes its results to
   mcx::HostStage stage;  // pinned staging of the per-call tables
   uint64_t cand_cap = MCX_DEFAULT_CAND_CAP, hit_cap = 1 << 16, pair_cap = 1 << 12;
 };
@@ -117,6 +122,19 @@ static void release(mcx_context* c, DevBuf& b, cudaStream_t s) {
   b.bytes = 0;
 }
 
+// MCX_TRACE=1: host timestamps of the runtime's stages on stderr (latency breakdown).
+static bool trace_on() {
+  static const bool on = getenv("MCX_TRACE") && atoi(getenv("MCX_TRACE")) > 0;
+  return on;
+}
+static void trace(const char* what) {
+  if (!trace_on()) return;
+  static thread_local std::chrono::steady_clock::time_point t0;
+  const auto now = std::chrono::steady_clock::now();
+  if (!strcmp(what, "begin")) t0 = now;
+  fprintf(stderr, "[mcx] %8.1f us  %s\n", std::chrono::duration<double, std::micro>(now - t0).count(), what);
+}
+
 static int bits_for(uint64_t v) {  // bits to represent every value in [0, v]
   int b = 0;
   while (b < 64 && (v >> b)) ++b;
@@ -124,6 +142,12 @@ static int bits_for(uint64_t v) {  // bits to represent every value in [0, v]
 }
 
 // ------------------------------------------------------------------ kernels
+// Order-preserving 64-bit key of a double (−0.0 just below +0.0).
+__device__ __forceinline__ uint64_t ordered_key(double x) {
+  const uint64_t u = __double_as_longlong(x);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+
 // 2. sort key of hit k: gid << 2 | τ_A << 1 | τ_B (job sorted in a second, stable pass)
 __global__ void key_kernel(const mcx_hit* __restrict__ hits, const uint32_t* __restrict__ hit_task, uint64_t n,
                            const JobDev* __restrict__ jobs, uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
@@ -164,8 +188,7 @@ __global__ void record_kernel(const mcx_hit* __restrict__ hits, const uint32_t* 
     R.pad[0] = R.pad[1] = R.pad[2] = 0;
     recs[r] = R;
     if (xkeys) {
-      uint64_t u = __double_as_longlong(R.point[0]);
-      xkeys[r] = (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+      xkeys[r] = ordered_key(R.point[0]);
       xvals[r] = (uint32_t)r;
     }
   }
@@ -177,21 +200,26 @@ __global__ void xtask_key_kernel(const uint32_t* __restrict__ xorder, const mcx_
     keys[p] = recs[xorder[p]].task;
 }
 
-// 5a. close pairs: from each position of the (job, x)-sorted order, scan forward while
-// the job matches and fl(x' − x) ≤ tol (monotone in the scan); test the other 3 coords.
-__global__ void close_pairs_kernel(const uint32_t* __restrict__ xorder, const mcx_record* __restrict__ recs,
-                                   uint64_t n, uint2* __restrict__ pairs, uint64_t cap,
-                                   unsigned long long* __restrict__ count, uint8_t* __restrict__ state) {
+// 5a. close pairs.  The records are in (job, x-bucket) order, the bucket being the top 32
+// bits of ordered_key(x) (relative width 2^-20; a 4-pass sort instead of 8).  From each
+// position scan forward while the job matches and the bucket does not exceed that of
+// fl(x + 2·tol) ≥ x + tol: every record within tol of x, before or after it in x, lies
+// in that range, so each close pair is found from its earlier position.  The exact test
+// is |fl(p − q)| ≤ tol in all 4 coordinates.  The count keeps running past cap.
+__global__ void close_pairs_kernel(const uint32_t* __restrict__ xorder, const uint64_t* __restrict__ xkeys,
+                                   const mcx_record* __restrict__ recs, uint64_t n, uint2* __restrict__ pairs,
+                                   uint64_t cap, unsigned long long* __restrict__ count, uint8_t* __restrict__ state) {
   for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n; p += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t r = xorder[p];
     const mcx_record& R = recs[r];
+    const uint64_t hi = ordered_key(dadd(R.point[0], 2.0 * MCX_DEDUP_TOL)) >> 32;
     for (uint64_t q = p + 1; q < n; ++q) {
+      if ((xkeys[q] >> 32) > hi) break;
       const uint32_t r2 = xorder[q];
       const mcx_record& S = recs[r2];
       if (S.task != R.task) break;
-      if (!(fabs(dsub(S.point[0], R.point[0])) <= MCX_DEDUP_TOL)) break;
-      if (fabs(dsub(S.point[1], R.point[1])) <= MCX_DEDUP_TOL && fabs(dsub(S.point[2], R.point[2])) <= MCX_DEDUP_TOL &&
-          fabs(dsub(S.point[3], R.point[3])) <= MCX_DEDUP_TOL) {
+      if (fabs(dsub(S.point[0], R.point[0])) <= MCX_DEDUP_TOL && fabs(dsub(S.point[1], R.point[1])) <= MCX_DEDUP_TOL &&
+          fabs(dsub(S.point[2], R.point[2])) <= MCX_DEDUP_TOL && fabs(dsub(S.point[3], R.point[3])) <= MCX_DEDUP_TOL) {
         const uint32_t e = min(r, r2), l = max(r, r2);
         const unsigned long long pos = atomicAdd(count, 1ull);
         if (pos < cap) pairs[pos] = make_uint2(e, l);
@@ -202,59 +230,88 @@ __global__ void close_pairs_kernel(const uint32_t* __restrict__ xorder, const mc
 }
 
 // 5b. greedy resolution in rounds (one CTA; close pairs are few).  state: 1 kept,
-// 2 dropped, 0 undecided.
-__global__ void __launch_bounds__(1024) resolve_kernel(const uint2* __restrict__ pairs, uint64_t np,
-                                                       uint8_t* __restrict__ state, uint8_t* __restrict__ blocked) {
-  for (int round = 0;; ++round) {
-    for (uint64_t k = threadIdx.x; k < np; k += blockDim.x) {  // a kept predecessor drops it
+// 2 dropped, 0 undecided.  Per round, one pass over the pairs marks "a kept
+// predecessor" (drop) and "an undecided predecessor" (wait) per record, one more
+// decides: drop, keep (all predecessors dropped) or wait.
+__global__ void __launch_bounds__(1024) resolve_kernel(const uint2* __restrict__ pairs,
+                                                       const unsigned long long* __restrict__ np_dev, uint64_t cap,
+                                                       uint8_t* __restrict__ state, uint8_t* __restrict__ mark) {
+  // an overflowed pair list leaves undecided records without stored pairs: the host
+  // sees the count, grows the list and reruns, so do nothing here
+  if ((uint64_t)*np_dev > cap) return;
+  const uint64_t np = *np_dev;
+  for (;;) {
+    for (uint64_t k = threadIdx.x; k < np; k += blockDim.x) {
       const uint2 e = pairs[k];
-      if (state[e.y] == 0 && state[e.x] == 1) state[e.y] = 2;
-    }
-    __syncthreads();
-    for (uint64_t k = threadIdx.x; k < np; k += blockDim.x) {  // an undecided predecessor blocks it
-      const uint2 e = pairs[k];
-      if (state[e.y] == 0 && state[e.x] != 2) blocked[e.y] = 1;
+      if (state[e.y] == 0) {
+        const uint8_t se = state[e.x];
+        if (se == 1) mark[e.y] |= 1;       // a kept predecessor: drop
+        else if (se == 0) mark[e.y] |= 2;  // an undecided predecessor: wait
+      }
     }
     __syncthreads();
     bool left = false;
-    for (uint64_t k = threadIdx.x; k < np; k += blockDim.x) {  // all predecessors dropped: keep
-      const uint2 e = pairs[k];
-      if (state[e.y] == 0 && !blocked[e.y]) state[e.y] = 1;
+    for (uint64_t k = threadIdx.x; k < np; k += blockDim.x) {
+      const uint32_t l = pairs[k].y;
+      const uint8_t m = mark[l];
+      if (state[l] == 0) {
+        if (m & 1) state[l] = 2;
+        else if (!(m & 2)) state[l] = 1;
+        else left = true;
+      }
     }
     __syncthreads();
-    for (uint64_t k = threadIdx.x; k < np; k += blockDim.x) {
-      const uint2 e = pairs[k];
-      blocked[e.y] = 0;
-      left |= state[e.y] == 0;
-    }
+    for (uint64_t k = threadIdx.x; k < np; k += blockDim.x) mark[pairs[k].y] = 0;
     if (!__syncthreads_or(left)) break;
   }
 }
 
-// 6. text lengths of the kept records (0 for dropped ones), then the text itself
-__global__ void line_len_kernel(const mcx_record* __restrict__ recs, const uint8_t* __restrict__ state, uint64_t n,
-                                const JobDev* __restrict__ jobs, uint32_t* __restrict__ lens,
-                                uint8_t* __restrict__ flags) {
+// 6. text, one thread per (record, field): field lengths; line lengths (0 for dropped
+// records) and keep flags; then every field written at its offset after the scan.
+__global__ void field_len_kernel(const mcx_record* __restrict__ recs, const uint8_t* __restrict__ state, uint64_t n,
+                                 const JobDev* __restrict__ jobs, uint8_t* __restrict__ flen) {
+  constexpr int F = fmt::LINE_FIELDS;
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < n * F; q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = q / F;
+    if (state && state[r] != 1) continue;
+    const mcx_record& R = recs[r];
+    const JobDev& J = jobs[R.task];
+    char f[32];
+    flen[q] = (uint8_t)fmt::fmt_field(f, (int)(q % F), J.n1, J.sign1, J.n2, J.sign2, R.gid, R.point, R.bary, R.params);
+  }
+}
+
+__global__ void line_len_kernel(const uint8_t* __restrict__ state, uint64_t n, const uint8_t* __restrict__ flen,
+                                uint32_t* __restrict__ lens, uint8_t* __restrict__ flags) {
+  constexpr int F = fmt::LINE_FIELDS;
   for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n; r += (uint64_t)gridDim.x * blockDim.x) {
     const bool keep = !state || state[r] == 1;
     flags[r] = keep;
     if (!lens) continue;
-    const mcx_record& R = recs[r];
-    const JobDev& J = jobs[R.task];
-    lens[r] = keep ? (uint32_t)fmt::fmt_record_line(nullptr, J.n1, J.sign1, J.n2, J.sign2, R.gid, R.point, R.bary,
-                                                    R.params)
-                   : 0u;
+    uint32_t len = 0;
+    if (keep)
+      for (int f = 0; f < F; ++f) len += flen[r * F + f] + 1u;
+    lens[r] = len;
   }
 }
 
-__global__ void line_write_kernel(const mcx_record* __restrict__ recs, const uint8_t* __restrict__ flags, uint64_t n,
-                                  const JobDev* __restrict__ jobs, const uint64_t* __restrict__ incl,
-                                  const uint32_t* __restrict__ lens, char* __restrict__ text) {
-  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n; r += (uint64_t)gridDim.x * blockDim.x) {
+__global__ void field_write_kernel(const mcx_record* __restrict__ recs, const uint8_t* __restrict__ flags, uint64_t n,
+                                   const JobDev* __restrict__ jobs, const uint64_t* __restrict__ incl,
+                                   const uint32_t* __restrict__ lens, const uint8_t* __restrict__ flen,
+                                   char* __restrict__ text) {
+  constexpr int F = fmt::LINE_FIELDS;
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < n * F; q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = q / F;
+    const int f = (int)(q % F);
     if (!flags[r]) continue;
+    uint64_t o = incl[r] - lens[r];
+    for (int g = 0; g < f; ++g) o += flen[r * F + g] + 1u;
     const mcx_record& R = recs[r];
     const JobDev& J = jobs[R.task];
-    fmt::fmt_record_line(text + (incl[r] - lens[r]), J.n1, J.sign1, J.n2, J.sign2, R.gid, R.point, R.bary, R.params);
+    char buf[32];
+    int k = fmt::fmt_field(buf, f, J.n1, J.sign1, J.n2, J.sign2, R.gid, R.point, R.bary, R.params);
+    buf[k++] = f == F - 1 ? '\n' : ' ';
+    for (int i = 0; i < k; ++i) text[o + i] = buf[i];
   }
 }
 
@@ -300,19 +357,49 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* warp_s
   return base + x - v;
 }
 
+struct SmallSmem {
+  unsigned long long key[SMALL_N];
+  uint16_t idx[SMALL_N];
+  uint16_t nb[SMALL_N][SMALL_K];
+  uint8_t nnb[SMALL_N], state[SMALL_N];
+  uint16_t kept_rec[SMALL_N];                       // kept position → record
+  uint32_t line_off[SMALL_N];                       // kept position → text offset
+  uint8_t flen[SMALL_N * fmt::LINE_FIELDS];          // field lengths (text)
+  uint32_t warp_sums[32];
+  int overflow;
+};
+
+// n = min(*n_dev, n_cap) is read on the device (the search's hit counter), so the
+// kernel can follow the search without a host round trip; more than SMALL_N hits sets
+// res->overflow = 2 and the host runs the general path.  Results (SmallOut, records,
+// text) go straight to mapped host memory with coalesced 16-byte stores.
 __global__ void __launch_bounds__(1024) post_small_kernel(const mcx_hit* __restrict__ hits,
-                                                          const uint32_t* __restrict__ hit_task, uint32_t n,
-                                                          const JobDev* __restrict__ jobs, int gid_shift, int dedup,
-                                                          int want_text, mcx_record* __restrict__ recs,
-                                                          mcx_record* __restrict__ out, char* __restrict__ text,
-                                                          SmallOut* __restrict__ res) {
-  __shared__ unsigned long long key[SMALL_N];
-  __shared__ uint16_t idx[SMALL_N];
-  __shared__ uint16_t nb[SMALL_N][SMALL_K];
-  __shared__ uint8_t nnb[SMALL_N], state[SMALL_N];
-  __shared__ uint32_t warp_sums[32];
-  __shared__ int overflow;
+                                                          const uint32_t* __restrict__ hit_task,
+                                                          const unsigned long long* __restrict__ n_dev,
+                                                          uint64_t n_cap, const JobDev* __restrict__ jobs,
+                                                          int gid_shift, int dedup, int want_text,
+                                                          mcx_record* __restrict__ recs, mcx_record* __restrict__ out,
+                                                          char* __restrict__ text, SmallOut* __restrict__ res,
+                                                          mcx_record* __restrict__ h_out, char* __restrict__ h_text) {
+  extern __shared__ __align__(16) unsigned char small_raw[];
+  SmallSmem& S = *reinterpret_cast<SmallSmem*>(small_raw);
+  unsigned long long* key = S.key;
+  uint16_t* idx = S.idx;
+  auto& nb = S.nb;
+  uint8_t* nnb = S.nnb;
+  uint8_t* state = S.state;
+  uint32_t* warp_sums = S.warp_sums;
+  int& overflow = S.overflow;
   const int tid = threadIdx.x;
+  const uint64_t n64 = min((uint64_t)*n_dev, n_cap);
+  if (n64 > (uint64_t)SMALL_N) {
+    if (tid == 0) {
+      res->kept = res->text_bytes = 0;
+      res->overflow = 2;
+    }
+    return;
+  }
+  const uint32_t n = (uint32_t)n64;
   uint32_t P = 1;
   while (P < n) P <<= 1;
   if (tid == 0) overflow = 0;
@@ -388,7 +475,10 @@ __global__ void __launch_bounds__(1024) post_small_kernel(const mcx_hit* __restr
   }
   __syncthreads();
   if (overflow) {
-    if (tid == 0) res->overflow = 1;
+    if (tid == 0) {
+      res->kept = res->text_bytes = 0;
+      res->overflow = 1;
+    }
     return;
   }
   if (dedup) {
@@ -411,25 +501,137 @@ __global__ void __launch_bounds__(1024) post_small_kernel(const mcx_hit* __restr
   const bool keep = valid && state[r] == 1;
   uint32_t total;
   const uint32_t pos = block_excl_scan(keep ? 1u : 0u, warp_sums, &total);
-  if (keep) out[pos] = recs[r];
-  uint32_t len = 0;
-  if (keep && want_text) {
-    const mcx_record& R = recs[r];
-    const JobDev& J = jobs[R.task];
-    len = (uint32_t)fmt::fmt_record_line(nullptr, J.n1, J.sign1, J.n2, J.sign2, R.gid, R.point, R.bary, R.params);
+  if (keep) {
+    out[pos] = recs[r];
+    S.kept_rec[pos] = (uint16_t)r;
   }
+  __syncthreads();
+  // text: one thread per (kept record, field) — field lengths, line offsets (block scan),
+  // then every field written at its offset; the exact conversions run side by side
+  constexpr int F = fmt::LINE_FIELDS;
   uint32_t tbytes = 0;
-  const uint32_t off = block_excl_scan(len, warp_sums, &tbytes);
-  if (len) {
-    const mcx_record& R = recs[r];
-    const JobDev& J = jobs[R.task];
-    fmt::fmt_record_line(text + off, J.n1, J.sign1, J.n2, J.sign2, R.gid, R.point, R.bary, R.params);
+  if (want_text) {
+    for (uint32_t q = tid; q < total * F; q += blockDim.x) {
+      const mcx_record& R = recs[S.kept_rec[q / F]];
+      const JobDev& J = jobs[R.task];
+      char f[32];
+      S.flen[q] = (uint8_t)fmt::fmt_field(f, (int)(q % F), J.n1, J.sign1, J.n2, J.sign2, R.gid, R.point, R.bary,
+                                          R.params);
+    }
+    __syncthreads();
+    uint32_t len = 0;
+    if (tid < total)
+      for (int f = 0; f < F; ++f) len += S.flen[tid * F + f] + 1u;  // + separator
+    const uint32_t off = block_excl_scan(len, warp_sums, &tbytes);
+    if (tid < total) S.line_off[tid] = off;
+    __syncthreads();
+    for (uint32_t q = tid; q < total * F; q += blockDim.x) {
+      const uint32_t p = q / F, f = q % F;
+      uint32_t o = S.line_off[p];
+      for (uint32_t g = 0; g < f; ++g) o += S.flen[p * F + g] + 1u;
+      const mcx_record& R = recs[S.kept_rec[p]];
+      const JobDev& J = jobs[R.task];
+      char buf[32];
+      int k = fmt::fmt_field(buf, (int)f, J.n1, J.sign1, J.n2, J.sign2, R.gid, R.point, R.bary, R.params);
+      buf[k++] = f == F - 1 ? '\n' : ' ';
+      for (int i = 0; i < k; ++i) text[o + i] = buf[i];
+    }
+  }
+  __syncthreads();
+  // coalesced copy-out to the mapped host buffers
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(out);
+    uint4* dst = reinterpret_cast<uint4*>(h_out);
+    for (uint32_t q = tid; q < total * (sizeof(mcx_record) / 16); q += blockDim.x) dst[q] = src[q];
+    const uint32_t t16 = tbytes / 16;
+    const uint4* ts = reinterpret_cast<const uint4*>(text);
+    uint4* td = reinterpret_cast<uint4*>(h_text);
+    for (uint32_t q = tid; q < t16; q += blockDim.x) td[q] = ts[q];
+    for (uint32_t q = 16 * t16 + tid; q <= tbytes; q += blockDim.x) h_text[q] = q < tbytes ? text[q] : '\0';
   }
   if (tid == 0) {
     res->kept = total;
     res->text_bytes = tbytes;
     res->overflow = 0;
   }
+}
+
+static size_t n_jobs_of(const std::vector<JobDev>& jobs) { return jobs.size(); }
+
+// Mapped host buffer of the small path: [SmallOut | SMALL_N records | SMALL_N lines].
+static int small_map(mcx_context* c, SmallOut** so, mcx_record** recs, char** text) {
+  const size_t bytes = 64 + sizeof(mcx_record) * SMALL_N + (size_t)REC_LINE_MAX * SMALL_N + 64;
+  if (!c->h_map.p) {
+    CUDA_TRY(cudaHostAlloc(&c->h_map.p, bytes, cudaHostAllocMapped));
+    c->h_map.bytes = bytes;
+  }
+  char* base = (char*)c->h_map.p;
+  *so = (SmallOut*)base;
+  *recs = (mcx_record*)(base + 64);
+  *text = base + 64 + sizeof(mcx_record) * SMALL_N;
+  return MCX_OK;
+}
+
+// Enqueue the single-kernel post-processing on c->s0: n hits (n_dev == nullptr) or
+// min(*n_dev, hit capacity) hits read on the device.  *queued = false if the sort key
+// does not fit 64 bits (the general path handles that).
+static int enqueue_small(mcx_context* c, const unsigned long long* n_dev, uint64_t n, const uint32_t* hit_task,
+                         const std::vector<JobDev>& jobs, const mcx_find_opts* fo, bool text_ok, bool* queued) {
+  cudaStream_t s = c->s0;
+  *queued = false;
+  uint64_t mg = 0;
+  for (const JobDev& j : jobs) mg = std::max<uint64_t>(mg, (uint64_t)j.NA * (j.MA - 1) * j.NB * (j.MB - 1));
+  const int shift = bits_for(mg) + 2, tb = std::max(1, bits_for(jobs.size() - 1));
+  if (shift + tb > 64) return MCX_OK;
+  const bool want_text = fo->text && text_ok;
+  int rc;
+  if ((rc = ensure(c, c->jobs, sizeof(JobDev) * jobs.size(), s)) ||
+      (rc = ensure(c, c->recs, sizeof(mcx_record) * SMALL_N, s)) ||
+      (rc = ensure(c, c->recs_out, sizeof(mcx_record) * SMALL_N, s)) || (rc = ensure(c, c->small, 64, s)) ||
+      (rc = ensure(c, c->text, (size_t)REC_LINE_MAX * SMALL_N, s)))
+    return rc;
+  CUDA_TRY(h2d_async(c->jobs.p, jobs.data(), sizeof(JobDev) * jobs.size(), s));
+  SmallOut* so;
+  mcx_record* hr;
+  char* ht;
+  if ((rc = small_map(c, &so, &hr, &ht))) return rc;
+  so->overflow = 3;  // "not run" until the kernel writes it
+  unsigned long long* nd = (unsigned long long*)c->small.p + 4;
+  if (!n_dev) {
+    CUDA_TRY(cudaMemcpyAsync(nd, &n, 8, cudaMemcpyHostToDevice, s));  // 8 bytes, staged by the driver
+    n_dev = nd;
+  }
+  CUDA_TRY(cudaFuncSetAttribute(post_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)sizeof(SmallSmem)));
+  SmallOut* d_so;
+  mcx_record* d_hr;
+  char* d_ht;
+  CUDA_TRY(cudaHostGetDevicePointer((void**)&d_so, so, 0));
+  CUDA_TRY(cudaHostGetDevicePointer((void**)&d_hr, hr, 0));
+  CUDA_TRY(cudaHostGetDevicePointer((void**)&d_ht, ht, 0));
+  post_small_kernel<<<1, 1024, sizeof(SmallSmem), s>>>(
+      (const mcx_hit*)c->hits.p, hit_task, n_dev, n_dev == nd ? n : c->hit_cap, (const JobDev*)c->jobs.p, shift,
+      fo->dedup ? 1 : 0, want_text ? 1 : 0, (mcx_record*)c->recs.p, (mcx_record*)c->recs_out.p, (char*)c->text.p,
+      d_so, d_hr, d_ht);
+  CUDA_TRY(cudaGetLastError());
+  *queued = true;
+  return MCX_OK;
+}
+
+// After the stream synchronised: the small path's results, if it completed.
+static bool take_small(mcx_context* c, const mcx_record** records, uint64_t* n_records, const char** text,
+                       uint64_t* text_bytes) {
+  SmallOut* so;
+  mcx_record* hr;
+  char* ht;
+  if (small_map(c, &so, &hr, &ht) || so->overflow) return false;
+  *records = hr;
+  *n_records = so->kept;
+  if (text && text_bytes) {
+    *text = ht;
+    *text_bytes = so->text_bytes;
+  }
+  return true;
 }
 
 static unsigned grid_of(uint64_t n) {
@@ -440,7 +642,7 @@ static unsigned grid_of(uint64_t n) {
 // Steps 2-7 for n hits already in c->hits (hit_task: c->hit_task or null for one job).
 static int postprocess(mcx_context* c, uint64_t n, const uint32_t* hit_task, const std::vector<JobDev>& jobs,
                        const mcx_find_opts* fo, const mcx_record** records, uint64_t* n_records, const char** text,
-                       uint64_t* text_bytes) {
+                       uint64_t* text_bytes, bool try_small = true) {
   cudaStream_t s = c->s0;
   *records = nullptr;
   *n_records = 0;
@@ -453,41 +655,16 @@ static int postprocess(mcx_context* c, uint64_t n, const uint32_t* hit_task, con
   CUDA_TRY(h2d_async(c->jobs.p, jobs.data(), sizeof(JobDev) * jobs.size(), s));
   const JobDev* J = (const JobDev*)c->jobs.p;
   const mcx_hit* H = (const mcx_hit*)c->hits.p;
-  {
-    uint64_t mg = 0;
-    for (const JobDev& j : jobs) mg = std::max<uint64_t>(mg, (uint64_t)j.NA * (j.MA - 1) * j.NB * (j.MB - 1));
-    const int shift = bits_for(mg) + 2, tb = std::max(1, bits_for(jobs.size() - 1));
-    if (n <= (uint64_t)SMALL_N && shift + tb <= 64) {
-      const bool want_text = fo->text && text && text_bytes;
-      if ((rc = ensure(c, c->recs, sizeof(mcx_record) * n, s)) ||
-          (rc = ensure(c, c->recs_out, sizeof(mcx_record) * n, s)) || (rc = ensure(c, c->small, 64, s)) ||
-          (want_text && (rc = ensure(c, c->text, (size_t)REC_LINE_MAX * n, s))) ||
-          (rc = ensure_host(c->h_recs, sizeof(mcx_record) * n)) || (rc = ensure_host(c->h_small, 64)) ||
-          (want_text && (rc = ensure_host(c->h_text, (size_t)REC_LINE_MAX * n + 1))))
-        return rc;
-      post_small_kernel<<<1, 1024, 0, s>>>(H, hit_task, (uint32_t)n, J, shift, fo->dedup ? 1 : 0, want_text ? 1 : 0,
-                                           (mcx_record*)c->recs.p, (mcx_record*)c->recs_out.p, (char*)c->text.p,
-                                           (SmallOut*)c->small.p);
-      CUDA_TRY(cudaGetLastError());
-      // upper-bound copies: no sync needed to learn the exact sizes first
-      CUDA_TRY(cudaMemcpyAsync(c->h_small.p, c->small.p, sizeof(SmallOut), cudaMemcpyDeviceToHost, s));
-      CUDA_TRY(cudaMemcpyAsync(c->h_recs.p, c->recs_out.p, sizeof(mcx_record) * n, cudaMemcpyDeviceToHost, s));
-      if (want_text)
-        CUDA_TRY(cudaMemcpyAsync(c->h_text.p, c->text.p, (size_t)REC_LINE_MAX * n, cudaMemcpyDeviceToHost, s));
+  if (try_small && n <= (uint64_t)SMALL_N) {
+    bool queued = false;
+    if ((rc = enqueue_small(c, nullptr, n, n_jobs_of(jobs) > 1 ? hit_task : nullptr, jobs, fo, text && text_bytes,
+                            &queued)))
+      return rc;
+    if (queued) {
       CUDA_TRY(cudaStreamSynchronize(s));
-      const SmallOut* so = (const SmallOut*)c->h_small.p;
-      if (!so->overflow) {
-        *records = (const mcx_record*)c->h_recs.p;
-        *n_records = so->kept;
-        if (want_text) {
-          ((char*)c->h_text.p)[so->text_bytes] = 0;
-          *text = (const char*)c->h_text.p;
-          *text_bytes = so->text_bytes;
-        }
-        return MCX_OK;
-      }
-      // more than SMALL_K close predecessors somewhere: the general path below
+      if (take_small(c, records, n_records, text, text_bytes)) return MCX_OK;
     }
+    // more than SMALL_K close predecessors somewhere: the general path below
   }
   if ((rc = ensure(c, c->k0, 8 * n, s)) || (rc = ensure(c, c->k1, 8 * n, s)) || (rc = ensure(c, c->v0, 4 * n, s)) ||
       (rc = ensure(c, c->v1, 4 * n, s)) || (rc = ensure(c, c->recs, sizeof(mcx_record) * n, s)) ||
@@ -515,6 +692,7 @@ static int postprocess(mcx_context* c, uint64_t n, const uint32_t* hit_task, con
     CUDA_TRY(cub::DeviceRadixSort::SortPairs(c->cub.p, tmp, keys, vals, ni, 0, bits, s));
     return MCX_OK;
   };
+  trace("big post: start");
   if ((rc = sort_pairs(key_bits))) return rc;
   if (hit_task && jobs.size() > 1) {
     task_key_kernel<<<grid_of(n), 256, 0, s>>>(vals.Current(), hit_task, n, keys.Current());
@@ -537,36 +715,40 @@ static int postprocess(mcx_context* c, uint64_t n, const uint32_t* hit_task, con
     cub::DoubleBuffer<uint32_t> xvals(xv, xv == (uint32_t*)c->v0.p ? (uint32_t*)c->v1.p : (uint32_t*)c->v0.p);
     keys = xkeys;
     vals = xvals;
-    if ((rc = sort_pairs(64))) return rc;
+    {  // by the x bucket only: bits [32, 64) of the ordered key
+      size_t tmp = 0;
+      CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, vals, ni, 32, 64, s));
+      if ((rc = ensure(c, c->cub, tmp, s))) return rc;
+      tmp = c->cub.bytes;
+      CUDA_TRY(cub::DeviceRadixSort::SortPairs(c->cub.p, tmp, keys, vals, ni, 32, 64, s));
+    }
     if (jobs.size() > 1) {
       xtask_key_kernel<<<grid_of(n), 256, 0, s>>>(vals.Current(), R, n, keys.Current());
       CUDA_TRY(cudaGetLastError());
       if ((rc = sort_pairs(task_bits))) return rc;
     }
-    for (int attempt = 0; attempt < 3; ++attempt) {
-      if ((rc = ensure(c, c->pairs, 8 * c->pair_cap, s))) return rc;
-      CUDA_TRY(cudaMemsetAsync(state, 1, n, s));
-      CUDA_TRY(cudaMemsetAsync(c->blocked.p, 0, n, s));
-      CUDA_TRY(cudaMemsetAsync(pair_count, 0, 8, s));
-      close_pairs_kernel<<<grid_of(n), 256, 0, s>>>(vals.Current(), R, n, (uint2*)c->pairs.p, c->pair_cap, pair_count,
-                                                     state);
-      CUDA_TRY(cudaGetLastError());
-      unsigned long long np = 0;
-      CUDA_TRY(cudaMemcpyAsync(&np, pair_count, 8, cudaMemcpyDeviceToHost, s));
-      CUDA_TRY(cudaStreamSynchronize(s));
-      if (np > c->pair_cap) {
-        c->pair_cap = np + 1024;
-        continue;
-      }
-      if (np) resolve_kernel<<<1, 1024, 0, s>>>((const uint2*)c->pairs.p, np, state, (uint8_t*)c->blocked.p);
-      CUDA_TRY(cudaGetLastError());
-      break;
-    }
+    // the pair count is checked at the next synchronisation (a rare overflow reruns this)
+    c->pair_cap = std::max<uint64_t>(c->pair_cap, 4 * n);
+    if ((rc = ensure(c, c->pairs, 8 * c->pair_cap, s))) return rc;
+    CUDA_TRY(cudaMemsetAsync(state, 1, n, s));
+    CUDA_TRY(cudaMemsetAsync(c->blocked.p, 0, n, s));
+    CUDA_TRY(cudaMemsetAsync(pair_count, 0, 8, s));
+    close_pairs_kernel<<<grid_of(n), 256, 0, s>>>(vals.Current(), keys.Current(), R, n, (uint2*)c->pairs.p,
+                                                   c->pair_cap, pair_count, state);
+    resolve_kernel<<<1, 1024, 0, s>>>((const uint2*)c->pairs.p, pair_count, c->pair_cap, state,
+                                      (uint8_t*)c->blocked.p);
+    CUDA_TRY(cudaGetLastError());
   }
   // 6: flags (+ text lengths), inclusive scan of the lengths, compaction, text
   uint8_t* flags = (uint8_t*)c->blocked.p;  // reused: resolution is done
   const bool want_text = fo->text && text && text_bytes;
-  line_len_kernel<<<grid_of(n), 256, 0, s>>>(R, dedup ? state : nullptr, n, J, want_text ? (uint32_t*)c->lens.p : nullptr,
+  uint8_t* flen = nullptr;
+  if (want_text) {
+    if ((rc = ensure(c, c->flen, (size_t)fmt::LINE_FIELDS * n, s))) return rc;
+    flen = (uint8_t*)c->flen.p;
+    field_len_kernel<<<grid_of(fmt::LINE_FIELDS * n), 256, 0, s>>>(R, dedup ? state : nullptr, n, J, flen);
+  }
+  line_len_kernel<<<grid_of(n), 256, 0, s>>>(dedup ? state : nullptr, n, flen, want_text ? (uint32_t*)c->lens.p : nullptr,
                                              flags);
   CUDA_TRY(cudaGetLastError());
   unsigned long long* n_sel = pair_count + 1;
@@ -589,12 +771,20 @@ static int postprocess(mcx_context* c, uint64_t n, const uint32_t* hit_task, con
   ensure_host(c->h_small, 64);
   uint64_t* hs = (uint64_t*)c->h_small.p;
   CUDA_TRY(cudaMemcpyAsync(hs, n_sel, 8, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(hs + 2, pair_count, 8, cudaMemcpyDeviceToHost, s));
   if (want_text) CUDA_TRY(cudaMemcpyAsync(hs + 1, incl + n - 1, 8, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
+  trace("big post: dedup + select + scan (synced)");
+  if (dedup && hs[2] > c->pair_cap) {  // close-pair list overflowed: grow it and redo the stage
+    c->pair_cap = hs[2] + 1024;
+    return postprocess(c, n, hit_task, jobs, fo, records, n_records, text, text_bytes, false);
+  }
   const uint64_t kept = hs[0], tbytes = want_text ? hs[1] : 0;
   if (want_text) {
     if ((rc = ensure(c, c->text, tbytes + 1, s))) return rc;
-    line_write_kernel<<<grid_of(n), 256, 0, s>>>(R, flags, n, J, incl, (const uint32_t*)c->lens.p, (char*)c->text.p);
+    field_write_kernel<<<grid_of(fmt::LINE_FIELDS * n), 256, 0, s>>>(R, flags, n, J, incl,
+                                                                      (const uint32_t*)c->lens.p, flen,
+                                                                      (char*)c->text.p);
     CUDA_TRY(cudaGetLastError());
   }
   // 7: D2H into pinned context memory
@@ -605,6 +795,7 @@ static int postprocess(mcx_context* c, uint64_t n, const uint32_t* hit_task, con
     CUDA_TRY(cudaMemcpyAsync(c->h_text.p, c->text.p, tbytes, cudaMemcpyDeviceToHost, s));
   }
   CUDA_TRY(cudaStreamSynchronize(s));
+  trace("big post: text + D2H (synced)");
   *records = (const mcx_record*)c->h_recs.p;
   *n_records = kept;
   if (want_text) {
@@ -668,15 +859,29 @@ static int intersect(mcx_context* c, const mcx_job* jobs, uint32_t n_jobs, const
   o.mode = fo->mode;
   o.pipeline = fo->pipeline;
   uint64_t total = 0;
+  bool small_done = false;
   for (int attempt = 0; attempt < 4; ++attempt) {
     o.cand_cap = c->cand_cap;
     const uint64_t wsb = mcx_batch_workspace_bytes(tasks.data(), n_jobs, &o);
     if ((rc = ensure(c, c->ws, wsb, c->s0)) || (rc = ensure(c, c->hits, sizeof(mcx_hit) * c->hit_cap, c->s0)) ||
-        (rc = ensure(c, c->hit_task, 4 * c->hit_cap, c->s0)))
+        (rc = ensure(c, c->hit_task, 4 * c->hit_cap, c->s0)) ||
+        (rc = ensure_host(c->h_counters, 8 * (8 + 8ull * n_jobs))))
       return rc;
     o.workspace = c->ws.p;
     o.workspace_bytes = c->ws.bytes;
-    rc = launch_batch(tasks.data(), n_jobs, &o, (mcx_hit*)c->hits.p, (uint32_t*)c->hit_task.p, c->hit_cap, stats);
+    // search, then (optimistically) the single-kernel post-processing straight after it
+    // on the device, one synchronisation for both
+    unsigned long long* hc = (unsigned long long*)c->h_counters.p;
+    rc = launch_batch(tasks.data(), n_jobs, &o, (mcx_hit*)c->hits.p, (uint32_t*)c->hit_task.p, c->hit_cap, stats, hc);
+    if (rc) return rc;
+    bool queued = false;
+    if ((rc = enqueue_small(c, (const unsigned long long*)c->ws.p, 0, n_jobs > 1 ? (const uint32_t*)c->hit_task.p
+                                                                                  : nullptr,
+                            jd, fo, text && text_bytes, &queued)))
+      return rc;
+    CUDA_TRY(cudaStreamSynchronize(c->s0));
+    trace("search + small post done (synced)");
+    rc = batch_stats(hc, n_jobs, &o, c->hit_cap, stats, 0.f);
     total = 0;
     uint64_t cands = 0;
     for (uint32_t t = 0; t < n_jobs; ++t) {
@@ -689,11 +894,13 @@ static int intersect(mcx_context* c, const mcx_job* jobs, uint32_t n_jobs, const
       continue;
     }
     if (rc) return rc;
+    small_done = queued && take_small(c, records, n_records, text, text_bytes);
     break;
   }
   if (rc) return rc;
+  if (small_done) return MCX_OK;
   return postprocess(c, total, n_jobs > 1 ? (const uint32_t*)c->hit_task.p : nullptr, jd, fo, records, n_records,
-                     text, text_bytes);
+                     text, text_bytes, /*try_small=*/false);
 }
 
 static int load_mesh(mcx_context* c, const double* coords, uint32_t N, uint32_t M, const double* s_values,
@@ -789,11 +996,11 @@ int mcx_context_destroy(mcx_context* c) {
   cudaSetDevice(c->device);
   if (c->s0) {
     for (DevBuf* b : {&c->ws, &c->hits, &c->hit_task, &c->jobs, &c->k0, &c->k1, &c->v0, &c->v1, &c->recs, &c->recs_out,
-                      &c->state, &c->blocked, &c->pairs, &c->lens, &c->offs, &c->cub, &c->text, &c->small})
+                      &c->state, &c->blocked, &c->pairs, &c->lens, &c->offs, &c->cub, &c->text, &c->small, &c->flen})
       release(c, *b, c->s0);
     cudaStreamSynchronize(c->s0);
   }
-  for (HostBuf* b : {&c->h_recs, &c->h_text, &c->h_small})
+  for (HostBuf* b : {&c->h_recs, &c->h_text, &c->h_small, &c->h_counters, &c->h_map})
     if (b->p) cudaFreeHost(b->p);
   if (c->stage.p) cudaFreeHost(c->stage.p);
   if (c->ev) cudaEventDestroy(c->ev);
@@ -848,12 +1055,15 @@ int mcx_find_intersections(mcx_context* c, const double* coords_a, uint32_t NA, 
   if (!c) return set_error(MCX_E_ARG, "null context");
   int rc = check_find_opts(fo);
   if (rc) return rc;
+  trace("begin");
   DeviceGuard guard;
   CUDA_TRY(cudaSetDevice(c->device));
   mcx_mesh *A = nullptr, *B = nullptr;
   // A on stream 0; B's copy on stream 1 overlaps A's packing; stream 0 waits for B.
   rc = load_mesh(c, coords_a, NA, MA, s_a, c->s0, &A);
+  trace("A enqueued");
   if (rc == MCX_OK) rc = load_mesh(c, coords_b, NB, MB, s_b, c->s1, &B);
+  trace("B enqueued");
   if (rc == MCX_OK) {
     cudaError_t e = cudaEventRecord(c->ev, c->s1);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(c->s0, c->ev, 0);
@@ -865,6 +1075,7 @@ int mcx_find_intersections(mcx_context* c, const double* coords_a, uint32_t NA, 
   }
   mcx_mesh_free(A);  // stream-ordered on s0, after everything above
   mcx_mesh_free(B);
+  trace("end");
   return rc;
 }
 

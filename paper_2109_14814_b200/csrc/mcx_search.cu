@@ -232,33 +232,60 @@ __global__ void status_kernel(const SearchParams* __restrict__ tasks, uint32_t n
 }
 
 // ------------------------------------------------------------ cull kernels
-// Level 1: (task, local A block x, B tile y) union-box tests over the flattened
-// unit space of all tasks, compacted with one atomic per warp.
+// Level 1: one CTA per unit of CULL_UNIT consecutive local A blocks of one task,
+// grid-stride: the blocks' union boxes are broadcast from shared memory and the CTA's
+// threads sweep the task's B tile boxes once per unit with coalesced 64-byte loads
+// (each tile box serves CULL_UNIT tests); overlapping (task, x, y) are compacted with
+// one atomic per warp.  Bt.prefix here is the per-task prefix of units.
+constexpr int CULL_UNIT = 4;
+
 __global__ void __launch_bounds__(256) cull_blocks_kernel(const Batch Bt) {
-  const uint64_t total = Bt.prefix[Bt.n_tasks];
-  const int lane = threadIdx.x & 31;
-  for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < total; base += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t e = base + threadIdx.x;
-    bool ov = false;
-    uint32_t t = 0, x = 0, y = 0;
-    if (e < total) {
-      t = find_task(Bt, e);
+  __shared__ Box abox[CULL_UNIT];
+  __shared__ const Box* s_tb;
+  __shared__ uint64_t s_ntiles;
+  __shared__ uint32_t s_t, s_x0, s_nx;
+  const uint64_t units = Bt.prefix[Bt.n_tasks];
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (uint64_t u = blockIdx.x; u < units; u += gridDim.x) {
+    if (tid == 0) {
+      const uint32_t t = find_task(Bt, u);
       const SearchParams& P = Bt.tasks[t];
-      const uint64_t u = e - __ldg(Bt.prefix + t);
-      const uint64_t ntiles = P.ntilesB;
-      x = (uint32_t)(u / ntiles);
-      y = (uint32_t)(u % ntiles);
-      const uint64_t gblk = P.blk_first + (uint64_t)x * P.shard_count;
-      ov = box_overlap(P.bboxA[gblk], P.tboxB[y]);
+      const uint64_t x0 = (u - Bt.prefix[t]) * CULL_UNIT;
+      const uint32_t nx = (uint32_t)min((uint64_t)CULL_UNIT, P.my_blocks - x0);
+      for (uint32_t k = 0; k < CULL_UNIT; ++k) {
+        if (k < nx) {
+          abox[k] = P.bboxA[P.blk_first + (x0 + k) * P.shard_count];
+        } else {
+          empty_box(abox[k].lo, abox[k].hi);
+        }
+      }
+      s_tb = P.tboxB;
+      s_ntiles = P.nB ? P.ntilesB : 0;
+      s_t = t;
+      s_x0 = (uint32_t)x0;
+      s_nx = nx;
     }
-    const unsigned m = __ballot_sync(0xffffffffu, ov);
-    if (m) {
-      const int leader = __ffs(m) - 1;
-      unsigned long long pos = 0;
-      if (lane == leader) pos = atomicAdd(Bt.list_count, (unsigned long long)__popc(m));
-      pos = __shfl_sync(0xffffffffu, pos, leader) + __popc(m & ((1u << lane) - 1u));
-      if (ov && pos < Bt.blk_cap) Bt.blk_list[pos] = make_uint4(t, x, y, 0);
+    __syncthreads();
+    const Box* tb = s_tb;
+    const uint64_t ntiles = s_ntiles;
+    const uint32_t t = s_t, x0 = s_x0, nx = s_nx;
+    for (uint64_t y0 = 0; y0 < ntiles; y0 += blockDim.x) {
+      const uint64_t y = y0 + tid;
+      Box b;
+      if (y < ntiles) b = tb[y];
+      for (uint32_t k = 0; k < nx; ++k) {
+        const bool ov = y < ntiles && box_overlap(abox[k], b);
+        const unsigned m = __ballot_sync(0xffffffffu, ov);
+        if (m) {
+          const int leader = __ffs(m) - 1;
+          unsigned long long pos = 0;
+          if (lane == leader) pos = atomicAdd(Bt.list_count, (unsigned long long)__popc(m));
+          pos = __shfl_sync(0xffffffffu, pos, leader) + __popc(m & ((1u << lane) - 1u));
+          if (ov && pos < Bt.blk_cap) Bt.blk_list[pos] = make_uint4(t, x0 + k, (uint32_t)y, 0);
+        }
+      }
     }
+    __syncthreads();  // abox is rewritten by the next unit
   }
 }
 
@@ -435,8 +462,9 @@ static int launch_brute(std::vector<SearchParams>& T, Batch& Bt, std::vector<uin
 template <int KIND>
 static int launch_cull(std::vector<SearchParams>& T, Batch& Bt, std::vector<uint64_t>& prefix, void* dev_tab,
                        int device, cudaStream_t stream) {
-  prefix.assign(T.size() + 1, 0);
-  for (size_t t = 0; t < T.size(); ++t) prefix[t + 1] = prefix[t] + T[t].my_blocks * (T[t].nB ? T[t].ntilesB : 0);
+  prefix.assign(T.size() + 1, 0);  // per-task prefix of level-1 units (CULL_UNIT A blocks each)
+  for (size_t t = 0; t < T.size(); ++t)
+    prefix[t + 1] = prefix[t] + (T[t].nB ? (T[t].my_blocks + CULL_UNIT - 1) / CULL_UNIT : 0);
   const uint64_t total = prefix.back();
   const size_t tab = sizeof(SearchParams) * T.size();
   CUDA_TRY(h2d_async(dev_tab, T.data(), tab, stream));
@@ -446,8 +474,8 @@ static int launch_cull(std::vector<SearchParams>& T, Batch& Bt, std::vector<uint
   Bt.prefix = reinterpret_cast<const uint64_t*>((char*)dev_tab + tab);
   int dev_sms = 148;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device);
-  uint64_t g1 = (total + 255) / 256;
-  if (g1 > (uint64_t)dev_sms * 16) g1 = (uint64_t)dev_sms * 16;
+  uint64_t g1 = total;
+  if (g1 > (uint64_t)dev_sms * 8) g1 = (uint64_t)dev_sms * 8;
   cull_blocks_kernel<<<(unsigned)g1, 256, 0, stream>>>(Bt);
   CUDA_TRY(cudaGetLastError());
   cull_pairs_kernel<KIND><<<(unsigned)(dev_sms * 8), CULL_THREADS, 0, stream>>>(Bt);
@@ -548,8 +576,31 @@ static WsLayout ws_layout(const mcx_task* tasks, uint32_t n, const mcx_opts* o) 
   return L;
 }
 
+// Per-task stats and status from the workspace header (h: 8 shared + 8 per task u64s).
+int batch_stats(const unsigned long long* h, uint32_t n, const mcx_opts* o, uint64_t cap, mcx_stats* st, float ms) {
+  const bool spec = o->pipeline == MCX_PIPE_SPEC;
+  const uint64_t cand_cap = o->cand_cap ? o->cand_cap : MCX_DEFAULT_CAND_CAP;
+  for (uint32_t t = 0; t < n; ++t) {
+    const unsigned long long* c = h + 8 + 8ull * t;
+    st[t].n_hits = c[0];
+    st[t].n_aabb_pass = c[1];
+    st[t].n_singular = c[2];
+    st[t].n_tested = o->mode == MCX_MODE_CULL ? c[3] : st[t].n_pairs;
+    st[t].n_exact_tests = o->mode == MCX_MODE_BRUTE ? st[t].n_pairs : c[3];
+    st[t].n_candidates = spec ? c[4] : c[1];
+    st[t].kernel_ms = ms;
+  }
+  if (h[2]) return set_error(MCX_E_ARG, "non-finite (NaN/Inf) coordinates in an input mesh (mcx_pack status)");
+  if (h[3] > cand_cap)
+    return set_error(MCX_E_CAPACITY, "candidate capacity %llu < %llu box-test survivors (opts->cand_cap)",
+                     (unsigned long long)cand_cap, h[3]);
+  if (h[0] > cap)
+    return set_error(MCX_E_CAPACITY, "hit capacity %llu < %llu hits", (unsigned long long)cap, h[0]);
+  return MCX_OK;
+}
+
 int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mcx_hit* hits, uint32_t* hit_task,
-                        uint64_t cap, mcx_stats* st) {
+                 uint64_t cap, mcx_stats* st, unsigned long long* h_counters) {
   if (!tasks || n == 0 || !o || !st) return set_error(MCX_E_ARG, "null argument or empty batch");
   cudaStream_t stream = (cudaStream_t)o->stream;
   const uint32_t scount = o->shard_count ? o->shard_count : 1;
@@ -670,28 +721,17 @@ int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mcx_hit* 
   status_kernel<<<1, 32, 0, stream>>>(reinterpret_cast<const SearchParams*>(ws + L.table), n,
                                       reinterpret_cast<unsigned long long*>(ws) + 2);
   CUDA_TRY(cudaGetLastError());
+  if (h_counters) {  // asynchronous: the caller synchronises and calls batch_stats
+    CUDA_TRY(cudaMemcpyAsync(h_counters, ws, sizeof(unsigned long long) * (8 + 8ull * n), cudaMemcpyDeviceToHost,
+                             stream));
+    return MCX_OK;
+  }
   std::vector<unsigned long long> h(8 + 8ull * n);
   CUDA_TRY(cudaMemcpyAsync(h.data(), ws, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, stream));
-  CUDA_TRY(cudaStreamSynchronize(stream));  // also keeps T / prefix alive until the copies are done
+  CUDA_TRY(cudaStreamSynchronize(stream));
   float ms = 0.f;
   if (o->timing) CUDA_TRY(cudaEventElapsedTime(&ms, tm.e0, tm.e1));
-  for (uint32_t t = 0; t < n; ++t) {
-    const unsigned long long* c = h.data() + 8 + 8ull * t;
-    st[t].n_hits = c[0];
-    st[t].n_aabb_pass = c[1];
-    st[t].n_singular = c[2];
-    st[t].n_tested = o->mode == MCX_MODE_CULL ? c[3] : st[t].n_pairs;
-    st[t].n_exact_tests = o->mode == MCX_MODE_BRUTE ? st[t].n_pairs : c[3];
-    st[t].n_candidates = spec ? c[4] : c[1];
-    st[t].kernel_ms = ms;
-  }
-  if (h[2]) return set_error(MCX_E_ARG, "non-finite (NaN/Inf) coordinates in an input mesh (mcx_pack status)");
-  if (h[3] > L.cand_cap)
-    return set_error(MCX_E_CAPACITY, "candidate capacity %llu < %llu box-test survivors (opts->cand_cap)",
-                     (unsigned long long)L.cand_cap, h[3]);
-  if (h[0] > cap)
-    return set_error(MCX_E_CAPACITY, "hit capacity %llu < %llu hits", (unsigned long long)cap, h[0]);
-  return MCX_OK;
+  return batch_stats(h.data(), n, o, cap, st, ms);
 }
 
 // Quad AABBs of a half-layer grid: quad q = i + N·k1 over vertices v00 v10 v01 v11.
@@ -904,7 +944,7 @@ int mcx_search(const mcx_mesh_dev* A, const mcx_mesh_dev* B, const mcx_opts* o, 
   DeviceGuard guard;
   CUDA_TRY(cudaSetDevice(o->device));
   mcx_task t = {A, B, o->a_begin, o->a_end};
-  return launch_batch(&t, 1, o, hits, nullptr, cap, st);
+  return launch_batch(&t, 1, o, hits, nullptr, cap, st, nullptr);
 }
 
 int mcx_search_batch(const mcx_task* tasks, uint32_t n_tasks, const mcx_opts* o, mcx_hit* hits, uint32_t* hit_task,
@@ -913,7 +953,7 @@ int mcx_search_batch(const mcx_task* tasks, uint32_t n_tasks, const mcx_opts* o,
   if (!o) return set_error(MCX_E_ARG, "null options");
   DeviceGuard guard;
   CUDA_TRY(cudaSetDevice(o->device));
-  return launch_batch(tasks, n_tasks, o, hits, hit_task, cap, stats);
+  return launch_batch(tasks, n_tasks, o, hits, hit_task, cap, stats, nullptr);
 }
 
 int mcx_pair_candidates(const double* coords_a, uint32_t NA, uint32_t MA, const double* coords_b, uint32_t NB,

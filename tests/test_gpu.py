@@ -670,13 +670,20 @@ def test_spec_pipeline_acceptance_set():
 
 
 # ------------------------------------------------------------ device records pipeline (§8(f) row 4)
-@pytest.mark.parametrize("name", ["C1", "C4i", "C4ii", "C5/8"])
+@pytest.mark.parametrize("name", ["C1", "C4i", "C4ii", "C5/8", "self-small"])
 @pytest.mark.parametrize("dedup", [True, False])
 def test_runtime_records_and_text_equal_host(name, dedup):
     """Device records (fields, (gid, τ_A, τ_B) order, 1e-9 dedup) and the device-formatted
-    records text equal the host path (isect.hits_to_records + to_line) byte for byte."""
+    records text equal the host path (isect.hits_to_records + to_line) byte for byte.
+    C1 / C5/8 / self-small take the single-kernel path (≤ 1024 hits; self-small = a small
+    mesh against itself, up to 36 hits per shared vertex, which overflows its 8-predecessor
+    lists and falls back), C4i / C4ii the general one."""
     from paper_2109_14814_b200 import runtime
-    A, sa, B, sb = config_pair(name)
+    if name == "self-small":
+        A, sa = manifold_like(12, 6, 3)
+        B, sb = A.copy(), sa
+    else:
+        A, sa, B, sb = config_pair(name)
     hits = D.search(A, B, mode=_lib.MODE_CULL).hits
     want = isect.hits_to_records(A, sa, B, sb, hits, layer=(3, "-", 2, "+"), dedup=dedup)
     recs, text, st = runtime.context(0).find(A, sa, B, sb, (3, "-", 2, "+"), mode=_lib.MODE_CULL,
