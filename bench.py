@@ -16,8 +16,10 @@ torchrun each rank owns one GPU and searches its cyclic share of A's
 ranks of CUDA-event device time.
 
 ``--impl reference`` times the reference's CPU search (the C port of the
-SPEC's all-pairs "parallel" backend, oracle/mcx_oracle.c, all host threads) on a
-bounded deterministic slice of the same workload; see DESIGN.md §Measurement.
+SPEC's all-pairs "parallel" backend, oracle/mcx_oracle.c, all host threads) on the
+deterministic slice A triangles [0, 8192) × all of B per step, plus
+the NumPy "parallel" backend (multiprocessing over A-row chunks) and the SPEC-literal
+serial NumPy backend on smaller slices; see DESIGN.md §Measurement.
 """
 from __future__ import annotations
 
@@ -49,7 +51,6 @@ def parse():
     ap.add_argument("--mode", default="prefilter", choices=["prefilter", "brute", "cull"],
                     help="primary mode for `value` (the others are measured too and reported alongside)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU-baseline sample duration")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-paper", action="store_true", help="skip the paper's 14-layer workload block")
@@ -75,28 +76,62 @@ def workload_desc(name, A, B):
 
 
 # ------------------------------------------------------------------ CPU baseline
-def cpu_reference_sample(A, B, target_s, threads=0):
-    """Time the C port of the SPEC all-pairs search (brute force, all threads) on a
-    deterministic slice A[0, n) × all of B, sized to ~target_s seconds."""
+REF_ROWS = 8192  # A triangles [0, 8192) x all of B per timed step
+
+
+def cpu_reference_sample(A, B, rows=REF_ROWS, threads=0, _pack_cache={}):
+    """The C port of the SPEC all-pairs search (brute force, all threads) on the fixed slice
+    A[0, rows) × all of B; the oracle packs both meshes per call, which is timed once with an
+    empty slice and subtracted."""
     from oracle import c_oracle
     c_oracle.build()
     nB = 2 * B.shape[2] * (B.shape[1] - 1)
     nA = 2 * A.shape[2] * (A.shape[1] - 1)
-    n = min(nA, 256)
-    t0 = time.perf_counter()
-    c_oracle.search(A, B, a_range=(0, n), sweep=False, threads=threads)
-    dt = time.perf_counter() - t0
-    # the call includes packing both meshes; estimate pack time with an empty slice
-    t1 = time.perf_counter()
-    c_oracle.search(A, B, a_range=(0, 0), sweep=False, threads=threads)
-    pack = time.perf_counter() - t1
-    rate = n * nB / max(dt - pack, 1e-6)
-    n = int(min(nA, max(256, rate * target_s / nB)))
+    n = min(nA, rows)
+    key = (A.shape, B.shape, threads)
+    if key not in _pack_cache:
+        t1 = time.perf_counter()
+        c_oracle.search(A, B, a_range=(0, 0), sweep=False, threads=threads)
+        _pack_cache[key] = time.perf_counter() - t1
+    pack = _pack_cache[key]
     t0 = time.perf_counter()
     r = c_oracle.search(A, B, a_range=(0, n), sweep=False, threads=threads)
-    dt = time.perf_counter() - t0 - pack
+    dt = max(time.perf_counter() - t0 - pack, 1e-9)
     return {"value": n * nB / dt, "seconds": dt, "a_triangles": n, "pairs": n * nB, "hits": len(r["ia"]),
             "threads": c_oracle.max_threads() if threads == 0 else threads, "pack_seconds": pack}
+
+
+_NP_PACKED = None  # packed meshes shared with the forked workers (copy-on-write)
+
+
+def _numpy_rows(rng):
+    from oracle import canonical
+    r = canonical.search(None, None, a_range=rng, packed=_NP_PACKED)
+    return len(r["ia"])
+
+
+def cpu_numpy_parallel_sample(A, B, rows=2048):
+    """the canonical NumPy oracle in the SPEC's "parallel" mode —
+    multiprocessing over A-row chunks on all cores — on A[0, rows) × all of B (both
+    meshes packed once in the parent, untimed, and shared with the forked workers)."""
+    global _NP_PACKED
+    import multiprocessing as mp
+    from oracle import canonical
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    cores = len(os.sched_getaffinity(0))
+    nB = 2 * B.shape[2] * (B.shape[1] - 1)
+    n = min(rows, 2 * A.shape[2] * (A.shape[1] - 1))
+    _NP_PACKED = (canonical.pack(A), canonical.pack(B))
+    cuts = np.linspace(0, n, cores + 1).astype(int)
+    with mp.get_context("fork").Pool(cores) as pool:
+        pool.map(_numpy_rows, [(0, 0)] * cores)  # workers up
+        t0 = time.perf_counter()
+        hits = sum(pool.map(_numpy_rows, [(int(cuts[k]), int(cuts[k + 1])) for k in range(cores)]))
+        dt = time.perf_counter() - t0
+    _NP_PACKED = None
+    return {"value": n * nB / dt, "unit": UNIT, "cores": cores, "seconds": dt, "hits": hits,
+            "sample": f"A triangles [0, {n}) x all {nB} B triangles, NumPy canonical oracle (oracle/canonical.py), "
+                      f"multiprocessing over {cores} A-row chunks, packing excluded"}
 
 
 def cpu_spec_literal_sample(A, B, target_s=3.0):
@@ -146,18 +181,20 @@ def run_reference(args):
     desc = workload_desc(args.config, A, B)
     cores = len(os.sched_getaffinity(0))
     os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
     for _ in range(max(0, args.warmup)):
-        cpu_reference_sample(A, B, min(2.0, args.cpu_seconds / 4))
-    vals, secs = [], []
+        cpu_reference_sample(A, B, rows=1024)
+    secs, pairs = [], 0
     for _ in range(max(1, args.steps)):
-        s = cpu_reference_sample(A, B, args.cpu_seconds / max(1, args.steps))
-        vals.append(s["value"])
+        s = cpu_reference_sample(A, B)
         secs.append(s["seconds"])
-    v = statistics.median(vals)
+        pairs += s["pairs"]
+    v = pairs / sum(secs)
+    ms = 1e3 * sum(secs) / len(secs)
     sample = (f"A triangles [0, {s['a_triangles']}) x all {desc['triangles_b']} B triangles per step "
-              f"({s['pairs']:.3e} pairs, brute force, packing excluded); full search extrapolated linearly")
+              f"({s['pairs']:.3e} pairs, brute force, packing excluded); ms_per_step is that slice")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": desc["pairs_per_step"] / v * 1e3, "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": bench_config(desc, args.mode, world),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": s["threads"], "kind": "port",
@@ -165,7 +202,9 @@ def run_reference(args):
                              "algorithm": "the SPEC's all-pairs search (every pair through the FP64 AABB test, "
                                           "canonical solve of the passes), C port, OpenMP over A"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "search_wall_s_extrapolated": desc["pairs_per_step"] / v}
+            "full_search_s_extrapolated": desc["pairs_per_step"] / v,
+            "numpy_parallel": None if args.no_cpu_baseline else cpu_numpy_parallel_sample(A, B),
+            "spec_literal_serial": None if args.no_cpu_baseline else cpu_spec_literal_sample(A, B)}
     print(json.dumps(line), flush=True)
 
 
@@ -209,9 +248,9 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ our arm
-# our kernels per search call: brute = search + status check; cull = 2 cull levels + status;
-# prefilter = fp32 boxes + search + status
-KERNEL_LAUNCHES = {"brute": 2, "cull": 3, "prefilter": 3}
+# our kernels per search call: brute = box sweep + solve + status check; cull = 2 cull levels +
+# solve + status; prefilter = fp32 boxes + box sweep + solve + status
+KERNEL_LAUNCHES = {"brute": 3, "cull": 4, "prefilter": 4}
 INT_LANES_PER_CLK_PER_SM = 64  # B200 fma-heavy (IMAD) and alu (LOP3) pipes, each; IMAD measured 62.7 lanes/clk/SM
                                # (tools/microbench/hprefilter.cu swar3_mix0); issue: 4 SMSP x 32 = 128 lanes/clk/SM
 # SASS of the prefilter inner loop, per 16 pair tests: 8 IMAD + 4 IMAD.X (fma-heavy pipe),
@@ -292,32 +331,53 @@ def run_ours(args):
                 "kernel_ms": reduce(st["kernel_ms"], MAX), "stats": st, "clocks": clocks,
                 "launches": KERNEL_LAUNCHES[mode_name] * args.steps}
 
-    def measure_e2e(mode_name, pairs_total):
-        mode = modes[mode_name]
-        pa = torch.from_numpy(np.ascontiguousarray(A)).pin_memory()
-        pb = torch.from_numpy(np.ascontiguousarray(B)).pin_memory()
-        h2d = (pa.numel() + pb.numel()) * 8
+    from paper_2109_14814_b200 import runtime
+    pin_a = torch.from_numpy(np.ascontiguousarray(A)).pin_memory()
+    pin_b = torch.from_numpy(np.ascontiguousarray(B)).pin_memory()
+    h2d_bytes = (pin_a.numel() + pin_b.numel() + len(sa) + len(sb)) * 8
 
-        def step():  # the public host-to-host call (B's upload overlaps A's packing)
-            return D.search_one(pa, pb, device=local, mode=mode, shard=shard, stream=stream)
+    def h2d_floor():
+        """The same grids copied host→device alone (pinned, CUDA events): the PCIe time
+        any implementation of the call pays."""
+        da, db = torch.empty_like(pin_a, device=dev), torch.empty_like(pin_b, device=dev)
+        ts = []
+        for _ in range(6):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            da.copy_(pin_a, non_blocking=True)
+            db.copy_(pin_b, non_blocking=True)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            ts.append(e0.elapsed_time(e1))
+        return min(ts[1:])
+
+    def measure_e2e(mode_name, pipeline, pairs_total, steps):
+        """The reference-facing call end to end: isect.find_intersections' C-ABI entry
+        (mcx_find_intersections) from pinned HOST grids — H2D of both grids, packing, the
+        search, records, (gid, τ) sort, 1e-9 dedup and the records text on the device, D2H
+        of records + text — timed on the host around synchronous calls, max over ranks."""
+        ctx = runtime.context(local)
+        mode, pipe = modes[mode_name], _lib.PIPELINE_NAMES[pipeline]
+
+        def step():
+            return ctx.find(pin_a, sa, pin_b, sb, mode=mode, pipeline=pipe, text=True)
 
         for _ in range(max(1, args.warmup)):
             step()
         barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         d2h = 0
-        e0.record(stream)
-        for _ in range(args.steps):
-            r = step()
-            d2h += 64 + 40 * len(r.hits)
-        e1.record(stream)
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            recs, text, _ = step()
+            d2h += 8 * (8 + 8) + recs.nbytes + len(text)
+        t_ms = reduce((time.perf_counter() - t0) * 1e3, MAX)
         barrier()
-        e_ms = reduce(e0.elapsed_time(e1), MAX)
-        return {"value": pairs_total / (e_ms * 1e-3), "unit": UNIT, "ms_per_step": e_ms / args.steps,
-                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h // args.steps,
-                "path": "device.search_one: pinned host grids -> H2D (B on a side stream) -> mcx_pack + mcx_levels -> "
-                        "mcx_search -> D2H counters + hits",
-                "mode": mode_name}
+        return {"value": pairs_total / (t_ms * 1e-3), "unit": UNIT, "ms_per_step": t_ms / steps,
+                "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h // steps, "records": len(recs),
+                "path": "runtime.Context.find -> mcx_find_intersections(host grids): H2D (4 column chunks per grid, "
+                        "B's on a second stream) pipelined with the fused pack, search, solve, records + sort + "
+                        "dedup + %.17g text on the device, D2H of records + text",
+                "mode": mode_name, "pipeline": pipeline}
 
     primary = args.mode
     others = [m for m in ("prefilter", "brute", "cull") if m != primary]
@@ -399,8 +459,15 @@ def run_ours(args):
 
     e2e = None
     if not args.no_e2e:
-        e2e = measure_e2e(primary, m1["pairs"])
-        e2e["other_modes"] = {m: measure_e2e(m, m1["pairs"]) for m in others}
+        floor_ms = reduce(h2d_floor(), MAX)
+        e2e = measure_e2e(primary, "triangle", m1["pairs"], args.steps)
+        e2e["h2d_floor_ms"] = floor_ms
+        cull_spec = measure_e2e("cull", "spec", m1["pairs"], max(args.steps, 10))
+        cull_spec["over_h2d_floor_ms"] = cull_spec["ms_per_step"] - floor_ms
+        cull_spec["note"] = ("the product default (isect.find_intersections: SPEC-literal pipeline on the culling "
+                             "kernels); logical pair tests per second")
+        e2e["other_modes"] = {"cull_spec": cull_spec,
+                              "brute_triangle": measure_e2e("brute", "triangle", m1["pairs"], min(args.steps, 3))}
 
     # ---- the paper's own benchmark shape: 14-layer search, 108 layer-pair tasks of
     # N1 = 1024 x N2 = 2048 grids with 35 s-values per half-layer (PAPER.md "Computational
@@ -440,6 +507,23 @@ def run_ours(args):
                             "pairs": pairs_total, "executed_pair_tests": reduce(sum(r.stats["n_tested"] for r in res), SUM),
                             "hits": reduce(sum(len(r.hits) for r in res), SUM),
                             "speedup_vs_dgx_v100_full_search": 16.0 / (ms / 1e3)}
+        # the whole plan through the reference-facing task loop: layers.search_plan (each distinct
+        # half-layer uploaded and packed once, one batched search, records + text on the device)
+        if rank == 0 and world == 1:
+            from paper_2109_14814_b200 import layers as LY
+            for pipe in ("spec", "triangle"):
+                LY.search_plan(um, sm, plan, pipeline=pipe, text=True)
+                ts = []
+                for _ in range(3):
+                    t0 = time.perf_counter()
+                    pr = LY.search_plan(um, sm, plan, pipeline=pipe, text=True)
+                    ts.append(time.perf_counter() - t0)
+                paper[f"search_plan_e2e_{pipe}"] = {
+                    "wall_s": min(ts), "records": len(pr.records), "text_bytes": len(pr.text),
+                    "h2d_bytes": int(sum(hh.coords.nbytes for hh in LY._halves(um, sm, plan).values())),
+                    "speedup_vs_dgx_v100_full_search": 16.0 / min(ts),
+                    "path": "layers.search_plan: host meshes -> 56 half-layer uploads + packs, one mcx_intersect "
+                            "(108 tasks in one batched search), records + text on the device"}
         # the paper's own GPU stage per task: quad-level bbox + Moller candidates (pair_candidates)
         if rank == 0:
             busiest = max(range(len(res)), key=lambda k: res[k].stats["n_aabb_pass"])
@@ -520,10 +604,12 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        s = cpu_reference_sample(A, B, args.cpu_seconds)
+        s = cpu_reference_sample(A, B)
         cpu = {"value": s["value"], "unit": UNIT, "cores": s["threads"], "kind": "port",
                "sample": f"C port of the SPEC all-pairs search, A triangles [0, {s['a_triangles']}) x all B "
-                         f"({s['pairs']:.3e} pairs, {s['seconds']:.1f} s, packing excluded)", "cpu": cpu_model(),
+                         f"({s['pairs']:.3e} pairs, {s['seconds']:.1f} s, packing excluded) - the same slice and "
+                         "code as one step of --impl reference", "cpu": cpu_model(),
+               "numpy_parallel": cpu_numpy_parallel_sample(A, B),
                "spec_literal_serial": cpu_spec_literal_sample(A, B)}
         # the culling counterpart on the CPU: the C oracle's exact x-sweep-and-prune over the
         # whole workload (all threads, packing included) - the CPU analogue of `cull`

@@ -624,6 +624,8 @@ def test_bench_json_contract():
     for k in ("value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"):
         assert k in d["e2e"], k
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["gpu_launches"] > 0
+    assert d["e2e"]["h2d_floor_ms"] > 0 and d["e2e"]["records"] == 4
+    assert d["e2e"]["other_modes"]["cull_spec"]["records"] == 4
     assert d["hits"] == d["cull"]["hits"] == 4
 
 
