@@ -156,21 +156,19 @@ int mcxo_max_threads(void) {
  * stats[0] = pairs enumerated (logical), stats[1] = AABB pass, stats[2] = singular.
  * Returns 0, or 1 if cap was exceeded.
  */
-int mcxo_search(const double* coords_a, uint32_t NA, uint32_t MA,
-                const double* coords_b, uint32_t NB, uint32_t MB,
-                uint64_t a0, uint64_t a1, int sweep, int nthreads,
-                uint32_t* ia, uint32_t* ib, double* stab, uint64_t cap,
-                uint64_t* n_hits, uint64_t* stats) {
-  packed_t A, B;
-  pack(coords_a, NA, MA, &A);
-  pack(coords_b, NB, MB, &B);
+/* emit_all: record every AABB-pass pair (not only the accepted ones), stab = the solve's
+ * (s, t, a, b) or NaNs if singular — the survivor list for arithmetic comparisons. */
+static int search_packed(const packed_t* pA, const packed_t* pB, uint64_t a0, uint64_t a1, int sweep,
+                         int nthreads, uint32_t* ia, uint32_t* ib, double* stab, uint64_t cap, uint64_t* n_hits,
+                         uint64_t* stats, int emit_all) {
+  const packed_t A = *pA, B = *pB;
   if (a1 > A.n) a1 = A.n;
   if (a0 > a1) a0 = a1;
   uint64_t nB = B.n;
-  /* optional x-sort of B for sweep-and-prune */
+  /* optional x-sort of B for sweep-and-prune (brute force reads B's packed arrays as they are) */
   uint64_t* perm = (uint64_t*)malloc(sizeof(uint64_t) * (nB ? nB : 1));
-  double* slo = (double*)malloc(sizeof(double) * 4 * (nB ? nB : 1));
-  double* shi = (double*)malloc(sizeof(double) * 4 * (nB ? nB : 1));
+  double* slo = sweep ? (double*)malloc(sizeof(double) * 4 * (nB ? nB : 1)) : B.lo;
+  double* shi = sweep ? (double*)malloc(sizeof(double) * 4 * (nB ? nB : 1)) : B.hi;
   double maxw = 0.0;
   if (sweep) {
     kv_t* kv = (kv_t*)malloc(sizeof(kv_t) * (nB ? nB : 1));
@@ -181,14 +179,15 @@ int mcxo_search(const double* coords_a, uint32_t NA, uint32_t MA,
   } else {
     for (uint64_t j = 0; j < nB; ++j) perm[j] = j;
   }
-  for (uint64_t j = 0; j < nB; ++j) {
-    for (int c = 0; c < 4; ++c) {
-      slo[(uint64_t)c * nB + j] = B.lo[(uint64_t)c * nB + perm[j]];
-      shi[(uint64_t)c * nB + j] = B.hi[(uint64_t)c * nB + perm[j]];
+  if (sweep)
+    for (uint64_t j = 0; j < nB; ++j) {
+      for (int c = 0; c < 4; ++c) {
+        slo[(uint64_t)c * nB + j] = B.lo[(uint64_t)c * nB + perm[j]];
+        shi[(uint64_t)c * nB + j] = B.hi[(uint64_t)c * nB + perm[j]];
+      }
+      double w = shi[j] - slo[j];
+      if (w > maxw) maxw = w;
     }
-    double w = shi[j] - slo[j];
-    if (w > maxw) maxw = w;
-  }
   maxw = maxw * (1.0 + 1e-9);
   (void)cmp_double;
   uint64_t tot_hits = 0, tot_pass = 0, tot_sing = 0, tot_pairs = 0;
@@ -235,10 +234,10 @@ int mcxo_search(const double* coords_a, uint32_t NA, uint32_t MA,
             if (!m[j + u]) continue;
             uint64_t tb = perm[b0 + j + u];
             ++tot_pass;
-            double sol[4];
+            double sol[4] = {NAN, NAN, NAN, NAN};
             int rc = solve(A.geo + 19 * ta, B.geo + 19 * tb, sol);
-            if (rc == 2) { ++tot_sing; continue; }
-            if (rc == 1) {
+            if (rc == 2) ++tot_sing;
+            if (rc == 1 || emit_all) {
               if (nloc == capl) { capl = capl ? 2 * capl : 256; local = (hit_t*)realloc(local, sizeof(hit_t) * capl); }
               local[nloc].ia = (uint32_t)ta; local[nloc].ib = (uint32_t)tb;
               memcpy(local[nloc].v, sol, sizeof(sol));
@@ -262,9 +261,49 @@ int mcxo_search(const double* coords_a, uint32_t NA, uint32_t MA,
   if (tot_hits > cap) overflow = 1;
   *n_hits = tot_hits;
   stats[0] = tot_pairs; stats[1] = tot_pass; stats[2] = tot_sing;
-  free(perm); free(slo); free(shi);
-  unpack_free(&A); unpack_free(&B);
+  free(perm);
+  if (sweep) { free(slo); free(shi); }
   return overflow;
+}
+
+int mcxo_search(const double* coords_a, uint32_t NA, uint32_t MA,
+                const double* coords_b, uint32_t NB, uint32_t MB,
+                uint64_t a0, uint64_t a1, int sweep, int nthreads,
+                uint32_t* ia, uint32_t* ib, double* stab, uint64_t cap,
+                uint64_t* n_hits, uint64_t* stats) {
+  packed_t A, B;
+  pack(coords_a, NA, MA, &A);
+  pack(coords_b, NB, MB, &B);
+  int rc = search_packed(&A, &B, a0, a1, sweep, nthreads, ia, ib, stab, cap, n_hits, stats, 0);
+  unpack_free(&A); unpack_free(&B);
+  return rc;
+}
+
+/* Packed meshes kept across searches (the timed CPU baseline packs once, untimed). */
+void* mcxo_pack_new(const double* coords, uint32_t N, uint32_t M) {
+  packed_t* p = (packed_t*)malloc(sizeof(packed_t));
+  pack(coords, N, M, p);
+  return p;
+}
+
+void mcxo_pack_free(void* p) {
+  if (!p) return;
+  unpack_free((packed_t*)p);
+  free(p);
+}
+
+int mcxo_search_packed(const void* A, const void* B, uint64_t a0, uint64_t a1, int sweep, int nthreads,
+                       uint32_t* ia, uint32_t* ib, double* stab, uint64_t cap, uint64_t* n_hits, uint64_t* stats) {
+  return search_packed((const packed_t*)A, (const packed_t*)B, a0, a1, sweep, nthreads, ia, ib, stab, cap, n_hits,
+                       stats, 0);
+}
+
+/* Every AABB-pass pair of A x B (exact sweep), with the canonical solve's (s, t, a, b)
+ * (NaNs when the singular gate fired or the solve produced none). */
+int mcxo_survivors(const void* A, const void* B, int nthreads, uint32_t* ia, uint32_t* ib, double* stab,
+                   uint64_t cap, uint64_t* n_out, uint64_t* stats) {
+  return search_packed((const packed_t*)A, (const packed_t*)B, 0, ((const packed_t*)A)->n, 1, nthreads, ia, ib, stab,
+                       cap, n_out, stats, 1);
 }
 
 /* Export the canonical packing (for checking the device packer): box [n][8] (lo4 hi4), geo [n][19]. */
@@ -276,4 +315,153 @@ int mcxo_pack(const double* coords, uint32_t N, uint32_t M, double* box, double*
   memcpy(geo, P.geo, sizeof(double) * 19 * P.n);
   unpack_free(&P);
   return 0;
+}
+
+/* ------------------------------------------------------------------------------------
+ * O3 in C — the SPEC-literal serial backend (oracle/serial.py) at full scale: quad AABB
+ * (exact x-sweep over quad boxes), the Moller quick test with serial.py's op sequence,
+ * then the 4 canonical triangle-pair precise tests of every candidate.
+ * stats: [0] quad pairs, [1] quad-AABB passes, [2] candidates, [3] singular solves.
+ */
+#define DEGEN_RTOL2 1e-28
+
+static void quad_verts(const double* c, uint32_t N, uint32_t M, uint64_t q, double V[4][3]) {
+  const uint32_t i = (uint32_t)(q % N), k = (uint32_t)(q / N), ip = (i + 1) % N;
+  const uint64_t idx[4] = {(uint64_t)k * N + i, (uint64_t)k * N + ip, (uint64_t)(k + 1) * N + i,
+                           (uint64_t)(k + 1) * N + ip};
+  for (int v = 0; v < 4; ++v)
+    for (int d = 0; d < 3; ++d) V[v][d] = c[(uint64_t)d * M * N + idx[v]];
+}
+
+static int side_reject(const double Vq[4][3], const double Vo[4][3]) {
+  static const int tri[2][3] = {{0, 1, 2}, {2, 1, 3}};
+  int out = 1;
+  for (int T = 0; T < 2; ++T) {
+    const double* O = Vq[tri[T][0]];
+    double U[3], W[3];
+    for (int d = 0; d < 3; ++d) {
+      U[d] = Vq[tri[T][1]][d] - O[d];
+      W[d] = Vq[tri[T][2]][d] - O[d];
+    }
+    const double N0 = U[1] * W[2] - U[2] * W[1];
+    const double N1 = U[2] * W[0] - U[0] * W[2];
+    const double N2 = U[0] * W[1] - U[1] * W[0];
+    const double nn = (N0 * N0 + N1 * N1) + N2 * N2;
+    const double uu = (U[0] * U[0] + U[1] * U[1]) + U[2] * U[2];
+    const double ww = (W[0] * W[0] + W[1] * W[1]) + W[2] * W[2];
+    const int degen = nn < (uu * ww) * DEGEN_RTOL2;
+    int pos = 1, neg = 1;
+    for (int m = 0; m < 4; ++m) {
+      const double f = (N0 * (Vo[m][0] - O[0]) + N1 * (Vo[m][1] - O[1])) + N2 * (Vo[m][2] - O[2]);
+      pos = pos && (f > 0.0);
+      neg = neg && (f < 0.0);
+    }
+    out = out && !degen && (pos || neg);
+  }
+  return out;
+}
+
+typedef struct {
+  uint64_t n;
+  double *lo, *hi; /* [4][n] */
+} qbox_t;
+
+static void quad_boxes(const double* c, uint32_t N, uint32_t M, qbox_t* out) {
+  const uint64_t n = (uint64_t)N * (M - 1);
+  out->n = n;
+  out->lo = (double*)malloc(sizeof(double) * 4 * (n ? n : 1));
+  out->hi = (double*)malloc(sizeof(double) * 4 * (n ? n : 1));
+  for (uint64_t q = 0; q < n; ++q) {
+    double V[4][4];
+    const uint32_t i = (uint32_t)(q % N), k = (uint32_t)(q / N), ip = (i + 1) % N;
+    const uint64_t idx[4] = {(uint64_t)k * N + i, (uint64_t)k * N + ip, (uint64_t)(k + 1) * N + i,
+                             (uint64_t)(k + 1) * N + ip};
+    for (int v = 0; v < 4; ++v)
+      for (int d = 0; d < 4; ++d) V[v][d] = c[(uint64_t)d * M * N + idx[v]];
+    for (int d = 0; d < 4; ++d) {
+      out->lo[(uint64_t)d * n + q] = fmin(fmin(fmin(V[0][d], V[1][d]), V[2][d]), V[3][d]);
+      out->hi[(uint64_t)d * n + q] = fmax(fmax(fmax(V[0][d], V[1][d]), V[2][d]), V[3][d]);
+    }
+  }
+}
+
+int mcxo_spec_search(const double* coords_a, uint32_t NA, uint32_t MA, const double* coords_b, uint32_t NB,
+                     uint32_t MB, int nthreads, uint32_t* ia, uint32_t* ib, double* stab, uint64_t cap,
+                     uint64_t* n_hits, uint64_t* stats) {
+  packed_t A, B;
+  pack(coords_a, NA, MA, &A);
+  pack(coords_b, NB, MB, &B);
+  qbox_t QA, QB;
+  quad_boxes(coords_a, NA, MA, &QA);
+  quad_boxes(coords_b, NB, MB, &QB);
+  const uint64_t nB = QB.n;
+  kv_t* kv = (kv_t*)malloc(sizeof(kv_t) * (nB ? nB : 1));
+  for (uint64_t j = 0; j < nB; ++j) { kv[j].key = QB.lo[j]; kv[j].idx = j; }
+  qsort(kv, nB, sizeof(kv_t), cmp_kv);
+  double maxw = 0.0;
+  for (uint64_t j = 0; j < nB; ++j) {
+    double w = QB.hi[j] - QB.lo[j];
+    if (w > maxw) maxw = w;
+  }
+  maxw = maxw * (1.0 + 1e-9);
+  uint64_t tot_hits = 0, tot_pass = 0, tot_cand = 0, tot_sing = 0;
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel reduction(+ : tot_pass, tot_cand, tot_sing)
+  {
+    hit_t* local = NULL;
+    uint64_t nloc = 0, capl = 0;
+#pragma omp for schedule(dynamic, 64)
+    for (int64_t qa = 0; qa < (int64_t)QA.n; ++qa) {
+      double la[4], ha[4];
+      for (int c = 0; c < 4; ++c) { la[c] = QA.lo[(uint64_t)c * QA.n + qa]; ha[c] = QA.hi[(uint64_t)c * QA.n + qa]; }
+      const double lo_key = (la[0] - maxw) - 1e-9 * (fabs(la[0]) + maxw);
+      uint64_t L = 0, R = nB;
+      while (L < R) { uint64_t mid = (L + R) / 2; if (kv[mid].key < lo_key) L = mid + 1; else R = mid; }
+      uint64_t j = L > 0 ? L - 1 : 0;
+      double VA[4][3];
+      int have_va = 0;
+      for (; j < nB && kv[j].key <= ha[0]; ++j) {
+        const uint64_t qb = kv[j].idx;
+        int ov = 1;
+        for (int c = 0; c < 4 && ov; ++c)
+          ov = !(ha[c] < QB.lo[(uint64_t)c * nB + qb] || QB.hi[(uint64_t)c * nB + qb] < la[c]);
+        if (!ov) continue;
+        ++tot_pass;
+        if (!have_va) { quad_verts(coords_a, NA, MA, (uint64_t)qa, VA); have_va = 1; }
+        double VB[4][3];
+        quad_verts(coords_b, NB, MB, qb, VB);
+        if (side_reject(VA, VB) || side_reject(VB, VA)) continue;
+        ++tot_cand;
+        for (int v = 0; v < 4; ++v) {
+          const uint64_t ta = 2 * (uint64_t)qa + (v >> 1), tb = 2 * qb + (v & 1);
+          double sol[4];
+          const int rc = solve(A.geo + 19 * ta, B.geo + 19 * tb, sol);
+          if (rc == 2) { ++tot_sing; continue; }
+          if (rc == 1) {
+            if (nloc == capl) { capl = capl ? 2 * capl : 256; local = (hit_t*)realloc(local, sizeof(hit_t) * capl); }
+            local[nloc].ia = (uint32_t)ta; local[nloc].ib = (uint32_t)tb;
+            memcpy(local[nloc].v, sol, sizeof(sol));
+            ++nloc;
+          }
+        }
+      }
+    }
+    uint64_t base;
+#pragma omp atomic capture
+    { base = tot_hits; tot_hits += nloc; }
+    for (uint64_t u = 0; u < nloc; ++u)
+      if (base + u < cap) {
+        ia[base + u] = local[u].ia; ib[base + u] = local[u].ib;
+        memcpy(stab + 4 * (base + u), local[u].v, sizeof(double) * 4);
+      }
+    free(local);
+  }
+  *n_hits = tot_hits;
+  stats[0] = QA.n * QB.n; stats[1] = tot_pass; stats[2] = tot_cand; stats[3] = tot_sing;
+  free(kv);
+  free(QA.lo); free(QA.hi); free(QB.lo); free(QB.hi);
+  unpack_free(&A); unpack_free(&B);
+  return tot_hits > cap;
 }

@@ -325,6 +325,34 @@ def unbalanced_pair(scale: int = 1, dense: bool = False):
     return A, sA, B + 0.0, sB
 
 
+def ruled_pair(NA: int = 128, MA: int = 33, NB: int = 96, MB: int = 9, a: float = 0.5):
+    """Two ruled-surface meshes crossing along a known curve (SPEC.md:485's synthetic
+    geometry oracle).  A(θ, s) = (cos θ, sin θ, s, 0): a cylinder in the hyperplane py = 0,
+    ruled along px.  B(φ, t) = c(φ) + t·d(φ) with c(φ) = (cos φ, sin φ, h(φ), 0) on that
+    cylinder, h(φ) = 0.3 sin 2φ + 0.1, and d(φ) = (a cos φ, a sin φ, 0, 1) leaving the
+    hyperplane, so A ∩ B is exactly the curve c(φ) (B's py = t vanishes only at t = 0).
+    B's t grid avoids 0 and its θ grid differs from A's, so the discrete surfaces cross
+    transversally near the curve.  Returns (A, s_A, B, t_B); ``curve(φ)`` gives c."""
+    th = grid_points(NA)
+    s = np.linspace(-1.0, 1.0, MA)
+    A = np.empty((4, MA, NA))
+    A[0], A[1], A[2], A[3] = np.cos(th)[None, :], np.sin(th)[None, :], s[:, None], 0.0
+    ph = grid_points(NB)
+    t = np.linspace(-0.31, 0.29, MB)
+    R = 1.0 + a * t[:, None]
+    B = np.empty((4, MB, NB))
+    B[0], B[1] = R * np.cos(ph)[None, :], R * np.sin(ph)[None, :]
+    B[2] = (0.3 * np.sin(2.0 * ph) + 0.1)[None, :]
+    B[3] = t[:, None]
+    return A + 0.0, s, B + 0.0, t
+
+
+def ruled_curve(phi):
+    """The analytic intersection curve of ``ruled_pair``: (cos φ, sin φ, 0.3 sin 2φ + 0.1, 0)."""
+    phi = np.asarray(phi, dtype=np.float64)
+    return np.stack([np.cos(phi), np.sin(phi), 0.3 * np.sin(2.0 * phi) + 0.1, 0.0 * phi], axis=-1)
+
+
 CONFIGS = {
     # name: (NA, MA, seedA, NB, MB, seedB)
     "C1": (64, 64, 1, 64, 64, 2),

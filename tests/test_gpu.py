@@ -787,3 +787,72 @@ def test_device_guard_preserves_current_device():
     isect.find_intersections(A, B, devices=(0,))
     D.search(A, B, devices=(0,))
     assert t.cuda.current_device() == before
+
+
+# ------------------------------------------------------------ SPEC.md:485 geometric oracle
+@pytest.mark.parametrize("pipeline", ["spec", "triangle"])
+def test_ruled_surfaces_cross_along_known_curve(pipeline):
+    """Two ruled-surface meshes constructed to cross along a known curve: every returned
+    point lies within one mesh-cell diameter of the analytic curve, the hits
+    cover the whole curve, and the records' parameter estimates (Eqs. 28-29) agree with the
+    analytic parametrisations: θ_u ≈ θ_s ≈ the point's angle, s_u ≈ px, s_s ≈ 0 (t at py = 0)."""
+    from paper_2109_14814_b200.mesh import ruled_curve, ruled_pair
+    A, sa, B, sb = ruled_pair()
+    from paper_2109_14814_b200.mesh import HalfLayer, ManifoldMesh
+    ua = HalfLayer.whole(ManifoldMesh(coords=A, s_values=sa), 1, 1)
+    sbh = HalfLayer.whole(ManifoldMesh(coords=B, s_values=sb, kind="stable"), 1, -1)
+    recs = isect.find_intersections(ua, sbh, pipeline=pipeline)
+    assert len(recs) > 50
+    pts = np.array([r.point for r in recs])
+    ang = np.arctan2(pts[:, 1], pts[:, 0]) % (2 * np.pi)
+    phi = np.linspace(0.0, 2 * np.pi, 400001)
+    curve = ruled_curve(phi)
+    cellA = np.hypot(2 * np.pi / A.shape[2], sa[1] - sa[0])
+    cellB = np.hypot(2 * np.pi / B.shape[2] * 1.2, np.hypot(0.5, 1.0) * (sb[1] - sb[0]))
+    cell = max(cellA, cellB)
+    for p, g in zip(pts, ang):
+        k = int(g / (2 * np.pi) * 400000)
+        idx = np.arange(k - 4000, k + 4000) % len(phi)
+        assert np.min(np.linalg.norm(curve[idx] - p, axis=1)) <= cell
+    gaps = np.diff(np.sort(ang))
+    assert max(gaps.max(), 2 * np.pi - ang.max() + ang.min()) <= 3 * 2 * np.pi / B.shape[2]
+    par = np.array([r.params for r in recs])  # θ_u, s_u, θ_s, s_s
+    wrap = lambda x: (x + np.pi) % (2 * np.pi) - np.pi
+    assert np.max(np.abs(wrap(par[:, 0] - ang))) <= 2 * np.pi / A.shape[2]
+    assert np.max(np.abs(wrap(par[:, 2] - ang))) <= 2 * np.pi / B.shape[2]
+    assert np.max(np.abs(par[:, 1] - pts[:, 2])) <= sa[1] - sa[0]
+    assert np.max(np.abs(par[:, 3])) <= sb[1] - sb[0]
+
+
+# ------------------------------------------------------------ full-scale parity (C5, C5hd, C3)
+@pytest.fixture(scope="module")
+def c5_full(oracle_lib):
+    A, sa, B, sb = config_pair("C5")
+    return A, sa, B, sb, oracle_lib.search(A, B, sweep=True, cap=1 << 20)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_parity_c5_full(mode, c5_full):
+    """The survey-frozen configs[4] pair at full scale (A 4,194,304 x B 65,536 triangles):
+    hit set, s/t/a/b bits and counters equal the C oracle's exact sweep in every mode."""
+    A, _, B, _, ref = c5_full
+    r = D.search(A, B, mode=mode)
+    assert_same_hits(ref, r.hits, r.stats)
+    assert len(ref["ia"]) == 645
+
+
+@pytest.mark.parametrize("name", ["C5", "C5hd", "C3"])
+def test_spec_pipeline_full_scale(name, oracle_lib):
+    """SPEC-literal pipeline at full scale against the C restatement of the serial backend
+    (quad AABB sweep + Moller + 4 precise tests, bit-identical to oracle/serial.py on the
+    reduced configs): hits, s/t/a/b bits, quad-AABB and candidate counts, and the records
+    built from them."""
+    A, sa, B, sb = config_pair(name)
+    ref = oracle_lib.spec_search(A, B)
+    r = D.search(A, B, mode=_lib.MODE_CULL, pipeline=_lib.PIPE_SPEC)
+    assert_same_hits(ref, r.hits)
+    assert r.stats["n_aabb_pass"] == ref["n_quad_aabb_pass"] and r.stats["n_candidates"] == ref["n_candidates"]
+    assert r.stats["n_singular"] == ref["n_singular"] and r.stats["n_pairs"] == ref["n_quad_pairs"]
+    want = isect.hits_to_records(A, sa, B, sb, _as_hits(ref))
+    got = isect.find_intersections(A, B)
+    assert [g.to_line() for g in got] == [w.to_line() for w in want]
