@@ -359,8 +359,8 @@ def run_ours(args):
         ctx = runtime.context(local)
         mode, pipe = modes[mode_name], _lib.PIPELINE_NAMES[pipeline]
 
-        def step():
-            return ctx.find(pin_a, sa, pin_b, sb, mode=mode, pipeline=pipe, text=True)
+        def step():  # this rank's cyclic share of the larger mesh's blocks (all of it at N = 1)
+            return ctx.find(pin_a, sa, pin_b, sb, mode=mode, pipeline=pipe, text=True, shard=shard)
 
         for _ in range(max(1, args.warmup)):
             step()
@@ -468,6 +468,12 @@ def run_ours(args):
                              "kernels); logical pair tests per second")
         e2e["other_modes"] = {"cull_spec": cull_spec,
                               "brute_triangle": measure_e2e("brute", "triangle", m1["pairs"], min(args.steps, 3))}
+        if world > 1:  # per-rank fixed costs (every rank uploads and packs both grids) vs its shard's kernel
+            mine = {"rank": rank, "h2d_floor_ms": h2d_floor(), "e2e_ms": e2e["ms_per_step"],
+                    "kernel_ms": m1["stats"]["kernel_ms"], "cull_spec_e2e_ms": cull_spec["ms_per_step"]}
+            allr = [None] * world
+            dist.all_gather_object(allr, mine)
+            e2e["per_rank"] = allr
 
     # ---- the paper's own benchmark shape: 14-layer search, 108 layer-pair tasks of
     # N1 = 1024 x N2 = 2048 grids with 35 s-values per half-layer (PAPER.md "Computational

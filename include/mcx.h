@@ -129,7 +129,17 @@ typedef struct mcx_opts {
                             workspace (16 B each); 0 → MCX_DEFAULT_CAND_CAP.  On
                             overflow the call fails with MCX_E_CAPACITY and the
                             stats' n_aabb_pass sum is the exact size to regrow to  */
+  int orient;            /* MCX_ORIENT_AS_GIVEN (0) or MCX_ORIENT_LARGER_A: a task whose
+                            B has more triangles than A (and no A range) is searched
+                            with the roles exchanged, so the larger mesh is the one
+                            that is blocked and sharded and the
+                            smaller one is replicated; the precise test still runs as
+                            (A, B) and hits keep A/B indices, so results are
+                            bit-identical to MCX_ORIENT_AS_GIVEN                    */
 } mcx_opts;
+
+#define MCX_ORIENT_AS_GIVEN 0
+#define MCX_ORIENT_LARGER_A 1
 
 #define MCX_DEFAULT_CAND_CAP (1u << 20)
 
@@ -269,6 +279,7 @@ typedef struct mcx_find_opts {
                           record of the same job                          */
   int text;            /* nonzero: also produce the records text          */
   uint32_t shard_index, shard_count; /* cyclic A-block shard of every job (0, 0 → all) */
+  int orient;          /* MCX_ORIENT_*, as mcx_opts.orient                               */
 } mcx_find_opts;
 
 /* Run every job on the context's device as one batched search, then on the device:

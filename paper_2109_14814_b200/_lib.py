@@ -26,6 +26,7 @@ ORDER_NATURAL, ORDER_TILED = 0, 1
 BOX_STRIDE = 8
 GROUP, TILE, BLOCK = 32, 512, 1024
 DEFAULT_CAND_CAP = 1 << 20
+ORIENT_AS_GIVEN, ORIENT_LARGER_A = 0, 1
 
 EXPORTS = ("mcx_a_block", "mcx_workspace_bytes", "mcx_batch_workspace_bytes", "mcx_pack", "mcx_levels",
            "mcx_search", "mcx_search_batch", "mcx_pair_candidates", "mcx_pair_candidates_mesh",
@@ -64,7 +65,8 @@ class Opts(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int), ("stream", ctypes.c_void_p), ("a_begin", ctypes.c_uint64),
                 ("a_end", ctypes.c_uint64), ("shard_index", ctypes.c_uint32), ("shard_count", ctypes.c_uint32),
                 ("mode", ctypes.c_int), ("timing", ctypes.c_int), ("workspace", ctypes.c_void_p),
-                ("workspace_bytes", ctypes.c_uint64), ("pipeline", ctypes.c_int), ("cand_cap", ctypes.c_uint64)]
+                ("workspace_bytes", ctypes.c_uint64), ("pipeline", ctypes.c_int), ("cand_cap", ctypes.c_uint64),
+                ("orient", ctypes.c_int)]
 
 
 class Record(ctypes.Structure):  # mcx_record, 128 bytes
@@ -83,7 +85,7 @@ class Job(ctypes.Structure):
 
 class FindOpts(ctypes.Structure):
     _fields_ = [("mode", ctypes.c_int), ("pipeline", ctypes.c_int), ("dedup", ctypes.c_int), ("text", ctypes.c_int),
-                ("shard_index", ctypes.c_uint32), ("shard_count", ctypes.c_uint32)]
+                ("shard_index", ctypes.c_uint32), ("shard_count", ctypes.c_uint32), ("orient", ctypes.c_int)]
 
 
 assert ctypes.sizeof(Hit) == 40

@@ -858,6 +858,7 @@ static int intersect(mcx_context* c, const mcx_job* jobs, uint32_t n_jobs, const
   o.shard_count = fo->shard_count;
   o.mode = fo->mode;
   o.pipeline = fo->pipeline;
+  o.orient = fo->orient;
   uint64_t total = 0;
   bool small_done = false;
   for (int attempt = 0; attempt < 4; ++attempt) {

@@ -522,6 +522,28 @@ static ShardGeom shard_geom(uint64_t a_begin, uint64_t a_end, uint32_t sidx, uin
   return g;
 }
 
+// The roles a task is searched with (MCX_ORIENT_LARGER_A exchanges A and B when B is the
+// larger mesh and A has no range): *A is blocked / sharded, [*a0, *a1) its range.
+struct Oriented {
+  const mcx_mesh_dev *A, *B;
+  uint64_t a0, a1;
+  bool swap;
+};
+
+static Oriented orient_task(const mcx_task& tk, const mcx_opts* o) {
+  Oriented r{tk.A, tk.B, tk.a_begin, 0, false};
+  if (!tk.A || !tk.B) return r;
+  const bool whole = tk.a_begin == 0 && (tk.a_end == 0 || tk.a_end == tk.A->n_tri);
+  r.swap = o && o->orient == MCX_ORIENT_LARGER_A && whole && tk.B->n_tri > tk.A->n_tri;
+  if (r.swap) {
+    r.A = tk.B;
+    r.B = tk.A;
+    r.a0 = 0;
+  }
+  r.a1 = r.swap ? r.A->n_tri : (tk.a_end ? tk.a_end : tk.A->n_tri);
+  return r;
+}
+
 // Workspace layout: [0, 64) shared counters (emit, list count); then 64 B of
 // counters per task; then the task table + prefix; then the cull block list.
 static uint64_t align16(uint64_t v) { return (v + 15) & ~15ull; }
@@ -553,11 +575,11 @@ static WsLayout ws_layout(const mcx_task* tasks, uint32_t n, const mcx_opts* o) 
   if (o && (o->mode == MCX_MODE_CULL || o->pipeline == MCX_PIPE_SPEC)) {
     const uint32_t scount = o->shard_count ? o->shard_count : 1;
     for (uint32_t t = 0; t < n; ++t) {
-      const mcx_mesh_dev* A = tasks[t].A;
-      const mcx_mesh_dev* B = tasks[t].B;
+      const Oriented ot = orient_task(tasks[t], o);
+      const mcx_mesh_dev* A = ot.A;
+      const mcx_mesh_dev* B = ot.B;
       if (!A || !B) continue;
-      const uint64_t a_end = tasks[t].a_end ? tasks[t].a_end : A->n_tri;
-      const ShardGeom g = shard_geom(tasks[t].a_begin, a_end, o->shard_index % scount, scount);
+      const ShardGeom g = shard_geom(ot.a0, ot.a1, o->shard_index % scount, scount);
       L.list_cap += g.my_blocks * ((B->n_tri + TILE - 1) / TILE);
     }
   }
@@ -635,13 +657,21 @@ int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mcx_hit* 
     }
   }
   auto fbox_of = [&](const mcx_mesh_dev* m) -> float4* { return jobs[mesh_index.at(m->box)].dst; };
+  if (o->orient != MCX_ORIENT_AS_GIVEN && o->orient != MCX_ORIENT_LARGER_A)
+    return set_error(MCX_E_ARG, "unknown orient %d", o->orient);
   std::vector<SearchParams> T(n);
   for (uint32_t t = 0; t < n; ++t) {
-    const mcx_mesh_dev* A = tasks[t].A;
-    const mcx_mesh_dev* B = tasks[t].B;
-    if (!A || !B) return set_error(MCX_E_ARG, "task %u: null mesh", t);
-    const uint64_t a_begin = tasks[t].a_begin;
-    const uint64_t a_end = tasks[t].a_end ? tasks[t].a_end : A->n_tri;
+    if (!tasks[t].A || !tasks[t].B) return set_error(MCX_E_ARG, "task %u: null mesh", t);
+    if (tasks[t].a_end > tasks[t].A->n_tri || tasks[t].a_begin > (tasks[t].a_end ? tasks[t].a_end : tasks[t].A->n_tri))
+      return set_error(MCX_E_ARG, "task %u: A range [%llu, %llu) outside [0, %llu)", t,
+                       (unsigned long long)tasks[t].a_begin, (unsigned long long)tasks[t].a_end,
+                       (unsigned long long)tasks[t].A->n_tri);
+    const Oriented ot = orient_task(tasks[t], o);  // the sweep blocks / shards the larger mesh; the solve un-swaps
+    const bool swap = ot.swap;
+    const mcx_mesh_dev* A = ot.A;
+    const mcx_mesh_dev* B = ot.B;
+    const uint64_t a_begin = ot.a0;
+    const uint64_t a_end = ot.a1;
     if (a_end > A->n_tri || a_begin > a_end)
       return set_error(MCX_E_ARG, "task %u: A range [%llu, %llu) outside [0, %llu)", t, (unsigned long long)a_begin,
                        (unsigned long long)a_end, (unsigned long long)A->n_tri);
@@ -673,6 +703,7 @@ int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mcx_hit* 
     P.ntilesB = (B->n_tri + TILE - 1) / TILE;
     P.shard_count = scount;
     P.task = t;
+    P.swapped = swap ? 1u : 0u;
     P.counters = reinterpret_cast<unsigned long long*>(ws + L.counters + 64ull * t);
     P.gboxA = reinterpret_cast<const Box*>(A->gbox);
     P.bboxA = reinterpret_cast<const Box*>(A->bbox);

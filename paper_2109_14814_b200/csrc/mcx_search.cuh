@@ -52,6 +52,7 @@ struct __align__(16) SearchParams {
   uint64_t b_chunk, nchunk; // brute: B triangles per CTA (multiple of TILE), chunks
   uint64_t ntilesB;
   uint32_t shard_count, task;
+  uint32_t swapped;  // MCX_ORIENT_LARGER_A exchanged the roles: "A" here is the caller's B
   // per task: [0] emitted, [1] aabb pass, [2] singular (KIND_QUAD: Moller-rejected), [3] tested,
   // [4] KIND_SPEC: Moller survivors (candidates)
   unsigned long long* counters;
@@ -184,14 +185,21 @@ __global__ void __launch_bounds__(256) solve_kernel(const Batch Bt) {
     const bool valid = k < n;
     const uint4 c = valid ? Bt.cand[k] : make_uint4(0u, 0u, 0u, 0u);
     const SearchParams& P = Bt.tasks[c.z];
+    // the caller's (A, B) roles: the sweep may have run them exchanged (P.swapped)
+    const double* cA = P.swapped ? P.coordsB : P.coordsA;
+    const double* cB = P.swapped ? P.coordsA : P.coordsB;
+    const uint32_t NA = P.swapped ? P.NB : P.NA, MA = P.swapped ? P.MB : P.MA;
+    const uint32_t NB = P.swapped ? P.NA : P.NB, MB = P.swapped ? P.MA : P.MB;
     if (KIND == KIND_TRI) {
       double sol[4];
       int rc = 0;
       uint32_t ia = 0, ib = 0;
       if (valid) {
-        ia = P.permA ? __ldg(P.permA + c.x) : c.x;
-        ib = P.permB ? __ldg(P.permB + c.y) : c.y;
-        rc = solve_tri(P.coordsA, P.NA, P.MA, ia, P.coordsB, P.NB, P.MB, ib, sol);
+        const uint32_t i1 = P.permA ? __ldg(P.permA + c.x) : c.x;
+        const uint32_t i2 = P.permB ? __ldg(P.permB + c.y) : c.y;
+        ia = P.swapped ? i2 : i1;
+        ib = P.swapped ? i1 : i2;
+        rc = solve_tri(cA, NA, MA, ia, cB, NB, MB, ib, sol);
         if (rc == 2) atomicAdd(P.counters + 2, 1ull);
       }
       emit_hits(Bt, rc == 1, ia, ib, sol, c.z, P.counters, lane);
@@ -218,15 +226,16 @@ __global__ void __launch_bounds__(256) solve_kernel(const Batch Bt) {
       }
     } else {
       // KIND_SPEC: "for each surviving gid, runs all 4 triangle-pair precise tests"
-      const bool cand = valid && !moller_reject(P.coordsA, P.NA, P.MA, c.x, P.coordsB, P.NB, P.MB, c.y);
+      const uint32_t qa = P.swapped ? c.y : c.x, qb = P.swapped ? c.x : c.y;
+      const bool cand = valid && !moller_reject(cA, NA, MA, qa, cB, NB, MB, qb);
       if (cand) atomicAdd(P.counters + 4, 1ull);
 #pragma unroll 1
       for (int v = 0; v < 4; ++v) {
-        const uint32_t ia = 2 * c.x + (v >> 1), ib = 2 * c.y + (v & 1);
+        const uint32_t ia = 2 * qa + (v >> 1), ib = 2 * qb + (v & 1);
         double sol[4];
         int rc = 0;
         if (cand) {
-          rc = solve_tri(P.coordsA, P.NA, P.MA, ia, P.coordsB, P.NB, P.MB, ib, sol);
+          rc = solve_tri(cA, NA, MA, ia, cB, NB, MB, ib, sol);
           if (rc == 2) atomicAdd(P.counters + 2, 1ull);
         }
         emit_hits(Bt, rc == 1, ia, ib, sol, c.z, P.counters, lane);

@@ -179,8 +179,10 @@ def _grow_for(rc, stats_list, cap, cand_cap):
 
 def search_device(A: DeviceMesh, B: DeviceMesh, *, mode: int = _lib.MODE_BRUTE, a_range=None,
                   shard=(0, 1), cap: int = 1 << 16, timing: bool = False, stream=None, task=None,
-                  sort: bool = True, pipeline: int = _lib.PIPE_TRIANGLE) -> SearchResult:
-    """Run one search call on A.device; grows the hit / candidate buffers and reruns on overflow."""
+                  sort: bool = True, pipeline: int = _lib.PIPE_TRIANGLE,
+                  orient: int = _lib.ORIENT_LARGER_A) -> SearchResult:
+    """Run one search call on A.device; grows the hit / candidate buffers and reruns on overflow.
+    ``orient`` (default: the larger mesh is blocked / sharded) never changes the results."""
     t = torch()
     if A.device != B.device:
         raise ConfigError("A and B must live on the same device")
@@ -194,7 +196,7 @@ def search_device(A: DeviceMesh, B: DeviceMesh, *, mode: int = _lib.MODE_BRUTE, 
         s = stream or t.cuda.current_stream(A.device)
         for _attempt in range(4):
             opts = _lib.Opts(A.device, s.cuda_stream, a0, a1, int(shard[0]), int(shard[1]), int(mode), int(timing),
-                             None, 0, int(pipeline), cand_cap)
+                             None, 0, int(pipeline), cand_cap, int(orient))
             ws = W.workspace(L.mcx_workspace_bytes(As, Bs, opts))
             opts.workspace, opts.workspace_bytes = ws.data_ptr(), ws.numel()
             buf = W.hit_buffer(cap)
@@ -218,7 +220,7 @@ def search_device(A: DeviceMesh, B: DeviceMesh, *, mode: int = _lib.MODE_BRUTE, 
 
 
 def search_batch(pairs, *, mode: int = _lib.MODE_BRUTE, shard=(0, 1), cap: int = 1 << 16, timing: bool = False,
-                 stream=None, task_ids=None, pipeline: int = _lib.PIPE_TRIANGLE):
+                 stream=None, task_ids=None, pipeline: int = _lib.PIPE_TRIANGLE, orient: int = _lib.ORIENT_LARGER_A):
     """Many (A, B) DeviceMesh searches in one launch per kernel (mcx_search_batch).
 
     ``pairs``: list of (A, B) or (A, B, (a_begin, a_end)).  Returns one
@@ -247,7 +249,7 @@ def search_batch(pairs, *, mode: int = _lib.MODE_BRUTE, shard=(0, 1), cap: int =
         s = stream or t.cuda.current_stream(dev)
         for _attempt in range(4):
             opts = _lib.Opts(dev, s.cuda_stream, 0, 0, int(shard[0]), int(shard[1]), int(mode), int(timing), None, 0,
-                             int(pipeline), cand_cap)
+                             int(pipeline), cand_cap, int(orient))
             ws = W.workspace(L.mcx_batch_workspace_bytes(tasks, n, opts))
             opts.workspace, opts.workspace_bytes = ws.data_ptr(), ws.numel()
             buf = W.hit_buffer(cap)
@@ -335,7 +337,8 @@ def run_on_devices(fn, devices):
 
 
 def search_one(coords_a, coords_b, *, device: int = 0, mode: int = _lib.MODE_BRUTE, shard=(0, 1),
-               timing: bool = False, task=None, stream=None, pipeline: int = _lib.PIPE_TRIANGLE) -> SearchResult:
+               timing: bool = False, task=None, stream=None, pipeline: int = _lib.PIPE_TRIANGLE,
+               orient: int = _lib.ORIENT_LARGER_A) -> SearchResult:
     """Host grids → hits on one device: B is uploaded and packed on a side stream so
     its H2D overlaps A's packing; then one search call.  Pinned CPU tensors give
     asynchronous copies."""
@@ -349,13 +352,13 @@ def search_one(coords_a, coords_b, *, device: int = 0, mode: int = _lib.MODE_BRU
         Am = DeviceMesh(coords_a, device, stream=main)
         main.wait_event(ready)
         return search_device(Am, Bm, mode=mode, shard=shard, timing=timing, stream=main, task=task,
-                             pipeline=pipeline)
+                             pipeline=pipeline, orient=orient)
 
 
 def search(coords_a, coords_b, *, devices=(0,), mode: int = _lib.MODE_BRUTE, timing: bool = False,
-           task=None, pipeline: int = _lib.PIPE_TRIANGLE) -> SearchResult:
+           task=None, pipeline: int = _lib.PIPE_TRIANGLE, orient: int = _lib.ORIENT_LARGER_A) -> SearchResult:
     """Host-to-host triangle search: upload, pack, search (sharded over ``devices``,
-    one persistent host thread per GPU), gather, sort."""
+    one persistent host thread per GPU; the larger mesh is the sharded one), gather, sort."""
     devices = list(devices)
     if not devices:
         raise ConfigError("devices must be non-empty")
@@ -363,7 +366,7 @@ def search(coords_a, coords_b, *, devices=(0,), mode: int = _lib.MODE_BRUTE, tim
         _require_cuda(d)
     G = len(devices)
     results = run_on_devices(lambda r: search_one(coords_a, coords_b, device=devices[r], mode=mode, shard=(r, G),
-                                                  timing=timing, task=task, pipeline=pipeline), devices)
+                                                  timing=timing, task=task, pipeline=pipeline, orient=orient), devices)
     return _merge(results)
 
 
@@ -445,7 +448,7 @@ def pair_candidates_mesh(A: DeviceMesh, B: DeviceMesh, *, shard=(0, 1), cap: int
         s = stream or t.cuda.current_stream(A.device)
         for _ in range(4):
             opts = _lib.Opts(A.device, s.cuda_stream, 0, 0, int(shard[0]), int(shard[1]), _lib.MODE_CULL, int(timing),
-                             None, 0, _lib.PIPE_TRIANGLE, cand_cap)
+                             None, 0, _lib.PIPE_TRIANGLE, cand_cap, _lib.ORIENT_AS_GIVEN)
             ws = W.workspace(L.mcx_pair_candidates_mesh_workspace_bytes(As, Bs, opts))
             opts.workspace, opts.workspace_bytes = ws.data_ptr(), ws.numel()
             gids = t.empty(max(cap, 1), dtype=t.int64, device=dev)

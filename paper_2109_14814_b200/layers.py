@@ -123,6 +123,60 @@ def _halves(u_mesh, s_mesh, plan):
     return halves
 
 
+def plan_parts(u_mesh, s_mesh, plan, n_parts: int):
+    """(half-layers by key, task-index lists): whole tasks dealt over n_parts GPUs/ranks by
+    estimated cost (triangle pairs), deterministically."""
+    halves = _halves(u_mesh, s_mesh, plan)
+    costs = [halves[("u", n1, s1)].n_triangles * halves[("s", n2, s2)].n_triangles
+             for (n1, s1, n2, s2) in plan.tasks]
+    return halves, assign_tasks(costs, n_parts)
+
+
+def run_part(halves, plan, mine, device: int, mode: int, pipeline: int, dedup: bool, text: bool):
+    """One GPU's share: upload and pack each half-layer its tasks need once, one
+    mcx_intersect over the tasks.  Returns (records with task = index into ``mine``, text,
+    per-task stats)."""
+    if not mine:
+        return np.zeros(0, runtime.RECORD_DTYPE), b"", []
+    ctx = runtime.context(device)
+    meshes = {}
+    try:
+        jobs = []
+        for k in mine:
+            n1, s1, n2, s2 = plan.tasks[k]
+            for key in (("u", n1, s1), ("s", n2, s2)):
+                if key not in meshes:
+                    h = halves[key]
+                    meshes[key] = ctx.mesh(np.ascontiguousarray(h.coords), h.s_values)
+            jobs.append((meshes[("u", n1, s1)], meshes[("s", n2, s2)], plan.tasks[k]))
+        return ctx.intersect(jobs, mode=mode, pipeline=pipeline, dedup=dedup, text=text,
+                             task_ids=[plan.tasks[k] for k in mine])
+    finally:
+        for mesh in meshes.values():
+            mesh.free()
+
+
+def merge_parts(plan, halves, parts, outs, devices, text: bool) -> PlanResult:
+    """Plan-order records / stats / text from every part's (records, text, stats)."""
+    per_task = [None] * len(plan)
+    for rank, (recs, txt, stats) in enumerate(outs):
+        mine = parts[rank]
+        lines = txt.split(b"\n")[:-1] if txt else []
+        cut = np.searchsorted(recs["task"], np.arange(len(mine) + 1)) if len(recs) else np.zeros(len(mine) + 1, int)
+        for j, k in enumerate(mine):
+            seg = recs[cut[j]:cut[j + 1]]
+            body = b"".join(ln + b"\n" for ln in lines[cut[j]:cut[j + 1]]) if text else b""
+            per_task[k] = (seg, body, {"layer": plan.tasks[k], "device": devices[rank], **stats[j]})
+    records, stats, chunks = [], [], []
+    for k, (seg, body, st) in enumerate(per_task):
+        n1, s1, n2, s2 = plan.tasks[k]
+        hu, hs = halves[("u", n1, s1)], halves[("s", n2, s2)]
+        records.extend(isect.records_to_objects(seg, hu.N, hs.N, layer=plan.tasks[k], tof=plan.tof[k]))
+        stats.append(st)
+        chunks.append(body)
+    return PlanResult(records=records, stats=stats, text=b"".join(chunks))
+
+
 def search_plan(u_mesh: ManifoldMesh, s_mesh: ManifoldMesh, plan: LayerPairPlan, backend: str = "cuda", *,
                 mode: str = "cull", pipeline: str = "spec", device: int = 0, devices=None, dedup: bool = True,
                 text: bool = False) -> PlanResult:
@@ -139,47 +193,27 @@ def search_plan(u_mesh: ManifoldMesh, s_mesh: ManifoldMesh, plan: LayerPairPlan,
     devices = list(devices) if devices is not None else [device]
     if not devices:
         raise ConfigError("devices must be non-empty")
-    halves = _halves(u_mesh, s_mesh, plan)
-    costs = [halves[("u", n1, s1)].n_triangles * halves[("s", n2, s2)].n_triangles
-             for (n1, s1, n2, s2) in plan.tasks]
-    parts = assign_tasks(costs, len(devices))
+    halves, parts = plan_parts(u_mesh, s_mesh, plan, len(devices))
+    outs = _device.run_on_devices(lambda r: run_part(halves, plan, parts[r], devices[r], m, p, dedup, text), devices)
+    return merge_parts(plan, halves, parts, outs, devices, text)
 
-    def run(rank):
-        mine = parts[rank]
-        if not mine:
-            return [], b"", []
-        ctx = runtime.context(devices[rank])
-        meshes = {}
-        try:
-            jobs = []
-            for k in mine:
-                n1, s1, n2, s2 = plan.tasks[k]
-                for key in (("u", n1, s1), ("s", n2, s2)):
-                    if key not in meshes:
-                        h = halves[key]
-                        meshes[key] = ctx.mesh(np.ascontiguousarray(h.coords), h.s_values)
-                jobs.append((meshes[("u", n1, s1)], meshes[("s", n2, s2)], plan.tasks[k]))
-            return ctx.intersect(jobs, mode=m, pipeline=p, dedup=dedup, text=text,
-                                 task_ids=[plan.tasks[k] for k in mine])
-        finally:
-            for mesh in meshes.values():
-                mesh.free()
 
-    outs = _device.run_on_devices(run, devices)
-    per_task = [None] * len(plan)
-    for rank, (recs, txt, stats) in enumerate(outs):
-        mine = parts[rank]
-        lines = txt.split(b"\n")[:-1] if txt else []
-        cut = np.searchsorted(recs["task"], np.arange(len(mine) + 1)) if len(recs) else np.zeros(len(mine) + 1, int)
-        for j, k in enumerate(mine):
-            seg = recs[cut[j]:cut[j + 1]]
-            body = b"".join(l + b"\n" for l in lines[cut[j]:cut[j + 1]]) if text else b""
-            per_task[k] = (seg, body, {"layer": plan.tasks[k], "device": devices[rank], **stats[j]})
-    records, stats, chunks = [], [], []
-    for k, (seg, body, st) in enumerate(per_task):
-        n1, s1, n2, s2 = plan.tasks[k]
-        hu, hs = halves[("u", n1, s1)], halves[("s", n2, s2)]
-        records.extend(isect.records_to_objects(seg, hu.N, hs.N, layer=plan.tasks[k], tof=plan.tof[k]))
-        stats.append(st)
-        chunks.append(body)
-    return PlanResult(records=records, stats=stats, text=b"".join(chunks))
+def search_plan_distributed(u_mesh: ManifoldMesh, s_mesh: ManifoldMesh, plan: LayerPairPlan,
+                            backend: str = "cuda", *, mode: str = "cull", pipeline: str = "spec", device: int = 0,
+                            dedup: bool = True, text: bool = False, dst: int = 0, group=None):
+    """``search_plan`` as one rank of a torch.distributed job (one process per GPU,
+    torchrun): every rank runs its whole tasks on ``device`` and the (small) record
+    lists are gathered to ``dst``, which returns the plan-order PlanResult (None on the
+    other ranks).  Result collection only — no collective on the data path."""
+    import torch.distributed as dist
+    isect._check_backend(backend)
+    m, p = isect._mode_pipeline(mode, pipeline)
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    halves, parts = plan_parts(u_mesh, s_mesh, plan, world)
+    out = run_part(halves, plan, parts[rank], device, m, p, dedup, text)
+    gathered = [None] * world if rank == dst else None
+    dist.gather_object((out[0].tobytes(), out[1], out[2], device), gathered, dst=dst, group=group)
+    if rank != dst:
+        return None
+    outs = [(np.frombuffer(r, dtype=runtime.RECORD_DTYPE), t, st) for r, t, st, _ in gathered]
+    return merge_parts(plan, halves, parts, outs, [g[3] for g in gathered], text)

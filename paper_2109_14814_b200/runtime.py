@@ -51,8 +51,10 @@ def _host_f64(a):
     return a.ctypes.data, a
 
 
-def find_opts(mode: int, pipeline: int, dedup: bool, text: bool, shard=(0, 1)) -> _lib.FindOpts:
-    return _lib.FindOpts(int(mode), int(pipeline), int(bool(dedup)), int(bool(text)), int(shard[0]), int(shard[1]))
+def find_opts(mode: int, pipeline: int, dedup: bool, text: bool, shard=(0, 1),
+              orient: int = _lib.ORIENT_LARGER_A) -> _lib.FindOpts:
+    return _lib.FindOpts(int(mode), int(pipeline), int(bool(dedup)), int(bool(text)), int(shard[0]), int(shard[1]),
+                         int(orient))
 
 
 class Mesh:
@@ -118,8 +120,11 @@ class Context:
         return recs, text
 
     def find(self, coords_a, s_a, coords_b, s_b, layer=(0, "+", 0, "+"), *, mode=_lib.MODE_CULL,
-             pipeline=_lib.PIPE_SPEC, dedup=True, text=False, task=None):
-        """mcx_find_intersections: host grids → (records, text bytes, stats dict)."""
+             pipeline=_lib.PIPE_SPEC, dedup=True, text=False, task=None, shard=(0, 1),
+             orient=_lib.ORIENT_LARGER_A):
+        """mcx_find_intersections: host grids → (records, text bytes, stats dict).  ``shard``
+        restricts the search to a cyclic share of the (larger) mesh's blocks, as one rank
+        of a multi-GPU job (the records are then that shard's)."""
         pa, ka = _host_f64(coords_a)
         pb, kb = _host_f64(coords_b)
         sa = np.ascontiguousarray(s_a, dtype=np.float64)
@@ -130,7 +135,7 @@ class Context:
             raise ConfigError("a half-layer needs >= 2 columns (SPEC.md:473)")
         if sa.shape != (MA,) or sb.shape != (MB,):
             raise ConfigError("s_values must have one entry per column")
-        fo = find_opts(mode, pipeline, dedup, text)
+        fo = find_opts(mode, pipeline, dedup, text, shard, orient)
         recp, n, textp, tlen, st = ctypes.POINTER(_lib.Record)(), ctypes.c_uint64(), ctypes.c_void_p(), \
             ctypes.c_uint64(), _lib.Stats()
         rc = _lib.load().mcx_find_intersections(self.handle, pa, NA, MA, sa.ctypes.data, pb, NB, MB, sb.ctypes.data,

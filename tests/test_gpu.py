@@ -856,3 +856,23 @@ def test_spec_pipeline_full_scale(name, oracle_lib):
     want = isect.hits_to_records(A, sa, B, sb, _as_hits(ref))
     got = isect.find_intersections(A, B)
     assert [g.to_line() for g in got] == [w.to_line() for w in want]
+
+
+# ------------------------------------------------------------ orientation
+@pytest.mark.parametrize("mode", MODES)
+def test_orientation_swap_bit_identical(mode, oracle_lib):
+    """A small A against a large B: with MCX_ORIENT_LARGER_A the sweep blocks and shards B
+    (the larger mesh) and replicates A, but the precise test still runs as (A, B), so hits,
+    s/t/a/b bits and counters equal the as-given search and the oracle — unsharded and over
+    3 cyclic shards of B's blocks."""
+    B, _, A, _ = config_pair("C5/8")  # A: 32x17 grid, B: 256x129 grid
+    ref = oracle_lib.search(A, B, sweep=True)
+    Am, Bm = D.DeviceMesh(A, 0), D.DeviceMesh(B, 0)
+    for orient in (_lib.ORIENT_AS_GIVEN, _lib.ORIENT_LARGER_A):
+        r = D.search_device(Am, Bm, mode=mode, orient=orient)
+        assert_same_hits(ref, r.hits, r.stats)
+        parts = [D.search_device(Am, Bm, mode=mode, orient=orient, shard=(g, 3)) for g in range(3)]
+        assert_same_hits(ref, D._merge(parts).hits)
+    spec = D.search_device(Am, Bm, mode=_lib.MODE_CULL, pipeline=_lib.PIPE_SPEC, orient=_lib.ORIENT_AS_GIVEN)
+    spec2 = D.search_device(Am, Bm, mode=_lib.MODE_CULL, pipeline=_lib.PIPE_SPEC, orient=_lib.ORIENT_LARGER_A)
+    assert np.array_equal(spec.hits, spec2.hits) and spec.stats["n_candidates"] == spec2.stats["n_candidates"]

@@ -41,13 +41,14 @@ LAYOUT = [  # (C expression, ctypes value)
     ("sizeof(mcx_stats)", ctypes.sizeof(_lib.Stats)), ("offsetof(mcx_stats, n_candidates)", _lib.Stats.n_candidates.offset),
     ("sizeof(mcx_opts)", ctypes.sizeof(_lib.Opts)), ("offsetof(mcx_opts, mode)", _lib.Opts.mode.offset),
     ("offsetof(mcx_opts, workspace)", _lib.Opts.workspace.offset), ("offsetof(mcx_opts, pipeline)", _lib.Opts.pipeline.offset),
-    ("offsetof(mcx_opts, cand_cap)", _lib.Opts.cand_cap.offset),
+    ("offsetof(mcx_opts, cand_cap)", _lib.Opts.cand_cap.offset), ("offsetof(mcx_opts, orient)", _lib.Opts.orient.offset),
     ("sizeof(mcx_task)", ctypes.sizeof(_lib.Task)), ("sizeof(mcx_record)", ctypes.sizeof(_lib.Record)),
     ("offsetof(mcx_record, point)", _lib.Record.point.offset), ("offsetof(mcx_record, params)", _lib.Record.params.offset),
     ("offsetof(mcx_record, task)", _lib.Record.task.offset), ("sizeof(mcx_layer)", ctypes.sizeof(_lib.Layer)),
     ("sizeof(mcx_job)", ctypes.sizeof(_lib.Job)), ("offsetof(mcx_job, layer)", _lib.Job.layer.offset),
     ("sizeof(mcx_find_opts)", ctypes.sizeof(_lib.FindOpts)),
     ("offsetof(mcx_find_opts, shard_count)", _lib.FindOpts.shard_count.offset),
+    ("offsetof(mcx_find_opts, orient)", _lib.FindOpts.orient.offset),
 ]
 
 
