@@ -164,20 +164,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-// 1-D bulk async copy shared → global (SASS: UBLKCP), tracked by a bulk group.  The
-// shared data must be made visible to the async proxy first (fence_proxy_async).
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-
-__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
-               "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void bulk_commit_and_wait_read() {
-  asm volatile("cp.async.bulk.commit_group;\n cp.async.bulk.wait_group.read 0;" ::: "memory");
-}
-
 // Non-coherent 16-byte load that the compiler cannot CSE (used to rematerialise
 // register-resident data instead of keeping it live across a rare slow path).
 __device__ __forceinline__ void ld_nc_v2(const double* p, double& x, double& y) {

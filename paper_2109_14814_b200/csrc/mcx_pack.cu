@@ -9,10 +9,12 @@
 // maps storage position → t so searches can emit original indices.
 //
 // Output is destination-ordered: the block's 1024 boxes (64 KB) are staged in shared
-// memory and leave with ONE bulk async copy (cp.async.bulk shared → global), perm with
-// coalesced 8-byte stores, and the level boxes of the block come from the same
-// registers: 16 quads (a half warp) = one 32-record group (shuffles), 8 warps = one
-// 512-record tile, the CTA = one 1024-record block.  A union box is disjoint from
+// memory and leave as fully coalesced 16-byte stores (consecutive threads, consecutive
+// 16 B), perm with coalesced 8-byte stores, and the level boxes of the block come from
+// the same registers: 16 quads (a half warp) = one 32-record group (shuffles), 8 warps
+// = one 512-record tile, the CTA = one 1024-record block.  (A single cp.async.bulk
+// shared → global copy measured the same and is invisible to compute-sanitizer's
+// initcheck, which then flags every later read of the boxes.)  A union box is disjoint from
 // another box only if every member is, so culling never changes the hit set.
 //
 // Per record: 16 B of grid read (each vertex is shared by 4 quads; L1), 64 B box +
@@ -93,13 +95,13 @@ __global__ void __launch_bounds__(PACK_THREADS, 3) pack_kernel(const double* __r
     if (perm) reinterpret_cast<uint2*>(perm)[sq] = make_uint2(t0, t0 + 1);
   }
   if (status && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status, 1u);
-  // every generic smem write above must be visible to the bulk copy engine
-  fence_proxy_async();
   __syncthreads();
-  if (tid == 0) {
+  {
     const uint64_t r0 = blk * A_BLOCK;
-    const uint64_t nrec = min((uint64_t)A_BLOCK, n - r0);
-    bulk_s2g(box + r0, S.box, (uint32_t)(nrec * sizeof(Box)));
+    const uint32_t n16 = (uint32_t)(min((uint64_t)A_BLOCK, n - r0) * (sizeof(Box) / 16));
+    const uint4* src = reinterpret_cast<const uint4*>(S.box);
+    uint4* dst = reinterpret_cast<uint4*>(box + r0);
+    for (uint32_t q = tid; q < n16; q += PACK_THREADS) dst[q] = src[q];
   }
   if (gbox) {
     // group = 16 consecutive storage quads = half a warp
@@ -141,7 +143,6 @@ __global__ void __launch_bounds__(PACK_THREADS, 3) pack_kernel(const double* __r
       }
     }
   }
-  if (tid == 0) bulk_commit_and_wait_read();  // shared memory must outlive the copy's reads
 }
 
 // Culling hierarchy of an arbitrary box array: one CTA per 1024-record block.  Each
