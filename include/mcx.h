@@ -58,7 +58,8 @@ extern "C" {
 #define MCX_MODE_CULL 1      /* exact union-box culling first                          */
 #define MCX_MODE_PREFILTER 2 /* every pair tested, first by a conservative packed-
                                 integer test on 3-bit quantised boxes (fma + alu
-                                pipes), its rare passes by the exact FP64 test         */
+                                pipes), its rare passes by the exact FP64 test; calls
+                                below 2^28 pairs use the FP64 sweep (faster there)   */
 
 /* Pipelines (what is searched). */
 #define MCX_PIPE_TRIANGLE 0 /* triangle pairs: triangle AABB test, then the precise test */

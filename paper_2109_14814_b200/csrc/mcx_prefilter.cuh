@@ -362,8 +362,9 @@ static int launch_local_cfg(std::vector<SearchParams>& T, Batch& Bt, std::vector
 }
 
 // Variant selection (MCX_VARIANT, experiments; 0 = the tuned default: 16 A records per
-// thread, 2-warp CTAs, 8 CTAs/SM, one frame per warp, one vote per 64 B records, one
-// LOP3 per two pair tests, 4 of 16 subtractions on the alu pipe — DESIGN.md §5).
+// thread, 2-warp CTAs, 9 CTAs/SM (86 registers: the survivor flush only appends to the
+// candidate list), one frame per warp, one vote per 64 B records, one LOP3 per two pair
+// tests, 4 of 16 subtractions on the alu pipe — DESIGN.md §5).
 static int launch_prefilter(std::vector<SearchParams>& T, Batch& Bt, std::vector<uint64_t>& prefix,
                             void* dev_tab, const std::vector<FboxJob>& jobs, void* dev_jobs, int device,
                             cudaStream_t stream) {
@@ -381,7 +382,12 @@ static int launch_prefilter(std::vector<SearchParams>& T, Batch& Bt, std::vector
     case 10: return MCX_LOCAL(8, 8, 1, 1, true, true);
     case 11: return MCX_LOCAL(16, 32, 1, 8, true, true, 4);
     case 12: return MCX_LOCAL(16, 16, 1, 8, true, true, 4);
-    default: return MCX_LOCAL(16, 64, 1, 8, true, true, 4);
+    case 13: return MCX_LOCAL(16, 64, 1, 9, true, true, 4);   // 9 CTAs/SM (112 registers)
+    case 14: return MCX_LOCAL(16, 64, 1, 10, true, true, 4);  // 10 CTAs/SM
+    case 15: return MCX_LOCAL(16, 32, 1, 10, true, true, 4);  // one vote per 32 B records, 10 CTAs/SM
+    case 16: return MCX_LOCAL(16, 32, 1, 9, true, true, 4);
+    case 17: return MCX_LOCAL(16, 64, 1, 8, true, true, 4);  // round 1 default (8 CTAs/SM, 116 registers)
+    default: return MCX_LOCAL(16, 64, 1, 9, true, true, 4);
   }
 #undef MCX_LOCAL
 }

@@ -598,17 +598,30 @@ static WsLayout ws_layout(const mcx_task* tasks, uint32_t n, const mcx_opts* o) 
   return L;
 }
 
-// Per-task stats and status from the workspace header (h: 8 shared + 8 per task u64s).
+// MCX_MODE_PREFILTER below this many pairs per call runs the FP64 sweep instead: the
+// quantised sweep's per-warp setup (frames, A words, B quantisation) and its slow path
+// dominate small or dense batches (measured crossover between 6.7e7 and 1.1e9 pairs,
+// DESIGN.md §5); results are identical either way.
+// MCX_PREFILTER_MIN_PAIRS overrides it (tests use 0 to exercise the quantised kernel on
+// small inputs).
+static uint64_t prefilter_min_pairs() {
+  const char* v = getenv("MCX_PREFILTER_MIN_PAIRS");
+  return v ? strtoull(v, nullptr, 10) : (1ull << 28);
+}
+
+// Per-task stats and status from the workspace header (h: 8 shared + 8 per task u64s;
+// h[4] = 1 if MCX_MODE_PREFILTER ran as the FP64 sweep).
 int batch_stats(const unsigned long long* h, uint32_t n, const mcx_opts* o, uint64_t cap, mcx_stats* st, float ms) {
   const bool spec = o->pipeline == MCX_PIPE_SPEC;
+  const int mode = (o->mode == MCX_MODE_PREFILTER && (h[4] & 0xff)) ? MCX_MODE_BRUTE : o->mode;
   const uint64_t cand_cap = o->cand_cap ? o->cand_cap : MCX_DEFAULT_CAND_CAP;
   for (uint32_t t = 0; t < n; ++t) {
     const unsigned long long* c = h + 8 + 8ull * t;
     st[t].n_hits = c[0];
     st[t].n_aabb_pass = c[1];
     st[t].n_singular = c[2];
-    st[t].n_tested = o->mode == MCX_MODE_CULL ? c[3] : st[t].n_pairs;
-    st[t].n_exact_tests = o->mode == MCX_MODE_BRUTE ? st[t].n_pairs : c[3];
+    st[t].n_tested = mode == MCX_MODE_CULL ? c[3] : st[t].n_pairs;
+    st[t].n_exact_tests = mode == MCX_MODE_BRUTE ? st[t].n_pairs : c[3];
     st[t].n_candidates = spec ? c[4] : c[1];
     st[t].kernel_ms = ms;
   }
@@ -719,6 +732,10 @@ int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mcx_hit* 
     st[t].n_pairs = spec ? (g.na / 2) * (B->n_tri / 2) : g.na * B->n_tri;
   }
   CUDA_TRY(cudaMemsetAsync(ws, 0, L.counters + 64ull * n, stream));
+  uint64_t batch_pairs = 0;
+  for (uint32_t t = 0; t < n; ++t) batch_pairs += st[t].n_pairs;
+  const bool pf_as_brute = o->mode == MCX_MODE_PREFILTER && batch_pairs < prefilter_min_pairs();
+  if (pf_as_brute) CUDA_TRY(cudaMemsetAsync(ws + 32, 1, 1, stream));  // header word 4: "ran as the FP64 sweep"
   Batch Bt = {};
   Bt.n_tasks = n;
   Bt.hits = hits;
@@ -739,7 +756,8 @@ int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mcx_hit* 
   }
   std::vector<uint64_t> prefix;
   int rc = spec ? launch_cull<KIND_SPEC>(T, Bt, prefix, ws + L.table, o->device, stream)
-                 : o->mode == MCX_MODE_BRUTE ? launch_brute<KIND_TRI>(T, Bt, prefix, ws + L.table, o->device, stream)
+                 : (o->mode == MCX_MODE_BRUTE || pf_as_brute)
+                     ? launch_brute<KIND_TRI>(T, Bt, prefix, ws + L.table, o->device, stream)
                  : o->mode == MCX_MODE_CULL ? launch_cull<KIND_TRI>(T, Bt, prefix, ws + L.table, o->device, stream)
                                             : launch_prefilter(T, Bt, prefix, ws + L.table, jobs, ws + L.jobs,
                                                                o->device, stream);

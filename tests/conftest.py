@@ -3,6 +3,11 @@ import sys
 
 import pytest
 
+# the GPU tests exercise the quantised prefilter kernel on small inputs too (by default
+# MCX_MODE_PREFILTER runs the FP64 sweep below 2^28 pairs per call); test_prefilter_size_rule
+# checks the default rule explicitly
+os.environ.setdefault("MCX_PREFILTER_MIN_PAIRS", "0")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)

@@ -876,3 +876,17 @@ def test_orientation_swap_bit_identical(mode, oracle_lib):
     spec = D.search_device(Am, Bm, mode=_lib.MODE_CULL, pipeline=_lib.PIPE_SPEC, orient=_lib.ORIENT_AS_GIVEN)
     spec2 = D.search_device(Am, Bm, mode=_lib.MODE_CULL, pipeline=_lib.PIPE_SPEC, orient=_lib.ORIENT_LARGER_A)
     assert np.array_equal(spec.hits, spec2.hits) and spec.stats["n_candidates"] == spec2.stats["n_candidates"]
+
+
+def test_prefilter_size_rule(monkeypatch):
+    """By default MCX_MODE_PREFILTER runs the FP64 sweep for calls below 2^28 pairs (C1:
+    6.5e7; every pair then gets the exact test) and the quantised sweep above (C2: 1.7e10,
+    exact tests only on quantised passes); hits are identical either way."""
+    monkeypatch.delenv("MCX_PREFILTER_MIN_PAIRS", raising=False)
+    for name, quantised in (("C1", False), ("C2", True)):
+        A, _, B, _ = config_pair(name)
+        Am, Bm = D.DeviceMesh(A, 0), D.DeviceMesh(B, 0)
+        rp = D.search_device(Am, Bm, mode=_lib.MODE_PREFILTER)
+        rb = D.search_device(Am, Bm, mode=_lib.MODE_BRUTE)
+        assert np.array_equal(rp.hits, rb.hits)
+        assert (rp.stats["n_exact_tests"] < rp.stats["n_pairs"]) == quantised
