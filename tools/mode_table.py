@@ -1,8 +1,12 @@
 """Kernel time of every search mode on every BASELINE config (+ the C5hd and dense
 self-search stress shapes): one JSON line per (config, mode), median of 5 timed calls
-with inputs resident.  `python tools/mode_table.py > profiles/r01_modes.jsonl`"""
+with inputs resident (MCX_MODE_PREFILTER forced onto the quantised kernel for every size
+so the table compares the kernels; by default calls under 2^28 pairs use the FP64 sweep).
+`python tools/mode_table.py > profiles/r02_modes.jsonl`"""
 import json
 import os
+
+os.environ.setdefault("MCX_PREFILTER_MIN_PAIRS", "0")
 import statistics
 import sys
 
