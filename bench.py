@@ -248,9 +248,9 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ our arm
-# our kernels per search call: brute = box sweep + solve + status check; cull = 2 cull levels +
-# solve + status; prefilter = fp32 boxes + box sweep + solve + status
-KERNEL_LAUNCHES = {"brute": 3, "cull": 4, "prefilter": 4}
+# our kernels per search call: brute = box sweep + solve (which also checks the meshes'
+# non-finite flags); cull = 2 cull levels + solve; prefilter = fp32 boxes + box sweep + solve
+KERNEL_LAUNCHES = {"brute": 2, "cull": 3, "prefilter": 3}
 INT_LANES_PER_CLK_PER_SM = 64  # B200 fma-heavy (IMAD) and alu (LOP3) pipes, each; IMAD measured 62.7 lanes/clk/SM
                                # (tools/microbench/hprefilter.cu swar3_mix0); issue: 4 SMSP x 32 = 128 lanes/clk/SM
 # SASS of the prefilter inner loop, per 16 pair tests: 8 IMAD + 4 IMAD.X (fma-heavy pipe),
@@ -611,11 +611,15 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu_reference_sample(A, B, rows=1024)  # warm-up, as the reference arm does
-        s = cpu_reference_sample(A, B)
-        cpu = {"value": s["value"], "unit": UNIT, "cores": s["threads"], "kind": "port",
+        cpu_steps = min(max(args.steps, 1), 5)
+        runs = [cpu_reference_sample(A, B) for _ in range(cpu_steps)]
+        s = runs[-1]
+        cpu = {"value": sum(r["pairs"] for r in runs) / sum(r["seconds"] for r in runs), "unit": UNIT,
+               "cores": s["threads"], "kind": "port",
                "sample": f"C port of the SPEC all-pairs search, A triangles [0, {s['a_triangles']}) x all B "
-                         f"({s['pairs']:.3e} pairs, {s['seconds']:.1f} s, packing excluded) - the same slice and "
-                         "code as one step of --impl reference", "cpu": cpu_model(),
+                         f"({s['pairs']:.3e} pairs per step, packing excluded), mean of {cpu_steps} steps after a "
+                         "warm-up - the same slice, code and protocol as --impl reference",
+               "step_values": [r["value"] for r in runs], "cpu": cpu_model(),
                "numpy_parallel": cpu_numpy_parallel_sample(A, B),
                "spec_literal_serial": cpu_spec_literal_sample(A, B)}
         # the culling counterpart on the CPU: the C oracle's exact x-sweep-and-prune over the

@@ -931,7 +931,7 @@ static int load_mesh(mcx_context* c, const double* coords, uint32_t N, uint32_t 
   // the last chunk's packing follows the last byte of the H2D copy.
   const uint32_t MQ = M - 1, ntr = (MQ + ORDER_TILE_Q - 1) / ORDER_TILE_Q;
   const uint64_t nblk = pack_blocks(N, M), plane = (uint64_t)N * M * 8;
-  const uint32_t nch = n >= (1u << 18) ? std::min<uint32_t>(4, ntr) : 1;
+  const uint32_t nch = std::min<uint32_t>(n >= (1u << 20) ? 8 : (n >= (1u << 18) ? 4 : 1), ntr);
   uint64_t b_done = 0;
   uint32_t col_done = 0;
   for (uint32_t j = 0; j < nch && e == cudaSuccess && rc == MCX_OK; ++j) {

@@ -762,14 +762,17 @@ int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mcx_hit* 
                                             : launch_prefilter(T, Bt, prefix, ws + L.table, jobs, ws + L.jobs,
                                                                o->device, stream);
   if (rc != MCX_OK) return rc;
-  if (Bt.tasks) {  // no work units → no table, no candidates
+  if (Bt.tasks) {  // the solve stage also ORs the tasks' non-finite flags into the header
+    Bt.status_flag = reinterpret_cast<unsigned long long*>(ws) + 2;
     rc = spec ? launch_solve<KIND_SPEC>(Bt, o->device, stream) : launch_solve<KIND_TRI>(Bt, o->device, stream);
     if (rc != MCX_OK) return rc;
+  } else {  // no work units → no table upload by a launcher: check the flags directly
+    CUDA_TRY(h2d_async(ws + L.table, T.data(), sizeof(SearchParams) * n, stream));
+    status_kernel<<<1, 32, 0, stream>>>(reinterpret_cast<const SearchParams*>(ws + L.table), n,
+                                        reinterpret_cast<unsigned long long*>(ws) + 2);
+    CUDA_TRY(cudaGetLastError());
   }
   if (o->timing) CUDA_TRY(cudaEventRecord(tm.e1, stream));
-  status_kernel<<<1, 32, 0, stream>>>(reinterpret_cast<const SearchParams*>(ws + L.table), n,
-                                      reinterpret_cast<unsigned long long*>(ws) + 2);
-  CUDA_TRY(cudaGetLastError());
   if (h_counters) {  // asynchronous: the caller synchronises and calls batch_stats
     CUDA_TRY(cudaMemcpyAsync(h_counters, ws, sizeof(unsigned long long) * (8 + 8ull * n), cudaMemcpyDeviceToHost,
                              stream));

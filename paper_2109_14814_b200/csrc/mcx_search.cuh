@@ -89,6 +89,7 @@ struct Batch {
   uint64_t* gids;                // KIND_QUAD output
   uint64_t cap;
   unsigned long long* emit;      // shared output position counter
+  unsigned long long* status_flag;  // header word: any task's mesh has non-finite coordinates
   uint4* cand;                   // box-test survivors {A index, B index, task, 0} (compacted)
   uint64_t cand_cap;
   unsigned long long* cand_count;
@@ -180,6 +181,15 @@ template <int KIND>
 __global__ void __launch_bounds__(256) solve_kernel(const Batch Bt) {
   const uint64_t n = min((uint64_t)*(volatile unsigned long long*)Bt.cand_count, Bt.cand_cap);
   const int lane = threadIdx.x & 31;
+  if (blockIdx.x == 0 && threadIdx.x < 32 && Bt.status_flag) {
+    // OR of every task's mcx_pack non-finite flags into the header (no separate launch)
+    unsigned v = 0;
+    for (uint32_t t = threadIdx.x; t < Bt.n_tasks; t += 32) {
+      if (Bt.tasks[t].statusA) v |= *Bt.tasks[t].statusA;
+      if (Bt.tasks[t].statusB) v |= *Bt.tasks[t].statusB;
+    }
+    if (__any_sync(0xffffffffu, v != 0) && threadIdx.x == 0) atomicOr(Bt.status_flag, 1ull);
+  }
   for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < n; base += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t k = base + threadIdx.x;
     const bool valid = k < n;
