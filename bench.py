@@ -411,10 +411,10 @@ def run_ours(args):
                        "MEASURED_PEAKS.json has no FP64 entry)",
         "work_per_launch": "8 FP64 compare lane-ops per pair + ~100 FP64 lane-ops per AABB survivor",
         "kernel_ms": st["kernel_ms"],
-        "traffic": (2140494000.0 + 14626304.0) if args.config == "C3" else None,
+        "traffic": (1935119000.0 + 16355584.0) if args.config == "C3" else None,
         "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum of one C3 launch, ncu --set full "
-                        "(profiles/r01_ncu_brute_c3.txt): 2.16 GB vs 68 GB of algorithmic L2->SMEM tile "
-                        "traffic; B's 67 MB of boxes are re-read from HBM ~32x per launch (L2 is split "
+                        "(profiles/r02_ncu_brute_c3.txt): 1.95 GB vs 68 GB of algorithmic L2->SMEM tile "
+                        "traffic; B's 67 MB of boxes are re-read from HBM ~29x per launch (L2 is split "
                         "over two dies) at ~4 GB/s - negligible against the FP64 bound"}
     # ---- roofline of the prefilter kernel: every pair = 12/16 IMAD-class op (fma-heavy pipe,
     # 64 lanes/clk/SM) + 4/16 IADD3 + 1/2 LOP3 (alu pipe, 64 lanes/clk/SM): 1.5 instructions per
@@ -434,9 +434,9 @@ def run_ours(args):
                            "n_exact_tests FP64 box tests",
         "exact_tests_per_step": pst["n_exact_tests"], "kernel_ms": pst["kernel_ms"],
         "kernel_ms_note": "CUDA events around the whole call: fp32 box kernel (~0.03 ms) + search",
-        "traffic": (68652288.0 + 3390464.0) if args.config == "C3" else None,
+        "traffic": (68277760.0 + 3075840.0) if args.config == "C3" else None,
         "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum of one C3 launch, ncu --set full "
-                        "(profiles/r01_ncu_prefilter_c3.txt): B's 33 MB of fp32 boxes + A's, read ~once; the "
+                        "(profiles/r02_ncu_prefilter_c3.txt): B's 33 MB of fp32 boxes + A's, read ~once; the "
                         "1.1e12 pair tests touch only registers and shared memory"}
     roofline = pf_roofline if primary == "prefilter" else fp64_roofline
     fp64_block = {"mode": "brute", "value": brute["value"], "unit": UNIT, "ms_per_step": brute["ms_per_step"],
