@@ -91,6 +91,10 @@ typedef struct mcx_mesh_dev {
   const double* bbox;     /* device, [⌈n/1024⌉][8]                                   */
   const uint32_t* status; /* device flag written by mcx_pack (nonzero: non-finite
                              coordinates); checked by the searches; may be NULL      */
+  uint32_t plane_rows;    /* rows between the x, y, px, py planes: 0 → M (a contiguous
+                             grid); the parent's M when coords is a column range of a
+                             larger resident grid (a half-layer view, mcx_mesh_view_columns) */
+  uint32_t reserved;
 } mcx_mesh_dev;
 
 /* One intersecting triangle pair: A triangle ia, B triangle ib (original indices
@@ -266,6 +270,15 @@ int mcx_mesh_load(mcx_context* ctx, const double* coords, uint32_t N, uint32_t M
                   mcx_mesh** mesh);
 int mcx_mesh_free(mcx_mesh* mesh);
 const mcx_mesh_dev* mcx_mesh_view(const mcx_mesh* mesh);
+
+/* A whole globalized mesh uploaded once, NOT packed: the source of zero-copy half-layer
+ * views (a half-layer is a contiguous column range of its mesh). */
+int mcx_grid_load(mcx_context* ctx, const double* coords, uint32_t N, uint32_t M, const double* s_values,
+                  mcx_mesh** grid);
+/* The half-layer of columns [c0, c1] (c1 > c0) of a resident grid or mesh, packed on the
+ * device from the parent's memory (no upload; plane_rows = the parent's M).  The parent
+ * must outlive the view. */
+int mcx_mesh_view_columns(mcx_context* ctx, const mcx_mesh* parent, uint32_t c0, uint32_t c1, mcx_mesh** view);
 
 typedef struct mcx_job {
   const mcx_mesh* A;   /* unstable half-layer U_n1^sign1                                */

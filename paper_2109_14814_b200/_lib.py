@@ -31,7 +31,8 @@ ORIENT_AS_GIVEN, ORIENT_LARGER_A = 0, 1
 EXPORTS = ("mcx_a_block", "mcx_workspace_bytes", "mcx_batch_workspace_bytes", "mcx_pack", "mcx_levels",
            "mcx_search", "mcx_search_batch", "mcx_pair_candidates", "mcx_pair_candidates_mesh",
            "mcx_pair_candidates_mesh_workspace_bytes", "mcx_records", "mcx_context_create",
-           "mcx_context_destroy", "mcx_mesh_load", "mcx_mesh_free", "mcx_mesh_view", "mcx_intersect",
+           "mcx_context_destroy", "mcx_mesh_load", "mcx_mesh_free", "mcx_mesh_view", "mcx_grid_load",
+           "mcx_mesh_view_columns", "mcx_intersect",
            "mcx_find_intersections", "mcx_finish_hits", "mcx_format_g17", "mcx_last_error", "mcx_version")
 
 
@@ -39,7 +40,7 @@ class MeshDev(ctypes.Structure):
     _fields_ = [("n_tri", ctypes.c_uint64), ("coords", ctypes.c_void_p), ("N", ctypes.c_uint32),
                 ("M", ctypes.c_uint32), ("box", ctypes.c_void_p), ("perm", ctypes.c_void_p),
                 ("gbox", ctypes.c_void_p), ("tbox", ctypes.c_void_p), ("bbox", ctypes.c_void_p),
-                ("status", ctypes.c_void_p)]
+                ("status", ctypes.c_void_p), ("plane_rows", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
 
 
 class Task(ctypes.Structure):
@@ -148,6 +149,10 @@ def _load():
     L.mcx_mesh_free.argtypes = [vp]
     L.mcx_mesh_view.restype = P(MeshDev)
     L.mcx_mesh_view.argtypes = [vp]
+    L.mcx_grid_load.restype = i32
+    L.mcx_grid_load.argtypes = [vp, vp, u32, u32, vp, P(vp)]
+    L.mcx_mesh_view_columns.restype = i32
+    L.mcx_mesh_view_columns.argtypes = [vp, vp, u32, u32, P(vp)]
     cp = ctypes.c_char_p
     L.mcx_intersect.restype = i32
     L.mcx_intersect.argtypes = [vp, P(Job), u32, P(FindOpts), P(P(Record)), P(u64), P(vp), P(u64), P(Stats)]

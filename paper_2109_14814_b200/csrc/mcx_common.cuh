@@ -178,26 +178,6 @@ __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a,
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 
-// Vertices of original triangle t = 2·(i + N·k) + τ of a (4, M, N) grid, −0.0
-// canonicalised (x + 0.0): T¹ = (v00, v10, v01), T² = (v01, v10, v11), i + 1 mod N
-// (the packing origin is the first vertex).  Used
-// by pack_kernel for the boxes and by the solve, so both see identical vertices.
-__device__ __forceinline__ void tri_verts(const double* __restrict__ c, uint32_t N, uint32_t M, uint32_t t,
-                                          double v0[4], double v1[4], double v2[4]) {
-  const uint32_t q = t >> 1, tau = t & 1;
-  const uint32_t i = q % N, k = q / N;
-  const uint32_t ip = (i + 1 == N) ? 0 : i + 1;
-  const uint64_t r0 = (uint64_t)k * N, r1 = r0 + N;
-  const uint64_t plane = (uint64_t)M * N;
-#pragma unroll
-  for (int d = 0; d < 4; ++d) {
-    const double* pl = c + d * plane;
-    v0[d] = dadd(__ldg(pl + (tau ? r1 : r0) + i), 0.0);
-    v1[d] = dadd(__ldg(pl + r0 + ip), 0.0);
-    v2[d] = dadd(__ldg(pl + r1 + (tau ? ip : i)), 0.0);
-  }
-}
-
 // Vertex addressing of original triangle t for the solve.  The solve reads vertices
 // through non-CSE-able loads and re-derives an edge each time it needs one: the
 // values (and bits) are those of the packing, v + 0.0 then v1 − v0, while the live
@@ -207,14 +187,15 @@ struct TriRef {
   uint32_t plane, o[3];  // plane stride; offsets of v0, v1, v2 within a plane (N·M < 2^32)
 };
 
-__device__ __forceinline__ TriRef tri_ref(const double* c, uint32_t N, uint32_t M, uint32_t t) {
+// Mp = rows between the x, y, px, py planes (M, or the parent grid's M for a column view).
+__device__ __forceinline__ TriRef tri_ref(const double* c, uint32_t N, uint32_t Mp, uint32_t t) {
   const uint32_t q = t >> 1, tau = t & 1;
   const uint32_t i = q % N, k = q / N;
   const uint32_t ip = (i + 1 == N) ? 0 : i + 1;
   const uint32_t r0 = k * N, r1 = r0 + N;
   TriRef T;
   T.c = c;
-  T.plane = M * N;
+  T.plane = Mp * N;
   T.o[0] = (tau ? r1 : r0) + i;
   T.o[1] = r0 + ip;
   T.o[2] = r1 + (tau ? ip : i);
@@ -271,13 +252,13 @@ __device__ __forceinline__ double dot4(const double c[4], const double x[4]) {
 }
 
 // The precise test of original triangles ta of grid A and tb of
-// grid B.  Returns 0 = miss, 1 = hit (sol = s, t, a, b), 2 = singular (gate,
+// grid B (MpA / MpB: their plane strides in rows, see tri_ref).  Returns 0 = miss, 1 = hit (sol = s, t, a, b), 2 = singular (gate,
 // SPEC.md:464).  Only AABB survivors get here (1e-7..1e-3 of the pairs), so the
 // triangle geometry is rebuilt from the grids (L1/L2) instead of being stored.
-__device__ __forceinline__ int solve_tri(const double* __restrict__ cA, uint32_t NA, uint32_t MA, uint32_t ta,
-                                         const double* __restrict__ cB, uint32_t NB, uint32_t MB, uint32_t tb,
+__device__ __forceinline__ int solve_tri(const double* __restrict__ cA, uint32_t NA, uint32_t MpA, uint32_t ta,
+                                         const double* __restrict__ cB, uint32_t NB, uint32_t MpB, uint32_t tb,
                                          double sol[4]) {
-  const TriRef A = tri_ref(cA, NA, MA, ta), B = tri_ref(cB, NB, MB, tb);
+  const TriRef A = tri_ref(cA, NA, MpA, ta), B = tri_ref(cB, NB, MpB, tb);
   double Pa[6], Qb[6], nA, nB;
   biv_norm(A, Pa, nA);
   biv_norm(B, Qb, nB);
@@ -317,7 +298,7 @@ __device__ __forceinline__ int solve_tri(const double* __restrict__ cA, uint32_t
 // (4, M, N) grid; vertices v00 v10 v01 v11; projection (x, y, px).
 #define MCX_DEGEN_RTOL2 1e-28
 
-__device__ __forceinline__ void quad_verts(const double* __restrict__ c, uint32_t N, uint32_t M, uint32_t q,
+__device__ __forceinline__ void quad_verts(const double* __restrict__ c, uint32_t N, uint32_t Mp, uint32_t q,
                                            double V[4][3]) {
   const uint32_t i = q % N, k = q / N;
   const uint32_t ip = (i + 1 == N) ? 0 : i + 1;
@@ -326,7 +307,7 @@ __device__ __forceinline__ void quad_verts(const double* __restrict__ c, uint32_
 #pragma unroll
   for (int v = 0; v < 4; ++v)
 #pragma unroll
-    for (int d = 0; d < 3; ++d) V[v][d] = __ldg(c + (uint64_t)d * M * N + idx[v]);
+    for (int d = 0; d < 3; ++d) V[v][d] = __ldg(c + (uint64_t)d * Mp * N + idx[v]);
 }
 
 // All four Vo vertices strictly on one side of the plane of T¹(Vq) and of T²(Vq).
@@ -362,11 +343,11 @@ __device__ __forceinline__ bool side_reject(const double Vq[4][3], const double 
   return out;
 }
 
-__device__ __forceinline__ bool moller_reject(const double* cA, uint32_t NA, uint32_t MA, uint32_t qa,
-                                              const double* cB, uint32_t NB, uint32_t MB, uint32_t qb) {
+__device__ __forceinline__ bool moller_reject(const double* cA, uint32_t NA, uint32_t MpA, uint32_t qa,
+                                              const double* cB, uint32_t NB, uint32_t MpB, uint32_t qb) {
   double VA[4][3], VB[4][3];
-  quad_verts(cA, NA, MA, qa, VA);
-  quad_verts(cB, NB, MB, qb, VB);
+  quad_verts(cA, NA, MpA, qa, VA);
+  quad_verts(cB, NB, MpB, qb, VB);
   return side_reject(VA, VB) || side_reject(VB, VA);
 }
 

@@ -11,8 +11,10 @@ namespace mcx {
 // mcx_pack.cu: the fused pack + levels kernel over 1024-record blocks [b0, b1) (b1 = 0:
 // all), enqueued on `stream` (device current); pack_blocks = the block count.
 uint64_t pack_blocks(uint32_t N, uint32_t M);
+// Mp = plane stride in rows (0 → M; the parent's M for a column view of a larger grid).
 int pack_enqueue(const double* coords, uint32_t N, uint32_t M, int order, double* box, uint32_t* perm, double* gbox,
-                 double* tbox, double* bbox, uint32_t* status, cudaStream_t stream, uint64_t b0, uint64_t b1);
+                 double* tbox, double* bbox, uint32_t* status, cudaStream_t stream, uint64_t b0, uint64_t b1,
+                 uint32_t Mp);
 
 // mcx_search.cu: a batch of searches (device current).  h_counters == nullptr:
 // synchronises o->stream and fills the stats.  Otherwise the workspace header (8 + 8·n

@@ -36,7 +36,7 @@ struct PackSmem {
 };
 
 __global__ void __launch_bounds__(PACK_THREADS, 3) pack_kernel(const double* __restrict__ coords, uint32_t N,
-                                                               uint32_t M, int tiled, Box* __restrict__ box,
+                                                               uint32_t M, uint32_t Mp, int tiled, Box* __restrict__ box,
                                                                uint32_t* __restrict__ perm, Box* __restrict__ gbox,
                                                                Box* __restrict__ tbox, Box* __restrict__ bbox,
                                                                uint32_t* __restrict__ status, uint32_t blk0) {
@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(PACK_THREADS, 3) pack_kernel(const double* __r
     // the quad's 4 vertices once (16 loads, all issued before use): T¹ = (v00, v10,
     // v01), T² = (v01, v10, v11) — the vertex sets of tri_verts, −0.0 canonicalised
     const uint32_t ip = (i + 1 == N) ? 0 : i + 1;
-    const uint64_t r0 = (uint64_t)k * N, r1 = r0 + N, plane = (uint64_t)M * N;
+    const uint64_t r0 = (uint64_t)k * N, r1 = r0 + N, plane = (uint64_t)Mp * N;  // Mp: plane stride in rows
     double w00[4], w10[4], w01[4], w11[4];
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
@@ -78,15 +78,20 @@ __global__ void __launch_bounds__(PACK_THREADS, 3) pack_kernel(const double* __r
       w01[c] = __ldg(pl + r1 + i);
       w11[c] = __ldg(pl + r1 + ip);
     }
+    // B200 has no FP64 min/max instruction (each is a DSETP + 2 selects), so the two
+    // triangles share min/max(v10, v01); min/max of finite non-NaN values is exact and
+    // order-free, so the boxes are the bits of the three-way min/max (NaN/Inf inputs flag
+    // the mesh as unusable anyway).
     Box b1, b2;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const double a = dadd(w00[c], 0.0), b = dadd(w10[c], 0.0), d = dadd(w01[c], 0.0), e = dadd(w11[c], 0.0);
       bad |= !(isfinite(a) && isfinite(b) && isfinite(d) && isfinite(e));
-      b1.lo[c] = fmin(fmin(a, b), d);
-      b1.hi[c] = fmax(fmax(a, b), d);
-      b2.lo[c] = fmin(fmin(d, b), e);
-      b2.hi[c] = fmax(fmax(d, b), e);
+      const double mn = fmin(b, d), mx = fmax(b, d);
+      b1.lo[c] = fmin(a, mn);
+      b1.hi[c] = fmax(a, mx);
+      b2.lo[c] = fmin(e, mn);
+      b2.hi[c] = fmax(e, mx);
       qlo[c] = fmin(b1.lo[c], b2.lo[c]);
       qhi[c] = fmax(b1.hi[c], b2.hi[c]);
     }
@@ -125,22 +130,23 @@ __global__ void __launch_bounds__(PACK_THREADS, 3) pack_kernel(const double* __r
       if (g < ng) gbox[g] = r;
     }
     __syncthreads();
-    if (tid < 3 && tbox && bbox) {
-      const int g0 = tid == 2 ? 0 : tid * (TILE / GROUP);
-      const int g1 = tid == 2 ? A_BLOCK / GROUP : g0 + TILE / GROUP;
-      Box r = S.gsm[g0];
-      for (int g = g0 + 1; g < g1; ++g)
+    if (tid < 32 && tbox && bbox) {
+      // warp 0: lane g holds group box g; 4 butterfly rounds give each 16-lane half its
+      // 512-record tile box, one more the 1024-record block box
+      Box r = S.gsm[tid];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        if (o == 16 && (tid & 15) == 0) {
+          const uint64_t tt = blk * (A_BLOCK / TILE) + (tid >> 4);
+          if (tt < (n + TILE - 1) / TILE) tbox[tt] = r;
+        }
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          r.lo[c] = fmin(r.lo[c], S.gsm[g].lo[c]);
-          r.hi[c] = fmax(r.hi[c], S.gsm[g].hi[c]);
+          r.lo[c] = fmin(r.lo[c], __shfl_xor_sync(0xffffffffu, r.lo[c], o));
+          r.hi[c] = fmax(r.hi[c], __shfl_xor_sync(0xffffffffu, r.hi[c], o));
         }
-      if (tid == 2) {
-        bbox[blk] = r;
-      } else {
-        const uint64_t tt = blk * (A_BLOCK / TILE) + tid;
-        if (tt < (n + TILE - 1) / TILE) tbox[tt] = r;
       }
+      if (tid == 0) bbox[blk] = r;
     }
   }
 }
@@ -205,7 +211,10 @@ uint64_t pack_blocks(uint32_t N, uint32_t M) { return (2ull * N * (M - 1) + A_BL
 // Enqueue the fused pack of blocks [b0, b1) (b1 = 0: all) on `stream` (device already
 // current).  The status flag is cleared by the launch that starts at block 0.
 int pack_enqueue(const double* coords, uint32_t N, uint32_t M, int order, double* box, uint32_t* perm, double* gbox,
-                 double* tbox, double* bbox, uint32_t* status, cudaStream_t stream, uint64_t b0, uint64_t b1) {
+                 double* tbox, double* bbox, uint32_t* status, cudaStream_t stream, uint64_t b0, uint64_t b1,
+                 uint32_t Mp) {
+  if (Mp == 0) Mp = M;
+  if (Mp < M) return set_error(MCX_E_ARG, "plane stride of %u rows < M = %u", Mp, M);
   if (N < 1 || M < 2) return set_error(MCX_E_ARG, "pack needs N >= 1 and M >= 2 (got N=%u, M=%u)", N, M);
   if (2ull * N * (M - 1) >= (1ull << 31)) return set_error(MCX_E_ARG, "triangle count must be < 2^31");
   if (order != MCX_ORDER_NATURAL && order != MCX_ORDER_TILED) return set_error(MCX_E_ARG, "unknown order %d", order);
@@ -225,7 +234,7 @@ int pack_enqueue(const double* coords, uint32_t N, uint32_t M, int order, double
   CUDA_TRY(cudaFuncSetAttribute(pack_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   if (status && b0 == 0) CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(uint32_t), stream));
   pack_kernel<<<(unsigned)(b1 - b0), PACK_THREADS, sizeof(PackSmem), stream>>>(
-      coords, N, M, order == MCX_ORDER_TILED, reinterpret_cast<Box*>(box), perm, reinterpret_cast<Box*>(gbox),
+      coords, N, M, Mp, order == MCX_ORDER_TILED, reinterpret_cast<Box*>(box), perm, reinterpret_cast<Box*>(gbox),
       reinterpret_cast<Box*>(tbox), reinterpret_cast<Box*>(bbox), status, (uint32_t)b0);
   CUDA_TRY(cudaGetLastError());
   return MCX_OK;
@@ -240,7 +249,7 @@ int mcx_pack(const double* coords, uint32_t N, uint32_t M, int order, double* bo
   using namespace mcx;
   DeviceGuard guard;
   CUDA_TRY(cudaSetDevice(device));
-  return pack_enqueue(coords, N, M, order, box, perm, gbox, tbox, bbox, status, (cudaStream_t)stream, 0, 0);
+  return pack_enqueue(coords, N, M, order, box, perm, gbox, tbox, bbox, status, (cudaStream_t)stream, 0, 0, M);
 }
 
 int mcx_levels(const double* box, uint64_t n_tri, double* gbox, double* tbox, double* bbox, int device,

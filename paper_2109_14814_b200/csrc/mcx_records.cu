@@ -22,7 +22,7 @@ __global__ void records_kernel(const mcx_hit* __restrict__ hits, uint64_t n, con
     }
     uint64_t g;
     double pt[4], pr[4];
-    record_fields(H, cA, NA, MA, sA, NB, MB, sB, g, pt, pr);
+    record_fields(H, cA, NA, MA, MA, sA, NB, MB, sB, g, pt, pr);
     gid[h] = g;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {

@@ -40,10 +40,11 @@ __device__ __forceinline__ bool hit_in_range(const mcx_hit& H, uint32_t NA, uint
   return (uint64_t)H.ia < 2ull * NA * (MA - 1) && (uint64_t)H.ib < 2ull * NB * (MB - 1);
 }
 
+// MpA: plane stride of A's grid in rows (MA for a contiguous grid).
 __device__ __forceinline__ void record_fields(const mcx_hit& H, const double* __restrict__ cA, uint32_t NA,
-                                              uint32_t MA, const double* __restrict__ sA, uint32_t NB, uint32_t MB,
-                                              const double* __restrict__ sB, uint64_t& gid, double point[4],
-                                              double params[4]) {
+                                              uint32_t MA, uint32_t MpA, const double* __restrict__ sA, uint32_t NB,
+                                              uint32_t MB, const double* __restrict__ sB, uint64_t& gid,
+                                              double point[4], double params[4]) {
   const int tauA = H.ia & 1, tauB = H.ib & 1;
   const uint32_t qa = H.ia >> 1, qb = H.ib >> 1;
   const uint32_t i = qa % NA, k1 = qa / NA, j = qb % NB, l1 = qb / NB;
@@ -52,7 +53,7 @@ __device__ __forceinline__ void record_fields(const mcx_hit& H, const double* __
   const uint32_t ip = (i + 1 == NA) ? 0 : i + 1;
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
-    const double* pl = cA + (uint64_t)c * MA * NA;
+    const double* pl = cA + (uint64_t)c * MpA * NA;
     const double v00 = pl[(uint64_t)k1 * NA + i], v10 = pl[(uint64_t)k1 * NA + ip];
     const double v01 = pl[(uint64_t)(k1 + 1) * NA + i], v11 = pl[(uint64_t)(k1 + 1) * NA + ip];
     const double p = tauA ? v01 : v00;

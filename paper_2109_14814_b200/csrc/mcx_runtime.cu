@@ -68,6 +68,7 @@ struct JobDev {
   const double* sB;
   uint32_t NA, MA, NB, MB;
   int32_t n1, sign1, n2, sign2;
+  uint32_t MpA, pad;  // plane stride of A's grid in rows
 };
 
 }  // namespace mcx
@@ -87,6 +88,7 @@ struct mcx_context {
 
 struct mcx_mesh {
   mcx_context* ctx = nullptr;
+  bool owns_grid = true;  // false for a column view: coords / s_values belong to the parent
   double *coords = nullptr, *s_values = nullptr, *box = nullptr, *gbox = nullptr, *tbox = nullptr, *bbox = nullptr;
   uint32_t *perm = nullptr, *status = nullptr;
   mcx_mesh_dev view{};
@@ -180,7 +182,7 @@ __global__ void record_kernel(const mcx_hit* __restrict__ hits, const uint32_t* 
     const uint32_t task = hit_task ? hit_task[k] : 0;
     const JobDev& J = jobs[task];
     mcx_record R;
-    record_fields(H, J.cA, J.NA, J.MA, J.sA, J.NB, J.MB, J.sB, R.gid, R.point, R.params);
+    record_fields(H, J.cA, J.NA, J.MA, J.MpA, J.sA, J.NB, J.MB, J.sB, R.gid, R.point, R.params);
     R.ia = H.ia;
     R.ib = H.ib;
     R.bary[0] = H.s; R.bary[1] = H.t; R.bary[2] = H.a; R.bary[3] = H.b;
@@ -445,7 +447,7 @@ __global__ void __launch_bounds__(1024) post_small_kernel(const mcx_hit* __restr
     const uint32_t t = hit_task ? hit_task[k] : 0u;
     const JobDev& J = jobs[t];
     mcx_record R;
-    record_fields(H, J.cA, J.NA, J.MA, J.sA, J.NB, J.MB, J.sB, R.gid, R.point, R.params);
+    record_fields(H, J.cA, J.NA, J.MA, J.MpA, J.sA, J.NB, J.MB, J.sB, R.gid, R.point, R.params);
     R.ia = H.ia;
     R.ib = H.ib;
     R.bary[0] = H.s; R.bary[1] = H.t; R.bary[2] = H.a; R.bary[3] = H.b;
@@ -815,6 +817,8 @@ static JobDev job_of(const mcx_mesh* A, const mcx_mesh* B, mcx_layer L) {
   j.MA = A->view.M;
   j.NB = B->view.N;
   j.MB = B->view.M;
+  j.MpA = A->view.plane_rows ? A->view.plane_rows : A->view.M;
+  j.pad = 0;
   j.n1 = L.n1;
   j.sign1 = L.sign1;
   j.n2 = L.n2;
@@ -848,6 +852,8 @@ static int intersect(mcx_context* c, const mcx_job* jobs, uint32_t n_jobs, const
   for (uint32_t t = 0; t < n_jobs; ++t) {
     if (!jobs[t].A || !jobs[t].B) return set_error(MCX_E_ARG, "job %u: null mesh", t);
     if (jobs[t].A->ctx != c || jobs[t].B->ctx != c) return set_error(MCX_E_ARG, "job %u: mesh of another context", t);
+    if (!jobs[t].A->box || !jobs[t].B->box)
+      return set_error(MCX_E_ARG, "job %u: an unpacked grid (mcx_grid_load) — search its column views", t);
     tasks[t] = mcx_task{&jobs[t].A->view, &jobs[t].B->view, 0, 0};
     jd[t] = job_of(jobs[t].A, jobs[t].B, jobs[t].layer);
   }
@@ -894,6 +900,19 @@ static int intersect(mcx_context* c, const mcx_job* jobs, uint32_t n_jobs, const
       if (total > c->hit_cap) c->hit_cap = total + 1024;
       continue;
     }
+    if (rc == MCX_E_ARG && hc[2]) {  // non-finite coordinates: name the failing task
+      for (uint32_t t = 0; t < n_jobs; ++t)
+        for (const mcx_mesh* m : {jobs[t].A, jobs[t].B}) {
+          uint32_t flag = 0;
+          if (m->status) CUDA_TRY(cudaMemcpy(&flag, m->status, sizeof(flag), cudaMemcpyDeviceToHost));
+          if (flag) {
+            const mcx_layer& L = jobs[t].layer;
+            return set_error(MCX_E_ARG, "job %u (layer pair %d %c %d %c): non-finite (NaN/Inf) coordinates in its %s "
+                             "half-layer", t, L.n1, L.sign1 >= 0 ? '+' : '-', L.n2, L.sign2 >= 0 ? '+' : '-',
+                             m == jobs[t].A ? "unstable (A)" : "stable (B)");
+          }
+        }
+    }
     if (rc) return rc;
     small_done = queued && take_small(c, records, n_records, text, text_bytes);
     break;
@@ -905,7 +924,7 @@ static int intersect(mcx_context* c, const mcx_job* jobs, uint32_t n_jobs, const
 }
 
 static int load_mesh(mcx_context* c, const double* coords, uint32_t N, uint32_t M, const double* s_values,
-                     cudaStream_t s, mcx_mesh** out) {
+                     cudaStream_t s, mcx_mesh** out, bool pack = true) {
   if (!coords || !s_values || !out) return set_error(MCX_E_ARG, "null argument");
   if (N < 1 || M < 2) return set_error(MCX_E_ARG, "a half-layer needs N >= 1 and M >= 2 (SPEC.md:473)");
   const uint64_t n = 2ull * N * (M - 1);
@@ -918,7 +937,17 @@ static int load_mesh(mcx_context* c, const double* coords, uint32_t N, uint32_t 
   };
   int rc = MCX_OK;
   if ((rc = alloc((void**)&m->coords, 32ull * N * M)) || (rc = alloc((void**)&m->s_values, 8ull * M)) ||
-      (rc = alloc((void**)&m->box, 64 * n)) || (rc = alloc((void**)&m->perm, 4 * n)) ||
+      (!pack && (cudaMemcpyAsync(m->s_values, s_values, 8ull * M, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+                 cudaMemcpyAsync(m->coords, coords, 32ull * N * M, cudaMemcpyHostToDevice, s) != cudaSuccess))) {
+    mcx_mesh_free(m);
+    return rc ? rc : set_error(MCX_E_CUDA, "grid upload failed");
+  }
+  if (!pack) {  // a grid: the source of column views only
+    m->view = mcx_mesh_dev{n, m->coords, N, M, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, M, 0};
+    *out = m;
+    return MCX_OK;
+  }
+  if ((rc = alloc((void**)&m->box, 64 * n)) || (rc = alloc((void**)&m->perm, 4 * n)) ||
       (rc = alloc((void**)&m->gbox, 64 * ((n + GROUP - 1) / GROUP))) ||
       (rc = alloc((void**)&m->tbox, 64 * ((n + TILE - 1) / TILE))) ||
       (rc = alloc((void**)&m->bbox, 64 * ((n + A_BLOCK - 1) / A_BLOCK))) || (rc = alloc((void**)&m->status, 16))) {
@@ -944,7 +973,7 @@ static int load_mesh(mcx_context* c, const double* coords, uint32_t N, uint32_t 
     const uint64_t b1 = last ? nblk : 2ull * N * std::min<uint32_t>(MQ, ORDER_TILE_Q * tr1) / A_BLOCK;
     if (e == cudaSuccess && b1 > b_done)  // (b1 = 0 would mean "all blocks" to pack_enqueue)
       rc = pack_enqueue(m->coords, N, M, MCX_ORDER_TILED, m->box, m->perm, m->gbox, m->tbox, m->bbox, m->status, s,
-                        b_done, b1);
+                        b_done, b1, M);
     b_done = std::max(b_done, b1);
     col_done = col1;
   }
@@ -953,7 +982,7 @@ static int load_mesh(mcx_context* c, const double* coords, uint32_t N, uint32_t 
     mcx_mesh_free(m);
     return rc;
   }
-  m->view = mcx_mesh_dev{n, m->coords, N, M, m->box, m->perm, m->gbox, m->tbox, m->bbox, m->status};
+  m->view = mcx_mesh_dev{n, m->coords, N, M, m->box, m->perm, m->gbox, m->tbox, m->bbox, m->status, M, 0};
   *out = m;
   return MCX_OK;
 }
@@ -1029,14 +1058,61 @@ int mcx_mesh_free(mcx_mesh* m) {
   mcx_context* c = m->ctx;
   DeviceGuard guard;
   cudaSetDevice(c->device);
-  for (void* p : {(void*)m->coords, (void*)m->s_values, (void*)m->box, (void*)m->perm, (void*)m->gbox, (void*)m->tbox,
-                  (void*)m->bbox, (void*)m->status})
+  for (void* p : {m->owns_grid ? (void*)m->coords : nullptr, m->owns_grid ? (void*)m->s_values : nullptr, (void*)m->box,
+                  (void*)m->perm, (void*)m->gbox, (void*)m->tbox, (void*)m->bbox, (void*)m->status})
     if (p) cudaFreeAsync(p, c->s0);
   delete m;
   return MCX_OK;
 }
 
 const mcx_mesh_dev* mcx_mesh_view(const mcx_mesh* m) { return m ? &m->view : nullptr; }
+
+int mcx_grid_load(mcx_context* c, const double* coords, uint32_t N, uint32_t M, const double* s_values,
+                  mcx_mesh** grid) {
+  using namespace mcx;
+  if (!c) return set_error(MCX_E_ARG, "null context");
+  DeviceGuard guard;
+  CUDA_TRY(cudaSetDevice(c->device));
+  int rc = load_mesh(c, coords, N, M, s_values, c->s0, grid, /*pack=*/false);
+  if (rc == MCX_OK) CUDA_TRY(cudaStreamSynchronize(c->s0));
+  return rc;
+}
+
+int mcx_mesh_view_columns(mcx_context* c, const mcx_mesh* parent, uint32_t c0, uint32_t c1, mcx_mesh** out) {
+  using namespace mcx;
+  if (!c || !parent || !out) return set_error(MCX_E_ARG, "null argument");
+  if (parent->ctx != c) return set_error(MCX_E_ARG, "parent grid of another context");
+  const uint32_t N = parent->view.N, Mp = parent->view.M;
+  if (!(c0 < c1 && c1 < Mp))
+    return set_error(MCX_E_ARG, "column range [%u, %u] must satisfy c0 < c1 < M = %u (SPEC.md:473)", c0, c1, Mp);
+  const uint32_t M = c1 - c0 + 1;
+  const uint64_t n = 2ull * N * (M - 1);
+  DeviceGuard guard;
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t s = c->s0;
+  mcx_mesh* m = new mcx_mesh();
+  m->ctx = c;
+  m->owns_grid = false;
+  m->coords = parent->coords + (uint64_t)c0 * N;
+  m->s_values = parent->s_values + c0;
+  auto alloc = [&](void** p, size_t bytes) -> int {
+    CUDA_TRY(cudaMallocFromPoolAsync(p, std::max<size_t>(bytes, 16), c->pool, s));
+    return MCX_OK;
+  };
+  int rc = MCX_OK;
+  if ((rc = alloc((void**)&m->box, 64 * n)) || (rc = alloc((void**)&m->perm, 4 * n)) ||
+      (rc = alloc((void**)&m->gbox, 64 * ((n + GROUP - 1) / GROUP))) ||
+      (rc = alloc((void**)&m->tbox, 64 * ((n + TILE - 1) / TILE))) ||
+      (rc = alloc((void**)&m->bbox, 64 * ((n + A_BLOCK - 1) / A_BLOCK))) || (rc = alloc((void**)&m->status, 16)) ||
+      (rc = pack_enqueue(m->coords, N, M, MCX_ORDER_TILED, m->box, m->perm, m->gbox, m->tbox, m->bbox, m->status, s,
+                         0, 0, Mp))) {
+    mcx_mesh_free(m);
+    return rc;
+  }
+  m->view = mcx_mesh_dev{n, m->coords, N, M, m->box, m->perm, m->gbox, m->tbox, m->bbox, m->status, Mp, 0};
+  *out = m;
+  return MCX_OK;
+}
 
 int mcx_intersect(mcx_context* c, const mcx_job* jobs, uint32_t n_jobs, const mcx_find_opts* fo,
                   const mcx_record** records, uint64_t* n_records, const char** text, uint64_t* text_bytes,

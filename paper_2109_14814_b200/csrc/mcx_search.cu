@@ -707,6 +707,8 @@ int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mcx_hit* 
     P.coordsA = A->coords;
     P.coordsB = B->coords;
     P.NA = A->N; P.MA = A->M; P.NB = B->N; P.MB = B->M;
+    P.MpA = A->plane_rows ? A->plane_rows : A->M;
+    P.MpB = B->plane_rows ? B->plane_rows : B->M;
     P.nA = A->n_tri;
     P.a_begin = a_begin;
     P.a_end = a_end;
@@ -842,6 +844,7 @@ static int launch_pair_candidates(const double* cA, uint32_t NA, uint32_t MA, co
   P.coordsA = cA;
   P.coordsB = cB;
   P.NA = NA; P.MA = MA; P.NB = NB; P.MB = MB;
+  P.MpA = MA; P.MpB = MB;
   Batch Bt = {};
   Bt.n_tasks = 1;
   Bt.gids = gids;
@@ -919,6 +922,8 @@ static int launch_pair_candidates_mesh(const mcx_mesh_dev* A, const mcx_mesh_dev
   P.coordsA = cA;
   P.coordsB = cB;
   P.NA = NA; P.MA = MA; P.NB = NB; P.MB = MB;
+  P.MpA = A->plane_rows ? A->plane_rows : MA;
+  P.MpB = B->plane_rows ? B->plane_rows : MB;
   *st = mcx_stats{};
   st->n_pairs = (g.na / 2) * (B->n_tri / 2);  // quad pairs
   CUDA_TRY(cudaMemsetAsync(ws, 0, L.counters + 64, stream));

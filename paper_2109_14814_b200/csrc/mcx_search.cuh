@@ -67,6 +67,7 @@ struct __align__(16) SearchParams {
   const double* coordsA;
   const double* coordsB;
   uint32_t NA, MA, NB, MB;
+  uint32_t MpA, MpB;  // plane strides in rows (the parent grid's M for a column view)
   // MCX_MODE_PREFILTER only: conservative fp32 boxes {lo_rd[4]}, {hi_ru[4]} per record
   float4* fA;
   float4* fB;
@@ -198,8 +199,8 @@ __global__ void __launch_bounds__(256) solve_kernel(const Batch Bt) {
     // the caller's (A, B) roles: the sweep may have run them exchanged (P.swapped)
     const double* cA = P.swapped ? P.coordsB : P.coordsA;
     const double* cB = P.swapped ? P.coordsA : P.coordsB;
-    const uint32_t NA = P.swapped ? P.NB : P.NA, MA = P.swapped ? P.MB : P.MA;
-    const uint32_t NB = P.swapped ? P.NA : P.NB, MB = P.swapped ? P.MA : P.MB;
+    const uint32_t NA = P.swapped ? P.NB : P.NA, MA = P.swapped ? P.MpB : P.MpA;  // MA/MB: plane rows
+    const uint32_t NB = P.swapped ? P.NA : P.NB, MB = P.swapped ? P.MpA : P.MpB;
     if (KIND == KIND_TRI) {
       double sol[4];
       int rc = 0;
@@ -214,7 +215,7 @@ __global__ void __launch_bounds__(256) solve_kernel(const Batch Bt) {
       }
       emit_hits(Bt, rc == 1, ia, ib, sol, c.z, P.counters, lane);
     } else if (KIND == KIND_QUAD) {
-      const bool cand = valid && !moller_reject(P.coordsA, P.NA, P.MA, c.x, P.coordsB, P.NB, P.MB, c.y);
+      const bool cand = valid && !moller_reject(P.coordsA, P.NA, P.MpA, c.x, P.coordsB, P.NB, P.MpB, c.y);
       if (valid && !cand) atomicAdd(P.counters + 2, 1ull);
       const unsigned hm = __ballot_sync(0xffffffffu, cand);
       if (hm) {

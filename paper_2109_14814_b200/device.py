@@ -103,7 +103,7 @@ class DeviceMesh:
             self._struct = _lib.MeshDev(self.n_tri, self.coords.data_ptr(), self.N, self.M, self.box.data_ptr(),
                                         self.perm.data_ptr() if self.perm is not None else None,
                                         self.gbox.data_ptr(), self.tbox.data_ptr(), self.bbox.data_ptr(),
-                                        self.status.data_ptr())
+                                        self.status.data_ptr(), self.M, 0)
             self._struct_ptr = ctypes_pointer(self._struct)
         return self._struct
 

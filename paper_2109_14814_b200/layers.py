@@ -133,13 +133,14 @@ def plan_parts(u_mesh, s_mesh, plan, n_parts: int):
 
 
 def run_part(halves, plan, mine, device: int, mode: int, pipeline: int, dedup: bool, text: bool):
-    """One GPU's share: upload and pack each half-layer its tasks need once, one
-    mcx_intersect over the tasks.  Returns (records with task = index into ``mine``, text,
+    """One GPU's share: each mesh its tasks need uploaded once (mcx_grid_load), every
+    half-layer a zero-copy column view of it packed in place, one mcx_intersect over the
+    tasks.  Returns (records with task = index into ``mine``, text,
     per-task stats)."""
     if not mine:
         return np.zeros(0, runtime.RECORD_DTYPE), b"", []
     ctx = runtime.context(device)
-    meshes = {}
+    grids, meshes = {}, {}
     try:
         jobs = []
         for k in mine:
@@ -147,13 +148,18 @@ def run_part(halves, plan, mine, device: int, mode: int, pipeline: int, dedup: b
             for key in (("u", n1, s1), ("s", n2, s2)):
                 if key not in meshes:
                     h = halves[key]
-                    meshes[key] = ctx.mesh(np.ascontiguousarray(h.coords), h.s_values)
+                    parent = id(h.mesh)
+                    if parent not in grids:  # each mesh crosses PCIe once, in one copy
+                        grids[parent] = ctx.grid(h.mesh.coords, h.mesh.s_values)
+                    meshes[key] = ctx.view(grids[parent], *h.col_range)
             jobs.append((meshes[("u", n1, s1)], meshes[("s", n2, s2)], plan.tasks[k]))
         return ctx.intersect(jobs, mode=mode, pipeline=pipeline, dedup=dedup, text=text,
                              task_ids=[plan.tasks[k] for k in mine])
     finally:
         for mesh in meshes.values():
             mesh.free()
+        for g in grids.values():
+            g.free()
 
 
 def merge_parts(plan, halves, parts, outs, devices, text: bool) -> PlanResult:

@@ -58,9 +58,18 @@ def find_opts(mode: int, pipeline: int, dedup: bool, text: bool, shard=(0, 1),
 
 
 class Mesh:
-    """A half-layer resident on a context's device (mcx_mesh_load)."""
+    """A half-layer resident on a context's device (mcx_mesh_load), a whole mesh uploaded
+    unpacked (``grid=True``, mcx_grid_load) as the source of half-layer views, or a view
+    (``Context.view``: columns [c0, c1] of a resident grid, packed in place, no upload)."""
 
-    def __init__(self, ctx: "Context", coords, s_values):
+    @classmethod
+    def _from_handle(cls, ctx, handle, N, M, parent=None):
+        m = cls.__new__(cls)
+        m.ctx, m.handle, m.N, m.M, m.parent = ctx, handle, N, M, parent
+        return m
+
+    def __init__(self, ctx: "Context", coords, s_values, grid: bool = False):
+        self.parent = None
         c = np.asarray(coords) if isinstance(coords, np.ndarray) else coords
         if c.ndim != 3 or c.shape[0] != 4:
             raise ConfigError(f"coords must have shape (4, M, N), got {tuple(c.shape)}")
@@ -72,7 +81,8 @@ class Mesh:
             raise ConfigError(f"s_values must have length M = {M}")
         p, keep = _host_f64(c)
         h = ctypes.c_void_p()
-        _lib.check(_lib.load().mcx_mesh_load(ctx.handle, p, N, M, sv.ctypes.data, ctypes.byref(h)), "mcx_mesh_load")
+        fn = _lib.load().mcx_grid_load if grid else _lib.load().mcx_mesh_load
+        _lib.check(fn(ctx.handle, p, N, M, sv.ctypes.data, ctypes.byref(h)), "mcx_grid_load" if grid else "mcx_mesh_load")
         self.ctx, self.handle, self.N, self.M = ctx, h, N, M
         del keep
 
@@ -109,6 +119,18 @@ class Context:
 
     def mesh(self, coords, s_values) -> Mesh:
         return Mesh(self, coords, s_values)
+
+    def grid(self, coords, s_values) -> Mesh:
+        """A whole mesh uploaded once, unpacked: the source of ``view`` half-layers."""
+        return Mesh(self, coords, s_values, grid=True)
+
+    def view(self, parent: Mesh, c0: int, c1: int) -> Mesh:
+        """Columns [c0, c1] of a resident grid as a packed half-layer, without copying
+        (a half-layer is a contiguous column range of its mesh)."""
+        h = ctypes.c_void_p()
+        _lib.check(_lib.load().mcx_mesh_view_columns(self.handle, parent.handle, int(c0), int(c1), ctypes.byref(h)),
+                   "mcx_mesh_view_columns")
+        return Mesh._from_handle(self, h, parent.N, int(c1) - int(c0) + 1, parent=parent)
 
     @staticmethod
     def _out(recp, n, textp, tlen):
@@ -164,7 +186,10 @@ class Context:
         rc = _lib.load().mcx_intersect(self.handle, arr, n, ctypes.byref(fo), ctypes.byref(recp), ctypes.byref(cnt),
                                        ctypes.byref(textp), ctypes.byref(tlen), stats)
         if rc != _lib.MCX_OK:
-            _lib.check(rc, "mcx_intersect", task=task_ids)
+            import re
+            m = re.match(r"job (\d+) ", _lib.last_error())
+            task = task_ids[int(m.group(1))] if (m and task_ids is not None) else task_ids
+            _lib.check(rc, "mcx_intersect", task=task)
         recs, txt = self._out(recp, cnt, textp, tlen)
         return recs, txt, [s.as_dict() for s in stats]
 

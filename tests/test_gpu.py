@@ -890,3 +890,46 @@ def test_prefilter_size_rule(monkeypatch):
         rb = D.search_device(Am, Bm, mode=_lib.MODE_BRUTE)
         assert np.array_equal(rp.hits, rb.hits)
         assert (rp.stats["n_exact_tests"] < rp.stats["n_pairs"]) == quantised
+
+
+def test_column_views_equal_copied_half_layers():
+    """A half-layer as a zero-copy column view of its resident mesh (plane stride = the
+    parent's M) gives exactly the records of the same columns copied to a contiguous grid —
+    both pipelines, both roles, ragged ranges."""
+    from paper_2109_14814_b200 import runtime
+    from paper_2109_14814_b200.mesh import layered_mesh
+    u = layered_mesh(96, "unstable", 3, 1.6, 0.1, 1)
+    s = layered_mesh(80, "stable", 3, 1 / 1.6, 0.1, 2)
+    ctx = runtime.context(0)
+    gu, gs = ctx.grid(u.coords, u.s_values), ctx.grid(s.coords, s.s_values)
+    for (a0, a1), (b0, b1) in (((3, 17), (0, 9)), ((20, u.M - 1), (5, 40)), ((0, 1), (s.M - 6, s.M - 1))):
+        va, vb = ctx.view(gu, a0, a1), ctx.view(gs, b0, b1)
+        ca, cb = np.ascontiguousarray(u.coords[:, a0:a1 + 1]), np.ascontiguousarray(s.coords[:, b0:b1 + 1])
+        ma, mb = ctx.mesh(ca, u.s_values[a0:a1 + 1]), ctx.mesh(cb, s.s_values[b0:b1 + 1])
+        for pipe in (_lib.PIPE_SPEC, _lib.PIPE_TRIANGLE):
+            r1, t1, st1 = ctx.intersect([(va, vb, (1, "+", 2, "-")), (vb, va, (2, "-", 1, "+"))], pipeline=pipe,
+                                        text=True)
+            r2, t2, st2 = ctx.intersect([(ma, mb, (1, "+", 2, "-")), (mb, ma, (2, "-", 1, "+"))], pipeline=pipe,
+                                        text=True)
+            assert t1 == t2 and np.array_equal(r1, r2)
+            assert [x["n_aabb_pass"] for x in st1] == [x["n_aabb_pass"] for x in st2]
+        for m in (va, vb, ma, mb):
+            m.free()
+    gu.free()
+    gs.free()
+
+
+def test_plan_failure_names_the_layer_pair():
+    """a device failure surfaces as a task error carrying the layer-pair id —
+    a NaN in one half-layer of a plan names that task, not the whole plan."""
+    from paper_2109_14814_b200 import errors, layers
+    from paper_2109_14814_b200.mesh import half_layer, layered_mesh
+    u = layered_mesh(48, "unstable", 2, 1.6, 0.1, 1)
+    s = layered_mesh(48, "stable", 2, 1 / 1.6, 0.1, 2)
+    plan = layers.enumerate_layer_pairs(u, s, 2)
+    c0, c1 = half_layer(s, 2, -1).col_range
+    s.coords[1, (c0 + c1) // 2, 7] = np.nan  # only S_2^- is poisoned
+    with pytest.raises(errors.BackendError) as exc:
+        layers.search_plan(u, s, plan)
+    assert exc.value.task is not None and exc.value.task[2:] == (2, "-")
+    assert "non-finite" in str(exc.value)

@@ -1,8 +1,11 @@
 """Randomised parity soak: many random mesh pairs (shapes, surfaces, affine scalings,
 translations, near-coincident and identical copies, dyadic lattices), each searched in
-every mode — single call, 3-way cyclic shards and inside a batch — against the C
-oracle's exact sweep.  Prints one summary line per 50 cases and a final JSON line.
-    python tools/soak.py [n_cases] [seed]"""
+every mode — single call, 3-way cyclic shards, inside a batch, and with the roles
+oriented (MCX_ORIENT_LARGER_A) — against the C oracle's exact sweep; the SPEC pipeline
+against the C restatement of the serial backend (hits, candidate counts); and the host
+runtime's records text (device sort / dedup / %.17g) against the host path built from the
+oracle's hits.  Prints one summary line per 50 cases and a final JSON line.
+    MCX_PREFILTER_MIN_PAIRS=0 python tools/soak.py [n_cases] [seed]"""
 import json
 import os
 import sys
@@ -12,7 +15,8 @@ import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from oracle import c_oracle as C  # noqa: E402
-from paper_2109_14814_b200 import _lib, device as D  # noqa: E402
+os.environ.setdefault("MCX_PREFILTER_MIN_PAIRS", "0")  # the quantised kernel at every size
+from paper_2109_14814_b200 import _lib, device as D, isect, runtime  # noqa: E402
 from paper_2109_14814_b200.mesh import dyadic, manifold_like  # noqa: E402
 
 n_cases = int(sys.argv[1]) if len(sys.argv) > 1 else 200
@@ -61,6 +65,18 @@ for case in range(n_cases):
         ok &= same(ref, parts.hits)
         bt = D.search_batch([(Bm, Am), (Am, Bm)], mode=mode)[1]
         ok &= same(ref, bt.hits)
+        for orient in (_lib.ORIENT_AS_GIVEN, _lib.ORIENT_LARGER_A):
+            ok &= same(ref, D.search_device(Am, Bm, mode=mode, orient=orient).hits)
+    spec = C.spec_search(A, B, cap=1 << 22)
+    rs = D.search_device(Am, Bm, mode=_lib.MODE_CULL, pipeline=_lib.PIPE_SPEC)
+    ok &= same(spec, rs.hits) and rs.stats["n_candidates"] == spec["n_candidates"]
+    sa, sb = np.linspace(-1, 1, A.shape[1]), np.linspace(-1, 1, B.shape[1])
+    h = np.zeros(len(ref["ia"]), dtype=D.HIT_DTYPE)
+    for f in ("ia", "ib", "s", "t", "a", "b"):
+        h[f] = ref[f]
+    want = "".join(w.to_line() + "\n" for w in isect.hits_to_records(A, sa, B, sb, h, layer=(2, "-", 1, "+")))
+    _, text, _ = runtime.context(0).find(A, sa, B, sb, (2, "-", 1, "+"), pipeline=_lib.PIPE_TRIANGLE, text=True)
+    ok &= text == want.encode()
     if not ok:
         bad.append(case)
     hits_total += len(ref["ia"])
@@ -69,4 +85,4 @@ for case in range(n_cases):
     if (case + 1) % 50 == 0:
         print(f"{case + 1} cases, {len(bad)} mismatches, {hits_total} hits, {time.time() - t0:.0f} s", flush=True)
 print(json.dumps({"cases": n_cases, "mismatches": bad, "hits": hits_total, "aabb_passes": pass_total,
-                  "pairs": pairs_total, "checks_per_case": 3 * len(MODES), "seconds": round(time.time() - t0, 1)}))
+                  "pairs": pairs_total, "checks_per_case": 5 * len(MODES) + 2, "seconds": round(time.time() - t0, 1)}))
