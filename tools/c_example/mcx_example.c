@@ -17,6 +17,7 @@
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include <cuda_runtime.h>
 
@@ -69,6 +70,7 @@ static void upload(mesh_t* m, const double* host, uint32_t N, uint32_t M) {
   CK(cudaMalloc((void**)&m->tbox, sizeof(double) * 8 * ((n + MCX_TILE - 1) / MCX_TILE)));
   CK(cudaMalloc((void**)&m->bbox, sizeof(double) * 8 * ((n + MCX_BLOCK - 1) / MCX_BLOCK)));
   MK(mcx_pack(m->coords, N, M, MCX_ORDER_TILED, m->box, m->perm, m->gbox, m->tbox, m->bbox, m->status, 0, NULL));
+  memset(&m->dev, 0, sizeof(m->dev));  /* plane_rows = 0: a contiguous grid */
   m->dev.n_tri = n;
   m->dev.coords = m->coords;
   m->dev.N = N;
@@ -122,7 +124,7 @@ int main(int argc, char** argv) {
   for (uint32_t k = 0; k < M; ++k) sv[k] = -1.0 + 2.0 * k / (M - 1);
   mcx_context* ctx = NULL;
   MK(mcx_context_create(0, &ctx));
-  mcx_find_opts fo = {MCX_MODE_CULL, MCX_PIPE_TRIANGLE, 0, 1, 0, 0}; /* no dedup: one record per hit */
+  mcx_find_opts fo = {MCX_MODE_CULL, MCX_PIPE_TRIANGLE, 0, 1, 0, 0, MCX_ORIENT_LARGER_A}; /* no dedup */
   mcx_layer layer = {1, 1, 1, -1};
   const mcx_record* recs = NULL;
   const char* text = NULL;
