@@ -63,3 +63,41 @@ def test_cli_layers_and_errors(tmp_path):
     assert cli.main(["intersect", "--umesh", str(tmp_path / "u.mnf"), "--smesh", str(tmp_path / "s.mnf"),
                      "--plan", str(tmp_path / "plan.txt"), "--backend", "serial", "--out", str(tmp_path / "r")]) == 2
     assert cli.main(["bogus"]) == 2
+
+
+def test_include_core():  # --include-core re-enables the fundamental-domain cores
+    u, s = _meshes(2, 8)
+    plan = layers.enumerate_layer_pairs(u, s, 2, omega_p=2.0, include_core=True)
+    assert len(plan) == 12 + 3
+    assert plan.tasks[:3] == [(0, "+", 0, "+"), (1, "+", 0, "+"), (1, "-", 0, "+")]
+    assert plan.tof[:3] == [0.0, pytest.approx(math.pi), pytest.approx(math.pi)]
+    core = half_layer(u, 0, +1)
+    lo, hi = core.col_range
+    assert u.s_values[lo] == pytest.approx(-u.D) and u.s_values[hi] == pytest.approx(u.D)
+    with pytest.raises(errors.ConfigError):
+        half_layer(u, 0, -1)  # the core is one half-layer
+
+
+def test_cli_layers_include_core(tmp_path):
+    u, s = _meshes(2, 8)
+    write_mesh(tmp_path / "u.mnf", u)
+    write_mesh(tmp_path / "s.mnf", s)
+    assert cli.main(["layers", "--umesh", str(tmp_path / "u.mnf"), "--smesh", str(tmp_path / "s.mnf"), "--nmax", "2",
+                     "--plan", str(tmp_path / "plan.txt"), "--include-core"]) == 0
+    assert layers.read_plan(tmp_path / "plan.txt").tasks[0] == (0, "+", 0, "+")
+
+
+def test_read_plan_rejects_malformed_signs(tmp_path):  # '+-' used to pass a substring test
+    p = tmp_path / "plan.txt"
+    p.write_text("1 +- 1 + 6.28\n")
+    with pytest.raises(errors.FileFormatError):
+        layers.read_plan(p)
+
+
+def test_assign_tasks_is_balanced_and_deterministic():
+    costs = [9.0, 1.0, 5.0, 5.0, 3.0, 3.0, 2.0, 8.0]
+    parts = layers.assign_tasks(costs, 3)
+    assert sorted(k for p in parts for k in p) == list(range(8))
+    assert parts == layers.assign_tasks(costs, 3)
+    loads = [sum(costs[k] for k in p) for p in parts]
+    assert max(loads) - min(loads) <= max(costs)
