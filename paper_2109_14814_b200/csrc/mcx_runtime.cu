@@ -41,6 +41,8 @@
 #include <cub/device/device_select.cuh>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "../../include/mcx.h"
 #include "mcx_common.cuh"
 #include "mcx_format.cuh"
@@ -48,6 +50,8 @@
 #include "mcx_records.cuh"
 
 #define MCX_DEDUP_TOL 1e-9
+
+namespace cg = cooperative_groups;
 
 namespace mcx {
 
@@ -231,40 +235,49 @@ __global__ void close_pairs_kernel(const uint32_t* __restrict__ xorder, const ui
   }
 }
 
-// 5b. greedy resolution in rounds (one CTA; close pairs are few).  state: 1 kept,
-// 2 dropped, 0 undecided.  Per round, one pass over the pairs marks "a kept
-// predecessor" (drop) and "an undecided predecessor" (wait) per record, one more
-// decides: drop, keep (all predecessors dropped) or wait.
-__global__ void __launch_bounds__(1024) resolve_kernel(const uint2* __restrict__ pairs,
-                                                       const unsigned long long* __restrict__ np_dev, uint64_t cap,
-                                                       uint8_t* __restrict__ state, uint8_t* __restrict__ mark) {
+// 5b. greedy resolution in rounds, grid-wide (a cooperative launch: one grid sync per
+// pass).  state: 1 kept, 2 dropped, 0 undecided.  Per round, one pass over the pairs
+// marks "a kept predecessor" (bit 0: drop) and "an undecided predecessor" (bit 1: wait)
+// per record — word-level atomicOr, so concurrent marks of one record never lose a bit —
+// and one more decides: drop, keep (all predecessors dropped) or wait.
+__global__ void __launch_bounds__(256) resolve_kernel(const uint2* __restrict__ pairs,
+                                                      const unsigned long long* __restrict__ np_dev, uint64_t cap,
+                                                      uint8_t* __restrict__ state, uint32_t* __restrict__ mark,
+                                                      unsigned* __restrict__ left_flag) {
+  cg::grid_group grid = cg::this_grid();
   // an overflowed pair list leaves undecided records without stored pairs: the host
   // sees the count, grows the list and reruns, so do nothing here
   if ((uint64_t)*np_dev > cap) return;
   const uint64_t np = *np_dev;
-  for (;;) {
-    for (uint64_t k = threadIdx.x; k < np; k += blockDim.x) {
+  const uint64_t t0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, stride = (uint64_t)gridDim.x * blockDim.x;
+  for (int round = 0;; ++round) {
+    for (uint64_t k = t0; k < np; k += stride) {
       const uint2 e = pairs[k];
       if (state[e.y] == 0) {
         const uint8_t se = state[e.x];
-        if (se == 1) mark[e.y] |= 1;       // a kept predecessor: drop
-        else if (se == 0) mark[e.y] |= 2;  // an undecided predecessor: wait
+        const uint32_t bit = se == 1 ? 1u : (se == 0 ? 2u : 0u);
+        if (bit) atomicOr(mark + (e.y >> 2), bit << (8 * (e.y & 3)));
       }
     }
-    __syncthreads();
-    bool left = false;
-    for (uint64_t k = threadIdx.x; k < np; k += blockDim.x) {
+    if (t0 == 0) left_flag[round & 1] = 0;  // the flag the next decision pass writes
+    grid.sync();
+    for (uint64_t k = t0; k < np; k += stride) {
       const uint32_t l = pairs[k].y;
-      const uint8_t m = mark[l];
+      const uint32_t m = (mark[l >> 2] >> (8 * (l & 3))) & 3u;
       if (state[l] == 0) {
-        if (m & 1) state[l] = 2;
-        else if (!(m & 2)) state[l] = 1;
-        else left = true;
+        if (m & 1u) state[l] = 2;
+        else if (!(m & 2u)) state[l] = 1;
+        else left_flag[round & 1] = 1;
       }
     }
-    __syncthreads();
-    for (uint64_t k = threadIdx.x; k < np; k += blockDim.x) mark[pairs[k].y] = 0;
-    if (!__syncthreads_or(left)) break;
+    grid.sync();
+    for (uint64_t k = t0; k < np; k += stride) {  // clear the marks of this round
+      const uint32_t l = pairs[k].y;
+      mark[l >> 2] = 0;
+    }
+    const bool more = *(volatile unsigned*)(left_flag + (round & 1)) != 0;
+    grid.sync();
+    if (!more) break;
   }
 }
 
@@ -671,7 +684,7 @@ static int postprocess(mcx_context* c, uint64_t n, const uint32_t* hit_task, con
   if ((rc = ensure(c, c->k0, 8 * n, s)) || (rc = ensure(c, c->k1, 8 * n, s)) || (rc = ensure(c, c->v0, 4 * n, s)) ||
       (rc = ensure(c, c->v1, 4 * n, s)) || (rc = ensure(c, c->recs, sizeof(mcx_record) * n, s)) ||
       (rc = ensure(c, c->recs_out, sizeof(mcx_record) * n, s)) || (rc = ensure(c, c->state, n, s)) ||
-      (rc = ensure(c, c->blocked, n, s)) || (rc = ensure(c, c->lens, 4 * n, s)) ||
+      (rc = ensure(c, c->blocked, n + 4, s)) || (rc = ensure(c, c->lens, 4 * n, s)) ||
       (rc = ensure(c, c->offs, 8 * n, s)) || (rc = ensure(c, c->small, 64, s)))
     return rc;
   uint64_t max_gid = 0;
@@ -733,13 +746,23 @@ static int postprocess(mcx_context* c, uint64_t n, const uint32_t* hit_task, con
     c->pair_cap = std::max<uint64_t>(c->pair_cap, 4 * n);
     if ((rc = ensure(c, c->pairs, 8 * c->pair_cap, s))) return rc;
     CUDA_TRY(cudaMemsetAsync(state, 1, n, s));
-    CUDA_TRY(cudaMemsetAsync(c->blocked.p, 0, n, s));
+    CUDA_TRY(cudaMemsetAsync(c->blocked.p, 0, n + 4, s));
     CUDA_TRY(cudaMemsetAsync(pair_count, 0, 8, s));
     close_pairs_kernel<<<grid_of(n), 256, 0, s>>>(vals.Current(), keys.Current(), R, n, (uint2*)c->pairs.p,
                                                    c->pair_cap, pair_count, state);
-    resolve_kernel<<<1, 1024, 0, s>>>((const uint2*)c->pairs.p, pair_count, c->pair_cap, state,
-                                      (uint8_t*)c->blocked.p);
     CUDA_TRY(cudaGetLastError());
+    {  // cooperative launch: every CTA co-resident (grid syncs between the passes)
+      int per_sm = 0, sms = 148;
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, resolve_kernel, 256, 0));
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+      const unsigned g = (unsigned)std::max(1, std::min(per_sm * sms, sms * 2));
+      const uint2* pr = (const uint2*)c->pairs.p;
+      uint64_t pcap = c->pair_cap;
+      uint32_t* mark = (uint32_t*)c->blocked.p;
+      unsigned* left = (unsigned*)(pair_count + 2);
+      void* args[] = {(void*)&pr, (void*)&pair_count, (void*)&pcap, (void*)&state, (void*)&mark, (void*)&left};
+      CUDA_TRY(cudaLaunchCooperativeKernel((void*)resolve_kernel, dim3(g), dim3(256), args, 0, s));
+    }
   }
   // 6: flags (+ text lengths), inclusive scan of the lengths, compaction, text
   uint8_t* flags = (uint8_t*)c->blocked.p;  // reused: resolution is done
