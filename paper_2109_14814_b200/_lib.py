@@ -14,7 +14,7 @@ import threading
 from .errors import BackendError, CapacityError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmcx.so")
+LIB_PATH = os.environ.get("MCX_LIB") or os.path.join(HERE, "libmcx.so")  # MCX_LIB: A/B builds (tools)
 
 ABI_VERSION = 3  # include/mcx.h MCX_ABI_VERSION
 MCX_OK, MCX_E_CAPACITY, MCX_E_CUDA, MCX_E_ARG = 0, 1, 2, 3

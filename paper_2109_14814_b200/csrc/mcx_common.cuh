@@ -62,6 +62,27 @@ __host__ __device__ __forceinline__ void quad_of_storage(uint64_t sq, uint32_t N
   k = tk * T + sk * S + r / ws;
 }
 
+// The same map in 32-bit arithmetic (every storage index is < 2^30: the triangle count
+// is < 2^31) — no 64-bit division subroutine in the device code that calls it.
+__device__ __forceinline__ void quad_of_storage32(uint32_t sq, uint32_t N, uint32_t MQ, uint32_t& i, uint32_t& k) {
+  const uint32_t T = ORDER_TILE_Q, S = ORDER_SUB_Q;
+  const uint32_t TN = N <= (0xffffffffu / T) ? T * N : 0xffffffffu;  // sq < TN whenever T·N overflows
+  const uint32_t tk = sq / TN;
+  uint32_t r = sq - tk * TN;
+  const uint32_t hq = min(T, MQ - tk * T);
+  const uint32_t ti = r / (T * hq);
+  r -= ti * T * hq;
+  const uint32_t wq = min(T, N - ti * T);
+  const uint32_t sk = r / (S * wq);
+  r -= sk * S * wq;
+  const uint32_t hs = min(S, hq - sk * S);
+  const uint32_t si = r / (S * hs);
+  r -= si * S * hs;
+  const uint32_t ws = min(S, wq - si * S);
+  i = ti * T + si * S + r % ws;
+  k = tk * T + sk * S + r / ws;
+}
+
 // ------------------------------------------------------------ error state
 // Thread-local, so concurrent host threads (one per GPU) never clobber each other.
 extern thread_local char g_err[512];

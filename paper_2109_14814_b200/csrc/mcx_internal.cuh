@@ -24,4 +24,10 @@ int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mcx_hit* 
                  uint64_t cap, mcx_stats* st, unsigned long long* h_counters);
 int batch_stats(const unsigned long long* h, uint32_t n, const mcx_opts* o, uint64_t cap, mcx_stats* st, float ms);
 
+// mcx_search.cu: one-time per (kernel, device, threads, smem) launch setup — the
+// dynamic shared memory opt-in (+ the shared-memory carveout when carveout >= 0) and
+// the resident CTAs per SM × SM count — cached, since each of these host calls costs
+// microseconds on every small search otherwise.  `device` is the current device.
+int kernel_prepare(const void* fn, int threads, size_t smem, int carveout, int device, uint64_t* slots);
+
 }  // namespace mcx

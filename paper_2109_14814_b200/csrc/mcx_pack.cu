@@ -30,12 +30,28 @@ namespace mcx {
 
 constexpr int PACK_THREADS = A_BLOCK / 2;  // one thread per storage quad of a block
 
+// 16-byte slot q of the staged boxes lives at q with its column (q mod 8) XORed by its
+// 128-byte row (q / 8) mod 8
+__device__ __forceinline__ uint32_t swz(uint32_t q) { return q ^ ((q >> 3) & 7); }
+__device__ __forceinline__ unsigned dlo(double x) { return (unsigned)__double2loint(x); }
+__device__ __forceinline__ unsigned dhi(double x) { return (unsigned)__double2hiint(x); }
+
 struct PackSmem {
   Box box[A_BLOCK];
   Box gsm[A_BLOCK / GROUP];
 };
 
-__global__ void __launch_bounds__(PACK_THREADS, 3) pack_kernel(const double* __restrict__ coords, uint32_t N,
+#ifndef PACK_MIN_BLOCKS
+#define PACK_MIN_BLOCKS 3
+#endif
+
+// min / max of canonical values (finite or ±Inf, no −0.0 mixed with +0.0 — see the
+// callers) as compare + select: 3 instructions where fmin/fmax spend 4 on NaN quieting.
+// A NaN input makes the mesh unusable (status flag), so its boxes are never searched.
+__device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : a; }
+__device__ __forceinline__ double dmax(double a, double b) { return b > a ? b : a; }
+
+__global__ void __launch_bounds__(PACK_THREADS, PACK_MIN_BLOCKS) pack_kernel(const double* __restrict__ coords, uint32_t N,
                                                                uint32_t M, uint32_t Mp, int tiled, Box* __restrict__ box,
                                                                uint32_t* __restrict__ perm, Box* __restrict__ gbox,
                                                                Box* __restrict__ tbox, Box* __restrict__ bbox,
@@ -56,13 +72,26 @@ __global__ void __launch_bounds__(PACK_THREADS, 3) pack_kernel(const double* __r
     qlo[c] = __longlong_as_double(0x7ff0000000000000ll);
     qhi[c] = -qlo[c];
   }
+  // The storage map inverted.  Fast path: a CTA whose 512 quads lie in full 16×16
+  // tiles of one tile row (all but the ragged edge CTAs) decodes its quads by bit fields
+  // after one CTA-uniform 32-bit division; the rest call quad_of_storage.  (sq < 2^30:
+  // the triangle count is < 2^31.)
+  const uint32_t sq0 = (uint32_t)(blk * PACK_THREADS);
+  const uint32_t TN = N <= (0xffffffffu / ORDER_TILE_Q) ? (uint32_t)ORDER_TILE_Q * N : 0xffffffffu;
+  const uint32_t tk0 = sq0 / TN, rt0 = sq0 - tk0 * TN;
+  const bool regular = tiled && tk0 * ORDER_TILE_Q + ORDER_TILE_Q <= MQ &&
+                       rt0 + PACK_THREADS <= ((N / ORDER_TILE_Q) << 8);
   if (valid) {
     uint32_t i, k;
-    if (tiled) {
-      quad_of_storage(sq, N, MQ, i, k);
+    if (regular) {
+      const uint32_t r = rt0 + tid, rr = r & 255;  // tile r >> 8, 4×4 sub-tile rr >> 4, quad rr & 15
+      i = (r >> 8) * ORDER_TILE_Q + ((rr >> 4) & 3) * ORDER_SUB_Q + (rr & 3);
+      k = tk0 * ORDER_TILE_Q + (rr >> 6) * ORDER_SUB_Q + ((rr >> 2) & 3);
+    } else if (tiled) {
+      quad_of_storage32((uint32_t)sq, N, MQ, i, k);
     } else {
-      i = (uint32_t)(sq % N);
-      k = (uint32_t)(sq / N);
+      i = (uint32_t)sq % N;
+      k = (uint32_t)sq / N;
     }
     const uint32_t t0 = 2 * (i + N * k);
     // the quad's 4 vertices once (16 loads, all issued before use): T¹ = (v00, v10,
@@ -87,16 +116,27 @@ __global__ void __launch_bounds__(PACK_THREADS, 3) pack_kernel(const double* __r
     for (int c = 0; c < 4; ++c) {
       const double a = dadd(w00[c], 0.0), b = dadd(w10[c], 0.0), d = dadd(w01[c], 0.0), e = dadd(w11[c], 0.0);
       bad |= !(isfinite(a) && isfinite(b) && isfinite(d) && isfinite(e));
-      const double mn = fmin(b, d), mx = fmax(b, d);
-      b1.lo[c] = fmin(a, mn);
-      b1.hi[c] = fmax(a, mx);
-      b2.lo[c] = fmin(e, mn);
-      b2.hi[c] = fmax(e, mx);
-      qlo[c] = fmin(b1.lo[c], b2.lo[c]);
-      qhi[c] = fmax(b1.hi[c], b2.hi[c]);
+      const double mn = dmin(b, d), mx = dmax(b, d);
+      b1.lo[c] = dmin(a, mn);
+      b1.hi[c] = dmax(a, mx);
+      b2.lo[c] = dmin(e, mn);
+      b2.hi[c] = dmax(e, mx);
+      qlo[c] = dmin(b1.lo[c], b2.lo[c]);
+      qhi[c] = dmax(b1.hi[c], b2.hi[c]);
     }
-    S.box[2 * tid] = b1;
-    S.box[2 * tid + 1] = b2;
+    // staging stores: chunk j (16 B) of record r = 2·tid + τ sits at 16-byte slot
+    // swz(4r + j); lanes are 128 B apart, so the XOR swizzle spreads each 8-lane phase
+    // over all 8 bank columns (unswizzled: 8-way conflicts)
+    uint4* st = reinterpret_cast<uint4*>(S.box);
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      st[swz(8 * tid + j)] = make_uint4(dlo(b1.lo[2 * j]), dhi(b1.lo[2 * j]), dlo(b1.lo[2 * j + 1]), dhi(b1.lo[2 * j + 1]));
+      st[swz(8 * tid + 2 + j)] =
+          make_uint4(dlo(b1.hi[2 * j]), dhi(b1.hi[2 * j]), dlo(b1.hi[2 * j + 1]), dhi(b1.hi[2 * j + 1]));
+      st[swz(8 * tid + 4 + j)] = make_uint4(dlo(b2.lo[2 * j]), dhi(b2.lo[2 * j]), dlo(b2.lo[2 * j + 1]), dhi(b2.lo[2 * j + 1]));
+      st[swz(8 * tid + 6 + j)] =
+          make_uint4(dlo(b2.hi[2 * j]), dhi(b2.hi[2 * j]), dlo(b2.hi[2 * j + 1]), dhi(b2.hi[2 * j + 1]));
+    }
     if (perm) reinterpret_cast<uint2*>(perm)[sq] = make_uint2(t0, t0 + 1);
   }
   if (status && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status, 1u);
@@ -106,47 +146,53 @@ __global__ void __launch_bounds__(PACK_THREADS, 3) pack_kernel(const double* __r
     const uint32_t n16 = (uint32_t)(min((uint64_t)A_BLOCK, n - r0) * (sizeof(Box) / 16));
     const uint4* src = reinterpret_cast<const uint4*>(S.box);
     uint4* dst = reinterpret_cast<uint4*>(box + r0);
-    for (uint32_t q = tid; q < n16; q += PACK_THREADS) dst[q] = src[q];
+    for (uint32_t q = tid; q < n16; q += PACK_THREADS) dst[q] = src[swz(q)];
   }
   if (gbox) {
-    // group = 16 consecutive storage quads = half a warp
+    // group = 16 consecutive storage quads = half a warp.  Reduce-scatter instead of an
+    // all-reduce: v = the quad box with its hi half negated (every step is then a min;
+    // the canonicalised inputs hold no −0, so the negated zeros are all −0 and the result
+    // bits equal the unnegated max); at xor 8 / 4 / 2 each lane keeps half of what it
+    // holds, xor 1 completes, and lane pair p of the half-warp holds component p of the
+    // group box — 8 shuffled values per lane instead of 32.
+    const int hl = lane & 15;
+    const bool x3 = hl & 8, x2 = hl & 4, x1 = hl & 2;
+    double v4[4], v2[2];
 #pragma unroll
-    for (int o = 1; o < 16; o <<= 1)
+    for (int j = 0; j < 4; ++j) {
+      const double lo = qlo[j], nhi = -qhi[j];
+      v4[j] = dmin(x3 ? nhi : lo, __shfl_xor_sync(0xffffffffu, x3 ? lo : nhi, 8));
+    }
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        qlo[c] = fmin(qlo[c], __shfl_xor_sync(0xffffffffu, qlo[c], o));
-        qhi[c] = fmax(qhi[c], __shfl_xor_sync(0xffffffffu, qhi[c], o));
-      }
+    for (int j = 0; j < 2; ++j)
+      v2[j] = dmin(x2 ? v4[2 + j] : v4[j], __shfl_xor_sync(0xffffffffu, x2 ? v4[j] : v4[2 + j], 4));
+    double v1 = dmin(x1 ? v2[1] : v2[0], __shfl_xor_sync(0xffffffffu, x1 ? v2[0] : v2[1], 2));
+    v1 = dmin(v1, __shfl_xor_sync(0xffffffffu, v1, 1));
+    const int comp = (hl >> 1);  // = 4·x3 + 2·x2 + x1: lo[0..3], hi[0..3]
     const uint64_t ng = (n + GROUP - 1) / GROUP;
-    if ((tid & 15) == 0) {
-      Box r;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        r.lo[c] = qlo[c];
-        r.hi[c] = qhi[c];
-      }
-      S.gsm[tid >> 4] = r;
+    double* gs = reinterpret_cast<double*>(S.gsm);
+    if (!(lane & 1)) {
       const uint64_t g = blk * (A_BLOCK / GROUP) + (tid >> 4);
-      if (g < ng) gbox[g] = r;
+      const double val = x3 ? -v1 : v1;
+      gs[(tid >> 4) * 8 + comp] = val;
+      if (g < ng) reinterpret_cast<double*>(gbox)[g * 8 + comp] = val;
     }
     __syncthreads();
     if (tid < 32 && tbox && bbox) {
-      // warp 0: lane g holds group box g; 4 butterfly rounds give each 16-lane half its
-      // 512-record tile box, one more the 1024-record block box
-      Box r = S.gsm[tid];
+      // warp 0: lane l reduces component c = l & 7 over groups 8·(l >> 3) .. +7 (hi
+      // components negated again), xor 8 gives the lane's 512-record tile, xor 16 the block
+      const int c = lane & 7;
+      const unsigned long long neg = c >= 4 ? 0x8000000000000000ull : 0ull;
+      const double* src = gs + 64 * (lane >> 3) + c;
+      double m = __longlong_as_double(__double_as_longlong(src[0]) ^ neg);
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        if (o == 16 && (tid & 15) == 0) {
-          const uint64_t tt = blk * (A_BLOCK / TILE) + (tid >> 4);
-          if (tt < (n + TILE - 1) / TILE) tbox[tt] = r;
-        }
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          r.lo[c] = fmin(r.lo[c], __shfl_xor_sync(0xffffffffu, r.lo[c], o));
-          r.hi[c] = fmax(r.hi[c], __shfl_xor_sync(0xffffffffu, r.hi[c], o));
-        }
-      }
-      if (tid == 0) bbox[blk] = r;
+      for (int g = 1; g < 8; ++g) m = dmin(m, __longlong_as_double(__double_as_longlong(src[8 * g]) ^ neg));
+      m = dmin(m, __shfl_xor_sync(0xffffffffu, m, 8));
+      const uint64_t tt = blk * (A_BLOCK / TILE) + (lane >> 4);
+      if (!(lane & 8) && tt < (n + TILE - 1) / TILE)
+        reinterpret_cast<double*>(tbox)[tt * 8 + c] = __longlong_as_double(__double_as_longlong(m) ^ neg);
+      m = dmin(m, __shfl_xor_sync(0xffffffffu, m, 16));
+      if (lane < 8) reinterpret_cast<double*>(bbox)[blk * 8 + c] = __longlong_as_double(__double_as_longlong(m) ^ neg);
     }
   }
 }
@@ -230,8 +276,12 @@ int pack_enqueue(const double* coords, uint32_t N, uint32_t M, int order, double
   if (b1 == 0 || b1 > nblk) b1 = nblk;
   if (b0 >= b1) return MCX_OK;
   static_assert(sizeof(PackSmem) <= 227 * 1024, "pack smem");
-  CUDA_TRY(cudaFuncSetAttribute(pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PackSmem)));
-  CUDA_TRY(cudaFuncSetAttribute(pack_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  int dev = 0;
+  uint64_t slots;
+  CUDA_TRY(cudaGetDevice(&dev));
+  if (int rc = kernel_prepare(reinterpret_cast<const void*>(pack_kernel), PACK_THREADS, sizeof(PackSmem), 100, dev,
+                              &slots))
+    return rc;
   if (status && b0 == 0) CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(uint32_t), stream));
   pack_kernel<<<(unsigned)(b1 - b0), PACK_THREADS, sizeof(PackSmem), stream>>>(
       coords, N, M, Mp, order == MCX_ORDER_TILED, reinterpret_cast<Box*>(box), perm, reinterpret_cast<Box*>(gbox),

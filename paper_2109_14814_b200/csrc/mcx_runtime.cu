@@ -616,8 +616,10 @@ static int enqueue_small(mcx_context* c, const unsigned long long* n_dev, uint64
     CUDA_TRY(cudaMemcpyAsync(nd, &n, 8, cudaMemcpyHostToDevice, s));  // 8 bytes, staged by the driver
     n_dev = nd;
   }
-  CUDA_TRY(cudaFuncSetAttribute(post_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)sizeof(SmallSmem)));
+  uint64_t slots;
+  if ((rc = kernel_prepare(reinterpret_cast<const void*>(post_small_kernel), 1024, sizeof(SmallSmem), -1,
+                           c->device, &slots)))
+    return rc;
   SmallOut* d_so;
   mcx_record* d_hr;
   char* d_ht;
@@ -752,10 +754,11 @@ static int postprocess(mcx_context* c, uint64_t n, const uint32_t* hit_task, con
                                                    c->pair_cap, pair_count, state);
     CUDA_TRY(cudaGetLastError());
     {  // cooperative launch: every CTA co-resident (grid syncs between the passes)
-      int per_sm = 0, sms = 148;
-      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, resolve_kernel, 256, 0));
+      int sms = 148;
+      uint64_t slots;
+      if ((rc = kernel_prepare(reinterpret_cast<const void*>(resolve_kernel), 256, 0, -1, c->device, &slots))) return rc;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-      const unsigned g = (unsigned)std::max(1, std::min(per_sm * sms, sms * 2));
+      const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(slots, (uint64_t)sms * 2));
       const uint2* pr = (const uint2*)c->pairs.p;
       uint64_t pcap = c->pair_cap;
       uint32_t* mark = (uint32_t*)c->blocked.p;

@@ -45,6 +45,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <mutex>
 #include <type_traits>
 #include <unordered_map>
 #include <vector>
@@ -56,6 +57,43 @@
 #include "mcx_internal.cuh"
 
 namespace mcx {
+
+int kernel_prepare(const void* fn, int threads, size_t smem, int carveout, int device, uint64_t* slots) {
+  struct Key {
+    const void* fn;
+    int device, threads, carveout;
+    size_t smem;
+    bool operator==(const Key& o) const {
+      return fn == o.fn && device == o.device && threads == o.threads && carveout == o.carveout && smem == o.smem;
+    }
+  };
+  struct Hash {
+    size_t operator()(const Key& k) const {
+      return std::hash<const void*>()(k.fn) ^ (size_t)k.device * 0x9e3779b97f4a7c15ull ^ (k.smem << 20) ^
+             ((size_t)k.threads << 8) ^ (size_t)(k.carveout + 1);
+    }
+  };
+  static std::mutex mu;
+  static std::unordered_map<Key, uint64_t, Hash> cache;
+  const Key key{fn, device, threads, carveout, smem};
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      *slots = it->second;
+      return MCX_OK;
+    }
+  }
+  int sms = 148, occ = 1;
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (carveout >= 0) CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, carveout));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem));
+  *slots = (uint64_t)sms * (occ > 0 ? occ : 1);
+  std::lock_guard<std::mutex> lk(mu);
+  cache[key] = *slots;
+  return MCX_OK;
+}
 
 // ------------------------------------------------------------ brute kernel
 template <int KIND, class C>

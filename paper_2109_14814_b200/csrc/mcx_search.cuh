@@ -11,6 +11,7 @@
 
 #include "../../include/mcx.h"
 #include "mcx_common.cuh"
+#include "mcx_internal.cuh"
 
 namespace mcx {
 
@@ -315,13 +316,7 @@ static int upload_plan(std::vector<SearchParams>& T, Batch& Bt, std::vector<uint
 // Resident CTAs of `kernel` on the whole device (at least one per SM).
 template <class K>
 static int resident_slots(K kernel, int threads, size_t smem, int device, uint64_t* slots) {
-  int dev_sms = 148;
-  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device);
-  CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int occ = 1;
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem));
-  *slots = (uint64_t)dev_sms * (occ > 0 ? occ : 1);
-  return MCX_OK;
+  return kernel_prepare(reinterpret_cast<const void*>(kernel), threads, smem, -1, device, slots);
 }
 
 // Variant selection (MCX_VARIANT=0..3, for experiments; 0 = the tuned default:
