@@ -1,12 +1,18 @@
 // mcx_pack.cu — canonical triangle boxes and the culling hierarchy in one pass (libmcx.so).
 //
-// pack_kernel: one CTA per 1024-record block of the storage order, one thread per
-// storage quad.  The thread inverts the storage map to its quad (i, k) of the
-// (4, M, N) half-layer grid, builds T¹ = {v00, v10, v01} and T² = {v10, v01, v11}
-// with θ wrapping mod N (PAPER.md T^{u1}/T^{u2} vertex sets) from
-// tri_verts (the same vertex code the solve uses) and writes their exact AABBs.
-// Original triangle index t = 2·(i + N·k) + τ (PAPER.md kernel step 3); perm[]
-// maps storage position → t so searches can emit original indices.
+// pack_kernel: persistent CTAs, each walking 1024-record blocks of the storage order
+// (blk0 + blockIdx.x, step gridDim.x), one thread per storage quad of a block.  The
+// thread inverts the storage map to its quad (i, k) of the (4, M, N) half-layer grid,
+// builds T¹ = {v00, v10, v01} and T² = {v10, v01, v11} with θ wrapping mod N
+// (PAPER.md T^{u1}/T^{u2} vertex sets) and writes their exact AABBs.
+// Original triangle index t = 2·(i + N·k) + τ (PAPER.md kernel step 3); perm[] maps
+// storage position → t so searches can emit original indices.
+//
+// Input: a block of two full 16×16-quad tiles reads a 17 × 33-vertex window of each of
+// the 4 planes.  The window of the NEXT block is copied into shared memory (cp.async,
+// no registers) while the current one is computed and written, so the grid reads
+// overlap the stores and each vertex is read from HBM/L2 once instead of by 4 quads.
+// Ragged edge blocks (partial tiles) load their vertices directly.
 //
 // Output is destination-ordered: the block's 1024 boxes (64 KB) are staged in shared
 // memory and leave as fully coalesced 16-byte stores (consecutive threads, consecutive
@@ -17,10 +23,12 @@
 // initcheck, which then flags every later read of the boxes.)  A union box is disjoint from
 // another box only if every member is, so culling never changes the hit set.
 //
-// Per record: 16 B of grid read (each vertex is shared by 4 quads; L1), 64 B box +
-// 4 B perm + 2.2 B of level boxes written — HBM-bound.
+// Per record: 16 B of grid read, 64 B box + 4 B perm + 2.2 B of level boxes written —
+// HBM-bound.
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <algorithm>
 
 #include "../../include/mcx.h"
 #include "mcx_common.cuh"
@@ -29,6 +37,15 @@
 namespace mcx {
 
 constexpr int PACK_THREADS = A_BLOCK / 2;  // one thread per storage quad of a block
+
+// The grid window of a block of two full tiles: 17 vertex rows × 33 vertex columns per
+// plane, rows padded to 36 doubles (≡ 4 mod 16, so the 4×4-quad sub-tile a half-warp
+// reads covers 16 distinct bank pairs).
+constexpr int WIN_ROWS = ORDER_TILE_Q + 1;
+constexpr int WIN_COLS = 2 * ORDER_TILE_Q + 1;
+constexpr int WIN_STRIDE = 36;
+constexpr int WIN_PLANE = WIN_ROWS * WIN_STRIDE;
+constexpr int WIN_LOADS = 4 * WIN_ROWS * WIN_COLS;
 
 // 16-byte slot q of the staged boxes lives at q with its column (q mod 8) XORed by its
 // 128-byte row (q / 8) mod 8
@@ -39,10 +56,11 @@ __device__ __forceinline__ unsigned dhi(double x) { return (unsigned)__double2hi
 struct PackSmem {
   Box box[A_BLOCK];
   Box gsm[A_BLOCK / GROUP];
+  double win[2][4 * WIN_PLANE];
 };
 
 #ifndef PACK_MIN_BLOCKS
-#define PACK_MIN_BLOCKS 3
+#define PACK_MIN_BLOCKS 2
 #endif
 
 // min / max of canonical values (finite or ±Inf, no −0.0 mixed with +0.0 — see the
@@ -51,150 +69,222 @@ struct PackSmem {
 __device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : a; }
 __device__ __forceinline__ double dmax(double a, double b) { return b > a ? b : a; }
 
-__global__ void __launch_bounds__(PACK_THREADS, PACK_MIN_BLOCKS) pack_kernel(const double* __restrict__ coords, uint32_t N,
-                                                               uint32_t M, uint32_t Mp, int tiled, Box* __restrict__ box,
-                                                               uint32_t* __restrict__ perm, Box* __restrict__ gbox,
-                                                               Box* __restrict__ tbox, Box* __restrict__ bbox,
-                                                               uint32_t* __restrict__ status, uint32_t blk0) {
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// Storage-map geometry of block blk: tile row tk, offset rt inside it; `regular` = the
+// block lies in full tiles of one tile row (bit-field decode), `windowed` = and starts
+// on a tile boundary (exactly two tiles: the shared-memory window path).  One 32-bit
+// division (storage indices are < 2^30: the triangle count is < 2^31).
+struct BlockGeom {
+  uint32_t tk, rt;
+  bool regular, windowed;
+};
+__device__ __forceinline__ BlockGeom block_geom(uint64_t blk, uint32_t N, uint32_t MQ, uint32_t TN, int tiled) {
+  BlockGeom g;
+  const uint32_t sq0 = (uint32_t)(blk * PACK_THREADS);
+  g.tk = sq0 / TN;
+  g.rt = sq0 - g.tk * TN;
+  g.regular = tiled && g.tk * ORDER_TILE_Q + ORDER_TILE_Q <= MQ && g.rt + PACK_THREADS <= ((N / ORDER_TILE_Q) << 8);
+  g.windowed = g.regular && (g.rt & 255) == 0;
+  return g;
+}
+
+// All threads: cp.async the window of a windowed block into `win` (one commit group).
+__device__ __forceinline__ void fetch_window(double* win, const double* __restrict__ coords, uint32_t N,
+                                             uint64_t plane, const BlockGeom& g, int tid) {
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(win);
+  const uint32_t row0 = g.tk * ORDER_TILE_Q, i0 = (g.rt >> 8) * ORDER_TILE_Q;
+#pragma unroll
+  for (int u = 0; u < (WIN_LOADS + PACK_THREADS - 1) / PACK_THREADS; ++u) {
+    const int e = tid + u * PACK_THREADS;
+    if (e < WIN_LOADS) {
+      const int p = e / (WIN_ROWS * WIN_COLS), rem = e - p * (WIN_ROWS * WIN_COLS);
+      const int r = rem / WIN_COLS, cc = rem - r * WIN_COLS;
+      uint32_t col = i0 + cc;
+      if (col >= N) col -= N;  // the last window column of the last tiles wraps to θ index 0
+      cp_async8(sbase + 8u * (p * WIN_PLANE + r * WIN_STRIDE + cc), coords + p * plane + (uint64_t)(row0 + r) * N + col);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(PACK_THREADS, PACK_MIN_BLOCKS)
+    pack_kernel(const double* __restrict__ coords, uint32_t N, uint32_t M, uint32_t Mp, int tiled,
+                Box* __restrict__ box, uint32_t* __restrict__ perm, Box* __restrict__ gbox, Box* __restrict__ tbox,
+                Box* __restrict__ bbox, uint32_t* __restrict__ status, uint32_t blk0, uint32_t blk1) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   PackSmem& S = *reinterpret_cast<PackSmem*>(smem_raw);
   const uint32_t MQ = M - 1;
   const uint64_t nq = (uint64_t)N * MQ;
   const uint64_t n = 2 * nq;
   const int tid = threadIdx.x, lane = tid & 31;
-  const uint64_t blk = blk0 + blockIdx.x;
-  const uint64_t sq = blk * PACK_THREADS + tid;  // storage quad of this thread
-  const bool valid = sq < nq;
-  bool bad = false;
-  double qlo[4], qhi[4];  // union of the quad's two triangle boxes
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    qlo[c] = __longlong_as_double(0x7ff0000000000000ll);
-    qhi[c] = -qlo[c];
-  }
-  // The storage map inverted.  Fast path: a CTA whose 512 quads lie in full 16×16
-  // tiles of one tile row (all but the ragged edge CTAs) decodes its quads by bit fields
-  // after one CTA-uniform 32-bit division; the rest call quad_of_storage.  (sq < 2^30:
-  // the triangle count is < 2^31.)
-  const uint32_t sq0 = (uint32_t)(blk * PACK_THREADS);
   const uint32_t TN = N <= (0xffffffffu / ORDER_TILE_Q) ? (uint32_t)ORDER_TILE_Q * N : 0xffffffffu;
-  const uint32_t tk0 = sq0 / TN, rt0 = sq0 - tk0 * TN;
-  const bool regular = tiled && tk0 * ORDER_TILE_Q + ORDER_TILE_Q <= MQ &&
-                       rt0 + PACK_THREADS <= ((N / ORDER_TILE_Q) << 8);
-  if (valid) {
-    uint32_t i, k;
-    if (regular) {
-      const uint32_t r = rt0 + tid, rr = r & 255;  // tile r >> 8, 4×4 sub-tile rr >> 4, quad rr & 15
-      i = (r >> 8) * ORDER_TILE_Q + ((rr >> 4) & 3) * ORDER_SUB_Q + (rr & 3);
-      k = tk0 * ORDER_TILE_Q + (rr >> 6) * ORDER_SUB_Q + ((rr >> 2) & 3);
-    } else if (tiled) {
-      quad_of_storage32((uint32_t)sq, N, MQ, i, k);
-    } else {
-      i = (uint32_t)sq % N;
-      k = (uint32_t)sq / N;
+  const uint64_t plane = (uint64_t)Mp * N;  // Mp: plane stride in rows
+  // the thread's quad inside a windowed block: tile tid >> 8, 4×4 sub-tile, quad
+  const uint32_t rr = tid & 255;
+  const uint32_t li = (tid >> 8) * ORDER_TILE_Q + ((rr >> 4) & 3) * ORDER_SUB_Q + (rr & 3);
+  const uint32_t lk = (rr >> 6) * ORDER_SUB_Q + ((rr >> 2) & 3);
+  bool bad = false;
+  uint64_t blk = blk0 + blockIdx.x;
+  if (blk < blk1) {
+    const BlockGeom g = block_geom(blk, N, MQ, TN, tiled);
+    if (g.windowed) fetch_window(S.win[0], coords, N, plane, g, tid);
+  }
+  cp_async_commit();
+  for (int it = 0; blk < blk1; ++it, blk += gridDim.x) {
+    const BlockGeom g = block_geom(blk, N, MQ, TN, tiled);
+    const double* win = S.win[it & 1];
+    cp_async_wait_all();
+    __syncthreads();  // the window is visible; every thread is done with the previous block
+    {
+      const uint64_t nb = blk + gridDim.x;
+      if (nb < blk1) {
+        const BlockGeom gn = block_geom(nb, N, MQ, TN, tiled);
+        if (gn.windowed) fetch_window(S.win[(it + 1) & 1], coords, N, plane, gn, tid);
+      }
+      cp_async_commit();
     }
-    const uint32_t t0 = 2 * (i + N * k);
-    // the quad's 4 vertices once (16 loads, all issued before use): T¹ = (v00, v10,
-    // v01), T² = (v01, v10, v11) — the vertex sets of tri_verts, −0.0 canonicalised
-    const uint32_t ip = (i + 1 == N) ? 0 : i + 1;
-    const uint64_t r0 = (uint64_t)k * N, r1 = r0 + N, plane = (uint64_t)Mp * N;  // Mp: plane stride in rows
-    double w00[4], w10[4], w01[4], w11[4];
+    const uint64_t sq = blk * PACK_THREADS + tid;  // storage quad of this thread
+    double qlo[4], qhi[4];  // union of the quad's two triangle boxes
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      const double* pl = coords + c * plane;
-      w00[c] = __ldg(pl + r0 + i);
-      w10[c] = __ldg(pl + r0 + ip);
-      w01[c] = __ldg(pl + r1 + i);
-      w11[c] = __ldg(pl + r1 + ip);
+      qlo[c] = __longlong_as_double(0x7ff0000000000000ll);
+      qhi[c] = -qlo[c];
     }
-    // B200 has no FP64 min/max instruction (each is a DSETP + 2 selects), so the two
-    // triangles share min/max(v10, v01); min/max of finite non-NaN values is exact and
-    // order-free, so the boxes are the bits of the three-way min/max (NaN/Inf inputs flag
-    // the mesh as unusable anyway).
-    Box b1, b2;
+    if (sq < nq) {
+      uint32_t i, k;
+      double w00[4], w10[4], w01[4], w11[4];
+      if (g.windowed) {
+        i = (g.rt >> 8) * ORDER_TILE_Q + li;
+        k = g.tk * ORDER_TILE_Q + lk;
+        const double* w = win + lk * WIN_STRIDE + li;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const double a = dadd(w00[c], 0.0), b = dadd(w10[c], 0.0), d = dadd(w01[c], 0.0), e = dadd(w11[c], 0.0);
-      bad |= !(isfinite(a) && isfinite(b) && isfinite(d) && isfinite(e));
-      const double mn = dmin(b, d), mx = dmax(b, d);
-      b1.lo[c] = dmin(a, mn);
-      b1.hi[c] = dmax(a, mx);
-      b2.lo[c] = dmin(e, mn);
-      b2.hi[c] = dmax(e, mx);
-      qlo[c] = dmin(b1.lo[c], b2.lo[c]);
-      qhi[c] = dmax(b1.hi[c], b2.hi[c]);
-    }
-    // staging stores: chunk j (16 B) of record r = 2·tid + τ sits at 16-byte slot
-    // swz(4r + j); lanes are 128 B apart, so the XOR swizzle spreads each 8-lane phase
-    // over all 8 bank columns (unswizzled: 8-way conflicts)
-    uint4* st = reinterpret_cast<uint4*>(S.box);
+        for (int c = 0; c < 4; ++c) {
+          w00[c] = w[c * WIN_PLANE];
+          w10[c] = w[c * WIN_PLANE + 1];
+          w01[c] = w[c * WIN_PLANE + WIN_STRIDE];
+          w11[c] = w[c * WIN_PLANE + WIN_STRIDE + 1];
+        }
+      } else {
+        if (g.regular) {
+          const uint32_t r = g.rt + tid, q = r & 255;  // tile r >> 8, 4×4 sub-tile q >> 4, quad q & 15
+          i = (r >> 8) * ORDER_TILE_Q + ((q >> 4) & 3) * ORDER_SUB_Q + (q & 3);
+          k = g.tk * ORDER_TILE_Q + (q >> 6) * ORDER_SUB_Q + ((q >> 2) & 3);
+        } else if (tiled) {
+          quad_of_storage32((uint32_t)sq, N, MQ, i, k);
+        } else {
+          i = (uint32_t)sq % N;
+          k = (uint32_t)sq / N;
+        }
+        const uint32_t ip = (i + 1 == N) ? 0 : i + 1;
+        const uint64_t r0 = (uint64_t)k * N, r1 = r0 + N;
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      st[swz(8 * tid + j)] = make_uint4(dlo(b1.lo[2 * j]), dhi(b1.lo[2 * j]), dlo(b1.lo[2 * j + 1]), dhi(b1.lo[2 * j + 1]));
-      st[swz(8 * tid + 2 + j)] =
-          make_uint4(dlo(b1.hi[2 * j]), dhi(b1.hi[2 * j]), dlo(b1.hi[2 * j + 1]), dhi(b1.hi[2 * j + 1]));
-      st[swz(8 * tid + 4 + j)] = make_uint4(dlo(b2.lo[2 * j]), dhi(b2.lo[2 * j]), dlo(b2.lo[2 * j + 1]), dhi(b2.lo[2 * j + 1]));
-      st[swz(8 * tid + 6 + j)] =
-          make_uint4(dlo(b2.hi[2 * j]), dhi(b2.hi[2 * j]), dlo(b2.hi[2 * j + 1]), dhi(b2.hi[2 * j + 1]));
-    }
-    if (perm) reinterpret_cast<uint2*>(perm)[sq] = make_uint2(t0, t0 + 1);
-  }
-  if (status && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status, 1u);
-  __syncthreads();
-  {
-    const uint64_t r0 = blk * A_BLOCK;
-    const uint32_t n16 = (uint32_t)(min((uint64_t)A_BLOCK, n - r0) * (sizeof(Box) / 16));
-    const uint4* src = reinterpret_cast<const uint4*>(S.box);
-    uint4* dst = reinterpret_cast<uint4*>(box + r0);
-    for (uint32_t q = tid; q < n16; q += PACK_THREADS) dst[q] = src[swz(q)];
-  }
-  if (gbox) {
-    // group = 16 consecutive storage quads = half a warp.  Reduce-scatter instead of an
-    // all-reduce: v = the quad box with its hi half negated (every step is then a min;
-    // the canonicalised inputs hold no −0, so the negated zeros are all −0 and the result
-    // bits equal the unnegated max); at xor 8 / 4 / 2 each lane keeps half of what it
-    // holds, xor 1 completes, and lane pair p of the half-warp holds component p of the
-    // group box — 8 shuffled values per lane instead of 32.
-    const int hl = lane & 15;
-    const bool x3 = hl & 8, x2 = hl & 4, x1 = hl & 2;
-    double v4[4], v2[2];
+        for (int c = 0; c < 4; ++c) {
+          const double* pl = coords + c * plane;
+          w00[c] = __ldg(pl + r0 + i);
+          w10[c] = __ldg(pl + r0 + ip);
+          w01[c] = __ldg(pl + r1 + i);
+          w11[c] = __ldg(pl + r1 + ip);
+        }
+      }
+      const uint32_t t0 = 2 * (i + N * k);
+      // T¹ = (v00, v10, v01), T² = (v01, v10, v11) — the vertex sets of tri_verts, −0.0
+      // canonicalised.  B200 has no FP64 min/max instruction (each is a DSETP + 2
+      // selects), so the two triangles share min/max(v10, v01); min/max of finite
+      // non-NaN values is exact and order-free, so the boxes are the bits of the
+      // three-way min/max (NaN/Inf inputs flag the mesh as unusable anyway).
+      Box b1, b2;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const double lo = qlo[j], nhi = -qhi[j];
-      v4[j] = dmin(x3 ? nhi : lo, __shfl_xor_sync(0xffffffffu, x3 ? lo : nhi, 8));
-    }
+      for (int c = 0; c < 4; ++c) {
+        const double a = dadd(w00[c], 0.0), b = dadd(w10[c], 0.0), d = dadd(w01[c], 0.0), e = dadd(w11[c], 0.0);
+        bad |= !(isfinite(a) && isfinite(b) && isfinite(d) && isfinite(e));
+        const double mn = dmin(b, d), mx = dmax(b, d);
+        b1.lo[c] = dmin(a, mn);
+        b1.hi[c] = dmax(a, mx);
+        b2.lo[c] = dmin(e, mn);
+        b2.hi[c] = dmax(e, mx);
+        qlo[c] = dmin(b1.lo[c], b2.lo[c]);
+        qhi[c] = dmax(b1.hi[c], b2.hi[c]);
+      }
+      // staging stores: chunk j (16 B) of record r = 2·tid + τ sits at 16-byte slot
+      // swz(4r + j); lanes are 128 B apart, so the XOR swizzle spreads each 8-lane phase
+      // over all 8 bank columns (unswizzled: 8-way conflicts)
+      uint4* st = reinterpret_cast<uint4*>(S.box);
 #pragma unroll
-    for (int j = 0; j < 2; ++j)
-      v2[j] = dmin(x2 ? v4[2 + j] : v4[j], __shfl_xor_sync(0xffffffffu, x2 ? v4[j] : v4[2 + j], 4));
-    double v1 = dmin(x1 ? v2[1] : v2[0], __shfl_xor_sync(0xffffffffu, x1 ? v2[0] : v2[1], 2));
-    v1 = dmin(v1, __shfl_xor_sync(0xffffffffu, v1, 1));
-    const int comp = (hl >> 1);  // = 4·x3 + 2·x2 + x1: lo[0..3], hi[0..3]
-    const uint64_t ng = (n + GROUP - 1) / GROUP;
-    double* gs = reinterpret_cast<double*>(S.gsm);
-    if (!(lane & 1)) {
-      const uint64_t g = blk * (A_BLOCK / GROUP) + (tid >> 4);
-      const double val = x3 ? -v1 : v1;
-      gs[(tid >> 4) * 8 + comp] = val;
-      if (g < ng) reinterpret_cast<double*>(gbox)[g * 8 + comp] = val;
+      for (int j = 0; j < 2; ++j) {
+        st[swz(8 * tid + j)] =
+            make_uint4(dlo(b1.lo[2 * j]), dhi(b1.lo[2 * j]), dlo(b1.lo[2 * j + 1]), dhi(b1.lo[2 * j + 1]));
+        st[swz(8 * tid + 2 + j)] =
+            make_uint4(dlo(b1.hi[2 * j]), dhi(b1.hi[2 * j]), dlo(b1.hi[2 * j + 1]), dhi(b1.hi[2 * j + 1]));
+        st[swz(8 * tid + 4 + j)] =
+            make_uint4(dlo(b2.lo[2 * j]), dhi(b2.lo[2 * j]), dlo(b2.lo[2 * j + 1]), dhi(b2.lo[2 * j + 1]));
+        st[swz(8 * tid + 6 + j)] =
+            make_uint4(dlo(b2.hi[2 * j]), dhi(b2.hi[2 * j]), dlo(b2.hi[2 * j + 1]), dhi(b2.hi[2 * j + 1]));
+      }
+      if (perm) reinterpret_cast<uint2*>(perm)[sq] = make_uint2(t0, t0 + 1);
     }
     __syncthreads();
-    if (tid < 32 && tbox && bbox) {
-      // warp 0: lane l reduces component c = l & 7 over groups 8·(l >> 3) .. +7 (hi
-      // components negated again), xor 8 gives the lane's 512-record tile, xor 16 the block
-      const int c = lane & 7;
-      const unsigned long long neg = c >= 4 ? 0x8000000000000000ull : 0ull;
-      const double* src = gs + 64 * (lane >> 3) + c;
-      double m = __longlong_as_double(__double_as_longlong(src[0]) ^ neg);
+    {
+      const uint64_t r0 = blk * A_BLOCK;
+      const uint32_t n16 = (uint32_t)(min((uint64_t)A_BLOCK, n - r0) * (sizeof(Box) / 16));
+      const uint4* src = reinterpret_cast<const uint4*>(S.box);
+      uint4* dst = reinterpret_cast<uint4*>(box + r0);
+      for (uint32_t q = tid; q < n16; q += PACK_THREADS) dst[q] = src[swz(q)];
+    }
+    if (gbox) {
+      // group = 16 consecutive storage quads = half a warp.  Reduce-scatter instead of an
+      // all-reduce: v = the quad box with its hi half negated (every step is then a min;
+      // the canonicalised inputs hold no −0, so the negated zeros are all −0 and the
+      // result bits equal the unnegated max); at xor 8 / 4 / 2 each lane keeps half of
+      // what it holds, xor 1 completes, and lane pair p of the half-warp holds component
+      // p of the group box — 8 shuffled values per lane instead of 32.
+      const int hl = lane & 15;
+      const bool x3 = hl & 8, x2 = hl & 4, x1 = hl & 2;
+      double v4[4], v2[2];
 #pragma unroll
-      for (int g = 1; g < 8; ++g) m = dmin(m, __longlong_as_double(__double_as_longlong(src[8 * g]) ^ neg));
-      m = dmin(m, __shfl_xor_sync(0xffffffffu, m, 8));
-      const uint64_t tt = blk * (A_BLOCK / TILE) + (lane >> 4);
-      if (!(lane & 8) && tt < (n + TILE - 1) / TILE)
-        reinterpret_cast<double*>(tbox)[tt * 8 + c] = __longlong_as_double(__double_as_longlong(m) ^ neg);
-      m = dmin(m, __shfl_xor_sync(0xffffffffu, m, 16));
-      if (lane < 8) reinterpret_cast<double*>(bbox)[blk * 8 + c] = __longlong_as_double(__double_as_longlong(m) ^ neg);
+      for (int j = 0; j < 4; ++j) {
+        const double lo = qlo[j], nhi = -qhi[j];
+        v4[j] = dmin(x3 ? nhi : lo, __shfl_xor_sync(0xffffffffu, x3 ? lo : nhi, 8));
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        v2[j] = dmin(x2 ? v4[2 + j] : v4[j], __shfl_xor_sync(0xffffffffu, x2 ? v4[j] : v4[2 + j], 4));
+      double v1 = dmin(x1 ? v2[1] : v2[0], __shfl_xor_sync(0xffffffffu, x1 ? v2[0] : v2[1], 2));
+      v1 = dmin(v1, __shfl_xor_sync(0xffffffffu, v1, 1));
+      const int comp = (hl >> 1);  // = 4·x3 + 2·x2 + x1: lo[0..3], hi[0..3]
+      const uint64_t ng = (n + GROUP - 1) / GROUP;
+      double* gs = reinterpret_cast<double*>(S.gsm);
+      if (!(lane & 1)) {
+        const uint64_t gi = blk * (A_BLOCK / GROUP) + (tid >> 4);
+        const double val = x3 ? -v1 : v1;
+        gs[(tid >> 4) * 8 + comp] = val;
+        if (gi < ng) reinterpret_cast<double*>(gbox)[gi * 8 + comp] = val;
+      }
+      __syncthreads();
+      if (tid < 32 && tbox && bbox) {
+        // warp 0: lane l reduces component c = l & 7 over groups 8·(l >> 3) .. +7 (hi
+        // components negated again), xor 8 gives the lane's 512-record tile, xor 16 the block
+        const int c = lane & 7;
+        const unsigned long long neg = c >= 4 ? 0x8000000000000000ull : 0ull;
+        const double* src = gs + 64 * (lane >> 3) + c;
+        double m = __longlong_as_double(__double_as_longlong(src[0]) ^ neg);
+#pragma unroll
+        for (int q = 1; q < 8; ++q) m = dmin(m, __longlong_as_double(__double_as_longlong(src[8 * q]) ^ neg));
+        m = dmin(m, __shfl_xor_sync(0xffffffffu, m, 8));
+        const uint64_t tt = blk * (A_BLOCK / TILE) + (lane >> 4);
+        if (!(lane & 8) && tt < (n + TILE - 1) / TILE)
+          reinterpret_cast<double*>(tbox)[tt * 8 + c] = __longlong_as_double(__double_as_longlong(m) ^ neg);
+        m = dmin(m, __shfl_xor_sync(0xffffffffu, m, 16));
+        if (lane < 8)
+          reinterpret_cast<double*>(bbox)[blk * 8 + c] = __longlong_as_double(__double_as_longlong(m) ^ neg);
+      }
     }
   }
+  cp_async_wait_all();
+  if (status && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status, 1u);
 }
 
 // Culling hierarchy of an arbitrary box array: one CTA per 1024-record block.  Each
@@ -283,9 +373,10 @@ int pack_enqueue(const double* coords, uint32_t N, uint32_t M, int order, double
                               &slots))
     return rc;
   if (status && b0 == 0) CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(uint32_t), stream));
-  pack_kernel<<<(unsigned)(b1 - b0), PACK_THREADS, sizeof(PackSmem), stream>>>(
+  const unsigned grid = (unsigned)std::min<uint64_t>(b1 - b0, slots);  // persistent CTAs
+  pack_kernel<<<grid, PACK_THREADS, sizeof(PackSmem), stream>>>(
       coords, N, M, Mp, order == MCX_ORDER_TILED, reinterpret_cast<Box*>(box), perm, reinterpret_cast<Box*>(gbox),
-      reinterpret_cast<Box*>(tbox), reinterpret_cast<Box*>(bbox), status, (uint32_t)b0);
+      reinterpret_cast<Box*>(tbox), reinterpret_cast<Box*>(bbox), status, (uint32_t)b0, (uint32_t)b1);
   CUDA_TRY(cudaGetLastError());
   return MCX_OK;
 }
