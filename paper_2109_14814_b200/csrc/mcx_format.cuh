@@ -105,13 +105,25 @@ MCX_HD uint32_t pow10u(int k) {  // k in [0, 9]
   return p;
 }
 
+// 10^k for k in [0, 19] (< 2^64): five predicated multiplies instead of a k-long chain
+MCX_HD uint64_t pow10_u64(int k) {
+  uint64_t p = 1;
+  if (k & 1) p *= 10u;
+  if (k & 2) p *= 100u;
+  if (k & 4) p *= 10000u;
+  if (k & 8) p *= 100000000u;
+  if (k & 16) p *= 10000000000000000ull;
+  return p;
+}
+
 // round-half-even(|v| · 10^k) for finite v = m·2^e2 (m > 0)
 MCX_HD uint64_t scaled_round(uint64_t m, int e2, int k) {
   // Fast path in 128-bit registers for the usual magnitudes (2m·10^k and its shift fit):
   // no local-memory big integer.  Same exact arithmetic, so the same digits.
   if (k >= 0 && k <= 22 && e2 > -127 && e2 <= 0) {
-    unsigned __int128 q = (unsigned __int128)(2 * m);
-    for (int r = 0; r < k; ++r) q *= 10u;  // 2m·10^k < 2^54 · 10^22 < 2^128
+    // 2m·10^k < 2^54 · 10^22 < 2^128
+    unsigned __int128 q = (unsigned __int128)(2 * m) * pow10_u64(k <= 19 ? k : 19);
+    if (k > 19) q *= pow10_u64(k - 19);
     const int sh = -e2;
     const bool sticky = sh && (q & (((unsigned __int128)1 << sh) - 1)) != 0;
     q >>= sh;
@@ -134,21 +146,38 @@ MCX_HD uint64_t scaled_round(uint64_t m, int e2, int k) {
 }
 
 // floor(log10(m·2^e2)) estimate, exact to ±1 (corrected by the caller)
+MCX_HD int bit_length(uint64_t x) {  // x > 0
+#ifdef __CUDA_ARCH__
+  return 64 - __clzll((long long)x);
+#else
+  return 64 - __builtin_clzll(x);
+#endif
+}
+
 MCX_HD int log10_estimate(uint64_t m, int e2) {
-  int bits = 0;
-  for (uint64_t x = m; x; x >>= 1) ++bits;
+  const int bits = bit_length(m);
   const int e = e2 + bits - 1;  // 2^e <= v < 2^(e+1)
   // floor(e · log10 2) with log10 2 ≈ 78913 / 2^18 (exact floor for |e| < 1650)
   return (int)(((int64_t)e * 78913) >> 18);  // arithmetic shift: floor for e < 0 too
 }
 
 MCX_HD int put_u64(char* o, uint64_t v) {
+  // 9-digit chunks in 32-bit arithmetic (one 64-bit division by a constant per chunk)
   char t[24];
   int n = 0;
+  while (v >= 1000000000ull) {
+    uint32_t c = (uint32_t)(v % 1000000000ull);
+    v /= 1000000000ull;
+    for (int i = 0; i < 9; ++i) {
+      t[n++] = (char)('0' + c % 10u);
+      c /= 10u;
+    }
+  }
+  uint32_t c = (uint32_t)v;
   do {
-    t[n++] = (char)('0' + v % 10);
-    v /= 10;
-  } while (v);
+    t[n++] = (char)('0' + c % 10u);
+    c /= 10u;
+  } while (c);
   for (int i = 0; i < n; ++i) o[i] = t[n - 1 - i];
   return n;
 }
@@ -191,10 +220,16 @@ MCX_HD int fmt_g17(double v, char* o) {
     if (D < LO) { --E; continue; }
     break;
   }
+  // the 17 digits as two independent 32-bit chains: D = hi·10^8 + lo (hi < 10^9)
   char d[17];
-  for (int i = 16; i >= 0; --i) {
-    d[i] = (char)('0' + D % 10);
-    D /= 10;
+  uint32_t hi = (uint32_t)(D / 100000000ull), lo = (uint32_t)(D - (uint64_t)hi * 100000000ull);
+  for (int i = 16; i >= 9; --i) {
+    d[i] = (char)('0' + lo % 10u);
+    lo /= 10u;
+  }
+  for (int i = 8; i >= 0; --i) {
+    d[i] = (char)('0' + hi % 10u);
+    hi /= 10u;
   }
   int last = 16;  // last significant digit
   while (last > 0 && d[last] == '0') --last;

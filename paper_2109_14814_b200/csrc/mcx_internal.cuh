@@ -20,8 +20,20 @@ int pack_enqueue(const double* coords, uint32_t N, uint32_t M, int order, double
 // synchronises o->stream and fills the stats.  Otherwise the workspace header (8 + 8·n
 // u64s) is copied to h_counters (pinned) asynchronously, only stats[t].n_pairs is set,
 // and the caller synchronises and calls batch_stats (requires o->timing == 0).
+//
+// step != nullptr: this call is one step of a sequence over A-ranges of the same tasks
+// sharing one workspace (MCX_MODE_CULL only): the workspace layout is that of
+// step->whole (the tasks with their full ranges), only the first step zeroes the
+// counters, each step's cull / solve kernels take the block-list and candidate entries
+// the previous steps left unprocessed (header words 5 and 6), and the tasks are used as
+// given with the solve un-swapping every hit when step->swap (the caller oriented them).
+struct BatchStep {
+  const mcx_task* whole;
+  bool first;
+  bool swap;
+};
 int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mcx_hit* hits, uint32_t* hit_task,
-                 uint64_t cap, mcx_stats* st, unsigned long long* h_counters);
+                 uint64_t cap, mcx_stats* st, unsigned long long* h_counters, const BatchStep* step = nullptr);
 int batch_stats(const unsigned long long* h, uint32_t n, const mcx_opts* o, uint64_t cap, mcx_stats* st, float ms);
 
 // mcx_search.cu: one-time per (kernel, device, threads, smem) launch setup — the

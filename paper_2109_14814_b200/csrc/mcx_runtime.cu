@@ -36,6 +36,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <functional>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
@@ -80,10 +81,12 @@ struct JobDev {
 struct mcx_context {
   int device = 0;
   cudaStream_t s0 = nullptr, s1 = nullptr;
+  cudaStream_t sc = nullptr;  // H2D copies of a chunked upload whose packs and searches run on s0
   cudaEvent_t ev = nullptr;
+  cudaEvent_t cev[9] = {};  // chunk j copied (cev[8]: the allocations are made)
   cudaMemPool_t pool = nullptr;
   mcx::DevBuf ws, hits, hit_task, jobs, k0, k1, v0, v1, recs, recs_out, state, blocked, pairs, lens, offs, cub,
-      text, small, flen;
+      text, small, flen, lines;
   mcx::HostBuf h_recs, h_text, h_small, h_counters;
   mcx::HostBuf h_map;    // mapped pinned memory the small-path kernel writes its results to
   mcx::HostStage stage;  // pinned staging of the per-call tables
@@ -330,16 +333,26 @@ __global__ void field_write_kernel(const mcx_record* __restrict__ recs, const ui
   }
 }
 
+// find_intersections searches the larger mesh chunk by chunk during its upload
+// (find_stepped) from this many triangles on (load_mesh splits it into >= 4 chunks)
+// and is at least STEP_RATIO times the other mesh (which must be uploaded before the
+// first step: two similar meshes share the link until the end, and the per-step fixed
+// costs then follow the copy instead of hiding under it — measured on C3)
+constexpr uint64_t STEP_MIN_TRI = 1ull << 18;
+constexpr uint64_t STEP_RATIO = 4;
+
 // ------------------------------------------------------------------ small hit counts
 // Steps 2-6 in ONE single-CTA kernel for n ≤ SMALL_N hits (the common case: a handful
 // to a few hundred intersections per layer pair): bitonic sort of the (job, gid, τ_A,
 // τ_B) keys in shared memory, records, the 1e-9 dedup (all earlier records of the job
 // scanned; ≤ SMALL_K close predecessors each, else the general path reruns it), the
 // greedy rule resolved in rounds, and block-scan compaction of records and text.
-// Keys are unique ((gid, τ) ↔ (iA, iB) within a job), so sort stability is moot.
+// The dedup scan reads the points and job ids from shared memory (structure of arrays:
+// consecutive threads, consecutive words).  Keys are unique ((gid, τ) ↔ (iA, iB) within a job), so sort stability is moot.
 constexpr int SMALL_N = 1024;
 constexpr int SMALL_K = 8;
 constexpr int REC_LINE_MAX = 352;  // ≥ the longest records line (349 bytes)
+constexpr unsigned SMALL_NONE = 0xffffffffu;  // "no small-path text" (small_lines / small_pack)
 
 struct SmallOut {
   unsigned long long kept, text_bytes, overflow;
@@ -377,9 +390,8 @@ struct SmallSmem {
   uint16_t idx[SMALL_N];
   uint16_t nb[SMALL_N][SMALL_K];
   uint8_t nnb[SMALL_N], state[SMALL_N];
-  uint16_t kept_rec[SMALL_N];                       // kept position → record
-  uint32_t line_off[SMALL_N];                       // kept position → text offset
-  uint8_t flen[SMALL_N * fmt::LINE_FIELDS];          // field lengths (text)
+  double px[4][SMALL_N];                             // record points (dedup scan)
+  uint32_t ptask[SMALL_N];                           // record jobs
   uint32_t warp_sums[32];
   int overflow;
 };
@@ -394,8 +406,8 @@ __global__ void __launch_bounds__(1024) post_small_kernel(const mcx_hit* __restr
                                                           uint64_t n_cap, const JobDev* __restrict__ jobs,
                                                           int gid_shift, int dedup, int want_text,
                                                           mcx_record* __restrict__ recs, mcx_record* __restrict__ out,
-                                                          char* __restrict__ text, SmallOut* __restrict__ res,
-                                                          mcx_record* __restrict__ h_out, char* __restrict__ h_text) {
+                                                          unsigned* __restrict__ total_dev, SmallOut* __restrict__ res,
+                                                          mcx_record* __restrict__ h_out) {
   extern __shared__ __align__(16) unsigned char small_raw[];
   SmallSmem& S = *reinterpret_cast<SmallSmem*>(small_raw);
   unsigned long long* key = S.key;
@@ -406,6 +418,23 @@ __global__ void __launch_bounds__(1024) post_small_kernel(const mcx_hit* __restr
   uint32_t* warp_sums = S.warp_sums;
   int& overflow = S.overflow;
   const int tid = threadIdx.x;
+  if (tid == 0) {
+    total_dev[0] = SMALL_NONE;  // until the records are complete (early exits)
+    total_dev[1] = 0;           // small_text_kernel's CTA counter
+  }
+#if MCX_SMALL_PROF  // phase clocks (tools/microbench/build_variant.py -DMCX_SMALL_PROF=1)
+  __shared__ long long tprof[11];
+  if (tid == 0) tprof[10] = clock64();
+#define SMALL_PHASE(id)              \
+  do {                               \
+    __syncthreads();                 \
+    if (tid == 0) tprof[id] = clock64(); \
+  } while (0)
+#else
+#define SMALL_PHASE(id) \
+  do {                  \
+  } while (0)
+#endif
   const uint64_t n64 = min((uint64_t)*n_dev, n_cap);
   if (n64 > (uint64_t)SMALL_N) {
     if (tid == 0) {
@@ -433,6 +462,7 @@ __global__ void __launch_bounds__(1024) post_small_kernel(const mcx_hit* __restr
     key[k] = kk;
     idx[k] = (uint16_t)k;
   }
+  SMALL_PHASE(0);
   __syncthreads();
   for (uint32_t k = 2; k <= P; k <<= 1)
     for (uint32_t j = k >> 1; j > 0; j >>= 1) {
@@ -452,6 +482,7 @@ __global__ void __launch_bounds__(1024) post_small_kernel(const mcx_hit* __restr
       }
       __syncthreads();
     }
+  SMALL_PHASE(1);
   const uint32_t r = tid;  // one record per thread (n ≤ 1024 = blockDim)
   const bool valid = r < n;
   if (valid) {
@@ -467,17 +498,47 @@ __global__ void __launch_bounds__(1024) post_small_kernel(const mcx_hit* __restr
     R.task = t;
     R.pad[0] = R.pad[1] = R.pad[2] = 0;
     recs[r] = R;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) S.px[c][r] = R.point[c];
+    S.ptask[r] = t;
   }
-  __syncthreads();  // records visible (global, L1 of this SM)
+  __syncthreads();  // records visible (global, L1 of this SM; points and jobs in shared memory)
+  SMALL_PHASE(2);
   // dedup: close predecessors of r within its job (records of a job are contiguous)
   uint8_t cnt = 0;
   if (valid && dedup) {
-    const mcx_record& R = recs[r];
-    for (int e = (int)r - 1; e >= 0; --e) {
-      const mcx_record& E = recs[e];
-      if (E.task != R.task) break;
-      if (fabs(dsub(R.point[0], E.point[0])) <= MCX_DEDUP_TOL && fabs(dsub(R.point[1], E.point[1])) <= MCX_DEDUP_TOL &&
-          fabs(dsub(R.point[2], E.point[2])) <= MCX_DEDUP_TOL && fabs(dsub(R.point[3], E.point[3])) <= MCX_DEDUP_TOL) {
+    const double x0 = S.px[0][r], x1 = S.px[1][r], x2 = S.px[2][r], x3 = S.px[3][r];
+    const uint32_t tr = S.ptask[r];
+    // predecessors in descending order, 4 per iteration (independent shared loads);
+    // the scan stops at the first record of another job
+    auto close = [&](int e) {
+      return fabs(dsub(x0, S.px[0][e])) <= MCX_DEDUP_TOL && fabs(dsub(x1, S.px[1][e])) <= MCX_DEDUP_TOL &&
+             fabs(dsub(x2, S.px[2][e])) <= MCX_DEDUP_TOL && fabs(dsub(x3, S.px[3][e])) <= MCX_DEDUP_TOL;
+    };
+    bool stop = false;
+    int e = (int)r - 1;
+    for (; e >= 3 && !stop; e -= 4) {
+      double xs[4];
+      uint32_t ts[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        xs[u] = S.px[0][e - u];
+        ts[u] = S.ptask[e - u];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (stop) break;
+        if (ts[u] != tr) {
+          stop = true;
+        } else if (fabs(dsub(x0, xs[u])) <= MCX_DEDUP_TOL && close(e - u)) {
+          if (cnt < SMALL_K) nb[r][cnt] = (uint16_t)(e - u);
+          ++cnt;
+        }
+      }
+    }
+    for (; e >= 0 && !stop; --e) {
+      if (S.ptask[e] != tr) break;
+      if (close(e)) {
         if (cnt < SMALL_K) nb[r][cnt] = (uint16_t)e;
         ++cnt;
       }
@@ -489,6 +550,7 @@ __global__ void __launch_bounds__(1024) post_small_kernel(const mcx_hit* __restr
     state[r] = cnt ? 0 : 1;
   }
   __syncthreads();
+  SMALL_PHASE(3);
   if (overflow) {
     if (tid == 0) {
       res->kept = res->text_bytes = 0;
@@ -513,61 +575,135 @@ __global__ void __launch_bounds__(1024) post_small_kernel(const mcx_hit* __restr
       if (!__syncthreads_or(left)) break;
     }
   }
+  SMALL_PHASE(4);
   const bool keep = valid && state[r] == 1;
   uint32_t total;
   const uint32_t pos = block_excl_scan(keep ? 1u : 0u, warp_sums, &total);
   if (keep) {
     out[pos] = recs[r];
-    S.kept_rec[pos] = (uint16_t)r;
   }
   __syncthreads();
-  // text: one thread per (kept record, field) — field lengths, line offsets (block scan),
-  // then every field written at its offset; the exact conversions run side by side
-  constexpr int F = fmt::LINE_FIELDS;
-  uint32_t tbytes = 0;
-  if (want_text) {
-    for (uint32_t q = tid; q < total * F; q += blockDim.x) {
-      const mcx_record& R = recs[S.kept_rec[q / F]];
-      const JobDev& J = jobs[R.task];
-      char f[32];
-      S.flen[q] = (uint8_t)fmt::fmt_field(f, (int)(q % F), J.n1, J.sign1, J.n2, J.sign2, R.gid, R.point, R.bary,
-                                          R.params);
-    }
-    __syncthreads();
-    uint32_t len = 0;
-    if (tid < total)
-      for (int f = 0; f < F; ++f) len += S.flen[tid * F + f] + 1u;  // + separator
-    const uint32_t off = block_excl_scan(len, warp_sums, &tbytes);
-    if (tid < total) S.line_off[tid] = off;
-    __syncthreads();
-    for (uint32_t q = tid; q < total * F; q += blockDim.x) {
-      const uint32_t p = q / F, f = q % F;
-      uint32_t o = S.line_off[p];
-      for (uint32_t g = 0; g < f; ++g) o += S.flen[p * F + g] + 1u;
-      const mcx_record& R = recs[S.kept_rec[p]];
-      const JobDev& J = jobs[R.task];
-      char buf[32];
-      int k = fmt::fmt_field(buf, (int)f, J.n1, J.sign1, J.n2, J.sign2, R.gid, R.point, R.bary, R.params);
-      buf[k++] = f == F - 1 ? '\n' : ' ';
-      for (int i = 0; i < k; ++i) text[o + i] = buf[i];
-    }
-  }
-  __syncthreads();
+  SMALL_PHASE(5);
+  // the text lines are formatted by small_lines_kernel / small_pack_kernel (many SMs)
+  SMALL_PHASE(6);
   // coalesced copy-out to the mapped host buffers
   {
     const uint4* src = reinterpret_cast<const uint4*>(out);
     uint4* dst = reinterpret_cast<uint4*>(h_out);
     for (uint32_t q = tid; q < total * (sizeof(mcx_record) / 16); q += blockDim.x) dst[q] = src[q];
-    const uint32_t t16 = tbytes / 16;
-    const uint4* ts = reinterpret_cast<const uint4*>(text);
-    uint4* td = reinterpret_cast<uint4*>(h_text);
-    for (uint32_t q = tid; q < t16; q += blockDim.x) td[q] = ts[q];
-    for (uint32_t q = 16 * t16 + tid; q <= tbytes; q += blockDim.x) h_text[q] = q < tbytes ? text[q] : '\0';
   }
+  SMALL_PHASE(7);
   if (tid == 0) {
+#if MCX_SMALL_PROF
+    const char* nm[8] = {"keys", "sort", "records", "dedup", "resolve", "compact", "-", "copyout"};
+    for (int q = 0; q < 8; ++q)
+      printf("small %-10s %7lld cycles\n", nm[q], tprof[q] - (q ? tprof[q - 1] : tprof[10]));
+#endif
     res->kept = total;
-    res->text_bytes = tbytes;
+    res->text_bytes = 0;  // small_pack_kernel
     res->overflow = 0;
+    *total_dev = want_text ? total : SMALL_NONE;
+  }
+}
+
+// The records text of the small path (after post_small_kernel, same stream), 32 CTAs of
+// 32 warps, one warp per kept line: lane f formats field f (a line's 17 exact conversions
+// side by side) and a warp scan places them in the line's fixed-stride slot.  The last
+// CTA to finish (a device-scope counter) then scans the line lengths and writes the
+// contiguous text to the mapped host buffer in 16-byte stores, each gathered from the
+// line slots.  *total_dev = the kept count
+// (SMALL_NONE: no text — overflow, general path or text not wanted).
+__global__ void __launch_bounds__(1024) small_text_kernel(const mcx_record* __restrict__ recs,
+                                                          const JobDev* __restrict__ jobs,
+                                                          const unsigned* __restrict__ total_dev,
+                                                          unsigned* __restrict__ done, char* __restrict__ slots,
+                                                          uint16_t* __restrict__ line_len, char* __restrict__ h_text,
+                                                          SmallOut* __restrict__ res) {
+  constexpr int F = fmt::LINE_FIELDS;
+  __shared__ uint32_t warp_sums[32];
+  __shared__ uint32_t line_off[SMALL_N + 1];
+  __shared__ bool last;
+#if MCX_SMALL_PROF
+  unsigned long long g0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+#endif
+  const uint32_t total = *total_dev;
+  if (total > (uint32_t)SMALL_N) return;  // uniform over the grid
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t p = warp * gridDim.x + blockIdx.x;  // lines dealt over the CTAs (SMs) first
+  if (p < total) {
+    const mcx_record& R = recs[p];
+    const JobDev& J = jobs[R.task];
+    char f[32];
+    int k = 0;
+    if (lane < F) k = fmt::fmt_field(f, lane, J.n1, J.sign1, J.n2, J.sign2, R.gid, R.point, R.bary, R.params);
+    const uint32_t lenf = lane < F ? k + 1u : 0u;  // + separator
+    uint32_t incl = lenf;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane < F) {
+      f[k] = lane == F - 1 ? '\n' : ' ';
+      char* d = slots + (uint64_t)p * REC_LINE_MAX + (incl - lenf);
+      for (int q = 0; q <= k; ++q) d[q] = f[q];
+    }
+    if (lane == F - 1) line_len[p] = (uint16_t)incl;
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+#if MCX_SMALL_PROF
+  unsigned long long g1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+#endif
+  uint32_t tbytes = 0;
+  const uint32_t len_t = tid < total ? (uint32_t)*(volatile uint16_t*)(line_len + tid) : 0u;
+  const uint32_t off = block_excl_scan(len_t, warp_sums, &tbytes);
+  if (tid < total) line_off[tid] = off;
+  if (tid == 0) line_off[total] = tbytes;
+  __syncthreads();
+  // each 16-byte chunk of the text gathered from the line slots (binary search for the
+  // line of its first byte) and stored to the mapped host buffer in one store
+  const uint32_t nchunk = (tbytes + 1 + 15) / 16;  // + the terminator
+  for (uint32_t q = tid; q < nchunk; q += blockDim.x) {
+    uint32_t lo = 0, hi = total;  // the last line with line_off <= 16q
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (line_off[mid] <= 16 * q) lo = mid;
+      else hi = mid;
+    }
+    union {
+      char c[16];
+      uint4 v;
+    } w;
+    uint32_t line = lo, src[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {  // source offsets first (shared memory only) ...
+      const uint32_t b = 16 * q + i;
+      while (line < total && b >= line_off[line + 1]) ++line;
+      src[i] = b < tbytes ? line * REC_LINE_MAX + (b - line_off[line]) : 0xffffffffu;
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i)  // ... then 16 independent loads (other CTAs wrote the slots: past L1)
+      w.c[i] = src[i] != 0xffffffffu ? __ldcg(slots + src[i]) : '\0';
+    reinterpret_cast<uint4*>(h_text)[q] = w.v;
+  }
+#if MCX_SMALL_PROF
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long g2;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g2));
+    printf("small_text: last CTA %u started +%llu ns after its start, pack %llu ns\n", blockIdx.x, g1 - g0, g2 - g1);
+  }
+#endif
+  if (tid == 0) {
+    res->text_bytes = tbytes;
+    *done = 0;  // for the next call
   }
 }
 
@@ -603,7 +739,8 @@ static int enqueue_small(mcx_context* c, const unsigned long long* n_dev, uint64
   if ((rc = ensure(c, c->jobs, sizeof(JobDev) * jobs.size(), s)) ||
       (rc = ensure(c, c->recs, sizeof(mcx_record) * SMALL_N, s)) ||
       (rc = ensure(c, c->recs_out, sizeof(mcx_record) * SMALL_N, s)) || (rc = ensure(c, c->small, 64, s)) ||
-      (rc = ensure(c, c->text, (size_t)REC_LINE_MAX * SMALL_N, s)))
+      (rc = ensure(c, c->text, (size_t)REC_LINE_MAX * SMALL_N, s)) ||
+      (rc = ensure(c, c->lines, (size_t)(REC_LINE_MAX + 2) * SMALL_N, s)))
     return rc;
   CUDA_TRY(h2d_async(c->jobs.p, jobs.data(), sizeof(JobDev) * jobs.size(), s));
   SmallOut* so;
@@ -626,11 +763,19 @@ static int enqueue_small(mcx_context* c, const unsigned long long* n_dev, uint64
   CUDA_TRY(cudaHostGetDevicePointer((void**)&d_so, so, 0));
   CUDA_TRY(cudaHostGetDevicePointer((void**)&d_hr, hr, 0));
   CUDA_TRY(cudaHostGetDevicePointer((void**)&d_ht, ht, 0));
+  unsigned* total_dev = (unsigned*)c->small.p + 12;  // bytes 48-51 of the 64-byte scratch
   post_small_kernel<<<1, 1024, sizeof(SmallSmem), s>>>(
       (const mcx_hit*)c->hits.p, hit_task, n_dev, n_dev == nd ? n : c->hit_cap, (const JobDev*)c->jobs.p, shift,
-      fo->dedup ? 1 : 0, want_text ? 1 : 0, (mcx_record*)c->recs.p, (mcx_record*)c->recs_out.p, (char*)c->text.p,
-      d_so, d_hr, d_ht);
+      fo->dedup ? 1 : 0, want_text ? 1 : 0, (mcx_record*)c->recs.p, (mcx_record*)c->recs_out.p, total_dev, d_so,
+      d_hr);
   CUDA_TRY(cudaGetLastError());
+  if (want_text) {  // exits at once unless post_small_kernel produced records and wants text
+    char* slots = (char*)c->lines.p;
+    uint16_t* line_len = (uint16_t*)(slots + (size_t)REC_LINE_MAX * SMALL_N);
+    small_text_kernel<<<SMALL_N / 32, 1024, 0, s>>>((const mcx_record*)c->recs_out.p, (const JobDev*)c->jobs.p,
+                                                    total_dev, total_dev + 1, slots, line_len, d_ht, d_so);
+    CUDA_TRY(cudaGetLastError());
+  }
   *queued = true;
   return MCX_OK;
 }
@@ -861,6 +1006,53 @@ static int check_find_opts(const mcx_find_opts* fo) {
   return MCX_OK;
 }
 
+// After a search is enqueued on c->s0 (header copied to c->h_counters): queue the
+// single-kernel post-processing, synchronise once, read the stats.  *retry: a capacity
+// was exceeded (regrown here) — search again; *small_done: the records are ready.
+static int after_search(mcx_context* c, const mcx_job* jobs, uint32_t n_jobs, const mcx_find_opts* fo,
+                        const mcx_opts* o, const std::vector<JobDev>& jd, const mcx_record** records,
+                        uint64_t* n_records, const char** text, uint64_t* text_bytes, mcx_stats* stats, bool* retry,
+                        bool* small_done, uint64_t* total_hits) {
+  *retry = false;
+  *small_done = false;
+  const unsigned long long* hc = (const unsigned long long*)c->h_counters.p;
+  bool queued = false;
+  int rc = enqueue_small(c, (const unsigned long long*)c->ws.p, 0,
+                         n_jobs > 1 ? (const uint32_t*)c->hit_task.p : nullptr, jd, fo, text && text_bytes, &queued);
+  if (rc) return rc;
+  CUDA_TRY(cudaStreamSynchronize(c->s0));
+  trace("search + small post done (synced)");
+  rc = batch_stats(hc, n_jobs, o, c->hit_cap, stats, 0.f);
+  uint64_t total = 0, cands = 0;
+  for (uint32_t t = 0; t < n_jobs; ++t) {
+    total += stats[t].n_hits;
+    cands += stats[t].n_aabb_pass;
+  }
+  *total_hits = total;
+  if (rc == MCX_E_CAPACITY) {
+    if (cands > c->cand_cap) c->cand_cap = cands + 1024;
+    if (total > c->hit_cap) c->hit_cap = total + 1024;
+    *retry = true;
+    return MCX_OK;
+  }
+  if (rc == MCX_E_ARG && hc[2]) {  // non-finite coordinates: name the failing task
+    for (uint32_t t = 0; t < n_jobs; ++t)
+      for (const mcx_mesh* m : {jobs[t].A, jobs[t].B}) {
+        uint32_t flag = 0;
+        if (m->status) CUDA_TRY(cudaMemcpy(&flag, m->status, sizeof(flag), cudaMemcpyDeviceToHost));
+        if (flag) {
+          const mcx_layer& L = jobs[t].layer;
+          return set_error(MCX_E_ARG, "job %u (layer pair %d %c %d %c): non-finite (NaN/Inf) coordinates in its %s "
+                           "half-layer", t, L.n1, L.sign1 >= 0 ? '+' : '-', L.n2, L.sign2 >= 0 ? '+' : '-',
+                           m == jobs[t].A ? "unstable (A)" : "stable (B)");
+        }
+      }
+  }
+  if (rc) return rc;
+  *small_done = queued && take_small(c, records, n_records, text, text_bytes);
+  return MCX_OK;
+}
+
 // Steps 1-7 for jobs whose meshes are resident (device current, all work on c->s0).
 static int intersect(mcx_context* c, const mcx_job* jobs, uint32_t n_jobs, const mcx_find_opts* fo,
                      const mcx_record** records, uint64_t* n_records, const char** text, uint64_t* text_bytes,
@@ -907,40 +1099,10 @@ static int intersect(mcx_context* c, const mcx_job* jobs, uint32_t n_jobs, const
     unsigned long long* hc = (unsigned long long*)c->h_counters.p;
     rc = launch_batch(tasks.data(), n_jobs, &o, (mcx_hit*)c->hits.p, (uint32_t*)c->hit_task.p, c->hit_cap, stats, hc);
     if (rc) return rc;
-    bool queued = false;
-    if ((rc = enqueue_small(c, (const unsigned long long*)c->ws.p, 0, n_jobs > 1 ? (const uint32_t*)c->hit_task.p
-                                                                                  : nullptr,
-                            jd, fo, text && text_bytes, &queued)))
-      return rc;
-    CUDA_TRY(cudaStreamSynchronize(c->s0));
-    trace("search + small post done (synced)");
-    rc = batch_stats(hc, n_jobs, &o, c->hit_cap, stats, 0.f);
-    total = 0;
-    uint64_t cands = 0;
-    for (uint32_t t = 0; t < n_jobs; ++t) {
-      total += stats[t].n_hits;
-      cands += stats[t].n_aabb_pass;
-    }
-    if (rc == MCX_E_CAPACITY) {
-      if (cands > c->cand_cap) c->cand_cap = cands + 1024;
-      if (total > c->hit_cap) c->hit_cap = total + 1024;
-      continue;
-    }
-    if (rc == MCX_E_ARG && hc[2]) {  // non-finite coordinates: name the failing task
-      for (uint32_t t = 0; t < n_jobs; ++t)
-        for (const mcx_mesh* m : {jobs[t].A, jobs[t].B}) {
-          uint32_t flag = 0;
-          if (m->status) CUDA_TRY(cudaMemcpy(&flag, m->status, sizeof(flag), cudaMemcpyDeviceToHost));
-          if (flag) {
-            const mcx_layer& L = jobs[t].layer;
-            return set_error(MCX_E_ARG, "job %u (layer pair %d %c %d %c): non-finite (NaN/Inf) coordinates in its %s "
-                             "half-layer", t, L.n1, L.sign1 >= 0 ? '+' : '-', L.n2, L.sign2 >= 0 ? '+' : '-',
-                             m == jobs[t].A ? "unstable (A)" : "stable (B)");
-          }
-        }
-    }
-    if (rc) return rc;
-    small_done = queued && take_small(c, records, n_records, text, text_bytes);
+    bool retry = false;
+    rc = after_search(c, jobs, n_jobs, fo, &o, jd, records, n_records, text, text_bytes, stats, &retry, &small_done,
+                      &total);
+    if (retry) continue;
     break;
   }
   if (rc) return rc;
@@ -949,8 +1111,16 @@ static int intersect(mcx_context* c, const mcx_job* jobs, uint32_t n_jobs, const
                      text, text_bytes, /*try_small=*/false);
 }
 
+// on_chunk(m, b0, b1): called after the pack of blocks [b0, b1) is enqueued (m->view
+// is complete; the blocks are ready in stream order), e.g. to search them at once.
+using ChunkFn = std::function<int(mcx_mesh*, uint64_t, uint64_t)>;
+
+// cs (optional): the stream of the chunk copies — chunk j is copied on cs, then packed
+// (and searched) on s after event cev[j], so the copies run back to back however long
+// the per-chunk work on s takes.
 static int load_mesh(mcx_context* c, const double* coords, uint32_t N, uint32_t M, const double* s_values,
-                     cudaStream_t s, mcx_mesh** out, bool pack = true) {
+                     cudaStream_t s, mcx_mesh** out, bool pack = true, const ChunkFn& on_chunk = ChunkFn(),
+                     cudaStream_t cs = nullptr) {
   if (!coords || !s_values || !out) return set_error(MCX_E_ARG, "null argument");
   if (N < 1 || M < 2) return set_error(MCX_E_ARG, "a half-layer needs N >= 1 and M >= 2 (SPEC.md:473)");
   const uint64_t n = 2ull * N * (M - 1);
@@ -980,7 +1150,15 @@ static int load_mesh(mcx_context* c, const double* coords, uint32_t N, uint32_t 
     mcx_mesh_free(m);
     return rc;
   }
-  cudaError_t e = cudaMemcpyAsync(m->s_values, s_values, 8ull * M, cudaMemcpyHostToDevice, s);
+  m->view = mcx_mesh_dev{n, m->coords, N, M, m->box, m->perm, m->gbox, m->tbox, m->bbox, m->status, M, 0};
+  cudaError_t e = cudaSuccess;
+  if (cs) {  // the copy stream waits for the (stream-ordered) allocations on s
+    e = cudaEventRecord(c->cev[8], s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, c->cev[8], 0);
+  } else {
+    cs = s;
+  }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(m->s_values, s_values, 8ull * M, cudaMemcpyHostToDevice, cs);
   // Upload and pack pipelined over chunks of whole 16-column tile rows: the blocks of
   // the tile rows a chunk completes are packed while the next chunk is copied, so only
   // the last chunk's packing follows the last byte of the H2D copy.
@@ -995,22 +1173,96 @@ static int load_mesh(mcx_context* c, const double* coords, uint32_t N, uint32_t 
     const uint32_t col1 = last ? M : std::min<uint32_t>(M, ORDER_TILE_Q * tr1 + 1);
     if (col1 > col_done)
       e = cudaMemcpy2DAsync(m->coords + (uint64_t)col_done * N, plane, coords + (uint64_t)col_done * N, plane,
-                            (uint64_t)(col1 - col_done) * N * 8, 4, cudaMemcpyHostToDevice, s);
+                            (uint64_t)(col1 - col_done) * N * 8, 4, cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess && cs != s) {
+      e = cudaEventRecord(c->cev[j], cs);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(s, c->cev[j], 0);
+    }
     const uint64_t b1 = last ? nblk : 2ull * N * std::min<uint32_t>(MQ, ORDER_TILE_Q * tr1) / A_BLOCK;
-    if (e == cudaSuccess && b1 > b_done)  // (b1 = 0 would mean "all blocks" to pack_enqueue)
+    if (e == cudaSuccess && b1 > b_done) {  // (b1 = 0 would mean "all blocks" to pack_enqueue)
       rc = pack_enqueue(m->coords, N, M, MCX_ORDER_TILED, m->box, m->perm, m->gbox, m->tbox, m->bbox, m->status, s,
                         b_done, b1, M);
+      if (rc == MCX_OK && on_chunk) rc = on_chunk(m, b_done, b1);
+    }
     b_done = std::max(b_done, b1);
     col_done = col1;
   }
   if (e != cudaSuccess) rc = set_error(MCX_E_CUDA, "mesh upload: %s", cudaGetErrorString(e));
   if (rc) {
+    if (cs != s) cudaStreamSynchronize(cs);  // no copy may still target the buffers freed below
     mcx_mesh_free(m);
     return rc;
   }
-  m->view = mcx_mesh_dev{n, m->coords, N, M, m->box, m->perm, m->gbox, m->tbox, m->bbox, m->status, M, 0};
   *out = m;
   return MCX_OK;
+}
+
+// mcx_find_intersections, MCX_MODE_CULL on one device: the smaller mesh S is uploaded
+// and packed on s1; the larger mesh L (the sweep side, SURVEY.md:379) is uploaded in
+// chunks on s0 and the blocks of each chunk are searched against S as soon as they are
+// packed (a stepped batch), so the search runs under the rest of the PCIe copy.
+static int find_stepped(mcx_context* c, const double* coords_a, uint32_t NA, uint32_t MA, const double* s_a,
+                        const double* coords_b, uint32_t NB, uint32_t MB, const double* s_b, mcx_layer layer,
+                        const mcx_find_opts* fo, bool swap, mcx_mesh** A, mcx_mesh** B, const mcx_record** records,
+                        uint64_t* n_records, const char** text, uint64_t* text_bytes, mcx_stats* stats) {
+  if (!c->stage.p) {
+    CUDA_TRY(cudaMallocHost((void**)&c->stage.p, 1 << 20));
+    c->stage.cap = 1 << 20;
+  }
+  StageScope scope(&c->stage);
+  mcx_mesh** S = swap ? A : B;
+  mcx_mesh** Lm = swap ? B : A;
+  int rc = swap ? load_mesh(c, coords_a, NA, MA, s_a, c->s1, S) : load_mesh(c, coords_b, NB, MB, s_b, c->s1, S);
+  trace("small mesh enqueued");
+  if (rc) return rc;
+  cudaError_t e = cudaEventRecord(c->ev, c->s1);
+  if (e != cudaSuccess) return set_error(MCX_E_CUDA, "event: %s", cudaGetErrorString(e));
+  mcx_opts o{};
+  o.device = c->device;
+  o.stream = c->s0;
+  o.mode = MCX_MODE_CULL;
+  o.pipeline = fo->pipeline;
+  o.orient = MCX_ORIENT_AS_GIVEN;  // oriented here: L is the sweep side
+  mcx_task whole{};
+  uint64_t steps = 0;
+  auto on_chunk = [&](mcx_mesh* m, uint64_t b0, uint64_t b1) -> int {
+    int r = MCX_OK;
+    if (steps == 0) {
+      cudaError_t w = cudaStreamWaitEvent(c->s0, c->ev, 0);  // S is uploaded and packed
+      if (w != cudaSuccess) return set_error(MCX_E_CUDA, "stream join: %s", cudaGetErrorString(w));
+      whole = mcx_task{&m->view, &(*S)->view, 0, 0};
+      o.cand_cap = c->cand_cap;
+      const uint64_t wsb = mcx_batch_workspace_bytes(&whole, 1, &o);
+      if ((r = ensure(c, c->ws, wsb, c->s0)) || (r = ensure(c, c->hits, sizeof(mcx_hit) * c->hit_cap, c->s0)) ||
+          (r = ensure(c, c->hit_task, 4 * c->hit_cap, c->s0)) || (r = ensure_host(c->h_counters, 8 * 16)))
+        return r;
+      o.workspace = c->ws.p;
+      o.workspace_bytes = c->ws.bytes;
+    }
+    const mcx_task t{&m->view, &(*S)->view, b0 * A_BLOCK, std::min<uint64_t>(b1 * A_BLOCK, m->view.n_tri)};
+    const BatchStep step{&whole, steps == 0, swap};
+    mcx_stats st{};
+    r = launch_batch(&t, 1, &o, (mcx_hit*)c->hits.p, nullptr, c->hit_cap, &st,
+                     (unsigned long long*)c->h_counters.p, &step);
+    ++steps;
+    return r;
+  };
+  rc = swap ? load_mesh(c, coords_b, NB, MB, s_b, c->s0, Lm, true, on_chunk, c->sc)
+            : load_mesh(c, coords_a, NA, MA, s_a, c->s0, Lm, true, on_chunk, c->sc);
+  trace("large mesh enqueued (stepped search)");
+  if (rc) return rc;
+  const mcx_job job{*A, *B, layer};
+  const std::vector<JobDev> jd{job_of(*A, *B, layer)};
+  bool retry = false, small_done = false;
+  uint64_t total = 0;
+  rc = after_search(c, &job, 1, fo, &o, jd, records, n_records, text, text_bytes, stats, &retry, &small_done, &total);
+  if (rc) return rc;
+  const bool spec = fo->pipeline == MCX_PIPE_SPEC;
+  const uint64_t nA = (*A)->view.n_tri, nB = (*B)->view.n_tri;
+  stats->n_pairs = spec ? (nA / 2) * (nB / 2) : nA * nB;
+  if (retry) return intersect(c, &job, 1, fo, records, n_records, text, text_bytes, stats);  // regrown: from scratch
+  if (small_done) return MCX_OK;
+  return postprocess(c, total, nullptr, jd, fo, records, n_records, text, text_bytes, /*try_small=*/false);
 }
 
 }  // namespace mcx
@@ -1036,7 +1288,10 @@ int mcx_context_create(int device, mcx_context** out) {
   }
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->s0, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->s1, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->sc, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev, cudaEventDisableTiming);
+  for (cudaEvent_t& ce : c->cev)
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ce, cudaEventDisableTiming);
   if (e != cudaSuccess) {
     mcx_context_destroy(c);
     return set_error(MCX_E_CUDA, "context creation: %s", cudaGetErrorString(e));
@@ -1052,7 +1307,8 @@ int mcx_context_destroy(mcx_context* c) {
   cudaSetDevice(c->device);
   if (c->s0) {
     for (DevBuf* b : {&c->ws, &c->hits, &c->hit_task, &c->jobs, &c->k0, &c->k1, &c->v0, &c->v1, &c->recs, &c->recs_out,
-                      &c->state, &c->blocked, &c->pairs, &c->lens, &c->offs, &c->cub, &c->text, &c->small, &c->flen})
+                      &c->state, &c->blocked, &c->pairs, &c->lens, &c->offs, &c->cub, &c->text, &c->small, &c->flen,
+                      &c->lines})
       release(c, *b, c->s0);
     cudaStreamSynchronize(c->s0);
   }
@@ -1060,8 +1316,11 @@ int mcx_context_destroy(mcx_context* c) {
     if (b->p) cudaFreeHost(b->p);
   if (c->stage.p) cudaFreeHost(c->stage.p);
   if (c->ev) cudaEventDestroy(c->ev);
+  for (cudaEvent_t ce : c->cev)
+    if (ce) cudaEventDestroy(ce);
   if (c->s0) cudaStreamDestroy(c->s0);
   if (c->s1) cudaStreamDestroy(c->s1);
+  if (c->sc) cudaStreamDestroy(c->sc);
   if (c->pool) cudaMemPoolDestroy(c->pool);
   delete c;
   return MCX_OK;
@@ -1162,6 +1421,18 @@ int mcx_find_intersections(mcx_context* c, const double* coords_a, uint32_t NA, 
   DeviceGuard guard;
   CUDA_TRY(cudaSetDevice(c->device));
   mcx_mesh *A = nullptr, *B = nullptr;
+  const uint64_t nA = (NA && MA >= 2) ? 2ull * NA * (MA - 1) : 0, nB = (NB && MB >= 2) ? 2ull * NB * (MB - 1) : 0;
+  const bool swap = fo->orient == MCX_ORIENT_LARGER_A && nB > nA;
+  const uint64_t nL = swap ? nB : nA, nS = swap ? nA : nB;  // L: the sweep side
+  if (fo->mode == MCX_MODE_CULL && fo->shard_count <= 1 && nL >= STEP_MIN_TRI && nS && nS * STEP_RATIO <= nL &&
+      !getenv("MCX_NO_STEPS")) {
+    rc = find_stepped(c, coords_a, NA, MA, s_a, coords_b, NB, MB, s_b, layer, fo, swap, &A, &B, records, n_records,
+                      text, text_bytes, stats);
+    mcx_mesh_free(A);  // stream-ordered on s0, after everything above
+    mcx_mesh_free(B);
+    trace("end");
+    return rc;
+  }
   // A on stream 0; B's copy on stream 1 overlaps A's packing; stream 0 waits for B.
   rc = load_mesh(c, coords_a, NA, MA, s_a, c->s0, &A);
   trace("A enqueued");

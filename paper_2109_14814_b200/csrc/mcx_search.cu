@@ -353,7 +353,8 @@ __global__ void __launch_bounds__(CULL_THREADS) cull_pairs_kernel(const Batch Bt
   int qn = 0;
   uint32_t cur_task = 0xffffffffu;
   const uint64_t nlist = min((uint64_t)*(volatile unsigned long long*)Bt.list_count, Bt.blk_cap);
-  for (uint64_t e = blockIdx.x; e < nlist; e += gridDim.x) {
+  const uint64_t e0 = Bt.list_done ? min((uint64_t)*Bt.list_done, nlist) : 0;
+  for (uint64_t e = e0 + blockIdx.x; e < nlist; e += gridDim.x) {
     const uint4 txy = Bt.blk_list[e];
     if (txy.x != cur_task) {
       // task switch: drain this warp's queue and counters against the old task first
@@ -604,6 +605,12 @@ static void distinct_meshes(const mcx_task* tasks, uint32_t n, std::vector<const
       if (m && idx.emplace(m->box, out.size()).second) out.push_back(m);
 }
 
+// Stepped batches: header words 5 / 6 ← the block-list / candidate counts (1 and 3).
+__global__ void mark_done_kernel(unsigned long long* h) {
+  h[5] = h[1];
+  h[6] = h[3];
+}
+
 static WsLayout ws_layout(const mcx_task* tasks, uint32_t n, const mcx_opts* o) {
   WsLayout L;
   L.counters = 64;
@@ -673,7 +680,7 @@ int batch_stats(const unsigned long long* h, uint32_t n, const mcx_opts* o, uint
 }
 
 int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mcx_hit* hits, uint32_t* hit_task,
-                 uint64_t cap, mcx_stats* st, unsigned long long* h_counters) {
+                 uint64_t cap, mcx_stats* st, unsigned long long* h_counters, const BatchStep* step) {
   if (!tasks || n == 0 || !o || !st) return set_error(MCX_E_ARG, "null argument or empty batch");
   cudaStream_t stream = (cudaStream_t)o->stream;
   const uint32_t scount = o->shard_count ? o->shard_count : 1;
@@ -691,7 +698,9 @@ int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mcx_hit* 
       if ((tasks[t].a_begin | tasks[t].a_end) & 1)
         return set_error(MCX_E_ARG, "task %u: MCX_PIPE_SPEC needs an A range of whole quads (even bounds)", t);
   if (cap > 0 && !hits) return set_error(MCX_E_ARG, "null hit buffer with nonzero capacity");
-  const WsLayout L = ws_layout(tasks, n, o);
+  if (step && (o->mode != MCX_MODE_CULL || o->orient != MCX_ORIENT_AS_GIVEN || !step->whole))
+    return set_error(MCX_E_ARG, "stepped batches run MCX_MODE_CULL on pre-oriented tasks");
+  const WsLayout L = ws_layout(step ? step->whole : tasks, n, o);
   if (!o->workspace || o->workspace_bytes < L.total || ((uintptr_t)o->workspace & 15))
     return set_error(MCX_E_ARG, "workspace too small or misaligned (need %llu bytes, 16-byte aligned)",
                      (unsigned long long)L.total);
@@ -756,7 +765,7 @@ int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mcx_hit* 
     P.ntilesB = (B->n_tri + TILE - 1) / TILE;
     P.shard_count = scount;
     P.task = t;
-    P.swapped = swap ? 1u : 0u;
+    P.swapped = (swap || (step && step->swap)) ? 1u : 0u;
     P.counters = reinterpret_cast<unsigned long long*>(ws + L.counters + 64ull * t);
     P.gboxA = reinterpret_cast<const Box*>(A->gbox);
     P.bboxA = reinterpret_cast<const Box*>(A->bbox);
@@ -771,7 +780,7 @@ int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mcx_hit* 
     st[t] = mcx_stats{};
     st[t].n_pairs = spec ? (g.na / 2) * (B->n_tri / 2) : g.na * B->n_tri;
   }
-  CUDA_TRY(cudaMemsetAsync(ws, 0, L.counters + 64ull * n, stream));
+  if (!step || step->first) CUDA_TRY(cudaMemsetAsync(ws, 0, L.counters + 64ull * n, stream));
   uint64_t batch_pairs = 0;
   for (uint32_t t = 0; t < n; ++t) batch_pairs += st[t].n_pairs;
   const bool pf_as_brute = o->mode == MCX_MODE_PREFILTER && batch_pairs < prefilter_min_pairs();
@@ -788,6 +797,8 @@ int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mcx_hit* 
   Bt.cand = reinterpret_cast<uint4*>(ws + L.cand);
   Bt.cand_cap = L.cand_cap;
   Bt.cand_count = reinterpret_cast<unsigned long long*>(ws) + 3;
+  Bt.list_done = reinterpret_cast<unsigned long long*>(ws) + 5;
+  Bt.cand_done = reinterpret_cast<unsigned long long*>(ws) + 6;
   Timing tm;
   if (o->timing) {
     CUDA_TRY(cudaEventCreate(&tm.e0));
@@ -810,6 +821,10 @@ int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mcx_hit* 
     CUDA_TRY(h2d_async(ws + L.table, T.data(), sizeof(SearchParams) * n, stream));
     status_kernel<<<1, 32, 0, stream>>>(reinterpret_cast<const SearchParams*>(ws + L.table), n,
                                         reinterpret_cast<unsigned long long*>(ws) + 2);
+    CUDA_TRY(cudaGetLastError());
+  }
+  if (step) {  // the next step starts where this one's lists end
+    mark_done_kernel<<<1, 1, 0, stream>>>(reinterpret_cast<unsigned long long*>(ws));
     CUDA_TRY(cudaGetLastError());
   }
   if (o->timing) CUDA_TRY(cudaEventRecord(tm.e1, stream));
@@ -976,6 +991,8 @@ static int launch_pair_candidates_mesh(const mcx_mesh_dev* A, const mcx_mesh_dev
   Bt.cand = reinterpret_cast<uint4*>(ws + L.cand);
   Bt.cand_cap = L.cand_cap;
   Bt.cand_count = reinterpret_cast<unsigned long long*>(ws) + 3;
+  Bt.list_done = reinterpret_cast<unsigned long long*>(ws) + 5;
+  Bt.cand_done = reinterpret_cast<unsigned long long*>(ws) + 6;
   Timing tm;
   if (o->timing) {
     CUDA_TRY(cudaEventCreate(&tm.e0));

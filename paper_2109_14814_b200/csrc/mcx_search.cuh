@@ -98,6 +98,10 @@ struct Batch {
   uint4* blk_list;               // cull: overlapping (task, local A block, B tile)
   uint64_t blk_cap;
   unsigned long long* list_count;
+  // entries [*list_done, *list_count) / [*cand_done, *cand_count) are this launch's work
+  // (header words 5 / 6: nonzero only in the later steps of a stepped batch)
+  const unsigned long long* list_done;
+  const unsigned long long* cand_done;
   uint32_t neg1;                 // 0xffffffff, a runtime operand so the packed subtract stays an IMAD
   const struct FboxJob* fjobs;   // MCX_MODE_PREFILTER: one fp32-box conversion per distinct mesh
   uint32_t n_fjobs;
@@ -182,6 +186,7 @@ __device__ __forceinline__ void emit_hits(const Batch& Bt, bool hit, uint32_t ia
 template <int KIND>
 __global__ void __launch_bounds__(256) solve_kernel(const Batch Bt) {
   const uint64_t n = min((uint64_t)*(volatile unsigned long long*)Bt.cand_count, Bt.cand_cap);
+  const uint64_t k0 = Bt.cand_done ? min((uint64_t)*Bt.cand_done, n) : 0;
   const int lane = threadIdx.x & 31;
   if (blockIdx.x == 0 && threadIdx.x < 32 && Bt.status_flag) {
     // OR of every task's mcx_pack non-finite flags into the header (no separate launch)
@@ -192,7 +197,7 @@ __global__ void __launch_bounds__(256) solve_kernel(const Batch Bt) {
     }
     if (__any_sync(0xffffffffu, v != 0) && threadIdx.x == 0) atomicOr(Bt.status_flag, 1ull);
   }
-  for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < n; base += (uint64_t)gridDim.x * blockDim.x) {
+  for (uint64_t base = k0 + blockIdx.x * (uint64_t)blockDim.x; base < n; base += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t k = base + threadIdx.x;
     const bool valid = k < n;
     const uint4 c = valid ? Bt.cand[k] : make_uint4(0u, 0u, 0u, 0u);

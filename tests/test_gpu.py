@@ -696,6 +696,32 @@ def test_runtime_records_and_text_equal_host(name, dedup):
     assert st["n_hits"] == len(hits)
 
 
+@pytest.mark.parametrize("name,swap", [("C5", False), ("C5/4", True), ("C5hd", False), ("C5hd", True)])
+def test_runtime_stepped_search_equals_unstepped(name, swap, monkeypatch):
+    """mcx_find_intersections searches a large mesh chunk by chunk during its upload
+    (find_stepped): records, text and stats equal the single-batch search (MCX_NO_STEPS)
+    in both pipelines, with the larger mesh passed as A or as B (oriented: the solve
+    un-swaps).  Fresh contexts also take the regrow path on C5hd (2.4M box survivors >
+    the default 1M candidate capacity: the stepped attempt overflows and reruns)."""
+    from paper_2109_14814_b200 import runtime
+    A, sa, B, sb = config_pair(name)
+    if swap:
+        A, sa, B, sb = B, sb, A, sa
+    keys = ("n_hits", "n_aabb_pass", "n_tested", "n_pairs", "n_candidates", "n_singular")
+    for pipe in (_lib.PIPE_SPEC, _lib.PIPE_TRIANGLE):
+        ctx = runtime.Context(0)
+        got = ctx.find(A, sa, B, sb, (1, "+", 2, "-"), pipeline=pipe, text=True)
+        again = ctx.find(A, sa, B, sb, (1, "+", 2, "-"), pipeline=pipe, text=True)  # capacities now sufficient
+        monkeypatch.setenv("MCX_NO_STEPS", "1")
+        want = runtime.Context(0).find(A, sa, B, sb, (1, "+", 2, "-"), pipeline=pipe, text=True)
+        monkeypatch.delenv("MCX_NO_STEPS")
+        for g in (got, again):
+            assert g[1] == want[1] and len(want[1]) > 0
+            assert np.array_equal(g[0], want[0])
+            assert {k: g[2][k] for k in keys} == {k: want[2][k] for k in keys}
+        ctx.close()
+
+
 def test_runtime_batch_and_finish_hits():
     """mcx_intersect over several resident jobs equals one find per job; mcx_finish_hits
     (host hit list, e.g. gathered from several GPUs) equals find."""

@@ -74,11 +74,50 @@ def test_device_formatter_matches_python_g17():
         vals += [x, np.nextafter(x, 0.0), np.nextafter(x, np.inf)]
     vals += list(rng.integers(0, 2 ** 64, size=20000, dtype=np.uint64).view(np.float64))
     vals += list(rng.normal(size=20000)) + list(rng.uniform(0, 1, 20000))
+    # dyadic rationals (terminating decimal expansions: exact ties at the 17th digit occur)
+    vals += list(rng.integers(1, 2 ** 53, 20000) / 2.0 ** rng.integers(0, 80, 20000))
+    vals += [float(v) for v in rng.integers(0, 2 ** 63, 2000, dtype=np.int64)]  # integers (gid-sized)
     buf = ctypes.create_string_buffer(64)
     for v in vals:
         n = L.mcx_format_g17(float(v), buf)
         assert buf.value.decode() == f"{float(v):.17g}", repr(v)
         assert n == len(buf.value)
+
+
+def test_formatter_integers_match_printf(tmp_path):
+    """put_u64 (the gid field and exponents of the device records text) against printf
+    %llu over edge and random 64-bit values: the header compiled as plain C++ (g++)."""
+    import shutil
+    import subprocess
+    if not shutil.which("g++"):
+        pytest.skip("g++ not available")
+    src = tmp_path / "fmt.cpp"
+    src.write_text(
+        '#include <cstdio>\n#include <cstdint>\n#include "mcx_format.cuh"\n'
+        "int main() {\n"
+        "  uint64_t x = 88172645463325252ull;\n"
+        "  uint64_t edge[] = {0, 1, 9, 10, 999999999ull, 1000000000ull, 1000000001ull, 4294967295ull,\n"
+        "                     4294967296ull, 999999999999999999ull, 1000000000000000000ull,\n"
+        "                     10000000000000000000ull, 18446744073709551615ull};\n"
+        "  char buf[32], ref[32];\n"
+        "  for (int i = 0; i < 200000 + 13; ++i) {\n"
+        "    uint64_t v;\n"
+        "    if (i < 13) v = edge[i];\n"
+        "    else { x ^= x << 13; x ^= x >> 7; x ^= x << 17; v = x >> (x % 64); }\n"
+        "    int n = mcx::fmt::put_u64(buf, v);\n"
+        "    buf[n] = 0;\n"
+        "    snprintf(ref, sizeof ref, \"%llu\", (unsigned long long)v);\n"
+        "    for (int k = 0; ; ++k) { if (buf[k] != ref[k]) { printf(\"bad %s %s\\n\", buf, ref); return 1; }\n"
+        "                            if (!ref[k]) break; }\n"
+        "  }\n"
+        "  printf(\"ok\\n\");\n"
+        "  return 0;\n"
+        "}\n")
+    exe = tmp_path / "fmt"
+    subprocess.run(["g++", "-O1", "-I", os.path.join(ROOT, "paper_2109_14814_b200", "csrc"), "-o", str(exe), str(src)],
+                   check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert out.returncode == 0 and out.stdout.strip() == "ok", out.stdout
 
 
 def test_only_cuda_backend():
