@@ -339,7 +339,10 @@ __global__ void field_write_kernel(const mcx_record* __restrict__ recs, const ui
 // first step: two similar meshes share the link until the end, and the per-step fixed
 // costs then follow the copy instead of hiding under it — measured on C3)
 constexpr uint64_t STEP_MIN_TRI = 1ull << 18;
-constexpr uint64_t STEP_RATIO = 4;
+static uint64_t step_ratio() {  // MCX_STEP_RATIO overrides (experiments)
+  const char* v = getenv("MCX_STEP_RATIO");
+  return v ? strtoull(v, nullptr, 10) : 4;
+}
 
 // ------------------------------------------------------------------ small hit counts
 // Steps 2-6 in ONE single-CTA kernel for n ≤ SMALL_N hits (the common case: a handful
@@ -1212,7 +1215,10 @@ static int find_stepped(mcx_context* c, const double* coords_a, uint32_t NA, uin
   StageScope scope(&c->stage);
   mcx_mesh** S = swap ? A : B;
   mcx_mesh** Lm = swap ? B : A;
-  int rc = swap ? load_mesh(c, coords_a, NA, MA, s_a, c->s1, S) : load_mesh(c, coords_b, NB, MB, s_b, c->s1, S);
+  // every H2D copy on the one copy stream c->sc: S's chunks first at the full link rate,
+  // then L's (packs of S on s1, packs and searches of L on s0, gated by chunk events)
+  int rc = swap ? load_mesh(c, coords_a, NA, MA, s_a, c->s1, S, true, ChunkFn(), c->sc)
+                : load_mesh(c, coords_b, NB, MB, s_b, c->s1, S, true, ChunkFn(), c->sc);
   trace("small mesh enqueued");
   if (rc) return rc;
   cudaError_t e = cudaEventRecord(c->ev, c->s1);
@@ -1424,7 +1430,7 @@ int mcx_find_intersections(mcx_context* c, const double* coords_a, uint32_t NA, 
   const uint64_t nA = (NA && MA >= 2) ? 2ull * NA * (MA - 1) : 0, nB = (NB && MB >= 2) ? 2ull * NB * (MB - 1) : 0;
   const bool swap = fo->orient == MCX_ORIENT_LARGER_A && nB > nA;
   const uint64_t nL = swap ? nB : nA, nS = swap ? nA : nB;  // L: the sweep side
-  if (fo->mode == MCX_MODE_CULL && fo->shard_count <= 1 && nL >= STEP_MIN_TRI && nS && nS * STEP_RATIO <= nL &&
+  if (fo->mode == MCX_MODE_CULL && fo->shard_count <= 1 && nL >= STEP_MIN_TRI && nS && nS * step_ratio() <= nL &&
       !getenv("MCX_NO_STEPS")) {
     rc = find_stepped(c, coords_a, NA, MA, s_a, coords_b, NB, MB, s_b, layer, fo, swap, &A, &B, records, n_records,
                       text, text_bytes, stats);
