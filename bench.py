@@ -42,6 +42,17 @@ UNIT = "pair-tests/s"
 FP64_LANES_PER_CLK_PER_SM = 64  # B200 FP64 pipe; verified by tools/microbench/pipes.cu (dadd 63.5)
 
 
+def hbm_peak():
+    """Measured HBM copy bandwidth (MEASURED_PEAKS.json, driver-written), else the profiling
+    guide's fallback."""
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy bandwidth, read + write bytes)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md; MEASURED_PEAKS.json absent)"
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -374,9 +385,10 @@ def run_ours(args):
         barrier()
         return {"value": pairs_total / (t_ms * 1e-3), "unit": UNIT, "ms_per_step": t_ms / steps,
                 "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h // steps, "records": len(recs),
-                "path": "runtime.Context.find -> mcx_find_intersections(host grids): H2D (4 column chunks per grid, "
-                        "B's on a second stream) pipelined with the fused pack, search, solve, records + sort + "
-                        "dedup + %.17g text on the device, D2H of records + text",
+                "path": "runtime.Context.find -> mcx_find_intersections(host grids): H2D in column chunks (8 per "
+                        "grid from 2^20 triangles) on two streams, each chunk packed as it lands (when one mesh is "
+                        ">= 4x the other, the larger one's chunks are also searched as they land), solve, "
+                        "records + sort + dedup + %.17g text on the device, D2H of records + text",
                 "mode": mode_name, "pipeline": pipeline}
 
     primary = args.mode
@@ -456,6 +468,43 @@ def run_ours(args):
                                         (cst["kernel_ms"] * 1e-3) / 1e12 / peak,
                   "note": "identical hit set / AABB-pass / singular counts; exact union-box culling over the "
                           "tiled storage order skips only provably disjoint pairs"}
+
+    # ---- roofline of the fused pack kernel (mcx_pack of A: boxes + perm + level boxes)
+    def measure_pack(reps=10):
+        L = _lib.load()
+        outs = [torch.empty_like(t) for t in (Am.box, Am.perm, Am.gbox, Am.tbox, Am.bbox, Am.status)]
+        ts = []
+        for it in range(reps + 2):
+            flush.zero_()  # the pack reads its grid from HBM, not from the L2 copy a previous launch left
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            rc = L.mcx_pack(Am.coords.data_ptr(), Am.N, Am.M, _lib.ORDER_TILED, *(o.data_ptr() for o in outs), local,
+                            stream.cuda_stream)
+            e1.record(stream)
+            _lib.check(rc, "mcx_pack")
+            torch.cuda.synchronize(dev)
+            if it >= 2:
+                ts.append(e0.elapsed_time(e1))
+        ms = statistics.median(ts)
+        n = Am.n_tri
+        alg = Am.coords.numel() * 8 + n * (64 + 4) + (Am.gbox.numel() + Am.tbox.numel() + Am.bbox.numel()) * 8
+        peak, src = hbm_peak()
+        return {"bound": "hbm", "kernel": "pack_kernel (mcx_pack of A: exact triangle boxes in the tiled order, "
+                                           "perm, group/tile/block union boxes; persistent CTAs, cp.async grid window)",
+                "achieved": alg / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                "frac": alg / (ms * 1e-3) / 1e9 / peak, "peak_source": src,
+                "work_per_launch": f"{alg} algorithmic bytes: grid 32 B/vertex read once, 64 B box + 4 B perm per "
+                                   "record, 64 B per 32/512/1024-record union box written",
+                "kernel_ms": ms, "timing": "CUDA events on the launching stream around one mcx_pack, L2 flushed "
+                                           "(256 MB write) before each, median of 10",
+                "traffic": (16805120.0 + 17992704.0) if args.config == "C3" else None,
+                "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum of one C3 launch, ncu --set full "
+                                "(profiles/r02_ncu_pack_c3.txt): the 71 MB of boxes stay in the 126 MB L2 during the "
+                                "launch and are written back later",
+                "note": "in find_intersections every chunk's pack overlaps the next chunk's PCIe copy, so only the "
+                        "last chunk's pack is on the e2e critical path"}
+
+    pack_roofline = measure_pack()
 
     e2e = None
     if not args.no_e2e:
@@ -641,6 +690,7 @@ def run_ours(args):
                 "config": bench_config(desc, primary, world),
                 "search_wall_s": m1["ms_per_step"] / 1e3, "hits": m1["hits"], "kernel_ms": m1["kernel_ms"],
                 "roofline": roofline, "fp64_brute": fp64_block, "prefilter": pre_block, "cull": cull_block,
+                "pack": pack_roofline,
                 "e2e": e2e, "cpu_baseline": cpu, "paper_workload": paper, "c5_unbalanced": c5, "shards8": shards8, "clocks": m1["clocks"],
                 "gpu_launches": m1["launches"], "gpu": props.name, "sms": sms}
         print(json.dumps(line), flush=True)

@@ -1,7 +1,8 @@
 """Kernel time of every search mode on every BASELINE config (+ the C5hd and dense
 self-search stress shapes): one JSON line per (config, mode), median of 5 timed calls
-with inputs resident (MCX_MODE_PREFILTER forced onto the quantised kernel for every size
-so the table compares the kernels; by default calls under 2^28 pairs use the FP64 sweep).
+with inputs resident.  "prefilter" forces the quantised kernel at every size (kernel
+comparison); "prefilter_default" is what MCX_MODE_PREFILTER does for a user (calls under
+2^28 pairs run the FP64 sweep, same results).
 `python tools/mode_table.py > profiles/r02_modes.jsonl`"""
 import json
 import os
@@ -29,8 +30,11 @@ def shapes():
 for name, A, B in shapes():
     Am, Bm = D.DeviceMesh(A, 0), D.DeviceMesh(B, 0)
     hits = None
-    for mode in (("prefilter", "cull") if name == "4Mx4M" else ("brute", "prefilter", "cull")):
-        m = _lib.MODE_NAMES[mode]
+    for mode in (("prefilter", "cull") if name == "4Mx4M" else ("brute", "prefilter", "prefilter_default", "cull")):
+        # prefilter: the quantised kernel forced at every size; prefilter_default: the
+        # product rule (calls under 2^28 pairs run the FP64 sweep — identical results)
+        os.environ["MCX_PREFILTER_MIN_PAIRS"] = "0" if mode == "prefilter" else str(1 << 28)
+        m = _lib.MODE_NAMES["prefilter" if mode == "prefilter_default" else mode]
         D.search_device(Am, Bm, mode=m)
         runs = [D.search_device(Am, Bm, mode=m, timing=True) for _ in range(5)]
         st = runs[0].stats

@@ -8,7 +8,8 @@ mkdir -p "$out"
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > "$out/r02_smoke.txt" 2>&1
 python bench.py > "$out/r02_bench_c3.json" 2> "$out/r02_bench_c3.err"
 python bench.py --impl reference --steps 5 --warmup 2 > "$out/r02_reference_c3.json" 2> /dev/null
-python tools/e2e_runtime.py C3 C2 C5hd > "$out/r02_e2e_runtime.jsonl" 2>&1
+python tools/e2e_runtime.py C3 C2 C5 C5hd > "$out/r02_e2e_runtime.jsonl" 2>&1
+python tools/microbench/pack_bench.py C2 C3 C5 > "$out/r02_pack.jsonl" 2>&1
 python tools/mode_table.py > "$out/r02_modes.jsonl" 2>&1
 # launch lists: a short bench run, and one find_intersections call (C3, cull, spec pipeline)
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file "$out/launches.csv" \
@@ -20,7 +21,11 @@ python tools/ncu_summary.py list "$out/find.csv" > "$out/r02_launches_find_c3.tx
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file "$out/find5.csv" \
     python tools/debug/trace_find.py C5hd > /dev/null 2>&1
 python tools/ncu_summary.py list "$out/find5.csv" > "$out/r02_launches_find_c5hd.txt"
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file "$out/find5s.csv" \
+    python tools/debug/trace_find.py C5 > /dev/null 2>&1
+python tools/ncu_summary.py list "$out/find5s.csv" > "$out/r02_launches_find_c5.txt"
 MCX_TRACE=1 python tools/debug/trace_find.py C3 > "$out/r02_trace_find_c3.txt" 2>&1
+MCX_TRACE=1 python tools/debug/trace_find.py C5 > "$out/r02_trace_find_c5.txt" 2>&1
 MCX_TRACE=1 python tools/debug/trace_find.py C5hd > "$out/r02_trace_find_c5hd.txt" 2>&1
 ncu_rep() {  # name, kernel regex, launch count, config, mode
   ncu --set full --import-source on --clock-control none -k regex:"$2" -c "$3" \
