@@ -32,8 +32,11 @@ struct BatchStep {
   bool first;
   bool swap;
 };
+// header_later: with h_counters, skip the header copy — the caller enqueues it (e.g.
+// after kernels that only need the header on the device).
 int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mcx_hit* hits, uint32_t* hit_task,
-                 uint64_t cap, mcx_stats* st, unsigned long long* h_counters, const BatchStep* step = nullptr);
+                 uint64_t cap, mcx_stats* st, unsigned long long* h_counters, const BatchStep* step = nullptr,
+                 bool header_later = false);
 int batch_stats(const unsigned long long* h, uint32_t n, const mcx_opts* o, uint64_t cap, mcx_stats* st, float ms);
 
 // mcx_search.cu: one-time per (kernel, device, threads, smem) launch setup — the
@@ -41,5 +44,9 @@ int batch_stats(const unsigned long long* h, uint32_t n, const mcx_opts* o, uint
 // the resident CTAs per SM × SM count — cached, since each of these host calls costs
 // microseconds on every small search otherwise.  `device` is the current device.
 int kernel_prepare(const void* fn, int threads, size_t smem, int carveout, int device, uint64_t* slots);
+
+// mcx_runtime.cu: MCX_TRACE=2 device-side stamp (a CUDA event recorded on s, printed
+// when the runtime call ends); no-op otherwise.
+void dstamp(cudaStream_t s, const char* what);
 
 }  // namespace mcx

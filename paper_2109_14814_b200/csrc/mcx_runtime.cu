@@ -144,6 +144,38 @@ static void trace(const char* what) {
   fprintf(stderr, "[mcx] %8.1f us  %s\n", std::chrono::duration<double, std::micro>(now - t0).count(), what);
 }
 
+// MCX_TRACE=2 adds device-side stamps: CUDA events recorded on the streams at the stages
+// of a call, printed (µs after the first stamp) when the call ends.
+struct DevStamps {
+  cudaEvent_t ev[24] = {};
+  const char* name[24] = {};
+  int n = 0;
+};
+static thread_local DevStamps g_stamps;
+static bool dtrace_on() {
+  static const bool on = getenv("MCX_TRACE") && atoi(getenv("MCX_TRACE")) > 1;
+  return on;
+}
+void dstamp(cudaStream_t s, const char* what) {
+  if (!dtrace_on()) return;
+  if (!strcmp(what, "begin")) g_stamps.n = 0;
+  if (g_stamps.n >= 24) return;
+  cudaEvent_t& e = g_stamps.ev[g_stamps.n];
+  if (!e) cudaEventCreate(&e);
+  cudaEventRecord(e, s);
+  g_stamps.name[g_stamps.n++] = what;
+}
+static void dstamp_print() {
+  if (!dtrace_on() || g_stamps.n == 0) return;
+  for (int i = 0; i < g_stamps.n; ++i) {
+    float ms = 0.f;
+    cudaEventSynchronize(g_stamps.ev[i]);
+    cudaEventElapsedTime(&ms, g_stamps.ev[0], g_stamps.ev[i]);
+    fprintf(stderr, "[mcx-dev] %8.1f us  %s\n", 1e3 * ms, g_stamps.name[i]);
+  }
+  g_stamps.n = 0;
+}
+
 static int bits_for(uint64_t v) {  // bits to represent every value in [0, v]
   int b = 0;
   while (b < 64 && (v >> b)) ++b;
@@ -355,7 +387,8 @@ static uint64_t step_ratio() {  // MCX_STEP_RATIO overrides (experiments)
 constexpr int SMALL_N = 1024;
 constexpr int SMALL_K = 8;
 constexpr int REC_LINE_MAX = 352;  // ≥ the longest records line (349 bytes)
-constexpr unsigned SMALL_NONE = 0xffffffffu;  // "no small-path text" (small_lines / small_pack)
+constexpr unsigned SMALL_NONE = 0xffffffffu;  // "no small-path text" (small_text_kernel)
+constexpr int SMALL_TEXT_INLINE = 60;         // kept lines whose text post_small_kernel writes itself (≤ 1 field per thread)
 
 struct SmallOut {
   unsigned long long kept, text_bytes, overflow;
@@ -399,6 +432,11 @@ struct SmallSmem {
   int overflow;
 };
 
+__device__ void format_line(uint32_t p, const mcx_record* __restrict__ recs, const JobDev* __restrict__ jobs,
+                            char* __restrict__ slots, uint16_t* __restrict__ line_len, int lane);
+__device__ uint32_t pack_text(uint32_t total, const char* __restrict__ slots, const uint16_t* __restrict__ line_len,
+                              uint32_t* line_off, uint32_t* warp_sums, char* __restrict__ h_text);
+
 // n = min(*n_dev, n_cap) is read on the device (the search's hit counter), so the
 // kernel can follow the search without a host round trip; more than SMALL_N hits sets
 // res->overflow = 2 and the host runs the general path.  Results (SmallOut, records,
@@ -409,8 +447,9 @@ __global__ void __launch_bounds__(1024) post_small_kernel(const mcx_hit* __restr
                                                           uint64_t n_cap, const JobDev* __restrict__ jobs,
                                                           int gid_shift, int dedup, int want_text,
                                                           mcx_record* __restrict__ recs, mcx_record* __restrict__ out,
-                                                          unsigned* __restrict__ total_dev, SmallOut* __restrict__ res,
-                                                          mcx_record* __restrict__ h_out) {
+                                                          unsigned* __restrict__ total_dev, char* __restrict__ slots,
+                                                          uint16_t* __restrict__ line_len, SmallOut* __restrict__ res,
+                                                          mcx_record* __restrict__ h_out, char* __restrict__ h_text) {
   extern __shared__ __align__(16) unsigned char small_raw[];
   SmallSmem& S = *reinterpret_cast<SmallSmem*>(small_raw);
   unsigned long long* key = S.key;
@@ -587,7 +626,46 @@ __global__ void __launch_bounds__(1024) post_small_kernel(const mcx_hit* __restr
   }
   __syncthreads();
   SMALL_PHASE(5);
-  // the text lines are formatted by small_lines_kernel / small_pack_kernel (many SMs)
+  // text: up to SMALL_TEXT_INLINE kept lines here (one warp per line), more by
+  // small_text_kernel over many SMs
+  const bool text_here = want_text && total <= (uint32_t)SMALL_TEXT_INLINE;
+  uint32_t tbytes = 0;
+  if (text_here) {
+    // one thread per (line, field) — all of a few lines' conversions side by side — each
+    // field kept in its thread across the scans: lengths, line offsets, then the bytes
+    // into the contiguous text (slots buffer) and 16-byte copies to the mapped host buffer
+    constexpr int F = fmt::LINE_FIELDS;
+    uint16_t* flen = S.idx;                                    // dead after the records
+    uint32_t* line_off = reinterpret_cast<uint32_t*>(S.key);  // dead after the sort
+    const uint32_t nf = total * F, p = tid / F, fi = tid % F;
+    char f[32];
+    int k = 0;
+    if (tid < nf) {
+      const mcx_record& R = out[p];
+      const JobDev& J = jobs[R.task];
+      k = fmt::fmt_field(f, (int)fi, J.n1, J.sign1, J.n2, J.sign2, R.gid, R.point, R.bary, R.params);
+      f[k++] = fi == F - 1 ? '\n' : ' ';
+    }
+    flen[tid] = (uint16_t)k;
+    __syncthreads();
+    uint32_t len = 0;
+    if (tid < total)
+      for (int g = 0; g < F; ++g) len += flen[tid * F + g];
+    const uint32_t off = block_excl_scan(len, warp_sums, &tbytes);
+    if (tid < total) line_off[tid] = off;
+    __syncthreads();
+    if (tid < nf) {
+      uint32_t o = line_off[p];
+      for (uint32_t g = 0; g < fi; ++g) o += flen[p * F + g];
+      for (int q = 0; q < k; ++q) slots[o + q] = f[q];
+    }
+    __syncthreads();
+    const uint32_t t16 = tbytes / 16;
+    const uint4* ts = reinterpret_cast<const uint4*>(slots);
+    uint4* td = reinterpret_cast<uint4*>(h_text);
+    for (uint32_t q = tid; q < t16; q += blockDim.x) td[q] = ts[q];
+    for (uint32_t q = 16 * t16 + tid; q <= tbytes; q += blockDim.x) h_text[q] = q < tbytes ? slots[q] : '\0';
+  }
   SMALL_PHASE(6);
   // coalesced copy-out to the mapped host buffers
   {
@@ -598,80 +676,56 @@ __global__ void __launch_bounds__(1024) post_small_kernel(const mcx_hit* __restr
   SMALL_PHASE(7);
   if (tid == 0) {
 #if MCX_SMALL_PROF
-    const char* nm[8] = {"keys", "sort", "records", "dedup", "resolve", "compact", "-", "copyout"};
+    const char* nm[8] = {"keys", "sort", "records", "dedup", "resolve", "compact", "text", "copyout"};
     for (int q = 0; q < 8; ++q)
       printf("small %-10s %7lld cycles\n", nm[q], tprof[q] - (q ? tprof[q - 1] : tprof[10]));
 #endif
     res->kept = total;
-    res->text_bytes = 0;  // small_pack_kernel
+    res->text_bytes = tbytes;  // (small_text_kernel's otherwise)
     res->overflow = 0;
-    *total_dev = want_text ? total : SMALL_NONE;
+    *total_dev = want_text && !text_here ? total : SMALL_NONE;
   }
 }
 
-// The records text of the small path (after post_small_kernel, same stream), 32 CTAs of
-// 32 warps, one warp per kept line: lane f formats field f (a line's 17 exact conversions
-// side by side) and a warp scan places them in the line's fixed-stride slot.  The last
-// CTA to finish (a device-scope counter) then scans the line lengths and writes the
-// contiguous text to the mapped host buffer in 16-byte stores, each gathered from the
-// line slots.  *total_dev = the kept count
-// (SMALL_NONE: no text — overflow, general path or text not wanted).
-__global__ void __launch_bounds__(1024) small_text_kernel(const mcx_record* __restrict__ recs,
-                                                          const JobDev* __restrict__ jobs,
-                                                          const unsigned* __restrict__ total_dev,
-                                                          unsigned* __restrict__ done, char* __restrict__ slots,
-                                                          uint16_t* __restrict__ line_len, char* __restrict__ h_text,
-                                                          SmallOut* __restrict__ res) {
+// Records text of the small path.  format_line: one warp formats kept line p into its
+// fixed-stride slot — lane f formats field f (a line's 17 exact conversions side by side),
+// a warp scan places them — and records the line length.
+__device__ void format_line(uint32_t p, const mcx_record* __restrict__ recs, const JobDev* __restrict__ jobs,
+                            char* __restrict__ slots, uint16_t* __restrict__ line_len, int lane) {
   constexpr int F = fmt::LINE_FIELDS;
-  __shared__ uint32_t warp_sums[32];
-  __shared__ uint32_t line_off[SMALL_N + 1];
-  __shared__ bool last;
-#if MCX_SMALL_PROF
-  unsigned long long g0;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
-#endif
-  const uint32_t total = *total_dev;
-  if (total > (uint32_t)SMALL_N) return;  // uniform over the grid
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t p = warp * gridDim.x + blockIdx.x;  // lines dealt over the CTAs (SMs) first
-  if (p < total) {
-    const mcx_record& R = recs[p];
-    const JobDev& J = jobs[R.task];
-    char f[32];
-    int k = 0;
-    if (lane < F) k = fmt::fmt_field(f, lane, J.n1, J.sign1, J.n2, J.sign2, R.gid, R.point, R.bary, R.params);
-    const uint32_t lenf = lane < F ? k + 1u : 0u;  // + separator
-    uint32_t incl = lenf;
+  const mcx_record& R = recs[p];
+  const JobDev& J = jobs[R.task];
+  char f[32];
+  int k = 0;
+  if (lane < F) k = fmt::fmt_field(f, lane, J.n1, J.sign1, J.n2, J.sign2, R.gid, R.point, R.bary, R.params);
+  const uint32_t lenf = lane < F ? k + 1u : 0u;  // + separator
+  uint32_t incl = lenf;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (lane < F) {
-      f[k] = lane == F - 1 ? '\n' : ' ';
-      char* d = slots + (uint64_t)p * REC_LINE_MAX + (incl - lenf);
-      for (int q = 0; q <= k; ++q) d[q] = f[q];
-    }
-    if (lane == F - 1) line_len[p] = (uint16_t)incl;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
   }
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-#if MCX_SMALL_PROF
-  unsigned long long g1;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
-#endif
+  if (lane < F) {
+    f[k] = lane == F - 1 ? '\n' : ' ';
+    char* d = slots + (uint64_t)p * REC_LINE_MAX + (incl - lenf);
+    for (int q = 0; q <= k; ++q) d[q] = f[q];
+  }
+  if (lane == F - 1) line_len[p] = (uint16_t)incl;
+}
+
+// pack_text (one CTA of 1024 threads): line offsets by a block scan, then the text written
+// to the mapped host buffer in 16-byte stores, each gathered from the line slots (binary
+// search for the line of its first byte; the 16 source offsets first, then 16 independent
+// loads past L1 — other CTAs may have written the slots).  Returns the text length.
+__device__ uint32_t pack_text(uint32_t total, const char* __restrict__ slots, const uint16_t* __restrict__ line_len,
+                              uint32_t* line_off, uint32_t* warp_sums, char* __restrict__ h_text) {
+  const int tid = threadIdx.x;
   uint32_t tbytes = 0;
-  const uint32_t len_t = tid < total ? (uint32_t)*(volatile uint16_t*)(line_len + tid) : 0u;
+  const uint32_t len_t = tid < total ? (uint32_t)*(const volatile uint16_t*)(line_len + tid) : 0u;
   const uint32_t off = block_excl_scan(len_t, warp_sums, &tbytes);
   if (tid < total) line_off[tid] = off;
   if (tid == 0) line_off[total] = tbytes;
   __syncthreads();
-  // each 16-byte chunk of the text gathered from the line slots (binary search for the
-  // line of its first byte) and stored to the mapped host buffer in one store
   const uint32_t nchunk = (tbytes + 1 + 15) / 16;  // + the terminator
   for (uint32_t q = tid; q < nchunk; q += blockDim.x) {
     uint32_t lo = 0, hi = total;  // the last line with line_off <= 16q
@@ -686,24 +740,44 @@ __global__ void __launch_bounds__(1024) small_text_kernel(const mcx_record* __re
     } w;
     uint32_t line = lo, src[16];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {  // source offsets first (shared memory only) ...
+    for (int i = 0; i < 16; ++i) {
       const uint32_t b = 16 * q + i;
       while (line < total && b >= line_off[line + 1]) ++line;
       src[i] = b < tbytes ? line * REC_LINE_MAX + (b - line_off[line]) : 0xffffffffu;
     }
 #pragma unroll
-    for (int i = 0; i < 16; ++i)  // ... then 16 independent loads (other CTAs wrote the slots: past L1)
-      w.c[i] = src[i] != 0xffffffffu ? __ldcg(slots + src[i]) : '\0';
+    for (int i = 0; i < 16; ++i) w.c[i] = src[i] != 0xffffffffu ? __ldcg(slots + src[i]) : '\0';
     reinterpret_cast<uint4*>(h_text)[q] = w.v;
   }
-#if MCX_SMALL_PROF
+  return tbytes;
+}
+
+// The text of more than SMALL_TEXT_INLINE kept records (after post_small_kernel, same
+// stream): 32 CTAs of 32 warps, lines dealt over the CTAs (SMs) first, one warp per line;
+// the last CTA to finish (a device-scope counter) packs the text.  *total_dev = the kept
+// count, SMALL_NONE when there is nothing to do here (overflow, general path, no text
+// wanted, or post_small_kernel wrote the text itself).
+__global__ void __launch_bounds__(1024) small_text_kernel(const mcx_record* __restrict__ recs,
+                                                          const JobDev* __restrict__ jobs,
+                                                          const unsigned* __restrict__ total_dev,
+                                                          unsigned* __restrict__ done, char* __restrict__ slots,
+                                                          uint16_t* __restrict__ line_len, char* __restrict__ h_text,
+                                                          SmallOut* __restrict__ res) {
+  __shared__ uint32_t warp_sums[32];
+  __shared__ uint32_t line_off[SMALL_N + 1];
+  __shared__ bool last;
+  const uint32_t total = *total_dev;
+  if (total > (uint32_t)SMALL_N) return;  // uniform over the grid
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t p = warp * gridDim.x + blockIdx.x;
+  if (p < total) format_line(p, recs, jobs, slots, line_len, lane);
+  __threadfence();
   __syncthreads();
-  if (tid == 0) {
-    unsigned long long g2;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g2));
-    printf("small_text: last CTA %u started +%llu ns after its start, pack %llu ns\n", blockIdx.x, g1 - g0, g2 - g1);
-  }
-#endif
+  if (tid == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const uint32_t tbytes = pack_text(total, slots, line_len, line_off, warp_sums, h_text);
   if (tid == 0) {
     res->text_bytes = tbytes;
     *done = 0;  // for the next call
@@ -746,6 +820,7 @@ static int enqueue_small(mcx_context* c, const unsigned long long* n_dev, uint64
       (rc = ensure(c, c->lines, (size_t)(REC_LINE_MAX + 2) * SMALL_N, s)))
     return rc;
   CUDA_TRY(h2d_async(c->jobs.p, jobs.data(), sizeof(JobDev) * jobs.size(), s));
+  dstamp(s, "  small: job table uploaded");
   SmallOut* so;
   mcx_record* hr;
   char* ht;
@@ -756,9 +831,9 @@ static int enqueue_small(mcx_context* c, const unsigned long long* n_dev, uint64
     CUDA_TRY(cudaMemcpyAsync(nd, &n, 8, cudaMemcpyHostToDevice, s));  // 8 bytes, staged by the driver
     n_dev = nd;
   }
-  uint64_t slots;
+  uint64_t resident;
   if ((rc = kernel_prepare(reinterpret_cast<const void*>(post_small_kernel), 1024, sizeof(SmallSmem), -1,
-                           c->device, &slots)))
+                           c->device, &resident)))
     return rc;
   SmallOut* d_so;
   mcx_record* d_hr;
@@ -766,15 +841,16 @@ static int enqueue_small(mcx_context* c, const unsigned long long* n_dev, uint64
   CUDA_TRY(cudaHostGetDevicePointer((void**)&d_so, so, 0));
   CUDA_TRY(cudaHostGetDevicePointer((void**)&d_hr, hr, 0));
   CUDA_TRY(cudaHostGetDevicePointer((void**)&d_ht, ht, 0));
-  unsigned* total_dev = (unsigned*)c->small.p + 12;  // bytes 48-51 of the 64-byte scratch
+  unsigned* total_dev = (unsigned*)c->small.p + 12;  // bytes 48-55 of the 64-byte scratch (+ the CTA counter)
+  char* slots = (char*)c->lines.p;
+  uint16_t* line_len = (uint16_t*)(slots + (size_t)REC_LINE_MAX * SMALL_N);
   post_small_kernel<<<1, 1024, sizeof(SmallSmem), s>>>(
       (const mcx_hit*)c->hits.p, hit_task, n_dev, n_dev == nd ? n : c->hit_cap, (const JobDev*)c->jobs.p, shift,
-      fo->dedup ? 1 : 0, want_text ? 1 : 0, (mcx_record*)c->recs.p, (mcx_record*)c->recs_out.p, total_dev, d_so,
-      d_hr);
+      fo->dedup ? 1 : 0, want_text ? 1 : 0, (mcx_record*)c->recs.p, (mcx_record*)c->recs_out.p, total_dev, slots,
+      line_len, d_so, d_hr, d_ht);
   CUDA_TRY(cudaGetLastError());
-  if (want_text) {  // exits at once unless post_small_kernel produced records and wants text
-    char* slots = (char*)c->lines.p;
-    uint16_t* line_len = (uint16_t*)(slots + (size_t)REC_LINE_MAX * SMALL_N);
+  dstamp(s, "  small: post_small_kernel done");
+  if (want_text) {  // exits at once unless post_small_kernel left more than SMALL_TEXT_INLINE lines to it
     small_text_kernel<<<SMALL_N / 32, 1024, 0, s>>>((const mcx_record*)c->recs_out.p, (const JobDev*)c->jobs.p,
                                                     total_dev, total_dev + 1, slots, line_len, d_ht, d_so);
     CUDA_TRY(cudaGetLastError());
@@ -1023,6 +1099,11 @@ static int after_search(mcx_context* c, const mcx_job* jobs, uint32_t n_jobs, co
   int rc = enqueue_small(c, (const unsigned long long*)c->ws.p, 0,
                          n_jobs > 1 ? (const uint32_t*)c->hit_task.p : nullptr, jd, fo, text && text_bytes, &queued);
   if (rc) return rc;
+  dstamp(c->s0, "small post (+ text) done");
+  // the search header (hit / candidate counts, flags) after the post kernels, which read it
+  // on the device: the copy is not on their critical path
+  CUDA_TRY(cudaMemcpyAsync(c->h_counters.p, c->ws.p, sizeof(unsigned long long) * (8 + 8ull * n_jobs),
+                           cudaMemcpyDeviceToHost, c->s0));
   CUDA_TRY(cudaStreamSynchronize(c->s0));
   trace("search + small post done (synced)");
   rc = batch_stats(hc, n_jobs, o, c->hit_cap, stats, 0.f);
@@ -1100,8 +1181,11 @@ static int intersect(mcx_context* c, const mcx_job* jobs, uint32_t n_jobs, const
     // search, then (optimistically) the single-kernel post-processing straight after it
     // on the device, one synchronisation for both
     unsigned long long* hc = (unsigned long long*)c->h_counters.p;
-    rc = launch_batch(tasks.data(), n_jobs, &o, (mcx_hit*)c->hits.p, (uint32_t*)c->hit_task.p, c->hit_cap, stats, hc);
+    dstamp(c->s0, "search start (s0)");
+    rc = launch_batch(tasks.data(), n_jobs, &o, (mcx_hit*)c->hits.p, (uint32_t*)c->hit_task.p, c->hit_cap, stats, hc,
+                      nullptr, /*header_later=*/true);
     if (rc) return rc;
+    dstamp(c->s0, "search done");
     bool retry = false;
     rc = after_search(c, jobs, n_jobs, fo, &o, jd, records, n_records, text, text_bytes, stats, &retry, &small_done,
                       &total);
@@ -1190,6 +1274,8 @@ static int load_mesh(mcx_context* c, const double* coords, uint32_t N, uint32_t 
     b_done = std::max(b_done, b1);
     col_done = col1;
   }
+  dstamp(cs, "  last copy of a mesh done");
+  dstamp(s, "  its last pack (+ step) done");
   if (e != cudaSuccess) rc = set_error(MCX_E_CUDA, "mesh upload: %s", cudaGetErrorString(e));
   if (rc) {
     if (cs != s) cudaStreamSynchronize(cs);  // no copy may still target the buffers freed below
@@ -1249,7 +1335,7 @@ static int find_stepped(mcx_context* c, const double* coords_a, uint32_t NA, uin
     const BatchStep step{&whole, steps == 0, swap};
     mcx_stats st{};
     r = launch_batch(&t, 1, &o, (mcx_hit*)c->hits.p, nullptr, c->hit_cap, &st,
-                     (unsigned long long*)c->h_counters.p, &step);
+                     (unsigned long long*)c->h_counters.p, &step, /*header_later=*/true);
     ++steps;
     return r;
   };
@@ -1426,6 +1512,7 @@ int mcx_find_intersections(mcx_context* c, const double* coords_a, uint32_t NA, 
   trace("begin");
   DeviceGuard guard;
   CUDA_TRY(cudaSetDevice(c->device));
+  dstamp(c->s0, "begin");
   mcx_mesh *A = nullptr, *B = nullptr;
   const uint64_t nA = (NA && MA >= 2) ? 2ull * NA * (MA - 1) : 0, nB = (NB && MB >= 2) ? 2ull * NB * (MB - 1) : 0;
   const bool swap = fo->orient == MCX_ORIENT_LARGER_A && nB > nA;
@@ -1437,12 +1524,16 @@ int mcx_find_intersections(mcx_context* c, const double* coords_a, uint32_t NA, 
     mcx_mesh_free(A);  // stream-ordered on s0, after everything above
     mcx_mesh_free(B);
     trace("end");
+    dstamp_print();
     return rc;
   }
-  // A on stream 0; B's copy on stream 1 overlaps A's packing; stream 0 waits for B.
-  rc = load_mesh(c, coords_a, NA, MA, s_a, c->s0, &A);
+  // A packed on stream 0, B on stream 1; stream 0 waits for B.
+  // every H2D copy on the copy stream c->sc, back to back at the link rate (A's chunks,
+  // then B's); A's packs on s0 and B's on s1 follow their chunks through events, so no
+  // copy waits for a pack
+  rc = load_mesh(c, coords_a, NA, MA, s_a, c->s0, &A, true, ChunkFn(), c->sc);
   trace("A enqueued");
-  if (rc == MCX_OK) rc = load_mesh(c, coords_b, NB, MB, s_b, c->s1, &B);
+  if (rc == MCX_OK) rc = load_mesh(c, coords_b, NB, MB, s_b, c->s1, &B, true, ChunkFn(), c->sc);
   trace("B enqueued");
   if (rc == MCX_OK) {
     cudaError_t e = cudaEventRecord(c->ev, c->s1);
@@ -1456,6 +1547,7 @@ int mcx_find_intersections(mcx_context* c, const double* coords_a, uint32_t NA, 
   mcx_mesh_free(A);  // stream-ordered on s0, after everything above
   mcx_mesh_free(B);
   trace("end");
+  dstamp_print();
   return rc;
 }
 

@@ -508,6 +508,7 @@ static int launch_cull(std::vector<SearchParams>& T, Batch& Bt, std::vector<uint
   const size_t tab = sizeof(SearchParams) * T.size();
   CUDA_TRY(h2d_async(dev_tab, T.data(), tab, stream));
   CUDA_TRY(h2d_async((char*)dev_tab + tab, prefix.data(), sizeof(uint64_t) * prefix.size(), stream));
+  dstamp(stream, "    cull: task table uploaded");
   if (total == 0) return MCX_OK;
   Bt.tasks = reinterpret_cast<const SearchParams*>(dev_tab);
   Bt.prefix = reinterpret_cast<const uint64_t*>((char*)dev_tab + tab);
@@ -517,8 +518,10 @@ static int launch_cull(std::vector<SearchParams>& T, Batch& Bt, std::vector<uint
   if (g1 > (uint64_t)dev_sms * 8) g1 = (uint64_t)dev_sms * 8;
   cull_blocks_kernel<<<(unsigned)g1, 256, 0, stream>>>(Bt);
   CUDA_TRY(cudaGetLastError());
+  dstamp(stream, "    cull: level 1 done");
   cull_pairs_kernel<KIND><<<(unsigned)(dev_sms * 8), CULL_THREADS, 0, stream>>>(Bt);
   CUDA_TRY(cudaGetLastError());
+  dstamp(stream, "    cull: level 2 + pair tests done");
   return MCX_OK;
 }
 
@@ -680,7 +683,8 @@ int batch_stats(const unsigned long long* h, uint32_t n, const mcx_opts* o, uint
 }
 
 int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mcx_hit* hits, uint32_t* hit_task,
-                 uint64_t cap, mcx_stats* st, unsigned long long* h_counters, const BatchStep* step) {
+                 uint64_t cap, mcx_stats* st, unsigned long long* h_counters, const BatchStep* step,
+                 bool header_later) {
   if (!tasks || n == 0 || !o || !st) return set_error(MCX_E_ARG, "null argument or empty batch");
   cudaStream_t stream = (cudaStream_t)o->stream;
   const uint32_t scount = o->shard_count ? o->shard_count : 1;
@@ -817,6 +821,7 @@ int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mcx_hit* 
     Bt.status_flag = reinterpret_cast<unsigned long long*>(ws) + 2;
     rc = spec ? launch_solve<KIND_SPEC>(Bt, o->device, stream) : launch_solve<KIND_TRI>(Bt, o->device, stream);
     if (rc != MCX_OK) return rc;
+    dstamp(stream, "    solve done");
   } else {  // no work units → no table upload by a launcher: check the flags directly
     CUDA_TRY(h2d_async(ws + L.table, T.data(), sizeof(SearchParams) * n, stream));
     status_kernel<<<1, 32, 0, stream>>>(reinterpret_cast<const SearchParams*>(ws + L.table), n,
@@ -829,8 +834,9 @@ int launch_batch(const mcx_task* tasks, uint32_t n, const mcx_opts* o, mcx_hit* 
   }
   if (o->timing) CUDA_TRY(cudaEventRecord(tm.e1, stream));
   if (h_counters) {  // asynchronous: the caller synchronises and calls batch_stats
-    CUDA_TRY(cudaMemcpyAsync(h_counters, ws, sizeof(unsigned long long) * (8 + 8ull * n), cudaMemcpyDeviceToHost,
-                             stream));
+    if (!header_later)
+      CUDA_TRY(cudaMemcpyAsync(h_counters, ws, sizeof(unsigned long long) * (8 + 8ull * n), cudaMemcpyDeviceToHost,
+                               stream));
     return MCX_OK;
   }
   std::vector<unsigned long long> h(8 + 8ull * n);
