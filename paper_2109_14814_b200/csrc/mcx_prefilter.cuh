@@ -54,11 +54,28 @@ __device__ __forceinline__ void sub2_cc(unsigned& xa, unsigned& xb, unsigned ha,
   asm("sub.cc.u32 %0, %2, %4;\n subc.u32 %1, %3, %4;" : "=r"(xa), "=r"(xb) : "r"(ha), "r"(hb), "r"(l));
 }
 
+// Half words (LCfg::HALF): the fast sweep tests 4 of the 8 compares (both bounds of dims 0
+// and 1) on 16-bit halves of the same words — nibbles 0, 1, 4, 5 — so one 32-bit subtraction
+// tests two pairs: H = half(A_r) | half(A_r') << 16, L = half(B) · 0x10001.  Fields never
+// borrow (H nibble ≥ 7 ≥ L nibble), and the frame-miss code (B nibble 0 = 7) is in the half.
+// "All fail" must hold for every pair a LOP3 covers, and a 32-bit LOP3 ORs its bits, so one
+// LOP3 per half: ~x_a & ~x_b & G_LO (pairs (r, u), (r″, u) fail at a common compare) and the
+// same with G_HI — 1 instruction per pair instead of 1.5 (1 subtraction per 2 pairs on the
+// fma pipe, 1 LOP3 per 2 pairs on the alu pipe).  A 4-compare pass is conservative for the
+// 8-compare test, which the vote path then runs on the full words, so the exact-test, pass
+// and hit sets are unchanged.
+constexpr unsigned G_LO = 0x00008888u, G_HI = 0x88880000u;
+__device__ __forceinline__ unsigned half16(unsigned w) { return (w & 0xffu) | ((w >> 8) & 0xff00u); }
+
 constexpr int FTILE = 256;  // B records per stage (256 × 32 B = 8 KB)
 constexpr unsigned G4 = 0x88888888u;
 
-template <int QR_, int JB_, int UNROLL_, int MINB_ = 1, bool PAIR2_ = false, bool WFRAME_ = false, int CHAINS_ = 0>
+template <int QR_, int JB_, int UNROLL_, int MINB_ = 1, bool PAIR2_ = false, bool WFRAME_ = false, int CHAINS_ = 0,
+          bool HALF_ = false>
 struct LCfg {
+  // two pair tests per subtraction: 16-bit words holding the 4 compares of dims 0 and 1
+  // (the full 8-compare word is re-tested on a vote) — see "Half words" above
+  static constexpr bool HALF = HALF_;
   // pairs of A slots (of every 8) whose two subtractions form a borrow chain, so that ptxas
   // must put the first on the alu pipe (IADD3 with carry-out) instead of the fma pipe
   static constexpr int CHAINS = CHAINS_;
@@ -95,6 +112,14 @@ __device__ __forceinline__ void fail_and2(unsigned& allfail, unsigned xa, unsign
       " selp.u32 %0, 1, 0, p;\n}"
       : "+r"(allfail)
       : "r"(xa), "r"(xb), "r"(G4));
+}
+
+// allfail &= "x_a and x_b have a guard bit of mask g clear at a common position".
+__device__ __forceinline__ void fail_and2m(unsigned& allfail, unsigned xa, unsigned xb, unsigned g) {
+  asm("{\n .reg .pred p;\n .reg .b32 d;\n setp.ne.u32 p, %0, 0;\n lop3.and.b32 d|p, %1, %2, %3, 0x02, p;\n"
+      " selp.u32 %0, 1, 0, p;\n}"
+      : "+r"(allfail)
+      : "r"(xa), "r"(xb), "r"(g));
 }
 
 // allfail &= "x has a guard bit clear" (LOP3 LUT 0x0a = ~x & G4).
@@ -219,10 +244,18 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_local_kernel(const
     S.aw[warp][r][lane] = (ia >= P.a_begin && ia < P.a_end) ? a_word(ia) : 0x77777777u;  // all guards clear
   }
   __syncwarp();
-  unsigned hw[QR];
+  constexpr int NH = C::HALF ? QR / 2 : QR;
+  unsigned hw[NH];
   auto load_a = [&]() {
+    if constexpr (C::HALF) {
 #pragma unroll
-    for (int r = 0; r < QR; ++r) hw[r] = *(volatile unsigned*)&S.aw[warp][r][lane];
+      for (int k = 0; k < NH; ++k)
+        hw[k] = half16(*(volatile unsigned*)&S.aw[warp][2 * k][lane]) |
+                (half16(*(volatile unsigned*)&S.aw[warp][2 * k + 1][lane]) << 16);
+    } else {
+#pragma unroll
+      for (int r = 0; r < QR; ++r) hw[r] = *(volatile unsigned*)&S.aw[warp][r][lane];
+    }
   };
   load_a();
 
@@ -273,7 +306,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_local_kernel(const
     const uint64_t tb = b0 + (uint64_t)t * FTILE;
     const int nvalid = (int)min((uint64_t)FTILE, b1 - tb);
     // quantise this tile's B records into the frame (per CTA: all threads; per warp: its lanes)
-    for (int j = C::WFRAME ? lane : tid; j < nvalid; j += C::WFRAME ? 32 : C::THREADS) {
+    auto b_word = [&](int j) -> unsigned {
       const float* fr = S.fr[fi];
       const float4 l = S.tile[s][j][0], h = S.tile[s][j][1];
       const bool in = (l.x <= fr[12]) & (fr[8] <= h.x) & (l.y <= fr[13]) & (fr[9] <= h.y) & (l.z <= fr[14]) &
@@ -284,7 +317,11 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_local_kernel(const
             (qfloor(l.w, fr[3], fr[7]) << 12) | ((6u - qceil(h.x, fr[0], fr[4])) << 16) |
             ((6u - qceil(h.y, fr[1], fr[5])) << 20) | ((6u - qceil(h.z, fr[2], fr[6])) << 24) |
             ((6u - qceil(h.w, fr[3], fr[7])) << 28);
-      S.qt[fi][j] = w;
+      return w;
+    };
+    for (int j = C::WFRAME ? lane : tid; j < nvalid; j += C::WFRAME ? 32 : C::THREADS) {
+      const unsigned w = b_word(j);
+      S.qt[fi][j] = C::HALF ? half16(w) * 0x10001u : w;  // HALF: the B half in both halves
     }
     if constexpr (C::WFRAME) __syncwarp();  // each warp reads only the words it wrote
     else __syncthreads();
@@ -295,7 +332,14 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_local_kernel(const
 #pragma unroll
       for (int u = 0; u < NJ; ++u) {
         bw[u] = S.qt[fi][j + u];
-        if constexpr (C::PAIR2) {
+        if constexpr (C::HALF) {
+#pragma unroll
+          for (int k = 0; k < NH; k += 2) {
+            const unsigned xa = imad_sub(hw[k], m1, bw[u]), xb = imad_sub(hw[k + 1], m1, bw[u]);
+            fail_and2m(allfail[k & 3], xa, xb, G_LO);
+            fail_and2m(allfail[(k + 1) & 3], xa, xb, G_HI);
+          }
+        } else if constexpr (C::PAIR2) {
 #pragma unroll
           for (int r = 0; r < QR; r += 2) {
             const int st = (r >> 1) & 7;  // chains spread evenly over the 8 slot pairs
@@ -314,7 +358,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_local_kernel(const
       }
       if (__any_sync(0xffffffffu, (allfail[0] & allfail[1] & allfail[2] & allfail[3]) == 0)) {
 #pragma unroll 1
-        for (int u = 0; u < NJ; ++u) slow((uint32_t)(tb + j + u), S.qt[fi][j + u]);
+        for (int u = 0; u < NJ; ++u) slow((uint32_t)(tb + j + u), C::HALF ? b_word(j + u) : S.qt[fi][j + u]);
         load_a();
       }
     };
@@ -362,9 +406,9 @@ static int launch_local_cfg(std::vector<SearchParams>& T, Batch& Bt, std::vector
 }
 
 // Variant selection (MCX_VARIANT, experiments; 0 = the tuned default: 16 A records per
-// thread, 2-warp CTAs, 9 CTAs/SM (86 registers: the survivor flush only appends to the
-// candidate list), one frame per warp, one vote per 64 B records, one LOP3 per two pair
-// tests, 4 of 16 subtractions on the alu pipe — DESIGN.md §5).
+// thread, 2-warp CTAs, 9 CTAs/SM (75 registers: the survivor flush only appends to the
+// candidate list), one frame per warp, one vote per 64 B records, half words — two pair
+// tests per IMAD subtraction, one LOP3 per two pair tests — DESIGN.md §5).
 static int launch_prefilter(std::vector<SearchParams>& T, Batch& Bt, std::vector<uint64_t>& prefix,
                             void* dev_tab, const std::vector<FboxJob>& jobs, void* dev_jobs, int device,
                             cudaStream_t stream) {
@@ -387,7 +431,11 @@ static int launch_prefilter(std::vector<SearchParams>& T, Batch& Bt, std::vector
     case 15: return MCX_LOCAL(16, 32, 1, 10, true, true, 4);  // one vote per 32 B records, 10 CTAs/SM
     case 16: return MCX_LOCAL(16, 32, 1, 9, true, true, 4);
     case 17: return MCX_LOCAL(16, 64, 1, 8, true, true, 4);  // round 1 default (8 CTAs/SM, 116 registers)
-    default: return MCX_LOCAL(16, 64, 1, 9, true, true, 4);
+    case 18: return MCX_LOCAL(16, 64, 1, 9, true, true, 4);         // round 2a: full words, 9 CTAs/SM
+    case 19: return MCX_LOCAL(32, 64, 1, 9, true, true, 0, true);   // half words, 32 A records per lane
+    case 20: return MCX_LOCAL(16, 32, 1, 9, true, true, 0, true);   // half words, one vote per 32 B records
+    case 21: return MCX_LOCAL(32, 32, 1, 8, true, true, 0, true);
+    default: return MCX_LOCAL(16, 64, 1, 9, true, true, 0, true);   // half words
   }
 #undef MCX_LOCAL
 }

@@ -122,7 +122,7 @@ def test_parity_small(name, mode, oracle_lib):
 
 
 @pytest.mark.parametrize("mode", [_lib.MODE_BRUTE, _lib.MODE_PREFILTER])
-@pytest.mark.parametrize("variant", ["0", "1", "2", "3", "4", "5", "6", "7", "8", "9", "10", "11", "12"])
+@pytest.mark.parametrize("variant", [str(v) for v in range(22)])
 def test_kernel_variants_identical(variant, mode, monkeypatch, oracle_lib):
     monkeypatch.setenv("MCX_VARIANT", variant)
     A, _, B, _ = config_pair("C4i")

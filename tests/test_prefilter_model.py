@@ -125,3 +125,76 @@ def test_out_of_frame_b_never_passes():
     loB[:, 0] = -np.inf  # overlaps in x, disjoint elsewhere
     _, quant, _ = model(loA, hiA, np.nan_to_num(loB, neginf=-1e308), hiB)
     assert not quant.any()
+
+
+# ---- half words (LCfg::HALF, the default): nibbles 0, 1, 4, 5 of each word = both bounds of
+# dims 0 and 1; two A halves per 32-bit register, the B half in both halves.
+G_LO, G_HI = np.uint32(0x00008888), np.uint32(0x88880000)
+
+
+def half16(w):
+    return (w & np.uint32(0xFF)) | ((w >> np.uint32(8)) & np.uint32(0xFF00))
+
+
+def half_model(loA, hiA, loB, hiB):
+    la, ha, lb, hb = f32_down(loA), f32_up(hiA), f32_down(loB), f32_up(hiB)
+    o, k, fl, fh = frame(la, ha)
+    wa, wb = a_words(la, ha, o, k), b_words(lb, hb, o, k, fl, fh)
+    ha2 = half16(wa[0::2]) | (half16(wa[1::2]) << np.uint32(16))  # A slots 2k, 2k+1
+    lb2 = (half16(wb) * np.uint32(0x10001)).astype(np.uint32)
+    x = (ha2[:, None] - lb2[None, :]).astype(np.uint32)  # one IMAD per two pairs
+    exact = ((loB[None] <= hiA[:, None]) & (loA[:, None] <= hiB[None])).all(2)
+    full = ((wa[:, None] - wb[None, :]).astype(np.uint32) & G4) == G4
+    return exact, full, x
+
+
+def test_half_words_are_conservative_and_never_borrow():
+    rng = np.random.default_rng(17)
+    for scale in (1.0, 1e-30, 1e300):
+        loA, hiA = boxes(rng, 256, scale, size=0.2)
+        loB, hiB = boxes(rng, 512, scale, size=0.2)
+        exact, full, x = half_model(loA, hiA, loB, hiB)
+        pass_lo = (x & G_LO) == G_LO  # pair (2k, u)
+        pass_hi = (x & G_HI) == G_HI  # pair (2k + 1, u)
+        half_pass = np.empty_like(full)
+        half_pass[0::2], half_pass[1::2] = pass_lo, pass_hi
+        # the 4-compare half test keeps every pair the 8-compare word test keeps (so every exact pass)
+        assert not (full & ~half_pass).any() and not (exact & ~full).any()
+        # and it equals the 4-compare test on the nibbles directly: no borrow crossed a field
+        la, ha, lb, hb = f32_down(loA), f32_up(hiA), f32_down(loB), f32_up(hiB)
+        o, k, fl, fh = frame(la, ha)
+        wa, wb = a_words(la, ha, o, k), b_words(lb, hb, o, k, fl, fh)
+        direct = np.ones_like(full)
+        for nib in (0, 1, 4, 5):
+            s = np.uint32(4 * nib)
+            fa, fb = (wa >> s) & np.uint32(15), (wb >> s) & np.uint32(15)
+            direct &= (fa[:, None] - fb[None, :].astype(np.int64)) >= 8
+        assert np.array_equal(direct, half_pass)
+
+
+def test_half_lop3_per_half_is_conservative():
+    """Two LOP3s per two subtraction results: ~x_a & ~x_b & G_LO (resp. G_HI) != 0 only if
+    both low (resp. high) pairs fail; a single LOP3 with the full G would not be."""
+    rng = np.random.default_rng(23)
+    loA, hiA = boxes(rng, 256, 1.0, size=0.4)
+    loB, hiB = boxes(rng, 256, 1.0, size=0.4)
+    _, _, x = half_model(loA, hiA, loB, hiB)
+    xa, xb = x[0::2], x[1::2]  # registers k, k+1: pairs (4m, u), (4m+1, u) and (4m+2, u), (4m+3, u)
+    pa_lo, pa_hi = (xa & G_LO) == G_LO, (xa & G_HI) == G_HI
+    pb_lo, pb_hi = (xb & G_LO) == G_LO, (xb & G_HI) == G_HI
+    lo_fail = (~xa & ~xb & G_LO) != 0
+    hi_fail = (~xa & ~xb & G_HI) != 0
+    assert (pa_lo | pb_lo).any() and not (lo_fail & (pa_lo | pb_lo)).any()
+    assert not (hi_fail & (pa_hi | pb_hi)).any()
+    # the unmasked fold is not a "both fail" over all four pairs
+    full_fold = (~xa & ~xb & G4) != 0
+    assert (full_fold & (pa_lo | pa_hi | pb_lo | pb_hi)).any()
+
+
+def test_half_words_out_of_frame_and_invalid_slots():
+    """The frame-miss code (B nibble 0 = 7) and invalid A slots (0x77777777) stay in the half."""
+    assert half16(np.uint32(7)) == 7 and half16(np.uint32(0x77777777)) == 0x7777
+    for a in range(8, 15):  # every valid A nibble 8 + qhi, qhi in 0..6
+        assert ((a - 7) & 8) == 0  # against B's 7: guard clear, the pair fails
+    for b in range(0, 8):  # invalid A nibble 7 against any B nibble: no borrow, guard clear
+        assert 0 <= 7 - b < 8
