@@ -71,8 +71,12 @@ constexpr int FTILE = 256;  // B records per stage (256 × 32 B = 8 KB)
 constexpr unsigned G4 = 0x88888888u;
 
 template <int QR_, int JB_, int UNROLL_, int MINB_ = 1, bool PAIR2_ = false, bool WFRAME_ = false, int CHAINS_ = 0,
-          bool HALF_ = false>
+          bool HALF_ = false, int FT_ = FTILE, bool SHQ_ = false>
 struct LCfg {
+  // per-warp frames, quantised by the whole CTA: a B record outside the union of the
+  // CTA's frames is coded "miss" for every warp after ONE in-frame test instead of one per warp
+  static constexpr bool SHQ = SHQ_ && WFRAME_;
+  static constexpr int FT = FT_;  // B records per shared-memory stage
   // two pair tests per subtraction: 16-bit words holding the 4 compares of dims 0 and 1
   // (the full 8-compare word is re-tested on a vote) — see "Half words" above
   static constexpr bool HALF = HALF_;
@@ -93,11 +97,12 @@ struct LCfg {
 
 template <class C>
 struct __align__(16) LSmem {
-  float4 tile[STAGES][FTILE][2];
-  unsigned qt[C::NF][FTILE];
+  float4 tile[STAGES][C::FT][2];
+  unsigned qt[C::NF][C::FT];
   uint2 queue[C::WARPS][Q_QCAP];
   float frame[C::WARPS][8];
   float fr[C::NF][16];
+  float cfr[8];  // SHQ: union of the CTA's frames (lo_c, hi_c)
   unsigned aw[C::WARPS][C::QR][32];  // the A words, reloaded from here after a slow path
   unsigned long long full[STAGES];
 };
@@ -170,7 +175,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_local_kernel(const
   const uint64_t a0 = gblk * A_BLOCK;
   const uint64_t b0 = (unit % P.nchunk) * P.b_chunk;
   const uint64_t b1 = min(b0 + P.b_chunk, P.nB);
-  const int ntiles = (int)((b1 - b0 + FTILE - 1) / FTILE);
+  const int ntiles = (int)((b1 - b0 + C::FT - 1) / C::FT);
   const unsigned m1 = Bt.neg1;
 
   if (tid == 0) {
@@ -180,8 +185,8 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_local_kernel(const
   __syncthreads();
   if (tid == 0) {
     for (int s = 0; s < STAGES && s < ntiles; ++s) {
-      const uint64_t tb = b0 + (uint64_t)s * FTILE;
-      const uint32_t bytes = (uint32_t)(min((uint64_t)FTILE, b1 - tb) * 32);
+      const uint64_t tb = b0 + (uint64_t)s * C::FT;
+      const uint32_t bytes = (uint32_t)(min((uint64_t)C::FT, b1 - tb) * 32);
       mbar_arrive_expect_tx(&S.full[s], bytes);
       bulk_g2s(&S.tile[s][0][0], P.fB + 2 * tb, bytes, &S.full[s]);
     }
@@ -227,6 +232,11 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_local_kernel(const
     S.fr[fi][4 + c] = k;
     S.fr[fi][8 + c] = l;
     S.fr[fi][12 + c] = h;
+  }
+  if (C::SHQ && tid < 8) {
+    float v = S.frame[0][tid];
+    for (int w = 1; w < C::WARPS; ++w) v = tid < 4 ? fminf(v, S.frame[w][tid]) : fmaxf(v, S.frame[w][tid]);
+    S.cfr[tid] = v;
   }
   __syncthreads();
 
@@ -303,12 +313,10 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_local_kernel(const
   for (int t = 0; t < ntiles; ++t) {
     const int s = t % STAGES;
     mbar_wait(&S.full[s], (uint32_t)((t / STAGES) & 1));
-    const uint64_t tb = b0 + (uint64_t)t * FTILE;
-    const int nvalid = (int)min((uint64_t)FTILE, b1 - tb);
+    const uint64_t tb = b0 + (uint64_t)t * C::FT;
+    const int nvalid = (int)min((uint64_t)C::FT, b1 - tb);
     // quantise this tile's B records into the frame (per CTA: all threads; per warp: its lanes)
-    auto b_word = [&](int j) -> unsigned {
-      const float* fr = S.fr[fi];
-      const float4 l = S.tile[s][j][0], h = S.tile[s][j][1];
+    auto b_word_f = [&](const float4& l, const float4& h, const float* fr) -> unsigned {
       const bool in = (l.x <= fr[12]) & (fr[8] <= h.x) & (l.y <= fr[13]) & (fr[9] <= h.y) & (l.z <= fr[14]) &
                       (fr[10] <= h.z) & (l.w <= fr[15]) & (fr[11] <= h.w);
       unsigned w = 7u;  // misses the frame: nibble 0 = 7 fails against every A word
@@ -319,12 +327,28 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_local_kernel(const
             ((6u - qceil(h.w, fr[3], fr[7])) << 28);
       return w;
     };
-    for (int j = C::WFRAME ? lane : tid; j < nvalid; j += C::WFRAME ? 32 : C::THREADS) {
-      const unsigned w = b_word(j);
-      S.qt[fi][j] = C::HALF ? half16(w) * 0x10001u : w;  // HALF: the B half in both halves
+    auto b_word = [&](int j) -> unsigned { return b_word_f(S.tile[s][j][0], S.tile[s][j][1], S.fr[fi]); };
+    auto enc = [](unsigned w) -> unsigned { return C::HALF ? half16(w) * 0x10001u : w; };  // HALF: the B half twice
+    if constexpr (C::SHQ) {
+      const float* cf = S.cfr;
+      for (int j = tid; j < nvalid; j += C::THREADS) {
+        const float4 l = S.tile[s][j][0], h = S.tile[s][j][1];
+        const bool in = (l.x <= cf[4]) & (cf[0] <= h.x) & (l.y <= cf[5]) & (cf[1] <= h.y) & (l.z <= cf[6]) &
+                        (cf[2] <= h.z) & (l.w <= cf[7]) & (cf[3] <= h.w);
+        if (in) {
+#pragma unroll
+          for (int f = 0; f < C::NF; ++f) S.qt[f][j] = enc(b_word_f(l, h, S.fr[f]));
+        } else {
+#pragma unroll
+          for (int f = 0; f < C::NF; ++f) S.qt[f][j] = enc(7u);
+        }
+      }
+      __syncthreads();
+    } else {
+      for (int j = C::WFRAME ? lane : tid; j < nvalid; j += C::WFRAME ? 32 : C::THREADS) S.qt[fi][j] = enc(b_word(j));
+      if constexpr (C::WFRAME) __syncwarp();  // each warp reads only the words it wrote
+      else __syncthreads();
     }
-    if constexpr (C::WFRAME) __syncwarp();  // each warp reads only the words it wrote
-    else __syncthreads();
     auto step = [&](int j, auto jb_c) {
       constexpr int NJ = decltype(jb_c)::value;
       unsigned bw[NJ];
@@ -368,8 +392,8 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_local_kernel(const
     for (int j = nmain; j < nvalid; ++j) step(j, std::integral_constant<int, 1>());
     __syncthreads();  // every warp is done reading stage s and qt
     if (tid == 0 && t + STAGES < ntiles) {
-      const uint64_t nb = b0 + (uint64_t)(t + STAGES) * FTILE;
-      const uint32_t bytes = (uint32_t)(min((uint64_t)FTILE, b1 - nb) * 32);
+      const uint64_t nb = b0 + (uint64_t)(t + STAGES) * C::FT;
+      const uint32_t bytes = (uint32_t)(min((uint64_t)C::FT, b1 - nb) * 32);
       mbar_arrive_expect_tx(&S.full[s], bytes);
       bulk_g2s(&S.tile[s][0][0], P.fB + 2 * nb, bytes, &S.full[s]);
     }
@@ -386,7 +410,7 @@ static int launch_local_cfg(std::vector<SearchParams>& T, Batch& Bt, std::vector
   const size_t smem = sizeof(LSmem<C>);
   uint64_t slots = 0, total = 0;
   int rc = resident_slots(search_local_kernel<C>, C::THREADS, smem, device, &slots);
-  if (rc == MCX_OK) rc = upload_plan(T, Bt, prefix, dev_tab, slots, 8, stream, &total, FTILE);
+  if (rc == MCX_OK) rc = upload_plan(T, Bt, prefix, dev_tab, slots, 8, stream, &total, C::FT);
   if (rc != MCX_OK || total == 0) return rc;
   if (jobs.size() > 65535) return set_error(MCX_E_ARG, "MCX_MODE_PREFILTER supports at most 65535 meshes per batch");
   Bt.neg1 = 0xffffffffu;
@@ -407,8 +431,9 @@ static int launch_local_cfg(std::vector<SearchParams>& T, Batch& Bt, std::vector
 
 // Variant selection (MCX_VARIANT, experiments; 0 = the tuned default: 16 A records per
 // thread, 2-warp CTAs, 9 CTAs/SM (75 registers: the survivor flush only appends to the
-// candidate list), one frame per warp, one vote per 64 B records, half words — two pair
-// tests per IMAD subtraction, one LOP3 per two pair tests — DESIGN.md §5).
+// candidate list), one frame per warp, B tiles quantised by the whole CTA, one vote per 64 B
+// records, half words — two pair tests per IMAD subtraction, one LOP3 per two pair tests —
+// DESIGN.md §5).
 static int launch_prefilter(std::vector<SearchParams>& T, Batch& Bt, std::vector<uint64_t>& prefix,
                             void* dev_tab, const std::vector<FboxJob>& jobs, void* dev_jobs, int device,
                             cudaStream_t stream) {
@@ -435,7 +460,18 @@ static int launch_prefilter(std::vector<SearchParams>& T, Batch& Bt, std::vector
     case 19: return MCX_LOCAL(32, 64, 1, 9, true, true, 0, true);   // half words, 32 A records per lane
     case 20: return MCX_LOCAL(16, 32, 1, 9, true, true, 0, true);   // half words, one vote per 32 B records
     case 21: return MCX_LOCAL(32, 32, 1, 8, true, true, 0, true);
-    default: return MCX_LOCAL(16, 64, 1, 9, true, true, 0, true);   // half words
+    case 22: return MCX_LOCAL(16, 64, 1, 9, true, false, 0, true);        // half words, one frame per CTA
+    case 23: return MCX_LOCAL(16, 64, 1, 12, true, true, 0, true, 128);   // 128-record stages, 12 CTAs/SM
+    case 24: return MCX_LOCAL(16, 32, 1, 12, true, true, 0, true, 128);
+    case 25: return MCX_LOCAL(16, 128, 1, 9, true, true, 0, true);        // one vote per 128 B records
+    case 26: return MCX_LOCAL(16, 64, 1, 6, true, true, 0, true, 512);    // 512-record stages
+    case 27: return MCX_LOCAL(16, 64, 1, 9, true, true, 0, true, FTILE, true);  // CTA-shared quantisation
+    case 28: return MCX_LOCAL(16, 32, 1, 9, true, true, 0, true, FTILE, true);
+    case 29: return MCX_LOCAL(8, 64, 1, 8, true, true, 0, true, FTILE, true);   // 4 warps of 256-record frames
+    case 30: return MCX_LOCAL(8, 128, 1, 8, true, true, 0, true, FTILE, true);
+    case 31: return MCX_LOCAL(8, 64, 1, 6, true, true, 0, true, 512, true);
+    case 32: return MCX_LOCAL(16, 64, 1, 9, true, true, 0, true);   // half words, per-warp quantisation
+    default: return MCX_LOCAL(16, 64, 1, 9, true, true, 0, true, FTILE, true);  // half words, CTA-shared quantisation
   }
 #undef MCX_LOCAL
 }
