@@ -54,9 +54,10 @@ __device__ __forceinline__ unsigned dlo(double x) { return (unsigned)__double2lo
 __device__ __forceinline__ unsigned dhi(double x) { return (unsigned)__double2hiint(x); }
 
 struct PackSmem {
-  Box box[A_BLOCK];
-  Box gsm[A_BLOCK / GROUP];
+  Box box[A_BLOCK];              // staging: warp w owns records [64 w, 64 w + 64)
+  Box gsm[2][A_BLOCK / GROUP];   // group boxes of this block and of the previous one
   double win[2][4 * WIN_PLANE];
+  unsigned long long wbar[2];    // bulk-copy completion of win[0], win[1]
 };
 
 #ifndef PACK_MIN_BLOCKS
@@ -128,22 +129,82 @@ __global__ void __launch_bounds__(PACK_THREADS, PACK_MIN_BLOCKS)
   const uint32_t li = (tid >> 8) * ORDER_TILE_Q + ((rr >> 4) & 3) * ORDER_SUB_Q + (rr & 3);
   const uint32_t lk = (rr >> 6) * ORDER_SUB_Q + ((rr >> 2) & 3);
   bool bad = false;
-  uint64_t blk = blk0 + blockIdx.x;
+  const int warp = tid >> 5;
+  // window rows by bulk copies (one 272-byte row per thread of warps 0-2: plane wp, row wr;
+  // measured faster than one lane per plane issuing 17 rows) when every row start is
+  // 16-byte aligned; else 8-byte cp.async per element
+  const bool bulk = !(N & 1u) && !(reinterpret_cast<uintptr_t>(coords) & 15);
+  const uint32_t wp = tid / WIN_ROWS, wr = tid - wp * WIN_ROWS;
+  if (tid == 0) {
+    mbar_init(&S.wbar[0], 1);
+    mbar_init(&S.wbar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  // windowed blocks only.  Columns [i0, i0 + 34) of rows row0 .. row0 + 16 (column i0 + 33
+  // is padding: N even and i0 + 32 < N give i0 + 34 <= N); at the right edge (i0 + 32 = N)
+  // window column 32 is θ index 0, copied as the 16 bytes of columns 0-1.  Thread 0's
+  // arrive.expect_tx may land before or after the copies' complete_tx (tx-count is signed).
+  auto issue_window = [&](int buf, const BlockGeom& gw) {
+    if (bulk) {
+      const uint32_t row0 = gw.tk * ORDER_TILE_Q, i0 = (gw.rt >> 8) * ORDER_TILE_Q;
+      const bool wrap = i0 + 2 * ORDER_TILE_Q == N;
+      if (tid == 0) mbar_arrive_expect_tx(&S.wbar[buf], 4 * WIN_ROWS * (wrap ? 256 + 16 : 272));
+      if (tid < 4 * WIN_ROWS) {
+        double* dst = S.win[buf] + wp * WIN_PLANE + wr * WIN_STRIDE;
+        const double* src = coords + wp * plane + (uint64_t)(row0 + wr) * N;
+        bulk_g2s(dst, src + i0, wrap ? 256 : 272, &S.wbar[buf]);
+        if (wrap) bulk_g2s(dst + 2 * ORDER_TILE_Q, src, 16, &S.wbar[buf]);
+      }
+    } else {
+      fetch_window(S.win[buf], coords, N, plane, gw, tid);
+    }
+  };
+  // tile and block boxes of block pb from its 32 group boxes gs (warp 0): lane l reduces
+  // component c = l & 7 over groups 8·(l >> 3) .. +7 (hi components negated), xor 8 gives
+  // the lane's 512-record tile, xor 16 the block
+  auto level_boxes = [&](const Box* gsb, uint64_t pb) {
+    const double* gs = reinterpret_cast<const double*>(gsb);
+    const int c = lane & 7;
+    const unsigned long long neg = c >= 4 ? 0x8000000000000000ull : 0ull;
+    const double* src = gs + 64 * (lane >> 3) + c;
+    double m = __longlong_as_double(__double_as_longlong(src[0]) ^ neg);
+#pragma unroll
+    for (int q = 1; q < 8; ++q) m = dmin(m, __longlong_as_double(__double_as_longlong(src[8 * q]) ^ neg));
+    m = dmin(m, __shfl_xor_sync(0xffffffffu, m, 8));
+    const uint64_t tt = pb * (A_BLOCK / TILE) + (lane >> 4);
+    if (!(lane & 8) && tt < (n + TILE - 1) / TILE)
+      reinterpret_cast<double*>(tbox)[tt * 8 + c] = __longlong_as_double(__double_as_longlong(m) ^ neg);
+    m = dmin(m, __shfl_xor_sync(0xffffffffu, m, 16));
+    if (lane < 8) reinterpret_cast<double*>(bbox)[pb * 8 + c] = __longlong_as_double(__double_as_longlong(m) ^ neg);
+  };
+  const bool levels = gbox && tbox && bbox;
+  uint64_t blk = blk0 + blockIdx.x, prev = ~0ull;
+  uint32_t wph = 0;  // bit b: parity of the next wait on wbar[b]
   if (blk < blk1) {
     const BlockGeom g = block_geom(blk, N, MQ, TN, tiled);
-    if (g.windowed) fetch_window(S.win[0], coords, N, plane, g, tid);
+    if (g.windowed) issue_window(0, g);
   }
   cp_async_commit();
-  for (int it = 0; blk < blk1; ++it, blk += gridDim.x) {
+  int it = 0;
+  for (; blk < blk1; ++it, blk += gridDim.x) {
     const BlockGeom g = block_geom(blk, N, MQ, TN, tiled);
-    const double* win = S.win[it & 1];
+    const int buf = it & 1;
+    const double* win = S.win[buf];
+    if (g.windowed && bulk) {
+      mbar_wait(&S.wbar[buf], (wph >> buf) & 1u);
+      wph ^= 1u << buf;
+    }
     cp_async_wait_all();
-    __syncthreads();  // the window is visible; every thread is done with the previous block
+    // the window is visible; every thread is done with the previous block (its window
+    // buffer is free, its group boxes are in gsm[buf ^ 1])
+    __syncthreads();
+    if (levels && warp == 0 && prev != ~0ull) level_boxes(S.gsm[buf ^ 1], prev);
     {
       const uint64_t nb = blk + gridDim.x;
       if (nb < blk1) {
         const BlockGeom gn = block_geom(nb, N, MQ, TN, tiled);
-        if (gn.windowed) fetch_window(S.win[(it + 1) & 1], coords, N, plane, gn, tid);
+        if (gn.windowed) issue_window(buf ^ 1, gn);
       }
       cp_async_commit();
     }
@@ -226,15 +287,18 @@ __global__ void __launch_bounds__(PACK_THREADS, PACK_MIN_BLOCKS)
       }
       if (perm) reinterpret_cast<uint2*>(perm)[sq] = make_uint2(t0, t0 + 1);
     }
-    __syncthreads();
+    // the warp's staged records leave as coalesced 16-byte stores (no CTA barrier: each
+    // warp stages and copies only its own 64 records)
+    __syncwarp();
     {
       const uint64_t r0 = blk * A_BLOCK;
       const uint32_t n16 = (uint32_t)(min((uint64_t)A_BLOCK, n - r0) * (sizeof(Box) / 16));
+      const uint32_t q1 = min(n16, (uint32_t)(warp + 1) * 256u);
       const uint4* src = reinterpret_cast<const uint4*>(S.box);
       uint4* dst = reinterpret_cast<uint4*>(box + r0);
-      for (uint32_t q = tid; q < n16; q += PACK_THREADS) dst[q] = src[swz(q)];
+      for (uint32_t q = warp * 256u + lane; q < q1; q += 32) dst[q] = src[swz(q)];
     }
-    if (gbox) {
+    if (levels) {
       // group = 16 consecutive storage quads = half a warp.  Reduce-scatter instead of an
       // all-reduce: v = the quad box with its hi half negated (every step is then a min;
       // the canonicalised inputs hold no −0, so the negated zeros are all −0 and the
@@ -256,33 +320,18 @@ __global__ void __launch_bounds__(PACK_THREADS, PACK_MIN_BLOCKS)
       v1 = dmin(v1, __shfl_xor_sync(0xffffffffu, v1, 1));
       const int comp = (hl >> 1);  // = 4·x3 + 2·x2 + x1: lo[0..3], hi[0..3]
       const uint64_t ng = (n + GROUP - 1) / GROUP;
-      double* gs = reinterpret_cast<double*>(S.gsm);
+      double* gs = reinterpret_cast<double*>(S.gsm[buf]);
       if (!(lane & 1)) {
         const uint64_t gi = blk * (A_BLOCK / GROUP) + (tid >> 4);
         const double val = x3 ? -v1 : v1;
         gs[(tid >> 4) * 8 + comp] = val;
         if (gi < ng) reinterpret_cast<double*>(gbox)[gi * 8 + comp] = val;
       }
-      __syncthreads();
-      if (tid < 32 && tbox && bbox) {
-        // warp 0: lane l reduces component c = l & 7 over groups 8·(l >> 3) .. +7 (hi
-        // components negated again), xor 8 gives the lane's 512-record tile, xor 16 the block
-        const int c = lane & 7;
-        const unsigned long long neg = c >= 4 ? 0x8000000000000000ull : 0ull;
-        const double* src = gs + 64 * (lane >> 3) + c;
-        double m = __longlong_as_double(__double_as_longlong(src[0]) ^ neg);
-#pragma unroll
-        for (int q = 1; q < 8; ++q) m = dmin(m, __longlong_as_double(__double_as_longlong(src[8 * q]) ^ neg));
-        m = dmin(m, __shfl_xor_sync(0xffffffffu, m, 8));
-        const uint64_t tt = blk * (A_BLOCK / TILE) + (lane >> 4);
-        if (!(lane & 8) && tt < (n + TILE - 1) / TILE)
-          reinterpret_cast<double*>(tbox)[tt * 8 + c] = __longlong_as_double(__double_as_longlong(m) ^ neg);
-        m = dmin(m, __shfl_xor_sync(0xffffffffu, m, 16));
-        if (lane < 8)
-          reinterpret_cast<double*>(bbox)[blk * 8 + c] = __longlong_as_double(__double_as_longlong(m) ^ neg);
-      }
     }
+    prev = blk;
   }
+  __syncthreads();  // the last block's group boxes
+  if (levels && warp == 0 && prev != ~0ull) level_boxes(S.gsm[(it - 1) & 1], prev);
   cp_async_wait_all();
   if (status && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status, 1u);
 }

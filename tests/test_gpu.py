@@ -44,7 +44,7 @@ def c1():
 
 
 @pytest.mark.parametrize("order", [_lib.ORDER_TILED, _lib.ORDER_NATURAL])
-@pytest.mark.parametrize("shape", [(64, 64), (37, 23), (5, 2), (1024, 3), (33, 50)])
+@pytest.mark.parametrize("shape", [(64, 64), (37, 23), (5, 2), (1024, 3), (33, 50), (48, 40), (96, 33), (256, 129), (66, 35)])
 def test_device_pack_bit_exact(order, shape):
     """Every packed box equals the oracle's box of its original triangle (tiled order:
     via perm, which must be a bijection), and the level boxes written by the same
