@@ -14,6 +14,8 @@ ie, st = h.index("Instructions Executed"), h.index("Warp Stall Sampling (All Sam
 warps = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
 by, ss, tot = collections.Counter(), collections.Counter(), 0
 for x in rows[2:]:
+    if len(x) <= max(ie, st) or not x[ie].strip().isdigit():
+        continue  # another kernel's header / section line
     toks = x[1].split()
     if not toks:
         continue
