@@ -264,10 +264,11 @@ class ClockSampler:
 KERNEL_LAUNCHES = {"brute": 2, "cull": 3, "prefilter": 3}
 INT_LANES_PER_CLK_PER_SM = 64  # B200 fma-heavy (IMAD) and alu (LOP3) pipes, each; IMAD measured 62.7 lanes/clk/SM
                                # (tools/microbench/hprefilter.cu swar3_mix0); issue: 4 SMSP x 32 = 128 lanes/clk/SM
-# SASS of the prefilter inner loop (half words), per 16 pair tests: 8 IMAD (fma-heavy pipe; each
-# subtraction tests two pairs) + 8 LOP3.LUT.PAND (alu pipe; each folds two subtraction results'
-# halves into a "both fail" predicate chain) - 16 instructions, balanced over the two pipes
-PREFILTER_IMAD_PER_PAIR = 8.0 / 16.0
+# SASS of the prefilter inner loop (half words, accumulated folds), per 16 pair tests: 8
+# subtractions (each tests two pairs): 4 IMAD + 2 IMAD.X (fma-heavy pipe) + 2 IADD3 (alu pipe),
+# and 4 LOP3.LUT (alu pipe; each folds two subtraction results into an accumulator) - 12
+# instructions, 6 per pipe
+PREFILTER_IMAD_PER_PAIR = 6.0 / 16.0
 
 
 def run_ours(args):
@@ -429,9 +430,9 @@ def run_ours(args):
                         "(profiles/r02_ncu_brute_c3.txt): 1.95 GB vs 68 GB of algorithmic L2->SMEM tile "
                         "traffic; B's 67 MB of boxes are re-read from HBM ~29x per launch (L2 is split "
                         "over two dies) at ~4 GB/s - negligible against the FP64 bound"}
-    # ---- roofline of the prefilter kernel: every pair = 1/2 IMAD (fma-heavy pipe, 64 lanes/clk/SM)
-    # + 1/2 LOP3 (alu pipe, 64 lanes/clk/SM): 1 instruction per pair, so the fma pipe, the alu
-    # pipe and instruction issue all bind at 128 pairs/clk/SM
+    # ---- roofline of the prefilter kernel: every pair = 6/16 IMAD-class op (fma-heavy pipe, 64
+    # lanes/clk/SM) + 2/16 IADD3 + 1/4 LOP3 (alu pipe, 64 lanes/clk/SM): 0.75 instructions per
+    # pair, so the fma pipe, the alu pipe and instruction issue all bind at 170.7 pairs/clk/SM
     pst = pre["stats"]
     pf_peak = sms * INT_LANES_PER_CLK_PER_SM / PREFILTER_IMAD_PER_PAIR * f_max * 1e6
     pf_achieved = pst["n_tested"] / (pst["kernel_ms"] * 1e-3)
@@ -441,11 +442,13 @@ def run_ours(args):
         "achieved": pf_achieved, "peak": pf_peak, "unit": "pair-tests/s", "frac": pf_achieved / pf_peak,
         "peak_source": f"{sms} SMs x {INT_LANES_PER_CLK_PER_SM} IMAD lanes/clk (fma-heavy pipe) / "
                        f"{PREFILTER_IMAD_PER_PAIR:.4f} IMAD-class ops per pair x {f_max:.0f} MHz (IMAD rate "
-                       "measured 62.7 lanes/clk/SM, tools/microbench/hprefilter.cu); the alu pipe (1/2 LOP3 per "
-                       "pair) and issue (1 instruction per pair, 4 SMSP x 32 lanes/clk) bind at the same rate",
-        "work_per_launch": "n_pairs quantised pair tests (1/2 IMAD + 1/2 LOP3 each: two pairs per 32-bit "
-                           "subtraction of 16-bit half words) + the full 8-compare word test of every pair in "
-                           "a voting 64-record group + n_exact_tests FP64 box tests",
+                       "measured 62.7 lanes/clk/SM, tools/microbench/hprefilter.cu); the alu pipe (6/16 per "
+                       "pair) and issue (0.75 instructions per pair, 4 SMSP x 32 lanes/clk) bind at the same rate",
+        "work_per_launch": "n_pairs quantised pair tests (4 of the 8 box compares at 3-bit resolution in the "
+                           "warp's frame; 1/2 subtraction + 1/4 LOP3 each: two pairs per 32-bit subtraction "
+                           "of 16-bit half words, four per accumulating LOP3) + per voting 64-record group "
+                           "the per-record half test and the full 8-compare word test of its passes + "
+                           "n_exact_tests FP64 box tests",
         "exact_tests_per_step": pst["n_exact_tests"], "kernel_ms": pst["kernel_ms"],
         "kernel_ms_note": "CUDA events around the whole call: fp32 box kernel (~0.03 ms) + search",
         "traffic": (68039680.0 + 3686144.0) if args.config == "C3" else None,

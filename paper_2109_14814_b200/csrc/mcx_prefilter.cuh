@@ -67,12 +67,32 @@ __device__ __forceinline__ void sub2_cc(unsigned& xa, unsigned& xb, unsigned ha,
 constexpr unsigned G_LO = 0x00008888u, G_HI = 0x88880000u;
 __device__ __forceinline__ unsigned half16(unsigned w) { return (w & 0xffu) | ((w >> 8) & 0xff00u); }
 
+// Accumulated folds (LCfg::ACC): y_k = ~x_a & ~x_b & y_k over the whole vote group of JB B
+// records (y_k starts at G4; one LOP3 per two subtraction results = per 4 pair tests, no
+// mask operand), then per accumulator "(y_k & G_LO) != 0 and (y_k & G_HI) != 0": every low
+// (high) pair the accumulator saw fails at one common compare — a conservative "all fail".
+// Weaker than the per-LOP3 test (the common compare must be shared by the whole group), but
+// the B records that miss the warp's frame — nearly all of them — all fail at nibble 0, so
+// a group votes only when it holds a record inside the frame; a vote re-runs the per-LOP3
+// half test per record (exact "all four fail"), and its passes go to the full word test.
+// Per 16 pairs: 8 subtractions (6 IMAD + 2 IADD3 via borrow chains) + 4 LOP3 = 12
+// instructions, 6 per pipe: 0.75 per pair.
+__device__ __forceinline__ unsigned fold2(unsigned xa, unsigned xb, unsigned y) {
+  unsigned r;
+  asm("lop3.b32 %0, %1, %2, %3, 0x02;" : "=r"(r) : "r"(xa), "r"(xb), "r"(y));
+  return r;
+}
+
 constexpr int FTILE = 256;  // B records per stage (256 × 32 B = 8 KB)
 constexpr unsigned G4 = 0x88888888u;
 
 template <int QR_, int JB_, int UNROLL_, int MINB_ = 1, bool PAIR2_ = false, bool WFRAME_ = false, int CHAINS_ = 0,
-          bool HALF_ = false, int FT_ = FTILE, bool SHQ_ = false>
+          bool HALF_ = false, int FT_ = FTILE, bool SHQ_ = false, bool ACC_ = false>
 struct LCfg {
+  // HALF only: fold every subtraction result of a vote group into 4 accumulators (one LOP3
+  // per two results, no mask operand) and test the accumulators once per group — see
+  // "Accumulated folds" above
+  static constexpr bool ACC = ACC_ && HALF_;
   // per-warp frames, quantised by the whole CTA: a B record outside the union of the
   // CTA's frames is coded "miss" for every warp after ONE in-frame test instead of one per warp
   static constexpr bool SHQ = SHQ_ && WFRAME_;
@@ -386,9 +406,68 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_local_kernel(const
         load_a();
       }
     };
+    // the per-record half test (HALF): true if some lane has a pair of B record j + u that
+    // passes the 4 compares
+    auto half_any = [&](unsigned b) -> bool {
+      unsigned af[4] = {1, 1, 1, 1};
+#pragma unroll
+      for (int k = 0; k < NH; k += 2) {
+        const unsigned xa = imad_sub(hw[k], m1, b), xb = imad_sub(hw[k + 1], m1, b);
+        fail_and2m(af[k & 3], xa, xb, G_LO);
+        fail_and2m(af[(k + 1) & 3], xa, xb, G_HI);
+      }
+      return __any_sync(0xffffffffu, (af[0] & af[1] & af[2] & af[3]) == 0);
+    };
+    auto step_acc = [&](int j, auto jb_c) {
+      constexpr int NJ = decltype(jb_c)::value;
+      static_assert(NJ <= 64, "the vote path keeps one bit per B record of the group");
+      unsigned y[NH / 2];
+#pragma unroll
+      for (int k = 0; k < NH / 2; ++k) y[k] = G4;
+#pragma unroll
+      for (int u = 0; u < NJ; ++u) {
+        const unsigned b = S.qt[fi][j + u];
+#pragma unroll
+        for (int k = 0; k < NH; k += 2) {
+          const int st = (k >> 1) & 3;
+          unsigned xa, xb;
+          constexpr int CH = C::CHAINS < 0 ? -C::CHAINS : C::CHAINS;
+          if (((st + 1) * CH) / 4 != (st * CH) / 4) {
+            if constexpr (C::CHAINS < 0) {  // IADD3 with a (dead) carry-out: alu pipe, no chain
+              asm("sub.cc.u32 %0, %1, %2;" : "=r"(xa) : "r"(hw[k]), "r"(b));
+              xb = imad_sub(hw[k + 1], m1, b);
+            } else {
+              sub2_cc(xa, xb, hw[k], hw[k + 1], b);  // the first subtraction on the alu pipe
+            }
+          } else {
+            xa = imad_sub(hw[k], m1, b);
+            xb = imad_sub(hw[k + 1], m1, b);
+          }
+          y[k >> 1] = fold2(xa, xb, y[k >> 1]);
+        }
+      }
+      bool fail = true;
+#pragma unroll
+      for (int k = 0; k < NH / 2; ++k) fail &= ((y[k] & G_LO) != 0u) & ((y[k] & G_HI) != 0u);
+      if (__any_sync(0xffffffffu, !fail)) {
+        uint64_t need = 0;  // B records of the group with a 4-compare pass somewhere in the warp
+#pragma unroll 1
+        for (int u = 0; u < NJ; ++u)
+          if (half_any(S.qt[fi][j + u])) need |= 1ull << u;
+        while (need) {
+          const int u = __ffsll((long long)need) - 1;
+          need &= need - 1;
+          slow((uint32_t)(tb + j + u), b_word(j + u));
+        }
+        load_a();
+      }
+    };
     const int nmain = nvalid - nvalid % C::JB;
 #pragma unroll(C::UNROLL)
-    for (int j = 0; j < nmain; j += C::JB) step(j, std::integral_constant<int, C::JB>());
+    for (int j = 0; j < nmain; j += C::JB) {
+      if constexpr (C::ACC) step_acc(j, std::integral_constant<int, C::JB>());
+      else step(j, std::integral_constant<int, C::JB>());
+    }
     for (int j = nmain; j < nvalid; ++j) step(j, std::integral_constant<int, 1>());
     __syncthreads();  // every warp is done reading stage s and qt
     if (tid == 0 && t + STAGES < ntiles) {
@@ -432,8 +511,8 @@ static int launch_local_cfg(std::vector<SearchParams>& T, Batch& Bt, std::vector
 // Variant selection (MCX_VARIANT, experiments; 0 = the tuned default: 16 A records per
 // thread, 2-warp CTAs, 9 CTAs/SM (75 registers: the survivor flush only appends to the
 // candidate list), one frame per warp, B tiles quantised by the whole CTA, one vote per 64 B
-// records, half words — two pair tests per IMAD subtraction, one LOP3 per two pair tests —
-// DESIGN.md §5).
+// records, half words — two pair tests per subtraction — folded into 4 accumulators (one
+// LOP3 per four pair tests), 2 of every 8 subtractions on the alu pipe — DESIGN.md §5).
 static int launch_prefilter(std::vector<SearchParams>& T, Batch& Bt, std::vector<uint64_t>& prefix,
                             void* dev_tab, const std::vector<FboxJob>& jobs, void* dev_jobs, int device,
                             cudaStream_t stream) {
@@ -471,7 +550,16 @@ static int launch_prefilter(std::vector<SearchParams>& T, Batch& Bt, std::vector
     case 30: return MCX_LOCAL(8, 128, 1, 8, true, true, 0, true, FTILE, true);
     case 31: return MCX_LOCAL(8, 64, 1, 6, true, true, 0, true, 512, true);
     case 32: return MCX_LOCAL(16, 64, 1, 9, true, true, 0, true);   // half words, per-warp quantisation
-    default: return MCX_LOCAL(16, 64, 1, 9, true, true, 0, true, FTILE, true);  // half words, CTA-shared quantisation
+    case 33: return MCX_LOCAL(16, 64, 1, 9, true, true, 2, true, FTILE, true, true);  // accumulated folds
+    case 34: return MCX_LOCAL(16, 32, 1, 9, true, true, 2, true, FTILE, true, true);
+    case 35: return MCX_LOCAL(16, 64, 1, 9, true, true, 0, true, FTILE, true, true);  // no borrow chains
+    case 36: return MCX_LOCAL(16, 64, 1, 9, true, true, 1, true, FTILE, true, true);
+    case 37: return MCX_LOCAL(16, 64, 1, 9, true, true, -2, true, FTILE, true, true);  // plain IADD3 subtractions
+    case 38: return MCX_LOCAL(16, 64, 1, 10, true, true, 2, true, FTILE, true, true);
+    case 39: return MCX_LOCAL(16, 32, 1, 10, true, true, 2, true, FTILE, true, true);
+    case 40: return MCX_LOCAL(16, 64, 2, 9, true, true, 2, true, FTILE, true, true);
+    case 41: return MCX_LOCAL(16, 64, 1, 9, true, true, 0, true, FTILE, true);  // half words, CTA-shared quantisation
+    default: return MCX_LOCAL(16, 64, 1, 9, true, true, 2, true, FTILE, true, true);  // + accumulated folds
   }
 #undef MCX_LOCAL
 }

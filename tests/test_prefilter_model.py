@@ -198,3 +198,43 @@ def test_half_words_out_of_frame_and_invalid_slots():
         assert ((a - 7) & 8) == 0  # against B's 7: guard clear, the pair fails
     for b in range(0, 8):  # invalid A nibble 7 against any B nibble: no borrow, guard clear
         assert 0 <= 7 - b < 8
+
+
+def test_accumulated_folds_are_conservative():
+    """LCfg::ACC: y = G4; y = ~x_a & ~x_b & y over a group of B records; the group is declared
+    all-fail only if (y & G_LO) != 0 and (y & G_HI) != 0 — then every pair it covered fails.
+    Frame-miss B records (code 7) keep nibble 0's guard, so all-miss groups never vote."""
+    rng = np.random.default_rng(29)
+    loA, hiA = boxes(rng, 64, 1.0, size=0.2)
+    la, ha = f32_down(loA), f32_up(hiA)
+    o, k, fl, fh = frame(la, ha)
+    wa = a_words(la, ha, o, k)
+    ha2 = half16(wa[0::2]) | (half16(wa[1::2]) << np.uint32(16))
+    declared, votes = 0, 0
+    for trial in range(400):
+        # groups mixing far-away records (frame misses) with a few near ones
+        nb = 16
+        loB, hiB = boxes(rng, nb, 1.0, size=0.2, center=rng.choice([0.0, 40.0], p=[0.15, 0.85]))
+        lb, hb = f32_down(loB), f32_up(hiB)
+        wb = b_words(lb, hb, o, k, fl, fh)
+        lb2 = (half16(wb) * np.uint32(0x10001)).astype(np.uint32)
+        x = (ha2[:, None] - lb2[None, :]).astype(np.uint32)  # (registers, B records)
+        exact = ((loB[None] <= hiA[:, None]) & (loA[:, None] <= hiB[None])).all(2)
+        for acc in range(0, x.shape[0], 2):  # accumulator over registers acc, acc+1
+            y = np.uint32(G4)
+            for u in range(nb):
+                y = ~x[acc, u] & ~x[acc + 1, u] & y
+            all_fail = bool(y & G_LO) and bool(y & G_HI)
+            rows = [2 * acc, 2 * acc + 1, 2 * acc + 2, 2 * acc + 3]  # A slots of the two registers
+            if all_fail:
+                declared += 1
+                assert not exact[rows].any()
+            else:
+                votes += 1
+        if (wb == 7).all():  # an all-miss group never votes
+            for acc in range(0, x.shape[0], 2):
+                y = np.uint32(G4)
+                for u in range(nb):
+                    y = ~x[acc, u] & ~x[acc + 1, u] & y
+                assert (y & np.uint32(0x00080008)) == np.uint32(0x00080008)
+    assert declared > 0 and votes > 0
