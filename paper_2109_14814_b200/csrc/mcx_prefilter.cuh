@@ -260,6 +260,10 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_local_kernel(const
   }
   __syncthreads();
 
+  float cfr[8];  // SHQ: the CTA frame in registers (read once per B record)
+#pragma unroll
+  for (int c = 0; c < 8; ++c) cfr[c] = C::SHQ ? S.cfr[c] : 0.f;
+
   // ---- A words in registers
   auto a_word = [&](uint32_t ia) -> unsigned {
     const float* fr = S.fr[fi];
@@ -350,18 +354,33 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_local_kernel(const
     auto b_word = [&](int j) -> unsigned { return b_word_f(S.tile[s][j][0], S.tile[s][j][1], S.fr[fi]); };
     auto enc = [](unsigned w) -> unsigned { return C::HALF ? half16(w) * 0x10001u : w; };  // HALF: the B half twice
     if constexpr (C::SHQ) {
-      const float* cf = S.cfr;
-      for (int j = tid; j < nvalid; j += C::THREADS) {
-        const float4 l = S.tile[s][j][0], h = S.tile[s][j][1];
-        const bool in = (l.x <= cf[4]) & (cf[0] <= h.x) & (l.y <= cf[5]) & (cf[1] <= h.y) & (l.z <= cf[6]) &
-                        (cf[2] <= h.z) & (l.w <= cf[7]) & (cf[3] <= h.w);
+      // a B record inside the CTA frame (rare) is quantised into each warp frame, every other
+      // one gets the miss code; the frame test of a full tile's PER records per thread is
+      // issued as independent loads and compare chains (it was latency-bound)
+      auto in_cta = [&](const float4& l, const float4& h) -> bool {
+        const bool i0 = (l.x <= cfr[4]) & (cfr[0] <= h.x) & (l.y <= cfr[5]) & (cfr[1] <= h.y);
+        const bool i1 = (l.z <= cfr[6]) & (cfr[2] <= h.z) & (l.w <= cfr[7]) & (cfr[3] <= h.w);
+        return i0 & i1;
+      };
+      auto put = [&](int j, bool in) {
         if (in) {
+          const float4 l = S.tile[s][j][0], h = S.tile[s][j][1];
 #pragma unroll
           for (int f = 0; f < C::NF; ++f) S.qt[f][j] = enc(b_word_f(l, h, S.fr[f]));
         } else {
 #pragma unroll
           for (int f = 0; f < C::NF; ++f) S.qt[f][j] = enc(7u);
         }
+      };
+      constexpr int PER = C::FT / C::THREADS;
+      if (PER >= 1 && C::FT % C::THREADS == 0 && nvalid == C::FT) {
+        bool in[PER];
+#pragma unroll
+        for (int q = 0; q < PER; ++q) in[q] = in_cta(S.tile[s][tid + q * C::THREADS][0], S.tile[s][tid + q * C::THREADS][1]);
+#pragma unroll
+        for (int q = 0; q < PER; ++q) put(tid + q * C::THREADS, in[q]);
+      } else {
+        for (int j = tid; j < nvalid; j += C::THREADS) put(j, in_cta(S.tile[s][j][0], S.tile[s][j][1]));
       }
       __syncthreads();
     } else {
