@@ -578,6 +578,9 @@ static int launch_prefilter(std::vector<SearchParams>& T, Batch& Bt, std::vector
     case 39: return MCX_LOCAL(16, 32, 1, 10, true, true, 2, true, FTILE, true, true);
     case 40: return MCX_LOCAL(16, 64, 2, 9, true, true, 2, true, FTILE, true, true);
     case 41: return MCX_LOCAL(16, 64, 1, 9, true, true, 0, true, FTILE, true);  // half words, CTA-shared quantisation
+    case 42: return MCX_LOCAL(16, 64, 1, 12, true, true, 2, true, 128, true, true);  // 128-record stages, 12 CTAs/SM
+    case 43: return MCX_LOCAL(16, 64, 1, 11, true, true, 2, true, 128, true, true);
+    case 44: return MCX_LOCAL(16, 64, 1, 6, true, true, 2, true, 512, true, true);   // 512-record stages
     default: return MCX_LOCAL(16, 64, 1, 9, true, true, 2, true, FTILE, true, true);  // + accumulated folds
   }
 #undef MCX_LOCAL
