@@ -258,10 +258,13 @@ __global__ void __launch_bounds__(PACK_THREADS, PACK_MIN_BLOCKS)
       // non-NaN values is exact and order-free, so the boxes are the bits of the
       // three-way min/max (NaN/Inf inputs flag the mesh as unusable anyway).
       Box b1, b2;
+      // non-finite check: x − x is 0 for finite x and NaN for ±Inf / NaN, so the sum of the
+      // 16 differences is NaN iff some vertex coordinate is not finite (no overflow possible)
+      double nf = 0.0;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const double a = dadd(w00[c], 0.0), b = dadd(w10[c], 0.0), d = dadd(w01[c], 0.0), e = dadd(w11[c], 0.0);
-        bad |= !(isfinite(a) && isfinite(b) && isfinite(d) && isfinite(e));
+        nf = dadd(nf, dadd(dadd(dsub(a, a), dsub(b, b)), dadd(dsub(d, d), dsub(e, e))));
         const double mn = dmin(b, d), mx = dmax(b, d);
         b1.lo[c] = dmin(a, mn);
         b1.hi[c] = dmax(a, mx);
@@ -270,6 +273,7 @@ __global__ void __launch_bounds__(PACK_THREADS, PACK_MIN_BLOCKS)
         qlo[c] = dmin(b1.lo[c], b2.lo[c]);
         qhi[c] = dmax(b1.hi[c], b2.hi[c]);
       }
+      bad |= !(nf == 0.0);
       // staging stores: chunk j (16 B) of record r = 2·tid + τ sits at 16-byte slot
       // swz(4r + j); lanes are 128 B apart, so the XOR swizzle spreads each 8-lane phase
       // over all 8 bank columns (unswizzled: 8-way conflicts)
@@ -296,7 +300,18 @@ __global__ void __launch_bounds__(PACK_THREADS, PACK_MIN_BLOCKS)
       const uint32_t q1 = min(n16, (uint32_t)(warp + 1) * 256u);
       const uint4* src = reinterpret_cast<const uint4*>(S.box);
       uint4* dst = reinterpret_cast<uint4*>(box + r0);
-      for (uint32_t q = warp * 256u + lane; q < q1; q += 32) dst[q] = src[swz(q)];
+      const uint32_t q0 = warp * 256u + lane;
+      if (q1 == (uint32_t)(warp + 1) * 256u) {
+        // full warp range: swz(q0 + 32 k) = (q0 ^ s0 ^ 4·(k & 1)) + 32 k with s0 = (q0 >> 3) & 7
+        // (adding 32 k leaves bits 0-2 alone and adds 4 k to bits 3-5), so two base addresses
+        // and immediate offsets
+        const uint4* se = src + (q0 ^ ((q0 >> 3) & 7u));
+        const uint4* so = src + (q0 ^ ((q0 >> 3) & 7u) ^ 4u);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) dst[q0 + 32 * k] = (k & 1) ? so[32 * k] : se[32 * k];
+      } else {
+        for (uint32_t q = q0; q < q1; q += 32) dst[q] = src[swz(q)];
+      }
     }
     if (levels) {
       // group = 16 consecutive storage quads = half a warp.  Reduce-scatter instead of an

@@ -37,6 +37,9 @@ ncu_rep brute_c3 "search_brute|solve" 2 C3 brute
 ncu_rep cull_c3 "cull_|solve" 3 C3 cull
 ncu_rep pack_c3 "pack_kernel" 1 C3 cull
 ncu_rep cull_c5hd "cull_|solve" 3 C5hd cull
+python tools/ncu_opmix.py "$out/ncu_prefilter_c3.ncu-rep" > "$out/r02_opmix_prefilter_c3.txt" 2>&1
+python tools/ncu_opmix.py "$out/ncu_pack_c3.ncu-rep" > "$out/r02_opmix_pack_c3.txt" 2>&1
+rm -f "$out"/*.ncu-rep  # the merge back is capped at 64 MiB
 for t in memcheck racecheck synccheck initcheck; do
   echo "== $t"; timeout 600 compute-sanitizer --tool $t --error-exitcode 7 python tools/sanitize_run.py 2>&1 \
     | grep -E "SUMMARY|workload"
