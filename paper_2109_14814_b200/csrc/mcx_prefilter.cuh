@@ -87,8 +87,10 @@ constexpr int FTILE = 256;  // B records per stage (256 × 32 B = 8 KB)
 constexpr unsigned G4 = 0x88888888u;
 
 template <int QR_, int JB_, int UNROLL_, int MINB_ = 1, bool PAIR2_ = false, bool WFRAME_ = false, int CHAINS_ = 0,
-          bool HALF_ = false, int FT_ = FTILE, bool SHQ_ = false, bool ACC_ = false>
+          bool HALF_ = false, int FT_ = FTILE, bool SHQ_ = false, bool ACC_ = false, int CHMASK_ = 0>
 struct LCfg {
+  // ACC: bit st set = slot pair st (of 4 per B record) uses a borrow chain (overrides CHAINS)
+  static constexpr int CHMASK = CHMASK_;
   // HALF only: fold every subtraction result of a vote group into 4 accumulators (one LOP3
   // per two results, no mask operand) and test the accumulators once per group — see
   // "Accumulated folds" above
@@ -451,7 +453,8 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_local_kernel(const
           const int st = (k >> 1) & 3;
           unsigned xa, xb;
           constexpr int CH = C::CHAINS < 0 ? -C::CHAINS : C::CHAINS;
-          if (((st + 1) * CH) / 4 != (st * CH) / 4) {
+          const bool chain = C::CHMASK ? ((C::CHMASK >> st) & 1) : (((st + 1) * CH) / 4 != (st * CH) / 4);
+          if (chain) {
             if constexpr (C::CHAINS < 0) {  // IADD3 with a (dead) carry-out: alu pipe, no chain
               asm("sub.cc.u32 %0, %1, %2;" : "=r"(xa) : "r"(hw[k]), "r"(b));
               xb = imad_sub(hw[k + 1], m1, b);
@@ -581,6 +584,9 @@ static int launch_prefilter(std::vector<SearchParams>& T, Batch& Bt, std::vector
     case 42: return MCX_LOCAL(16, 64, 1, 12, true, true, 2, true, 128, true, true);  // 128-record stages, 12 CTAs/SM
     case 43: return MCX_LOCAL(16, 64, 1, 11, true, true, 2, true, 128, true, true);
     case 44: return MCX_LOCAL(16, 64, 1, 6, true, true, 2, true, 512, true, true);   // 512-record stages
+    case 45: return MCX_LOCAL(16, 64, 1, 9, true, true, 2, true, FTILE, true, true, 0x5);  // chains on slot pairs 0, 2
+    case 46: return MCX_LOCAL(16, 64, 1, 9, true, true, 2, true, FTILE, true, true, 0x3);  // 0, 1
+    case 47: return MCX_LOCAL(16, 64, 1, 9, true, true, 2, true, FTILE, true, true, 0x9);  // 0, 3
     default: return MCX_LOCAL(16, 64, 1, 9, true, true, 2, true, FTILE, true, true);  // + accumulated folds
   }
 #undef MCX_LOCAL
