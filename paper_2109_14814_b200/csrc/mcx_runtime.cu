@@ -47,6 +47,7 @@
 #include <vector>
 
 #include <cooperative_groups.h>
+#include <immintrin.h>
 
 #include "../../include/mcx.h"
 #include "mcx_common.cuh"
@@ -84,6 +85,33 @@ struct JobDev {
 // own pinned buffer with one thread, ~12 GB/s on these hosts (97 MB in 8.1 ms, pinned
 // 1.8 ms).  StagePool copies pageable bytes into a ring of pinned slots with several host
 // threads while the previous slot's DMA runs.
+// Copy into pinned staging memory with non-temporal stores: no read-for-ownership of the
+// destination lines (host DRAM traffic 2 streams instead of 3) and the staged data does not
+// evict the caches.  Falls back to memcpy without AVX2.
+__attribute__((target("avx2"))) static void nt_copy_avx2(char* dst, const char* src, size_t n) {
+  const size_t head = std::min(n, (size_t)((32 - ((uintptr_t)dst & 31)) & 31));
+  memcpy(dst, src, head);
+  dst += head; src += head; n -= head;
+  size_t i = 0;
+  for (; i + 128 <= n; i += 128) {
+    const __m256i a = _mm256_loadu_si256((const __m256i*)(src + i));
+    const __m256i b = _mm256_loadu_si256((const __m256i*)(src + i + 32));
+    const __m256i c = _mm256_loadu_si256((const __m256i*)(src + i + 64));
+    const __m256i d = _mm256_loadu_si256((const __m256i*)(src + i + 96));
+    _mm256_stream_si256((__m256i*)(dst + i), a);
+    _mm256_stream_si256((__m256i*)(dst + i + 32), b);
+    _mm256_stream_si256((__m256i*)(dst + i + 64), c);
+    _mm256_stream_si256((__m256i*)(dst + i + 96), d);
+  }
+  memcpy(dst + i, src + i, n - i);
+  _mm_sfence();
+}
+static void stage_copy(char* dst, const char* src, size_t n) {
+  static const bool avx2 = __builtin_cpu_supports("avx2") && !getenv("MCX_STAGE_MEMCPY");
+  if (avx2 && n >= 4096) nt_copy_avx2(dst, src, n);
+  else memcpy(dst, src, n);
+}
+
 struct StagePool {
   static constexpr int SLOTS = 3;
   static constexpr size_t SLOT_BYTES = 8u << 20;
@@ -110,7 +138,7 @@ struct StagePool {
     size_t off = 0;
     for (int k = 0; k < nseg && lo < hi; ++k) {
       const size_t a = std::max(lo, off), b = std::min(hi, off + seg_len[k]);
-      if (a < b) memcpy(dst + a, seg_src[k] + (a - off), b - a);
+      if (a < b) stage_copy(dst + a, seg_src[k] + (a - off), b - a);
       off += seg_len[k];
     }
   }
@@ -133,7 +161,8 @@ struct StagePool {
     for (int k = 0; k < n; ++k) t += len[k];
     if (th.empty()) {
       const unsigned hw = std::thread::hardware_concurrency();
-      const int nt = (int)std::min<unsigned>(8, hw > 2 ? hw / 2 : 1);
+      int nt = (int)std::min<unsigned>(8, hw > 2 ? hw / 2 : 1);
+      if (const char* v = getenv("MCX_STAGE_THREADS")) nt = std::max(1, atoi(v));  // experiments
       for (int i = 1; i < nt; ++i) th.emplace_back(&StagePool::worker, this, i);
     }
     {
