@@ -959,3 +959,45 @@ def test_plan_failure_names_the_layer_pair():
         layers.search_plan(u, s, plan)
     assert exc.value.task is not None and exc.value.task[2:] == (2, "-")
     assert "non-finite" in str(exc.value)
+
+
+@pytest.mark.parametrize("shape", [((333, 701), (257, 129)), ((1024, 257), (96, 257)), ((512, 513), (384, 385))])
+def test_pageable_staged_upload_identical(shape, monkeypatch):
+    """Grids of >= 2 MB from pageable NumPy memory go through the pinned staging ring
+    (host copy threads, non-temporal stores, pieces of the 4 planes per slot); the results
+    must equal those of pinned sources and of the driver's own pageable copy
+    (MCX_NO_STAGE), for the plain and the stepped (unbalanced) search and for grid loads."""
+    import torch
+    from paper_2109_14814_b200 import runtime
+    (na, ma), (nb, mb) = shape
+    A, sa = manifold_like(na, ma, 1)
+    B, sb = manifold_like(nb, mb, 2)
+    ctx = runtime.context(0)
+    got = ctx.find(A, sa, B, sb, pipeline=_lib.PIPE_TRIANGLE, text=True)
+    pa, pb = torch.from_numpy(A).pin_memory(), torch.from_numpy(B).pin_memory()
+    pinned = ctx.find(pa, sa, pb, sb, pipeline=_lib.PIPE_TRIANGLE, text=True)
+    monkeypatch.setenv("MCX_NO_STAGE", "1")
+    driver = ctx.find(A, sa, B, sb, pipeline=_lib.PIPE_TRIANGLE, text=True)
+    monkeypatch.delenv("MCX_NO_STAGE")
+    for other in (pinned, driver):
+        assert np.array_equal(got[0], other[0]) and got[1] == other[1]
+    assert len(got[0]) > 0
+    g = ctx.grid(A, sa)  # unpacked grid load (the plan path) through the staging ring
+    try:
+        v = ctx.view(g, 0, ma - 1)
+        try:
+            w = ctx.mesh(A, sa)
+            try:
+                rb = ctx.mesh(B, sb)
+                try:
+                    r1 = ctx.intersect([(v, rb, (1, "+", 1, "-"))], pipeline=_lib.PIPE_TRIANGLE, text=True)
+                    r2 = ctx.intersect([(w, rb, (1, "+", 1, "-"))], pipeline=_lib.PIPE_TRIANGLE, text=True)
+                    assert r1[1] == r2[1] and np.array_equal(r1[0]["gid"], r2[0]["gid"])
+                finally:
+                    rb.free()
+            finally:
+                w.free()
+        finally:
+            v.free()
+    finally:
+        g.free()
