@@ -315,6 +315,16 @@ int mcx_find_intersections(mcx_context* ctx, const double* coords_a, uint32_t NA
                            const mcx_record** records, uint64_t* n_records, const char** text,
                            uint64_t* text_bytes, mcx_stats* stats);
 
+/* mcx_find_intersections on half-layers read in place from larger host meshes: plane_a /
+ * plane_b = the host grid's plane stride in doubles (0: N·M).  A half-layer is a column
+ * range of its mesh, contiguous within each plane, so the reference's
+ * HalfLayer views need no host copy. */
+int mcx_find_intersections_strided(mcx_context* ctx, const double* coords_a, uint32_t NA, uint32_t MA,
+                                   uint64_t plane_a, const double* s_a, const double* coords_b, uint32_t NB,
+                                   uint32_t MB, uint64_t plane_b, const double* s_b, mcx_layer layer,
+                                   const mcx_find_opts* opts, const mcx_record** records, uint64_t* n_records,
+                                   const char** text, uint64_t* text_bytes, mcx_stats* stats);
+
 /* Post-process a hit list that is already on the host (e.g. gathered from several
  * GPUs' shards of one job): records, sort, dedup and text exactly as mcx_intersect. */
 int mcx_finish_hits(mcx_context* ctx, const mcx_hit* hits, uint64_t n_hits, const mcx_mesh* A,

@@ -33,7 +33,7 @@ EXPORTS = ("mcx_a_block", "mcx_workspace_bytes", "mcx_batch_workspace_bytes", "m
            "mcx_pair_candidates_mesh_workspace_bytes", "mcx_records", "mcx_context_create",
            "mcx_context_destroy", "mcx_mesh_load", "mcx_mesh_free", "mcx_mesh_view", "mcx_grid_load",
            "mcx_mesh_view_columns", "mcx_intersect",
-           "mcx_find_intersections", "mcx_finish_hits", "mcx_format_g17", "mcx_last_error", "mcx_version")
+           "mcx_find_intersections", "mcx_find_intersections_strided", "mcx_finish_hits", "mcx_format_g17", "mcx_last_error", "mcx_version")
 
 
 class MeshDev(ctypes.Structure):
@@ -159,6 +159,9 @@ def _load():
     L.mcx_find_intersections.restype = i32
     L.mcx_find_intersections.argtypes = [vp, vp, u32, u32, vp, vp, u32, u32, vp, Layer, P(FindOpts), P(P(Record)),
                                          P(u64), P(vp), P(u64), P(Stats)]
+    L.mcx_find_intersections_strided.restype = i32
+    L.mcx_find_intersections_strided.argtypes = [vp, vp, u32, u32, u64, vp, vp, u32, u32, u64, vp, Layer, P(FindOpts),
+                                                 P(P(Record)), P(u64), P(vp), P(u64), P(Stats)]
     L.mcx_finish_hits.restype = i32
     L.mcx_finish_hits.argtypes = [vp, vp, u64, vp, vp, Layer, P(FindOpts), P(P(Record)), P(u64), P(vp), P(u64)]
     L.mcx_format_g17.restype = i32

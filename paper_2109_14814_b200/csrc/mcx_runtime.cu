@@ -1373,11 +1373,18 @@ using ChunkFn = std::function<int(mcx_mesh*, uint64_t, uint64_t)>;
 // cs (optional): the stream of the chunk copies — chunk j is copied on cs, then packed
 // (and searched) on s after event cev[j], so the copies run back to back however long
 // the per-chunk work on s takes.
+// hplane: the host grid's plane stride in doubles (0: N·M, planes back to back) — a
+// half-layer that is a column range of a larger host mesh is read in place.
 static int load_mesh(mcx_context* c, const double* coords, uint32_t N, uint32_t M, const double* s_values,
                      cudaStream_t s, mcx_mesh** out, bool pack = true, const ChunkFn& on_chunk = ChunkFn(),
-                     cudaStream_t cs = nullptr) {
+                     cudaStream_t cs = nullptr, uint64_t hplane = 0) {
   if (!coords || !s_values || !out) return set_error(MCX_E_ARG, "null argument");
   if (N < 1 || M < 2) return set_error(MCX_E_ARG, "a half-layer needs N >= 1 and M >= 2 (SPEC.md:473)");
+  if (hplane == 0) hplane = (uint64_t)N * M;
+  if (hplane < (uint64_t)N * M)
+    return set_error(MCX_E_ARG, "host plane stride %llu < N*M = %llu", (unsigned long long)hplane,
+                     (unsigned long long)N * M);
+  const size_t hpitch = 8 * hplane;
   const uint64_t n = 2ull * N * (M - 1);
   if (n >= (1ull << 31)) return set_error(MCX_E_ARG, "triangle count must be < 2^31");
   mcx_mesh* m = new mcx_mesh();
@@ -1390,7 +1397,10 @@ static int load_mesh(mcx_context* c, const double* coords, uint32_t N, uint32_t 
   const bool stage = 32ull * N * M >= STAGE_MIN_BYTES && !getenv("MCX_NO_STAGE") && pageable(coords);
   if ((rc = alloc((void**)&m->coords, 32ull * N * M)) || (rc = alloc((void**)&m->s_values, 8ull * M)) ||
       (!pack && (cudaMemcpyAsync(m->s_values, s_values, 8ull * M, cudaMemcpyHostToDevice, s) != cudaSuccess ||
-                 h2d_rows(c, m->coords, 0, coords, 0, 32ull * N * M, 1, s, stage) != cudaSuccess))) {
+                 (hplane == (uint64_t)N * M
+                      ? h2d_rows(c, m->coords, 0, coords, 0, 32ull * N * M, 1, s, stage)
+                      : h2d_rows(c, m->coords, 8ull * N * M, coords, hpitch, 8ull * N * M, 4, s, stage)) !=
+                     cudaSuccess))) {
     mcx_mesh_free(m);
     return rc ? rc : set_error(MCX_E_CUDA, "grid upload failed");
   }
@@ -1428,7 +1438,7 @@ static int load_mesh(mcx_context* c, const double* coords, uint32_t N, uint32_t 
     const uint32_t tr1 = (uint32_t)((uint64_t)ntr * (j + 1) / nch);
     const uint32_t col1 = last ? M : std::min<uint32_t>(M, ORDER_TILE_Q * tr1 + 1);
     if (col1 > col_done)
-      e = h2d_rows(c, m->coords + (uint64_t)col_done * N, plane, coords + (uint64_t)col_done * N, plane,
+      e = h2d_rows(c, m->coords + (uint64_t)col_done * N, plane, coords + (uint64_t)col_done * N, hpitch,
                    (uint64_t)(col1 - col_done) * N * 8, 4, cs, stage);
     if (e == cudaSuccess && cs != s) {
       e = cudaEventRecord(c->cev[j], cs);
@@ -1459,10 +1469,11 @@ static int load_mesh(mcx_context* c, const double* coords, uint32_t N, uint32_t 
 // and packed on s1; the larger mesh L (the sweep side, SURVEY.md:379) is uploaded in
 // chunks on s0 and the blocks of each chunk are searched against S as soon as they are
 // packed (a stepped batch), so the search runs under the rest of the PCIe copy.
-static int find_stepped(mcx_context* c, const double* coords_a, uint32_t NA, uint32_t MA, const double* s_a,
-                        const double* coords_b, uint32_t NB, uint32_t MB, const double* s_b, mcx_layer layer,
-                        const mcx_find_opts* fo, bool swap, mcx_mesh** A, mcx_mesh** B, const mcx_record** records,
-                        uint64_t* n_records, const char** text, uint64_t* text_bytes, mcx_stats* stats) {
+static int find_stepped(mcx_context* c, const double* coords_a, uint32_t NA, uint32_t MA, uint64_t pa,
+                        const double* s_a, const double* coords_b, uint32_t NB, uint32_t MB, uint64_t pb,
+                        const double* s_b, mcx_layer layer, const mcx_find_opts* fo, bool swap, mcx_mesh** A,
+                        mcx_mesh** B, const mcx_record** records, uint64_t* n_records, const char** text,
+                        uint64_t* text_bytes, mcx_stats* stats) {
   if (!c->stage.p) {
     CUDA_TRY(cudaMallocHost((void**)&c->stage.p, 1 << 20));
     c->stage.cap = 1 << 20;
@@ -1472,8 +1483,8 @@ static int find_stepped(mcx_context* c, const double* coords_a, uint32_t NA, uin
   mcx_mesh** Lm = swap ? B : A;
   // every H2D copy on the one copy stream c->sc: S's chunks first at the full link rate,
   // then L's (packs of S on s1, packs and searches of L on s0, gated by chunk events)
-  int rc = swap ? load_mesh(c, coords_a, NA, MA, s_a, c->s1, S, true, ChunkFn(), c->sc)
-                : load_mesh(c, coords_b, NB, MB, s_b, c->s1, S, true, ChunkFn(), c->sc);
+  int rc = swap ? load_mesh(c, coords_a, NA, MA, s_a, c->s1, S, true, ChunkFn(), c->sc, pa)
+                : load_mesh(c, coords_b, NB, MB, s_b, c->s1, S, true, ChunkFn(), c->sc, pb);
   trace("small mesh enqueued");
   if (rc) return rc;
   cudaError_t e = cudaEventRecord(c->ev, c->s1);
@@ -1508,8 +1519,8 @@ static int find_stepped(mcx_context* c, const double* coords_a, uint32_t NA, uin
     ++steps;
     return r;
   };
-  rc = swap ? load_mesh(c, coords_b, NB, MB, s_b, c->s0, Lm, true, on_chunk, c->sc)
-            : load_mesh(c, coords_a, NA, MA, s_a, c->s0, Lm, true, on_chunk, c->sc);
+  rc = swap ? load_mesh(c, coords_b, NB, MB, s_b, c->s0, Lm, true, on_chunk, c->sc, pb)
+            : load_mesh(c, coords_a, NA, MA, s_a, c->s0, Lm, true, on_chunk, c->sc, pa);
   trace("large mesh enqueued (stepped search)");
   if (rc) return rc;
   const mcx_job job{*A, *B, layer};
@@ -1676,6 +1687,15 @@ int mcx_find_intersections(mcx_context* c, const double* coords_a, uint32_t NA, 
                            const double* coords_b, uint32_t NB, uint32_t MB, const double* s_b, mcx_layer layer,
                            const mcx_find_opts* fo, const mcx_record** records, uint64_t* n_records,
                            const char** text, uint64_t* text_bytes, mcx_stats* stats) {
+  return mcx_find_intersections_strided(c, coords_a, NA, MA, 0, s_a, coords_b, NB, MB, 0, s_b, layer, fo, records,
+                                        n_records, text, text_bytes, stats);
+}
+
+int mcx_find_intersections_strided(mcx_context* c, const double* coords_a, uint32_t NA, uint32_t MA,
+                                   uint64_t plane_a, const double* s_a, const double* coords_b, uint32_t NB,
+                                   uint32_t MB, uint64_t plane_b, const double* s_b, mcx_layer layer,
+                                   const mcx_find_opts* fo, const mcx_record** records, uint64_t* n_records,
+                                   const char** text, uint64_t* text_bytes, mcx_stats* stats) {
   using namespace mcx;
   if (!c) return set_error(MCX_E_ARG, "null context");
   int rc = check_find_opts(fo);
@@ -1690,8 +1710,8 @@ int mcx_find_intersections(mcx_context* c, const double* coords_a, uint32_t NA, 
   const uint64_t nL = swap ? nB : nA, nS = swap ? nA : nB;  // L: the sweep side
   if (fo->mode == MCX_MODE_CULL && fo->shard_count <= 1 && nL >= STEP_MIN_TRI && nS && nS * step_ratio() <= nL &&
       !getenv("MCX_NO_STEPS")) {
-    rc = find_stepped(c, coords_a, NA, MA, s_a, coords_b, NB, MB, s_b, layer, fo, swap, &A, &B, records, n_records,
-                      text, text_bytes, stats);
+    rc = find_stepped(c, coords_a, NA, MA, plane_a, s_a, coords_b, NB, MB, plane_b, s_b, layer, fo, swap, &A, &B,
+                      records, n_records, text, text_bytes, stats);
     mcx_mesh_free(A);  // stream-ordered on s0, after everything above
     mcx_mesh_free(B);
     trace("end");
@@ -1702,9 +1722,9 @@ int mcx_find_intersections(mcx_context* c, const double* coords_a, uint32_t NA, 
   // every H2D copy on the copy stream c->sc, back to back at the link rate (A's chunks,
   // then B's); A's packs on s0 and B's on s1 follow their chunks through events, so no
   // copy waits for a pack
-  rc = load_mesh(c, coords_a, NA, MA, s_a, c->s0, &A, true, ChunkFn(), c->sc);
+  rc = load_mesh(c, coords_a, NA, MA, s_a, c->s0, &A, true, ChunkFn(), c->sc, plane_a);
   trace("A enqueued");
-  if (rc == MCX_OK) rc = load_mesh(c, coords_b, NB, MB, s_b, c->s1, &B, true, ChunkFn(), c->sc);
+  if (rc == MCX_OK) rc = load_mesh(c, coords_b, NB, MB, s_b, c->s1, &B, true, ChunkFn(), c->sc, plane_b);
   trace("B enqueued");
   if (rc == MCX_OK) {
     cudaError_t e = cudaEventRecord(c->ev, c->s1);

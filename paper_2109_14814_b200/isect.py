@@ -113,9 +113,9 @@ def pair_counts(N1: int, N2: int, M1: int, M2: int):
 
 
 # ---------------------------------------------------------------- helpers
-def _coords(h) -> np.ndarray:
+def _coords(h, copy: bool = True) -> np.ndarray:
     if isinstance(h, HalfLayer):
-        return np.ascontiguousarray(h.coords)
+        return np.ascontiguousarray(h.coords) if copy else h.coords
     c = np.asarray(h, dtype=np.float64)
     if c.ndim != 3 or c.shape[0] != 4:
         raise ConfigError("expected a HalfLayer or a (4, M, N) grid")
@@ -319,7 +319,9 @@ def find_intersections(u_half, s_half, backend: str = "cuda", *, devices=(0,), m
     from . import runtime
     _check_backend(backend)
     m, p = _mode_pipeline(mode, pipeline)
-    ca, cb = _coords(u_half), _coords(s_half)
+    # a HalfLayer is read in place from its mesh (column range: contiguous within each
+    # plane, the planes at the mesh's plane stride) — no host copy
+    ca, cb = _coords(u_half, copy=False), _coords(s_half, copy=False)
     layer = _task(u_half, s_half) or (0, "+", 0, "+")
     sa, sb = _svals(u_half, ca.shape[1]), _svals(s_half, cb.shape[1])
     devices = list(devices)
@@ -329,6 +331,7 @@ def find_intersections(u_half, s_half, backend: str = "cuda", *, devices=(0,), m
     if len(devices) == 1:
         recs, _, _ = ctx.find(ca, sa, cb, sb, layer, mode=m, pipeline=p, dedup=dedup, task=_task(u_half, s_half))
     else:
+        ca, cb = np.ascontiguousarray(ca), np.ascontiguousarray(cb)
         res = _device.search(ca, cb, devices=devices, mode=m, task=_task(u_half, s_half), pipeline=p)
         A, B = ctx.mesh(ca, sa), ctx.mesh(cb, sb)
         try:

@@ -51,6 +51,19 @@ def _host_f64(a):
     return a.ctypes.data, a
 
 
+def _host_grid(a):
+    """(pointer, keep-alive, plane stride in doubles) of a (4, M, N) float64 host grid.  A
+    NumPy view whose rows are contiguous within each plane (a half-layer's column range of
+    a larger mesh) is passed in place with its plane stride (0: dense)."""
+    if (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.ndim == 3 and a.shape[0] == 4
+            and a.strides[2] == 8 and a.strides[1] == 8 * a.shape[2] and a.strides[0] % 8 == 0
+            and a.strides[0] >= 8 * a.shape[1] * a.shape[2]):
+        plane = a.strides[0] // 8
+        return a.ctypes.data, a, (0 if plane == a.shape[1] * a.shape[2] else plane)
+    p, keep = _host_f64(a)
+    return p, keep, 0
+
+
 def find_opts(mode: int, pipeline: int, dedup: bool, text: bool, shard=(0, 1),
               orient: int = _lib.ORIENT_LARGER_A) -> _lib.FindOpts:
     return _lib.FindOpts(int(mode), int(pipeline), int(bool(dedup)), int(bool(text)), int(shard[0]), int(shard[1]),
@@ -147,8 +160,8 @@ class Context:
         """mcx_find_intersections: host grids → (records, text bytes, stats dict).  ``shard``
         restricts the search to a cyclic share of the (larger) mesh's blocks, as one rank
         of a multi-GPU job (the records are then that shard's)."""
-        pa, ka = _host_f64(coords_a)
-        pb, kb = _host_f64(coords_b)
+        pa, ka, plane_a = _host_grid(coords_a)
+        pb, kb, plane_b = _host_grid(coords_b)
         sa = np.ascontiguousarray(s_a, dtype=np.float64)
         sb = np.ascontiguousarray(s_b, dtype=np.float64)
         _, MA, NA = (int(v) for v in ka.shape)
@@ -160,10 +173,10 @@ class Context:
         fo = find_opts(mode, pipeline, dedup, text, shard, orient)
         recp, n, textp, tlen, st = ctypes.POINTER(_lib.Record)(), ctypes.c_uint64(), ctypes.c_void_p(), \
             ctypes.c_uint64(), _lib.Stats()
-        rc = _lib.load().mcx_find_intersections(self.handle, pa, NA, MA, sa.ctypes.data, pb, NB, MB, sb.ctypes.data,
-                                                layer_struct(layer), ctypes.byref(fo), ctypes.byref(recp),
-                                                ctypes.byref(n), ctypes.byref(textp), ctypes.byref(tlen),
-                                                ctypes.byref(st))
+        rc = _lib.load().mcx_find_intersections_strided(self.handle, pa, NA, MA, plane_a, sa.ctypes.data, pb, NB, MB,
+                                                        plane_b, sb.ctypes.data, layer_struct(layer),
+                                                        ctypes.byref(fo), ctypes.byref(recp), ctypes.byref(n),
+                                                        ctypes.byref(textp), ctypes.byref(tlen), ctypes.byref(st))
         _lib.check(rc, "mcx_find_intersections", task=task)
         recs, txt = self._out(recp, n, textp, tlen)
         return recs, txt, st.as_dict()

@@ -1001,3 +1001,30 @@ def test_pageable_staged_upload_identical(shape, monkeypatch):
             v.free()
     finally:
         g.free()
+
+
+@pytest.mark.parametrize("sizes", [((64, 200), (48, 120)), ((512, 900), (300, 400)), ((1024, 700), (96, 300))])
+def test_strided_half_layers_read_in_place(sizes):
+    """mcx_find_intersections_strided: column ranges of larger host meshes (the reference's
+    HalfLayer views, plane stride > N·M) give the records and text of their contiguous
+    copies — small (driver copy), staged (>= 2 MB pageable) and stepped (unbalanced) — and
+    isect.find_intersections passes HalfLayers without a host copy."""
+    from paper_2109_14814_b200 import runtime
+    from paper_2109_14814_b200.mesh import ManifoldMesh, HalfLayer
+    (na, ma), (nb, mb) = sizes
+    A, sa = manifold_like(na, ma, 1)
+    B, sb = manifold_like(nb, mb, 2)
+    ha = HalfLayer(ManifoldMesh(A, sa), n=2, sign=1, col_range=(ma // 5, ma - ma // 7))
+    hb = HalfLayer(ManifoldMesh(B, sb), n=3, sign=-1, col_range=(mb // 9, mb - 2))
+    va, vb = ha.coords, hb.coords
+    assert not va.flags.c_contiguous and runtime._host_grid(va)[2] == ma * na
+    ctx = runtime.context(0)
+    texts = {}
+    for pipe in (_lib.PIPE_SPEC, _lib.PIPE_TRIANGLE):
+        got = ctx.find(va, ha.s_values, vb, hb.s_values, (2, "+", 3, "-"), pipeline=pipe, text=True)
+        ref = ctx.find(np.ascontiguousarray(va), ha.s_values, np.ascontiguousarray(vb), hb.s_values,
+                       (2, "+", 3, "-"), pipeline=pipe, text=True)
+        assert np.array_equal(got[0], ref[0]) and got[1] == ref[1]
+        texts[pipe] = got[1]
+    recs = isect.find_intersections(ha, hb)  # the plugin call on HalfLayers (spec pipeline)
+    assert [r.to_line() for r in recs] == texts[_lib.PIPE_SPEC].decode().splitlines()
