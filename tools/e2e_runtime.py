@@ -71,6 +71,18 @@ def main(configs=("C3", "C2", "C5hd")):
     um = layered_mesh(1024, "unstable", 14, 1.6, 0.1, 1, K=17, per_layer=34)
     sm = layered_mesh(2048, "stable", 14, 1 / 1.6, 0.1, 2, K=17, per_layer=34)
     plan = layers.enumerate_layer_pairs(um, sm, 14)
+    # the plugin call on HalfLayer views of the paper meshes (the plan's busiest task, U13+ x S13+):
+    # read in place with the mesh's plane stride vs a contiguous host copy first
+    from paper_2109_14814_b200 import isect
+    from paper_2109_14814_b200.mesh import half_layer
+    hu, hs = half_layer(um, 13, 1), half_layer(sm, 13, 1)
+    t_view, _ = wall(lambda: isect.find_intersections(hu, hs), reps=10)
+    t_copy, _ = wall(lambda: ctx.find(np.ascontiguousarray(hu.coords), hu.s_values, np.ascontiguousarray(hs.coords),
+                                      hs.s_values, (13, "+", 13, "+")), reps=10)
+    print(json.dumps({"plugin_halflayer": "isect.find_intersections(U13+, S13+) on HalfLayer views of the paper "
+                      "meshes (pageable, read in place)", "grid_bytes": hu.coords.nbytes + hs.coords.nbytes,
+                      "view_ms_min": t_view, "copy_then_find_ms_min": t_copy,
+                      "records": len(isect.find_intersections(hu, hs))}), flush=True)
     for pipe in ("spec", "triangle"):
         best, med = wall(lambda: layers.search_plan(um, sm, plan, pipeline=pipe, text=True), reps=5)
         res = layers.search_plan(um, sm, plan, pipeline=pipe, text=True)
