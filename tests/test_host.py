@@ -299,3 +299,19 @@ def test_dedup_greedy_chain():
     pts = np.concatenate([base, base + 1e-12, base[::-1]])
     keep = isect._dedup_mask(pts, 1e-9)
     assert keep.sum() == 50 and keep[:50].all()
+
+
+def test_host_grid_plane_stride():
+    """runtime._host_grid: a HalfLayer view (column range of its mesh) is passed in place
+    with the mesh's plane stride; dense grids get stride 0; other layouts are copied."""
+    from paper_2109_14814_b200 import runtime
+    from paper_2109_14814_b200.mesh import HalfLayer, ManifoldMesh, manifold_like
+    A, s = manifold_like(16, 40, 1)
+    h = HalfLayer(ManifoldMesh(A, s), col_range=(5, 20))
+    p, keep, plane = runtime._host_grid(h.coords)
+    assert plane == 40 * 16 and p == A.ctypes.data + 5 * 16 * 8 and keep is h.coords or keep.base is not None
+    assert runtime._host_grid(A)[2] == 0                      # dense
+    assert runtime._host_grid(HalfLayer.whole(ManifoldMesh(A, s)).coords)[2] == 0
+    T = np.ascontiguousarray(A.transpose(0, 2, 1)).transpose(0, 2, 1)  # rows not contiguous
+    p2, keep2, plane2 = runtime._host_grid(T)
+    assert plane2 == 0 and keep2.flags.c_contiguous and np.array_equal(keep2, A)
