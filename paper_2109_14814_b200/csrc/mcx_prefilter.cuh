@@ -27,11 +27,14 @@ namespace mcx {
 //   * A words: nibble c = 8 + qhi_c, nibble 4+c = 14 − qlo_c.  H − L then has, per
 //     nibble, 8 + qhi_A − qlo_B ∈ [1, 15] (no borrow between nibbles) — guard bit
 //     set iff qlo_B ≤ qhi_A — and 8 + qhi_B − qlo_A.  Invalid A slots: 0x77777777.
-//   * Pair test = IMAD (L·(−1) + H, fma pipe) + half a LOP3.LUT.PAND (alu pipe): one
-//     LOP3 with LUT ~x_a & ~x_b & G per two A words, predicate output ANDed into one of
-//     4 "all fail" chains — "both fail at a common guard position", a conservative
-//     "both fail".  1.5 instructions per pair; the fma pipe (IMAD, 64 lanes/clk/SM)
-//     binds.  One warp vote per JB B records.
+//   * Pair test (full words) = IMAD (L·(−1) + H, fma pipe) + half a LOP3.LUT.PAND (alu
+//     pipe): one LOP3 with LUT ~x_a & ~x_b & G per two A words, predicate output ANDed
+//     into one of 4 "all fail" chains — "both fail at a common guard position", a
+//     conservative "both fail".  1.5 instructions per pair.  One warp vote per JB B
+//     records.  The default kernel tests 4 of the 8 compares on 16-bit half words, two
+//     pairs per subtraction, folded four per LOP3 into per-group accumulators (0.75
+//     instructions per pair: "Half words" and "Accumulated folds" below), and runs the
+//     full word test only on voting groups.
 //   * B records reach shared memory as fp32 boxes (bulk copies, 8 KB stages); each
 //     warp quantises each tile into its own frame (~1/20 of the test work) before
 //     testing it.
