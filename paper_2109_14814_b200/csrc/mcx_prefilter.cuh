@@ -90,8 +90,12 @@ constexpr int FTILE = 256;  // B records per stage (256 × 32 B = 8 KB)
 constexpr unsigned G4 = 0x88888888u;
 
 template <int QR_, int JB_, int UNROLL_, int MINB_ = 1, bool PAIR2_ = false, bool WFRAME_ = false, int CHAINS_ = 0,
-          bool HALF_ = false, int FT_ = FTILE, bool SHQ_ = false, bool ACC_ = false, int CHMASK_ = 0>
+          bool HALF_ = false, int FT_ = FTILE, bool SHQ_ = false, bool ACC_ = false, int CHMASK_ = 0,
+          int ACCSETS_ = 1>
 struct LCfg {
+  // ACC: accumulator sets, alternated by B record (more independent fold chains, and each
+  // accumulator covers fewer pairs, so fewer spurious votes)
+  static constexpr int ACCSETS = ACCSETS_;
   // ACC: bit st set = slot pair st (of 4 per B record) uses a borrow chain (overrides CHAINS)
   static constexpr int CHMASK = CHMASK_;
   // HALF only: fold every subtraction result of a vote group into 4 accumulators (one LOP3
@@ -445,9 +449,10 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_local_kernel(const
     auto step_acc = [&](int j, auto jb_c) {
       constexpr int NJ = decltype(jb_c)::value;
       static_assert(NJ <= 64, "the vote path keeps one bit per B record of the group");
-      unsigned y[NH / 2];
+      constexpr int NY = NH / 2 * C::ACCSETS;
+      unsigned y[NY];
 #pragma unroll
-      for (int k = 0; k < NH / 2; ++k) y[k] = G4;
+      for (int k = 0; k < NY; ++k) y[k] = G4;
 #pragma unroll
       for (int u = 0; u < NJ; ++u) {
         const unsigned b = S.qt[fi][j + u];
@@ -468,12 +473,13 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_local_kernel(const
             xa = imad_sub(hw[k], m1, b);
             xb = imad_sub(hw[k + 1], m1, b);
           }
-          y[k >> 1] = fold2(xa, xb, y[k >> 1]);
+          const int ya = (u % C::ACCSETS) * (NH / 2) + (k >> 1);
+          y[ya] = fold2(xa, xb, y[ya]);
         }
       }
       bool fail = true;
 #pragma unroll
-      for (int k = 0; k < NH / 2; ++k) fail &= ((y[k] & G_LO) != 0u) & ((y[k] & G_HI) != 0u);
+      for (int k = 0; k < NY; ++k) fail &= ((y[k] & G_LO) != 0u) & ((y[k] & G_HI) != 0u);
       if (__any_sync(0xffffffffu, !fail)) {
         uint64_t need = 0;  // B records of the group with a 4-compare pass somewhere in the warp
 #pragma unroll 1
@@ -590,6 +596,8 @@ static int launch_prefilter(std::vector<SearchParams>& T, Batch& Bt, std::vector
     case 45: return MCX_LOCAL(16, 64, 1, 9, true, true, 2, true, FTILE, true, true, 0x5);  // chains on slot pairs 0, 2
     case 46: return MCX_LOCAL(16, 64, 1, 9, true, true, 2, true, FTILE, true, true, 0x3);  // 0, 1
     case 47: return MCX_LOCAL(16, 64, 1, 9, true, true, 2, true, FTILE, true, true, 0x9);  // 0, 3
+    case 48: return MCX_LOCAL(16, 64, 1, 9, true, true, 2, true, FTILE, true, true, 0, 2);  // 2 accumulator sets
+    case 49: return MCX_LOCAL(16, 64, 1, 8, true, true, 2, true, FTILE, true, true, 0, 4);  // 4 sets
     default: return MCX_LOCAL(16, 64, 1, 9, true, true, 2, true, FTILE, true, true);  // + accumulated folds
   }
 #undef MCX_LOCAL
