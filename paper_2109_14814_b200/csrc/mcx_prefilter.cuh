@@ -91,8 +91,11 @@ constexpr unsigned G4 = 0x88888888u;
 
 template <int QR_, int JB_, int UNROLL_, int MINB_ = 1, bool PAIR2_ = false, bool WFRAME_ = false, int CHAINS_ = 0,
           bool HALF_ = false, int FT_ = FTILE, bool SHQ_ = false, bool ACC_ = false, int CHMASK_ = 0,
-          int ACCSETS_ = 1>
+          int ACCSETS_ = 1, bool ACCAND_ = false>
 struct LCfg {
+  // ACC: test the AND of the accumulators (one common failing compare over the whole group
+  // — still conservative, cheaper than testing each accumulator)
+  static constexpr bool ACCAND = ACCAND_;
   // ACC: accumulator sets, alternated by B record (more independent fold chains, and each
   // accumulator covers fewer pairs, so fewer spurious votes)
   static constexpr int ACCSETS = ACCSETS_;
@@ -448,7 +451,6 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_local_kernel(const
     };
     auto step_acc = [&](int j, auto jb_c) {
       constexpr int NJ = decltype(jb_c)::value;
-      static_assert(NJ <= 64, "the vote path keeps one bit per B record of the group");
       constexpr int NY = NH / 2 * C::ACCSETS;
       unsigned y[NY];
 #pragma unroll
@@ -478,17 +480,31 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) search_local_kernel(const
         }
       }
       bool fail = true;
+      if constexpr (C::ACCAND) {
+        unsigned t = y[0];
 #pragma unroll
-      for (int k = 0; k < NY; ++k) fail &= ((y[k] & G_LO) != 0u) & ((y[k] & G_HI) != 0u);
+        for (int k = 1; k < NY; ++k) t &= y[k];
+        fail = ((t & G_LO) != 0u) & ((t & G_HI) != 0u);
+      } else {
+#pragma unroll
+        for (int k = 0; k < NY; ++k) fail &= ((y[k] & G_LO) != 0u) & ((y[k] & G_HI) != 0u);
+      }
       if (__any_sync(0xffffffffu, !fail)) {
-        uint64_t need = 0;  // B records of the group with a 4-compare pass somewhere in the warp
+        // B records of the group with a 4-compare pass somewhere in the warp, 64 per word
+        constexpr int NW = (NJ + 63) / 64;
+        uint64_t need[NW];
+#pragma unroll
+        for (int w = 0; w < NW; ++w) need[w] = 0;
 #pragma unroll 1
         for (int u = 0; u < NJ; ++u)
-          if (half_any(S.qt[fi][j + u])) need |= 1ull << u;
-        while (need) {
-          const int u = __ffsll((long long)need) - 1;
-          need &= need - 1;
-          slow((uint32_t)(tb + j + u), b_word(j + u));
+          if (half_any(S.qt[fi][j + u])) need[u >> 6] |= 1ull << (u & 63);
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+          while (need[w]) {
+            const int u = w * 64 + __ffsll((long long)need[w]) - 1;
+            need[w] &= need[w] - 1;
+            slow((uint32_t)(tb + j + u), b_word(j + u));
+          }
         }
         load_a();
       }
@@ -598,7 +614,10 @@ static int launch_prefilter(std::vector<SearchParams>& T, Batch& Bt, std::vector
     case 47: return MCX_LOCAL(16, 64, 1, 9, true, true, 2, true, FTILE, true, true, 0x9);  // 0, 3
     case 48: return MCX_LOCAL(16, 64, 1, 9, true, true, 2, true, FTILE, true, true, 0, 2);  // 2 accumulator sets
     case 49: return MCX_LOCAL(16, 64, 1, 8, true, true, 2, true, FTILE, true, true, 0, 4);  // 4 sets
-    default: return MCX_LOCAL(16, 64, 1, 9, true, true, 2, true, FTILE, true, true);  // + accumulated folds
+    case 50: return MCX_LOCAL(16, 64, 1, 9, true, true, 2, true, FTILE, true, true, 0, 1, true);  // AND of the accumulators
+    case 51: return MCX_LOCAL(16, 128, 1, 9, true, true, 2, true, FTILE, true, true, 0, 1, true);
+    case 52: return MCX_LOCAL(16, 64, 1, 9, true, true, 2, true, FTILE, true, true);  // accumulators tested one by one
+    default: return MCX_LOCAL(16, 64, 1, 9, true, true, 2, true, FTILE, true, true, 0, 1, true);  // + accumulated folds
   }
 #undef MCX_LOCAL
 }

@@ -122,7 +122,7 @@ def test_parity_small(name, mode, oracle_lib):
 
 
 @pytest.mark.parametrize("mode", [_lib.MODE_BRUTE, _lib.MODE_PREFILTER])
-@pytest.mark.parametrize("variant", [str(v) for v in range(50)])
+@pytest.mark.parametrize("variant", [str(v) for v in range(53)])
 def test_kernel_variants_identical(variant, mode, monkeypatch, oracle_lib):
     monkeypatch.setenv("MCX_VARIANT", variant)
     A, _, B, _ = config_pair("C4i")

@@ -238,3 +238,15 @@ def test_accumulated_folds_are_conservative():
                     y = ~x[acc, u] & ~x[acc + 1, u] & y
                 assert (y & np.uint32(0x00080008)) == np.uint32(0x00080008)
     assert declared > 0 and votes > 0
+
+
+def test_accumulator_and_is_conservative():
+    """LCfg::ACCAND: the group is all-fail if the AND of the accumulators keeps a low and a
+    high guard bit — one compare at which every pair of the group fails (implies each
+    accumulator's own test)."""
+    rng = np.random.default_rng(31)
+    for _ in range(2000):
+        ys = rng.integers(0, 2**32, 4, dtype=np.uint64).astype(np.uint32) & G4
+        t = ys[0] & ys[1] & ys[2] & ys[3]
+        if (t & G_LO) and (t & G_HI):
+            assert all((y & G_LO) and (y & G_HI) for y in ys)
