@@ -626,6 +626,9 @@ def test_bench_json_contract():
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["gpu_launches"] > 0
     assert d["e2e"]["h2d_floor_ms"] > 0 and d["e2e"]["records"] == 4
     assert d["e2e"]["other_modes"]["cull_spec"]["records"] == 4
+    # every e2e leg's rate is pairs per step / its own per-step time (the legs run different step counts)
+    for leg in (d["e2e"], *d["e2e"]["other_modes"].values()):
+        assert leg["value"] == pytest.approx(d["config"]["pairs_per_step"] / (leg["ms_per_step"] * 1e-3), rel=1e-6)
     assert d["hits"] == d["cull"]["hits"] == 4
 
 
