@@ -270,60 +270,79 @@ __global__ void status_kernel(const SearchParams* __restrict__ tasks, uint32_t n
 }
 
 // ------------------------------------------------------------ cull kernels
-// Level 1: one CTA per unit of CULL_UNIT consecutive local A blocks of one task,
-// grid-stride: the blocks' union boxes are broadcast from shared memory and the CTA's
-// threads sweep the task's B tile boxes once per unit with coalesced 64-byte loads
-// (each tile box serves CULL_UNIT tests); overlapping (task, x, y) are compacted with
-// one atomic per warp.  Bt.prefix here is the per-task prefix of units.
+// Level 1: work item = (unit of CULL_UNIT consecutive local A blocks of one task, chunk of
+// CULL_YCHUNK B tiles), grid-stride: the blocks' union boxes are broadcast from shared
+// memory and the CTA's threads sweep the chunk's B tile boxes with coalesced 64-byte loads,
+// CULL_YB per thread issued before any is tested (each tile box serves CULL_UNIT tests);
+// overlapping (task, x, y) are compacted with one atomic per warp.  Bt.prefix here is the
+// per-task prefix of units.  The B tiles are chunked only when the units alone would not
+// fill the GPU (C3: 256 units = 1.7 CTAs per SM, each sweeping 2044 tiles).
 constexpr int CULL_UNIT = 4;
+constexpr int CULL_YB = 2;  // B tile boxes in flight per thread
+constexpr int CULL_YCHUNK = 256 * CULL_YB;
 
-__global__ void __launch_bounds__(256) cull_blocks_kernel(const Batch Bt) {
-  __shared__ Box abox[CULL_UNIT];
-  __shared__ const Box* s_tb;
-  __shared__ uint64_t s_ntiles;
-  __shared__ uint32_t s_t, s_x0, s_nx;
-  const uint64_t units = Bt.prefix[Bt.n_tasks];
+__device__ __forceinline__ Box ldg_box(const Box* p) {
+  const double2* s = reinterpret_cast<const double2*>(p);
+  const double2 a = __ldg(s), b = __ldg(s + 1), c = __ldg(s + 2), d = __ldg(s + 3);
+  Box r;
+  r.lo[0] = a.x; r.lo[1] = a.y; r.lo[2] = b.x; r.lo[3] = b.y;
+  r.hi[0] = c.x; r.hi[1] = c.y; r.hi[2] = d.x; r.hi[3] = d.y;
+  return r;
+}
+
+__global__ void __launch_bounds__(256, 3) cull_blocks_kernel(const Batch Bt) {
+  const uint64_t nyc = Bt.cull_ychunks;
+  const uint64_t items = Bt.prefix[Bt.n_tasks] * nyc;
   const int tid = threadIdx.x, lane = tid & 31;
-  for (uint64_t u = blockIdx.x; u < units; u += gridDim.x) {
-    if (tid == 0) {
-      const uint32_t t = find_task(Bt, u);
-      const SearchParams& P = Bt.tasks[t];
-      const uint64_t x0 = (u - Bt.prefix[t]) * CULL_UNIT;
-      const uint32_t nx = (uint32_t)min((uint64_t)CULL_UNIT, P.my_blocks - x0);
-      for (uint32_t k = 0; k < CULL_UNIT; ++k) {
-        if (k < nx) {
-          abox[k] = P.bboxA[P.blk_first + (x0 + k) * P.shard_count];
+  for (uint64_t w = blockIdx.x; w < items; w += gridDim.x) {
+    // every thread reads the item's task and A block boxes itself (same addresses: L1
+    // broadcasts) and keeps the boxes in registers — no single-thread prologue behind a CTA
+    // barrier (it was a third of the kernel's stall samples)
+    const uint64_t u = w / nyc, yc = (w - u * nyc) * Bt.cull_ychunk;
+    const uint32_t t = find_task(Bt, u);
+    const SearchParams& P = Bt.tasks[t];
+    const uint64_t x0 = (u - __ldg(Bt.prefix + t)) * CULL_UNIT;
+    const uint32_t nx = (uint32_t)min((uint64_t)CULL_UNIT, P.my_blocks - x0);
+    const Box* tb = P.tboxB;
+    const uint64_t yend = min(P.nB ? P.ntilesB : 0, yc + Bt.cull_ychunk);  // yc >= ntiles: nothing
+    Box abox[CULL_UNIT];
+#pragma unroll
+    for (uint32_t k = 0; k < CULL_UNIT; ++k) {
+      if (k < nx) {
+        abox[k] = ldg_box(P.bboxA + P.blk_first + (x0 + k) * P.shard_count);
+      } else {
+        empty_box(abox[k].lo, abox[k].hi);
+      }
+    }
+    for (uint64_t y0 = yc; y0 < yend; y0 += (uint64_t)blockDim.x * CULL_YB) {
+      Box b[CULL_YB];
+#pragma unroll
+      for (int i = 0; i < CULL_YB; ++i) {
+        const uint64_t y = y0 + (uint64_t)i * blockDim.x + tid;
+        if (y < yend) {
+          b[i] = ldg_box(tb + y);
         } else {
-          empty_box(abox[k].lo, abox[k].hi);
+          empty_box(b[i].lo, b[i].hi);
         }
       }
-      s_tb = P.tboxB;
-      s_ntiles = P.nB ? P.ntilesB : 0;
-      s_t = t;
-      s_x0 = (uint32_t)x0;
-      s_nx = nx;
-    }
-    __syncthreads();
-    const Box* tb = s_tb;
-    const uint64_t ntiles = s_ntiles;
-    const uint32_t t = s_t, x0 = s_x0, nx = s_nx;
-    for (uint64_t y0 = 0; y0 < ntiles; y0 += blockDim.x) {
-      const uint64_t y = y0 + tid;
-      Box b;
-      if (y < ntiles) b = tb[y];
-      for (uint32_t k = 0; k < nx; ++k) {
-        const bool ov = y < ntiles && box_overlap(abox[k], b);
-        const unsigned m = __ballot_sync(0xffffffffu, ov);
-        if (m) {
-          const int leader = __ffs(m) - 1;
-          unsigned long long pos = 0;
-          if (lane == leader) pos = atomicAdd(Bt.list_count, (unsigned long long)__popc(m));
-          pos = __shfl_sync(0xffffffffu, pos, leader) + __popc(m & ((1u << lane) - 1u));
-          if (ov && pos < Bt.blk_cap) Bt.blk_list[pos] = make_uint4(t, x0 + k, (uint32_t)y, 0);
+#pragma unroll
+      for (int i = 0; i < CULL_YB; ++i) {
+        if (y0 + (uint64_t)i * blockDim.x >= yend) break;  // CTA-uniform
+        const uint64_t y = y0 + (uint64_t)i * blockDim.x + tid;
+#pragma unroll
+        for (uint32_t k = 0; k < CULL_UNIT; ++k) {
+          const bool ov = k < nx && y < yend && box_overlap(abox[k], b[i]);
+          const unsigned m = __ballot_sync(0xffffffffu, ov);
+          if (m) {
+            const int leader = __ffs(m) - 1;
+            unsigned long long pos = 0;
+            if (lane == leader) pos = atomicAdd(Bt.list_count, (unsigned long long)__popc(m));
+            pos = __shfl_sync(0xffffffffu, pos, leader) + __popc(m & ((1u << lane) - 1u));
+            if (ov && pos < Bt.blk_cap) Bt.blk_list[pos] = make_uint4(t, (uint32_t)x0 + k, (uint32_t)y, 0);
+          }
         }
       }
     }
-    __syncthreads();  // abox is rewritten by the next unit
   }
 }
 
@@ -332,10 +351,10 @@ constexpr int CULL_WARPS = CULL_THREADS / 32;
 constexpr int GPAIRS = (A_BLOCK / GROUP) * (TILE / GROUP);  // 32 × 16 group pairs per block pair
 
 struct CullSmem {
-  SearchParams P;
+  Box bst[CULL_WARPS][GROUP];  // the B group of the warp's current group pair (one load per lane)
   uint2 queue[CULL_WARPS][64];
   uint16_t gpair[GPAIRS];
-  unsigned int n_gpair;
+  unsigned int n_gpair[2];  // by entry parity: the next entry's counter is reset before this one's barrier
 };
 
 // Level 2 + pair tests: one CTA per overlapping (task, A block, B tile), persistent.
@@ -352,40 +371,64 @@ __global__ void __launch_bounds__(CULL_THREADS) cull_pairs_kernel(const Batch Bt
   uint2* q = S.queue[warp];
   int qn = 0;
   uint32_t cur_task = 0xffffffffu;
+  if (tid < 2) S.n_gpair[tid] = 0;
+  __syncthreads();
   const uint64_t nlist = min((uint64_t)*(volatile unsigned long long*)Bt.list_count, Bt.blk_cap);
   const uint64_t e0 = Bt.list_done ? min((uint64_t)*Bt.list_done, nlist) : 0;
-  for (uint64_t e = e0 + blockIdx.x; e < nlist; e += gridDim.x) {
+  uint32_t par = 0;
+  // the task's parameters are read from the task table by every thread (L1 broadcasts), not
+  // copied to shared memory by one thread behind a barrier
+  for (uint64_t e = e0 + blockIdx.x; e < nlist; e += gridDim.x, par ^= 1u) {
     const uint4 txy = Bt.blk_list[e];
     if (txy.x != cur_task) {
       // task switch: drain this warp's queue and counters against the old task first
       if (cur_task != 0xffffffffu) {
         __syncwarp();
-        if (qn > 0) flush_queue(S.P, Bt, q, qn, lane);
+        if (qn > 0) flush_queue(Bt.tasks[cur_task], Bt, q, qn, lane);
         qn = 0;
-        flush_tested(S.P, lane, n_tested);
+        flush_tested(Bt.tasks[cur_task], lane, n_tested);
         n_tested = 0;
       }
-      __syncthreads();
-      if (tid == 0) S.P = Bt.tasks[txy.x];
       cur_task = txy.x;
-      __syncthreads();
     }
-    const SearchParams& P = S.P;
+    const SearchParams P = Bt.tasks[cur_task];  // by value: the fields stay in registers across the stores below
     const uint64_t gblk = P.blk_first + (uint64_t)txy.y * P.shard_count;
-    if (tid == 0) S.n_gpair = 0;
-    __syncthreads();
+    // the previous entry's counter: every thread read it before that entry's closing barrier,
+    // and the next entry's atomics come after this entry's barrier
+    if (tid == 0) S.n_gpair[par ^ 1u] = 0;
     const uint64_t ngA = (P.nA + GROUP - 1) / GROUP, ngB = (P.nB + GROUP - 1) / GROUP;
-    for (int k = tid; k < GPAIRS; k += CULL_THREADS) {
+    // every thread's group-box loads are issued before any compaction atomic
+    static_assert(GPAIRS % CULL_THREADS == 0, "group pairs per thread");
+    bool gov[GPAIRS / CULL_THREADS];
+#pragma unroll
+    for (int i = 0; i < GPAIRS / CULL_THREADS; ++i) {
+      const int k = tid + i * CULL_THREADS;
       const uint64_t ga = gblk * (A_BLOCK / GROUP) + k / (TILE / GROUP);
       const uint64_t gb = (uint64_t)txy.z * (TILE / GROUP) + k % (TILE / GROUP);
-      if (ga < ngA && gb < ngB && box_overlap(P.gboxA[ga], P.gboxB[gb])) S.gpair[atomicAdd(&S.n_gpair, 1u)] = (uint16_t)k;
+      gov[i] = ga < ngA && gb < ngB && box_overlap(ldg_box(P.gboxA + ga), ldg_box(P.gboxB + gb));
     }
+#pragma unroll
+    for (int i = 0; i < GPAIRS / CULL_THREADS; ++i)
+      if (gov[i]) S.gpair[atomicAdd(&S.n_gpair[par], 1u)] = (uint16_t)(tid + i * CULL_THREADS);
     __syncthreads();
-    const int ng = (int)S.n_gpair;
+    const int ng = (int)S.n_gpair[par];
     for (int w = warp; w < ng; w += CULL_WARPS) {
       const int k = S.gpair[w];
       const uint64_t ga0 = gblk * A_BLOCK + (uint64_t)(k / (TILE / GROUP)) * GROUP;
       const uint64_t jb0 = (uint64_t)txy.z * TILE + (uint64_t)(k % (TILE / GROUP)) * GROUP;
+      // stage the B group in shared memory, one record per lane, so the loop below reads
+      // it at shared-memory latency instead of one dependent L2 round trip per record
+      // (the load is issued here, the shared-memory store after the lane's A loads, so both
+      // round trips overlap)
+      Box* sb = S.bst[warp];
+      const bool vbl = jb0 + lane < P.nB;
+      Box bl;
+      if (vbl) bl = ldg_box(P.boxB + jb0 + lane);
+      auto stage = [&]() {
+        __syncwarp();  // the previous group pair's reads of sb are done
+        if (vbl) sb[lane] = bl;
+        __syncwarp();
+      };
       if constexpr (KIND == KIND_TRI) {
         const uint64_t ia = ga0 + lane;
         const bool va = ia >= P.a_begin && ia < P.a_end;
@@ -398,12 +441,13 @@ __global__ void __launch_bounds__(CULL_THREADS) cull_pairs_kernel(const Batch Bt
         } else {
           empty_box(alo, ahi);
         }
+        stage();
         const int nb = (int)min((uint64_t)GROUP, P.nB - jb0);
         const unsigned vmask = __ballot_sync(0xffffffffu, va);
         if (lane == 0) n_tested += (unsigned long long)__popc(vmask) * nb;
         for (int j = 0; j < nb; ++j) {
-          const double2* bp = reinterpret_cast<const double2*>(P.boxB + jb0 + j);
-          const double2 l01 = __ldg(bp), l23 = __ldg(bp + 1), h01 = __ldg(bp + 2), h23 = __ldg(bp + 3);
+          const double2* bp = reinterpret_cast<const double2*>(sb + j);
+          const double2 l01 = bp[0], l23 = bp[1], h01 = bp[2], h23 = bp[3];
           const bool p = (l01.x <= ahi[0]) & (alo[0] <= h01.x) & (l01.y <= ahi[1]) & (alo[1] <= h01.y) &
                          (l23.x <= ahi[2]) & (alo[2] <= h23.x) & (l23.y <= ahi[3]) & (alo[3] <= h23.y);
           const unsigned m = __ballot_sync(0xffffffffu, p);
@@ -431,6 +475,7 @@ __global__ void __launch_bounds__(CULL_THREADS) cull_pairs_kernel(const Batch Bt
           }
         }
         const uint32_t qa = va ? (P.permA ? __ldg(P.permA + ra) >> 1 : (uint32_t)(ra >> 1)) : 0u;
+        stage();
         for (int jj = 0; jj < (GROUP / 2) / 2; ++jj) {
           const uint64_t rb = jb0 + 2 * (uint64_t)((lane >> 4) * ((GROUP / 2) / 2) + jj);  // T¹ record of B quad
           const bool vb = rb + 1 < P.nB;
@@ -440,7 +485,7 @@ __global__ void __launch_bounds__(CULL_THREADS) cull_pairs_kernel(const Batch Bt
             empty_box(blo, bhi);
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
-              const Box bx = P.boxB[rb + u];
+              const Box bx = sb[rb - jb0 + u];
 #pragma unroll
               for (int c = 0; c < 4; ++c) { blo[c] = fmin(blo[c], bx.lo[c]); bhi[c] = fmax(bhi[c], bx.hi[c]); }
             }
@@ -468,8 +513,8 @@ __global__ void __launch_bounds__(CULL_THREADS) cull_pairs_kernel(const Batch Bt
   }
   if (cur_task != 0xffffffffu) {
     __syncwarp();
-    if (qn > 0) flush_queue(S.P, Bt, q, qn, lane);
-    flush_tested(S.P, lane, n_tested);
+    if (qn > 0) flush_queue(Bt.tasks[cur_task], Bt, q, qn, lane);
+    flush_tested(Bt.tasks[cur_task], lane, n_tested);
   }
 }
 
@@ -514,7 +559,15 @@ static int launch_cull(std::vector<SearchParams>& T, Batch& Bt, std::vector<uint
   Bt.prefix = reinterpret_cast<const uint64_t*>((char*)dev_tab + tab);
   int dev_sms = 148;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device);
-  uint64_t g1 = total;
+  uint64_t maxt = 1;
+  for (const SearchParams& P : T) maxt = std::max<uint64_t>(maxt, P.nB ? P.ntilesB : 0);
+  // split the B tiles only as far as needed to fill the resident CTA slots (C3: 256 units
+  // -> 4 chunks; 4096 A blocks -> 1 chunk), never below one sweep of CULL_YCHUNK tiles
+  const uint64_t want = std::max<uint64_t>(1, (uint64_t)dev_sms * 8 / total);
+  const uint64_t nyc = std::min<uint64_t>(want, (maxt + CULL_YCHUNK - 1) / CULL_YCHUNK);
+  Bt.cull_ychunk = (maxt + nyc - 1) / nyc;
+  Bt.cull_ychunks = (uint32_t)((maxt + Bt.cull_ychunk - 1) / Bt.cull_ychunk);
+  uint64_t g1 = total * Bt.cull_ychunks;
   if (g1 > (uint64_t)dev_sms * 8) g1 = (uint64_t)dev_sms * 8;
   cull_blocks_kernel<<<(unsigned)g1, 256, 0, stream>>>(Bt);
   CUDA_TRY(cudaGetLastError());

@@ -105,6 +105,8 @@ struct Batch {
   uint32_t neg1;                 // 0xffffffff, a runtime operand so the packed subtract stays an IMAD
   const struct FboxJob* fjobs;   // MCX_MODE_PREFILTER: one fp32-box conversion per distinct mesh
   uint32_t n_fjobs;
+  uint32_t cull_ychunks;         // cull level 1: B tile chunks per unit ...
+  uint64_t cull_ychunk;          // ... of this many tiles
 };
 
 // Task owning work unit u: the last t with prefix[t] <= u (n_tasks is small).
@@ -197,6 +199,35 @@ __global__ void __launch_bounds__(256) solve_kernel(const Batch Bt) {
     }
     if (__any_sync(0xffffffffu, v != 0) && threadIdx.x == 0) atomicOr(Bt.status_flag, 1ull);
   }
+  if constexpr (KIND == KIND_SPEC) {
+    // "for each surviving gid, runs all 4 triangle-pair precise tests": one
+    // thread per (candidate, test) — the 4 solves of a quad pair run side by side instead of
+    // as one thread's dependent chain (the stage is latency-bound: C3 has ~200 candidates);
+    // each of the 4 threads runs the (identical) Moller test, the first counts it
+    const uint64_t items = 4 * (n - k0);
+    for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < items; base += (uint64_t)gridDim.x * blockDim.x) {
+      const uint64_t it = base + threadIdx.x;
+      const bool valid = it < items;
+      const int v = (int)(it & 3);
+      const uint4 c = valid ? Bt.cand[k0 + (it >> 2)] : make_uint4(0u, 0u, 0u, 0u);
+      const SearchParams& P = Bt.tasks[c.z];
+      const double* cA = P.swapped ? P.coordsB : P.coordsA;
+      const double* cB = P.swapped ? P.coordsA : P.coordsB;
+      const uint32_t NA = P.swapped ? P.NB : P.NA, MA = P.swapped ? P.MpB : P.MpA;
+      const uint32_t NB = P.swapped ? P.NA : P.NB, MB = P.swapped ? P.MpA : P.MpB;
+      const uint32_t qa = P.swapped ? c.y : c.x, qb = P.swapped ? c.x : c.y;
+      const bool cand = valid && !moller_reject(cA, NA, MA, qa, cB, NB, MB, qb);
+      if (cand && v == 0) atomicAdd(P.counters + 4, 1ull);
+      const uint32_t ia = 2 * qa + (v >> 1), ib = 2 * qb + (v & 1);
+      double sol[4];
+      int rc = 0;
+      if (cand) {
+        rc = solve_tri(cA, NA, MA, ia, cB, NB, MB, ib, sol);
+        if (rc == 2) atomicAdd(P.counters + 2, 1ull);
+      }
+      emit_hits(Bt, rc == 1, ia, ib, sol, c.z, P.counters, lane);
+    }
+  } else {
   for (uint64_t base = k0 + blockIdx.x * (uint64_t)blockDim.x; base < n; base += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t k = base + threadIdx.x;
     const bool valid = k < n;
@@ -241,23 +272,8 @@ __global__ void __launch_bounds__(256) solve_kernel(const Batch Bt) {
           }
         }
       }
-    } else {
-      // KIND_SPEC: "for each surviving gid, runs all 4 triangle-pair precise tests"
-      const uint32_t qa = P.swapped ? c.y : c.x, qb = P.swapped ? c.x : c.y;
-      const bool cand = valid && !moller_reject(cA, NA, MA, qa, cB, NB, MB, qb);
-      if (cand) atomicAdd(P.counters + 4, 1ull);
-#pragma unroll 1
-      for (int v = 0; v < 4; ++v) {
-        const uint32_t ia = 2 * qa + (v >> 1), ib = 2 * qb + (v & 1);
-        double sol[4];
-        int rc = 0;
-        if (cand) {
-          rc = solve_tri(cA, NA, MA, ia, cB, NB, MB, ib, sol);
-          if (rc == 2) atomicAdd(P.counters + 2, 1ull);
-        }
-        emit_hits(Bt, rc == 1, ia, ib, sol, c.z, P.counters, lane);
-      }
     }
+  }
   }
 }
 
