@@ -271,15 +271,13 @@ __global__ void status_kernel(const SearchParams* __restrict__ tasks, uint32_t n
 
 // ------------------------------------------------------------ cull kernels
 // Level 1: work item = (unit of CULL_UNIT consecutive local A blocks of one task, chunk of
-// CULL_YCHUNK B tiles), grid-stride: the blocks' union boxes are broadcast from shared
-// memory and the CTA's threads sweep the chunk's B tile boxes with coalesced 64-byte loads,
-// CULL_YB per thread issued before any is tested (each tile box serves CULL_UNIT tests);
-// overlapping (task, x, y) are compacted with one atomic per warp.  Bt.prefix here is the
-// per-task prefix of units.  The B tiles are chunked only when the units alone would not
-// fill the GPU (C3: 256 units = 1.7 CTAs per SM, each sweeping 2044 tiles).
+// B tiles), grid-stride: every thread holds the unit's block boxes in registers and sweeps
+// the chunk's B tile boxes with coalesced 64-byte loads, the next one loaded while the
+// current one is tested (each tile box serves CULL_UNIT tests); overlapping (task, x, y)
+// are compacted with one atomic per warp.  Bt.prefix here is the per-task prefix of units.
+// The B tiles are chunked only when the units alone would not fill the resident CTA slots.
 constexpr int CULL_UNIT = 4;
-constexpr int CULL_YB = 2;  // B tile boxes in flight per thread
-constexpr int CULL_YCHUNK = 256 * CULL_YB;
+constexpr int CULL_YCHUNK = 512;  // fewest B tiles per chunk when the tiles are split
 
 __device__ __forceinline__ Box ldg_box(const Box* p) {
   const double2* s = reinterpret_cast<const double2*>(p);
@@ -290,7 +288,7 @@ __device__ __forceinline__ Box ldg_box(const Box* p) {
   return r;
 }
 
-__global__ void __launch_bounds__(256, 3) cull_blocks_kernel(const Batch Bt) {
+__global__ void __launch_bounds__(256, 2) cull_blocks_kernel(const Batch Bt) {
   const uint64_t nyc = Bt.cull_ychunks;
   const uint64_t items = Bt.prefix[Bt.n_tasks] * nyc;
   const int tid = threadIdx.x, lane = tid & 31;
@@ -314,34 +312,34 @@ __global__ void __launch_bounds__(256, 3) cull_blocks_kernel(const Batch Bt) {
         empty_box(abox[k].lo, abox[k].hi);
       }
     }
-    for (uint64_t y0 = yc; y0 < yend; y0 += (uint64_t)blockDim.x * CULL_YB) {
-      Box b[CULL_YB];
+    // software-pipelined sweep: the next round's tile box is loaded before this round's is
+    // tested, so a CTA's dependent chain is ~3 round trips plus compute, not one per round
+    auto tile = [&](uint64_t y) {
+      Box r;
+      if (y < yend) {
+        r = ldg_box(tb + y);
+      } else {
+        empty_box(r.lo, r.hi);
+      }
+      return r;
+    };
+    Box bc = tile(yc + tid);
+    for (uint64_t y0 = yc; y0 < yend; y0 += blockDim.x) {
+      const Box bn = tile(y0 + blockDim.x + tid);
+      const uint64_t y = y0 + tid;
 #pragma unroll
-      for (int i = 0; i < CULL_YB; ++i) {
-        const uint64_t y = y0 + (uint64_t)i * blockDim.x + tid;
-        if (y < yend) {
-          b[i] = ldg_box(tb + y);
-        } else {
-          empty_box(b[i].lo, b[i].hi);
+      for (uint32_t k = 0; k < CULL_UNIT; ++k) {
+        const bool ov = k < nx && y < yend && box_overlap(abox[k], bc);
+        const unsigned m = __ballot_sync(0xffffffffu, ov);
+        if (m) {
+          const int leader = __ffs(m) - 1;
+          unsigned long long pos = 0;
+          if (lane == leader) pos = atomicAdd(Bt.list_count, (unsigned long long)__popc(m));
+          pos = __shfl_sync(0xffffffffu, pos, leader) + __popc(m & ((1u << lane) - 1u));
+          if (ov && pos < Bt.blk_cap) Bt.blk_list[pos] = make_uint4(t, (uint32_t)x0 + k, (uint32_t)y, 0);
         }
       }
-#pragma unroll
-      for (int i = 0; i < CULL_YB; ++i) {
-        if (y0 + (uint64_t)i * blockDim.x >= yend) break;  // CTA-uniform
-        const uint64_t y = y0 + (uint64_t)i * blockDim.x + tid;
-#pragma unroll
-        for (uint32_t k = 0; k < CULL_UNIT; ++k) {
-          const bool ov = k < nx && y < yend && box_overlap(abox[k], b[i]);
-          const unsigned m = __ballot_sync(0xffffffffu, ov);
-          if (m) {
-            const int leader = __ffs(m) - 1;
-            unsigned long long pos = 0;
-            if (lane == leader) pos = atomicAdd(Bt.list_count, (unsigned long long)__popc(m));
-            pos = __shfl_sync(0xffffffffu, pos, leader) + __popc(m & ((1u << lane) - 1u));
-            if (ov && pos < Bt.blk_cap) Bt.blk_list[pos] = make_uint4(t, (uint32_t)x0 + k, (uint32_t)y, 0);
-          }
-        }
-      }
+      bc = bn;
     }
   }
 }
@@ -562,8 +560,8 @@ static int launch_cull(std::vector<SearchParams>& T, Batch& Bt, std::vector<uint
   uint64_t maxt = 1;
   for (const SearchParams& P : T) maxt = std::max<uint64_t>(maxt, P.nB ? P.ntilesB : 0);
   // split the B tiles only as far as needed to fill the resident CTA slots (C3: 256 units
-  // -> 4 chunks; 4096 A blocks -> 1 chunk), never below one sweep of CULL_YCHUNK tiles
-  const uint64_t want = std::max<uint64_t>(1, (uint64_t)dev_sms * 8 / total);
+  // -> 1 chunk, one wave), never below CULL_YCHUNK tiles
+  const uint64_t want = std::max<uint64_t>(1, (uint64_t)dev_sms * 2 / total);  // 2 resident CTAs per SM
   const uint64_t nyc = std::min<uint64_t>(want, (maxt + CULL_YCHUNK - 1) / CULL_YCHUNK);
   Bt.cull_ychunk = (maxt + nyc - 1) / nyc;
   Bt.cull_ychunks = (uint32_t)((maxt + Bt.cull_ychunk - 1) / Bt.cull_ychunk);
