@@ -443,20 +443,31 @@ __global__ void __launch_bounds__(CULL_THREADS) cull_pairs_kernel(const Batch Bt
         const int nb = (int)min((uint64_t)GROUP, P.nB - jb0);
         const unsigned vmask = __ballot_sync(0xffffffffu, va);
         if (lane == 0) n_tested += (unsigned long long)__popc(vmask) * nb;
-        for (int j = 0; j < nb; ++j) {
-          const double2* bp = reinterpret_cast<const double2*>(sb + j);
-          const double2 l01 = bp[0], l23 = bp[1], h01 = bp[2], h23 = bp[3];
-          const bool p = (l01.x <= ahi[0]) & (alo[0] <= h01.x) & (l01.y <= ahi[1]) & (alo[1] <= h01.y) &
-                         (l23.x <= ahi[2]) & (alo[2] <= h23.x) & (l23.y <= ahi[3]) & (alo[3] <= h23.y);
+        // all 32 tests first (independent shared loads and compares, a bit per B record),
+        // then one ballot per B record that some lane keeps
+        unsigned pm = 0;
+#pragma unroll
+        for (int j = 0; j < GROUP; ++j) {
+          if (j < nb) {
+            const double2* bp = reinterpret_cast<const double2*>(sb + j);
+            const double2 l01 = bp[0], l23 = bp[1], h01 = bp[2], h23 = bp[3];
+            const bool p = (l01.x <= ahi[0]) & (alo[0] <= h01.x) & (l01.y <= ahi[1]) & (alo[1] <= h01.y) &
+                           (l23.x <= ahi[2]) & (alo[2] <= h23.x) & (l23.y <= ahi[3]) & (alo[3] <= h23.y);
+            pm |= (unsigned)p << j;
+          }
+        }
+        unsigned anyj = __reduce_or_sync(0xffffffffu, pm);
+        while (anyj) {
+          const int j = __ffs(anyj) - 1;
+          anyj &= anyj - 1;
+          const bool p = (pm >> j) & 1u;
           const unsigned m = __ballot_sync(0xffffffffu, p);
-          if (m) {
-            if (p) q[qn + __popc(m & lt_mask)] = make_uint2((uint32_t)ia, (uint32_t)(jb0 + j));
-            qn += __popc(m);
-            __syncwarp();
-            if (qn >= 32) {
-              qn -= 32;
-              flush_queue(P, Bt, q + qn, 32, lane);
-            }
+          if (p) q[qn + __popc(m & lt_mask)] = make_uint2((uint32_t)ia, (uint32_t)(jb0 + j));
+          qn += __popc(m);
+          __syncwarp();
+          if (qn >= 32) {
+            qn -= 32;
+            flush_queue(P, Bt, q + qn, 32, lane);
           }
         }
       } else {
@@ -474,11 +485,15 @@ __global__ void __launch_bounds__(CULL_THREADS) cull_pairs_kernel(const Batch Bt
         }
         const uint32_t qa = va ? (P.permA ? __ldg(P.permA + ra) >> 1 : (uint32_t)(ra >> 1)) : 0u;
         stage();
-        for (int jj = 0; jj < (GROUP / 2) / 2; ++jj) {
-          const uint64_t rb = jb0 + 2 * (uint64_t)((lane >> 4) * ((GROUP / 2) / 2) + jj);  // T¹ record of B quad
-          const bool vb = rb + 1 < P.nB;
-          bool p = false;
-          if (vb && va) {
+        // all 8 quad-box tests first (a bit per B quad), then one ballot per B quad that some
+        // lane keeps
+        constexpr int NQ = (GROUP / 2) / 2;
+        const uint64_t rb0 = jb0 + 2 * (uint64_t)((lane >> 4) * NQ);  // T¹ record of the lane's first B quad
+        unsigned pm = 0;
+#pragma unroll
+        for (int jj = 0; jj < NQ; ++jj) {
+          const uint64_t rb = rb0 + 2 * (uint64_t)jj;
+          if (rb + 1 < P.nB && va) {
             double blo[4], bhi[4];
             empty_box(blo, bhi);
 #pragma unroll
@@ -488,21 +503,27 @@ __global__ void __launch_bounds__(CULL_THREADS) cull_pairs_kernel(const Batch Bt
               for (int c = 0; c < 4; ++c) { blo[c] = fmin(blo[c], bx.lo[c]); bhi[c] = fmax(bhi[c], bx.hi[c]); }
             }
             ++n_tested;
-            p = (blo[0] <= ahi[0]) & (alo[0] <= bhi[0]) & (blo[1] <= ahi[1]) & (alo[1] <= bhi[1]) &
-                (blo[2] <= ahi[2]) & (alo[2] <= bhi[2]) & (blo[3] <= ahi[3]) & (alo[3] <= bhi[3]);
+            const bool p = (blo[0] <= ahi[0]) & (alo[0] <= bhi[0]) & (blo[1] <= ahi[1]) & (alo[1] <= bhi[1]) &
+                           (blo[2] <= ahi[2]) & (alo[2] <= bhi[2]) & (blo[3] <= ahi[3]) & (alo[3] <= bhi[3]);
+            pm |= (unsigned)p << jj;
           }
+        }
+        unsigned anyj = __reduce_or_sync(0xffffffffu, pm);
+        while (anyj) {
+          const int jj = __ffs(anyj) - 1;
+          anyj &= anyj - 1;
+          const bool p = (pm >> jj) & 1u;
           const unsigned m = __ballot_sync(0xffffffffu, p);
-          if (m) {
-            if (p) {
-              const uint32_t qb = P.permB ? __ldg(P.permB + rb) >> 1 : (uint32_t)(rb >> 1);
-              q[qn + __popc(m & lt_mask)] = make_uint2(qa, qb);
-            }
-            qn += __popc(m);
-            __syncwarp();
-            if (qn >= 32) {
-              qn -= 32;
-              flush_queue(P, Bt, q + qn, 32, lane);
-            }
+          if (p) {
+            const uint64_t rb = rb0 + 2 * (uint64_t)jj;
+            const uint32_t qb = P.permB ? __ldg(P.permB + rb) >> 1 : (uint32_t)(rb >> 1);
+            q[qn + __popc(m & lt_mask)] = make_uint2(qa, qb);
+          }
+          qn += __popc(m);
+          __syncwarp();
+          if (qn >= 32) {
+            qn -= 32;
+            flush_queue(P, Bt, q + qn, 32, lane);
           }
         }
       }
