@@ -290,7 +290,7 @@ __device__ __forceinline__ Box ldg_box(const Box* p) {
 
 __global__ void __launch_bounds__(256, 2) cull_blocks_kernel(const Batch Bt) {
   const uint64_t nyc = Bt.cull_ychunks;
-  const uint64_t items = Bt.prefix[Bt.n_tasks] * nyc;
+  const uint64_t items = Bt.cull_items;  // a kernel parameter: no load before the first item
   const int tid = threadIdx.x, lane = tid & 31;
   for (uint64_t w = blockIdx.x; w < items; w += gridDim.x) {
     // every thread reads the item's task and A block boxes itself (same addresses: L1
@@ -586,7 +586,8 @@ static int launch_cull(std::vector<SearchParams>& T, Batch& Bt, std::vector<uint
   const uint64_t nyc = std::min<uint64_t>(want, (maxt + CULL_YCHUNK - 1) / CULL_YCHUNK);
   Bt.cull_ychunk = (maxt + nyc - 1) / nyc;
   Bt.cull_ychunks = (uint32_t)((maxt + Bt.cull_ychunk - 1) / Bt.cull_ychunk);
-  uint64_t g1 = total * Bt.cull_ychunks;
+  Bt.cull_items = total * Bt.cull_ychunks;
+  uint64_t g1 = Bt.cull_items;
   if (g1 > (uint64_t)dev_sms * 8) g1 = (uint64_t)dev_sms * 8;
   cull_blocks_kernel<<<(unsigned)g1, 256, 0, stream>>>(Bt);
   CUDA_TRY(cudaGetLastError());

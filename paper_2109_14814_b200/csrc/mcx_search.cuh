@@ -107,6 +107,7 @@ struct Batch {
   uint32_t n_fjobs;
   uint32_t cull_ychunks;         // cull level 1: B tile chunks per unit ...
   uint64_t cull_ychunk;          // ... of this many tiles
+  uint64_t cull_items;           // level-1 work items (units × chunks; known on the host)
 };
 
 // Task owning work unit u: the last t with prefix[t] <= u (n_tasks is small).
